@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Headline benchmark: foveated render + reconstruct frames/s at 1080p on B200.
+
+Workload (BASELINE.json configs[2], the north-star target; `--config c2` selects configs[1]):
+  512^3 sphere_shells volume, 1920x1080 film, 'hifi' preset (P_b=0.07, sigma=0.06),
+  FULL_BLOCKS W-Net (seed 0, fp16 weights), orbit camera path of 500 frames, noise frame i,
+  recurrent state carried across frames -- one `step` = one frame of
+  bench.cmd_bench_throughput's loop body (mask -> compact -> march -> reconstruct).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3|c2]
+
+Multi-GPU (torchrun, one process per GPU): every rank renders its own frame stream (an
+independent viewer session) -- the per-frame path has no exchange step, so there is no
+data-path collective; `value` is all ranks' frames / the max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c3": dict(vol=512, width=1920, height=1080, mode="hifi", pb=0.07, sigma=0.06,
+               name="512^3 sphere_shells, 1920x1080, hifi (P_b=0.07, sigma=0.06), FULL_BLOCKS fp16 net"),
+    "c2": dict(vol=256, width=1920, height=1080, mode="fast", pb=0.03, sigma=0.02,
+               name="256^3 sphere_shells, 1920x1080, fast (P_b=0.03, sigma=0.02), FULL_BLOCKS fp16 net"),
+}
+PATH_FRAMES = 500
+MAC_PER_PX = 275071.5  # FULL_BLOCKS multiply-accumulates per output pixel
+BYTES_PER_SAMPLE = 32  # algorithmic bytes of one trilinear sample (2x2x2 fp32 footprint)
+METRIC = "frames/sec at 1080p (render+reconstruct)"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, device: int, out: Path):
+        self.out = out
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(out, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait(timeout=10)
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU legs
+def cpu_frame_estimate(cfg, n_rays=20000, strip_rows=24, seed=0):
+    """Oracle (reference algorithm restated: NumPy fp64 mask, C fp64 marcher on all host
+    threads, NumPy/BLAS fp32 network) on a bounded sample of one frame; returns
+    (seconds per full frame extrapolated, sample description, threads)."""
+    from oracle import fovray_oracle as O
+
+    h, w, n = cfg["height"], cfg["width"], cfg["vol"]
+    stack = O.load_rnkstack(ROOT / "paper_2209_09965_b200" / "data" / "stbn_64x64x8_s1.noise")
+    sc = O.pixel_scale_for_film(h, w)
+    t0 = time.perf_counter()
+    tau = O.tau_map(h, w, ((w - 1) / 2, (h - 1) / 2), cfg["sigma"], cfg["pb"], sc)
+    bits = O.sample_mask(stack, h, w, 0, tau)
+    idx = O.compact(bits)
+    t_mask = time.perf_counter() - t0
+    vol = _oracle_volume(n)
+    pos, look = O.orbit_camera(0, PATH_FRAMES, (n, n, n))
+    rng = np.random.default_rng(seed)
+    sub = np.sort(rng.choice(idx, size=min(n_rays, idx.size), replace=False))
+    t0 = time.perf_counter()
+    O.render(vol, (1, 1, 1), O.DEFAULT_LUT, ("dir", (-1.0, -1.0, -0.5), (1, 1, 1)),
+             dict(position=pos, look_at=look, fov_y=45.0, width=w, height=h), pix=sub)
+    t_march = (time.perf_counter() - t0) * idx.size / sub.size
+    p = O.init_params(O.FULL_BLOCKS, 0, fp16_weights=True)
+    x = np.random.default_rng(1).random((5, strip_rows, w)).astype(np.float32)
+    t0 = time.perf_counter()
+    O.net_forward(p, O.FULL_BLOCKS, x, None)
+    t_net = (time.perf_counter() - t0) * h / strip_rows
+    total = t_mask + t_march + t_net
+    desc = (f"frame 0: full-frame mask+compaction ({t_mask*1e3:.0f} ms), {sub.size} of {idx.size} active rays "
+            f"marched in fp64 ({t_march:.1f} s extrapolated), FULL_BLOCKS fp32 net on a {w}x{strip_rows} "
+            f"strip ({t_net:.1f} s extrapolated to {h} rows)")
+    return total, desc, O.threads()
+
+
+_VOL_CACHE = {}
+
+
+def _oracle_volume(n):
+    """The procedural volume for the CPU legs (generated once; the oracle's own generator)."""
+    if n not in _VOL_CACHE:
+        from oracle import fovray_oracle as O
+
+        _VOL_CACHE[n], _ = O.procedural_volume("sphere_shells", (n, n, n)) if n <= 256 else \
+            _procedural_by_slabs(n)
+    return _VOL_CACHE[n]
+
+
+def _procedural_by_slabs(n):
+    """sphere_shells at n^3 without the fp64 full-volume temporaries (same values as the oracle)."""
+    ax = (np.arange(n) + 0.5) / n * 2.0 - 1.0
+    out = np.empty((n, n, n), np.float32)
+    lo, hi = np.inf, -np.inf
+    raws = []
+    for z in range(n):
+        r = np.sqrt(ax[None, :] ** 2 + ax[:, None] ** 2 + ax[z] ** 2)
+        raw = 0.5 * (1.0 + np.cos(2.0 * np.pi * 3.0 * r))
+        lo, hi = min(lo, raw.min()), max(hi, raw.max())
+        raws.append(raw)
+    for z in range(n):
+        out[z] = ((raws[z] - lo) / (hi - lo)).astype(np.float32)
+    return out, (lo, hi)
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    k, wu = args.steps, args.warmup
+    # each step = one bounded sample of a frame (the CPU needs minutes per full 1080p frame)
+    per = []
+    desc = threads = None
+    for s in range(wu + k):
+        sec, desc, threads = cpu_frame_estimate(cfg, n_rays=4000, strip_rows=8, seed=s)
+        if s >= wu:
+            per.append(sec)
+    fps = 1.0 / float(np.mean(per))
+    line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": k,
+            "warmup": wu, "ms_per_step": float(np.mean(per)) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp64 (march) / fp32 (net)",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["name"], "film": [cfg["width"], cfg["height"]],
+                       "volume": [cfg["vol"]] * 3, "path_frames": PATH_FRAMES, "parallelism": "host threads"},
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
+                             "sample": desc + "; per-frame time extrapolated from the sample"},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU leg
+def run_ours(args, cfg):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2209_09965_b200 import _lib
+    from paper_2209_09965_b200 import network as N
+    from paper_2209_09965_b200.noise import default_stack
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, RenderSettings, orbit_cameras
+    from paper_2209_09965_b200.sample_maps import FoveaConfig, pixel_scale_for_film
+    from paper_2209_09965_b200.throughput import default_scene
+
+    h, w, n = cfg["height"], cfg["width"], cfg["vol"]
+    scene = default_scene("sphere_shells", (n, n, n))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=PATH_FRAMES), scene.volume, w, h)
+    fovea = FoveaConfig(focus=((w - 1) / 2.0, (h - 1) / 2.0), sigma=cfg["sigma"], base_density=cfg["pb"],
+                        pixel_scale=pixel_scale_for_film((h, w)))
+    pipe = FramePipeline(scene, net, (h, w), default_stack(), RenderSettings())
+    ctx = pipe.ctx
+    stream = ctx.stream
+    base = rank * 977  # each rank = its own session, at its own point on the path
+    k, wu = args.steps, args.warmup
+
+    def frame(i):
+        j = base + i
+        pipe.step(cams[j % PATH_FRAMES], fovea, j)
+
+    for i in range(wu):
+        frame(i)
+    torch.cuda.synchronize()
+    # --- device-resident timed region -------------------------------------------------
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
+    clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_r{rank}.csv") if rank == 0 else None
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    l0 = ctx.launches()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(k):
+        j = base + wu + i
+        e = ev[i]
+        e[0].record(stream)
+        pipe.mask(fovea, j)
+        e[1].record(stream)
+        pipe.march(cams[j % PATH_FRAMES])
+        e[2].record(stream)
+        pipe.reconstruct()
+        e[3].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([elapsed_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    clk = clocks.stop() if clocks else None
+    st = ctx.stats()
+    mask_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
+    march_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
+    net_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    samples_per_frame = (st.samples_main + st.samples_shadow) / k
+    rays_per_frame = st.rays / k
+    fps = world * k / (elapsed_ms / 1e3)
+    # --- end to end through the C ABI with host buffers (fv_frame) --------------------
+    host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
+    ke = max(3, k // 2)
+    for i in range(2):
+        pipe.frame_to_host(cams[(base + i) % PATH_FRAMES], fovea, base + i, host)
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(ke):
+        j = base + wu + k + i
+        pipe.frame_to_host(cams[j % PATH_FRAMES], fovea, j, host)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_fps = world * ke / e2e_s
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    hbm, tf_burst, tf_sus, src = load_peaks()
+    march_gbs = samples_per_frame * BYTES_PER_SAMPLE / (march_ms / 1e3) / 1e9
+    net_tflops = 2 * MAC_PER_PX * h * w / (net_ms / 1e3) / 1e12
+    stages = {
+        "march": {"bound": "hbm", "achieved": march_gbs, "peak": hbm, "unit": "GB/s",
+                  "frac": march_gbs / hbm, "ms": march_ms, "gsamples_per_s": samples_per_frame / (march_ms / 1e3) / 1e9},
+        "reconstruct": {"bound": "tensor", "achieved": net_tflops, "peak": tf_sus, "unit": "TFLOP/s",
+                        "frac": net_tflops / tf_sus, "ms": net_ms},
+        "mask": {"ms": mask_ms},
+    }
+    dom = "march" if march_ms >= net_ms else "reconstruct"
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(dom)
+    roof = {k2: v for k2, v in stages[dom].items() if k2 in ("bound", "achieved", "peak", "unit", "frac")}
+    roof.update(traffic=traffic, kernel=("march_kernel" if dom == "march" else "W-Net forward (tcgen05 convs)"),
+                peak_source=f"{src} ({'sustained' if dom == 'reconstruct' else 'copy'})")
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        sec, desc, threads = cpu_frame_estimate(cfg)
+        cpu = {"value": 1.0 / sec, "unit": "frames/s", "cores": threads, "kind": "port", "sample": desc}
+    line = {
+        "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": k, "warmup": wu,
+        "ms_per_step": elapsed_ms / k, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp16 net (fp32 acc) / fp32 march", "data": "synthetic",
+        "config": {"workload": cfg["name"], "film": [w, h], "volume": [n, n, n], "path_frames": PATH_FRAMES,
+                   "parallelism": f"independent frame streams x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (512 MiB volume, ~1.6 GB activations per frame)"},
+        "gsamples_per_s": world * samples_per_frame * k / (elapsed_ms / 1e3) / 1e9,
+        "samples_per_frame": samples_per_frame, "active_rays_per_frame": rays_per_frame,
+        "phase_ms": {"mask": mask_ms, "march": march_ms, "reconstruct": net_ms},
+        "roofline": roof, "stages": stages,
+        "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": h * w * 3 * 4,
+                "how": "fv_frame C-ABI call per frame (camera/fovea by value, pinned host RGB out, sync)"},
+        "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,388 @@
+"""CPU ORACLE -- test infrastructure only.
+
+Only tests/, __graft_entry__.smoke() and bench.py (its cpu_baseline and
+--impl reference legs) may import this module, and only as the checker / the
+reported CPU baseline. The product (paper_2209_09965_b200) never calls it.
+
+A restatement of the reference FoVolNet hot path (pkg/src/fovray, NumPy/float64
+for masks and marching, float32 for the network) written for checking:
+
+  tau_map / sample_mask / compact          sample_maps.py:62-68, :89-105, :128-132, :161-171
+  procedural_volume                        volume.py:112-146 (+ _normalize :75-81)
+  camera_basis / render (C, march_oracle.c) volume.py:269-303, renderer.py:88-195
+  net_forward (conv/pool/up/K stage)       network.py:183-323, autograd.py:173-359
+  psnr / ssim                              metrics.py:40-87
+
+Parity of this restatement with the reference itself is pinned in
+tests/test_oracle.py against fixtures produced by running the reference
+(tests/golden/make_golden.py), including the reference's own golden SHA-256.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "_build" / "liboracle.so"
+
+FULL_BLOCKS = "e64-e64-e80-d96-d80-d64-d64"
+DESK_BLOCKS = "e16-e16-e24-d32-d24-d16-d16"
+DEFAULT_LUT = np.asarray([
+    [0.10, 0.10, 0.35, 0.00], [0.15, 0.35, 0.80, 0.02], [0.10, 0.75, 0.70, 0.12],
+    [0.55, 0.85, 0.25, 0.30], [0.95, 0.80, 0.15, 0.55], [0.95, 0.35, 0.10, 0.80],
+    [0.90, 0.90, 0.90, 0.95]], dtype=np.float32)
+
+
+# --------------------------------------------------------------------------- masks
+def pixel_scale_for_film(h: int, w: int, fraction: float = 0.45) -> float:
+    """sample_maps.py:31-40 with sigma_fast = 0.02."""
+    return float(np.sqrt(2.0 / 0.02) / (fraction * min(h, w)))
+
+
+def tau_map(h, w, focus, sigma, pb, scale) -> np.ndarray:
+    """Eq. 1-2 as the reference evaluates them (sample_maps.py:62-68, :101-105), fp64."""
+    dx = (np.arange(w, dtype=np.float64) - focus[0])[None, :] * scale
+    dy = (np.arange(h, dtype=np.float64) - focus[1])[:, None] * scale
+    pf = np.exp(-0.5 * (dx * dx + dy * dy) * sigma)
+    return np.minimum(pf + (1.0 - pf) * np.asarray(pb, dtype=np.float64), 1.0)
+
+
+def noise_field(stack: np.ndarray, h: int, w: int, frame: int) -> np.ndarray:
+    """Toroidal lookup stack[frame % T][v % Ht][u % Wt] (noise.py:378-384)."""
+    t, th, tw = stack.shape
+    return stack[frame % t][(np.arange(h) % th)[:, None], (np.arange(w) % tw)[None, :]]
+
+
+def sample_mask(stack, h, w, frame, tau) -> np.ndarray:
+    """M = float64(N) < tau (sample_maps.py:128-132)."""
+    return noise_field(stack, h, w, frame).astype(np.float64) < tau
+
+
+def compact(bits: np.ndarray) -> np.ndarray:
+    """Row-major flat indices v*W+u of the set bits (sample_maps.py:161-171)."""
+    return np.flatnonzero(bits.reshape(-1)).astype(np.int64)
+
+
+def load_rnkstack(path) -> np.ndarray:
+    import struct
+
+    blob = Path(path).read_bytes()
+    head = struct.calcsize("<8sIIIq dd")
+    magic, h, w, t, *_ = struct.unpack("<8sIIIq dd", blob[:head])
+    assert magic == b"RNKSTACK"
+    return np.frombuffer(blob[head:], dtype="<f4").reshape(t, h, w).copy()
+
+
+# --------------------------------------------------------------------------- volumes
+def procedural_volume(kind: str, dims) -> np.ndarray:
+    """volume.py:112-146 raw fields at voxel centres, global min-max to float32."""
+    nx, ny, nz = dims
+    ax = [(np.arange(n) + 0.5) / n * 2.0 - 1.0 for n in (nx, ny, nz)]
+    u, v, w = ax[0][None, None, :], ax[1][None, :, None], ax[2][:, None, None]
+    r = np.sqrt(u * u + v * v + w * w)
+    if kind == "sphere_shells":
+        raw = 0.5 * (1.0 + np.cos(2.0 * np.pi * 3.0 * r))
+    elif kind == "vortex_field":
+        raw = np.sin(3.0 * np.pi * u + 2.0 * v * w) * np.cos(2.0 * np.pi * v - 1.5 * u * w)
+        raw = raw + 0.5 * np.cos(4.0 * np.pi * r)
+    elif kind == "box_lattice":
+        par = (np.floor(2.0 * (u + 1.0)) + np.floor(2.0 * (v + 1.0)) + np.floor(2.0 * (w + 1.0))) % 2.0
+        raw = 0.7 * par + 0.3 * (u + 1.0) / 2.0
+    else:
+        raise ValueError(kind)
+    raw = np.ascontiguousarray(np.broadcast_to(raw, (nz, ny, nx)))
+    lo, hi = float(raw.min()), float(raw.max())
+    data = ((raw - lo) / (hi - lo)).astype(np.float32) if hi > lo else np.zeros(raw.shape, np.float32)
+    return data, (lo, hi)
+
+
+# --------------------------------------------------------------------------- marcher
+def build_lib() -> Path:
+    if not LIB.exists() or LIB.stat().st_mtime < (HERE / "march_oracle.c").stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB
+
+
+_clib = None
+
+
+def _lib():
+    global _clib
+    if _clib is None:
+        _clib = C.CDLL(str(build_lib()))
+        _clib.oracle_render.restype = None
+    return _clib
+
+
+def camera_basis(position, look_at, up=(0.0, 1.0, 0.0)):
+    """Camera.basis (volume.py:269-276), NumPy norms as the reference computes them."""
+    fwd = np.subtract(look_at, position, dtype=np.float64)
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, np.asarray(up, dtype=np.float64))
+    right /= np.linalg.norm(right)
+    return right, np.cross(right, fwd), fwd
+
+
+def orbit_camera(i: int, n_frames: int, dims, spacing=(1.0, 1.0, 1.0), radius_factor=2.2,
+                 zoom_amplitude=0.35, zoom_periods=2.0, yaw_turns=1.0, pitch_amp_deg=25.0,
+                 pitch_periods=1.0):
+    """orbit_cameras frame i (renderer.py:317-361) -> (position, look_at)."""
+    ext = np.asarray(dims, dtype=np.float64) * np.asarray(spacing, dtype=np.float64)
+    center = ext * 0.5
+    diag = float(np.linalg.norm(ext))
+    s = 0.0 if n_frames <= 1 else i / n_frames
+    yaw = 2.0 * np.pi * (yaw_turns * s + 0.0)
+    pitch = np.deg2rad(pitch_amp_deg) * np.sin(2.0 * np.pi * pitch_periods * s)
+    r = radius_factor * diag * (1.0 + zoom_amplitude * np.sin(2.0 * np.pi * zoom_periods * s))
+    pos = center + r * np.array([np.cos(pitch) * np.cos(yaw), np.sin(pitch), np.cos(pitch) * np.sin(yaw)])
+    return tuple(pos), tuple(center)
+
+
+def render(volume: np.ndarray, spacing, lut, light, cam: dict, pix=None, step_size=None,
+           shadow_step_factor=4.0, early_term_alpha=0.99, background=(0.0, 0.0, 0.0, 0.0),
+           ambient=0.25, reference_step=None, shadow_min_transmittance=1e-3, with_counts=False,
+           nthreads=None):
+    """March pixels `pix` (flat v*W+u; None = all) -> (rgba (n,4) f32, depth (n,) f32[, counts]).
+
+    light: None, ("dir", (x,y,z), intensity) or ("point", (x,y,z), intensity).
+    cam: dict(position, look_at, up, fov_y, width, height).
+    """
+    vol = np.ascontiguousarray(volume, dtype=np.float32)
+    nz, ny, nx = vol.shape
+    w, h = int(cam["width"]), int(cam["height"])
+    base = float(min(spacing))
+    step = step_size if step_size is not None else 0.5 * base
+    ref = reference_step if reference_step is not None else base
+    right, up, fwd = camera_basis(cam["position"], cam["look_at"], cam.get("up", (0.0, 1.0, 0.0)))
+    tan_half = np.tan(np.deg2rad(cam.get("fov_y", 45.0)) * 0.5)
+    aspect = w / h
+    camv = np.concatenate([np.asarray(cam["position"], np.float64), right, up, fwd,
+                           [tan_half, aspect]]).astype(np.float64)
+    kind, lvec, inten = 0, np.zeros(3), np.ones(3)
+    if light is not None:
+        if light[0] == "dir":
+            kind = 1
+            d = -np.asarray(light[1], dtype=np.float64)
+            lvec = d / np.linalg.norm(d)
+        else:
+            kind = 2
+            lvec = np.asarray(light[1], dtype=np.float64)
+        inten = np.asarray(light[2], dtype=np.float64)
+    cfg = np.asarray([step, ref, step * shadow_step_factor, early_term_alpha, ambient,
+                      shadow_min_transmittance, *background], dtype=np.float64)
+    pix = np.arange(w * h, dtype=np.int64) if pix is None else np.ascontiguousarray(pix, dtype=np.int64)
+    n = pix.shape[0]
+    rgba = np.zeros((n, 4), dtype=np.float32)
+    depth = np.zeros(n, dtype=np.float32)
+    counts = np.zeros((n, 2), dtype=np.int64) if with_counts else None
+    lut = np.ascontiguousarray(lut, dtype=np.float32)
+    dims = np.asarray([nx, ny, nz], dtype=np.int32)
+    sp = np.asarray(spacing, dtype=np.float64)
+
+    def P(a):
+        return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+    _lib().oracle_render(P(vol), P(dims), P(sp), P(lut), C.c_int(lut.shape[0]), C.c_int(kind),
+                         P(np.ascontiguousarray(lvec, np.float64)), P(np.ascontiguousarray(inten, np.float64)),
+                         P(cfg), P(camv), C.c_int(w), C.c_int(h), P(pix), C.c_int64(n), P(rgba),
+                         P(depth), P(counts), C.c_int(nthreads or threads()))
+    if with_counts:
+        return rgba, depth, counts
+    return rgba, depth
+
+
+def render_image(volume, spacing, lut, light, cam: dict, bits=None, **kw):
+    """(H,W,4) rgba + (H,W) depth; pixels outside `bits` stay zero (render_sparse_compact)."""
+    w, h = int(cam["width"]), int(cam["height"])
+    pix = None if bits is None else compact(bits)
+    rgba, depth = render(volume, spacing, lut, light, cam, pix=pix, **kw)
+    img = np.zeros((h * w, 4), np.float32)
+    dep = np.zeros(h * w, np.float32)
+    sel = np.arange(h * w) if pix is None else pix
+    img[sel] = rgba
+    dep[sel] = depth
+    return img.reshape(h, w, 4), dep.reshape(h, w)
+
+
+# --------------------------------------------------------------------------- network (fp32)
+def parse_blocks(s: str):
+    return [(t[0], int(t[1:])) for t in s.split("-")]
+
+
+def conv_layout(blocks: str, in_channels: int = 8, recurrent: bool = True):
+    """(cin, cout) per D block and K input widths (network.py:128-159)."""
+    cfg = parse_blocks(blocks)
+    ch = [c for _, c in cfg]
+    ne = sum(1 for k, _ in cfg if k == "e")
+    nd = len(cfg) - ne
+    d_ch = ch[ne:]
+    d_in = []
+    for j in range(nd):
+        inc = ch[ne - 1] if j == 0 else d_ch[j - 1] + ch[ne - j]
+        d_in.append(inc + (d_ch[j] if recurrent else 0))
+    e_in = [in_channels] + ch[: ne - 1]
+    levels = list(range(ne)) + [ne - j for j in range(nd)]
+    k_in = [d_ch[ne - lv] for lv in levels]
+    return list(zip(e_in, ch[:ne])) + list(zip(d_in, d_ch)), k_in, ne, nd, levels, cfg
+
+
+def init_params(blocks: str, seed: int, in_channels: int = 8, fp16_weights: bool = False):
+    """Seeded He-uniform weights in init_network's draw order (network.py:162-180)."""
+    rng = np.random.default_rng(seed)
+    layout, k_in, *_ = conv_layout(blocks, in_channels)
+    p = {}
+
+    def conv(name, cin, cout, k):
+        bound = np.sqrt(6.0 / (cin * k * k))
+        w = rng.uniform(-bound, bound, size=(cout, cin, k, k)).astype(np.float32)
+        if fp16_weights:
+            w = np.clip(w, -65504, 65504).astype(np.float16).astype(np.float32)
+        p[name + ".w"] = w
+        p[name + ".b"] = np.zeros(cout, np.float32)
+
+    for i, (cin, cout) in enumerate(layout):
+        conv(f"D.block{i}.conv1", cin, cout, 3)
+        conv(f"D.block{i}.conv2", cout, cout, 3)
+    conv("D.head", layout[-1][1], 3, 3)
+    for i, cin in enumerate(k_in):
+        conv(f"K.block{i}", cin, 9, 1)
+    return p
+
+
+def conv3x3(x: np.ndarray, w: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Cross-correlation, zero padding 1 (autograd.py:238-276), as 9 shifted matmuls. x (C,H,W)."""
+    c, h, wd = x.shape
+    xp = np.pad(x, ((0, 0), (1, 1), (1, 1)))
+    out = np.zeros((w.shape[0], h * wd), np.float32)
+    for ky in range(3):
+        for kx in range(3):
+            out += w[:, :, ky, kx] @ xp[:, ky:ky + h, kx:kx + wd].reshape(c, -1)
+    return (out + b[:, None]).reshape(w.shape[0], h, wd)
+
+
+def relu(x):
+    return x * (x > 0)
+
+
+def pool2(x):
+    return 0.25 * (x[:, 0::2, 0::2] + x[:, 1::2, 0::2] + x[:, 0::2, 1::2] + x[:, 1::2, 1::2])
+
+
+def up2(x):
+    """Half-pixel bilinear x2, edge clamp, rows then columns (autograd.py:294-329)."""
+    def axis(d, ax):
+        d = np.moveaxis(d, ax, -1)
+        prev = np.concatenate([d[..., :1], d[..., :-1]], axis=-1)
+        nxt = np.concatenate([d[..., 1:], d[..., -1:]], axis=-1)
+        out = np.empty(d.shape[:-1] + (2 * d.shape[-1],), dtype=d.dtype)
+        out[..., 0::2] = 0.25 * prev + 0.75 * d
+        out[..., 1::2] = 0.75 * d + 0.25 * nxt
+        return np.moveaxis(out, -1, ax)
+    return axis(axis(x, 1), 2)
+
+
+def kernel_filter(img, logits):
+    """softmax over 9 taps then per-pixel 3x3 filter, zero padding (autograd.py:188-199, :332-359)."""
+    m = logits.max(axis=0, keepdims=True)
+    e = np.exp(logits - m)
+    k = e / e.sum(axis=0, keepdims=True)
+    h, w = img.shape[1:]
+    ip = np.pad(img, ((0, 0), (1, 1), (1, 1)))
+    out = np.zeros_like(img)
+    for j in range(9):
+        dy, dx = divmod(j, 3)
+        out += k[j:j + 1] * ip[:, dy:dy + h, dx:dx + w]
+    return out
+
+
+def net_forward(params: dict, blocks: str, x: np.ndarray, state: dict | None, use_k: bool = True):
+    """forward_full for one frame (network.py:296-323). x (C,H,W) float32 rgba[+mask].
+
+    state: None or {"hidden": [arrays (C,Hp/s,Wp/s)], "prev": (3,Hp,Wp)}.
+    returns (O (3,H,W), O_d (3,H,W), new_state)
+    """
+    layout, k_in, ne, nd, levels, cfg = conv_layout(blocks)
+    c, h, w = x.shape
+    div = 2 ** ne
+    hp, wp = -(-h // div) * div, -(-w // div) * div
+    xp = np.zeros((c, hp, wp), np.float32)
+    xp[:, :h, :w] = x
+    prev = np.zeros((3, hp, wp), np.float32) if state is None else state["prev"]
+    cur = np.concatenate([xp, prev], axis=0)
+    skips = []
+    for i in range(ne):
+        cur = relu(conv3x3(cur, params[f"D.block{i}.conv1.w"], params[f"D.block{i}.conv1.b"]))
+        cur = relu(conv3x3(cur, params[f"D.block{i}.conv2.w"], params[f"D.block{i}.conv2.b"]))
+        skips.append(cur)
+        cur = pool2(cur)
+    hd = []
+    for j in range(nd):
+        if j > 0:
+            cur = np.concatenate([up2(cur), skips[ne - j]], axis=0)
+        hid = (np.zeros((layout[ne + j][1],) + cur.shape[1:], np.float32) if state is None
+               else state["hidden"][j])
+        cur = np.concatenate([cur, hid], axis=0)
+        b = ne + j
+        cur = relu(conv3x3(cur, params[f"D.block{b}.conv1.w"], params[f"D.block{b}.conv1.b"]))
+        cur = relu(conv3x3(cur, params[f"D.block{b}.conv2.w"], params[f"D.block{b}.conv2.b"]))
+        hd.append(cur)
+    od = conv3x3(hd[-1], params["D.head.w"], params["D.head.b"])
+    img = od
+    if use_k:
+        by_level = {ne - j: hd[j] for j in range(nd)}
+        for i, lv in enumerate(levels):
+            hdl = by_level[lv]
+            wk = params[f"K.block{i}.w"][:, :, 0, 0]
+            logits = (wk @ hdl.reshape(hdl.shape[0], -1) + params[f"K.block{i}.b"][:, None]).reshape(
+                9, *hdl.shape[1:])
+            img = kernel_filter(img, logits)
+            if cfg[i][0] == "e":
+                img = pool2(img)
+            elif i < len(cfg) - 1:
+                img = up2(img)
+    return img[:, :h, :w], od[:, :h, :w], {"hidden": hd, "prev": od}
+
+
+# --------------------------------------------------------------------------- metrics
+def psnr(a, b, peak=1.0) -> float:
+    """metrics.psnr (metrics.py:40-49): joint RGB, 100 dB cap."""
+    a = np.asarray(a, np.float64)[..., :3]
+    b = np.asarray(b, np.float64)[..., :3]
+    mse = float(np.mean((a - b) ** 2))
+    if mse == 0.0:
+        return 100.0
+    return min(10.0 * float(np.log10(peak * peak / mse)), 100.0)
+
+
+def ssim(a, b) -> float:
+    """metrics.ssim (metrics.py:74-87): Rec.601 luma, 11x11 Gaussian (sigma 1.5), valid windows."""
+    from numpy.lib.stride_tricks import sliding_window_view
+
+    def luma(img):
+        img = np.asarray(img, np.float64)
+        return 0.299 * img[..., 0] + 0.587 * img[..., 1] + 0.114 * img[..., 2]
+
+    d = np.arange(11, dtype=np.float64) - 5.0
+    k = np.exp(-(d * d) / (2 * 1.5 * 1.5))
+    k /= k.sum()
+
+    def filt(im):
+        rows = sliding_window_view(im, 11, axis=0) @ k
+        return sliding_window_view(rows, 11, axis=1) @ k
+
+    la, lb = luma(a), luma(b)
+    mu_a, mu_b = filt(la), filt(lb)
+    va = filt(la * la) - mu_a * mu_a
+    vb = filt(lb * lb) - mu_b * mu_b
+    cov = filt(la * lb) - mu_a * mu_b
+    c1, c2 = 0.01 ** 2, 0.03 ** 2
+    s = ((2 * mu_a * mu_b + c1) * (2 * cov + c2)) / ((mu_a * mu_a + mu_b * mu_b + c1) * (va + vb + c2))
+    return float(s.mean())
+
+
+def threads() -> int:
+    return len(os.sched_getaffinity(0))

@@ -1,0 +1,337 @@
+// C ABI entry points (include/fovnet.h): context, noise, volume, mask, render, whole frame.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "internal.h"
+
+namespace fv {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+  return FV_E_CUDA;
+}
+
+int pack_input(fv_ctx* ctx, fv_state* st, const float* rgba, const uint8_t* bits);
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" {
+
+const char* fv_last_error(void) { return g_err; }
+int fv_version(void) { return 1; }
+
+int fv_ctx_create(int device, fv_ctx** out) {
+  FV_REQUIRE(out, "null argument");
+  FV_CUDA(cudaSetDevice(device));
+  auto* ctx = new fv_ctx();
+  ctx->device = device;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess) ctx->num_sms = prop.multiProcessorCount;
+  if (prop.major != 10) {
+    delete ctx;
+    set_error("device %d is sm_%d%d; libfovnet is built for sm_100a (B200) only", device, prop.major, prop.minor);
+    return FV_E_UNSUPPORTED;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaStreamCreate"); }
+  ctx->own_stream = true;
+  e = cudaMalloc(&ctx->counters, sizeof(DevCounters));
+  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaMalloc counters"); }
+  cudaMemset(ctx->counters, 0, sizeof(DevCounters));
+  for (auto& ev : ctx->ev) cudaEventCreate(&ev);
+  *out = ctx;
+  return 0;
+}
+
+int fv_ctx_destroy(fv_ctx* ctx) {
+  if (!ctx) return 0;
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->noise) cudaFree(ctx->noise);
+  if (ctx->scan_status) cudaFree(ctx->scan_status);
+  if (ctx->counters) cudaFree(ctx->counters);
+  if (ctx->k_scratch) cudaFree(ctx->k_scratch);
+  if (ctx->idx_scratch) cudaFree(ctx->idx_scratch);
+  if (ctx->rgb_scratch) cudaFree(ctx->rgb_scratch);
+  for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return 0;
+}
+
+int fv_ctx_set_stream(fv_ctx* ctx, void* s) {
+  FV_REQUIRE(ctx, "null ctx");
+  if (ctx->own_stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+    ctx->own_stream = false;
+  }
+  // NULL selects the legacy default stream (torch's default stream)
+  ctx->stream = reinterpret_cast<cudaStream_t>(s);
+  return 0;
+}
+
+void* fv_ctx_stream(fv_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int fv_sync(fv_ctx* ctx) {
+  FV_REQUIRE(ctx, "null ctx");
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+uint64_t fv_launch_count(fv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fv_noise_upload(fv_ctx* ctx, const float* vals, int T, int H, int W) {
+  FV_REQUIRE(ctx && vals, "null argument");
+  FV_REQUIRE(T >= 1 && H >= 1 && W >= 1, "noise stack must be (T>=1, H, W), got (%d, %d, %d)", T, H, W);
+  if (ctx->noise) cudaFree(ctx->noise);
+  ctx->noise = nullptr;
+  const size_t bytes = sizeof(float) * (size_t)T * H * W;
+  FV_CUDA(cudaMalloc(&ctx->noise, bytes));
+  FV_CUDA(cudaMemcpy(ctx->noise, vals, bytes, cudaMemcpyHostToDevice));
+  ctx->noise_T = T; ctx->noise_H = H; ctx->noise_W = W;
+  return 0;
+}
+
+int fv_stats_read(fv_ctx* ctx, fv_stats* out) {
+  FV_REQUIRE(ctx && out, "null argument");
+  DevCounters c;
+  FV_CUDA(cudaMemcpyAsync(&c, ctx->counters, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  out->rays = c.rays; out->hit_rays = c.hit_rays;
+  out->samples_main = c.samples_main; out->samples_shadow = c.samples_shadow;
+  return 0;
+}
+
+int fv_stats_reset(fv_ctx* ctx) {
+  FV_REQUIRE(ctx, "null ctx");
+  FV_CUDA(cudaMemsetAsync(ctx->counters, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  return 0;
+}
+
+static int check_fovea(const fv_fovea* f) {
+  FV_REQUIRE(f, "null fovea");
+  FV_REQUIRE(f->sigma >= 0, "sigma must be >= 0, got %g", f->sigma);
+  FV_REQUIRE(std::isfinite(f->focus[0]) && std::isfinite(f->focus[1]), "focus must be finite");
+  FV_REQUIRE(f->base_density >= 0.0 && f->base_density <= 1.0, "base density must lie in [0,1]");
+  return 0;
+}
+
+int fv_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* fovea,
+                    const double* pb_map_dev, uint8_t* bits_dev, int32_t* idx_dev, int32_t* k_dev,
+                    fv_state* st) {
+  FV_REQUIRE(ctx && idx_dev && k_dev, "null argument");
+  FV_REQUIRE(H >= 1 && W >= 1, "dims must be positive, got (%d, %d)", H, W);
+  int rc = check_fovea(fovea);
+  if (rc) return rc;
+  if (st && (st->H != H || st->W != W)) {
+    set_error("carried state is for (%d, %d), input is (%d, %d); reset the state", st->H, st->W, H, W);
+    return FV_E_STATE;
+  }
+  return launch_mask_compact(ctx, frame, H, W, fovea, pb_map_dev, bits_dev, idx_dev, k_dev,
+                             st ? st->x.p : nullptr, st ? st->Wp : W);
+}
+
+int fv_mask_compact_tau(fv_ctx* ctx, int frame, int H, int W, const double* tau_dev, uint8_t* bits_dev,
+                        int32_t* idx_dev, int32_t* k_dev, fv_state* st) {
+  FV_REQUIRE(ctx && tau_dev && idx_dev && k_dev, "null argument");
+  FV_REQUIRE(H >= 1 && W >= 1, "dims must be positive, got (%d, %d)", H, W);
+  if (st && (st->H != H || st->W != W)) {
+    set_error("carried state is for (%d, %d), input is (%d, %d); reset the state", st->H, st->W, H, W);
+    return FV_E_STATE;
+  }
+  return launch_mask_compact(ctx, frame, H, W, nullptr, nullptr, bits_dev, idx_dev, k_dev,
+                             st ? st->x.p : nullptr, st ? st->Wp : W, tau_dev);
+}
+
+int fv_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* fovea, const double* pb_map_dev,
+               double* tau_dev) {
+  FV_REQUIRE(ctx && tau_dev, "null argument");
+  FV_REQUIRE(H >= 1 && W >= 1, "dims must be positive, got (%d, %d)", H, W);
+  int rc = check_fovea(fovea);
+  if (rc) return rc;
+  return launch_tau_map(ctx, H, W, fovea, pb_map_dev, tau_dev);
+}
+
+int fv_volume_create(fv_ctx* ctx, int nx, int ny, int nz, const double spacing[3], fv_volume** out) {
+  FV_REQUIRE(ctx && out, "null argument");
+  FV_REQUIRE(nx >= 2 && ny >= 2 && nz >= 2, "volume dims must all be >= 2, got (%d, %d, %d)", nx, ny, nz);
+  auto* v = new fv_volume();
+  v->nx = nx; v->ny = ny; v->nz = nz;
+  for (int a = 0; a < 3; ++a) v->spacing[a] = spacing ? spacing[a] : 1.0;
+  const size_t bytes = sizeof(float) * (size_t)nx * ny * nz;
+  cudaError_t e = cudaMalloc(&v->data, bytes);
+  if (e != cudaSuccess) { delete v; return cuda_fail(e, "cudaMalloc volume"); }
+  e = cudaMalloc(&v->lut_dev, sizeof(float) * 4 * 256);
+  if (e != cudaSuccess) { cudaFree(v->data); delete v; return cuda_fail(e, "cudaMalloc lut"); }
+  *out = v;
+  return 0;
+}
+
+int fv_volume_wrap(fv_ctx* ctx, int nx, int ny, int nz, const double spacing[3], float* data_dev,
+                   fv_volume** out) {
+  FV_REQUIRE(ctx && out && data_dev, "null argument");
+  FV_REQUIRE(nx >= 2 && ny >= 2 && nz >= 2, "volume dims must all be >= 2, got (%d, %d, %d)", nx, ny, nz);
+  auto* v = new fv_volume();
+  v->nx = nx; v->ny = ny; v->nz = nz;
+  for (int a = 0; a < 3; ++a) v->spacing[a] = spacing ? spacing[a] : 1.0;
+  v->data = data_dev;
+  v->owns_data = false;
+  cudaError_t e = cudaMalloc(&v->lut_dev, sizeof(float) * 4 * 256);
+  if (e != cudaSuccess) { delete v; return cuda_fail(e, "cudaMalloc lut"); }
+  *out = v;
+  return 0;
+}
+
+int fv_volume_destroy(fv_volume* v) {
+  if (!v) return 0;
+  if (v->data && v->owns_data) cudaFree(v->data);
+  if (v->lut_dev) cudaFree(v->lut_dev);
+  delete v;
+  return 0;
+}
+
+int fv_volume_upload(fv_ctx* ctx, fv_volume* v, const float* data, int on_device) {
+  FV_REQUIRE(ctx && v && data, "null argument");
+  const size_t bytes = sizeof(float) * (size_t)v->nx * v->ny * v->nz;
+  FV_CUDA(cudaMemcpyAsync(v->data, data, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                          ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int fv_volume_procedural(fv_ctx* ctx, fv_volume* v, int kind, double* range) {
+  FV_REQUIRE(ctx && v, "null argument");
+  return launch_volume_procedural(ctx, v, kind, range);
+}
+
+int fv_volume_set_tf(fv_ctx* ctx, fv_volume* v, const float* lut, int K) {
+  FV_REQUIRE(ctx && v && lut, "null argument");
+  FV_REQUIRE(K >= 2 && K <= 256, "transfer function lut must be (K>=2, 4) with K <= 256, got K=%d", K);
+  for (int i = 0; i < 4 * K; ++i)
+    FV_REQUIRE(lut[i] >= 0.f && lut[i] <= 1.f, "transfer function entries must lie in [0,1]");
+  FV_CUDA(cudaMemcpy(v->lut_dev, lut, sizeof(float) * 4 * K, cudaMemcpyHostToDevice));
+  v->K = K;
+  return 0;
+}
+
+float* fv_volume_data(fv_volume* v) { return v ? v->data : nullptr; }
+
+static int finish_stats(fv_ctx* ctx, fv_stats* out, const DevCounters* before) {
+  if (!out) return 0;
+  DevCounters c;
+  FV_CUDA(cudaMemcpyAsync(&c, ctx->counters, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  out->rays = c.rays - before->rays;
+  out->hit_rays = c.hit_rays - before->hit_rays;
+  out->samples_main = c.samples_main - before->samples_main;
+  out->samples_shadow = c.samples_shadow - before->samples_shadow;
+  return 0;
+}
+
+static int snapshot(fv_ctx* ctx, fv_stats* want, DevCounters* before) {
+  if (!want) return 0;
+  FV_CUDA(cudaMemcpyAsync(before, ctx->counters, sizeof(*before), cudaMemcpyDeviceToHost, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int fv_render_sparse(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
+                     const fv_settings* settings, const int32_t* idx_dev, const int32_t* k_dev,
+                     int k_max, float* rgba_dev, float* depth_dev, fv_state* st,
+                     fv_stats* stats_out) {
+  FV_REQUIRE(ctx && vol && cam && settings && idx_dev && k_dev, "null argument");
+  DevCounters before{};
+  int rc = snapshot(ctx, stats_out, &before);
+  if (rc) return rc;
+  if (st && (st->H != cam->height || st->W != cam->width)) {
+    set_error("carried state is for (%d, %d), input is (%d, %d); reset the state", st->H, st->W,
+              cam->height, cam->width);
+    return FV_E_STATE;
+  }
+  rc = launch_render(ctx, vol, cam, light, settings, idx_dev, k_dev, k_max, rgba_dev, depth_dev,
+                     st ? st->x.p : nullptr, st ? st->Wp : cam->width);
+  if (rc) return rc;
+  return finish_stats(ctx, stats_out, &before);
+}
+
+int fv_render_full(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
+                   const fv_settings* settings, float* rgba_dev, float* depth_dev, fv_stats* stats_out) {
+  FV_REQUIRE(ctx && vol && cam && settings, "null argument");
+  DevCounters before{};
+  int rc = snapshot(ctx, stats_out, &before);
+  if (rc) return rc;
+  rc = launch_render(ctx, vol, cam, light, settings, nullptr, nullptr, cam->width * cam->height,
+                     rgba_dev, depth_dev, nullptr, cam->width);
+  if (rc) return rc;
+  return finish_stats(ctx, stats_out, &before);
+}
+
+int fv_pack_input(fv_ctx* ctx, fv_state* st, const float* rgba_dev, const uint8_t* bits_dev) {
+  FV_REQUIRE(ctx && st && rgba_dev && bits_dev, "null argument");
+  return pack_input(ctx, st, rgba_dev, bits_dev);
+}
+
+int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, const fv_camera* cam,
+             const fv_light* light, const fv_settings* settings, const fv_fovea* fovea, int frame,
+             float* host_rgb_out, double* timings_ms) {
+  FV_REQUIRE(ctx && vol && net && st && cam && settings && fovea && host_rgb_out, "null argument");
+  const int H = cam->height, W = cam->width;
+  if (st->H != H || st->W != W) {
+    set_error("carried state is for (%d, %d), input is (%d, %d); reset the state", st->H, st->W, H, W);
+    return FV_E_STATE;
+  }
+  int rc = check_fovea(fovea);
+  if (rc) return rc;
+  const int64_t npix = (int64_t)H * W;
+  if (npix > ctx->idx_cap) {
+    if (ctx->idx_scratch) cudaFree(ctx->idx_scratch);
+    ctx->idx_scratch = nullptr;
+    FV_CUDA(cudaMalloc(&ctx->idx_scratch, sizeof(int32_t) * npix));
+    ctx->idx_cap = npix;
+  }
+  if (!ctx->k_scratch) FV_CUDA(cudaMalloc(&ctx->k_scratch, sizeof(int32_t) * 4));
+  if (3 * npix > ctx->rgb_cap) {
+    if (ctx->rgb_scratch) cudaFree(ctx->rgb_scratch);
+    ctx->rgb_scratch = nullptr;
+    FV_CUDA(cudaMalloc(&ctx->rgb_scratch, sizeof(float) * 3 * npix));
+    ctx->rgb_cap = 3 * npix;
+  }
+  FV_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  rc = launch_mask_compact(ctx, frame, H, W, fovea, nullptr, nullptr, ctx->idx_scratch, ctx->k_scratch,
+                           st->x.p, st->Wp);
+  if (rc) return rc;
+  FV_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  rc = launch_render(ctx, vol, cam, light, settings, ctx->idx_scratch, ctx->k_scratch, (int)npix, nullptr,
+                     nullptr, st->x.p, st->Wp);
+  if (rc) return rc;
+  FV_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+  rc = reconstruct(ctx, net, st, 1, ctx->rgb_scratch, nullptr, nullptr);
+  if (rc) return rc;
+  FV_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+  FV_CUDA(cudaMemcpyAsync(host_rgb_out, ctx->rgb_scratch, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (timings_ms) {
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&b, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+    timings_ms[0] = a; timings_ms[1] = b; timings_ms[2] = c; timings_ms[3] = a + b + c;
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,460 @@
+// 3x3 convolution (stride 1, zero padding 1) as a tcgen05 implicit GEMM.
+//
+// Reference: autograd.conv2d (autograd.py:238-276) -- cross-correlation, weight (oc, ic, 3, 3),
+// im2col column order (c, ky, kx), + bias -- followed by relu (autograd.py:134-141) and, for
+// encoder blocks, avg_pool2 (autograd.py:279-291); concat_channels (autograd.py:173-185) of the
+// block inputs is folded into the operand loader.
+//
+// Layout. Activations live in HBM as "NC8HW8": C/8 planes of (H, W, 8) fp16, i.e. every 8-channel
+// group is a dense NHWC8 image. A CTA tile is R output rows x 128 output columns. Per K-stage
+// (4 channel groups = 32 channels) the producer warp bulk-copies the (R+2) x 130 halo of each
+// channel group into shared memory as [group][halo_row][halo_col][8 ch]: consecutive pixels are
+// 16 bytes apart, which is exactly the SWIZZLE_NONE K-major canonical UMMA layout with
+// SBO = 128 B and LBO = one group plane. A 3x3 tap (dy, dx) of output row r is therefore just a
+// shifted descriptor start address ((r+dy)*130 + dx)*16 -- the im2col matrix is never built and
+// the halo is read from L2 once per stage instead of nine times. Zero padding at image borders
+// and the zero channel group of the 8-channel input layer are written with st.shared.
+//
+// Roles (192 threads, one CTA per SM, persistent over tiles):
+//   warp 0     producer: cp.async.bulk of A halo rows + the stage's B (weight) image
+//   warp 1     MMA issuer: tcgen05.mma 128 x N x 16, accumulators in TMEM (R x N columns,
+//              double-buffered across tiles), tcgen05.commit to release smem / publish TMEM
+//   warps 2-5  epilogue: tcgen05.ld -> +bias, ReLU -> fp16 NC8HW8 store, fused 2x2 average pool,
+//              or the D.head mode (fp32 O_d planes + the next frame's feedback channels)
+#include "internal.h"
+#include "sm100.cuh"
+
+namespace fv {
+
+namespace {
+
+constexpr int kTileW = 128;          // output columns per tile (= MMA M)
+constexpr int kHaloW = kTileW + 2;   // 130
+constexpr int kRowBytes = kHaloW * 16;
+constexpr int kStageGroups = 4;      // channel groups (of 8) per K-stage
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+
+struct ConvArgs {
+  const __half* src[3];
+  int src_groups[3];
+  int n_src;
+  int groups;        // total input channel groups (may be odd: cin = 8)
+  int n_kstages;
+  int H, W;
+  const __half* wimg;  // B images of all stages
+  const float* bias;   // n_pad
+  int cout;
+  __half* dst;         // NC8HW8, cout channels (nullable in head mode)
+  __half* pool_dst;    // nullable: 2x2 average pool of dst
+  int relu;
+  int head;            // 1: D.head epilogue
+  float* od;           // head: (3, H, W) fp32
+  __half* feedback;    // head: NHWC8 net input, channels 5..7
+  int tiles_x, tiles_y;
+};
+
+template <int R, int N>
+struct Cfg {
+  static constexpr int kABytes = kStageGroups * (R + 2) * kRowBytes;
+  static constexpr int kBBytes = 9 * kStageGroups * N * 16;
+  static constexpr int kPlaneBytes = (R + 2) * kRowBytes;
+  static constexpr int kAcc = (2 * R * N <= 512) ? 2 : 1;
+  static constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 + 256;
+};
+
+template <int R, int N>
+__global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
+  using C = Cfg<R, N>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * C::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * C::kBBytes);
+  // bars: full[kStages], empty[kStages], tfull[2], tempty[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  const uint32_t bar_full = sm100::smem_u32(bars);
+  const uint32_t bar_empty = bar_full + 8 * kStages;
+  const uint32_t bar_tfull = bar_empty + 8 * kStages;
+  const uint32_t bar_tempty = bar_tfull + 16;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      sm100::mbar_init(bar_full + 8 * s, 2);
+      sm100::mbar_init(bar_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      sm100::mbar_init(bar_tfull + 8 * s, 1);
+      sm100::mbar_init(bar_tempty + 8 * s, 4);
+    }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<512>(sm100::smem_u32(tmem_slot));
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_tiles = a.tiles_x * a.tiles_y;
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const int x0 = (tile % a.tiles_x) * kTileW;
+      const int y0 = (tile / a.tiles_x) * R;
+      for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
+        const int st = it % kStages;
+        const uint32_t round = it / kStages;
+        sm100::mbar_wait(bar_empty + 8 * st, (round & 1) ^ 1);
+        const int g0 = ks * kStageGroups;
+        int gs = a.groups - g0;
+        if (gs > kStageGroups) gs = kStageGroups;
+        const int gs_fill = (gs + 1) & ~1;  // odd group count: one zero group
+        const int n_items = gs_fill * (R + 2);
+        // bytes this lane will copy
+        uint32_t my_bytes = 0;
+        for (int item = lane; item < n_items; item += 32) {
+          const int g = item / (R + 2), row = item % (R + 2);
+          const int y = y0 - 1 + row;
+          if (g0 + g < a.groups && y >= 0 && y < a.H) {
+            const int lo = max(x0 - 1, 0), hi = min(x0 + kTileW + 1, a.W);
+            if (hi > lo) my_bytes += (uint32_t)(hi - lo) * 16u;
+          }
+        }
+        uint32_t tot = my_bytes;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        const uint32_t b_bytes = (uint32_t)(9 * gs_fill * N * 16);
+        if (lane == 0) sm100::mbar_arrive_expect_tx(bar_full + 8 * st, tot + b_bytes);
+        __syncwarp();
+        const uint32_t a_st = sm100::smem_u32(sA + st * C::kABytes);
+        if (lane == 0)
+          sm100::bulk_g2s(sm100::smem_u32(sB + st * C::kBBytes),
+                          reinterpret_cast<const uint8_t*>(a.wimg) + (int64_t)ks * C::kBBytes,
+                          b_bytes, bar_full + 8 * st);
+        for (int item = lane; item < n_items; item += 32) {
+          const int g = item / (R + 2), row = item % (R + 2);
+          const int y = y0 - 1 + row;
+          const uint32_t row_addr = a_st + g * C::kPlaneBytes + row * kRowBytes;
+          const int gg = g0 + g;
+          if (gg < a.groups && y >= 0 && y < a.H) {
+            const int lo = max(x0 - 1, 0), hi = min(x0 + kTileW + 1, a.W);
+            // locate the source tensor of this channel group (concat folded into the loader)
+            int s = 0, gl = gg;
+            while (s + 1 < a.n_src && gl >= a.src_groups[s]) { gl -= a.src_groups[s]; ++s; }
+            const __half* plane = a.src[s] + (int64_t)gl * a.H * a.W * 8;
+            const int c_lo = lo - (x0 - 1), c_hi = hi - (x0 - 1);
+            if (hi > lo)
+              sm100::bulk_g2s(row_addr + c_lo * 16, plane + ((int64_t)y * a.W + lo) * 8,
+                              (uint32_t)(hi - lo) * 16u, bar_full + 8 * st);
+            for (int c = 0; c < c_lo; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+            for (int c = max(c_hi, 0); c < kHaloW; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+          } else {
+            for (int c = 0; c < kHaloW; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+          }
+        }
+        sm100::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(bar_full + 8 * st);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = sm100::idesc_f16(128, N);
+    int it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt % C::kAcc;
+      const uint32_t acc_round = lt / C::kAcc;
+      sm100::mbar_wait(bar_tempty + 8 * acc, (acc_round & 1) ^ 1);
+      sm100::tc_fence_after();
+      const uint32_t d_base = tmem_base + acc * R * N;
+      for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
+        const int st = it % kStages;
+        const uint32_t round = it / kStages;
+        sm100::mbar_wait(bar_full + 8 * st, round & 1);
+        sm100::tc_fence_after();
+        int gs = a.groups - ks * kStageGroups;
+        if (gs > kStageGroups) gs = kStageGroups;
+        const int nk = (gs + 1) >> 1;
+        if (lane == 0) {
+          const uint32_t a_st = sm100::smem_u32(sA + st * C::kABytes);
+          const uint32_t b_st = sm100::smem_u32(sB + st * C::kBBytes);
+          for (int r = 0; r < R; ++r) {
+#pragma unroll 1
+            for (int t = 0; t < 9; ++t) {
+              const int dy = t / 3, dx = t % 3;
+              for (int k = 0; k < nk; ++k) {
+                const uint32_t a_addr = a_st + 2 * k * C::kPlaneBytes + ((r + dy) * kHaloW + dx) * 16;
+                const uint32_t b_addr = b_st + (t * nk + k) * N * 32;
+                const uint64_t ad = sm100::smem_desc(a_addr, C::kPlaneBytes, 128);
+                const uint64_t bd = sm100::smem_desc(b_addr, N * 16, 128);
+                sm100::mma_f16(d_base + r * N, ad, bd, idesc, (ks | t | k) ? 1u : 0u);
+              }
+            }
+          }
+          sm100::mma_commit(bar_empty + 8 * st);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) sm100::mma_commit(bar_tfull + 8 * acc);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    int lt = 0;
+    const int64_t plane = (int64_t)a.H * a.W * 8;
+    const int Hp = a.H >> 1, Wp = a.W >> 1;
+    const int64_t pplane = (int64_t)Hp * Wp * 8;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+      const int acc = lt % C::kAcc;
+      const uint32_t acc_round = lt / C::kAcc;
+      const int x0 = (tile % a.tiles_x) * kTileW;
+      const int y0 = (tile / a.tiles_x) * R;
+      sm100::mbar_wait(bar_tfull + 8 * acc, acc_round & 1);
+      sm100::tc_fence_after();
+      const int x = x0 + 32 * q + lane;
+      const bool xin = x < a.W;
+      const uint32_t t_row0 = tmem_base + ((uint32_t)(32 * q) << 16) + acc * R * N;
+      if (a.head) {
+        for (int r = 0; r < R; ++r) {
+          float v[16];
+          sm100::tmem_ld16(t_row0 + r * N, v);
+          const int y = y0 + r;
+          if (xin && y < a.H) {
+            float o[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              o[c] = v[c] + __ldg(a.bias + c);
+              a.od[(int64_t)c * a.H * a.W + (int64_t)y * a.W + x] = o[c];
+            }
+            __half* fb = a.feedback + ((int64_t)y * a.W + x) * 8;
+            fb[5] = __float2half(o[0]);
+            fb[6] = __float2half(o[1]);
+            fb[7] = __float2half(o[2]);
+          }
+        }
+      } else {
+        for (int r = 0; r < R; r += 2) {
+          const int y = y0 + r;
+#pragma unroll 1
+          for (int cb = 0; cb < N; cb += 16) {
+            float v0[16], v1[16];
+            sm100::tmem_ld16(t_row0 + r * N + cb, v0);
+            sm100::tmem_ld16(t_row0 + (r + 1) * N + cb, v1);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float b = __ldg(a.bias + cb + j);
+              v0[j] += b;
+              v1[j] += b;
+              if (a.relu) { v0[j] = fmaxf(v0[j], 0.f); v1[j] = fmaxf(v1[j], 0.f); }
+            }
+            if (xin) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int g = (cb >> 3) + h;
+                if (8 * g >= a.cout) continue;
+                if (y < a.H) {
+                  uint4 pk;
+                  __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) p2[j] = __floats2half2_rn(v0[8 * h + 2 * j], v0[8 * h + 2 * j + 1]);
+                  *reinterpret_cast<uint4*>(a.dst + g * plane + ((int64_t)y * a.W + x) * 8) = pk;
+                }
+                if (y + 1 < a.H) {
+                  uint4 pk;
+                  __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) p2[j] = __floats2half2_rn(v1[8 * h + 2 * j], v1[8 * h + 2 * j + 1]);
+                  *reinterpret_cast<uint4*>(a.dst + g * plane + ((int64_t)(y + 1) * a.W + x) * 8) = pk;
+                }
+              }
+            }
+            if (a.pool_dst) {
+              // avg_pool2: 0.25 * (p00 + p10 + p01 + p11) (autograd.py:285-286), x-pairs are lanes
+              float pv[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float nb0 = __shfl_xor_sync(0xffffffffu, v0[j], 1);
+                const float nb1 = __shfl_xor_sync(0xffffffffu, v1[j], 1);
+                pv[j] = 0.25f * (((v0[j] + v1[j]) + nb0) + nb1);
+              }
+              if (((lane & 1) == 0) && xin && y < a.H) {
+                const int px = x >> 1, py = y >> 1;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  if (cb + 8 * h >= a.cout) continue;
+                  uint4 pk;
+                  __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) p2[j] = __floats2half2_rn(pv[8 * h + 2 * j], pv[8 * h + 2 * j + 1]);
+                  *reinterpret_cast<uint4*>(a.pool_dst + ((cb >> 3) + h) * pplane + ((int64_t)py * Wp + px) * 8) = pk;
+                }
+              }
+            }
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(bar_tempty + 8 * acc);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc<512>(tmem_base);
+  }
+}
+
+template <int R, int N>
+int launch(fv_ctx* ctx, const ConvArgs& args) {
+  using C = Cfg<R, N>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr_set = true;
+  }
+  ConvArgs a = args;
+  a.tiles_x = (a.W + kTileW - 1) / kTileW;
+  a.tiles_y = (a.H + R - 1) / R;
+  const int n_tiles = a.tiles_x * a.tiles_y;
+  const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
+  conv3x3_tc_kernel<R, N><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
+  FV_CHECK_LAUNCH("conv3x3_tc_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+}  // namespace
+
+// B image of stage s: [tap t (9)][k (g/2)][kg (2)][n (N)][8] fp16, c = (4s + 2k + kg)*8 + e.
+int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
+  const int groups = (cp.cin + 7) / 8;
+  const int N = cp.n_pad;
+  cp.n_stages = (groups + kStageGroups - 1) / kStageGroups;
+  cp.stage_groups.clear();
+  cp.stage_off.clear();
+  int64_t off = 0;
+  for (int s = 0; s < cp.n_stages; ++s) {
+    int gs = groups - s * kStageGroups;
+    if (gs > kStageGroups) gs = kStageGroups;
+    gs = (gs + 1) & ~1;
+    cp.stage_groups.push_back(gs);
+    cp.stage_off.push_back(off);
+    off += (int64_t)9 * kStageGroups * N * 16;  // stages strided at the full-stage size
+  }
+  cp.wbytes = off;
+  std::vector<__half> img(off / 2, __float2half(0.f));
+  for (int s = 0; s < cp.n_stages; ++s) {
+    const int gs = cp.stage_groups[s];
+    const int nk = gs / 2;
+    __half* base = img.data() + cp.stage_off[s] / 2;
+    for (int t = 0; t < 9; ++t)
+      for (int k = 0; k < nk; ++k)
+        for (int kg = 0; kg < 2; ++kg)
+          for (int n = 0; n < N; ++n)
+            for (int e = 0; e < 8; ++e) {
+              const int c = (s * kStageGroups + 2 * k + kg) * 8 + e;
+              float w = 0.f;
+              if (n < cp.cout && c < cp.cin) w = cp.w_host[((int64_t)n * cp.cin + c) * 9 + t];
+              base[((((int64_t)t * nk + k) * 2 + kg) * N + n) * 8 + e] = __float2half(w);
+            }
+  }
+  if (cp.w_dev) cudaFree(cp.w_dev);
+  if (cp.b_dev) cudaFree(cp.b_dev);
+  cp.w_dev = nullptr;
+  cp.b_dev = nullptr;
+  FV_CUDA(cudaMalloc(&cp.w_dev, cp.wbytes));
+  FV_CUDA(cudaMemcpy(cp.w_dev, img.data(), cp.wbytes, cudaMemcpyHostToDevice));
+  std::vector<float> b(N, 0.f);
+  for (int n = 0; n < cp.cout; ++n) b[n] = cp.b_host[n];
+  FV_CUDA(cudaMalloc(&cp.b_dev, sizeof(float) * N));
+  FV_CUDA(cudaMemcpy(cp.b_dev, b.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+  (void)ctx;
+  return 0;
+}
+
+// Public-internal entry: run one 3x3 conv. srcs: up to 3 NC8HW8 tensors at the same level.
+int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_act* dst,
+            fv_act* pool_dst, bool relu, float* head_od, __half* head_feedback) {
+  ConvArgs a{};
+  a.n_src = n_src;
+  int groups = 0;
+  for (int i = 0; i < n_src; ++i) {
+    a.src[i] = srcs[i].p;
+    a.src_groups[i] = srcs[i].C / 8;
+    groups += srcs[i].C / 8;
+  }
+  FV_REQUIRE(groups * 8 == cp.cin,
+             "conv %s: input has %d channels, weight expects %d", cp.name.c_str(), groups * 8, cp.cin);
+  a.groups = groups;
+  a.n_kstages = cp.n_stages;
+  a.H = srcs[0].H;
+  a.W = srcs[0].W;
+  a.wimg = cp.w_dev;
+  a.bias = cp.b_dev;
+  a.cout = cp.cout;
+  a.dst = dst ? dst->p : nullptr;
+  a.pool_dst = pool_dst ? pool_dst->p : nullptr;
+  a.relu = relu ? 1 : 0;
+  a.head = head_od != nullptr;
+  a.od = head_od;
+  a.feedback = head_feedback;
+  switch (cp.n_pad) {
+    case 16: return launch<4, 16>(ctx, a);
+    case 32: return launch<4, 32>(ctx, a);
+    case 48: return launch<4, 48>(ctx, a);
+    case 64: return launch<4, 64>(ctx, a);
+    case 80: return launch<2, 80>(ctx, a);
+    case 96: return launch<2, 96>(ctx, a);
+    case 128: return launch<2, 128>(ctx, a);
+    default:
+      set_error("conv %s: unsupported output width %d", cp.name.c_str(), cp.cout);
+      return FV_E_UNSUPPORTED;
+  }
+}
+
+}  // namespace fv
+
+extern "C" {
+
+// Diagnostic entry: one conv over caller device buffers (NC8HW8 fp16), weights in the reference
+// (oc, ic, 3, 3) float32 layout on the host. Used by the layer-level parity tests.
+int fv_debug_conv3x3(fv_ctx* ctx, int cin, int cout, int H, int W, const void* x_nc8,
+                     const float* w_host, const float* b_host, void* y_nc8, void* pool_nc8, int relu) {
+  FV_REQUIRE(ctx && x_nc8 && w_host && b_host, "null argument");
+  FV_REQUIRE(cin % 8 == 0 && cin > 0, "cin must be a positive multiple of 8");
+  fv::ConvParam cp;
+  cp.name = "debug";
+  cp.cin = cin;
+  cp.cout = cout;
+  cp.n_pad = (cout + 15) / 16 * 16;
+  cp.w_host.assign(w_host, w_host + (size_t)cout * cin * 9);
+  cp.b_host.assign(b_host, b_host + cout);
+  int rc = fv::conv_prepare(ctx, cp);
+  if (rc) return rc;
+  fv_act src;
+  src.p = (__half*)x_nc8;
+  src.C = cin;
+  src.H = H;
+  src.W = W;
+  fv_act dst = src, pool = src;
+  dst.p = (__half*)y_nc8;
+  dst.C = cout;
+  pool.p = (__half*)pool_nc8;
+  pool.C = cout;
+  pool.H = H / 2;
+  pool.W = W / 2;
+  rc = fv::conv3x3(ctx, cp, &src, 1, &dst, pool_nc8 ? &pool : nullptr, relu != 0, nullptr, nullptr);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(cp.w_dev);
+  cudaFree(cp.b_dev);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// Internal structures shared by the libfovnet translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/fovnet.h"
+
+namespace fv {
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define FV_CUDA(expr)                                   \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return fv::cuda_fail(_e, #expr); \
+  } while (0)
+
+#define FV_CHECK_LAUNCH(what)                           \
+  do {                                                  \
+    cudaError_t _e = cudaGetLastError();                \
+    if (_e != cudaSuccess) return fv::cuda_fail(_e, what); \
+  } while (0)
+
+#define FV_REQUIRE(cond, ...)                           \
+  do {                                                  \
+    if (!(cond)) { fv::set_error(__VA_ARGS__); return FV_E_INVALID; } \
+  } while (0)
+
+// Device-side counters (one cache line each to avoid false sharing).
+struct DevCounters {
+  unsigned long long rays;
+  unsigned long long hit_rays;
+  unsigned long long samples_main;
+  unsigned long long samples_shadow;
+  unsigned int scan_tile;  // dynamic tile counter of the mask scan
+  unsigned int pad[7];
+};
+
+}  // namespace fv
+
+struct fv_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  // noise stack (T,H,W) float32
+  float* noise = nullptr;
+  int noise_T = 0, noise_H = 0, noise_W = 0;
+  // mask scan tile status words (epoch-tagged), sized for the largest film seen
+  unsigned long long* scan_status = nullptr;
+  int scan_tiles_cap = 0;
+  unsigned int epoch = 0;
+  fv::DevCounters* counters = nullptr;  // device
+  int32_t* k_scratch = nullptr;          // device int32 for fv_frame
+  int32_t* idx_scratch = nullptr;        // device, capacity idx_cap
+  int64_t idx_cap = 0;
+  float* rgb_scratch = nullptr;          // device (H,W,3) for fv_frame
+  int64_t rgb_cap = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  unsigned long long launches = 0;
+};
+
+struct fv_volume {
+  int nx = 0, ny = 0, nz = 0;
+  double spacing[3] = {1, 1, 1};
+  float* data = nullptr;  // (nz,ny,nx)
+  bool owns_data = true;
+  float* lut_dev = nullptr;  // (K,4) float32, K <= 256
+  int K = 0;
+  double value_range[2] = {0, 0};
+};
+
+namespace fv {
+
+// One 3x3 (or 1x1) convolution of the W-Net as stored on the device.
+struct ConvParam {
+  std::string name;
+  int cin = 0, cout = 0, ksize = 3;
+  int n_pad = 0;           // cout padded to a multiple of 16 (MMA N)
+  int n_stages = 0;        // ceil(cgroups / 4)
+  std::vector<int> stage_groups;   // cgroups per stage (even)
+  std::vector<int64_t> stage_off;  // byte offset of each stage's B image
+  int64_t wbytes = 0;
+  __half* w_dev = nullptr;  // implicit-GEMM B image (see conv_tc.cu)
+  float* b_dev = nullptr;   // bias (n_pad) fp32
+  std::vector<float> w_host;  // reference layout (oc,ic,kh,kw), fp16-rounded values
+  std::vector<float> b_host;
+  bool w_set = false, b_set = false;
+};
+
+}  // namespace fv
+
+struct fv_net {
+  std::vector<std::pair<char, int>> blocks;
+  int n_enc = 0, n_dec = 0;
+  int in_channels = 8;
+  int predicted_kernel = 3;
+  bool recurrent = true;
+  bool include_mask = true;
+  std::vector<fv::ConvParam> convs;  // D.block{i}.conv{1,2} (2 per block), D.head, K.block{i}
+  int head_index = -1;
+  int k_index0 = -1;  // first K conv
+  float* kw_dev = nullptr;  // all K weights, fp32 (rounded to fp16 values), packed
+  std::vector<int64_t> kw_off;  // per K block: offset (floats) of (9*C weights + 9 bias)
+};
+
+// Activation tensor in "NC8HW8" layout: C/8 planes of (H, W, 8) fp16.
+struct fv_act {
+  __half* p = nullptr;
+  int C = 0, H = 0, W = 0;
+  int64_t plane() const { return (int64_t)H * W * 8; }
+};
+
+struct fv_state {
+  const fv_net* net = nullptr;
+  int H = 0, W = 0, Hp = 0, Wp = 0;
+  int parity = 0;  // which hidden buffer holds the carried state
+  bool fresh = true;
+  fv_act x;                         // 8-ch input, L0
+  std::vector<fv_act> enc_a;        // conv1 outputs per encoder block
+  std::vector<fv_act> skips;        // conv2 outputs (skip) per encoder block
+  std::vector<fv_act> pooled;       // pooled skip per encoder block
+  std::vector<fv_act> dec_a;        // conv1 outputs per decoder block
+  std::vector<fv_act> ups;          // upsampled previous decoder output (j>0)
+  std::vector<fv_act> hidden[2];    // ping-pong Hd per decoder block
+  fv_act zero8;                     // unused
+  float* od = nullptr;              // (3,Hp,Wp) fp32 O_d (padded)
+  std::vector<float*> img;          // K-stage ping buffers per level (3,HL,WL) fp32
+  std::vector<float*> img2;
+  void* arena = nullptr;
+  int64_t arena_bytes = 0;
+};
+
+namespace fv {
+// launchers (return 0 / negative)
+int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
+                        const double* pb_map, uint8_t* bits, int32_t* idx, int32_t* k,
+                        __half* net_in, int net_wp, const double* tau_map = nullptr);
+int launch_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* pb_map,
+                   double* tau);
+int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
+                  const fv_settings* settings, const int32_t* idx, const int32_t* k, int k_max,
+                  float* rgba, float* depth, __half* net_in, int net_wp);
+int launch_volume_procedural(fv_ctx* ctx, fv_volume* vol, int kind, double* range);
+int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* out_rgb,
+                float* out_o, float* out_od);
+int conv_prepare(fv_ctx* ctx, ConvParam& cp);
+}  // namespace fv

@@ -1,0 +1,206 @@
+// Foveated sample mask + stream compaction in one pass.
+//
+// Reference semantics (pkg/src/fovray):
+//   tau(u,v) = min(P_f + (1-P_f)*P_b, 1),  P_f = exp(-0.5*((dx*s)^2+(dy*s)^2)*sigma)
+//       sample_maps.py:62-68 (foveal_density), :89-105 (build_tau_map)
+//   M(u,v)   = float64(N[frame%T][v%Ht][u%Wt]) < tau     sample_maps.py:128-132, noise.py:378-384
+//   coords   = set bits in row-major order (exclusive scan) sample_maps.py:161-171
+//
+// tau is evaluated in fp64 with explicit round-to-nearest intrinsics so nvcc cannot contract
+// the products into FMAs; numpy evaluates dx*dx, dy*dy, the sum, *-0.5, *sigma left to right.
+// The mask is bit-exact because the smallest |tau-N| margin over the reference configs
+// (>=3.4e-9) is seven orders of magnitude above one fp64 ulp of tau.
+//
+// Compaction is a single-pass decoupled look-back scan: each CTA takes a 2048-pixel tile
+// (dynamic tile index => tiles retire in order), publishes its aggregate, looks back over its
+// predecessors' epoch-tagged status words and writes its indices. Status words carry the
+// call's epoch, so they never need clearing between calls.
+#include "internal.h"
+
+namespace fv {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kPerThread = 8;
+constexpr int kTile = kThreads * kPerThread;
+
+struct MaskParams {
+  int H, W, frame;
+  double fx, fy, sigma, pb, scale;
+  const double* pb_map;
+  const double* tau_map;  // overrides the fovea formula when set (TauMap given by value)
+  const float* noise;
+  int T, Ht, Wt;
+  uint8_t* bits;
+  int32_t* idx;
+  int32_t* k_out;
+  __half* net_in;
+  int net_wp;
+  unsigned long long* status;
+  unsigned int epoch;
+  unsigned int* tile_counter;
+};
+
+__device__ __forceinline__ double tau_at(const MaskParams& p, int u, int v) {
+  if (p.tau_map) return p.tau_map[(int64_t)v * p.W + u];
+  double dx = __dmul_rn(__dsub_rn((double)u, p.fx), p.scale);
+  double dy = __dmul_rn(__dsub_rn((double)v, p.fy), p.scale);
+  double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  double pf = exp(__dmul_rn(__dmul_rn(-0.5, r2), p.sigma));
+  double pb = p.pb_map ? p.pb_map[(int64_t)v * p.W + u] : p.pb;
+  double tau = __dadd_rn(pf, __dmul_rn(__dsub_rn(1.0, pf), pb));
+  return tau < 1.0 ? tau : 1.0;
+}
+
+__device__ __forceinline__ unsigned long long pack_status(unsigned int epoch, unsigned flag,
+                                                          unsigned value) {
+  return ((unsigned long long)epoch << 32) | ((unsigned long long)flag << 30) | value;
+}
+
+__global__ void __launch_bounds__(kThreads) mask_compact_kernel(MaskParams p) {
+  __shared__ unsigned int s_tile;
+  __shared__ unsigned int s_warp[kThreads / 32];
+  __shared__ unsigned int s_prefix;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_tile = atomicAdd(p.tile_counter, 1u);
+  __syncthreads();
+  const unsigned int tile = s_tile;
+  const int64_t npix = (int64_t)p.H * p.W;
+  const int64_t base = (int64_t)tile * kTile + (int64_t)tid * kPerThread;
+  const float* nz = p.noise + (int64_t)(p.frame % p.T) * p.Ht * p.Wt;
+
+  unsigned int bits = 0;
+  int u = (int)(base % p.W), v = (int)(base / p.W);
+#pragma unroll
+  for (int j = 0; j < kPerThread; ++j) {
+    const int64_t pix = base + j;
+    if (pix < npix) {
+      const double n = (double)__ldg(nz + (v % p.Ht) * p.Wt + (u % p.Wt));
+      const bool m = n < tau_at(p, u, v);
+      bits |= (unsigned)m << j;
+      if (p.bits) p.bits[pix] = (uint8_t)m;
+      if (p.net_in) {
+        __half* px = p.net_in + ((int64_t)v * p.net_wp + u) * 8;
+        if (!m) *reinterpret_cast<uint2*>(px) = make_uint2(0u, 0u);
+        px[4] = m ? __float2half(1.0f) : __float2half(0.0f);
+      }
+    }
+    if (++u == p.W) { u = 0; ++v; }
+  }
+  const unsigned int cnt = __popc(bits);
+  // block-wide exclusive scan of cnt
+  const int lane = tid & 31, warp = tid >> 5;
+  unsigned int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned int w = lane < kThreads / 32 ? s_warp[lane] : 0u;
+    unsigned int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < kThreads / 32) s_warp[lane] = wi - w;  // exclusive per warp
+    const unsigned int aggregate = __shfl_sync(0xffffffffu, wi, kThreads / 32 - 1);
+    // decoupled look-back (lane 0)
+    if (lane == 0) {
+      volatile unsigned long long* st = p.status;
+      unsigned int excl = 0;
+      if (tile == 0) {
+        st[0] = pack_status(p.epoch, 2u, aggregate);
+      } else {
+        st[tile] = pack_status(p.epoch, 1u, aggregate);
+        __threadfence();
+        int j = (int)tile - 1;
+        while (true) {
+          unsigned long long s = st[j];
+          if ((unsigned int)(s >> 32) != p.epoch || ((s >> 30) & 3u) == 0u) continue;
+          excl += (unsigned int)(s & 0x3fffffffu);
+          if (((s >> 30) & 3u) == 2u) break;
+          --j;
+        }
+        __threadfence();
+        st[tile] = pack_status(p.epoch, 2u, excl + aggregate);
+      }
+      s_prefix = excl;
+      const int64_t ntiles = (npix + kTile - 1) / kTile;
+      if ((int64_t)tile == ntiles - 1) *p.k_out = (int32_t)(excl + aggregate);
+    }
+  }
+  __syncthreads();
+  unsigned int pos = s_prefix + s_warp[warp] + (incl - cnt);
+  while (bits) {
+    const int j = __ffs(bits) - 1;
+    bits &= bits - 1;
+    p.idx[pos++] = (int32_t)(base + j);
+  }
+}
+
+__global__ void tau_kernel(MaskParams p, double* tau) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)p.H * p.W) return;
+  tau[i] = tau_at(p, (int)(i % p.W), (int)(i / p.W));
+}
+
+MaskParams make_params(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
+                       const double* pb_map) {
+  MaskParams p{};
+  p.H = H; p.W = W; p.frame = frame;
+  if (f) {
+    p.fx = f->focus[0]; p.fy = f->focus[1]; p.sigma = f->sigma; p.pb = f->base_density;
+    p.scale = f->pixel_scale;
+  }
+  p.pb_map = pb_map;
+  p.noise = ctx->noise; p.T = ctx->noise_T; p.Ht = ctx->noise_H; p.Wt = ctx->noise_W;
+  return p;
+}
+
+}  // namespace
+
+int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
+                        const double* pb_map, uint8_t* bits, int32_t* idx, int32_t* k,
+                        __half* net_in, int net_wp, const double* tau_map) {
+  FV_REQUIRE(ctx->noise != nullptr, "no noise stack uploaded (fv_noise_upload)");
+  FV_REQUIRE(frame >= 0, "frame must be >= 0, got %d", frame);
+  const int64_t npix = (int64_t)H * W;
+  FV_REQUIRE(npix < (1ll << 30), "film too large for the 30-bit scan (%lld px)", (long long)npix);
+  const int ntiles = (int)((npix + kTile - 1) / kTile);
+  if (ntiles > ctx->scan_tiles_cap) {
+    if (ctx->scan_status) cudaFree(ctx->scan_status);
+    ctx->scan_status = nullptr;
+    FV_CUDA(cudaMalloc(&ctx->scan_status, sizeof(unsigned long long) * ntiles));
+    FV_CUDA(cudaMemsetAsync(ctx->scan_status, 0, sizeof(unsigned long long) * ntiles, ctx->stream));
+    ctx->scan_tiles_cap = ntiles;
+  }
+  MaskParams p = make_params(ctx, frame, H, W, f, pb_map);
+  p.tau_map = tau_map;
+  p.bits = bits; p.idx = idx; p.k_out = k; p.net_in = net_in; p.net_wp = net_wp;
+  p.status = ctx->scan_status;
+  if (++ctx->epoch == 0) ctx->epoch = 1;
+  p.epoch = ctx->epoch;
+  p.tile_counter = &ctx->counters->scan_tile;
+  FV_CUDA(cudaMemsetAsync(&ctx->counters->scan_tile, 0, sizeof(unsigned int), ctx->stream));
+  mask_compact_kernel<<<ntiles, kThreads, 0, ctx->stream>>>(p);
+  FV_CHECK_LAUNCH("mask_compact_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int launch_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* pb_map,
+                   double* tau) {
+  MaskParams p = make_params(ctx, 0, H, W, f, pb_map);
+  const int64_t n = (int64_t)H * W;
+  tau_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(p, tau);
+  FV_CHECK_LAUNCH("tau_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+}  // namespace fv

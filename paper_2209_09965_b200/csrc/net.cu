@@ -1,0 +1,482 @@
+// W-Net reconstruction: parameter store, recurrent state and the per-frame forward.
+//
+// Reference (pkg/src/fovray/network.py):
+//   NetConfig / _conv_channels / _block_levels   :37-91, :128-159
+//   init_network / load_network (param names)     :162-180, :342-357
+//   reset_state / RecurrentState                  :103-119
+//   forward_D (encoder, decoder, head)            :203-254
+//   forward_K (per-scale predicted kernels)       :280-293
+//   forward_full (pad to /divisor, crop)          :296-323
+// The recurrent hidden states are ping-ponged between two device buffers, so carrying the state
+// into the next frame costs no copy; O_d is written by the head conv straight into channels 5..7
+// of the next frame's input tensor.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+namespace fv {
+int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_act* dst,
+            fv_act* pool_dst, bool relu, float* head_od, __half* head_feedback);
+int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out);
+int kfilter(fv_ctx* ctx, const fv_act& hd, const float* kw, const float* img, float* out);
+int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out);
+int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in);
+int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw);
+int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out);
+int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a);
+int od_to_feedback(fv_ctx* ctx, fv_state* st);
+int set_input(fv_ctx* ctx, fv_state* st, const float* xin, int C);
+
+namespace {
+
+float truncate_fp16(float v) {
+  // autograd.truncate_fp16 (autograd.py:499-503): clip to +-65504, round through binary16
+  if (v > 65504.f) v = 65504.f;
+  if (v < -65504.f) v = -65504.f;
+  return __half2float(__float2half_rn(v));
+}
+
+int parse_blocks(const char* s, std::vector<std::pair<char, int>>& out) {
+  out.clear();
+  std::string str(s ? s : "");
+  size_t pos = 0;
+  while (pos <= str.size()) {
+    size_t e = str.find('-', pos);
+    if (e == std::string::npos) e = str.size();
+    std::string tok = str.substr(pos, e - pos);
+    if (tok.size() < 2 || (tok[0] != 'e' && tok[0] != 'd')) {
+      set_error("bad block token '%s'", tok.c_str());
+      return FV_E_INVALID;
+    }
+    char* endp = nullptr;
+    long ch = strtol(tok.c_str() + 1, &endp, 10);
+    if (*endp != 0 || ch <= 0) {
+      set_error("bad block token '%s'", tok.c_str());
+      return FV_E_INVALID;
+    }
+    out.push_back({tok[0], (int)ch});
+    pos = e + 1;
+  }
+  return 0;
+}
+
+std::vector<int> block_levels(const fv_net* net) {
+  std::vector<int> lv;
+  for (int i = 0; i < net->n_enc; ++i) lv.push_back(i);
+  for (int j = 0; j < net->n_dec; ++j) lv.push_back(net->n_enc - j);
+  return lv;
+}
+
+int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* out_rgb,
+                float* out_o, float* out_od) {
+  for (const auto& cp : net->convs)
+    if (!(cp.w_set && cp.b_set)) {
+      set_error("network parameter %s not set", cp.name.c_str());
+      return FV_E_INVALID;
+    }
+  const int ne = net->n_enc, nd = net->n_dec;
+  int rc;
+  const fv_act* cur = &st->x;
+  for (int i = 0; i < ne; ++i) {
+    rc = conv3x3(ctx, net->convs[2 * i], cur, 1, &st->enc_a[i], nullptr, true, nullptr, nullptr);
+    if (rc) return rc;
+    rc = conv3x3(ctx, net->convs[2 * i + 1], &st->enc_a[i], 1, &st->skips[i], &st->pooled[i], true,
+                 nullptr, nullptr);
+    if (rc) return rc;
+    cur = &st->pooled[i];
+  }
+  const int oldp = st->parity, newp = st->parity ^ 1;
+  for (int j = 0; j < nd; ++j) {
+    fv_act srcs[3];
+    int n = 0;
+    if (j > 0) {
+      rc = upsample2_nc8(ctx, st->hidden[newp][j - 1], st->ups[j]);
+      if (rc) return rc;
+      srcs[n++] = st->ups[j];
+      srcs[n++] = st->skips[ne - j];
+    } else {
+      srcs[n++] = *cur;
+    }
+    if (net->recurrent) srcs[n++] = st->hidden[oldp][j];
+    const int b = ne + j;
+    rc = conv3x3(ctx, net->convs[2 * b], srcs, n, &st->dec_a[j], nullptr, true, nullptr, nullptr);
+    if (rc) return rc;
+    rc = conv3x3(ctx, net->convs[2 * b + 1], &st->dec_a[j], 1, &st->hidden[newp][j], nullptr, true,
+                 nullptr, nullptr);
+    if (rc) return rc;
+  }
+  // D.head -> O_d (fp32 planes) + feedback channels 5..7 of the input for the next frame
+  rc = conv3x3(ctx, net->convs[net->head_index], &st->hidden[newp][nd - 1], 1, nullptr, nullptr,
+               false, st->od, net->recurrent ? st->x.p : nullptr);
+  if (rc) return rc;
+  const float* final_img = st->od;
+  if (use_k) {
+    const std::vector<int> lv = block_levels(net);
+    const int nb = (int)lv.size();
+    const float* img = st->od;
+    for (int i = 0; i < nb; ++i) {
+      const int L = lv[i];
+      const fv_act& hd = st->hidden[newp][ne - L];
+      float* out = st->img2[L];
+      rc = kfilter(ctx, hd, net->kw_dev + net->kw_off[i], img, out);
+      if (rc) return rc;
+      if (net->blocks[i].first == 'e') {
+        rc = pool3(ctx, out, st->img[L + 1], st->Hp >> (L + 1), st->Wp >> (L + 1));
+        if (rc) return rc;
+        img = st->img[L + 1];
+      } else if (i < nb - 1) {
+        rc = up3(ctx, out, st->img[L - 1], st->Hp >> L, st->Wp >> L);
+        if (rc) return rc;
+        img = st->img[L - 1];
+      } else {
+        img = out;
+      }
+    }
+    final_img = img;
+  }
+  rc = finalize(ctx, st, final_img, out_rgb, out_o, out_od);
+  if (rc) return rc;
+  st->parity = newp;
+  st->fresh = false;
+  return 0;
+}
+
+}  // namespace fv
+
+using namespace fv;
+
+extern "C" {
+
+int fv_net_create(fv_ctx* ctx, const char* blocks, int predicted_kernel, int recurrent,
+                  int include_mask_channel, fv_net** out) {
+  FV_REQUIRE(ctx && out, "null argument");
+  auto* net = new fv_net();
+  int rc = parse_blocks(blocks, net->blocks);
+  if (rc) { delete net; return rc; }
+  int ne = 0, nd = 0;
+  bool seen_d = false;
+  for (auto& b : net->blocks) {
+    if (b.first == 'e') {
+      if (seen_d) { delete net; set_error("block config must list e-blocks then d-blocks"); return FV_E_INVALID; }
+      ++ne;
+    } else { seen_d = true; ++nd; }
+  }
+  if (ne != nd - 1) {
+    delete net;
+    set_error("structural encoder count (e-blocks + bottleneck = %d) must be one more than decoder count (%d); got %d e and %d d blocks",
+              ne + 1, nd - 1, ne, nd);
+    return FV_E_INVALID;
+  }
+  if (predicted_kernel != 3) { delete net; set_error("only predicted_kernel = 3 is supported"); return FV_E_UNSUPPORTED; }
+  net->n_enc = ne;
+  net->n_dec = nd;
+  net->predicted_kernel = predicted_kernel;
+  net->recurrent = recurrent != 0;
+  net->include_mask = include_mask_channel != 0;
+  net->in_channels = 4 + (net->include_mask ? 1 : 0) + (net->recurrent ? 3 : 0);
+  std::vector<int> ch;
+  for (auto& b : net->blocks) ch.push_back(b.second);
+  for (int c : ch)
+    if (c % 8 != 0) { delete net; set_error("block widths must be multiples of 8 (got %d)", c); return FV_E_UNSUPPORTED; }
+  std::vector<int> d_ch(ch.begin() + ne, ch.end());
+  // _conv_channels (network.py:128-149)
+  std::vector<std::pair<int, int>> io;
+  for (int i = 0; i < ne; ++i) io.push_back({i == 0 ? 8 : ch[i - 1], ch[i]});  // block0 input padded to 8 slots
+  for (int j = 0; j < nd; ++j) {
+    int inc = j == 0 ? ch[ne - 1] : d_ch[j - 1] + ch[ne - j];
+    if (net->recurrent) inc += d_ch[j];
+    io.push_back({inc, d_ch[j]});
+  }
+  for (size_t i = 0; i < io.size(); ++i) {
+    for (int c = 1; c <= 2; ++c) {
+      ConvParam cp;
+      cp.name = "D.block" + std::to_string(i) + ".conv" + std::to_string(c);
+      cp.cin = c == 1 ? io[i].first : io[i].second;
+      cp.cout = io[i].second;
+      cp.n_pad = (cp.cout + 15) / 16 * 16;
+      net->convs.push_back(cp);
+    }
+  }
+  {
+    ConvParam cp;
+    cp.name = "D.head";
+    cp.cin = d_ch.back();
+    cp.cout = 3;
+    cp.n_pad = 16;
+    net->head_index = (int)net->convs.size();
+    net->convs.push_back(cp);
+  }
+  net->k_index0 = (int)net->convs.size();
+  const std::vector<int> lv = block_levels(net);
+  int64_t off = 0;
+  for (size_t i = 0; i < lv.size(); ++i) {
+    ConvParam cp;
+    cp.name = "K.block" + std::to_string(i);
+    cp.cin = d_ch[ne - lv[i]];
+    cp.cout = 9;
+    cp.ksize = 1;
+    net->convs.push_back(cp);
+    net->kw_off.push_back(off);
+    off += 9 * cp.cin + 9;
+  }
+  if (cudaMalloc(&net->kw_dev, sizeof(float) * off) != cudaSuccess) {
+    delete net;
+    set_error("cudaMalloc failed for K weights");
+    return FV_E_NOMEM;
+  }
+  cudaMemset(net->kw_dev, 0, sizeof(float) * off);
+  *out = net;
+  return 0;
+}
+
+int fv_net_destroy(fv_net* net) {
+  if (!net) return 0;
+  for (auto& cp : net->convs) {
+    if (cp.w_dev) cudaFree(cp.w_dev);
+    if (cp.b_dev) cudaFree(cp.b_dev);
+  }
+  if (net->kw_dev) cudaFree(net->kw_dev);
+  delete net;
+  return 0;
+}
+
+int fv_net_set_param(fv_ctx* ctx, fv_net* net, const char* name, const float* host, int64_t count) {
+  FV_REQUIRE(ctx && net && name && host, "null argument");
+  std::string n(name);
+  const bool is_w = n.size() > 2 && n.compare(n.size() - 2, 2, ".w") == 0;
+  const bool is_b = n.size() > 2 && n.compare(n.size() - 2, 2, ".b") == 0;
+  FV_REQUIRE(is_w || is_b, "checkpoint parameter '%s' not in network", name);
+  const std::string base = n.substr(0, n.size() - 2);
+  int idx = -1;
+  for (size_t i = 0; i < net->convs.size(); ++i)
+    if (net->convs[i].name == base) idx = (int)i;
+  FV_REQUIRE(idx >= 0, "checkpoint parameter '%s' not in network", name);
+  ConvParam& cp = net->convs[idx];
+  const int ks = cp.ksize;
+  // reference cin of block0.conv1 is in_channels; device layout uses 8 slots [rgba, m, prev]
+  const bool first = base == "D.block0.conv1";
+  const int ref_cin = first ? net->in_channels : cp.cin;
+  const int64_t expect = is_w ? (int64_t)cp.cout * ref_cin * ks * ks : cp.cout;
+  FV_REQUIRE(count == expect, "checkpoint shape mismatch for '%s' (%lld values, expected %lld)", name,
+             (long long)count, (long long)expect);
+  for (int64_t i = 0; i < count; ++i)
+    FV_REQUIRE(std::isfinite(host[i]), "parameter '%s' has a non-finite value", name);
+  if (is_w) {
+    cp.w_host.assign((size_t)cp.cout * cp.cin * ks * ks, 0.f);
+    for (int o = 0; o < cp.cout; ++o)
+      for (int c = 0; c < ref_cin; ++c) {
+        int slot = c;
+        if (first) {
+          // reference order: rgba(4), [mask], [prev(3)]
+          if (c < 4) slot = c;
+          else if (net->include_mask && c == 4) slot = 4;
+          else slot = 5 + (c - 4 - (net->include_mask ? 1 : 0));
+        }
+        for (int t = 0; t < ks * ks; ++t)
+          cp.w_host[((size_t)o * cp.cin + slot) * ks * ks + t] =
+              truncate_fp16(host[((size_t)o * ref_cin + c) * ks * ks + t]);
+      }
+    cp.w_set = true;
+  } else {
+    cp.b_host.assign(host, host + count);
+    cp.b_set = true;
+  }
+  if (!(cp.w_set && cp.b_set)) return 0;
+  if (cp.ksize == 1) {
+    const int k = idx - net->k_index0;
+    std::vector<float> packed(9 * cp.cin + 9);
+    for (int j = 0; j < 9; ++j)
+      for (int c = 0; c < cp.cin; ++c) packed[j * cp.cin + c] = cp.w_host[(size_t)j * cp.cin + c];
+    for (int j = 0; j < 9; ++j) packed[9 * cp.cin + j] = cp.b_host[j];
+    FV_CUDA(cudaMemcpy(net->kw_dev + net->kw_off[k], packed.data(), sizeof(float) * packed.size(),
+                       cudaMemcpyHostToDevice));
+    return 0;
+  }
+  return conv_prepare(ctx, cp);
+}
+
+int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out) {
+  FV_REQUIRE(ctx && net && out, "null argument");
+  FV_REQUIRE(H >= 1 && W >= 1, "dims must be positive, got (%d, %d)", H, W);
+  const int div = 1 << net->n_enc;
+  auto* st = new fv_state();
+  st->net = net;
+  st->H = H;
+  st->W = W;
+  st->Hp = (H + div - 1) / div * div;
+  st->Wp = (W + div - 1) / div * div;
+  const int ne = net->n_enc, nd = net->n_dec;
+  std::vector<int> ch;
+  for (auto& b : net->blocks) ch.push_back(b.second);
+  std::vector<int> d_ch(ch.begin() + ne, ch.end());
+  // plan the arena
+  struct Req { fv_act* a; int C, L; };
+  std::vector<Req> reqs;
+  st->enc_a.resize(ne); st->skips.resize(ne); st->pooled.resize(ne);
+  st->dec_a.resize(nd); st->ups.resize(nd); st->hidden[0].resize(nd); st->hidden[1].resize(nd);
+  reqs.push_back({&st->x, 8, 0});
+  for (int i = 0; i < ne; ++i) {
+    reqs.push_back({&st->enc_a[i], ch[i], i});
+    reqs.push_back({&st->skips[i], ch[i], i});
+    reqs.push_back({&st->pooled[i], ch[i], i + 1});
+  }
+  for (int j = 0; j < nd; ++j) {
+    const int L = ne - j;
+    reqs.push_back({&st->dec_a[j], d_ch[j], L});
+    if (j > 0) reqs.push_back({&st->ups[j], d_ch[j - 1], L});
+    reqs.push_back({&st->hidden[0][j], d_ch[j], L});
+    reqs.push_back({&st->hidden[1][j], d_ch[j], L});
+  }
+  int64_t bytes = 0;
+  std::vector<int64_t> offs;
+  for (auto& r : reqs) {
+    offs.push_back(bytes);
+    const int64_t h = st->Hp >> r.L, w = st->Wp >> r.L;
+    bytes += align_up((int64_t)r.C * h * w * 2, 256);
+  }
+  const int64_t od_off = bytes;
+  bytes += align_up((int64_t)3 * st->Hp * st->Wp * 4, 256);
+  std::vector<int64_t> img_off, img2_off;
+  for (int L = 0; L <= ne; ++L) {
+    img_off.push_back(bytes);
+    bytes += align_up((int64_t)3 * (st->Hp >> L) * (st->Wp >> L) * 4, 256);
+    img2_off.push_back(bytes);
+    bytes += align_up((int64_t)3 * (st->Hp >> L) * (st->Wp >> L) * 4, 256);
+  }
+  if (cudaMalloc(&st->arena, bytes) != cudaSuccess) {
+    delete st;
+    set_error("cudaMalloc of %lld bytes for the state failed", (long long)bytes);
+    return FV_E_NOMEM;
+  }
+  st->arena_bytes = bytes;
+  uint8_t* base = reinterpret_cast<uint8_t*>(st->arena);
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    reqs[i].a->p = reinterpret_cast<__half*>(base + offs[i]);
+    reqs[i].a->C = reqs[i].C;
+    reqs[i].a->H = st->Hp >> reqs[i].L;
+    reqs[i].a->W = st->Wp >> reqs[i].L;
+  }
+  st->od = reinterpret_cast<float*>(base + od_off);
+  for (int L = 0; L <= ne; ++L) {
+    st->img.push_back(reinterpret_cast<float*>(base + img_off[L]));
+    st->img2.push_back(reinterpret_cast<float*>(base + img2_off[L]));
+  }
+  if (cudaMemsetAsync(st->arena, 0, bytes, ctx->stream) != cudaSuccess) {
+    cudaFree(st->arena);
+    delete st;
+    set_error("cudaMemset of the state failed");
+    return FV_E_CUDA;
+  }
+  *out = st;
+  return 0;
+}
+
+int fv_state_reset(fv_ctx* ctx, fv_state* st) {
+  FV_REQUIRE(ctx && st, "null argument");
+  FV_CUDA(cudaMemsetAsync(st->arena, 0, st->arena_bytes, ctx->stream));
+  st->parity = 0;
+  st->fresh = true;
+  return 0;
+}
+
+int fv_state_destroy(fv_state* st) {
+  if (!st) return 0;
+  if (st->arena) cudaFree(st->arena);
+  delete st;
+  return 0;
+}
+
+void* fv_state_net_input(fv_state* st) { return st ? st->x.p : nullptr; }
+
+int fv_state_dims(const fv_state* st, int* H, int* W, int* Hp, int* Wp) {
+  FV_REQUIRE(st, "null state");
+  if (H) *H = st->H;
+  if (W) *W = st->W;
+  if (Hp) *Hp = st->Hp;
+  if (Wp) *Wp = st->Wp;
+  return 0;
+}
+
+int fv_reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_kernel_stage,
+                   float* out_rgb_dev, float* out_o_dev, float* out_od_dev) {
+  FV_REQUIRE(ctx && net && st, "null argument");
+  if (st->net != net) {
+    set_error("carried state belongs to a different network; reset the state");
+    return FV_E_STATE;
+  }
+  return reconstruct(ctx, net, st, use_kernel_stage, out_rgb_dev, out_o_dev, out_od_dev);
+}
+
+int fv_state_read(fv_ctx* ctx, const fv_state* st, int which, float* host, int64_t cap,
+                  int64_t* count) {
+  FV_REQUIRE(ctx && st, "null argument");
+  const fv_net* net = st->net;
+  int64_t n;
+  float* tmp = nullptr;
+  if (which == -1) {
+    n = (int64_t)3 * st->Hp * st->Wp;
+    if (count) *count = n;
+    if (!host) return 0;
+    FV_REQUIRE(cap >= n, "buffer too small (%lld < %lld)", (long long)cap, (long long)n);
+    FV_CUDA(cudaMemcpyAsync(host, st->od, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    FV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return 0;
+  }
+  FV_REQUIRE(which >= 0 && which < net->n_dec, "hidden index %d out of range", which);
+  const fv_act& a = st->hidden[st->parity][which];
+  n = (int64_t)a.C * a.H * a.W;
+  if (count) *count = n;
+  if (!host) return 0;
+  FV_REQUIRE(cap >= n, "buffer too small (%lld < %lld)", (long long)cap, (long long)n);
+  FV_CUDA(cudaMallocAsync(&tmp, n * 4, ctx->stream));
+  int rc = nc8_to_nchw(ctx, a, tmp);
+  if (rc) return rc;
+  FV_CUDA(cudaMemcpyAsync(host, tmp, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  FV_CUDA(cudaFreeAsync(tmp, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int fv_state_set_input(fv_ctx* ctx, fv_state* st, const float* x_dev, int channels) {
+  FV_REQUIRE(ctx && st && x_dev, "null argument");
+  const int expect = 4 + (st->net->include_mask ? 1 : 0);
+  FV_REQUIRE(channels == expect, "input has %d channels, expected %d", channels, expect);
+  return set_input(ctx, st, x_dev, channels);
+}
+
+int fv_state_write(fv_ctx* ctx, fv_state* st, int which, const float* host, int64_t count) {
+  FV_REQUIRE(ctx && st && host, "null argument");
+  const fv_net* net = st->net;
+  float* tmp = nullptr;
+  if (which == -1) {
+    const int64_t n = (int64_t)3 * st->Hp * st->Wp;
+    FV_REQUIRE(count == n, "prev_output must have %lld values (3 x padded film), got %lld", (long long)n,
+               (long long)count);
+    FV_CUDA(cudaMemcpyAsync(st->od, host, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    int rc = od_to_feedback(ctx, st);
+    if (rc) return rc;
+    FV_CUDA(cudaStreamSynchronize(ctx->stream));
+    st->fresh = false;
+    return 0;
+  }
+  FV_REQUIRE(which >= 0 && which < net->n_dec, "hidden index %d out of range", which);
+  fv_act& a = st->hidden[st->parity][which];
+  const int64_t n = (int64_t)a.C * a.H * a.W;
+  FV_REQUIRE(count == n, "hidden[%d] must have %lld values, got %lld", which, (long long)n, (long long)count);
+  FV_CUDA(cudaMallocAsync(&tmp, n * 4, ctx->stream));
+  FV_CUDA(cudaMemcpyAsync(tmp, host, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = nchw_to_nc8(ctx, tmp, a);
+  if (rc) return rc;
+  FV_CUDA(cudaFreeAsync(tmp, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  st->fresh = false;
+  return 0;
+}
+
+}  // extern "C"

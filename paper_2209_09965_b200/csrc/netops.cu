@@ -1,0 +1,335 @@
+// Memory-bound W-Net operators around the tcgen05 convolutions.
+//
+// Reference (pkg/src/fovray):
+//   upsample_bilinear2   autograd.py:294-305, :322-329 (half-pixel, edge clamp, rows then cols)
+//   avg_pool2            autograd.py:279-291
+//   softmax_channels     autograd.py:188-199 (max-subtracted softmax over the 9 taps)
+//   apply_kernel_field   autograd.py:332-359 (tap j = (dy, dx) = divmod(j, 3), zero padding,
+//                                             accumulated in tap order)
+//   predict_kernel_fields network.py:268-277 (1x1 conv of the decoder hidden state)
+//   forward_K            network.py:280-293 (pool after e-blocks, upsample after d-blocks)
+//   _reconstruct_frame   bench.py:166-175   (x = rgba*m ++ m; output clipped to [0,1])
+#include "internal.h"
+
+namespace fv {
+
+namespace {
+
+// ---- D-path 2x bilinear upsample, fp16 NC8HW8 -> fp16 NC8HW8 -------------------------------
+__global__ void upsample2_nc8_kernel(const __half* __restrict__ in, __half* __restrict__ out,
+                                     int groups, int h, int w) {
+  const int W2 = 2 * w, H2 = 2 * h;
+  const int64_t n = (int64_t)groups * H2 * W2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int X = (int)(i % W2);
+    const int Y = (int)((i / W2) % H2);
+    const int g = (int)(i / ((int64_t)W2 * H2));
+    const __half* pl = in + (int64_t)g * h * w * 8;
+    const int iy = Y >> 1, ix = X >> 1;
+    int ya, yb;
+    float wya, wyb;
+    if (Y & 1) { ya = iy; yb = min(iy + 1, h - 1); wya = 0.75f; wyb = 0.25f; }
+    else { ya = max(iy - 1, 0); yb = iy; wya = 0.25f; wyb = 0.75f; }
+    int xa, xb;
+    float wxa, wxb;
+    if (X & 1) { xa = ix; xb = min(ix + 1, w - 1); wxa = 0.75f; wxb = 0.25f; }
+    else { xa = max(ix - 1, 0); xb = ix; wxa = 0.25f; wxb = 0.75f; }
+    const uint4 qaa = *reinterpret_cast<const uint4*>(pl + ((int64_t)ya * w + xa) * 8);
+    const uint4 qba = *reinterpret_cast<const uint4*>(pl + ((int64_t)yb * w + xa) * 8);
+    const uint4 qab = *reinterpret_cast<const uint4*>(pl + ((int64_t)ya * w + xb) * 8);
+    const uint4 qbb = *reinterpret_cast<const uint4*>(pl + ((int64_t)yb * w + xb) * 8);
+    const __half2* aa = reinterpret_cast<const __half2*>(&qaa);
+    const __half2* ba = reinterpret_cast<const __half2*>(&qba);
+    const __half2* ab = reinterpret_cast<const __half2*>(&qab);
+    const __half2* bb = reinterpret_cast<const __half2*>(&qbb);
+    uint4 o;
+    __half2* o2 = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 faa = __half22float2(aa[j]), fba = __half22float2(ba[j]);
+      const float2 fab = __half22float2(ab[j]), fbb = __half22float2(bb[j]);
+      // rows first (axis 2), then columns (axis 3), as in upsample_bilinear2
+      const float ra0 = wya * faa.x + wyb * fba.x, ra1 = wya * faa.y + wyb * fba.y;
+      const float rb0 = wya * fab.x + wyb * fbb.x, rb1 = wya * fab.y + wyb * fbb.y;
+      o2[j] = __floats2half2_rn(wxa * ra0 + wxb * rb0, wxa * ra1 + wxb * rb1);
+    }
+    *reinterpret_cast<uint4*>(out + ((int64_t)g * H2 * W2 + (int64_t)Y * W2 + X) * 8) = o;
+  }
+}
+
+// ---- K stage: logits (1x1 conv) -> softmax -> per-pixel 3x3 filter -------------------------
+template <int C>
+__global__ void kfilter_kernel(const __half* __restrict__ hd, const float* __restrict__ kw,
+                               const float* __restrict__ img, float* __restrict__ out, int h, int w) {
+  __shared__ float sw[9 * C + 9];
+  for (int i = threadIdx.x; i < 9 * C + 9; i += blockDim.x) sw[i] = kw[i];
+  __syncthreads();
+  const int64_t n = (int64_t)h * w;
+  const int64_t plane = n * 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % w), y = (int)(i / w);
+    float lg[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) lg[j] = 0.f;
+#pragma unroll 2
+    for (int g = 0; g < C / 8; ++g) {
+      const uint4 q = *reinterpret_cast<const uint4*>(hd + g * plane + i * 8);
+      const __half2* h2 = reinterpret_cast<const __half2*>(&q);
+      float f[8];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 t = __half22float2(h2[e]);
+        f[2 * e] = t.x;
+        f[2 * e + 1] = t.y;
+      }
+#pragma unroll
+      for (int j = 0; j < 9; ++j)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) lg[j] = fmaf(sw[j * C + g * 8 + e], f[e], lg[j]);
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      lg[j] += sw[9 * C + j];
+      m = fmaxf(m, lg[j]);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      lg[j] = expf(lg[j] - m);
+      s += lg[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) lg[j] = lg[j] / s;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float* pl = img + (int64_t)c * n;
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const int yy = y + j / 3 - 1, xx = x + j % 3 - 1;
+        const float v = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
+        acc = acc + lg[j] * v;
+      }
+      out[(int64_t)c * n + i] = acc;
+    }
+  }
+}
+
+// 3-channel fp32 avg_pool2 (h, w are the OUTPUT dims)
+__global__ void pool3_kernel(const float* __restrict__ in, float* __restrict__ out, int h, int w) {
+  const int64_t n = (int64_t)3 * h * w;
+  const int W2 = 2 * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % w), y = (int)((i / w) % h), c = (int)(i / ((int64_t)h * w));
+    const float* p = in + (int64_t)c * 4 * h * w;
+    const float p00 = p[(int64_t)(2 * y) * W2 + 2 * x], p10 = p[(int64_t)(2 * y + 1) * W2 + 2 * x];
+    const float p01 = p[(int64_t)(2 * y) * W2 + 2 * x + 1], p11 = p[(int64_t)(2 * y + 1) * W2 + 2 * x + 1];
+    out[i] = 0.25f * (((p00 + p10) + p01) + p11);
+  }
+}
+
+// 3-channel fp32 2x bilinear upsample (h, w are the INPUT dims)
+__global__ void up3_kernel(const float* __restrict__ in, float* __restrict__ out, int h, int w) {
+  const int H2 = 2 * h, W2 = 2 * w;
+  const int64_t n = (int64_t)3 * H2 * W2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int X = (int)(i % W2), Y = (int)((i / W2) % H2), c = (int)(i / ((int64_t)H2 * W2));
+    const float* p = in + (int64_t)c * h * w;
+    const int iy = Y >> 1, ix = X >> 1;
+    int ya, yb, xa, xb;
+    float wya, wyb, wxa, wxb;
+    if (Y & 1) { ya = iy; yb = min(iy + 1, h - 1); wya = 0.75f; wyb = 0.25f; }
+    else { ya = max(iy - 1, 0); yb = iy; wya = 0.25f; wyb = 0.75f; }
+    if (X & 1) { xa = ix; xb = min(ix + 1, w - 1); wxa = 0.75f; wxb = 0.25f; }
+    else { xa = max(ix - 1, 0); xb = ix; wxa = 0.25f; wxb = 0.75f; }
+    const float ra = wya * p[(int64_t)ya * w + xa] + wyb * p[(int64_t)yb * w + xa];
+    const float rb = wya * p[(int64_t)ya * w + xb] + wyb * p[(int64_t)yb * w + xb];
+    out[i] = wxa * ra + wxb * rb;
+  }
+}
+
+// x = rgba*m ++ m into channels 0..4 of the NHWC8 input (film region only)
+__global__ void pack_input_kernel(const float* __restrict__ rgba, const uint8_t* __restrict__ bits,
+                                  __half* __restrict__ x, int H, int W, int Wp) {
+  const int64_t n = (int64_t)H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(i % W), v = (int)(i / W);
+    const float m = bits[i] ? 1.f : 0.f;
+    const float4 c = *reinterpret_cast<const float4*>(rgba + i * 4);
+    __half* px = x + ((int64_t)v * Wp + u) * 8;
+    __half2* p2 = reinterpret_cast<__half2*>(px);
+    p2[0] = __floats2half2_rn(c.x * m, c.y * m);
+    p2[1] = __floats2half2_rn(c.z * m, c.w * m);
+    px[4] = __float2half(m);
+  }
+}
+
+// forward_full input: NCHW (C,H,W) fp32 -> channels 0..C-1 of the NHWC8 input (C = 4 or 5)
+__global__ void set_input_kernel(const float* __restrict__ xin, int C, __half* __restrict__ x, int H,
+                                 int W, int Wp) {
+  const int64_t n = (int64_t)H * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(i % W), v = (int)(i / W);
+    __half* px = x + ((int64_t)v * Wp + u) * 8;
+    for (int c = 0; c < 5; ++c) px[c] = __float2half_rn(c < C ? xin[c * n + i] : 0.f);
+  }
+}
+
+// crop (3,Hp,Wp) -> (H,W,3) clipped, (3,H,W) raw O and O_d
+__global__ void finalize_kernel(const float* __restrict__ img, const float* __restrict__ od, int H,
+                                int W, int Hp, int Wp, float* __restrict__ rgb, float* __restrict__ o_raw,
+                                float* __restrict__ od_raw) {
+  const int64_t n = (int64_t)H * W;
+  const int64_t pp = (int64_t)Hp * Wp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(i % W), v = (int)(i / W);
+    const int64_t j = (int64_t)v * Wp + u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float o = img[c * pp + j];
+      if (rgb) rgb[i * 3 + c] = fminf(fmaxf(o, 0.f), 1.f);
+      if (o_raw) o_raw[c * n + i] = o;
+      if (od_raw) od_raw[c * n + i] = od[c * pp + j];
+    }
+  }
+}
+
+// NC8HW8 fp16 -> NCHW fp32
+__global__ void nc8_to_nchw_kernel(const __half* __restrict__ in, float* __restrict__ out, int C,
+                                   int h, int w) {
+  const int64_t n = (int64_t)C * h * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i % ((int64_t)h * w);
+    const int c = (int)(i / ((int64_t)h * w));
+    out[i] = __half2float(in[(int64_t)(c >> 3) * h * w * 8 + p * 8 + (c & 7)]);
+  }
+}
+
+// NCHW fp32 -> NC8HW8 fp16
+__global__ void nchw_to_nc8_kernel(const float* __restrict__ in, __half* __restrict__ out, int C,
+                                   int h, int w) {
+  const int64_t n = (int64_t)C * h * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i % ((int64_t)h * w);
+    const int c = (int)(i / ((int64_t)h * w));
+    out[(int64_t)(c >> 3) * h * w * 8 + p * 8 + (c & 7)] = __float2half_rn(in[i]);
+  }
+}
+
+// O_d (3,H,W) fp32 -> feedback channels 5..7 of the NHWC8 input
+__global__ void od_to_feedback_kernel(const float* __restrict__ od, __half* __restrict__ x, int h, int w) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) x[i * 8 + 5 + c] = __float2half_rn(od[c * n + i]);
+  }
+}
+
+inline int grid_for(fv_ctx* ctx, int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)ctx->num_sms * 16;
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+}  // namespace
+
+int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
+  const int64_t n = (int64_t)(in.C / 8) * 4 * in.H * in.W;
+  upsample2_nc8_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(in.p, out.p, in.C / 8, in.H, in.W);
+  FV_CHECK_LAUNCH("upsample2_nc8_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int kfilter(fv_ctx* ctx, const fv_act& hd, const float* kw, const float* img, float* out) {
+  const int64_t n = (int64_t)hd.H * hd.W;
+  const int g = grid_for(ctx, n);
+  switch (hd.C) {
+#define KF(CC) case CC: kfilter_kernel<CC><<<g, 256, 0, ctx->stream>>>(hd.p, kw, img, out, hd.H, hd.W); break;
+    KF(8) KF(16) KF(24) KF(32) KF(40) KF(48) KF(56) KF(64) KF(72) KF(80) KF(88) KF(96) KF(112) KF(128)
+#undef KF
+    default:
+      set_error("K stage: unsupported hidden width %d", hd.C);
+      return FV_E_UNSUPPORTED;
+  }
+  FV_CHECK_LAUNCH("kfilter_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out) {
+  pool3_kernel<<<grid_for(ctx, (int64_t)3 * h_out * w_out), 256, 0, ctx->stream>>>(in, out, h_out, w_out);
+  FV_CHECK_LAUNCH("pool3_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in) {
+  up3_kernel<<<grid_for(ctx, (int64_t)12 * h_in * w_in), 256, 0, ctx->stream>>>(in, out, h_in, w_in);
+  FV_CHECK_LAUNCH("up3_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int pack_input(fv_ctx* ctx, fv_state* st, const float* rgba, const uint8_t* bits) {
+  const int64_t n = (int64_t)st->H * st->W;
+  pack_input_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(rgba, bits, st->x.p, st->H, st->W, st->Wp);
+  FV_CHECK_LAUNCH("pack_input_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int set_input(fv_ctx* ctx, fv_state* st, const float* xin, int C) {
+  const int64_t n = (int64_t)st->H * st->W;
+  set_input_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(xin, C, st->x.p, st->H, st->W, st->Wp);
+  FV_CHECK_LAUNCH("set_input_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw) {
+  const int64_t n = (int64_t)st->H * st->W;
+  finalize_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(img, st->od, st->H, st->W, st->Hp, st->Wp,
+                                                              rgb, o_raw, od_raw);
+  FV_CHECK_LAUNCH("finalize_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out) {
+  const int64_t n = (int64_t)a.C * a.H * a.W;
+  nc8_to_nchw_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(a.p, out, a.C, a.H, a.W);
+  FV_CHECK_LAUNCH("nc8_to_nchw_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a) {
+  const int64_t n = (int64_t)a.C * a.H * a.W;
+  nchw_to_nc8_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(in, a.p, a.C, a.H, a.W);
+  FV_CHECK_LAUNCH("nchw_to_nc8_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int od_to_feedback(fv_ctx* ctx, fv_state* st) {
+  const int64_t n = (int64_t)st->Hp * st->Wp;
+  od_to_feedback_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(st->od, st->x.p, st->Hp, st->Wp);
+  FV_CHECK_LAUNCH("od_to_feedback_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+}  // namespace fv

@@ -1,0 +1,110 @@
+// Procedural test volumes generated on the GPU.
+//
+// Reference: volume.make_procedural_volume (volume.py:112-146) + _normalize (volume.py:75-81).
+// Raw fields are evaluated in fp64 at voxel centres u,v,w = (i+0.5)/n*2-1 with numpy's
+// left-to-right operation order, min-max normalised with the global extremes and cast to
+// float32. fp64 sin/cos differ from numpy's by at most an ulp, which survives the f32 cast only
+// for a vanishing fraction of voxels (the tests bound it).
+#include "internal.h"
+
+namespace fv {
+namespace {
+
+constexpr double kPi = 3.141592653589793;
+
+__device__ __forceinline__ double raw_field(int kind, int x, int y, int z, int nx, int ny, int nz) {
+  const double u = ((double)x + 0.5) / nx * 2.0 - 1.0;
+  const double v = ((double)y + 0.5) / ny * 2.0 - 1.0;
+  const double w = ((double)z + 0.5) / nz * 2.0 - 1.0;
+  if (kind == 2) {  // box_lattice
+    const double par = fmod(floor(2.0 * (u + 1.0)) + floor(2.0 * (v + 1.0)) + floor(2.0 * (w + 1.0)), 2.0);
+    return __dadd_rn(__dmul_rn(0.7, par), __dmul_rn(0.3, u + 1.0) / 2.0);
+  }
+  const double r = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(u, u), __dmul_rn(v, v)), __dmul_rn(w, w)));
+  if (kind == 0) {  // sphere_shells
+    return 0.5 * (1.0 + cos(__dmul_rn(2.0 * kPi * 3.0, r)));
+  }
+  // vortex_field
+  const double a = __dadd_rn(__dmul_rn(3.0 * kPi, u), __dmul_rn(__dmul_rn(2.0, v), w));
+  const double b = __dsub_rn(__dmul_rn(2.0 * kPi, v), __dmul_rn(__dmul_rn(1.5, u), w));
+  const double raw = __dmul_rn(sin(a), cos(b));
+  return __dadd_rn(raw, __dmul_rn(0.5, cos(__dmul_rn(4.0 * kPi, r))));
+}
+
+__global__ void minmax_kernel(int kind, int nx, int ny, int nz, double* partial) {
+  const int64_t n = (int64_t)nx * ny * nz;
+  double lo = INFINITY, hi = -INFINITY;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx);
+    const int y = (int)((i / nx) % ny);
+    const int z = (int)(i / ((int64_t)nx * ny));
+    const double r = raw_field(kind, x, y, z, nx, ny, nz);
+    lo = fmin(lo, r);
+    hi = fmax(hi, r);
+  }
+  __shared__ double slo[32], shi[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) { slo[threadIdx.x >> 5] = lo; shi[threadIdx.x >> 5] = hi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { lo = fmin(lo, slo[w]); hi = fmax(hi, shi[w]); }
+    partial[2 * blockIdx.x] = lo;
+    partial[2 * blockIdx.x + 1] = hi;
+  }
+}
+
+__global__ void minmax_final(const double* partial, int n, double* out) {
+  double lo = INFINITY, hi = -INFINITY;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    lo = fmin(lo, partial[2 * i]);
+    hi = fmax(hi, partial[2 * i + 1]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (threadIdx.x == 0) { out[0] = lo; out[1] = hi; }
+}
+
+__global__ void normalize_kernel(int kind, int nx, int ny, int nz, const double* range, float* out) {
+  const int64_t n = (int64_t)nx * ny * nz;
+  const double lo = range[0], hi = range[1];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx);
+    const int y = (int)((i / nx) % ny);
+    const int z = (int)(i / ((int64_t)nx * ny));
+    const double r = raw_field(kind, x, y, z, nx, ny, nz);
+    out[i] = hi > lo ? (float)(__dsub_rn(r, lo) / __dsub_rn(hi, lo)) : 0.0f;
+  }
+}
+
+}  // namespace
+
+int launch_volume_procedural(fv_ctx* ctx, fv_volume* vol, int kind, double* range_out) {
+  FV_REQUIRE(kind >= 0 && kind <= 2, "unknown procedural volume kind %d", kind);
+  FV_REQUIRE(vol->nx >= 8 && vol->ny >= 8 && vol->nz >= 8,
+             "procedural dims must be >= 8 per axis, got (%d, %d, %d)", vol->nx, vol->ny, vol->nz);
+  const int blocks = ctx->num_sms * 8;
+  double* tmp = nullptr;
+  FV_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (2 * blocks + 2), ctx->stream));
+  minmax_kernel<<<blocks, 256, 0, ctx->stream>>>(kind, vol->nx, vol->ny, vol->nz, tmp + 2);
+  minmax_final<<<1, 32, 0, ctx->stream>>>(tmp + 2, blocks, tmp);
+  normalize_kernel<<<blocks, 256, 0, ctx->stream>>>(kind, vol->nx, vol->ny, vol->nz, tmp, vol->data);
+  FV_CHECK_LAUNCH("procedural volume kernels");
+  ctx->launches += 3;
+  double r[2];
+  FV_CUDA(cudaMemcpyAsync(r, tmp, sizeof(r), cudaMemcpyDeviceToHost, ctx->stream));
+  FV_CUDA(cudaFreeAsync(tmp, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  vol->value_range[0] = r[0];
+  vol->value_range[1] = r[1];
+  if (range_out) { range_out[0] = r[0]; range_out[1] = r[1]; }
+  return 0;
+}
+
+}  // namespace fv

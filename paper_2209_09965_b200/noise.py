@@ -1,0 +1,85 @@
+"""Rank-noise stacks consumed by the foveated mask (lookup side only).
+
+Mirrors the reference's NoiseStack / RNKSTACK cache (pkg/src/fovray/noise.py:31-57,
+:432-468). Generating blue / spatio-temporal blue noise is an offline, sequential
+process the reference caches to disk once; this package ships that cache for the
+pipeline default (STBN 64x64x8, seed 1 -- `default_stack()` in noise.py:456-468)
+and uploads it to the GPU, where the mask kernel performs the toroidal lookup
+`stack[frame % T][v % H][u % W]` (noise.py:378-384).
+"""
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+DEFAULT_TILE = 64
+DEFAULT_FRAMES = 8
+_CACHE_MAGIC = b"RNKSTACK"
+_HEADER = "<8sIIIq dd"
+_DATA = Path(__file__).resolve().parent / "data"
+
+
+@dataclass(frozen=True)
+class NoiseStack:
+    """T x H x W stack of rank-noise values in [0,1) (noise.py:31-57)."""
+
+    values: np.ndarray  # (T, H, W) float32
+    seed: int = 0
+    sigma_spatial: float = 0.0
+    sigma_temporal: float = 0.0
+
+    def __post_init__(self):
+        v = np.asarray(self.values)
+        if v.ndim != 3 or v.shape[0] < 1:
+            raise ValueError(f"noise stack must be (T>=1, H, W), got {v.shape}")
+        n = v.shape[1] * v.shape[2]
+        ranks = ((np.arange(n) + 0.5) / n).astype(v.dtype)
+        for t in range(v.shape[0]):
+            if not np.array_equal(np.sort(v[t].ravel()), ranks):
+                raise ValueError(f"frame {t} is not a rank permutation")
+        v.setflags(write=False)
+        object.__setattr__(self, "values", v)
+
+    @property
+    def frames(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def dims(self) -> tuple[int, int]:
+        return self.values.shape[1], self.values.shape[2]
+
+
+def save_stack(stack: NoiseStack, path: str | Path) -> None:
+    """RNKSTACK cache: magic, (H, W, T, seed, sigma_s, sigma_t), float32 payload."""
+    t = stack.values.shape[0]
+    h, w = stack.dims
+    header = struct.pack(_HEADER, _CACHE_MAGIC, h, w, t, stack.seed, stack.sigma_spatial,
+                         stack.sigma_temporal)
+    with open(path, "wb") as f:
+        f.write(header)
+        f.write(np.ascontiguousarray(stack.values, dtype="<f4").tobytes())
+
+
+def load_stack(path: str | Path) -> NoiseStack:
+    blob = Path(path).read_bytes()
+    head = struct.calcsize(_HEADER)
+    magic, h, w, t, seed, ss, st = struct.unpack(_HEADER, blob[:head])
+    if magic != _CACHE_MAGIC:
+        raise ValueError(f"not a noise stack cache: {path}")
+    values = np.frombuffer(blob[head:], dtype="<f4").reshape(t, h, w).copy()
+    return NoiseStack(values=values, seed=seed, sigma_spatial=ss, sigma_temporal=st)
+
+
+def default_stack(cache_dir: str | Path | None = None, h: int = DEFAULT_TILE,
+                  w: int = DEFAULT_TILE, t: int = DEFAULT_FRAMES, seed: int = 1) -> NoiseStack:
+    """The pipeline's default STBN tile (noise.py:456-468), read from its RNKSTACK cache."""
+    name = f"stbn_{h}x{w}x{t}_s{seed}.noise"
+    for d in ([Path(cache_dir)] if cache_dir is not None else []) + [_DATA]:
+        if (d / name).exists():
+            return load_stack(d / name)
+    raise ValueError(
+        f"no cached noise stack {name}: generation is an offline step of the reference "
+        "(fovray.noise.gen_stbn); cache it with save_stack() and pass cache_dir")

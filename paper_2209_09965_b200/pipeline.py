@@ -1,0 +1,109 @@
+"""Device-resident per-frame pipeline: mask -> compaction -> march -> reconstruction.
+
+One FramePipeline owns everything a frame touches on the GPU (volume view, fp16
+weights, recurrent state + activations, compacted index list) and launches the
+whole of bench.cmd_bench_throughput's loop body (pkg/src/fovray/bench.py:194-209)
+without host round trips: the mask kernel writes channels 0..4 of the network
+input, the marcher writes the RGBA of active pixels into it, the network reads
+it, and the D.head epilogue writes next frame's O_d feedback into channels 5..7.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .network import WNetParams, _DevState
+from .noise import NoiseStack
+from .renderer import RenderSettings, Scene
+from .sample_maps import FoveaConfig
+from .volume import Camera
+
+
+class FramePipeline:
+    def __init__(self, scene: Scene, net: WNetParams | None, dims: tuple[int, int], noise: NoiseStack,
+                 settings: RenderSettings = RenderSettings(), ctx: _lib.Context | None = None):
+        import torch
+
+        self.ctx = ctx or _lib.context()
+        self.ctx.ensure_noise(noise)
+        self.scene = scene
+        self.h, self.w = dims
+        self.settings = settings
+        self._set = settings.c_struct()
+        self._light = scene.light.c_struct() if scene.light is not None else None
+        self.vol = scene.volume.handle(self.ctx, scene.tf)
+        self.net = net
+        self.net_h = net.handle(self.ctx) if net is not None else None
+        self.state = _DevState(self.ctx, self.net_h, self.h, self.w) if net is not None else None
+        n = self.h * self.w
+        self.idx = torch.empty((n,), dtype=torch.int32, device="cuda")
+        self.k = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        self.rgb = torch.empty((self.h, self.w, 3), dtype=torch.float32, device="cuda")
+        self.dense_rgba = None
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+
+    def reset(self) -> None:
+        if self.state is not None:
+            _lib.check(self.ctx.lib.fv_state_reset(self.ctx.h, self.state.h))
+
+    def _light_ref(self):
+        return C.byref(self._light) if self._light is not None else None
+
+    def mask(self, fovea: FoveaConfig, frame: int) -> None:
+        f = fovea.c_struct()
+        _lib.check(self.ctx.lib.fv_mask_compact(self.ctx.h, int(frame), self.h, self.w, C.byref(f), None,
+                                                None, _lib.ptr(self.idx), _lib.ptr(self.k),
+                                                self.state.h if self.state else None))
+
+    def march(self, cam: Camera) -> None:
+        camc = cam.c_struct()
+        _lib.check(self.ctx.lib.fv_render_sparse(
+            self.ctx.h, self.vol, C.byref(camc), self._light_ref(), C.byref(self._set),
+            _lib.ptr(self.idx), _lib.ptr(self.k), self.h * self.w, None, None,
+            self.state.h if self.state else None, None))
+
+    def reconstruct(self, use_kernel_stage: bool = True) -> None:
+        _lib.check(self.ctx.lib.fv_reconstruct(self.ctx.h, self.net_h, self.state.h, int(use_kernel_stage),
+                                               _lib.ptr(self.rgb), None, None))
+
+    def step(self, cam: Camera, fovea: FoveaConfig, frame: int, timed: bool = False):
+        """One foveated frame on the device; returns per-phase ms when timed (syncs)."""
+        s = self.ctx.stream
+        if timed:
+            self.ev[0].record(s)
+        self.mask(fovea, frame)
+        if timed:
+            self.ev[1].record(s)
+        self.march(cam)
+        if timed:
+            self.ev[2].record(s)
+        self.reconstruct()
+        if timed:
+            self.ev[3].record(s)
+            self.ev[3].synchronize()
+            return (self.ev[0].elapsed_time(self.ev[1]), self.ev[1].elapsed_time(self.ev[2]),
+                    self.ev[2].elapsed_time(self.ev[3]))
+        return None
+
+    def dense(self, cam: Camera):
+        """Dense baseline frame (render_full, renderer.py:211-222) into a device buffer."""
+        import torch
+
+        if self.dense_rgba is None:
+            self.dense_rgba = torch.empty((self.h, self.w, 4), dtype=torch.float32, device="cuda")
+        camc = cam.c_struct()
+        _lib.check(self.ctx.lib.fv_render_full(self.ctx.h, self.vol, C.byref(camc), self._light_ref(),
+                                               C.byref(self._set), _lib.ptr(self.dense_rgba), None, None))
+
+    def frame_to_host(self, cam: Camera, fovea: FoveaConfig, frame: int, host_rgb: np.ndarray):
+        """The whole frame through the C ABI's fv_frame with a host output buffer."""
+        camc = cam.c_struct()
+        f = fovea.c_struct()
+        t = (C.c_double * 4)()
+        _lib.check(self.ctx.lib.fv_frame(self.ctx.h, self.vol, self.net_h, self.state.h, C.byref(camc),
+                                         self._light_ref(), C.byref(self._set), C.byref(f), int(frame),
+                                         C.c_void_p(host_rgb.ctypes.data if isinstance(host_rgb, np.ndarray)
+                                                    else host_rgb.data_ptr()), t))
+        return tuple(t)

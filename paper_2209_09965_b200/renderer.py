@@ -1,0 +1,243 @@
+"""Ray-marched volume rendering on the GPU: dense frames and compacted sparse frames.
+
+Drop-in for the hot-path half of pkg/src/fovray/renderer.py. render_full
+(:211-222) and render_sparse_compact (:262-288) call the CUDA marcher
+(fv_render_full / fv_render_sparse) which follows _march (:150-195) and
+shadow_transmittance (:109-147): front-to-back emission-absorption with opacity
+correction 1-(1-a)^(dt/reference_step), depth at the first alpha>=0.5 crossing,
+early termination and one shadow ray toward the light per contributing sample.
+Frames keep their RGBA/depth on the device; `.rgba` / `.depth` copy to NumPy on
+first access. Camera paths (orbit_cameras, :317-361) are host math.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import csv
+import json
+import time
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _lib
+from .sample_maps import CompactIndexList, SampleMask
+from .volume import Camera, Light, TransferFunction, VolumeGrid
+
+
+@dataclass(frozen=True)
+class Scene:
+    volume: VolumeGrid
+    tf: TransferFunction
+    light: Light | None = None
+
+
+@dataclass(frozen=True)
+class RenderSettings:
+    """renderer.RenderSettings (renderer.py:44-65) + the device arithmetic tier.
+
+    precision="fp32" marches in float (the fast tier); "fp64" runs the per-sample
+    arithmetic in double. Step control and sample positions are fp64 in both.
+    """
+
+    step_size: float | None = None
+    shadow_step_factor: float = 4.0
+    early_term_alpha: float = 0.99
+    background: tuple[float, float, float, float] = (0.0, 0.0, 0.0, 0.0)
+    ambient: float = 0.25
+    reference_step: float | None = None
+    shadow_min_transmittance: float = 1e-3
+    precision: str = "fp32"
+
+    def __post_init__(self):
+        if self.step_size is not None and self.step_size <= 0:
+            raise ValueError("step_size must be > 0")
+        if self.shadow_step_factor < 1:
+            raise ValueError("shadow_step_factor must be >= 1")
+        if self.precision not in ("fp32", "fp64"):
+            raise ValueError(f"precision must be 'fp32' or 'fp64', got {self.precision!r}")
+
+    def resolve(self, vol: VolumeGrid) -> tuple[float, float]:
+        base = float(min(vol.spacing))
+        step = self.step_size if self.step_size is not None else 0.5 * base
+        ref = self.reference_step if self.reference_step is not None else base
+        return step, ref
+
+    def c_struct(self) -> _lib.FvSettings:
+        s = _lib.FvSettings()
+        s.step_size = float(self.step_size) if self.step_size is not None else 0.0
+        s.shadow_step_factor = float(self.shadow_step_factor)
+        s.early_term_alpha = float(self.early_term_alpha)
+        for i in range(4):
+            s.background[i] = float(self.background[i])
+        s.ambient = float(self.ambient)
+        s.reference_step = float(self.reference_step) if self.reference_step is not None else 0.0
+        s.shadow_min_transmittance = float(self.shadow_min_transmittance)
+        s.precision = _lib.PREC_FP64 if self.precision == "fp64" else _lib.PREC_FP32
+        return s
+
+
+class Frame:
+    """renderer.Frame (renderer.py:68-80) over device tensors."""
+
+    def __init__(self, rgba_dev, depth_dev=None, mask_ms=0.0, render_ms=0.0, reconstruct_ms=0.0,
+                 total_ms=0.0, work_items=0, stats=None):
+        self.rgba_dev = rgba_dev
+        self.depth_dev = depth_dev
+        self.mask_ms = mask_ms
+        self.render_ms = render_ms
+        self.reconstruct_ms = reconstruct_ms
+        self.total_ms = total_ms
+        self.work_items = work_items
+        self.stats = stats
+        self._rgba = None
+        self._depth = None
+
+    @property
+    def rgba(self) -> np.ndarray:
+        if self._rgba is None:
+            self._rgba = self.rgba_dev.cpu().numpy()
+        return self._rgba
+
+    @property
+    def depth(self) -> np.ndarray | None:
+        if self._depth is None and self.depth_dev is not None:
+            self._depth = self.depth_dev.cpu().numpy()
+        return self._depth
+
+    @property
+    def dims(self) -> tuple[int, int]:
+        return int(self.rgba_dev.shape[0]), int(self.rgba_dev.shape[1])
+
+
+class SparseFrame(Frame):
+    def __init__(self, *args, mask: SampleMask | None = None, **kw):
+        super().__init__(*args, **kw)
+        self.mask = mask
+
+
+def _light_ptr(scene: Scene):
+    return C.byref(scene.light.c_struct()) if scene.light is not None else None
+
+
+def render_full(scene: Scene, cam: Camera, settings: RenderSettings = RenderSettings(),
+                stats: bool = False) -> Frame:
+    """Dense baseline: one ray per pixel (renderer.py:211-222)."""
+    import torch
+
+    ctx = _lib.context()
+    vol = scene.volume.handle(ctx, scene.tf)
+    h, w = cam.height, cam.width
+    rgba = torch.empty((h, w, 4), dtype=torch.float32, device="cuda")
+    depth = torch.empty((h, w), dtype=torch.float32, device="cuda")
+    st = _lib.FvStats() if stats else None
+    camc, setc = cam.c_struct(), settings.c_struct()
+    lightc = scene.light.c_struct() if scene.light is not None else None
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(ctx.stream)
+    _lib.check(ctx.lib.fv_render_full(ctx.h, vol, C.byref(camc), C.byref(lightc) if lightc else None,
+                                      C.byref(setc), _lib.ptr(rgba), _lib.ptr(depth),
+                                      C.byref(st) if st is not None else None))
+    ev1.record(ctx.stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    return Frame(rgba, depth, render_ms=ms, total_ms=ms, work_items=w * h, stats=st)
+
+
+def render_sparse_compact(scene: Scene, cam: Camera, compact: CompactIndexList,
+                          settings: RenderSettings = RenderSettings(), stats: bool = False,
+                          net_state=None) -> SparseFrame:
+    """March exactly one work item per compacted entry and back-project (renderer.py:262-288)."""
+    import torch
+
+    if compact.dims != (cam.height, cam.width):
+        raise ValueError(f"compact dims {compact.dims} != film {cam.height}x{cam.width}")
+    if compact._coords is not None and compact.count and (
+            compact._coords[:, 0].max() >= cam.width or compact._coords[:, 1].max() >= cam.height):
+        raise ValueError("compact indices out of film range")
+    ctx = _lib.context()
+    vol = scene.volume.handle(ctx, scene.tf)
+    h, w = cam.height, cam.width
+    rgba = torch.zeros((h, w, 4), dtype=torch.float32, device="cuda")
+    depth = torch.zeros((h, w), dtype=torch.float32, device="cuda")
+    st = _lib.FvStats() if stats else None
+    camc, setc = cam.c_struct(), settings.c_struct()
+    lightc = scene.light.c_struct() if scene.light is not None else None
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(ctx.stream)
+    _lib.check(ctx.lib.fv_render_sparse(
+        ctx.h, vol, C.byref(camc), C.byref(lightc) if lightc else None, C.byref(setc),
+        _lib.ptr(compact.idx_dev), _lib.ptr(compact.k_dev), int(compact.idx_dev.numel()),
+        _lib.ptr(rgba), _lib.ptr(depth), net_state, C.byref(st) if st is not None else None))
+    ev1.record(ctx.stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    from .sample_maps import scatter
+
+    return SparseFrame(rgba, depth, render_ms=ms, total_ms=ms, work_items=compact.count,
+                       mask=scatter(compact), stats=st)
+
+
+@dataclass(frozen=True)
+class OrbitPathSpec:
+    """Oscillating-zoom orbit around the volume centre (renderer.py:317-339)."""
+
+    n_frames: int = 64
+    radius_factor: float = 2.2
+    zoom_amplitude: float = 0.35
+    zoom_periods: float = 2.0
+    yaw_turns: float = 1.0
+    pitch_amplitude_deg: float = 25.0
+    pitch_periods: float = 1.0
+    speed_profile: str = "uniform"
+    seed_phase: float = 0.0
+
+    def parameter(self, i: int) -> float:
+        if self.n_frames <= 1:
+            return 0.0
+        u = i / self.n_frames
+        if self.speed_profile == "fast_slow_fast":
+            return u + 0.22 * np.sin(2.0 * np.pi * u)
+        return u
+
+
+def orbit_cameras(spec: OrbitPathSpec, vol: VolumeGrid, width: int, height: int,
+                  fov_y: float = 45.0) -> list[Camera]:
+    """Camera path of renderer.orbit_cameras (renderer.py:342-361)."""
+    center = vol.center()
+    diag = float(np.linalg.norm(vol.extent))
+    cams = []
+    for i in range(spec.n_frames):
+        s = spec.parameter(i)
+        yaw = 2.0 * np.pi * (spec.yaw_turns * s + spec.seed_phase)
+        pitch = np.deg2rad(spec.pitch_amplitude_deg) * np.sin(2.0 * np.pi * spec.pitch_periods * s)
+        r = spec.radius_factor * diag * (1.0 + spec.zoom_amplitude *
+                                         np.sin(2.0 * np.pi * spec.zoom_periods * s))
+        pos = center + r * np.array([np.cos(pitch) * np.cos(yaw), np.sin(pitch),
+                                     np.cos(pitch) * np.sin(yaw)])
+        cams.append(Camera(position=tuple(pos), look_at=tuple(center), up=(0.0, 1.0, 0.0),
+                           fov_y=fov_y, width=width, height=height))
+    return cams
+
+
+def save_camera_path(cams: list[Camera], path: str | Path, spec: OrbitPathSpec | None = None) -> None:
+    doc = {"keyframes": [{"position": list(c.position), "look_at": list(c.look_at), "up": list(c.up),
+                          "fov_y": c.fov_y, "width": c.width, "height": c.height} for c in cams]}
+    if spec is not None:
+        doc["generator"] = {k: getattr(spec, k) for k in spec.__dataclass_fields__}
+    Path(path).write_text(json.dumps(doc, indent=1))
+
+
+def load_camera_path(path: str | Path) -> list[Camera]:
+    doc = json.loads(Path(path).read_text())
+    return [Camera(position=tuple(k["position"]), look_at=tuple(k["look_at"]), up=tuple(k["up"]),
+                   fov_y=k["fov_y"], width=k["width"], height=k["height"]) for k in doc["keyframes"]]
+
+
+def write_timing_csv(path: str | Path, rows, config_echo: dict | None = None) -> None:
+    with open(path, "w", newline="") as f:
+        if config_echo:
+            f.write("# " + json.dumps(config_echo) + "\n")
+        writer = csv.writer(f)
+        writer.writerow(["frame", "mask_ms", "render_ms", "reconstruct_ms", "total_ms"])
+        writer.writerows(rows)

@@ -1,0 +1,356 @@
+"""GPU parity: libfovnet (through the C ABI) against the oracle and the reference's golden fixtures.
+
+Tolerances (stated here, derived in DESIGN.md):
+  mask / compaction      bit-exact (bits and ordered index list)
+  procedural volume      bit-exact at golden sizes; <= 1 f32 ulp on a vanishing fraction at 256^3
+  marcher, fp64 tier     max |err| <= 1e-9 on RGBA/depth
+  marcher, fp32 tier     max |err| <= 2e-3, and <= 1e-4 on >= 99.9% of pixel values
+  conv layer (fp16 in, fp32 acc, fp16 out) vs fp32 conv of the same fp16 inputs: rel <= 2e-3
+  W-Net (fp16 storage) vs the fp32 oracle/reference: PSNR >= 60 dB (paper net), max|err| <= 5e-3
+  end to end (C1 golden, 2 carried frames): PSNR >= 55 dB, SSIM >= 0.99
+"""
+import ctypes as C
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no GPU", allow_module_level=True)
+
+from oracle import fovray_oracle as O  # noqa: E402
+from paper_2209_09965_b200 import _lib  # noqa: E402
+from paper_2209_09965_b200 import network as N  # noqa: E402
+from paper_2209_09965_b200 import sample_maps as S  # noqa: E402
+from paper_2209_09965_b200.noise import default_stack  # noqa: E402
+from paper_2209_09965_b200.renderer import RenderSettings, Scene, render_full, render_sparse_compact  # noqa: E402
+from paper_2209_09965_b200.volume import Camera, Light, TransferFunction, make_procedural_volume  # noqa: E402
+
+
+def sha(b):
+    return hashlib.sha256(b).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def stack():
+    return default_stack()
+
+
+# ---------------------------------------------------------------- mask
+def test_mask_compaction_bit_exact_all_golden_configs(golden, stack):
+    recs = json.loads((golden / "masks.json").read_text())
+    small = np.load(golden / "masks_small.npz")
+    for r in recs:
+        cfg = S.FoveaConfig(focus=tuple(r["focus"]), sigma=r["sigma"], base_density=r["pb"],
+                            pixel_scale=r["pixel_scale"])
+        m = S.build_sample_mask(stack, r["frame"], S.build_tau_map(cfg, (r["H"], r["W"])))
+        comp = S.compact_mask(m)
+        assert comp.count == r["k"], r["name"]
+        bits = m.bits
+        assert sha(np.packbits(bits.ravel()).tobytes()) == r["sha_bits"], r["name"]
+        flat = comp.idx_dev[: comp.count].cpu().numpy().astype(np.int32)
+        assert sha(flat.tobytes()) == r["sha_idx"], r["name"]
+        if r["name"] in small.files:
+            assert np.array_equal(bits, small[r["name"]])
+
+
+def test_mask_moving_gaze_500_frames_bit_exact(stack):
+    """Config 4's moving gaze over the 500-frame path at 1080p hifi (oracle each 25th frame)."""
+    h, w = 1080, 1920
+    sc = S.pixel_scale_for_film((h, w))
+    for i in range(0, 500, 25):
+        fx = (w - 1) / 2.0 + 0.4 * w * np.sin(2 * np.pi * i / 500)
+        fy = (h - 1) / 2.0 + 0.4 * h * np.sin(4 * np.pi * i / 500)
+        cfg = S.FoveaConfig(focus=(fx, fy), sigma=0.06, base_density=0.07, pixel_scale=sc)
+        m = S.build_sample_mask(stack, i, S.build_tau_map(cfg, (h, w)))
+        ref = O.sample_mask(stack.values, h, w, i, O.tau_map(h, w, (fx, fy), 0.06, 0.07, sc))
+        assert np.array_equal(m.bits, ref), i
+        assert np.array_equal(S.compact_mask(m).idx_dev[: int(ref.sum())].cpu().numpy(), O.compact(ref))
+
+
+def test_mask_edge_cases(stack):
+    # empty mask, full mask, 1-pixel film, explicit tau map, per-pixel base density
+    for tau_val, expect in ((0.0, 0), (1.0, 23 * 37)):
+        m = S.build_sample_mask(stack, 2, S.TauMap(values=np.full((23, 37), tau_val)))
+        assert S.compact_mask(m).count == expect
+    m = S.build_sample_mask(stack, 0, S.build_tau_map(S.FoveaConfig(focus=(0, 0)), (1, 1)))
+    assert S.compact_mask(m).count == 1  # tau == 1 at the focus
+    pb = np.full((40, 50), 0.2)
+    pb[:10] = 0.9
+    cfg = S.FoveaConfig(focus=(25, 20), sigma=10.0, base_density=pb, pixel_scale=0.1)
+    m = S.build_sample_mask(stack, 1, S.build_tau_map(cfg, (40, 50)))
+    ref = O.sample_mask(stack.values, 40, 50, 1, O.tau_map(40, 50, (25, 20), 10.0, pb, 0.1))
+    assert np.array_equal(m.bits, ref)
+    tau = S.build_tau_map(cfg, (40, 50))
+    np.testing.assert_allclose(tau.values, O.tau_map(40, 50, (25, 20), 10.0, pb, 0.1), rtol=0, atol=1e-15)
+    assert S.c_max(tau) == pytest.approx(O.tau_map(40, 50, (25, 20), 10.0, pb, 0.1).mean(), rel=1e-12)
+
+
+def test_scatter_roundtrip(stack):
+    cfg = S.FoveaConfig(focus=(30, 10), sigma=0.3, base_density=0.2, pixel_scale=0.1)
+    m = S.build_sample_mask(stack, 4, S.build_tau_map(cfg, (33, 61)))
+    back = S.scatter(S.compact_mask(m))
+    assert np.array_equal(back.bits, m.bits)
+
+
+# ---------------------------------------------------------------- volumes
+def test_procedural_volumes_bit_exact(golden):
+    for r in json.loads((golden / "volumes.json").read_text()):
+        v = make_procedural_volume(r["kind"], tuple(r["dims"]))
+        assert sha(v.data.tobytes()) == r["sha"], (r["kind"], r["dims"])
+        assert list(v.value_range) == pytest.approx(r["value_range"], rel=1e-15)
+
+
+def test_procedural_volume_256_within_one_ulp():
+    v = make_procedural_volume("sphere_shells", (256, 256, 256)).data
+    ref, _ = O.procedural_volume("sphere_shells", (256, 256, 256))
+    diff = np.abs(v.astype(np.float64) - ref)
+    assert diff.max() <= 1.2e-7
+    assert (diff > 0).mean() < 1e-4
+
+
+# ---------------------------------------------------------------- conv engine
+def to_nc8(x):  # (C,H,W) f32 -> NC8HW8 fp16 tensor
+    c, h, w = x.shape
+    return torch.as_tensor(x.reshape(c // 8, 8, h, w).transpose(0, 2, 3, 1).copy(), device="cuda").half()
+
+
+def from_nc8(t, c):
+    a = t.float().cpu().numpy()
+    g, h, w, _ = a.shape
+    return a.transpose(0, 3, 1, 2).reshape(g * 8, h, w)[:c]
+
+
+@pytest.mark.parametrize("cin,cout,h,w", [(8, 64, 20, 136), (64, 64, 16, 256), (64, 80, 14, 70),
+                                          (176, 96, 10, 30), (24, 16, 8, 9), (32, 32, 6, 300),
+                                          (192, 64, 12, 128), (48, 16, 7, 33)])
+def test_conv3x3_tcgen05_matches_fp32_reference(cin, cout, h, w):
+    rng = np.random.default_rng(cin * 1000 + cout + h + w)
+    x = rng.standard_normal((cin, h, w)).astype(np.float32)
+    wt = (rng.standard_normal((cout, cin, 3, 3)) * np.sqrt(2.0 / (9 * cin))).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32) * 0.1
+    xh = np.asarray(x, np.float16).astype(np.float32)
+    wh = np.asarray(wt, np.float16).astype(np.float32)
+    ref = O.relu(O.conv3x3(xh, wh, b))
+    ctx = _lib.context()
+    xt = to_nc8(x)
+    gout = (cout + 7) // 8
+    y = torch.zeros((gout, h, w, 8), dtype=torch.float16, device="cuda")
+    pool = torch.zeros((gout, h // 2, w // 2, 8), dtype=torch.float16, device="cuda")
+    _lib.check(ctx.lib.fv_debug_conv3x3(ctx.h, cin, cout, h, w, _lib.ptr(xt), wt.ctypes.data_as(C.c_void_p),
+                                        b.ctypes.data_as(C.c_void_p), _lib.ptr(y),
+                                        _lib.ptr(pool) if h % 2 == 0 and w % 2 == 0 else None, 1))
+    got = from_nc8(y, cout)
+    scale = np.abs(ref).max()
+    assert np.abs(got - ref).max() <= 2e-3 * scale + 1e-3
+    if h % 2 == 0 and w % 2 == 0:
+        np.testing.assert_allclose(from_nc8(pool, cout), O.pool2(ref), atol=2e-3 * scale + 1e-3)
+
+
+# ---------------------------------------------------------------- marcher
+CAM = dict(position=(80.0, 60.0, 90.0), look_at=(16.0, 16.0, 16.0), fov_y=40.0, width=64, height=36)
+
+
+@pytest.fixture(scope="module")
+def scene32():
+    vol = make_procedural_volume("sphere_shells", (32, 32, 32))
+    return Scene(volume=vol, tf=TransferFunction.default(),
+                 light=Light(direction=(-1.0, -1.0, -0.5), intensity=(1.0, 1.0, 1.0)))
+
+
+def check_fp32(got, ref):
+    d = np.abs(got - ref)
+    assert d.max() <= 2e-3, d.max()
+    assert (d <= 1e-4).mean() >= 0.999, (d <= 1e-4).mean()
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("key,kw,light", [
+    ("full64", {}, "dir"),
+    ("bg64", dict(background=(0.1, 0.2, 0.3, 0.5), early_term_alpha=1.1, step_size=0.37), "dir"),
+    ("nolight64", {}, None),
+    ("point64", {}, "point"),
+])
+def test_render_full_vs_reference_golden(golden, scene32, prec, key, kw, light):
+    g = np.load(golden / "render_small.npz")
+    lt = {"dir": scene32.light, None: None,
+          "point": Light(position=(40.0, 50.0, -10.0), intensity=(0.9, 1.0, 0.8))}[light]
+    sc = Scene(volume=scene32.volume, tf=scene32.tf, light=lt)
+    fr = render_full(sc, Camera(**CAM), RenderSettings(precision=prec, **kw))
+    if prec == "fp64":
+        np.testing.assert_allclose(fr.rgba, g[key + "_rgba"], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(fr.depth, g[key + "_depth"], rtol=0, atol=1e-6)
+    else:
+        check_fp32(fr.rgba, g[key + "_rgba"])
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_render_sparse_compact_vs_reference_golden(golden, scene32, stack, prec):
+    g = np.load(golden / "render_small.npz")
+    m = S.SampleMask(bits=g["sparse64_bits"])
+    fr = render_sparse_compact(scene32, Camera(**CAM), S.compact_mask(m), RenderSettings(precision=prec))
+    tol = 1e-9 if prec == "fp64" else 2e-3
+    assert np.abs(fr.rgba - g["sparse64_rgba"]).max() <= tol
+    assert np.all(fr.rgba[~g["sparse64_bits"]] == 0)
+    assert fr.work_items == int(g["sparse64_bits"].sum())
+
+
+def test_render_golden_160_fp64(golden, scene32):
+    g = np.load(golden / "render_small.npz")
+    fr = render_full(scene32, Camera(**dict(CAM, width=160, height=90)), RenderSettings(precision="fp64"))
+    np.testing.assert_allclose(fr.rgba, g["full160_rgba"], rtol=0, atol=1e-9)
+
+
+def test_render_anisotropic_volume(golden):
+    g = np.load(golden / "render_small.npz")
+    vv = make_procedural_volume("vortex_field", (33, 17, 9), spacing=(1.0, 2.0, 0.5))
+    sc = Scene(volume=vv, tf=TransferFunction.default(), light=Light(direction=(0.3, -1.0, 0.2)))
+    cam = Camera(position=(60.0, 50.0, -30.0), look_at=(16.0, 17.0, 2.0), fov_y=50.0, width=48, height=40,
+                 up=(0.0, 0.0, 1.0))
+    fr = render_full(sc, cam, RenderSettings(precision="fp64"))
+    np.testing.assert_allclose(fr.rgba, g["aniso_rgba"], rtol=0, atol=1e-9)
+    check_fp32(render_full(sc, cam).rgba, g["aniso_rgba"])
+
+
+def test_render_c1_orbit_frames(golden):
+    g = np.load(golden / "render_small.npz")
+    vol = make_procedural_volume("sphere_shells", (64, 64, 64))
+    sc = Scene(volume=vol, tf=TransferFunction.default(), light=Light(direction=(-1.0, -1.0, -0.5)))
+    for i in (0, 137):
+        pos, look = O.orbit_camera(i, 500, (64, 64, 64))
+        cam = Camera(position=pos, look_at=look, fov_y=45.0, width=96, height=96)
+        comp = S.compact_mask(S.SampleMask(bits=g[f"orbit{i}_bits"]))
+        for prec in ("fp64", "fp32"):
+            fr = render_sparse_compact(sc, cam, comp, RenderSettings(precision=prec), stats=True)
+            if prec == "fp64":
+                np.testing.assert_allclose(fr.rgba, g[f"orbit{i}_rgba"], rtol=0, atol=1e-9)
+            else:
+                check_fp32(fr.rgba, g[f"orbit{i}_rgba"])
+
+
+def test_sample_counts_match_oracle_512_subset(stack):
+    """Work accounting: device sample counters == oracle counts on a 1080p/512^3 ray subset."""
+    vol = make_procedural_volume("sphere_shells", (512, 512, 512))
+    sc = Scene(volume=vol, tf=TransferFunction.default(), light=Light(direction=(-1.0, -1.0, -0.5)))
+    pos, look = O.orbit_camera(0, 500, (512, 512, 512))
+    cam = Camera(position=pos, look_at=look, fov_y=45.0, width=1920, height=1080)
+    rng = np.random.default_rng(0)
+    pix = np.sort(rng.choice(1920 * 1080, 3000, replace=False))
+    pix = np.concatenate([pix, np.arange(540 * 1920 + 900, 540 * 1920 + 1020)])
+    pix = np.unique(pix)
+    coords = np.stack([pix % 1920, pix // 1920], 1)
+    comp = S.CompactIndexList(coords=coords, dims=(1080, 1920))
+    fr = render_sparse_compact(sc, cam, comp, RenderSettings(precision="fp64"), stats=True)
+    ref, rdep, counts = O.render(vol.data, (1, 1, 1), O.DEFAULT_LUT, ("dir", (-1.0, -1.0, -0.5), (1, 1, 1)),
+                                 dict(position=pos, look_at=look, fov_y=45.0, width=1920, height=1080),
+                                 pix=pix, with_counts=True)
+    got = fr.rgba.reshape(-1, 4)[pix]
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-9)
+    assert fr.stats.samples_main == counts[:, 0].sum()
+    assert fr.stats.samples_shadow == counts[:, 1].sum()
+    fr32 = render_sparse_compact(sc, cam, comp, RenderSettings(), stats=True)
+    check_fp32(fr32.rgba.reshape(-1, 4)[pix], ref)
+
+
+# ---------------------------------------------------------------- network
+@pytest.mark.parametrize("tag,blocks,seed,frames,fp16", [
+    ("desk", N.DESK_BLOCKS, 7, 2, False), ("deskpad", N.DESK_BLOCKS, 7, 2, False),
+    ("full", N.FULL_BLOCKS, 0, 3, True), ("fullwide", N.FULL_BLOCKS, 3, 2, True)])
+def test_forward_full_vs_reference_golden(golden, tag, blocks, seed, frames, fp16):
+    g = np.load(golden / "net_small.npz")
+    net = N.init_network(N.NetConfig.from_string(blocks), seed=seed)
+    if fp16:
+        net = N.quantized_net(net, "fp16")
+    x0 = g[f"{tag}_x0"]
+    state = N.reset_state(net.config, x0.shape[2:])
+    for f in range(frames):
+        o, od, state = N.forward_full(net, g[f"{tag}_x{f}"], state)
+        ref = g[f"{tag}_o{f}"]
+        q = O.psnr(np.moveaxis(o.data[0], 0, -1), np.moveaxis(ref[0], 0, -1))
+        assert q >= (60.0 if fp16 else 50.0), (f, q)
+        assert np.abs(o.data - ref).max() <= (5e-3 if fp16 else 2e-2)
+        assert np.abs(od.data - g[f"{tag}_od{f}"]).max() <= (5e-3 if fp16 else 2e-2)
+    for j, h in enumerate(state.hidden):
+        ref = g[f"{tag}_hidden{j}"]
+        assert np.abs(h.data - ref).max() <= 2e-2 * max(1.0, np.abs(ref).max())
+    # direct ablation (use_kernel_stage=False) on a fresh state
+    o2, od2, _ = N.forward_full(net, g[f"{tag}_x0"], N.reset_state(net.config, x0.shape[2:]),
+                                use_kernel_stage=False)
+    assert np.array_equal(o2.data, od2.data)
+
+
+def test_forward_state_semantics(golden):
+    g = np.load(golden / "net_small.npz")
+    net = N.init_network(N.NetConfig.from_string(N.DESK_BLOCKS), seed=7)
+    x = g["desk_x0"]
+    s = N.reset_state(net.config, (32, 32))
+    o1, _, s1 = N.forward_full(net, x, s)
+    oc, _, _ = N.forward_full(net, x, s1)
+    orr, _, _ = N.forward_full(net, x, N.reset_state(net.config, (32, 32)))
+    assert np.array_equal(orr.data, o1.data)
+    assert not np.array_equal(oc.data, o1.data)
+    with pytest.raises(ValueError, match="reset"):
+        N.forward_full(net, x, N.reset_state(net.config, (64, 64)))
+    with pytest.raises(ValueError, match="consumed"):
+        N.forward_full(net, x, s)
+    # explicit zero state equals the reset state (reference tests/test_network.py:93-109)
+    cfg = net.config
+    d_ch = cfg.channels()[cfg.n_enc:]
+    hid = [np.zeros((1, d_ch[j], 32 >> (cfg.n_enc - j), 32 >> (cfg.n_enc - j)), np.float32)
+           for j in range(cfg.n_dec)]
+    o2, _, _ = N.forward_full(net, x, N.RecurrentState((32, 32), hid, np.zeros((1, 3, 32, 32), np.float32),
+                                                       _config=cfg))
+    assert np.array_equal(o2.data, o1.data)
+
+
+def test_kernel_stage_identity_and_box_blur():
+    """Reference tests/test_network.py:123-198: forced K weights give identity / box-blur filters."""
+    cfg = N.NetConfig.from_string(N.DESK_BLOCKS)
+    net = N.init_network(cfg, seed=0)
+    for name in list(net.params):
+        if name.startswith("K."):
+            net.params[name] = np.zeros_like(net.params[name])
+    rng = np.random.default_rng(6)
+    rgba = rng.random((1, 4, 16, 16)).astype(np.float32)
+    m = (rng.random((1, 1, 16, 16)) < 0.2).astype(np.float32)
+    x = np.concatenate([rgba * m, m], 1)
+    o, od, _ = N.forward_full(net, x, N.reset_state(cfg, (16, 16)))
+    ref = od.data[0].astype(np.float64)
+    for i, (kind, _) in enumerate(cfg.block_config):
+        ref = O.kernel_filter(ref, np.zeros((9,) + ref.shape[1:]))
+        if kind == "e":
+            ref = O.pool2(ref)
+        elif i < len(cfg.block_config) - 1:
+            ref = O.up2(ref)
+    np.testing.assert_allclose(o.data[0], ref, atol=1e-4)
+
+
+# ---------------------------------------------------------------- end to end
+def test_end_to_end_c1_against_reference(golden, stack):
+    """C1: 64^3, 256x256, fast preset, FULL_BLOCKS seed 0 fp16 weights, two carried frames."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    g = np.load(golden / "e2e_c1.npz")
+    spec = ExperimentSpec(mode="fast", width=256, height=256)
+    scene = default_scene("sphere_shells", (64, 64, 64))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, 256, 256)
+    pipe = FramePipeline(scene, net, (256, 256), stack)
+    for i in range(2):
+        pipe.step(cams[i], spec.fovea(), i)
+        img = pipe.rgb.cpu().numpy()
+        ref = g[f"img{i}"]
+        q, s = O.psnr(img, ref), O.ssim(img, ref)
+        assert q >= 55.0 and s >= 0.99, (i, q, s)
+    # the C-ABI whole-frame call with a host output buffer gives the same frame-2 result path
+    host = np.empty((256, 256, 3), np.float32)
+    pipe.reset()
+    for i in range(2):
+        pipe.frame_to_host(cams[i], spec.fovea(), i, host)
+    assert O.psnr(host, g["img1"]) >= 55.0

@@ -1,0 +1,136 @@
+"""The CPU oracle is pinned to the reference: fixtures in tests/golden were produced by running
+the unmodified reference package (tests/golden/make_golden.py)."""
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import fovray_oracle as O
+
+
+def sha(b: bytes) -> str:
+    return hashlib.sha256(b).hexdigest()
+
+
+def test_stbn_stack_is_the_reference_default(stack_values):
+    # SHA-256 of default_stack() float32 LE values
+    assert sha(stack_values.astype("<f4").tobytes()) == \
+        "25e032671e1102611b5c2c8032037f58d8625c69635df88cde124426f68605d5"
+
+
+def test_masks_bit_exact_against_reference(golden, stack_values):
+    recs = json.loads((golden / "masks.json").read_text())
+    small = np.load(golden / "masks_small.npz")
+    for r in recs:
+        tau = O.tau_map(r["H"], r["W"], r["focus"], r["sigma"], r["pb"], r["pixel_scale"])
+        bits = O.sample_mask(stack_values, r["H"], r["W"], r["frame"], tau)
+        idx = O.compact(bits).astype(np.int32)
+        assert idx.size == r["k"], r["name"]
+        assert sha(np.packbits(bits.ravel()).tobytes()) == r["sha_bits"], r["name"]
+        assert sha(idx.tobytes()) == r["sha_idx"], r["name"]
+        if r["name"] in small.files:
+            assert np.array_equal(bits, small[r["name"]])
+
+
+def test_cmax_fsum_point():
+    # reference tests/test_sample_maps.py:134-152 (fsum oracle at 1280x720, rel 1e-12)
+    import math
+    tau = O.tau_map(720, 1280, (639.5, 359.5), 0.02, 0.03, 1.0 / 32.0)
+    s = 1.0 / 32.0
+    acc = []
+    for v in range(0, 720, 9):
+        dy2 = ((v - 359.5) * s) ** 2
+        acc.append(math.fsum(math.exp(-0.5 * (((u - 639.5) * s) ** 2 + dy2) * 0.02) * 0.97 + 0.03
+                             for u in range(1280)))
+    oracle = math.fsum(acc) / (80 * 1280)
+    assert tau[::9].mean() == pytest.approx(oracle, rel=1e-12)
+
+
+def test_focus_pixel_tau_is_one():
+    tau = O.tau_map(16, 16, (7.0, 3.0), 0.04, 0.03, 1.0 / 32)
+    assert tau[3, 7] == 1.0
+
+
+def test_procedural_volumes_bit_exact(golden):
+    for r in json.loads((golden / "volumes.json").read_text()):
+        d, vr = O.procedural_volume(r["kind"], tuple(r["dims"]))
+        assert sha(d.tobytes()) == r["sha"], (r["kind"], r["dims"])
+        assert list(vr) == r["value_range"]
+
+
+def _scene32():
+    vol, _ = O.procedural_volume("sphere_shells", (32, 32, 32))
+    return vol
+
+
+LIGHT = ("dir", (-1.0, -1.0, -0.5), (1.0, 1.0, 1.0))
+CAM = dict(position=(80.0, 60.0, 90.0), look_at=(16.0, 16.0, 16.0), fov_y=40.0, width=64, height=36)
+
+
+def test_marcher_reproduces_reference_golden_sha(golden):
+    # the reference's own golden image (pkg/tests/test_renderer.py:109-114, :276)
+    vol = _scene32()
+    rgba, _ = O.render_image(vol, (1, 1, 1), O.DEFAULT_LUT, LIGHT, dict(CAM, width=160, height=90))
+    assert sha(rgba.tobytes()) == "be47e7e86eaa47b07c7e0395a753a348844857a618006160f2dcdeead4407c0f"
+    meta = json.loads((golden / "render_small.json").read_text())
+    assert meta["full160_sha"] == sha(rgba.tobytes())
+
+
+@pytest.mark.parametrize("key,kw,light", [
+    ("full64", {}, LIGHT),
+    ("bg64", dict(background=(0.1, 0.2, 0.3, 0.5), early_term_alpha=1.1, step_size=0.37), LIGHT),
+    ("nolight64", {}, None),
+    ("point64", {}, ("point", (40.0, 50.0, -10.0), (0.9, 1.0, 0.8))),
+])
+def test_marcher_bit_exact(golden, key, kw, light):
+    g = np.load(golden / "render_small.npz")
+    rgba, depth = O.render_image(_scene32(), (1, 1, 1), O.DEFAULT_LUT, light, CAM, **kw)
+    assert np.array_equal(rgba, g[key + "_rgba"])
+    assert np.array_equal(depth, g[key + "_depth"])
+
+
+def test_sparse_and_anisotropic_bit_exact(golden):
+    g = np.load(golden / "render_small.npz")
+    rgba, depth = O.render_image(_scene32(), (1, 1, 1), O.DEFAULT_LUT, LIGHT, CAM, bits=g["sparse64_bits"])
+    assert np.array_equal(rgba, g["sparse64_rgba"]) and np.array_equal(depth, g["sparse64_depth"])
+    vv, _ = O.procedural_volume("vortex_field", (33, 17, 9))
+    cam = dict(position=(60.0, 50.0, -30.0), look_at=(16.0, 17.0, 2.0), fov_y=50.0, width=48, height=40,
+               up=(0.0, 0.0, 1.0))
+    rgba, depth = O.render_image(vv, (1.0, 2.0, 0.5), O.DEFAULT_LUT, ("dir", (0.3, -1.0, 0.2), (1, 1, 1)), cam)
+    assert np.array_equal(rgba, g["aniso_rgba"]) and np.array_equal(depth, g["aniso_depth"])
+
+
+def test_orbit_camera_sparse_frames(golden):
+    g = np.load(golden / "render_small.npz")
+    meta = json.loads((golden / "render_small.json").read_text())
+    vol, _ = O.procedural_volume("sphere_shells", (64, 64, 64))
+    for i in (0, 137):
+        pos, look = O.orbit_camera(i, 500, (64, 64, 64))
+        assert np.allclose(pos, meta[f"orbit{i}_cam"]["position"], rtol=0, atol=0)
+        rgba, depth = O.render_image(vol, (1, 1, 1), O.DEFAULT_LUT, LIGHT,
+                                     dict(position=pos, look_at=look, fov_y=45.0, width=96, height=96),
+                                     bits=g[f"orbit{i}_bits"])
+        assert np.array_equal(rgba, g[f"orbit{i}_rgba"])
+
+
+@pytest.mark.parametrize("tag,blocks,seed,frames,fp16", [
+    ("desk", O.DESK_BLOCKS, 7, 2, False), ("deskpad", O.DESK_BLOCKS, 7, 2, False),
+    ("full", O.FULL_BLOCKS, 0, 3, True), ("fullwide", O.FULL_BLOCKS, 3, 2, True)])
+def test_network_forward_matches_reference(golden, tag, blocks, seed, frames, fp16):
+    g = np.load(golden / "net_small.npz")
+    p = O.init_params(blocks, seed, fp16_weights=fp16)
+    st = None
+    for f in range(frames):
+        o, od, st = O.net_forward(p, blocks, g[f"{tag}_x{f}"][0], st)
+        # fp32 with a different summation order than the reference's BLAS
+        np.testing.assert_allclose(o, g[f"{tag}_o{f}"][0], atol=2e-5)
+        np.testing.assert_allclose(od, g[f"{tag}_od{f}"][0], atol=2e-5)
+    for j, h in enumerate(st["hidden"]):
+        np.testing.assert_allclose(h, g[f"{tag}_hidden{j}"][0], atol=2e-5)
+
+
+def test_psnr_ssim_identity():
+    a = np.random.default_rng(0).random((32, 32, 3))
+    assert O.psnr(a, a) == 100.0
+    assert O.ssim(a, a) == pytest.approx(1.0)
