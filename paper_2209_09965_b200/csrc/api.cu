@@ -199,6 +199,7 @@ int fv_volume_destroy(fv_volume* v) {
   if (!v) return 0;
   if (v->data && v->owns_data) cudaFree(v->data);
   if (v->lut_dev) cudaFree(v->lut_dev);
+  if (v->bricks) cudaFree(v->bricks);
   delete v;
   return 0;
 }
@@ -209,11 +210,13 @@ int fv_volume_upload(fv_ctx* ctx, fv_volume* v, const float* data, int on_device
   FV_CUDA(cudaMemcpyAsync(v->data, data, bytes, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                           ctx->stream));
   FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  ++v->version;
   return 0;
 }
 
 int fv_volume_procedural(fv_ctx* ctx, fv_volume* v, int kind, double* range) {
   FV_REQUIRE(ctx && v, "null argument");
+  ++v->version;
   return launch_volume_procedural(ctx, v, kind, range);
 }
 

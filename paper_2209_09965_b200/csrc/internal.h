@@ -71,6 +71,8 @@ struct fv_volume {
   float* data = nullptr;  // (nz,ny,nx)
   bool owns_data = true;
   float* lut_dev = nullptr;  // (K,4) float32, K <= 256
+  float* bricks = nullptr;   // 8^3-bricked copy used by the fp32 marcher
+  uint64_t version = 1, bricks_version = 0;
   int K = 0;
   double value_range[2] = {0, 0};
 };

@@ -16,6 +16,8 @@
 // arithmetic (trilinear lerps, transfer function, compositing) runs in `Real`: float for the
 // default fast path, double for the exact tier. One thread marches one compacted ray; its
 // shadow rays are marched inline. The TF LUT lives in shared memory.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace fv {
@@ -96,11 +98,14 @@ __device__ __forceinline__ Real trilinear(const MarchParams& P, const double p[3
   return c0 * (one - tz) + c1 * tz;
 }
 
+__device__ __forceinline__ int ifloor(float x) { return (int)floorf(x); }
+__device__ __forceinline__ int ifloor(double x) { return (int)floor(x); }
+
 template <typename Real>
 __device__ __forceinline__ void tf_apply(const float* lut, int K, Real s, Real out[4]) {
   s = s < Real(0) ? Real(0) : (s > Real(1) ? Real(1) : s);
   const Real x = s * (Real)(K - 1);
-  int i0 = (int)floor((double)x);
+  int i0 = ifloor(x);
   i0 = min(max(i0, 0), K - 2);
   const Real t = x - (Real)i0;
 #pragma unroll
@@ -112,7 +117,7 @@ template <typename Real>
 __device__ __forceinline__ Real tf_alpha(const float* lut, int K, Real s) {
   s = s < Real(0) ? Real(0) : (s > Real(1) ? Real(1) : s);
   const Real x = s * (Real)(K - 1);
-  int i0 = (int)floor((double)x);
+  int i0 = ifloor(x);
   i0 = min(max(i0, 0), K - 2);
   const Real t = x - (Real)i0;
   return (Real)lut[i0 * 4 + 3] * (Real(1) - t) + (Real)lut[(i0 + 1) * 4 + 3] * t;
@@ -254,12 +259,248 @@ __global__ void __launch_bounds__(128) march_kernel(MarchParams P) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fast tier: fp32 inner loops over a bricked copy of the volume.
+//
+// Per ray the setup (direction, slab test, entry point, main-step count) is fp64; the samples are
+// then generated as p = entry + d * (i*step + dt/2) in fp32 (<=1e-4 voxel from the reference's
+// fp64 positions) and the trilinear weights, TF and compositing run in fp32. The volume is read
+// from 8x8x8 bricks (2 KB, z-y-x inside a brick): a sample's 8 corners and the next few samples
+// of a ray share cache lines along any direction, which is what shadow rays (marching toward the
+// light at 4x the main step) need. Corner addresses are separable: addr = X[x] + Y[y] + Z[z].
+struct FastVol {
+  const float* bricks;
+  int nx, ny, nz;
+  int sby, sbz;        // brick strides (floats) in y and z
+  float ext[3];
+  float inv_sp[3];
+};
+
+__device__ __forceinline__ int bx_off(int x) { return ((x >> 3) << 9) | (x & 7); }
+
+__device__ __forceinline__ float tri_fast(const FastVol& V, float px, float py, float pz) {
+  if (!(px >= 0.f && px <= V.ext[0] && py >= 0.f && py <= V.ext[1] && pz >= 0.f && pz <= V.ext[2]))
+    return 0.f;
+  const float qx = px * V.inv_sp[0] - 0.5f, qy = py * V.inv_sp[1] - 0.5f, qz = pz * V.inv_sp[2] - 0.5f;
+  const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+  const float tx = qx - fx, ty = qy - fy, tz = qz - fz;
+  const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
+            z0 = min(max((int)fz, 0), V.nz - 1);
+  const int x1 = min(x0 + 1, V.nx - 1), y1 = min(y0 + 1, V.ny - 1), z1 = min(z0 + 1, V.nz - 1);
+  const int X0 = bx_off(x0), X1 = bx_off(x1);
+  const int Y0 = (y0 >> 3) * V.sby + ((y0 & 7) << 3), Y1 = (y1 >> 3) * V.sby + ((y1 & 7) << 3);
+  const int Z0 = (z0 >> 3) * V.sbz + ((z0 & 7) << 6), Z1 = (z1 >> 3) * V.sbz + ((z1 & 7) << 6);
+  const float* b = V.bricks;
+  const float d000 = __ldg(b + Z0 + Y0 + X0), d001 = __ldg(b + Z0 + Y0 + X1);
+  const float d010 = __ldg(b + Z0 + Y1 + X0), d011 = __ldg(b + Z0 + Y1 + X1);
+  const float d100 = __ldg(b + Z1 + Y0 + X0), d101 = __ldg(b + Z1 + Y0 + X1);
+  const float d110 = __ldg(b + Z1 + Y1 + X0), d111 = __ldg(b + Z1 + Y1 + X1);
+  const float c00 = d000 * (1.f - tx) + d001 * tx;
+  const float c10 = d010 * (1.f - tx) + d011 * tx;
+  const float c01 = d100 * (1.f - tx) + d101 * tx;
+  const float c11 = d110 * (1.f - tx) + d111 * tx;
+  const float c0 = c00 * (1.f - ty) + c10 * ty;
+  const float c1 = c01 * (1.f - ty) + c11 * ty;
+  return c0 * (1.f - tz) + c1 * tz;
+}
+
+// exponent classes of (1-a)^(dt/ref) on full steps: 0 sqrt, 1 identity, 2 square, 3 general
+__device__ __forceinline__ float keep_cls(float x, int cls, float e) {
+  if (cls == 0) return sqrtf(x);
+  if (cls == 1) return x;
+  if (cls == 2) return x * x;
+  return powf(x, e);
+}
+
+struct FastParams {
+  MarchParams P;
+  FastVol V;
+  float ld[3], ld_inv[3];  // directional light: unit direction toward the light (+ guarded inverse)
+  float lpos[3];
+  int cls_main, cls_sh;
+  float e_main, e_sh, inv_ref;
+};
+
+__device__ float shadow_fast(const FastParams& F, const float* lut, float px, float py, float pz,
+                             unsigned int& nsamp) {
+  const MarchParams& P = F.P;
+  float dir[3], inv[3], dist = INFINITY;
+  if (P.light_kind == FV_LIGHT_DIRECTIONAL) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { dir[a] = F.ld[a]; inv[a] = F.ld_inv[a]; }
+  } else {
+    const float dx = F.lpos[0] - px, dy = F.lpos[1] - py, dz = F.lpos[2] - pz;
+    dist = sqrtf(dx * dx + dy * dy + dz * dz);
+    const float m = fmaxf(dist, 1e-30f);
+    dir[0] = dx / m; dir[1] = dy / m; dir[2] = dz / m;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float s = dir[a];
+      if (fabsf(s) < 1e-30f) s = s < 0.f ? -1e-30f : 1e-30f;
+      inv[a] = 1.f / s;
+    }
+  }
+  const float p[3] = {px, py, pz};
+  float tmin = -INFINITY, tmax = INFINITY;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float ta = (0.f - p[a]) * inv[a], tb = (F.V.ext[a] - p[a]) * inv[a];
+    tmin = fmaxf(tmin, fminf(ta, tb));
+    tmax = fminf(tmax, fmaxf(ta, tb));
+  }
+  const float t0 = fmaxf(tmin, 0.f);
+  const float tend = fminf(tmax, dist);
+  float trans = 1.f;
+  if (!(tmax > t0 && tend > t0)) return trans;
+  const float step = (float)P.step_sh, mt = (float)P.min_trans;
+  float t = t0;
+#pragma unroll 1
+  while (true) {
+    const float dt = fminf(step, tend - t);
+    const float mid = t + 0.5f * dt;
+    const float a = tf_alpha<float>(lut, P.K, tri_fast(F.V, px + dir[0] * mid, py + dir[1] * mid, pz + dir[2] * mid));
+    const float keep = dt == step ? keep_cls(1.f - a, F.cls_sh, F.e_sh) : powf(1.f - a, dt * F.inv_ref);
+    trans = trans * (1.f - (1.f - keep));
+    ++nsamp;
+    t = t + dt;
+    if (!(t < tend) || !(trans > mt)) break;
+  }
+  return trans;
+}
+
+__global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
+  const MarchParams& P = F.P;
+  __shared__ float lut[4 * 256];
+  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  unsigned int n_main = 0, n_shadow = 0, hitc = 0;
+  if (i < k) {
+    const int pix = P.idx ? P.idx[i] : i;
+    const int u = pix % P.W, v = pix / P.W;
+    const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
+    const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+    const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
+    double t0, t_end;
+    bool hit;
+    ray_box(P.pos, d, P.ext, t0, t_end, hit);
+    float rgb[3] = {0.f, 0.f, 0.f};
+    float trans = 1.f;
+    double depth = 0.0;
+    const bool lit = P.light_kind != FV_LIGHT_NONE;
+    const float amb = lit ? (float)P.ambient : 1.f;
+    const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
+    const float early = (float)P.early;
+    if (hit) {
+      hitc = 1;
+      // iterations of the reference loop: t_{i+1} = t0 + (i+1)*step, stop once >= t_end - 1e-12
+      const double L = t_end - t0;
+      int n = (int)ceil((L - 1e-12) / P.step);
+      if (n < 1) n = 1;
+      const float last_dt = (float)(L - (double)(n - 1) * P.step);
+      const float ex = (float)(P.pos[0] + d[0] * t0), ey = (float)(P.pos[1] + d[1] * t0),
+                  ez = (float)(P.pos[2] + d[2] * t0);
+      const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
+      const float stepf = (float)P.step;
+#pragma unroll 1
+      for (int s = 0; s < n; ++s) {
+        const bool last = s == n - 1;
+        const float dt = last ? last_dt : stepf;
+        const float mid = (float)s * stepf + 0.5f * dt;
+        const float px = ex + dx * mid, py = ey + dy * mid, pz = ez + dz * mid;
+        float c[4];
+        tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
+        ++n_main;
+        const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+        const float a_step = 1.f - keep;
+        float shade = 1.f;
+        if (lit && a_step > 0.f) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
+        const float contrib = trans * a_step;
+        rgb[0] += contrib * (c[0] * (shade * I0));
+        rgb[1] += contrib * (c[1] * (shade * I1));
+        rgb[2] += contrib * (c[2] * (shade * I2));
+        trans = trans * (1.f - a_step);
+        const float acc = 1.f - trans;
+        if (depth == 0.0 && acc >= 0.5f) depth = t0 + (double)mid;
+        if (!(acc < early)) break;
+      }
+    }
+    const float bga = (float)P.bg[3];
+    float out[4];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) out[ch] = rgb[ch] + (trans * bga) * (float)P.bg[ch];
+    out[3] = (1.f - trans) + trans * bga;
+    if (P.rgba)
+      *reinterpret_cast<float4*>(P.rgba + (int64_t)pix * 4) = make_float4(out[0], out[1], out[2], out[3]);
+    if (P.depth) P.depth[pix] = (float)depth;
+    if (P.net_in) {
+      __half2* px = reinterpret_cast<__half2*>(P.net_in + ((int64_t)v * P.net_wp + u) * 8);
+      px[0] = __floats2half2_rn(out[0], out[1]);
+      px[1] = __floats2half2_rn(out[2], out[3]);
+    }
+  }
+  unsigned int r = (i < k) ? 1u : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r += __shfl_xor_sync(0xffffffffu, r, o);
+    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
+    n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
+    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  }
+  if ((threadIdx.x & 31) == 0 && r) {
+    atomicAdd(&P.counters->rays, (unsigned long long)r);
+    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
+    atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+  }
+}
+
+// linear (nz,ny,nx) -> 8^3 bricks
+__global__ void brick_kernel(const float* __restrict__ lin, float* __restrict__ bricks, int nx, int ny,
+                             int nz, int nbx, int nby, int nbz) {
+  const int64_t n = (int64_t)nbx * nby * nbz * 512;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(i & 511);
+    const int64_t b = i >> 9;
+    const int bx = (int)(b % nbx), by = (int)((b / nbx) % nby), bz = (int)(b / ((int64_t)nbx * nby));
+    const int x = bx * 8 + (e & 7), y = by * 8 + ((e >> 3) & 7), z = bz * 8 + (e >> 6);
+    bricks[i] = (x < nx && y < ny && z < nz) ? lin[((int64_t)z * ny + y) * nx + x] : 0.f;
+  }
+}
+
+int exp_class(double e) {
+  if (e == 0.5) return 0;
+  if (e == 1.0) return 1;
+  if (e == 2.0) return 2;
+  return 3;
+}
+
 void normalize3(double v[3]) {
   const double n = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
   v[0] /= n; v[1] /= n; v[2] /= n;
 }
 
 }  // namespace
+
+int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
+  if (vol->bricks && vol->bricks_version == vol->version) return 0;
+  const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8, nbz = (vol->nz + 7) / 8;
+  const int64_t n = (int64_t)nbx * nby * nbz * 512;
+  FV_REQUIRE(n < (1ll << 31), "volume too large for 32-bit brick addressing");
+  if (!vol->bricks) FV_CUDA(cudaMalloc(&vol->bricks, sizeof(float) * n));
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
+  brick_kernel<<<blocks, 256, 0, ctx->stream>>>(vol->data, vol->bricks, vol->nx, vol->ny, vol->nz, nbx, nby, nbz);
+  FV_CHECK_LAUNCH("brick_kernel");
+  ctx->launches += 1;
+  vol->bricks_version = vol->version;
+  return 0;
+}
 
 int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
                   const fv_settings* s, const int32_t* idx, const int32_t* k, int k_max,
@@ -324,10 +565,35 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
   if (k_max <= 0) return 0;
   const int threads = 128;
   const int blocks = (k_max + threads - 1) / threads;
-  if (s->precision == FV_PREC_FP64)
+  if (s->precision == FV_PREC_FP64) {
     march_kernel<double><<<blocks, threads, 0, ctx->stream>>>(P);
-  else
-    march_kernel<float><<<blocks, threads, 0, ctx->stream>>>(P);
+  } else {
+    fv_volume* mv = const_cast<fv_volume*>(vol);  // the brick copy is a cache of the grid
+    int rc = volume_bricks(ctx, mv);
+    if (rc) return rc;
+    FastParams F;
+    F.P = P;
+    F.V.bricks = mv->bricks;
+    F.V.nx = vol->nx; F.V.ny = vol->ny; F.V.nz = vol->nz;
+    const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8;
+    F.V.sby = nbx * 512;
+    F.V.sbz = nbx * nby * 512;
+    for (int a = 0; a < 3; ++a) {
+      F.V.ext[a] = (float)P.ext[a];
+      F.V.inv_sp[a] = (float)(1.0 / vol->spacing[a]);
+      F.ld[a] = (float)P.lvec[a];
+      F.lpos[a] = (float)P.lvec[a];
+      float sdir = F.ld[a];
+      if (fabsf(sdir) < 1e-30f) sdir = sdir < 0.f ? -1e-30f : 1e-30f;
+      F.ld_inv[a] = 1.f / sdir;
+    }
+    F.e_main = (float)(P.step / P.ref);
+    F.e_sh = (float)(P.step_sh / P.ref);
+    F.cls_main = exp_class(P.step / P.ref);
+    F.cls_sh = exp_class(P.step_sh / P.ref);
+    F.inv_ref = (float)(1.0 / P.ref);
+    march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F);
+  }
   FV_CHECK_LAUNCH("march_kernel");
   ctx->launches += 1;
   return 0;
