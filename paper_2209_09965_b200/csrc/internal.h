@@ -38,7 +38,8 @@ struct DevCounters {
   unsigned long long samples_main;
   unsigned long long samples_shadow;
   unsigned int scan_tile;  // dynamic tile counter of the mask scan
-  unsigned int pad[7];
+  unsigned int ray_next;   // work counter of the persistent marcher
+  unsigned int pad[6];
 };
 
 }  // namespace fv

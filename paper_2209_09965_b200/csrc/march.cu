@@ -17,6 +17,8 @@
 // default fast path, double for the exact tier. One thread marches one compacted ray; its
 // shadow rays are marched inline. The TF LUT lives in shared memory.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -264,19 +266,22 @@ __global__ void __launch_bounds__(128) march_kernel(MarchParams P) {
 //
 // Per ray the setup (direction, slab test, entry point, main-step count) is fp64; the samples are
 // then generated as p = entry + d * (i*step + dt/2) in fp32 (<=1e-4 voxel from the reference's
-// fp64 positions) and the trilinear weights, TF and compositing run in fp32. The volume is read
-// from 8x8x8 bricks (2 KB, z-y-x inside a brick): a sample's 8 corners and the next few samples
-// of a ray share cache lines along any direction, which is what shadow rays (marching toward the
-// light at 4x the main step) need. Corner addresses are separable: addr = X[x] + Y[y] + Z[z].
+// fp64 positions) and the trilinear weights, TF and compositing run in fp32.
+//
+// Volume layout for the fast tier ("quads"): every voxel (x,y,z) stores the float4
+//   (v[z][y][x], v[z][y][x1], v[z][y1][x], v[z][y1][x1]),  x1 = min(x+1,nx-1), y1 = min(y+1,ny-1)
+// -- the reference's clamped neighbours (volume.py:167-168) -- so the 8 trilinear corners are two
+// 16-byte loads (planes z0 and z1) instead of eight scalar gathers; that cuts the L1 wavefronts
+// per sample 4x, which is what bounds a gather-heavy marcher (ncu: L1/TEX 67% busy, DRAM idle).
+// Quads are stored in 8x8x8 bricks (8 KB, z-y-x inside a brick) so consecutive samples of a ray
+// in any direction -- shadow rays run diagonally toward the light -- stay in the same lines.
 struct FastVol {
-  const float* bricks;
+  const float4* quads;
   int nx, ny, nz;
-  int sby, sbz;        // brick strides (floats) in y and z
+  int sby, sbz;        // brick strides (quads) in y and z
   float ext[3];
   float inv_sp[3];
 };
-
-__device__ __forceinline__ int bx_off(int x) { return ((x >> 3) << 9) | (x & 7); }
 
 __device__ __forceinline__ float tri_fast(const FastVol& V, float px, float py, float pz) {
   if (!(px >= 0.f && px <= V.ext[0] && py >= 0.f && py <= V.ext[1] && pz >= 0.f && pz <= V.ext[2]))
@@ -286,19 +291,14 @@ __device__ __forceinline__ float tri_fast(const FastVol& V, float px, float py, 
   const float tx = qx - fx, ty = qy - fy, tz = qz - fz;
   const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
             z0 = min(max((int)fz, 0), V.nz - 1);
-  const int x1 = min(x0 + 1, V.nx - 1), y1 = min(y0 + 1, V.ny - 1), z1 = min(z0 + 1, V.nz - 1);
-  const int X0 = bx_off(x0), X1 = bx_off(x1);
-  const int Y0 = (y0 >> 3) * V.sby + ((y0 & 7) << 3), Y1 = (y1 >> 3) * V.sby + ((y1 & 7) << 3);
-  const int Z0 = (z0 >> 3) * V.sbz + ((z0 & 7) << 6), Z1 = (z1 >> 3) * V.sbz + ((z1 & 7) << 6);
-  const float* b = V.bricks;
-  const float d000 = __ldg(b + Z0 + Y0 + X0), d001 = __ldg(b + Z0 + Y0 + X1);
-  const float d010 = __ldg(b + Z0 + Y1 + X0), d011 = __ldg(b + Z0 + Y1 + X1);
-  const float d100 = __ldg(b + Z1 + Y0 + X0), d101 = __ldg(b + Z1 + Y0 + X1);
-  const float d110 = __ldg(b + Z1 + Y1 + X0), d111 = __ldg(b + Z1 + Y1 + X1);
-  const float c00 = d000 * (1.f - tx) + d001 * tx;
-  const float c10 = d010 * (1.f - tx) + d011 * tx;
-  const float c01 = d100 * (1.f - tx) + d101 * tx;
-  const float c11 = d110 * (1.f - tx) + d111 * tx;
+  const int z1 = min(z0 + 1, V.nz - 1);
+  const int xy = (y0 >> 3) * V.sby + ((x0 >> 3) << 9) + ((y0 & 7) << 3) + (x0 & 7);
+  const float4 A = __ldg(V.quads + xy + (z0 >> 3) * V.sbz + ((z0 & 7) << 6));
+  const float4 B = __ldg(V.quads + xy + (z1 >> 3) * V.sbz + ((z1 & 7) << 6));
+  const float c00 = A.x * (1.f - tx) + A.y * tx;
+  const float c10 = A.z * (1.f - tx) + A.w * tx;
+  const float c01 = B.x * (1.f - tx) + B.y * tx;
+  const float c11 = B.z * (1.f - tx) + B.w * tx;
   const float c0 = c00 * (1.f - ty) + c10 * ty;
   const float c1 = c01 * (1.f - ty) + c11 * ty;
   return c0 * (1.f - tz) + c1 * tz;
@@ -460,8 +460,212 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
   }
 }
 
-// linear (nz,ny,nx) -> 8^3 bricks
-__global__ void brick_kernel(const float* __restrict__ lin, float* __restrict__ bricks, int nx, int ny,
+// ---------------------------------------------------------------------------------------------
+// Persistent fast-tier marcher: one trilinear sample per lane per loop iteration.
+//
+// The inline-shadow kernel above nests a variable-length shadow march inside a variable-length
+// main march, so lanes of a warp idle while their neighbours finish (ncu: 14 of 32 threads
+// active, 15% achieved occupancy from the ray-length tail). Here every lane runs a small state
+// machine -- MAIN sample, SHADOW sample, or fetch a new ray -- and each iteration of the warp
+// loop takes exactly one volume sample per busy lane, whichever ray it belongs to. Lanes refill
+// from a global ray counter with one warp-aggregated atomic, so warps stay full until the list
+// runs dry. Each ray is still marched start to finish by one lane in the reference's order, so
+// the results are those of the per-ray kernel.
+__global__ void __launch_bounds__(128) march_persist_kernel(FastParams F, unsigned int* ray_counter) {
+  const MarchParams& P = F.P;
+  __shared__ float lut[4 * 256];
+  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __syncthreads();
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool lit = P.light_kind != FV_LIGHT_NONE;
+  const float amb = lit ? (float)P.ambient : 1.f;
+  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
+  const float early = (float)P.early, stepf = (float)P.step, step_sh = (float)P.step_sh;
+  const float mt = (float)P.min_trans;
+  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
+
+  // per-lane ray state
+  int pix = -1;            // -1: no ray
+  bool exhausted = false;
+  float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0;
+  int s = 0, n = 0;
+  float last_dt = 0.f;
+  double t0 = 0.0;
+  float rgb0 = 0, rgb1 = 0, rgb2 = 0, trans = 1.f, depth = 0.f;
+  bool in_shadow = false;
+  float pc0 = 0, pc1 = 0, pc2 = 0, pa = 0;          // pending main sample awaiting its shade
+  float spx = 0, spy = 0, spz = 0, sdx = 0, sdy = 0, sdz = 0, st = 0, stend = 0, strans = 1.f;
+
+  auto finish = [&](int p) {
+    const float bga = (float)P.bg[3];
+    const float o0 = rgb0 + (trans * bga) * (float)P.bg[0], o1 = rgb1 + (trans * bga) * (float)P.bg[1],
+                o2 = rgb2 + (trans * bga) * (float)P.bg[2], o3 = (1.f - trans) + trans * bga;
+    if (P.rgba) *reinterpret_cast<float4*>(P.rgba + (int64_t)p * 4) = make_float4(o0, o1, o2, o3);
+    if (P.depth) P.depth[p] = depth;
+    if (P.net_in) {
+      const int u = p % P.W, v = p / P.W;
+      __half2* px = reinterpret_cast<__half2*>(P.net_in + ((int64_t)v * P.net_wp + u) * 8);
+      px[0] = __floats2half2_rn(o0, o1);
+      px[1] = __floats2half2_rn(o2, o3);
+    }
+  };
+
+  while (true) {
+    // ---- refill lanes without a ray (rays that miss the box are finished right here) ----
+    while (true) {
+      const bool need = pix < 0 && !exhausted;
+      const unsigned m = __ballot_sync(0xffffffffu, need);
+      if (!m) break;
+      const int leader = __ffs(m) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(ray_counter, (unsigned)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int r = (int)(base + __popc(m & lt_mask));
+        if (r >= k) {
+          exhausted = true;
+        } else {
+          const int p = P.idx ? P.idx[r] : r;
+          ++nrays;
+          const int u = p % P.W, v = p / P.W;
+          const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
+          const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+          double d[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+          const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+          d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
+          double tend;
+          bool hit;
+          ray_box(P.pos, d, P.ext, t0, tend, hit);
+          rgb0 = rgb1 = rgb2 = 0.f;
+          trans = 1.f;
+          depth = 0.f;
+          if (!hit) {
+            finish(p);
+          } else {
+            ++hitc;
+            const double L = tend - t0;
+            n = (int)ceil((L - 1e-12) / P.step);
+            if (n < 1) n = 1;
+            last_dt = (float)(L - (double)(n - 1) * P.step);
+            ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
+            ez = (float)(P.pos[2] + d[2] * t0);
+            dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
+            s = 0;
+            in_shadow = false;
+            pix = p;
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, pix >= 0)) break;
+    if (pix < 0) continue;
+
+    // ---- one sample ----
+    float px, py, pz, dt, mid;
+    const bool last = s == n - 1;
+    if (in_shadow) {
+      dt = fminf(step_sh, stend - st);
+      mid = st + 0.5f * dt;
+      px = spx + sdx * mid; py = spy + sdy * mid; pz = spz + sdz * mid;
+    } else {
+      dt = last ? last_dt : stepf;
+      mid = (float)s * stepf + 0.5f * dt;
+      px = ex + dx * mid; py = ey + dy * mid; pz = ez + dz * mid;
+    }
+    float c[4];
+    tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
+    float shade = -1.f;  // >= 0: composite the pending main sample with this shade
+    if (in_shadow) {
+      ++n_shadow;
+      const float keep = dt == step_sh ? keep_cls(1.f - c[3], F.cls_sh, F.e_sh) : powf(1.f - c[3], dt * F.inv_ref);
+      strans = strans * (1.f - (1.f - keep));
+      st = st + dt;
+      if (!(st < stend) || !(strans > mt)) {
+        shade = amb + (1.f - amb) * strans;
+        in_shadow = false;
+      }
+    } else {
+      ++n_main;
+      const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+      pc0 = c[0]; pc1 = c[1]; pc2 = c[2];
+      pa = 1.f - keep;
+      shade = 1.f;
+      if (lit && pa > 0.f) {
+        // shadow ray from this sample toward the light (renderer.py:109-147)
+        float dir[3], inv[3], dist = INFINITY;
+        if (P.light_kind == FV_LIGHT_DIRECTIONAL) {
+          dir[0] = F.ld[0]; dir[1] = F.ld[1]; dir[2] = F.ld[2];
+          inv[0] = F.ld_inv[0]; inv[1] = F.ld_inv[1]; inv[2] = F.ld_inv[2];
+        } else {
+          const float lx = F.lpos[0] - px, ly = F.lpos[1] - py, lz = F.lpos[2] - pz;
+          dist = sqrtf(lx * lx + ly * ly + lz * lz);
+          const float mm = fmaxf(dist, 1e-30f);
+          dir[0] = lx / mm; dir[1] = ly / mm; dir[2] = lz / mm;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            float sd = dir[a];
+            if (fabsf(sd) < 1e-30f) sd = sd < 0.f ? -1e-30f : 1e-30f;
+            inv[a] = 1.f / sd;
+          }
+        }
+        const float pp[3] = {px, py, pz};
+        float tmin = -INFINITY, tmax = INFINITY;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float ta = (0.f - pp[a]) * inv[a], tb = (F.V.ext[a] - pp[a]) * inv[a];
+          tmin = fmaxf(tmin, fminf(ta, tb));
+          tmax = fminf(tmax, fmaxf(ta, tb));
+        }
+        const float ts0 = fmaxf(tmin, 0.f);
+        const float te = fminf(tmax, dist);
+        if (tmax > ts0 && te > ts0) {
+          in_shadow = true;
+          spx = px; spy = py; spz = pz;
+          sdx = dir[0]; sdy = dir[1]; sdz = dir[2];
+          st = ts0;
+          stend = te;
+          strans = 1.f;
+          shade = -1.f;
+        }
+      }
+    }
+    if (shade >= 0.f) {
+      const float contrib = trans * pa;
+      rgb0 += contrib * (pc0 * (shade * I0));
+      rgb1 += contrib * (pc1 * (shade * I1));
+      rgb2 += contrib * (pc2 * (shade * I2));
+      trans = trans * (1.f - pa);
+      const float acc = 1.f - trans;
+      const float mid_main = (float)s * stepf + 0.5f * (s == n - 1 ? last_dt : stepf);
+      if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid_main);
+      ++s;
+      if (s >= n || !(acc < early)) {
+        finish(pix);
+        pix = -1;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
+    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
+    n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
+    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  }
+  if (lane == 0 && nrays) {
+    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
+    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
+    atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+  }
+}
+
+// linear (nz,ny,nx) -> bricked quads (see FastVol)
+__global__ void brick_kernel(const float* __restrict__ lin, float4* __restrict__ quads, int nx, int ny,
                              int nz, int nbx, int nby, int nbz) {
   const int64_t n = (int64_t)nbx * nby * nbz * 512;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -470,7 +674,14 @@ __global__ void brick_kernel(const float* __restrict__ lin, float* __restrict__ 
     const int64_t b = i >> 9;
     const int bx = (int)(b % nbx), by = (int)((b / nbx) % nby), bz = (int)(b / ((int64_t)nbx * nby));
     const int x = bx * 8 + (e & 7), y = by * 8 + ((e >> 3) & 7), z = bz * 8 + (e >> 6);
-    bricks[i] = (x < nx && y < ny && z < nz) ? lin[((int64_t)z * ny + y) * nx + x] : 0.f;
+    float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (x < nx && y < ny && z < nz) {
+      const int x1 = min(x + 1, nx - 1), y1 = min(y + 1, ny - 1);
+      const float* pl = lin + (int64_t)z * ny * nx;
+      q = make_float4(pl[(int64_t)y * nx + x], pl[(int64_t)y * nx + x1], pl[(int64_t)y1 * nx + x],
+                      pl[(int64_t)y1 * nx + x1]);
+    }
+    quads[i] = q;
   }
 }
 
@@ -493,9 +704,10 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
   const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8, nbz = (vol->nz + 7) / 8;
   const int64_t n = (int64_t)nbx * nby * nbz * 512;
   FV_REQUIRE(n < (1ll << 31), "volume too large for 32-bit brick addressing");
-  if (!vol->bricks) FV_CUDA(cudaMalloc(&vol->bricks, sizeof(float) * n));
+  if (!vol->bricks) FV_CUDA(cudaMalloc(&vol->bricks, sizeof(float4) * n));
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
-  brick_kernel<<<blocks, 256, 0, ctx->stream>>>(vol->data, vol->bricks, vol->nx, vol->ny, vol->nz, nbx, nby, nbz);
+  brick_kernel<<<blocks, 256, 0, ctx->stream>>>(vol->data, reinterpret_cast<float4*>(vol->bricks), vol->nx,
+                                                vol->ny, vol->nz, nbx, nby, nbz);
   FV_CHECK_LAUNCH("brick_kernel");
   ctx->launches += 1;
   vol->bricks_version = vol->version;
@@ -573,7 +785,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     if (rc) return rc;
     FastParams F;
     F.P = P;
-    F.V.bricks = mv->bricks;
+    F.V.quads = reinterpret_cast<const float4*>(mv->bricks);
     F.V.nx = vol->nx; F.V.ny = vol->ny; F.V.nz = vol->nz;
     const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8;
     F.V.sby = nbx * 512;
@@ -592,7 +804,23 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     F.cls_main = exp_class(P.step / P.ref);
     F.cls_sh = exp_class(P.step_sh / P.ref);
     F.inv_ref = (float)(1.0 / P.ref);
-    march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F);
+    static int variant = -1;  // FV_MARCH_KERNEL=ray|persist (experiments); default per-ray
+    if (variant < 0) {
+      const char* e = getenv("FV_MARCH_KERNEL");
+      variant = (e && strcmp(e, "persist") == 0) ? 1 : 0;
+    }
+    if (variant == 1) {
+      static int per_sm = 0;
+      if (!per_sm) {
+        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_persist_kernel, threads, 0));
+        if (per_sm < 1) per_sm = 1;
+      }
+      const int pgrid = std::min(blocks, ctx->num_sms * per_sm);
+      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, sizeof(unsigned int), ctx->stream));
+      march_persist_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next);
+    } else {
+      march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F);
+    }
   }
   FV_CHECK_LAUNCH("march_kernel");
   ctx->launches += 1;
