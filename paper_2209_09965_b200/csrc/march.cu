@@ -283,6 +283,46 @@ struct FastVol {
   float inv_sp[3];
 };
 
+// Morton order inside a brick: a 128-byte line holds a 2x2x2 block of quads, so a step in any
+// direction (and the z0/z1 pair of one sample) usually stays in the same line.
+__host__ __device__ __forceinline__ int spread3(int v) { return (v & 1) | ((v & 2) << 2) | ((v & 4) << 4); }
+__host__ __device__ __forceinline__ int morton_xy(int x, int y) { return spread3(x) | (spread3(y) << 1); }
+__host__ __device__ __forceinline__ int morton_z(int z) { return spread3(z) << 2; }
+
+// Two-phase trilinear: tri_issue computes the weights and issues both loads, tri_finish blends.
+struct TriFetch {
+  float4 A, B;
+  float tx, ty, tz;
+  bool inside;
+};
+
+__device__ __forceinline__ TriFetch tri_issue(const FastVol& V, float px, float py, float pz) {
+  TriFetch f;
+  f.inside = px >= 0.f && px <= V.ext[0] && py >= 0.f && py <= V.ext[1] && pz >= 0.f && pz <= V.ext[2];
+  const float qx = px * V.inv_sp[0] - 0.5f, qy = py * V.inv_sp[1] - 0.5f, qz = pz * V.inv_sp[2] - 0.5f;
+  const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+  f.tx = qx - fx; f.ty = qy - fy; f.tz = qz - fz;
+  const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
+            z0 = min(max((int)fz, 0), V.nz - 1);
+  const int z1 = min(z0 + 1, V.nz - 1);
+  const int xy = (y0 >> 3) * V.sby + ((x0 >> 3) << 9) + morton_xy(x0 & 7, y0 & 7);
+  f.A = __ldg(V.quads + xy + (z0 >> 3) * V.sbz + morton_z(z0 & 7));
+  f.B = __ldg(V.quads + xy + (z1 >> 3) * V.sbz + morton_z(z1 & 7));
+  return f;
+}
+
+__device__ __forceinline__ float tri_finish(const TriFetch& f) {
+  if (!f.inside) return 0.f;
+  const float tx = f.tx, ty = f.ty, tz = f.tz;
+  const float c00 = f.A.x * (1.f - tx) + f.A.y * tx;
+  const float c10 = f.A.z * (1.f - tx) + f.A.w * tx;
+  const float c01 = f.B.x * (1.f - tx) + f.B.y * tx;
+  const float c11 = f.B.z * (1.f - tx) + f.B.w * tx;
+  const float c0 = c00 * (1.f - ty) + c10 * ty;
+  const float c1 = c01 * (1.f - ty) + c11 * ty;
+  return c0 * (1.f - tz) + c1 * tz;
+}
+
 __device__ __forceinline__ float tri_fast(const FastVol& V, float px, float py, float pz) {
   if (!(px >= 0.f && px <= V.ext[0] && py >= 0.f && py <= V.ext[1] && pz >= 0.f && pz <= V.ext[2]))
     return 0.f;
@@ -292,9 +332,9 @@ __device__ __forceinline__ float tri_fast(const FastVol& V, float px, float py, 
   const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
             z0 = min(max((int)fz, 0), V.nz - 1);
   const int z1 = min(z0 + 1, V.nz - 1);
-  const int xy = (y0 >> 3) * V.sby + ((x0 >> 3) << 9) + ((y0 & 7) << 3) + (x0 & 7);
-  const float4 A = __ldg(V.quads + xy + (z0 >> 3) * V.sbz + ((z0 & 7) << 6));
-  const float4 B = __ldg(V.quads + xy + (z1 >> 3) * V.sbz + ((z1 & 7) << 6));
+  const int xy = (y0 >> 3) * V.sby + ((x0 >> 3) << 9) + morton_xy(x0 & 7, y0 & 7);
+  const float4 A = __ldg(V.quads + xy + (z0 >> 3) * V.sbz + morton_z(z0 & 7));
+  const float4 B = __ldg(V.quads + xy + (z1 >> 3) * V.sbz + morton_z(z1 & 7));
   const float c00 = A.x * (1.f - tx) + A.y * tx;
   const float c10 = A.z * (1.f - tx) + A.w * tx;
   const float c01 = B.x * (1.f - tx) + B.y * tx;
@@ -353,17 +393,37 @@ __device__ float shadow_fast(const FastParams& F, const float* lut, float px, fl
   float trans = 1.f;
   if (!(tmax > t0 && tend > t0)) return trans;
   const float step = (float)P.step_sh, mt = (float)P.min_trans;
+  // The sample positions do not depend on the data, so kShadowU samples are addressed and their
+  // loads issued before any of them is consumed: one lane keeps 2*kShadowU 16-byte loads in
+  // flight. That shortens the longest rays, whose serial chains of L2 round trips otherwise set
+  // the kernel's tail. Samples past the exit are discarded, so results are unchanged.
+  constexpr int kShadowU = 4;
   float t = t0;
 #pragma unroll 1
   while (true) {
-    const float dt = fminf(step, tend - t);
-    const float mid = t + 0.5f * dt;
-    const float a = tf_alpha<float>(lut, P.K, tri_fast(F.V, px + dir[0] * mid, py + dir[1] * mid, pz + dir[2] * mid));
-    const float keep = dt == step ? keep_cls(1.f - a, F.cls_sh, F.e_sh) : powf(1.f - a, dt * F.inv_ref);
-    trans = trans * (1.f - (1.f - keep));
-    ++nsamp;
-    t = t + dt;
-    if (!(t < tend) || !(trans > mt)) break;
+    TriFetch f[kShadowU];
+    float dts[kShadowU];
+    float tj = t;
+#pragma unroll
+    for (int j = 0; j < kShadowU; ++j) {
+      const float dt = fminf(step, tend - tj);
+      const float mid = tj + 0.5f * dt;
+      dts[j] = dt;
+      f[j] = tri_issue(F.V, px + dir[0] * mid, py + dir[1] * mid, pz + dir[2] * mid);
+      tj = tj + dt;
+    }
+    bool stop = false;
+#pragma unroll
+    for (int j = 0; j < kShadowU; ++j) {
+      const float dt = dts[j];
+      const float a = tf_alpha<float>(lut, P.K, tri_finish(f[j]));
+      const float keep = dt == step ? keep_cls(1.f - a, F.cls_sh, F.e_sh) : powf(1.f - a, dt * F.inv_ref);
+      trans = trans * (1.f - (1.f - keep));
+      ++nsamp;
+      t = t + dt;
+      if (!(t < tend) || !(trans > mt)) { stop = true; break; }
+    }
+    if (stop) break;
   }
   return trans;
 }
@@ -664,6 +724,141 @@ __global__ void __launch_bounds__(128) march_persist_kernel(FastParams F, unsign
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Persistent per-lane-refill marcher (default fast tier).
+//
+// ncu on the one-ray-per-thread kernel: 12.7% achieved occupancy against 44% theoretical -- a
+// 128-thread block holds its slot until its slowest ray (thousands of shadow samples) is done,
+// and most of the 373k compacted rays miss the volume or stop early. Here a grid of
+// (SMs x resident blocks) warps loops over the compacted list: whenever a lane's ray finishes,
+// the lane takes the next ray index from a global counter (one warp-aggregated atomic per
+// refill), so warps stay full until the list drains. A loop iteration is one main sample plus
+// its inline shadow ray. Each ray is still marched start to finish by one lane in the
+// reference's order, so results equal the per-ray kernel's bit for bit.
+__global__ void __launch_bounds__(128) march_refill_kernel(FastParams F, unsigned int* ray_counter) {
+  const MarchParams& P = F.P;
+  __shared__ float lut[4 * 256];
+  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __syncthreads();
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool lit = P.light_kind != FV_LIGHT_NONE;
+  const float amb = lit ? (float)P.ambient : 1.f;
+  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
+  const float early = (float)P.early, stepf = (float)P.step;
+  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
+  int pix = -1;
+  bool exhausted = false;
+  float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0.f;
+  int s = 0, n = 0;
+  double t0 = 0.0;
+  float rgb0 = 0, rgb1 = 0, rgb2 = 0, trans = 1.f, depth = 0.f;
+  const float bga = (float)P.bg[3];
+
+  while (true) {
+    while (true) {
+      const bool need = pix < 0 && !exhausted;
+      const unsigned m = __ballot_sync(0xffffffffu, need);
+      if (!m) break;
+      const int leader = __ffs(m) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(ray_counter, (unsigned)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int r = (int)(base + __popc(m & lt_mask));
+        if (r >= k) {
+          exhausted = true;
+        } else {
+          const int p = P.idx ? P.idx[r] : r;
+          ++nrays;
+          const int u = p % P.W, v = p / P.W;
+          const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
+          const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+          double d[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+          const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+          d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
+          double tend;
+          bool hit;
+          ray_box(P.pos, d, P.ext, t0, tend, hit);
+          rgb0 = rgb1 = rgb2 = 0.f;
+          trans = 1.f;
+          depth = 0.f;
+          if (hit) {
+            ++hitc;
+            const double L = tend - t0;
+            n = (int)ceil((L - 1e-12) / P.step);
+            if (n < 1) n = 1;
+            last_dt = (float)(L - (double)(n - 1) * P.step);
+            ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
+            ez = (float)(P.pos[2] + d[2] * t0);
+            dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
+            s = 0;
+            pix = p;
+          } else {
+            pix = p;
+            n = 0;  // finished below without samples
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, pix >= 0)) break;
+    if (pix >= 0) {
+      bool done = s >= n;
+      if (!done) {
+        const bool last = s == n - 1;
+        const float dt = last ? last_dt : stepf;
+        const float mid = (float)s * stepf + 0.5f * dt;
+        const float px = ex + dx * mid, py = ey + dy * mid, pz = ez + dz * mid;
+        float c[4];
+        tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
+        ++n_main;
+        const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+        const float a_step = 1.f - keep;
+        float shade = 1.f;
+        if (lit && a_step > 0.f) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
+        const float contrib = trans * a_step;
+        rgb0 += contrib * (c[0] * (shade * I0));
+        rgb1 += contrib * (c[1] * (shade * I1));
+        rgb2 += contrib * (c[2] * (shade * I2));
+        trans = trans * (1.f - a_step);
+        const float acc = 1.f - trans;
+        if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid);
+        ++s;
+        done = s >= n || !(acc < early);
+      }
+      if (done) {
+        const float o0 = rgb0 + (trans * bga) * (float)P.bg[0], o1 = rgb1 + (trans * bga) * (float)P.bg[1],
+                    o2 = rgb2 + (trans * bga) * (float)P.bg[2], o3 = (1.f - trans) + trans * bga;
+        if (P.rgba) *reinterpret_cast<float4*>(P.rgba + (int64_t)pix * 4) = make_float4(o0, o1, o2, o3);
+        if (P.depth) P.depth[pix] = depth;
+        if (P.net_in) {
+          const int u = pix % P.W, v = pix / P.W;
+          __half2* hp = reinterpret_cast<__half2*>(P.net_in + ((int64_t)v * P.net_wp + u) * 8);
+          hp[0] = __floats2half2_rn(o0, o1);
+          hp[1] = __floats2half2_rn(o2, o3);
+        }
+        pix = -1;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
+    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
+    n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
+    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  }
+  if (lane == 0 && nrays) {
+    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
+    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
+    atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+  }
+}
+
 // linear (nz,ny,nx) -> bricked quads (see FastVol)
 __global__ void brick_kernel(const float* __restrict__ lin, float4* __restrict__ quads, int nx, int ny,
                              int nz, int nbx, int nby, int nbz) {
@@ -673,7 +868,11 @@ __global__ void brick_kernel(const float* __restrict__ lin, float4* __restrict__
     const int e = (int)(i & 511);
     const int64_t b = i >> 9;
     const int bx = (int)(b % nbx), by = (int)((b / nbx) % nby), bz = (int)(b / ((int64_t)nbx * nby));
-    const int x = bx * 8 + (e & 7), y = by * 8 + ((e >> 3) & 7), z = bz * 8 + (e >> 6);
+    // inverse of the in-brick Morton order (bits x: 0,3,6  y: 1,4,7  z: 2,5,8)
+    const int lx = (e & 1) | ((e >> 2) & 2) | ((e >> 4) & 4);
+    const int ly = ((e >> 1) & 1) | ((e >> 3) & 2) | ((e >> 5) & 4);
+    const int lz = ((e >> 2) & 1) | ((e >> 4) & 2) | ((e >> 6) & 4);
+    const int x = bx * 8 + lx, y = by * 8 + ly, z = bz * 8 + lz;
     float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
     if (x < nx && y < ny && z < nz) {
       const int x1 = min(x + 1, nx - 1), y1 = min(y + 1, ny - 1);
@@ -804,22 +1003,29 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     F.cls_main = exp_class(P.step / P.ref);
     F.cls_sh = exp_class(P.step_sh / P.ref);
     F.inv_ref = (float)(1.0 / P.ref);
-    static int variant = -1;  // FV_MARCH_KERNEL=ray|persist (experiments); default per-ray
+    // FV_MARCH_KERNEL=refill (default) | ray | persist -- the variants are kept for A/B runs
+    static int variant = -1;
     if (variant < 0) {
       const char* e = getenv("FV_MARCH_KERNEL");
-      variant = (e && strcmp(e, "persist") == 0) ? 1 : 0;
+      variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2 : 0;
     }
-    if (variant == 1) {
-      static int per_sm = 0;
-      if (!per_sm) {
-        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_persist_kernel, threads, 0));
-        if (per_sm < 1) per_sm = 1;
-      }
-      const int pgrid = std::min(blocks, ctx->num_sms * per_sm);
-      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, sizeof(unsigned int), ctx->stream));
-      march_persist_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next);
-    } else {
+    if (variant == 2) {
       march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F);
+    } else {
+      static int per_sm[2] = {0, 0};
+      if (!per_sm[variant]) {
+        if (variant == 1)
+          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], march_persist_kernel, threads, 0));
+        else
+          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], march_refill_kernel, threads, 0));
+        if (per_sm[variant] < 1) per_sm[variant] = 1;
+      }
+      const int pgrid = std::min(blocks, ctx->num_sms * per_sm[variant]);
+      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, sizeof(unsigned int), ctx->stream));
+      if (variant == 1)
+        march_persist_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next);
+      else
+        march_refill_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next);
     }
   }
   FV_CHECK_LAUNCH("march_kernel");
