@@ -63,6 +63,27 @@ struct Cfg {
   static constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 + 256;
 };
 
+// All MMAs of one K-stage: R output rows x 9 taps x NK k-steps, offsets folded at compile time.
+template <int R, int N, int NK>
+__device__ __forceinline__ void issue_stage(uint64_t a0, uint64_t b0, uint32_t d_base, uint32_t idesc,
+                                            bool first_stage) {
+  using C = Cfg<R, N>;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const uint64_t ad = a0 + (uint64_t)((2 * k * C::kPlaneBytes + ((r + t / 3) * kHaloW + t % 3) * 16) >> 4);
+        const uint64_t bd = b0 + (uint64_t)(((t * NK + k) * N * 32) >> 4);
+        sm100::mma_f16(d_base + r * N, ad, bd, idesc, (!first_stage || t || k) ? 1u : 0u);
+      }
+    }
+  }
+}
+
 template <int R, int N>
 __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   using C = Cfg<R, N>;
@@ -180,27 +201,22 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         int gs = a.groups - ks * kStageGroups;
         if (gs > kStageGroups) gs = kStageGroups;
         const int nk = (gs + 1) >> 1;
-        if (lane == 0) {
-          const uint32_t a_st = sm100::smem_u32(sA + st * C::kABytes);
-          const uint32_t b_st = sm100::smem_u32(sB + st * C::kBBytes);
-          for (int r = 0; r < R; ++r) {
-#pragma unroll 1
-            for (int t = 0; t < 9; ++t) {
-              const int dy = t / 3, dx = t % 3;
-              for (int k = 0; k < nk; ++k) {
-                const uint32_t a_addr = a_st + 2 * k * C::kPlaneBytes + ((r + dy) * kHaloW + dx) * 16;
-                const uint32_t b_addr = b_st + (t * nk + k) * N * 32;
-                const uint64_t ad = sm100::smem_desc(a_addr, C::kPlaneBytes, 128);
-                const uint64_t bd = sm100::smem_desc(b_addr, N * 16, 128);
-                sm100::mma_f16(d_base + r * N, ad, bd, idesc, (ks | t | k) ? 1u : 0u);
-              }
-            }
-          }
-          sm100::mma_commit(bar_empty + 8 * st);
+        // The whole warp walks the (warp-uniform) tap loop so descriptors stay in uniform
+        // registers; elect.sync picks the one thread that issues each tcgen05.mma. Descriptors are
+        // a base plus a 16-byte-unit offset in the start-address field.
+        const uint64_t a0 = sm100::smem_desc(sm100::smem_u32(sA + st * C::kABytes), C::kPlaneBytes, 128);
+        const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + st * C::kBBytes), N * 16, 128);
+        if (sm100::elect_one()) {
+          if (nk == 2)
+            issue_stage<R, N, 2>(a0, b0, d_base, idesc, ks == 0);
+          else
+            issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
         }
         __syncwarp();
+        sm100::mma_commit_elect(bar_empty + 8 * st);
+        __syncwarp();
       }
-      if (lane == 0) sm100::mma_commit(bar_tfull + 8 * acc);
+      sm100::mma_commit_elect(bar_tfull + 8 * acc);
       __syncwarp();
     }
   } else {
