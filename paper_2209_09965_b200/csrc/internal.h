@@ -39,7 +39,9 @@ struct DevCounters {
   unsigned long long samples_shadow;
   unsigned int scan_tile;  // dynamic tile counter of the mask scan
   unsigned int ray_next;   // work counter of the persistent marcher
-  unsigned int pad[6];
+  unsigned int wave_rec;   // wavefront marcher: records allocated
+  unsigned int wave_next;  // wavefront marcher: shadow-pass work counter
+  unsigned int pad[4];
 };
 
 }  // namespace fv
@@ -63,6 +65,11 @@ struct fv_ctx {
   float* rgb_scratch = nullptr;          // device (H,W,3) for fv_frame
   int64_t rgb_cap = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // wavefront marcher workspace
+  void* wave_rec = nullptr;   // 2 x cap float4 records
+  int64_t wave_cap = 0;
+  void* wave_ray = nullptr;   // int4 per compacted ray
+  int64_t wave_ray_cap = 0;
   unsigned long long launches = 0;
 };
 

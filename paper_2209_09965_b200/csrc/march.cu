@@ -859,6 +859,245 @@ __global__ void __launch_bounds__(128) march_refill_kernel(FastParams F, unsigne
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Wavefront marcher (default fast tier): main rays, shadow rays and compositing as three passes.
+//
+// In _march the shade of a sample enters only the colour sum (renderer.py:181-182); opacity,
+// depth and early termination never depend on it. So the main pass marches every compacted ray
+// without shadows and records, for each sample with a_step > 0, its position, its weight
+// T*a_step and its TF colour; the shadow pass then marches all those shadow rays as independent
+// work items (4.6M per C3 frame instead of 117k hit rays, so no ray's serial chain sets the
+// tail); the composite pass sums contrib*(c*(shade*I)) per ray in sample order -- the
+// reference's order, so the result equals the fused kernel's. A ray's records are allocated
+// after a counting march, so they are contiguous and in order. A ray whose records would not fit
+// the buffer is marched fused (inline shadows) instead.
+struct WaveBufs {
+  float4* rec0;            // (px, py, pz, contrib = T * a_step)
+  float4* rec1;            // (c0, c1, c2, shade)
+  int cap;
+  unsigned int* rec_count;
+  unsigned int* next;      // work counter of the shadow pass
+  int4* ray;               // per compacted ray: (record offset, record count, trans, depth) bits
+};
+
+__device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float r0, float r1, float r2,
+                                            float trans, float depth) {
+  const float bga = (float)P.bg[3];
+  const float o0 = r0 + (trans * bga) * (float)P.bg[0], o1 = r1 + (trans * bga) * (float)P.bg[1],
+              o2 = r2 + (trans * bga) * (float)P.bg[2], o3 = (1.f - trans) + trans * bga;
+  if (P.rgba) *reinterpret_cast<float4*>(P.rgba + (int64_t)pix * 4) = make_float4(o0, o1, o2, o3);
+  if (P.depth) P.depth[pix] = depth;
+  if (P.net_in) {
+    const int u = pix % P.W, v = pix / P.W;
+    __half2* hp = reinterpret_cast<__half2*>(P.net_in + ((int64_t)v * P.net_wp + u) * 8);
+    hp[0] = __floats2half2_rn(o0, o1);
+    hp[1] = __floats2half2_rn(o2, o3);
+  }
+}
+
+__global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, WaveBufs B, unsigned int* ray_counter) {
+  const MarchParams& P = F.P;
+  __shared__ float lut[4 * 256];
+  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __syncthreads();
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool lit = P.light_kind != FV_LIGHT_NONE;
+  const float amb = lit ? (float)P.ambient : 1.f;
+  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
+  const float early = (float)P.early, stepf = (float)P.step;
+  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
+  int pix = -1, ray = -1;
+  bool exhausted = false;
+  float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0.f;
+  int s = 0, n = 0, phase = 0, m = 0, off = 0, j = 0;  // phase 0 count, 1 emit, 2 fused
+  double t0 = 0.0;
+  float rgb0 = 0, rgb1 = 0, rgb2 = 0, trans = 1.f, depth = 0.f;
+
+  while (true) {
+    while (true) {
+      const bool need = pix < 0 && !exhausted;
+      const unsigned msk = __ballot_sync(0xffffffffu, need);
+      if (!msk) break;
+      const int leader = __ffs(msk) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(ray_counter, (unsigned)__popc(msk));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int r = (int)(base + __popc(msk & lt_mask));
+        if (r >= k) {
+          exhausted = true;
+        } else {
+          const int p = P.idx ? P.idx[r] : r;
+          ++nrays;
+          const int u = p % P.W, v = p / P.W;
+          const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
+          const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+          double d[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+          const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+          d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
+          double tend;
+          bool hit;
+          ray_box(P.pos, d, P.ext, t0, tend, hit);
+          rgb0 = rgb1 = rgb2 = 0.f;
+          trans = 1.f;
+          depth = 0.f;
+          if (!hit) {
+            write_pixel(P, p, 0.f, 0.f, 0.f, 1.f, 0.f);
+            B.ray[r] = make_int4(0, 0, 0, 0);
+          } else {
+            ++hitc;
+            const double L = tend - t0;
+            n = (int)ceil((L - 1e-12) / P.step);
+            if (n < 1) n = 1;
+            last_dt = (float)(L - (double)(n - 1) * P.step);
+            ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
+            ez = (float)(P.pos[2] + d[2] * t0);
+            dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
+            s = 0; m = 0; j = 0;
+            phase = 0;
+            pix = p;
+            ray = r;
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, pix >= 0)) break;
+    if (pix < 0) continue;
+
+    const bool last = s == n - 1;
+    const float dt = last ? last_dt : stepf;
+    const float mid = (float)s * stepf + 0.5f * dt;
+    const float px = ex + dx * mid, py = ey + dy * mid, pz = ez + dz * mid;
+    float c[4];
+    tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
+    const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+    const float a_step = 1.f - keep;
+    const bool needs_shadow = lit && a_step > 0.f;
+    if (phase == 0) {
+      ++n_main;
+      if (needs_shadow) ++m;
+      if (!lit) {
+        const float contrib = trans * a_step;
+        rgb0 += contrib * (c[0] * I0);
+        rgb1 += contrib * (c[1] * I1);
+        rgb2 += contrib * (c[2] * I2);
+      }
+    } else if (phase == 1) {
+      if (needs_shadow) {
+        B.rec0[off + j] = make_float4(px, py, pz, trans * a_step);
+        B.rec1[off + j] = make_float4(c[0], c[1], c[2], 0.f);
+        ++j;
+      }
+    } else {
+      float shade = 1.f;
+      if (needs_shadow) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
+      const float contrib = trans * a_step;
+      rgb0 += contrib * (c[0] * (shade * I0));
+      rgb1 += contrib * (c[1] * (shade * I1));
+      rgb2 += contrib * (c[2] * (shade * I2));
+    }
+    trans = trans * (1.f - a_step);
+    const float acc = 1.f - trans;
+    if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid);
+    ++s;
+    if (s >= n || !(acc < early)) {
+      if (phase == 0 && m > 0) {
+        const unsigned a0 = atomicAdd(B.rec_count, (unsigned)m);
+        if ((int64_t)a0 + m <= (int64_t)B.cap) {
+          off = (int)a0;
+          phase = 1;
+        } else {
+          phase = 2;
+        }
+        s = 0; j = 0;
+        trans = 1.f; depth = 0.f;
+        rgb0 = rgb1 = rgb2 = 0.f;
+      } else if (phase == 1) {
+        B.ray[ray] = make_int4(off, m, __float_as_int(trans), __float_as_int(depth));
+        pix = -1;
+      } else {
+        write_pixel(P, pix, rgb0, rgb1, rgb2, trans, depth);
+        B.ray[ray] = make_int4(0, 0, 0, 0);
+        pix = -1;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
+    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
+    n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
+    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  }
+  if (lane == 0 && nrays) {
+    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
+    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
+    atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+  }
+}
+
+// One shadow ray per record; lanes refill from a work counter so long shadow rays do not idle
+// their warp's neighbours.
+__global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
+  const MarchParams& P = F.P;
+  __shared__ float lut[4 * 256];
+  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __syncthreads();
+  const int nrec = (int)min(*B.rec_count, (unsigned)B.cap);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const float amb = (float)P.ambient;
+  unsigned int n_shadow = 0;
+  bool exhausted = false;
+  while (true) {
+    const bool need = !exhausted;
+    const unsigned msk = __ballot_sync(0xffffffffu, need);
+    if (!msk) break;
+    const int leader = __ffs(msk) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(B.next, (unsigned)__popc(msk));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (need) {
+      const int i = (int)(base + __popc(msk & lt_mask));
+      if (i >= nrec) {
+        exhausted = true;
+      } else {
+        const float4 r0 = B.rec0[i];
+        const float ts = shadow_fast(F, lut, r0.x, r0.y, r0.z, n_shadow);
+        B.rec1[i].w = amb + (1.f - amb) * ts;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  if (lane == 0 && n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+}
+
+// rgb = sum_j contrib_j * (c_j * (shade_j * I)) in sample order, then the background blend.
+__global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F, WaveBufs B) {
+  const MarchParams& P = F.P;
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k; r += gridDim.x * blockDim.x) {
+    const int4 v = B.ray[r];
+    if (v.y == 0) continue;
+    float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;
+    for (int j = 0; j < v.y; ++j) {
+      const float contrib = B.rec0[v.x + j].w;
+      const float4 c = B.rec1[v.x + j];
+      rgb0 += contrib * (c.x * (c.w * I0));
+      rgb1 += contrib * (c.y * (c.w * I1));
+      rgb2 += contrib * (c.z * (c.w * I2));
+    }
+    write_pixel(P, P.idx ? P.idx[r] : r, rgb0, rgb1, rgb2, __int_as_float(v.z), __int_as_float(v.w));
+  }
+}
+
 // linear (nz,ny,nx) -> bricked quads (see FastVol)
 __global__ void brick_kernel(const float* __restrict__ lin, float4* __restrict__ quads, int nx, int ny,
                              int nz, int nbx, int nby, int nbz) {
@@ -1003,13 +1242,52 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     F.cls_main = exp_class(P.step / P.ref);
     F.cls_sh = exp_class(P.step_sh / P.ref);
     F.inv_ref = (float)(1.0 / P.ref);
-    // FV_MARCH_KERNEL=refill (default) | ray | persist -- the variants are kept for A/B runs
+    // FV_MARCH_KERNEL=wave (default) | refill | ray | persist -- variants kept for A/B runs
     static int variant = -1;
     if (variant < 0) {
       const char* e = getenv("FV_MARCH_KERNEL");
-      variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2 : 0;
+      variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2
+              : (e && strcmp(e, "refill") == 0) ? 0 : 3;
     }
-    if (variant == 2) {
+    if (variant == 3) {
+      // wavefront: main -> shadow -> composite
+      const int64_t rec_cap = std::max<int64_t>(4 << 20, 8ll * k_max);
+      if (rec_cap > ctx->wave_cap) {
+        if (ctx->wave_rec) cudaFree(ctx->wave_rec);
+        ctx->wave_rec = nullptr;
+        FV_CUDA(cudaMalloc(&ctx->wave_rec, sizeof(float4) * 2 * rec_cap));
+        ctx->wave_cap = rec_cap;
+      }
+      if (k_max > ctx->wave_ray_cap) {
+        if (ctx->wave_ray) cudaFree(ctx->wave_ray);
+        ctx->wave_ray = nullptr;
+        FV_CUDA(cudaMalloc(&ctx->wave_ray, sizeof(int4) * k_max));
+        ctx->wave_ray_cap = k_max;
+      }
+      WaveBufs B;
+      B.rec0 = reinterpret_cast<float4*>(ctx->wave_rec);
+      B.rec1 = B.rec0 + ctx->wave_cap;
+      B.cap = (int)std::min<int64_t>(ctx->wave_cap, INT32_MAX);
+      B.rec_count = &ctx->counters->wave_rec;
+      B.next = &ctx->counters->wave_next;
+      B.ray = reinterpret_cast<int4*>(ctx->wave_ray);
+      static int per_sm_main = 0, per_sm_sh = 0;
+      if (!per_sm_main) {
+        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel, threads, 0));
+        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sh, march_wave_shadow_kernel, threads, 0));
+        per_sm_main = std::max(per_sm_main, 1);
+        per_sm_sh = std::max(per_sm_sh, 1);
+      }
+      // ray_next, wave_rec, wave_next are consecutive counters
+      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 3 * sizeof(unsigned int), ctx->stream));
+      march_wave_main_kernel<<<std::min(blocks, ctx->num_sms * per_sm_main), threads, 0, ctx->stream>>>(
+          F, B, &ctx->counters->ray_next);
+      if (P.light_kind != FV_LIGHT_NONE) {
+        march_wave_shadow_kernel<<<ctx->num_sms * per_sm_sh, threads, 0, ctx->stream>>>(F, B);
+        march_wave_composite_kernel<<<std::min(blocks, ctx->num_sms * 8), threads, 0, ctx->stream>>>(F, B);
+        ctx->launches += 2;
+      }
+    } else if (variant == 2) {
       march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F);
     } else {
       static int per_sm[2] = {0, 0};
