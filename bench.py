@@ -52,8 +52,32 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+RANK_STRIDE = 977  # each rank's session starts at its own point of the camera path / noise loop
+
+
+def rank_frames(rank: int, start: int, count: int) -> list[int]:
+    """Frame indices rank `rank` renders: its own stream (path frame = index % PATH_FRAMES)."""
+    return [rank * RANK_STRIDE + start + i for i in range(count)]
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """All-reduce MAX of a per-rank time (device tensor under NCCL, CPU tensor under gloo)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(units_per_rank: int, world: int, max_seconds: float) -> float:
+    return world * units_per_rank / max_seconds
+
+
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled every 20 ms around the timed region."""
 
     def __init__(self, device: int, out: Path):
         self.out = out
@@ -63,7 +87,7 @@ class ClockSampler:
         try:
             self.f = open(out, "w")
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(device), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
@@ -210,19 +234,14 @@ def run_ours(args, cfg):
     pipe = FramePipeline(scene, net, (h, w), default_stack(), RenderSettings())
     ctx = pipe.ctx
     stream = ctx.stream
-    base = rank * 977  # each rank = its own session, at its own point on the path
     k, wu = args.steps, args.warmup
-
-    def frame(i):
-        j = base + i
+    # clocks are sampled (every 20 ms) from the start of warm-up to the end of the timed region
+    clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_r{rank}.csv") if rank == 0 else None
+    for j in rank_frames(rank, 0, wu):
         pipe.step(cams[j % PATH_FRAMES], fovea, j)
-
-    for i in range(wu):
-        frame(i)
     torch.cuda.synchronize()
     # --- device-resident timed region -------------------------------------------------
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
-    clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_r{rank}.csv") if rank == 0 else None
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -231,8 +250,7 @@ def run_ours(args, cfg):
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for i in range(k):
-        j = base + wu + i
+    for i, j in enumerate(rank_frames(rank, wu, k)):
         e = ev[i]
         e[0].record(stream)
         pipe.mask(fovea, j)
@@ -244,13 +262,7 @@ def run_ours(args, cfg):
     t_end.record(stream)
     torch.cuda.synchronize()
     launches = ctx.launches() - l0
-    elapsed_ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([elapsed_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end), world, device="cuda")
     clk = clocks.stop() if clocks else None
     st = ctx.stats()
     mask_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
@@ -258,26 +270,19 @@ def run_ours(args, cfg):
     net_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
     samples_per_frame = (st.samples_main + st.samples_shadow) / k
     rays_per_frame = st.rays / k
-    fps = world * k / (elapsed_ms / 1e3)
+    fps = whole_job_rate(k, world, elapsed_ms / 1e3)
     # --- end to end through the C ABI with host buffers (fv_frame) --------------------
     host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
     ke = max(3, k // 2)
-    for i in range(2):
-        pipe.frame_to_host(cams[(base + i) % PATH_FRAMES], fovea, base + i, host)
+    for j in rank_frames(rank, wu + k, 2):
+        pipe.frame_to_host(cams[j % PATH_FRAMES], fovea, j, host)
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    for i in range(ke):
-        j = base + wu + k + i
+    for j in rank_frames(rank, wu + k + 2, ke):
         pipe.frame_to_host(cams[j % PATH_FRAMES], fovea, j, host)
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([e2e_s], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_fps = world * ke / e2e_s
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world, device="cuda")
+    e2e_fps = whole_job_rate(ke, world, e2e_s)
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()

@@ -1,0 +1,60 @@
+"""Multi-rank host logic of bench.py on CPU (gloo, world size 2, 127.0.0.1)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+
+    # each rank times a different amount; the job time is the slowest rank's
+    local = 10.0 + 5.0 * rank
+    tmax = bench.max_over_ranks(local, world)
+    frames = bench.rank_frames(rank, 5, 30)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, frames)
+    rate = bench.whole_job_rate(30, world, tmax / 1e3)
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, tmax, gathered, rate))
+
+
+@pytest.mark.timeout(120)
+def test_two_rank_timing_and_frame_streams():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=100) for _ in procs]
+    for p in procs:
+        p.join(timeout=30)
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, tmax, gathered, rate in res:
+        assert tmax == 15.0  # max over ranks, not the local time
+        a, b = set(gathered[0]), set(gathered[1])
+        assert len(a) == len(b) == 30 and not (a & b)  # independent frame streams
+        assert rate == pytest.approx(2 * 30 / 0.015)
+
+
+def test_single_rank_helpers():
+    import bench
+
+    assert bench.max_over_ranks(3.5, 1) == 3.5
+    assert bench.rank_frames(0, 2, 3) == [2, 3, 4]
+    assert bench.whole_job_rate(10, 1, 0.5) == 20.0
