@@ -872,8 +872,9 @@ __global__ void __launch_bounds__(128) march_refill_kernel(FastParams F, unsigne
 // after a counting march, so they are contiguous and in order. A ray whose records would not fit
 // the buffer is marched fused (inline shadows) instead.
 struct WaveBufs {
-  float4* rec0;            // (px, py, pz, contrib = T * a_step)
-  float4* rec1;            // (c0, c1, c2, shade)
+  float4* rec0;            // (px, py, pz, -): shadow-ray origin
+  float4* rec1;            // (c0, c1, c2, contrib = T * a_step)
+  float* shade;            // written by the shadow pass
   int cap;
   unsigned int* rec_count;
   unsigned int* next;      // work counter of the shadow pass
@@ -968,61 +969,77 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
     if (!__any_sync(0xffffffffu, pix >= 0)) break;
     if (pix < 0) continue;
 
-    const bool last = s == n - 1;
-    const float dt = last ? last_dt : stepf;
-    const float mid = (float)s * stepf + 0.5f * dt;
-    const float px = ex + dx * mid, py = ey + dy * mid, pz = ez + dz * mid;
-    float c[4];
-    tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
-    const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
-    const float a_step = 1.f - keep;
-    const bool needs_shadow = lit && a_step > 0.f;
-    if (phase == 0) {
-      ++n_main;
-      if (needs_shadow) ++m;
-      if (!lit) {
-        const float contrib = trans * a_step;
-        rgb0 += contrib * (c[0] * I0);
-        rgb1 += contrib * (c[1] * I1);
-        rgb2 += contrib * (c[2] * I2);
-      }
-    } else if (phase == 1) {
-      if (needs_shadow) {
-        B.rec0[off + j] = make_float4(px, py, pz, trans * a_step);
-        B.rec1[off + j] = make_float4(c[0], c[1], c[2], 0.f);
-        ++j;
-      }
-    } else {
-      float shade = 1.f;
-      if (needs_shadow) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
-      const float contrib = trans * a_step;
-      rgb0 += contrib * (c[0] * (shade * I0));
-      rgb1 += contrib * (c[1] * (shade * I1));
-      rgb2 += contrib * (c[2] * (shade * I2));
+    // Up to kMainU samples per iteration: their positions do not depend on the data, so all
+    // loads are issued before the first sample is consumed (the longest main rays are ~1000
+    // samples; a serial chain of L2 round trips would set the kernel's tail).
+    constexpr int kMainU = 4;
+    TriFetch f[kMainU];
+#pragma unroll
+    for (int u = 0; u < kMainU; ++u) {
+      const int si = s + u;
+      const float dt = si == n - 1 ? last_dt : stepf;
+      const float mid = (float)si * stepf + 0.5f * dt;
+      f[u] = tri_issue(F.V, ex + dx * mid, ey + dy * mid, ez + dz * mid);
     }
-    trans = trans * (1.f - a_step);
-    const float acc = 1.f - trans;
-    if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid);
-    ++s;
-    if (s >= n || !(acc < early)) {
-      if (phase == 0 && m > 0) {
-        const unsigned a0 = atomicAdd(B.rec_count, (unsigned)m);
-        if ((int64_t)a0 + m <= (int64_t)B.cap) {
-          off = (int)a0;
-          phase = 1;
-        } else {
-          phase = 2;
+#pragma unroll
+    for (int u = 0; u < kMainU; ++u) {
+      const bool last = s == n - 1;
+      const float dt = last ? last_dt : stepf;
+      const float mid = (float)s * stepf + 0.5f * dt;
+      float c[4];
+      tf_apply<float>(lut, P.K, tri_finish(f[u]), c);
+      const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+      const float a_step = 1.f - keep;
+      const bool needs_shadow = lit && a_step > 0.f;
+      if (phase == 0) {
+        ++n_main;
+        if (needs_shadow) ++m;
+        if (!lit) {
+          const float contrib = trans * a_step;
+          rgb0 += contrib * (c[0] * I0);
+          rgb1 += contrib * (c[1] * I1);
+          rgb2 += contrib * (c[2] * I2);
         }
-        s = 0; j = 0;
-        trans = 1.f; depth = 0.f;
-        rgb0 = rgb1 = rgb2 = 0.f;
       } else if (phase == 1) {
-        B.ray[ray] = make_int4(off, m, __float_as_int(trans), __float_as_int(depth));
-        pix = -1;
+        if (needs_shadow) {
+          B.rec0[off + j] = make_float4(ex + dx * mid, ey + dy * mid, ez + dz * mid, 0.f);
+          B.rec1[off + j] = make_float4(c[0], c[1], c[2], trans * a_step);
+          ++j;
+        }
       } else {
-        write_pixel(P, pix, rgb0, rgb1, rgb2, trans, depth);
-        B.ray[ray] = make_int4(0, 0, 0, 0);
-        pix = -1;
+        float shade = 1.f;
+        if (needs_shadow)
+          shade = amb + (1.f - amb) * shadow_fast(F, lut, ex + dx * mid, ey + dy * mid, ez + dz * mid, n_shadow);
+        const float contrib = trans * a_step;
+        rgb0 += contrib * (c[0] * (shade * I0));
+        rgb1 += contrib * (c[1] * (shade * I1));
+        rgb2 += contrib * (c[2] * (shade * I2));
+      }
+      trans = trans * (1.f - a_step);
+      const float acc = 1.f - trans;
+      if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid);
+      ++s;
+      if (s >= n || !(acc < early)) {
+        if (phase == 0 && m > 0) {
+          const unsigned a0 = atomicAdd(B.rec_count, (unsigned)m);
+          if ((int64_t)a0 + m <= (int64_t)B.cap) {
+            off = (int)a0;
+            phase = 1;
+          } else {
+            phase = 2;
+          }
+          s = 0; j = 0;
+          trans = 1.f; depth = 0.f;
+          rgb0 = rgb1 = rgb2 = 0.f;
+        } else if (phase == 1) {
+          B.ray[ray] = make_int4(off, m, __float_as_int(trans), __float_as_int(depth));
+          pix = -1;
+        } else {
+          write_pixel(P, pix, rgb0, rgb1, rgb2, trans, depth);
+          B.ray[ray] = make_int4(0, 0, 0, 0);
+          pix = -1;
+        }
+        break;
       }
     }
   }
@@ -1069,7 +1086,7 @@ __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, Wa
       } else {
         const float4 r0 = B.rec0[i];
         const float ts = shadow_fast(F, lut, r0.x, r0.y, r0.z, n_shadow);
-        B.rec1[i].w = amb + (1.f - amb) * ts;
+        B.shade[i] = amb + (1.f - amb) * ts;
       }
     }
   }
@@ -1078,23 +1095,34 @@ __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, Wa
   if (lane == 0 && n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
 }
 
-// rgb = sum_j contrib_j * (c_j * (shade_j * I)) in sample order, then the background blend.
+// rgb = sum_j contrib_j * (c_j * (shade_j * I)), then the background blend. One warp per ray:
+// lane l sums records l, l+32, ... (coalesced), then a fixed xor tree -- deterministic, and the
+// reordering versus the reference's sequential sum is an fp32 rounding effect (~1e-7).
 __global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
   const int k = P.k_dev ? *P.k_dev : P.k_max;
   const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k; r += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < k; r += warps) {
     const int4 v = B.ray[r];
     if (v.y == 0) continue;
     float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;
-    for (int j = 0; j < v.y; ++j) {
-      const float contrib = B.rec0[v.x + j].w;
+    for (int j = lane; j < v.y; j += 32) {
       const float4 c = B.rec1[v.x + j];
-      rgb0 += contrib * (c.x * (c.w * I0));
-      rgb1 += contrib * (c.y * (c.w * I1));
-      rgb2 += contrib * (c.z * (c.w * I2));
+      const float sh = B.shade[v.x + j];
+      rgb0 += c.w * (c.x * (sh * I0));
+      rgb1 += c.w * (c.y * (sh * I1));
+      rgb2 += c.w * (c.z * (sh * I2));
     }
-    write_pixel(P, P.idx ? P.idx[r] : r, rgb0, rgb1, rgb2, __int_as_float(v.z), __int_as_float(v.w));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rgb0 += __shfl_xor_sync(0xffffffffu, rgb0, o);
+      rgb1 += __shfl_xor_sync(0xffffffffu, rgb1, o);
+      rgb2 += __shfl_xor_sync(0xffffffffu, rgb2, o);
+    }
+    if (lane == 0)
+      write_pixel(P, P.idx ? P.idx[r] : r, rgb0, rgb1, rgb2, __int_as_float(v.z), __int_as_float(v.w));
   }
 }
 
@@ -1255,7 +1283,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       if (rec_cap > ctx->wave_cap) {
         if (ctx->wave_rec) cudaFree(ctx->wave_rec);
         ctx->wave_rec = nullptr;
-        FV_CUDA(cudaMalloc(&ctx->wave_rec, sizeof(float4) * 2 * rec_cap));
+        FV_CUDA(cudaMalloc(&ctx->wave_rec, (sizeof(float4) * 2 + sizeof(float)) * rec_cap));
         ctx->wave_cap = rec_cap;
       }
       if (k_max > ctx->wave_ray_cap) {
@@ -1267,6 +1295,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       WaveBufs B;
       B.rec0 = reinterpret_cast<float4*>(ctx->wave_rec);
       B.rec1 = B.rec0 + ctx->wave_cap;
+      B.shade = reinterpret_cast<float*>(B.rec1 + ctx->wave_cap);
       B.cap = (int)std::min<int64_t>(ctx->wave_cap, INT32_MAX);
       B.rec_count = &ctx->counters->wave_rec;
       B.next = &ctx->counters->wave_next;
@@ -1284,7 +1313,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           F, B, &ctx->counters->ray_next);
       if (P.light_kind != FV_LIGHT_NONE) {
         march_wave_shadow_kernel<<<ctx->num_sms * per_sm_sh, threads, 0, ctx->stream>>>(F, B);
-        march_wave_composite_kernel<<<std::min(blocks, ctx->num_sms * 8), threads, 0, ctx->stream>>>(F, B);
+        march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B);
         ctx->launches += 2;
       }
     } else if (variant == 2) {

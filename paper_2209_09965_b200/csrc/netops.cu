@@ -16,15 +16,13 @@ namespace fv {
 namespace {
 
 // ---- D-path 2x bilinear upsample, fp16 NC8HW8 -> fp16 NC8HW8 -------------------------------
-__global__ void upsample2_nc8_kernel(const __half* __restrict__ in, __half* __restrict__ out,
-                                     int groups, int h, int w) {
+// grid: (ceil(2w / 128), 2h, groups); one thread per output pixel (8 channels, 16 B)
+__global__ void __launch_bounds__(128) upsample2_nc8_kernel(const __half* __restrict__ in,
+                                                            __half* __restrict__ out, int h, int w) {
   const int W2 = 2 * w, H2 = 2 * h;
-  const int64_t n = (int64_t)groups * H2 * W2;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int X = (int)(i % W2);
-    const int Y = (int)((i / W2) % H2);
-    const int g = (int)(i / ((int64_t)W2 * H2));
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  const int Y = blockIdx.y, g = blockIdx.z;
+  if (X < W2) {
     const __half* pl = in + (int64_t)g * h * w * 8;
     const int iy = Y >> 1, ix = X >> 1;
     int ya, yb;
@@ -59,6 +57,91 @@ __global__ void upsample2_nc8_kernel(const __half* __restrict__ in, __half* __re
 }
 
 // ---- K stage: logits (1x1 conv) -> softmax -> per-pixel 3x3 filter -------------------------
+// Four horizontally adjacent pixels per thread: each 16-byte weight read from shared memory
+// feeds 16 FMAs (the one-pixel version was bound by its 9*C broadcast LDS per pixel).
+template <int C>
+__global__ void __launch_bounds__(128) kfilter4_kernel(const __half* __restrict__ hd,
+                                                       const float* __restrict__ kw,
+                                                       const float* __restrict__ img,
+                                                       float* __restrict__ out, int h, int w) {
+  __shared__ __align__(16) float sw[9 * C + 12];
+  for (int i = threadIdx.x; i < 9 * C + 9; i += blockDim.x) sw[i] = kw[i];
+  __syncthreads();
+  const int wq = (w + 3) >> 2;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y;
+  if (q >= wq) return;
+  const int x0 = 4 * q;
+  const int64_t n = (int64_t)h * w;
+  const int64_t plane = n * 8;
+  float lg[4][9];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int j = 0; j < 9; ++j) lg[p][j] = 0.f;
+#pragma unroll 1
+  for (int g = 0; g < C / 8; ++g) {
+    float f[4][8];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (x0 + p < w) v = *reinterpret_cast<const uint4*>(hd + g * plane + ((int64_t)y * w + x0 + p) * 8);
+      const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 t = __half22float2(h2[e]);
+        f[p][2 * e] = t.x;
+        f[p][2 * e + 1] = t.y;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+#pragma unroll
+      for (int e4 = 0; e4 < 2; ++e4) {
+        const float4 wv = *reinterpret_cast<const float4*>(sw + j * C + g * 8 + e4 * 4);
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          lg[p][j] = fmaf(wv.x, f[p][e4 * 4 + 0], lg[p][j]);
+          lg[p][j] = fmaf(wv.y, f[p][e4 * 4 + 1], lg[p][j]);
+          lg[p][j] = fmaf(wv.z, f[p][e4 * 4 + 2], lg[p][j]);
+          lg[p][j] = fmaf(wv.w, f[p][e4 * 4 + 3], lg[p][j]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int x = x0 + p;
+    if (x >= w) break;
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      lg[p][j] += sw[9 * C + j];
+      m = fmaxf(m, lg[p][j]);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      lg[p][j] = expf(lg[p][j] - m);
+      s += lg[p][j];
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) lg[p][j] = lg[p][j] / s;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float* pl = img + (int64_t)c * n;
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const int yy = y + j / 3 - 1, xx = x + j % 3 - 1;
+        const float v = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
+        acc = acc + lg[p][j] * v;
+      }
+      out[(int64_t)c * n + (int64_t)y * w + x] = acc;
+    }
+  }
+}
+
 template <int C>
 __global__ void kfilter_kernel(const __half* __restrict__ hd, const float* __restrict__ kw,
                                const float* __restrict__ img, float* __restrict__ out, int h, int w) {
@@ -246,18 +329,17 @@ inline int grid_for(fv_ctx* ctx, int64_t n, int threads = 256) {
 }  // namespace
 
 int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
-  const int64_t n = (int64_t)(in.C / 8) * 4 * in.H * in.W;
-  upsample2_nc8_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(in.p, out.p, in.C / 8, in.H, in.W);
+  const dim3 grid((2 * in.W + 127) / 128, 2 * in.H, in.C / 8);
+  upsample2_nc8_kernel<<<grid, 128, 0, ctx->stream>>>(in.p, out.p, in.H, in.W);
   FV_CHECK_LAUNCH("upsample2_nc8_kernel");
   ctx->launches += 1;
   return 0;
 }
 
 int kfilter(fv_ctx* ctx, const fv_act& hd, const float* kw, const float* img, float* out) {
-  const int64_t n = (int64_t)hd.H * hd.W;
-  const int g = grid_for(ctx, n);
+  const dim3 g(((hd.W + 3) / 4 + 127) / 128, hd.H);
   switch (hd.C) {
-#define KF(CC) case CC: kfilter_kernel<CC><<<g, 256, 0, ctx->stream>>>(hd.p, kw, img, out, hd.H, hd.W); break;
+#define KF(CC) case CC: kfilter4_kernel<CC><<<g, 128, 0, ctx->stream>>>(hd.p, kw, img, out, hd.H, hd.W); break;
     KF(8) KF(16) KF(24) KF(32) KF(40) KF(48) KF(56) KF(64) KF(72) KF(80) KF(88) KF(96) KF(112) KF(128)
 #undef KF
     default:
