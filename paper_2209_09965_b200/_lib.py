@@ -148,7 +148,7 @@ def ptr(t) -> C.c_void_p | None:
 class Context:
     """One fv_ctx bound to a device and to torch's current stream on that device."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, stream=None):
         import torch
 
         if not torch.cuda.is_available():
@@ -159,7 +159,7 @@ class Context:
         check(self.lib.fv_ctx_create(device, C.byref(h)))
         self.h = h
         torch.cuda.set_device(device)
-        self.stream = torch.cuda.current_stream(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
         check(self.lib.fv_ctx_set_stream(self.h, C.c_void_p(self.stream.cuda_stream)))
         self.noise_key = None
 

@@ -131,7 +131,8 @@ struct fv_state {
   int H = 0, W = 0, Hp = 0, Wp = 0;
   int parity = 0;  // which hidden buffer holds the carried state
   bool fresh = true;
-  fv_act x;                         // 8-ch input, L0
+  fv_act x;                         // 8-ch input the next reconstruct reads (render writes it)
+  fv_act xalt;                      // the other input buffer: receives O_d feedback, then swaps
   std::vector<fv_act> enc_a;        // conv1 outputs per encoder block
   std::vector<fv_act> skips;        // conv2 outputs (skip) per encoder block
   std::vector<fv_act> pooled;       // pooled skip per encoder block

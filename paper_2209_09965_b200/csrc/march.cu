@@ -896,6 +896,7 @@ __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float
   }
 }
 
+template <int kMainU>
 __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, WaveBufs B, unsigned int* ray_counter) {
   const MarchParams& P = F.P;
   __shared__ float lut[4 * 256];
@@ -972,7 +973,6 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
     // Up to kMainU samples per iteration: their positions do not depend on the data, so all
     // loads are issued before the first sample is consumed (the longest main rays are ~1000
     // samples; a serial chain of L2 round trips would set the kernel's tail).
-    constexpr int kMainU = 4;
     TriFetch f[kMainU];
 #pragma unroll
     for (int u = 0; u < kMainU; ++u) {
@@ -1300,17 +1300,25 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.rec_count = &ctx->counters->wave_rec;
       B.next = &ctx->counters->wave_next;
       B.ray = reinterpret_cast<int4*>(ctx->wave_ray);
-      static int per_sm_main = 0, per_sm_sh = 0;
+      static int main_u = 0, per_sm_main = 0, per_sm_sh = 0;
       if (!per_sm_main) {
-        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel, threads, 0));
+        const char* e = getenv("FV_MAIN_U");  // main-sample prefetch depth (A/B runs): 4 or 8
+        main_u = (e && atoi(e) == 8) ? 8 : 4;
+        if (main_u == 8)
+          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<8>, threads, 0));
+        else
+          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<4>, threads, 0));
         FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sh, march_wave_shadow_kernel, threads, 0));
         per_sm_main = std::max(per_sm_main, 1);
         per_sm_sh = std::max(per_sm_sh, 1);
       }
       // ray_next, wave_rec, wave_next are consecutive counters
       FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 3 * sizeof(unsigned int), ctx->stream));
-      march_wave_main_kernel<<<std::min(blocks, ctx->num_sms * per_sm_main), threads, 0, ctx->stream>>>(
-          F, B, &ctx->counters->ray_next);
+      const int mgrid = std::min(blocks, ctx->num_sms * per_sm_main);
+      if (main_u == 8)
+        march_wave_main_kernel<8><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next);
+      else
+        march_wave_main_kernel<4><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next);
       if (P.light_kind != FV_LIGHT_NONE) {
         march_wave_shadow_kernel<<<ctx->num_sms * per_sm_sh, threads, 0, ctx->stream>>>(F, B);
         march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B);

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <utility>
 
 #include "internal.h"
 
@@ -111,9 +112,11 @@ int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* 
                  nullptr, nullptr);
     if (rc) return rc;
   }
-  // D.head -> O_d (fp32 planes) + feedback channels 5..7 of the input for the next frame
+  // D.head -> O_d (fp32 planes) + feedback channels 5..7 of the NEXT frame's input buffer. The
+  // two input buffers alternate, so the next frame's mask + march (which write channels 0..4)
+  // may run on another stream while this frame's network still reads its own input.
   rc = conv3x3(ctx, net->convs[net->head_index], &st->hidden[newp][nd - 1], 1, nullptr, nullptr,
-               false, st->od, net->recurrent ? st->x.p : nullptr);
+               false, st->od, net->recurrent ? st->xalt.p : nullptr);
   if (rc) return rc;
   const float* final_img = st->od;
   if (use_k) {
@@ -142,6 +145,7 @@ int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* 
   }
   rc = finalize(ctx, st, final_img, out_rgb, out_o, out_od);
   if (rc) return rc;
+  std::swap(st->x, st->xalt);
   st->parity = newp;
   st->fresh = false;
   return 0;
@@ -321,6 +325,7 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
   st->enc_a.resize(ne); st->skips.resize(ne); st->pooled.resize(ne);
   st->dec_a.resize(nd); st->ups.resize(nd); st->hidden[0].resize(nd); st->hidden[1].resize(nd);
   reqs.push_back({&st->x, 8, 0});
+  reqs.push_back({&st->xalt, 8, 0});
   for (int i = 0; i < ne; ++i) {
     reqs.push_back({&st->enc_a[i], ch[i], i});
     reqs.push_back({&st->skips[i], ch[i], i});

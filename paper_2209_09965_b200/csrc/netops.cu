@@ -16,43 +16,60 @@ namespace fv {
 namespace {
 
 // ---- D-path 2x bilinear upsample, fp16 NC8HW8 -> fp16 NC8HW8 -------------------------------
-// grid: (ceil(2w / 128), 2h, groups); one thread per output pixel (8 channels, 16 B)
+// grid: (ceil(w / 128), h, groups); one thread per INPUT pixel (i, j) writes the 2x2 output
+// block (2i..2i+1, 2j..2j+1) of its 8 channels from the clamped 3x3 input neighbourhood.
+__device__ __forceinline__ void load8(const __half* p, float (&v)[8]) {
+  const uint4 q = *reinterpret_cast<const uint4*>(p);
+  const __half2* h2 = reinterpret_cast<const __half2*>(&q);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __half22float2(h2[e]);
+    v[2 * e] = t.x;
+    v[2 * e + 1] = t.y;
+  }
+}
+
 __global__ void __launch_bounds__(128) upsample2_nc8_kernel(const __half* __restrict__ in,
                                                             __half* __restrict__ out, int h, int w) {
-  const int W2 = 2 * w, H2 = 2 * h;
-  const int X = blockIdx.x * blockDim.x + threadIdx.x;
-  const int Y = blockIdx.y, g = blockIdx.z;
-  if (X < W2) {
-    const __half* pl = in + (int64_t)g * h * w * 8;
-    const int iy = Y >> 1, ix = X >> 1;
-    int ya, yb;
-    float wya, wyb;
-    if (Y & 1) { ya = iy; yb = min(iy + 1, h - 1); wya = 0.75f; wyb = 0.25f; }
-    else { ya = max(iy - 1, 0); yb = iy; wya = 0.25f; wyb = 0.75f; }
-    int xa, xb;
-    float wxa, wxb;
-    if (X & 1) { xa = ix; xb = min(ix + 1, w - 1); wxa = 0.75f; wxb = 0.25f; }
-    else { xa = max(ix - 1, 0); xb = ix; wxa = 0.25f; wxb = 0.75f; }
-    const uint4 qaa = *reinterpret_cast<const uint4*>(pl + ((int64_t)ya * w + xa) * 8);
-    const uint4 qba = *reinterpret_cast<const uint4*>(pl + ((int64_t)yb * w + xa) * 8);
-    const uint4 qab = *reinterpret_cast<const uint4*>(pl + ((int64_t)ya * w + xb) * 8);
-    const uint4 qbb = *reinterpret_cast<const uint4*>(pl + ((int64_t)yb * w + xb) * 8);
-    const __half2* aa = reinterpret_cast<const __half2*>(&qaa);
-    const __half2* ba = reinterpret_cast<const __half2*>(&qba);
-    const __half2* ab = reinterpret_cast<const __half2*>(&qab);
-    const __half2* bb = reinterpret_cast<const __half2*>(&qbb);
-    uint4 o;
-    __half2* o2 = reinterpret_cast<__half2*>(&o);
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y, g = blockIdx.z;
+  if (j >= w) return;
+  const __half* pl = in + (int64_t)g * h * w * 8;
+  const int rows[3] = {max(i - 1, 0), i, min(i + 1, h - 1)};
+  const int cols[3] = {max(j - 1, 0), j, min(j + 1, w - 1)};
+  // rows first (axis 2): even output row = 0.25*prev + 0.75*self, odd = 0.75*self + 0.25*next
+  float re[3][8], ro[3][8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float2 faa = __half22float2(aa[j]), fba = __half22float2(ba[j]);
-      const float2 fab = __half22float2(ab[j]), fbb = __half22float2(bb[j]);
-      // rows first (axis 2), then columns (axis 3), as in upsample_bilinear2
-      const float ra0 = wya * faa.x + wyb * fba.x, ra1 = wya * faa.y + wyb * fba.y;
-      const float rb0 = wya * fab.x + wyb * fbb.x, rb1 = wya * fab.y + wyb * fbb.y;
-      o2[j] = __floats2half2_rn(wxa * ra0 + wxb * rb0, wxa * ra1 + wxb * rb1);
+  for (int c = 0; c < 3; ++c) {
+    float a[8], b[8], d[8];
+    load8(pl + ((int64_t)rows[0] * w + cols[c]) * 8, a);
+    load8(pl + ((int64_t)rows[1] * w + cols[c]) * 8, b);
+    load8(pl + ((int64_t)rows[2] * w + cols[c]) * 8, d);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      re[c][e] = 0.25f * a[e] + 0.75f * b[e];
+      ro[c][e] = 0.75f * b[e] + 0.25f * d[e];
     }
-    *reinterpret_cast<uint4*>(out + ((int64_t)g * H2 * W2 + (int64_t)Y * W2 + X) * 8) = o;
+  }
+  const int W2 = 2 * w;
+  __half* ob = out + (int64_t)g * (2 * h) * W2 * 8;
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const float (&r)[3][8] = rr ? ro : re;
+    uint4 q0, q1;
+    __half2* o0 = reinterpret_cast<__half2*>(&q0);
+    __half2* o1 = reinterpret_cast<__half2*>(&q1);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      // then columns (axis 3)
+      o0[e] = __floats2half2_rn(0.25f * r[0][2 * e] + 0.75f * r[1][2 * e],
+                                0.25f * r[0][2 * e + 1] + 0.75f * r[1][2 * e + 1]);
+      o1[e] = __floats2half2_rn(0.75f * r[1][2 * e] + 0.25f * r[2][2 * e],
+                                0.75f * r[1][2 * e + 1] + 0.25f * r[2][2 * e + 1]);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(ob + ((int64_t)(2 * i + rr) * W2 + 2 * j) * 8);
+    dst[0] = q0;
+    dst[1] = q1;
   }
 }
 
@@ -111,8 +128,6 @@ __global__ void __launch_bounds__(128) kfilter4_kernel(const __half* __restrict_
   }
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    const int x = x0 + p;
-    if (x >= w) break;
     float m = -INFINITY;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
@@ -127,17 +142,28 @@ __global__ void __launch_bounds__(128) kfilter4_kernel(const __half* __restrict_
     }
 #pragma unroll
     for (int j = 0; j < 9; ++j) lg[p][j] = lg[p][j] / s;
+  }
+  // the 3 x 6 neighbourhood of the 4 pixels, loaded once per channel (zero padding)
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float* pl = img + (int64_t)c * n;
+  for (int c = 0; c < 3; ++c) {
+    const float* pl = img + (int64_t)c * n;
+    float nb[3][6];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy) {
+      const int yy = y + dy - 1;
+#pragma unroll
+      for (int dx = 0; dx < 6; ++dx) {
+        const int xx = x0 + dx - 1;
+        nb[dy][dx] = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      if (x0 + p >= w) break;
       float acc = 0.f;
 #pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        const int yy = y + j / 3 - 1, xx = x + j % 3 - 1;
-        const float v = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
-        acc = acc + lg[p][j] * v;
-      }
-      out[(int64_t)c * n + (int64_t)y * w + x] = acc;
+      for (int j = 0; j < 9; ++j) acc = acc + lg[p][j] * nb[j / 3][p + j % 3];
+      out[(int64_t)c * n + (int64_t)y * w + x0 + p] = acc;
     }
   }
 }
@@ -329,7 +355,7 @@ inline int grid_for(fv_ctx* ctx, int64_t n, int threads = 256) {
 }  // namespace
 
 int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
-  const dim3 grid((2 * in.W + 127) / 128, 2 * in.H, in.C / 8);
+  const dim3 grid((in.W + 127) / 128, in.H, in.C / 8);
   upsample2_nc8_kernel<<<grid, 128, 0, ctx->stream>>>(in.p, out.p, in.H, in.W);
   FV_CHECK_LAUNCH("upsample2_nc8_kernel");
   ctx->launches += 1;

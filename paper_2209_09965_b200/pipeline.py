@@ -87,6 +87,57 @@ class FramePipeline:
                     self.ev[2].elapsed_time(self.ev[3]))
         return None
 
+    def run_pipelined(self, frames) -> None:
+        """Render frame t+1 (mask + march) on one stream while frame t reconstructs on another.
+
+        `frames` is a sequence of (camera, fovea, frame index). The state's two input buffers
+        alternate per frame (net.cu), so the only cross-stream dependencies are: frame t's
+        network waits for frame t's render, and frame t's render waits for frame t-2's network
+        (the last reader of the buffer it overwrites). Launches only; call sync_pipelined().
+        """
+        import torch
+
+        if getattr(self, "_rctx", None) is None:
+            self._s_render = torch.cuda.Stream(device=self.ctx.device)
+            self._s_net = torch.cuda.Stream(device=self.ctx.device)
+            self._rctx = _lib.Context(self.ctx.device, stream=self._s_render)
+            self._nctx = _lib.Context(self.ctx.device, stream=self._s_net)
+            self._rctx.ensure_noise(self.ctx._noise_ref)
+            self._vol_r = self.scene.volume.handle(self._rctx, self.scene.tf)
+        s_r, s_n = self._s_render, self._s_net
+        # both streams start after everything already queued on the pipeline's own stream
+        start = torch.cuda.Event()
+        start.record(self.ctx.stream)
+        s_r.wait_event(start)
+        s_n.wait_event(start)
+        net_done = []
+        for t, (cam, fovea, j) in enumerate(frames):
+            if t >= 2:
+                s_r.wait_event(net_done[t - 2])
+            f = fovea.c_struct()
+            _lib.check(self._rctx.lib.fv_mask_compact(self._rctx.h, int(j), self.h, self.w, C.byref(f), None, None,
+                                                      _lib.ptr(self.idx), _lib.ptr(self.k), self.state.h))
+            camc = cam.c_struct()
+            _lib.check(self._rctx.lib.fv_render_sparse(
+                self._rctx.h, self._vol_r, C.byref(camc), self._light_ref(), C.byref(self._set),
+                _lib.ptr(self.idx), _lib.ptr(self.k), self.h * self.w, None, None, self.state.h, None))
+            rendered = torch.cuda.Event()
+            rendered.record(s_r)
+            s_n.wait_event(rendered)
+            _lib.check(self._nctx.lib.fv_reconstruct(self._nctx.h, self.net_h, self.state.h, 1,
+                                                     _lib.ptr(self.rgb), None, None))
+            done = torch.cuda.Event()
+            done.record(s_n)
+            net_done.append(done)
+        # rejoin the pipeline's own stream
+        self.ctx.stream.wait_event(net_done[-1])
+        rj = torch.cuda.Event()
+        rj.record(s_r)
+        self.ctx.stream.wait_event(rj)
+
+    def pipelined_contexts(self):
+        return [c for c in (getattr(self, "_rctx", None), getattr(self, "_nctx", None)) if c is not None]
+
     def dense(self, cam: Camera):
         """Dense baseline frame (render_full, renderer.py:211-222) into a device buffer."""
         import torch

@@ -354,3 +354,31 @@ def test_end_to_end_c1_against_reference(golden, stack):
     for i in range(2):
         pipe.frame_to_host(cams[i], spec.fovea(), i, host)
     assert O.psnr(host, g["img1"]) >= 55.0
+
+
+def test_pipelined_frames_equal_serial_frames(stack):
+    """Two-stream pipelining (render t+1 during reconstruct t) must not change any frame."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    spec = ExperimentSpec(mode="hifi", width=320, height=184)
+    scene = default_scene("sphere_shells", (96, 96, 96))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, 320, 184)
+    pipe = FramePipeline(scene, net, (184, 320), stack)
+    outs = []
+    for i in range(6):
+        pipe.step(cams[i], spec.fovea(), i)
+        outs.append(pipe.rgb.clone())
+    pipe.reset()
+    frames = [(cams[i], spec.fovea(), i) for i in range(6)]
+    pipe.run_pipelined(frames)
+    torch.cuda.synchronize()
+    assert torch.equal(pipe.rgb, outs[-1])
+    # and frame by frame
+    pipe.reset()
+    for i in range(6):
+        pipe.run_pipelined(frames[i:i + 1])
+        torch.cuda.synchronize()
+        assert torch.equal(pipe.rgb, outs[i]), i
