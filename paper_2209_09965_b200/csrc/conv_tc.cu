@@ -48,9 +48,12 @@ struct ConvArgs {
   __half* dst;         // NC8HW8, cout channels (nullable in head mode)
   __half* pool_dst;    // nullable: 2x2 average pool of dst
   int relu;
-  int head;            // 1: D.head epilogue
-  float* od;           // head: (3, H, W) fp32
-  __half* feedback;    // head: NHWC8 net input, channels 5..7
+  int head;            // 1: aux epilogue (D.head and/or K-stage logits)
+  float* od;           // head: (3, H, W) fp32 (nullable)
+  __half* feedback;    // head: NHWC8 net input, channels 5..7 (nullable)
+  float* kw[2];        // K-stage filter weights (9, H, W) fp32 per K block (nullable)
+  int kcol[2];         // first logit column of each K block
+  int center_only;     // 1x1 conv: only the centre tap's MMAs are issued
   int tiles_x, tiles_y;
 };
 
@@ -64,21 +67,21 @@ struct Cfg {
 };
 
 // All MMAs of one K-stage: R output rows x 9 taps x NK k-steps, offsets folded at compile time.
-template <int R, int N, int NK>
+// kCenter: 1x1 convolution -- only tap 4 (dy = dx = 1) is issued.
+template <int R, int N, int NK, bool kCenter = false>
 __device__ __forceinline__ void issue_stage(uint64_t a0, uint64_t b0, uint32_t d_base, uint32_t idesc,
                                             bool first_stage) {
   using C = Cfg<R, N>;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
 #pragma unroll
-    for (int t = 0; t < 9; ++t) {
+    for (int t = kCenter ? 4 : 0; t < (kCenter ? 5 : 9); ++t) {
 #pragma unroll
       for (int k = 0; k < NK; ++k) {
-        constexpr int dummy = 0;
-        (void)dummy;
         const uint64_t ad = a0 + (uint64_t)((2 * k * C::kPlaneBytes + ((r + t / 3) * kHaloW + t % 3) * 16) >> 4);
         const uint64_t bd = b0 + (uint64_t)(((t * NK + k) * N * 32) >> 4);
-        sm100::mma_f16(d_base + r * N, ad, bd, idesc, (!first_stage || t || k) ? 1u : 0u);
+        const bool acc = !first_stage || (kCenter ? k != 0 : (t | k) != 0);
+        sm100::mma_f16(d_base + r * N, ad, bd, idesc, acc ? 1u : 0u);
       }
     }
   }
@@ -207,10 +210,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         const uint64_t a0 = sm100::smem_desc(sm100::smem_u32(sA + st * C::kABytes), C::kPlaneBytes, 128);
         const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + st * C::kBBytes), N * 16, 128);
         if (sm100::elect_one()) {
-          if (nk == 2)
+          if (a.center_only) {
+            if (nk == 2)
+              issue_stage<R, N, 2, true>(a0, b0, d_base, idesc, ks == 0);
+            else
+              issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
+          } else if (nk == 2) {
             issue_stage<R, N, 2>(a0, b0, d_base, idesc, ks == 0);
-          else
+          } else {
             issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
+          }
         }
         __syncwarp();
         sm100::mma_commit_elect(bar_empty + 8 * st);
@@ -237,21 +246,52 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       const bool xin = x < a.W;
       const uint32_t t_row0 = tmem_base + ((uint32_t)(32 * q) << 16) + acc * R * N;
       if (a.head) {
+        // D.head (cols 0..2) and/or K-stage logits (9 cols per K block): O_d in fp32 planes +
+        // next frame's feedback channels; logits -> max-subtracted softmax (autograd.py:188-199)
+        // -> 9 fp32 filter-weight planes per K block.
+        const int64_t hw = (int64_t)a.H * a.W;
         for (int r = 0; r < R; ++r) {
-          float v[16];
-          sm100::tmem_ld16(t_row0 + r * N, v);
+          float v[N >= 32 ? 32 : 16];
+          sm100::tmem_ld16(t_row0 + r * N, *reinterpret_cast<float(*)[16]>(v));
+          if constexpr (N >= 32) sm100::tmem_ld16(t_row0 + r * N + 16, *reinterpret_cast<float(*)[16]>(v + 16));
           const int y = y0 + r;
           if (xin && y < a.H) {
-            float o[3];
+            const int64_t pix = (int64_t)y * a.W + x;
+            if (a.od) {
+              float o[3];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              o[c] = v[c] + __ldg(a.bias + c);
-              a.od[(int64_t)c * a.H * a.W + (int64_t)y * a.W + x] = o[c];
+              for (int c = 0; c < 3; ++c) {
+                o[c] = v[c] + __ldg(a.bias + c);
+                a.od[c * hw + pix] = o[c];
+              }
+              if (a.feedback) {
+                __half* fb = a.feedback + pix * 8;
+                fb[5] = __float2half(o[0]);
+                fb[6] = __float2half(o[1]);
+                fb[7] = __float2half(o[2]);
+              }
             }
-            __half* fb = a.feedback + ((int64_t)y * a.W + x) * 8;
-            fb[5] = __float2half(o[0]);
-            fb[6] = __float2half(o[1]);
-            fb[7] = __float2half(o[2]);
+            if constexpr (N >= 32) {
+#pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                if (!a.kw[s]) continue;
+                const int c0 = a.kcol[s];
+                float l[9], m = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 9; ++j) {
+                  l[j] = v[c0 + j] + __ldg(a.bias + c0 + j);
+                  m = fmaxf(m, l[j]);
+                }
+                float sum = 0.f;
+#pragma unroll
+                for (int j = 0; j < 9; ++j) {
+                  l[j] = expf(l[j] - m);
+                  sum += l[j];
+                }
+#pragma unroll
+                for (int j = 0; j < 9; ++j) a.kw[s][j * hw + pix] = l[j] / sum;
+              }
+            }
           }
         }
       } else {
@@ -397,7 +437,7 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
 
 // Public-internal entry: run one 3x3 conv. srcs: up to 3 NC8HW8 tensors at the same level.
 int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_act* dst,
-            fv_act* pool_dst, bool relu, float* head_od, __half* head_feedback) {
+            fv_act* pool_dst, bool relu, const ConvAux* aux) {
   ConvArgs a{};
   a.n_src = n_src;
   int groups = 0;
@@ -418,9 +458,17 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   a.dst = dst ? dst->p : nullptr;
   a.pool_dst = pool_dst ? pool_dst->p : nullptr;
   a.relu = relu ? 1 : 0;
-  a.head = head_od != nullptr;
-  a.od = head_od;
-  a.feedback = head_feedback;
+  if (aux) {
+    a.head = 1;
+    a.od = aux->od;
+    a.feedback = aux->feedback;
+    for (int s = 0; s < 2; ++s) {
+      a.kw[s] = aux->kw[s];
+      a.kcol[s] = aux->kcol[s];
+    }
+    a.center_only = aux->center_only ? 1 : 0;
+    FV_REQUIRE(!(aux->kw[0] || aux->kw[1]) || cp.n_pad >= 32, "conv %s: logits need N >= 32", cp.name.c_str());
+  }
   switch (cp.n_pad) {
     case 16: return launch<4, 16>(ctx, a);
     case 32: return launch<4, 32>(ctx, a);
@@ -466,7 +514,7 @@ int fv_debug_conv3x3(fv_ctx* ctx, int cin, int cout, int H, int W, const void* x
   pool.C = cout;
   pool.H = H / 2;
   pool.W = W / 2;
-  rc = fv::conv3x3(ctx, cp, &src, 1, &dst, pool_nc8 ? &pool : nullptr, relu != 0, nullptr, nullptr);
+  rc = fv::conv3x3(ctx, cp, &src, 1, &dst, pool_nc8 ? &pool : nullptr, relu != 0, nullptr);
   cudaStreamSynchronize(ctx->stream);
   cudaFree(cp.w_dev);
   cudaFree(cp.b_dev);

@@ -105,6 +105,17 @@ struct ConvParam {
 
 }  // namespace fv
 
+namespace fv {
+// Auxiliary epilogue of a conv: D.head outputs and/or K-stage logits -> softmax filter weights.
+struct ConvAux {
+  float* od = nullptr;         // (3,H,W) fp32, columns 0..2
+  __half* feedback = nullptr;  // NHWC8 input channels 5..7
+  float* kw[2] = {nullptr, nullptr};  // (9,H,W) fp32 per K block
+  int kcol[2] = {0, 0};
+  bool center_only = false;    // 1x1 conv (logits only)
+};
+}  // namespace fv
+
 struct fv_net {
   std::vector<std::pair<char, int>> blocks;
   int n_enc = 0, n_dec = 0;
@@ -115,8 +126,9 @@ struct fv_net {
   std::vector<fv::ConvParam> convs;  // D.block{i}.conv{1,2} (2 per block), D.head, K.block{i}
   int head_index = -1;
   int k_index0 = -1;  // first K conv
-  float* kw_dev = nullptr;  // all K weights, fp32 (rounded to fp16 values), packed
-  std::vector<int64_t> kw_off;  // per K block: offset (floats) of (9*C weights + 9 bias)
+  // K stage as tcgen05 convs, one per level: D.head (level 0) + the logits of the K blocks there
+  std::vector<fv::ConvParam> kconv;
+  bool kstage_dirty = true;
 };
 
 // Activation tensor in "NC8HW8" layout: C/8 planes of (H, W, 8) fp16.
@@ -143,6 +155,7 @@ struct fv_state {
   float* od = nullptr;              // (3,Hp,Wp) fp32 O_d (padded)
   std::vector<float*> img;          // K-stage ping buffers per level (3,HL,WL) fp32
   std::vector<float*> img2;
+  std::vector<float*> kw;           // per K block: softmax filter weights (9,HL,WL) fp32
   void* arena = nullptr;
   int64_t arena_bytes = 0;
 };

@@ -19,9 +19,10 @@
 
 namespace fv {
 int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_act* dst,
-            fv_act* pool_dst, bool relu, float* head_od, __half* head_feedback);
+            fv_act* pool_dst, bool relu, const ConvAux* aux);
 int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out);
-int kfilter(fv_ctx* ctx, const fv_act& hd, const float* kw, const float* img, float* out);
+int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w);
+constexpr int kLogitCol[2] = {4, 13};
 int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out);
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in);
 int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw);
@@ -74,21 +75,66 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 }  // namespace
 
-int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* out_rgb,
+// Build the level convs of the K stage from D.head + K.block{i} parameters: conv L reads the
+// decoder hidden state at level L; columns 0..2 = D.head (level 0 only, all 9 taps), columns
+// kLogitCol[s].. = the 9 logits of the s-th K block at that level (1x1 = centre tap).
+int build_kstage(fv_ctx* ctx, fv_net* net) {
+  const int ne = net->n_enc;
+  const std::vector<int> lv = block_levels(net);
+  const ConvParam& head = net->convs[net->head_index];
+  net->kconv.assign(ne + 1, ConvParam());
+  for (int L = 0; L <= ne; ++L) {
+    ConvParam& cp = net->kconv[L];
+    const int cin = net->blocks[ne + (ne - L)].second;  // decoder block at level L
+    cp.name = "K.level" + std::to_string(L);
+    cp.cin = cin;
+    cp.cout = 32;
+    cp.n_pad = 32;
+    cp.w_host.assign((size_t)32 * cin * 9, 0.f);
+    cp.b_host.assign(32, 0.f);
+    if (L == 0) {
+      for (size_t i = 0; i < (size_t)3 * cin * 9; ++i) cp.w_host[i] = head.w_host[i];
+      for (int o = 0; o < 3; ++o) cp.b_host[o] = head.b_host[o];
+    }
+    int s = 0;
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (lv[i] != L || s >= 2) continue;
+      const ConvParam& kp = net->convs[net->k_index0 + i];  // (9, cin, 1, 1)
+      for (int j = 0; j < 9; ++j) {
+        for (int c = 0; c < cin; ++c)
+          cp.w_host[((size_t)(kLogitCol[s] + j) * cin + c) * 9 + 4] = kp.w_host[(size_t)j * cin + c];
+        cp.b_host[kLogitCol[s] + j] = kp.b_host[j];
+      }
+      ++s;
+    }
+    cp.w_set = cp.b_set = true;
+    const int rc = conv_prepare(ctx, cp);
+    if (rc) return rc;
+  }
+  net->kstage_dirty = false;
+  return 0;
+}
+
+int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float* out_rgb,
                 float* out_o, float* out_od) {
+  fv_net* net = const_cast<fv_net*>(cnet);  // the fused K-stage convs are a cache of the params
   for (const auto& cp : net->convs)
     if (!(cp.w_set && cp.b_set)) {
       set_error("network parameter %s not set", cp.name.c_str());
       return FV_E_INVALID;
     }
+  if (net->kstage_dirty) {
+    const int rc0 = build_kstage(ctx, net);
+    if (rc0) return rc0;
+  }
   const int ne = net->n_enc, nd = net->n_dec;
   int rc;
   const fv_act* cur = &st->x;
   for (int i = 0; i < ne; ++i) {
-    rc = conv3x3(ctx, net->convs[2 * i], cur, 1, &st->enc_a[i], nullptr, true, nullptr, nullptr);
+    rc = conv3x3(ctx, net->convs[2 * i], cur, 1, &st->enc_a[i], nullptr, true, nullptr);
     if (rc) return rc;
     rc = conv3x3(ctx, net->convs[2 * i + 1], &st->enc_a[i], 1, &st->skips[i], &st->pooled[i], true,
-                 nullptr, nullptr);
+                 nullptr);
     if (rc) return rc;
     cur = &st->pooled[i];
   }
@@ -106,28 +152,45 @@ int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* 
     }
     if (net->recurrent) srcs[n++] = st->hidden[oldp][j];
     const int b = ne + j;
-    rc = conv3x3(ctx, net->convs[2 * b], srcs, n, &st->dec_a[j], nullptr, true, nullptr, nullptr);
+    rc = conv3x3(ctx, net->convs[2 * b], srcs, n, &st->dec_a[j], nullptr, true, nullptr);
     if (rc) return rc;
     rc = conv3x3(ctx, net->convs[2 * b + 1], &st->dec_a[j], 1, &st->hidden[newp][j], nullptr, true,
-                 nullptr, nullptr);
+                 nullptr);
     if (rc) return rc;
   }
-  // D.head -> O_d (fp32 planes) + feedback channels 5..7 of the NEXT frame's input buffer. The
-  // two input buffers alternate, so the next frame's mask + march (which write channels 0..4)
-  // may run on another stream while this frame's network still reads its own input.
-  rc = conv3x3(ctx, net->convs[net->head_index], &st->hidden[newp][nd - 1], 1, nullptr, nullptr,
-               false, st->od, net->recurrent ? st->xalt.p : nullptr);
-  if (rc) return rc;
+  // Level 0: one tcgen05 conv over Hd3 computes D.head (3x3, columns 0..2) AND the logits of
+  // the two K blocks at level 0 (1x1, centre tap only, columns 4.. and 13..); its epilogue writes
+  // O_d, the NEXT frame's feedback channels 5..7 (the two input buffers alternate, so the next
+  // frame's mask + march may already write channels 0..4 of it on another stream) and the
+  // softmax-normalised 3x3 filter weights of both K blocks. Levels > 0: a 1x1 logits conv each.
+  const std::vector<int> lv = block_levels(net);
+  const int nb = (int)lv.size();
+  for (int L = 0; L <= ne; ++L) {
+    if (L > 0 && !use_k) break;
+    ConvAux aux;
+    if (L == 0) {
+      aux.od = st->od;
+      aux.feedback = net->recurrent ? st->xalt.p : nullptr;
+    } else {
+      aux.center_only = true;
+    }
+    int s = 0;
+    for (int i = 0; i < nb; ++i)
+      if (lv[i] == L && s < 2) {
+        aux.kw[s] = st->kw[i];
+        aux.kcol[s] = kLogitCol[s];
+        ++s;
+      }
+    rc = conv3x3(ctx, net->kconv[L], &st->hidden[newp][ne - L], 1, nullptr, nullptr, false, &aux);
+    if (rc) return rc;
+  }
   const float* final_img = st->od;
   if (use_k) {
-    const std::vector<int> lv = block_levels(net);
-    const int nb = (int)lv.size();
     const float* img = st->od;
     for (int i = 0; i < nb; ++i) {
       const int L = lv[i];
-      const fv_act& hd = st->hidden[newp][ne - L];
       float* out = st->img2[L];
-      rc = kfilter(ctx, hd, net->kw_dev + net->kw_off[i], img, out);
+      rc = kapply(ctx, st->kw[i], img, out, st->Hp >> L, st->Wp >> L);
       if (rc) return rc;
       if (net->blocks[i].first == 'e') {
         rc = pool3(ctx, out, st->img[L + 1], st->Hp >> (L + 1), st->Wp >> (L + 1));
@@ -218,7 +281,6 @@ int fv_net_create(fv_ctx* ctx, const char* blocks, int predicted_kernel, int rec
   }
   net->k_index0 = (int)net->convs.size();
   const std::vector<int> lv = block_levels(net);
-  int64_t off = 0;
   for (size_t i = 0; i < lv.size(); ++i) {
     ConvParam cp;
     cp.name = "K.block" + std::to_string(i);
@@ -226,26 +288,18 @@ int fv_net_create(fv_ctx* ctx, const char* blocks, int predicted_kernel, int rec
     cp.cout = 9;
     cp.ksize = 1;
     net->convs.push_back(cp);
-    net->kw_off.push_back(off);
-    off += 9 * cp.cin + 9;
   }
-  if (cudaMalloc(&net->kw_dev, sizeof(float) * off) != cudaSuccess) {
-    delete net;
-    set_error("cudaMalloc failed for K weights");
-    return FV_E_NOMEM;
-  }
-  cudaMemset(net->kw_dev, 0, sizeof(float) * off);
   *out = net;
   return 0;
 }
 
 int fv_net_destroy(fv_net* net) {
   if (!net) return 0;
-  for (auto& cp : net->convs) {
-    if (cp.w_dev) cudaFree(cp.w_dev);
-    if (cp.b_dev) cudaFree(cp.b_dev);
-  }
-  if (net->kw_dev) cudaFree(net->kw_dev);
+  for (auto* v : {&net->convs, &net->kconv})
+    for (auto& cp : *v) {
+      if (cp.w_dev) cudaFree(cp.w_dev);
+      if (cp.b_dev) cudaFree(cp.b_dev);
+    }
   delete net;
   return 0;
 }
@@ -291,17 +345,8 @@ int fv_net_set_param(fv_ctx* ctx, fv_net* net, const char* name, const float* ho
     cp.b_host.assign(host, host + count);
     cp.b_set = true;
   }
-  if (!(cp.w_set && cp.b_set)) return 0;
-  if (cp.ksize == 1) {
-    const int k = idx - net->k_index0;
-    std::vector<float> packed(9 * cp.cin + 9);
-    for (int j = 0; j < 9; ++j)
-      for (int c = 0; c < cp.cin; ++c) packed[j * cp.cin + c] = cp.w_host[(size_t)j * cp.cin + c];
-    for (int j = 0; j < 9; ++j) packed[9 * cp.cin + j] = cp.b_host[j];
-    FV_CUDA(cudaMemcpy(net->kw_dev + net->kw_off[k], packed.data(), sizeof(float) * packed.size(),
-                       cudaMemcpyHostToDevice));
-    return 0;
-  }
+  if (idx == net->head_index || cp.ksize == 1) net->kstage_dirty = true;  // folded into kconv
+  if (!(cp.w_set && cp.b_set) || cp.ksize == 1 || idx == net->head_index) return 0;
   return conv_prepare(ctx, cp);
 }
 
@@ -354,6 +399,12 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
     img2_off.push_back(bytes);
     bytes += align_up((int64_t)3 * (st->Hp >> L) * (st->Wp >> L) * 4, 256);
   }
+  const std::vector<int> lv = block_levels(net);
+  std::vector<int64_t> kw_off;
+  for (int L : lv) {
+    kw_off.push_back(bytes);
+    bytes += align_up((int64_t)9 * (st->Hp >> L) * (st->Wp >> L) * 4, 256);
+  }
   if (cudaMalloc(&st->arena, bytes) != cudaSuccess) {
     delete st;
     set_error("cudaMalloc of %lld bytes for the state failed", (long long)bytes);
@@ -372,6 +423,7 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
     st->img.push_back(reinterpret_cast<float*>(base + img_off[L]));
     st->img2.push_back(reinterpret_cast<float*>(base + img2_off[L]));
   }
+  for (int64_t o : kw_off) st->kw.push_back(reinterpret_cast<float*>(base + o));
   if (cudaMemsetAsync(st->arena, 0, bytes, ctx->stream) != cudaSuccess) {
     cudaFree(st->arena);
     delete st;

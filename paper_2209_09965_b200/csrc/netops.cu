@@ -73,157 +73,29 @@ __global__ void __launch_bounds__(128) upsample2_nc8_kernel(const __half* __rest
   }
 }
 
-// ---- K stage: logits (1x1 conv) -> softmax -> per-pixel 3x3 filter -------------------------
-// Four horizontally adjacent pixels per thread: each 16-byte weight read from shared memory
-// feeds 16 FMAs (the one-pixel version was bound by its 9*C broadcast LDS per pixel).
-template <int C>
-__global__ void __launch_bounds__(128) kfilter4_kernel(const __half* __restrict__ hd,
-                                                       const float* __restrict__ kw,
-                                                       const float* __restrict__ img,
-                                                       float* __restrict__ out, int h, int w) {
-  __shared__ __align__(16) float sw[9 * C + 12];
-  for (int i = threadIdx.x; i < 9 * C + 9; i += blockDim.x) sw[i] = kw[i];
-  __syncthreads();
-  const int wq = (w + 3) >> 2;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
-  if (q >= wq) return;
-  const int x0 = 4 * q;
-  const int64_t n = (int64_t)h * w;
-  const int64_t plane = n * 8;
-  float lg[4][9];
+// ---- K stage: apply the per-pixel 3x3 filters ------------------------------------------------
+// out[c,y,x] = sum_j k[j,y,x] * img[c, y+j/3-1, x+j%3-1], zero padding, taps in order
+// (apply_kernel_field, autograd.py:332-359). The softmax-normalised weights k come from the
+// tcgen05 logits conv's epilogue (conv_tc.cu), so this pass only streams 9 + 3 planes.
+__global__ void __launch_bounds__(128) kapply_kernel(const float* __restrict__ kw, const float* __restrict__ img,
+                                                     float* __restrict__ out, int h, int w) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= w) return;
+  const int64_t n = (int64_t)h * w, pix = (int64_t)y * w + x;
+  float k[9];
 #pragma unroll
-  for (int p = 0; p < 4; ++p)
-#pragma unroll
-    for (int j = 0; j < 9; ++j) lg[p][j] = 0.f;
-#pragma unroll 1
-  for (int g = 0; g < C / 8; ++g) {
-    float f[4][8];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (x0 + p < w) v = *reinterpret_cast<const uint4*>(hd + g * plane + ((int64_t)y * w + x0 + p) * 8);
-      const __half2* h2 = reinterpret_cast<const __half2*>(&v);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 t = __half22float2(h2[e]);
-        f[p][2 * e] = t.x;
-        f[p][2 * e + 1] = t.y;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 9; ++j) {
-#pragma unroll
-      for (int e4 = 0; e4 < 2; ++e4) {
-        const float4 wv = *reinterpret_cast<const float4*>(sw + j * C + g * 8 + e4 * 4);
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          lg[p][j] = fmaf(wv.x, f[p][e4 * 4 + 0], lg[p][j]);
-          lg[p][j] = fmaf(wv.y, f[p][e4 * 4 + 1], lg[p][j]);
-          lg[p][j] = fmaf(wv.z, f[p][e4 * 4 + 2], lg[p][j]);
-          lg[p][j] = fmaf(wv.w, f[p][e4 * 4 + 3], lg[p][j]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    float m = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 9; ++j) {
-      lg[p][j] += sw[9 * C + j];
-      m = fmaxf(m, lg[p][j]);
-    }
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < 9; ++j) {
-      lg[p][j] = expf(lg[p][j] - m);
-      s += lg[p][j];
-    }
-#pragma unroll
-    for (int j = 0; j < 9; ++j) lg[p][j] = lg[p][j] / s;
-  }
-  // the 3 x 6 neighbourhood of the 4 pixels, loaded once per channel (zero padding)
+  for (int j = 0; j < 9; ++j) k[j] = __ldg(kw + j * n + pix);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float* pl = img + (int64_t)c * n;
-    float nb[3][6];
-#pragma unroll
-    for (int dy = 0; dy < 3; ++dy) {
-      const int yy = y + dy - 1;
-#pragma unroll
-      for (int dx = 0; dx < 6; ++dx) {
-        const int xx = x0 + dx - 1;
-        nb[dy][dx] = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
-      }
-    }
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      if (x0 + p >= w) break;
-      float acc = 0.f;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) acc = acc + lg[p][j] * nb[j / 3][p + j % 3];
-      out[(int64_t)c * n + (int64_t)y * w + x0 + p] = acc;
-    }
-  }
-}
-
-template <int C>
-__global__ void kfilter_kernel(const __half* __restrict__ hd, const float* __restrict__ kw,
-                               const float* __restrict__ img, float* __restrict__ out, int h, int w) {
-  __shared__ float sw[9 * C + 9];
-  for (int i = threadIdx.x; i < 9 * C + 9; i += blockDim.x) sw[i] = kw[i];
-  __syncthreads();
-  const int64_t n = (int64_t)h * w;
-  const int64_t plane = n * 8;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(i % w), y = (int)(i / w);
-    float lg[9];
-#pragma unroll
-    for (int j = 0; j < 9; ++j) lg[j] = 0.f;
-#pragma unroll 2
-    for (int g = 0; g < C / 8; ++g) {
-      const uint4 q = *reinterpret_cast<const uint4*>(hd + g * plane + i * 8);
-      const __half2* h2 = reinterpret_cast<const __half2*>(&q);
-      float f[8];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 t = __half22float2(h2[e]);
-        f[2 * e] = t.x;
-        f[2 * e + 1] = t.y;
-      }
-#pragma unroll
-      for (int j = 0; j < 9; ++j)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) lg[j] = fmaf(sw[j * C + g * 8 + e], f[e], lg[j]);
-    }
-    float m = -INFINITY;
+    float acc = 0.f;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      lg[j] += sw[9 * C + j];
-      m = fmaxf(m, lg[j]);
+      const int yy = y + j / 3 - 1, xx = x + j % 3 - 1;
+      const float v = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
+      acc = acc + k[j] * v;
     }
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < 9; ++j) {
-      lg[j] = expf(lg[j] - m);
-      s += lg[j];
-    }
-#pragma unroll
-    for (int j = 0; j < 9; ++j) lg[j] = lg[j] / s;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const float* pl = img + (int64_t)c * n;
-      float acc = 0.f;
-#pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        const int yy = y + j / 3 - 1, xx = x + j % 3 - 1;
-        const float v = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
-        acc = acc + lg[j] * v;
-      }
-      out[(int64_t)c * n + i] = acc;
-    }
+    out[(int64_t)c * n + pix] = acc;
   }
 }
 
@@ -362,17 +234,10 @@ int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
   return 0;
 }
 
-int kfilter(fv_ctx* ctx, const fv_act& hd, const float* kw, const float* img, float* out) {
-  const dim3 g(((hd.W + 3) / 4 + 127) / 128, hd.H);
-  switch (hd.C) {
-#define KF(CC) case CC: kfilter4_kernel<CC><<<g, 128, 0, ctx->stream>>>(hd.p, kw, img, out, hd.H, hd.W); break;
-    KF(8) KF(16) KF(24) KF(32) KF(40) KF(48) KF(56) KF(64) KF(72) KF(80) KF(88) KF(96) KF(112) KF(128)
-#undef KF
-    default:
-      set_error("K stage: unsupported hidden width %d", hd.C);
-      return FV_E_UNSUPPORTED;
-  }
-  FV_CHECK_LAUNCH("kfilter_kernel");
+int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w) {
+  const dim3 g((w + 127) / 128, h);
+  kapply_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w);
+  FV_CHECK_LAUNCH("kapply_kernel");
   ctx->launches += 1;
   return 0;
 }
