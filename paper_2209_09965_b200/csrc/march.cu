@@ -892,21 +892,24 @@ __global__ void __launch_bounds__(128) march_refill_kernel(FastParams F, unsigne
 //
 // In _march the shade of a sample enters only the colour sum (renderer.py:181-182); opacity,
 // depth and early termination never depend on it. So the main pass marches every compacted ray
-// without shadows and records, for each sample with a_step > 0, its position, its weight
+// once, without shadows, and records for each sample with a_step > 0 its position, its weight
 // T*a_step and its TF colour; the shadow pass then marches all those shadow rays as independent
 // work items (4.6M per C3 frame instead of 117k hit rays, so no ray's serial chain sets the
-// tail); the composite pass sums contrib*(c*(shade*I)) per ray in sample order -- the
-// reference's order, so the result equals the fused kernel's. A ray's records are allocated
-// after a counting march, so they are contiguous and in order. A ray whose records would not fit
-// the buffer is marched fused (inline shadows) instead.
+// tail); the composite pass sums contrib*(c*(shade*I)) per ray. Records are appended to 32-slot
+// chunks taken from a global counter (a ray's chunks form a linked list), so one march suffices.
+// A ray that cannot get a chunk (buffer full) is re-marched fused, with inline shadows.
+constexpr int kChunk = 32;
+
 struct WaveBufs {
   float4* rec0;            // (px, py, pz, -): shadow-ray origin
   float4* rec1;            // (c0, c1, c2, contrib = T * a_step)
   float* shade;            // written by the shadow pass
-  int cap;
-  unsigned int* rec_count;
+  int* chunk_next;         // next chunk of the same ray (-1 = last)
+  int* chunk_fill;         // used slots of a chunk
+  int n_chunks_cap;
+  unsigned int* chunk_count;
   unsigned int* next;      // work counter of the shadow pass
-  int4* ray;               // per compacted ray: (record offset, record count, trans, depth) bits
+  int4* ray;               // per compacted ray: (first chunk, record count, trans, depth) bits
 };
 
 __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float r0, float r1, float r2,
@@ -941,7 +944,9 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
   int pix = -1, ray = -1;
   bool exhausted = false;
   float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0.f;
-  int s = 0, n = 0, phase = 0, m = 0, off = 0, j = 0;  // phase 0 count, 1 emit, 2 fused
+  int s = 0, n = 0, m = 0;
+  bool fused = false;           // inline-shadow fallback for this ray
+  int first = -1, chunk = -1, fill = 0;
   double t0 = 0.0;
   float rgb0 = 0, rgb1 = 0, rgb2 = 0, trans = 1.f, depth = 0.f;
 
@@ -977,7 +982,7 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
           depth = 0.f;
           if (!hit) {
             write_pixel(P, p, 0.f, 0.f, 0.f, 1.f, 0.f);
-            B.ray[r] = make_int4(0, 0, 0, 0);
+            B.ray[r] = make_int4(-1, 0, 0, 0);
           } else {
             ++hitc;
             const double L = tend - t0;
@@ -987,8 +992,10 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
             ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
             ez = (float)(P.pos[2] + d[2] * t0);
             dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-            s = 0; m = 0; j = 0;
-            phase = 0;
+            s = 0; m = 0;
+            fused = false;
+            first = chunk = -1;
+            fill = kChunk;
             pix = p;
             ray = r;
           }
@@ -1019,22 +1026,14 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
       const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
       const float a_step = 1.f - keep;
       const bool needs_shadow = lit && a_step > 0.f;
-      if (phase == 0) {
-        ++n_main;
-        if (needs_shadow) ++m;
-        if (!lit) {
-          const float contrib = trans * a_step;
-          rgb0 += contrib * (c[0] * I0);
-          rgb1 += contrib * (c[1] * I1);
-          rgb2 += contrib * (c[2] * I2);
-        }
-      } else if (phase == 1) {
-        if (needs_shadow) {
-          B.rec0[off + j] = make_float4(ex + dx * mid, ey + dy * mid, ez + dz * mid, 0.f);
-          B.rec1[off + j] = make_float4(c[0], c[1], c[2], trans * a_step);
-          ++j;
-        }
-      } else {
+      bool restart = false;
+      if (!fused) ++n_main;
+      if (!lit) {
+        const float contrib = trans * a_step;
+        rgb0 += contrib * (c[0] * I0);
+        rgb1 += contrib * (c[1] * I1);
+        rgb2 += contrib * (c[2] * I2);
+      } else if (fused) {
         float shade = 1.f;
         if (needs_shadow)
           shade = amb + (1.f - amb) * shadow_fast(F, lut, ex + dx * mid, ey + dy * mid, ez + dz * mid, n_shadow);
@@ -1042,31 +1041,49 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
         rgb0 += contrib * (c[0] * (shade * I0));
         rgb1 += contrib * (c[1] * (shade * I1));
         rgb2 += contrib * (c[2] * (shade * I2));
+      } else if (needs_shadow) {
+        if (fill == kChunk) {
+          const int nc = (int)atomicAdd(B.chunk_count, 1u);
+          if (nc >= B.n_chunks_cap) {
+            restart = true;  // buffer full: discard this ray's records, march it fused
+          } else {
+            if (chunk >= 0) { B.chunk_fill[chunk] = kChunk; B.chunk_next[chunk] = nc; }
+            else first = nc;
+            chunk = nc;
+            fill = 0;
+          }
+        }
+        if (!restart) {
+          const int slot = chunk * kChunk + fill;
+          B.rec0[slot] = make_float4(ex + dx * mid, ey + dy * mid, ez + dz * mid, 0.f);
+          B.rec1[slot] = make_float4(c[0], c[1], c[2], trans * a_step);
+          ++fill;
+          ++m;
+        }
+      }
+      if (restart) {
+        for (int cc = first; cc >= 0; cc = (cc == chunk) ? -1 : B.chunk_next[cc]) B.chunk_fill[cc] = 0;
+        fused = true;
+        s = 0; m = 0;
+        first = chunk = -1;
+        trans = 1.f; depth = 0.f;
+        rgb0 = rgb1 = rgb2 = 0.f;
+        break;
       }
       trans = trans * (1.f - a_step);
       const float acc = 1.f - trans;
       if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid);
       ++s;
       if (s >= n || !(acc < early)) {
-        if (phase == 0 && m > 0) {
-          const unsigned a0 = atomicAdd(B.rec_count, (unsigned)m);
-          if ((int64_t)a0 + m <= (int64_t)B.cap) {
-            off = (int)a0;
-            phase = 1;
-          } else {
-            phase = 2;
-          }
-          s = 0; j = 0;
-          trans = 1.f; depth = 0.f;
-          rgb0 = rgb1 = rgb2 = 0.f;
-        } else if (phase == 1) {
-          B.ray[ray] = make_int4(off, m, __float_as_int(trans), __float_as_int(depth));
-          pix = -1;
+        if (lit && !fused && m > 0) {
+          B.chunk_fill[chunk] = fill;
+          B.chunk_next[chunk] = -1;
+          B.ray[ray] = make_int4(first, m, __float_as_int(trans), __float_as_int(depth));
         } else {
           write_pixel(P, pix, rgb0, rgb1, rgb2, trans, depth);
-          B.ray[ray] = make_int4(0, 0, 0, 0);
-          pix = -1;
+          B.ray[ray] = make_int4(-1, 0, 0, 0);
         }
+        pix = -1;
         break;
       }
     }
@@ -1086,36 +1103,42 @@ __global__ void __launch_bounds__(128) march_wave_main_kernel(FastParams F, Wave
   }
 }
 
-// One shadow ray per record; lanes refill from a work counter so long shadow rays do not idle
-// their warp's neighbours.
+// One shadow ray per record slot (empty tail slots of a ray's last chunk are skipped); lanes
+// refill from a work counter so long shadow rays do not idle their warp's neighbours.
 __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
   __shared__ float lut[4 * 256];
   for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
   __syncthreads();
-  const int nrec = (int)min(*B.rec_count, (unsigned)B.cap);
+  const int nslots = (int)min(*B.chunk_count, (unsigned)B.n_chunks_cap) * kChunk;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const float amb = (float)P.ambient;
   unsigned int n_shadow = 0;
   bool exhausted = false;
+  int my = -1;
   while (true) {
-    const bool need = !exhausted;
-    const unsigned msk = __ballot_sync(0xffffffffu, need);
-    if (!msk) break;
-    const int leader = __ffs(msk) - 1;
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(B.next, (unsigned)__popc(msk));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (need) {
-      const int i = (int)(base + __popc(msk & lt_mask));
-      if (i >= nrec) {
-        exhausted = true;
-      } else {
-        const float4 r0 = B.rec0[i];
-        const float ts = shadow_fast(F, lut, r0.x, r0.y, r0.z, n_shadow);
-        B.shade[i] = amb + (1.f - amb) * ts;
+    // refill until every lane holds a used slot (or the slots ran out), then march
+    while (true) {
+      const bool need = my < 0 && !exhausted;
+      const unsigned msk = __ballot_sync(0xffffffffu, need);
+      if (!msk) break;
+      const int leader = __ffs(msk) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(B.next, (unsigned)__popc(msk));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        const int i = (int)(base + __popc(msk & lt_mask));
+        if (i >= nslots) exhausted = true;
+        else if ((i % kChunk) < B.chunk_fill[i / kChunk]) my = i;
       }
+    }
+    if (!__any_sync(0xffffffffu, my >= 0)) break;
+    if (my >= 0) {
+      const float4 r0 = B.rec0[my];
+      const float ts = shadow_fast(F, lut, r0.x, r0.y, r0.z, n_shadow);
+      B.shade[my] = amb + (1.f - amb) * ts;
+      my = -1;
     }
   }
 #pragma unroll
@@ -1123,9 +1146,9 @@ __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, Wa
   if (lane == 0 && n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
 }
 
-// rgb = sum_j contrib_j * (c_j * (shade_j * I)), then the background blend. One warp per ray:
-// lane l sums records l, l+32, ... (coalesced), then a fixed xor tree -- deterministic, and the
-// reordering versus the reference's sequential sum is an fp32 rounding effect (~1e-7).
+// rgb = sum_j contrib_j * (c_j * (shade_j * I)), then the background blend. One warp per ray,
+// one chunk (32 records) per step of the chain; lane sums then a fixed xor tree -- deterministic;
+// the reordering versus the reference's sequential sum is an fp32 rounding effect (~1e-7).
 __global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
   const int k = P.k_dev ? *P.k_dev : P.k_max;
@@ -1134,14 +1157,18 @@ __global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F,
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < k; r += warps) {
     const int4 v = B.ray[r];
-    if (v.y == 0) continue;
+    if (v.x < 0) continue;
     float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;
-    for (int j = lane; j < v.y; j += 32) {
-      const float4 c = B.rec1[v.x + j];
-      const float sh = B.shade[v.x + j];
-      rgb0 += c.w * (c.x * (sh * I0));
-      rgb1 += c.w * (c.y * (sh * I1));
-      rgb2 += c.w * (c.z * (sh * I2));
+    for (int c = v.x, j = 0; j < v.y; j += kChunk) {
+      if (lane < B.chunk_fill[c]) {
+        const int slot = c * kChunk + lane;
+        const float4 q = B.rec1[slot];
+        const float sh = B.shade[slot];
+        rgb0 += q.w * (q.x * (sh * I0));
+        rgb1 += q.w * (q.y * (sh * I1));
+        rgb2 += q.w * (q.z * (sh * I2));
+      }
+      c = B.chunk_next[c];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1308,11 +1335,13 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     }
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
-      const int64_t rec_cap = std::max<int64_t>(4 << 20, 8ll * k_max);
+      // record slots: 16 per compacted ray (C3 needs ~12 incl. chunk tails), at least 4M
+      const int64_t rec_cap = std::max<int64_t>(4 << 20, 16ll * k_max) / kChunk * kChunk;
       if (rec_cap > ctx->wave_cap) {
         if (ctx->wave_rec) cudaFree(ctx->wave_rec);
         ctx->wave_rec = nullptr;
-        FV_CUDA(cudaMalloc(&ctx->wave_rec, (sizeof(float4) * 2 + sizeof(float)) * rec_cap));
+        FV_CUDA(cudaMalloc(&ctx->wave_rec, (sizeof(float4) * 2 + sizeof(float)) * rec_cap +
+                                               2 * sizeof(int) * (rec_cap / kChunk)));
         ctx->wave_cap = rec_cap;
       }
       if (k_max > ctx->wave_ray_cap) {
@@ -1325,8 +1354,10 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.rec0 = reinterpret_cast<float4*>(ctx->wave_rec);
       B.rec1 = B.rec0 + ctx->wave_cap;
       B.shade = reinterpret_cast<float*>(B.rec1 + ctx->wave_cap);
-      B.cap = (int)std::min<int64_t>(ctx->wave_cap, INT32_MAX);
-      B.rec_count = &ctx->counters->wave_rec;
+      B.n_chunks_cap = (int)std::min<int64_t>(ctx->wave_cap / kChunk, INT32_MAX / kChunk);
+      B.chunk_next = reinterpret_cast<int*>(B.shade + ctx->wave_cap);
+      B.chunk_fill = B.chunk_next + ctx->wave_cap / kChunk;
+      B.chunk_count = &ctx->counters->wave_rec;
       B.next = &ctx->counters->wave_next;
       B.ray = reinterpret_cast<int4*>(ctx->wave_ray);
       static int main_u = 0, per_sm_main = 0, per_sm_sh = 0;

@@ -99,39 +99,42 @@ __global__ void __launch_bounds__(128) kapply_kernel(const float* __restrict__ k
   }
 }
 
-// 3-channel fp32 avg_pool2 (h, w are the OUTPUT dims)
-__global__ void pool3_kernel(const float* __restrict__ in, float* __restrict__ out, int h, int w) {
-  const int64_t n = (int64_t)3 * h * w;
+// 3-channel fp32 avg_pool2; grid (ceil(w/128), h, 3), h, w the OUTPUT dims
+__global__ void __launch_bounds__(128) pool3_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                    int h, int w) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y, c = blockIdx.z;
+  if (x >= w) return;
   const int W2 = 2 * w;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(i % w), y = (int)((i / w) % h), c = (int)(i / ((int64_t)h * w));
-    const float* p = in + (int64_t)c * 4 * h * w;
-    const float p00 = p[(int64_t)(2 * y) * W2 + 2 * x], p10 = p[(int64_t)(2 * y + 1) * W2 + 2 * x];
-    const float p01 = p[(int64_t)(2 * y) * W2 + 2 * x + 1], p11 = p[(int64_t)(2 * y + 1) * W2 + 2 * x + 1];
-    out[i] = 0.25f * (((p00 + p10) + p01) + p11);
-  }
+  const float* p = in + (int64_t)c * 4 * h * w;
+  const float2 r0 = *reinterpret_cast<const float2*>(p + (int64_t)(2 * y) * W2 + 2 * x);
+  const float2 r1 = *reinterpret_cast<const float2*>(p + (int64_t)(2 * y + 1) * W2 + 2 * x);
+  // 0.25 * (p00 + p10 + p01 + p11), left to right as autograd.avg_pool2
+  out[(int64_t)c * h * w + (int64_t)y * w + x] = 0.25f * (((r0.x + r1.x) + r0.y) + r1.y);
 }
 
-// 3-channel fp32 2x bilinear upsample (h, w are the INPUT dims)
-__global__ void up3_kernel(const float* __restrict__ in, float* __restrict__ out, int h, int w) {
-  const int H2 = 2 * h, W2 = 2 * w;
-  const int64_t n = (int64_t)3 * H2 * W2;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int X = (int)(i % W2), Y = (int)((i / W2) % H2), c = (int)(i / ((int64_t)H2 * W2));
-    const float* p = in + (int64_t)c * h * w;
-    const int iy = Y >> 1, ix = X >> 1;
-    int ya, yb, xa, xb;
-    float wya, wyb, wxa, wxb;
-    if (Y & 1) { ya = iy; yb = min(iy + 1, h - 1); wya = 0.75f; wyb = 0.25f; }
-    else { ya = max(iy - 1, 0); yb = iy; wya = 0.25f; wyb = 0.75f; }
-    if (X & 1) { xa = ix; xb = min(ix + 1, w - 1); wxa = 0.75f; wxb = 0.25f; }
-    else { xa = max(ix - 1, 0); xb = ix; wxa = 0.25f; wxb = 0.75f; }
-    const float ra = wya * p[(int64_t)ya * w + xa] + wyb * p[(int64_t)yb * w + xa];
-    const float rb = wya * p[(int64_t)ya * w + xb] + wyb * p[(int64_t)yb * w + xb];
-    out[i] = wxa * ra + wxb * rb;
+// 3-channel fp32 2x bilinear upsample; grid (ceil(w/128), h, 3), h, w the INPUT dims; one thread
+// writes the 2x2 output block of one input pixel
+__global__ void __launch_bounds__(128) up3_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                  int h, int w) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y, c = blockIdx.z;
+  if (j >= w) return;
+  const float* p = in + (int64_t)c * h * w;
+  const int rows[3] = {max(i - 1, 0), i, min(i + 1, h - 1)};
+  const int cols[3] = {max(j - 1, 0), j, min(j + 1, w - 1)};
+  float re[3], ro[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float a = p[(int64_t)rows[0] * w + cols[k]], b = p[(int64_t)rows[1] * w + cols[k]],
+                d = p[(int64_t)rows[2] * w + cols[k]];
+    re[k] = 0.25f * a + 0.75f * b;
+    ro[k] = 0.75f * b + 0.25f * d;
   }
+  float* o = out + (int64_t)c * 4 * h * w;
+  const int W2 = 2 * w;
+  *reinterpret_cast<float2*>(o + (int64_t)(2 * i) * W2 + 2 * j) =
+      make_float2(0.25f * re[0] + 0.75f * re[1], 0.75f * re[1] + 0.25f * re[2]);
+  *reinterpret_cast<float2*>(o + (int64_t)(2 * i + 1) * W2 + 2 * j) =
+      make_float2(0.25f * ro[0] + 0.75f * ro[1], 0.75f * ro[1] + 0.25f * ro[2]);
 }
 
 // x = rgba*m ++ m into channels 0..4 of the NHWC8 input (film region only)
@@ -243,14 +246,14 @@ int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, in
 }
 
 int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out) {
-  pool3_kernel<<<grid_for(ctx, (int64_t)3 * h_out * w_out), 256, 0, ctx->stream>>>(in, out, h_out, w_out);
+  pool3_kernel<<<dim3((w_out + 127) / 128, h_out, 3), 128, 0, ctx->stream>>>(in, out, h_out, w_out);
   FV_CHECK_LAUNCH("pool3_kernel");
   ctx->launches += 1;
   return 0;
 }
 
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in) {
-  up3_kernel<<<grid_for(ctx, (int64_t)12 * h_in * w_in), 256, 0, ctx->stream>>>(in, out, h_in, w_in);
+  up3_kernel<<<dim3((w_in + 127) / 128, h_in, 3), 128, 0, ctx->stream>>>(in, out, h_in, w_in);
   FV_CHECK_LAUNCH("up3_kernel");
   ctx->launches += 1;
   return 0;
