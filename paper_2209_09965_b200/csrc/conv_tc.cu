@@ -31,8 +31,8 @@ namespace {
 constexpr int kTileW = 128;          // output columns per tile (= MMA M)
 constexpr int kHaloW = kTileW + 2;   // 130
 constexpr int kRowBytes = kHaloW * 16;
-constexpr int kStageGroups = 4;      // channel groups (of 8) per K-stage
-constexpr int kStages = 2;
+constexpr int kStageGroups = 2;      // channel groups (of 8) per K-stage = one MMA K of 16
+constexpr int kBResStages = 4;       // resident-weight kernels hold up to 4 stages (cin <= 64)
 constexpr int kThreads = 192;
 
 struct ConvArgs {
@@ -57,13 +57,17 @@ struct ConvArgs {
   int tiles_x, tiles_y;
 };
 
-template <int R, int N>
+// R output rows per tile, N output channels (MMA N), S pipeline stages; BRES: the whole weight
+// image (<= kBResStages stages, i.e. cin <= 64) is loaded once per CTA and stays in smem, so
+// only activations stream (the weights were ~40% of the L2->SM bytes of a 64->64 conv).
+template <int R, int N, int S = 2, bool BRES = false>
 struct Cfg {
   static constexpr int kABytes = kStageGroups * (R + 2) * kRowBytes;
   static constexpr int kBBytes = 9 * kStageGroups * N * 16;
   static constexpr int kPlaneBytes = (R + 2) * kRowBytes;
   static constexpr int kAcc = (2 * R * N <= 512) ? 2 : 1;
-  static constexpr int kSmem = kStages * (kABytes + kBBytes) + 1024 + 256;
+  static constexpr int kBSlots = BRES ? kBResStages : S;
+  static constexpr int kSmem = S * kABytes + kBSlots * kBBytes + 1024 + 256;
 };
 
 // All MMAs of one K-stage: R output rows x 9 taps x NK k-steps, offsets folded at compile time.
@@ -87,20 +91,21 @@ __device__ __forceinline__ void issue_stage(uint64_t a0, uint64_t b0, uint32_t d
   }
 }
 
-template <int R, int N>
+template <int R, int N, int kStages, bool BRES>
 __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
-  using C = Cfg<R, N>;
+  using C = Cfg<R, N, kStages, BRES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * C::kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * C::kBBytes);
-  // bars: full[kStages], empty[kStages], tfull[2], tempty[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::kBSlots * C::kBBytes);
+  // bars: full[kStages], empty[kStages], tfull[2], tempty[2], weights-resident
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
   const uint32_t bar_full = sm100::smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * kStages;
   const uint32_t bar_tfull = bar_empty + 8 * kStages;
   const uint32_t bar_tempty = bar_tfull + 16;
+  const uint32_t bar_bres = bar_tempty + 16;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       sm100::mbar_init(bar_tfull + 8 * s, 1);
       sm100::mbar_init(bar_tempty + 8 * s, 4);
     }
+    sm100::mbar_init(bar_bres, 1);
     sm100::fence_mbar_init();
   }
   if (warp == 1) sm100::tmem_alloc<512>(sm100::smem_u32(tmem_slot));
@@ -126,6 +132,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
 
   if (warp == 0) {
     // ---------------- producer ----------------
+    if (BRES && lane == 0) {
+      const uint32_t wb = (uint32_t)(a.n_kstages * C::kBBytes);
+      sm100::mbar_arrive_expect_tx(bar_bres, wb);
+      sm100::bulk_g2s(sm100::smem_u32(sB), a.wimg, wb, bar_bres);
+    }
     int it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int x0 = (tile % a.tiles_x) * kTileW;
@@ -152,11 +163,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         uint32_t tot = my_bytes;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        const uint32_t b_bytes = (uint32_t)(9 * gs_fill * N * 16);
+        const uint32_t b_bytes = BRES ? 0u : (uint32_t)(9 * gs_fill * N * 16);
         if (lane == 0) sm100::mbar_arrive_expect_tx(bar_full + 8 * st, tot + b_bytes);
         __syncwarp();
         const uint32_t a_st = sm100::smem_u32(sA + st * C::kABytes);
-        if (lane == 0)
+        if (!BRES && lane == 0)
           sm100::bulk_g2s(sm100::smem_u32(sB + st * C::kBBytes),
                           reinterpret_cast<const uint8_t*>(a.wimg) + (int64_t)ks * C::kBBytes,
                           b_bytes, bar_full + 8 * st);
@@ -189,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc = sm100::idesc_f16(128, N);
+    if (BRES) sm100::mbar_wait(bar_bres, 0);
     int it = 0, lt = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt % C::kAcc;
@@ -208,18 +220,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         // registers; elect.sync picks the one thread that issues each tcgen05.mma. Descriptors are
         // a base plus a 16-byte-unit offset in the start-address field.
         const uint64_t a0 = sm100::smem_desc(sm100::smem_u32(sA + st * C::kABytes), C::kPlaneBytes, 128);
-        const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + st * C::kBBytes), N * 16, 128);
+        const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + (BRES ? ks : st) * C::kBBytes), N * 16, 128);
+        (void)nk;  // one 16-channel MMA K-step per stage
         if (sm100::elect_one()) {
-          if (a.center_only) {
-            if (nk == 2)
-              issue_stage<R, N, 2, true>(a0, b0, d_base, idesc, ks == 0);
-            else
-              issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
-          } else if (nk == 2) {
-            issue_stage<R, N, 2>(a0, b0, d_base, idesc, ks == 0);
-          } else {
+          if (a.center_only)
+            issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
+          else
             issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
-          }
         }
         __syncwarp();
         sm100::mma_commit_elect(bar_empty + 8 * st);
@@ -367,12 +374,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   }
 }
 
-template <int R, int N>
+template <int R, int N, int S, bool BRES>
 int launch(fv_ctx* ctx, const ConvArgs& args) {
-  using C = Cfg<R, N>;
+  using C = Cfg<R, N, S, BRES>;
+  static_assert(C::kSmem <= 227 * 1024, "conv tile configuration exceeds shared memory");
   static bool attr_set = false;
   if (!attr_set) {
-    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::kSmem));
     attr_set = true;
   }
   ConvArgs a = args;
@@ -380,7 +389,7 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   a.tiles_y = (a.H + R - 1) / R;
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
-  conv3x3_tc_kernel<R, N><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
+  conv3x3_tc_kernel<R, N, S, BRES><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
   FV_CHECK_LAUNCH("conv3x3_tc_kernel");
   ctx->launches += 1;
   return 0;
@@ -469,14 +478,16 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
     a.center_only = aux->center_only ? 1 : 0;
     FV_REQUIRE(!(aux->kw[0] || aux->kw[1]) || cp.n_pad >= 32, "conv %s: logits need N >= 32", cp.name.c_str());
   }
+  // stage = 16 input channels; weights resident when they fit (<= 4 stages, i.e. cin <= 64)
+  const bool res = cp.n_stages <= kBResStages;
   switch (cp.n_pad) {
-    case 16: return launch<4, 16>(ctx, a);
-    case 32: return launch<4, 32>(ctx, a);
-    case 48: return launch<4, 48>(ctx, a);
-    case 64: return launch<4, 64>(ctx, a);
-    case 80: return launch<2, 80>(ctx, a);
-    case 96: return launch<2, 96>(ctx, a);
-    case 128: return launch<2, 128>(ctx, a);
+    case 16: return res ? launch<4, 16, 6, true>(ctx, a) : launch<4, 16, 6, false>(ctx, a);
+    case 32: return res ? launch<4, 32, 5, true>(ctx, a) : launch<4, 32, 5, false>(ctx, a);
+    case 48: return res ? launch<4, 48, 5, true>(ctx, a) : launch<4, 48, 4, false>(ctx, a);
+    case 64: return res ? launch<4, 64, 5, true>(ctx, a) : launch<4, 64, 4, false>(ctx, a);
+    case 80: return res ? launch<2, 80, 5, true>(ctx, a) : launch<2, 80, 4, false>(ctx, a);
+    case 96: return res ? launch<2, 96, 5, true>(ctx, a) : launch<2, 96, 4, false>(ctx, a);
+    case 128: return res ? launch<2, 128, 4, true>(ctx, a) : launch<2, 128, 4, false>(ctx, a);
     default:
       set_error("conv %s: unsupported output width %d", cp.name.c_str(), cp.cout);
       return FV_E_UNSUPPORTED;
