@@ -33,7 +33,8 @@ constexpr int kHaloW = kTileW + 2;   // 130
 constexpr int kRowBytes = kHaloW * 16;
 constexpr int kStageGroups = 2;      // channel groups (of 8) per K-stage = one MMA K of 16
 constexpr int kBResStages = 4;       // resident-weight kernels hold up to 4 stages (cin <= 64)
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;      // two epilogue warps per TMEM lane quarter
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 struct ConvArgs {
   const __half* src[3];
@@ -85,13 +86,48 @@ __device__ __forceinline__ void issue_stage(uint64_t a0, uint64_t b0, uint32_t d
         const uint64_t ad = a0 + (uint64_t)((2 * k * C::kPlaneBytes + ((r + t / 3) * kHaloW + t % 3) * 16) >> 4);
         const uint64_t bd = b0 + (uint64_t)(((t * NK + k) * N * 32) >> 4);
         const bool acc = !first_stage || (kCenter ? k != 0 : (t | k) != 0);
-        sm100::mma_f16(d_base + r * N, ad, bd, idesc, acc ? 1u : 0u);
+        sm100::mma_f16(d_base + (R - 1 - r) * N, ad, bd, idesc, acc ? 1u : 0u);
       }
     }
   }
 }
 
-template <int R, int N, int kStages, bool BRES>
+// Row-fused issue (3N <= 256). Input (halo) row h feeds output rows h-dy for dy = 0..2 through
+// the weights of tap (dy, dx). The B image stacks the three dy slices along N ([dx][kg][dy*N+n]),
+// and accumulator row r sits at column (R-1-r)*N, so ONE MMA of width (#dy)*N covers every output
+// row an (h, dx) pair feeds: the A tile (the shifted halo row) is read from shared memory once
+// instead of three times -- at N = 64 the A reads alone otherwise saturate the SM's operand
+// bandwidth (ncu: L1/TEX 86% busy, tensor pipe 57%). In the first K-stage the dy = 0 slice (the
+// row's first contribution) is issued separately without accumulate.
+template <int R, int N>
+__device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint32_t d_base, bool first_stage) {
+  using C = Cfg<R, N>;
+#pragma unroll
+  for (int h = 0; h < R + 2; ++h) {
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int dy_lo = h - R + 1 > 0 ? h - R + 1 : 0;
+    const int dy_hi = h < 2 ? h : 2;
+    const int r_first = h - dy_lo;
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      const uint64_t ad = a0 + (uint64_t)(((h * kHaloW + dx) * 16) >> 4);
+      const uint64_t bdx = b0 + (uint64_t)((dx * 2 * 3 * N * 16) >> 4);
+      const uint32_t d0 = d_base + (R - 1 - r_first) * N;
+      if (first_stage && dx == 0 && dy_lo == 0) {
+        // row h's first contribution (dy = 0): overwrite; the older rows accumulate
+        sm100::mma_f16(d0, ad, bdx, sm100::idesc_f16(128, N), 0u);
+        if (dy_hi >= 1)
+          sm100::mma_f16(d0 + N, ad, bdx + (uint64_t)((N * 16) >> 4), sm100::idesc_f16(128, dy_hi * N), 1u);
+      } else {
+        sm100::mma_f16(d0, ad, bdx + (uint64_t)((dy_lo * N * 16) >> 4),
+                       sm100::idesc_f16(128, (dy_hi - dy_lo + 1) * N), 1u);
+      }
+    }
+  }
+}
+
+template <int R, int N, int kStages, bool BRES, bool FUSED>
 __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   using C = Cfg<R, N, kStages, BRES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -117,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     }
     for (int s = 0; s < 2; ++s) {
       sm100::mbar_init(bar_tfull + 8 * s, 1);
-      sm100::mbar_init(bar_tempty + 8 * s, 4);
+      sm100::mbar_init(bar_tempty + 8 * s, kEpiWarps);
     }
     sm100::mbar_init(bar_bres, 1);
     sm100::fence_mbar_init();
@@ -220,13 +256,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         // registers; elect.sync picks the one thread that issues each tcgen05.mma. Descriptors are
         // a base plus a 16-byte-unit offset in the start-address field.
         const uint64_t a0 = sm100::smem_desc(sm100::smem_u32(sA + st * C::kABytes), C::kPlaneBytes, 128);
-        const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + (BRES ? ks : st) * C::kBBytes), N * 16, 128);
+        const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + (BRES ? ks : st) * C::kBBytes),
+                                             (FUSED && !a.center_only ? 3 : 1) * N * 16, 128);
         (void)nk;  // one 16-channel MMA K-step per stage
         if (sm100::elect_one()) {
           if (a.center_only)
             issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
           else
-            issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
+            FUSED ? issue_stage_rows<R, N>(a0, b0, d_base, ks == 0)
+                  : issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
         }
         __syncwarp();
         sm100::mma_commit_elect(bar_empty + 8 * st);
@@ -238,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   } else {
     // ---------------- epilogue ----------------
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int half = (warp - 2) >> 2;  // the two warps of a quarter split the tile's rows/columns
     int lt = 0;
     const int64_t plane = (int64_t)a.H * a.W * 8;
     const int Hp = a.H >> 1, Wp = a.W >> 1;
@@ -257,10 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         // next frame's feedback channels; logits -> max-subtracted softmax (autograd.py:188-199)
         // -> 9 fp32 filter-weight planes per K block.
         const int64_t hw = (int64_t)a.H * a.W;
-        for (int r = 0; r < R; ++r) {
+        for (int r = half; r < R; r += 2) {
           float v[N >= 32 ? 32 : 16];
-          sm100::tmem_ld16(t_row0 + r * N, *reinterpret_cast<float(*)[16]>(v));
-          if constexpr (N >= 32) sm100::tmem_ld16(t_row0 + r * N + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          sm100::tmem_ld16(t_row0 + (R - 1 - r) * N, *reinterpret_cast<float(*)[16]>(v));
+          if constexpr (N >= 32) sm100::tmem_ld16(t_row0 + (R - 1 - r) * N + 16, *reinterpret_cast<float(*)[16]>(v + 16));
           const int y = y0 + r;
           if (xin && y < a.H) {
             const int64_t pix = (int64_t)y * a.W + x;
@@ -302,13 +341,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
           }
         }
       } else {
-        for (int r = 0; r < R; r += 2) {
-          const int y = y0 + r;
+        constexpr int kCb = N / 16;
 #pragma unroll 1
-          for (int cb = 0; cb < N; cb += 16) {
+        for (int item = half; item < (R / 2) * kCb; item += 2) {
+          const int r = 2 * (item / kCb);
+          const int cb = 16 * (item % kCb);
+          const int y = y0 + r;
+          {
             float v0[16], v1[16];
-            sm100::tmem_ld16(t_row0 + r * N + cb, v0);
-            sm100::tmem_ld16(t_row0 + (r + 1) * N + cb, v1);
+            sm100::tmem_ld16(t_row0 + (R - 1 - r) * N + cb, v0);
+            sm100::tmem_ld16(t_row0 + (R - 2 - r) * N + cb, v1);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const float b = __ldg(a.bias + cb + j);
@@ -374,13 +416,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   }
 }
 
-template <int R, int N, int S, bool BRES>
+template <int R, int N, int S, bool BRES, bool FUSED>
 int launch(fv_ctx* ctx, const ConvArgs& args) {
   using C = Cfg<R, N, S, BRES>;
   static_assert(C::kSmem <= 227 * 1024, "conv tile configuration exceeds shared memory");
   static bool attr_set = false;
   if (!attr_set) {
-    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::kSmem));
     attr_set = true;
   }
@@ -389,7 +431,7 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   a.tiles_y = (a.H + R - 1) / R;
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
-  conv3x3_tc_kernel<R, N, S, BRES><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
+  conv3x3_tc_kernel<R, N, S, BRES, FUSED><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
   FV_CHECK_LAUNCH("conv3x3_tc_kernel");
   ctx->launches += 1;
   return 0;
@@ -397,10 +439,12 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
 
 }  // namespace
 
-// B image of stage s: [tap t (9)][k (g/2)][kg (2)][n (N)][8] fp16, c = (4s + 2k + kg)*8 + e.
+// B image of stage s (channels c = (2s + kg)*8 + e): [tap t (9)][kg (2)][n (N)][8] fp16, or for
+// row-fused convs [dx (3)][kg (2)][dy*N + n][8] (see issue_stage_rows).
 int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
   const int groups = (cp.cin + 7) / 8;
   const int N = cp.n_pad;
+  cp.row_fused = !cp.center_only && 3 * N <= 256;
   cp.n_stages = (groups + kStageGroups - 1) / kStageGroups;
   cp.stage_groups.clear();
   cp.stage_off.clear();
@@ -427,7 +471,10 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
               const int c = (s * kStageGroups + 2 * k + kg) * 8 + e;
               float w = 0.f;
               if (n < cp.cout && c < cp.cin) w = cp.w_host[((int64_t)n * cp.cin + c) * 9 + t];
-              base[((((int64_t)t * nk + k) * 2 + kg) * N + n) * 8 + e] = __float2half(w);
+              if (cp.row_fused)  // nk == 1
+                base[(((int64_t)(t % 3) * 2 + kg) * 3 * N + (t / 3) * N + n) * 8 + e] = __float2half(w);
+              else
+                base[((((int64_t)t * nk + k) * 2 + kg) * N + n) * 8 + e] = __float2half(w);
             }
   }
   if (cp.w_dev) cudaFree(cp.w_dev);
@@ -476,18 +523,28 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
       a.kcol[s] = aux->kcol[s];
     }
     a.center_only = aux->center_only ? 1 : 0;
+    FV_REQUIRE(aux->center_only == cp.center_only, "conv %s: 1x1 use needs a center-only weight image",
+               cp.name.c_str());
     FV_REQUIRE(!(aux->kw[0] || aux->kw[1]) || cp.n_pad >= 32, "conv %s: logits need N >= 32", cp.name.c_str());
   }
-  // stage = 16 input channels; weights resident when they fit (<= 4 stages, i.e. cin <= 64)
+  // stage = 16 input channels; weights resident when they fit (<= 4 stages, i.e. cin <= 64);
+  // row-fused MMAs whenever 3N <= 256 (the B image was laid out for it in conv_prepare)
   const bool res = cp.n_stages <= kBResStages;
+  const bool fu = cp.row_fused;
+#define FV_LAUNCH(R_, N_, S_) \
+  (res ? (fu ? launch<R_, N_, S_, true, true>(ctx, a) : launch<R_, N_, S_, true, false>(ctx, a)) \
+       : (fu ? launch<R_, N_, S_, false, true>(ctx, a) : launch<R_, N_, S_, false, false>(ctx, a)))
   switch (cp.n_pad) {
-    case 16: return res ? launch<4, 16, 6, true>(ctx, a) : launch<4, 16, 6, false>(ctx, a);
-    case 32: return res ? launch<4, 32, 5, true>(ctx, a) : launch<4, 32, 5, false>(ctx, a);
-    case 48: return res ? launch<4, 48, 5, true>(ctx, a) : launch<4, 48, 4, false>(ctx, a);
-    case 64: return res ? launch<4, 64, 5, true>(ctx, a) : launch<4, 64, 4, false>(ctx, a);
-    case 80: return res ? launch<2, 80, 5, true>(ctx, a) : launch<2, 80, 4, false>(ctx, a);
-    case 96: return res ? launch<2, 96, 5, true>(ctx, a) : launch<2, 96, 4, false>(ctx, a);
-    case 128: return res ? launch<2, 128, 4, true>(ctx, a) : launch<2, 128, 4, false>(ctx, a);
+    case 16: return FV_LAUNCH(4, 16, 6);
+    case 32: return FV_LAUNCH(4, 32, 5);
+    case 48: return FV_LAUNCH(4, 48, 4);
+    case 64: return res ? (fu ? launch<4, 64, 5, true, true>(ctx, a) : launch<4, 64, 5, true, false>(ctx, a))
+                        : (fu ? launch<4, 64, 4, false, true>(ctx, a) : launch<4, 64, 4, false, false>(ctx, a));
+    case 80: return res ? (fu ? launch<2, 80, 5, true, true>(ctx, a) : launch<2, 80, 5, true, false>(ctx, a))
+                        : (fu ? launch<2, 80, 4, false, true>(ctx, a) : launch<2, 80, 4, false, false>(ctx, a));
+    case 96: return res ? launch<2, 96, 5, true, false>(ctx, a) : launch<2, 96, 4, false, false>(ctx, a);
+    case 128: return res ? launch<2, 128, 4, true, false>(ctx, a) : launch<2, 128, 4, false, false>(ctx, a);
+#undef FV_LAUNCH
     default:
       set_error("conv %s: unsupported output width %d", cp.name.c_str(), cp.cout);
       return FV_E_UNSUPPORTED;

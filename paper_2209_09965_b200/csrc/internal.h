@@ -98,6 +98,8 @@ struct ConvParam {
   int64_t wbytes = 0;
   __half* w_dev = nullptr;  // implicit-GEMM B image (see conv_tc.cu)
   float* b_dev = nullptr;   // bias (n_pad) fp32
+  bool center_only = false;   // used as a 1x1 conv (K-stage logits at levels > 0)
+  bool row_fused = false;     // B image stacked by dy for row-fused MMAs (conv_tc.cu)
   std::vector<float> w_host;  // reference layout (oc,ic,kh,kw), fp16-rounded values
   std::vector<float> b_host;
   bool w_set = false, b_set = false;

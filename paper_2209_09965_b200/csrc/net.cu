@@ -108,6 +108,7 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
       ++s;
     }
     cp.w_set = cp.b_set = true;
+    cp.center_only = L > 0;
     const int rc = conv_prepare(ctx, cp);
     if (rc) return rc;
   }
