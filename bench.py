@@ -277,9 +277,19 @@ def run_ours(args, cfg):
     t_end.record(stream)
     torch.cuda.synchronize()
     serial_ms = max_over_ranks(t_start.elapsed_time(t_end), world, device="cuda")
+    st = ctx.stats()  # work counters of region 2 only
+    # --- timed region 3: the same frames again with CUDA events around every library launch
+    # (per-kernel-class launch durations for the roofline; kept out of regions 1 and 2) ---
+    ctx.set_kernel_timing(True)
+    for j in timed_frames:
+        pipe.mask(fovea, j)
+        pipe.march(cams[j % PATH_FRAMES])
+        pipe.reconstruct()
+    torch.cuda.synchronize()
+    kern = {name: ctx.kernel_time(cls) for name, cls in _lib.KERNEL_CLASSES.items()}
+    ctx.set_kernel_timing(False)
     elapsed_ms = pipe_ms
     clk = clocks.stop() if clocks else None
-    st = ctx.stats()
     mask_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in ev]))
     march_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in ev]))
     net_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
@@ -312,14 +322,33 @@ def run_ours(args, cfg):
                         "frac": net_tflops / tf_sus, "ms": net_ms},
         "mask": {"ms": mask_ms},
     }
-    dom = "march" if march_ms >= net_ms else "reconstruct"
+    # per-kernel-class launch time per frame (region 3)
+    kernels = {name: {"ms_per_frame": v[0] / k, "launches_per_frame": v[2] / k} for name, v in kern.items() if v[2]}
+    conv_ms, conv_flops, conv_n = kern["conv"]
+    conv_tf = conv_flops / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
+    kernels["conv"].update(bound="tensor", achieved=conv_tf, peak=tf_sus, unit="TFLOP/s", frac=conv_tf / tf_sus,
+                           flops_per_launch=conv_flops / max(conv_n, 1))
+    m_ms = sum(kern[c][0] for c in ("march_main", "march_shadow", "march_composite"))
+    m_gbs = (samples_per_frame * BYTES_PER_SAMPLE + rays_per_frame * 20) * k / (m_ms / 1e3) / 1e9 if m_ms > 0 else 0.0
+    marcher = {"bound": "hbm", "achieved": m_gbs, "peak": hbm, "unit": "GB/s", "frac": m_gbs / hbm,
+               "ms_per_frame": m_ms / k}
+    # dominant kernel = the class with the most launch time per frame: the tcgen05 conv engine
+    # (every D/K conv of the W-Net) or the three wavefront marcher passes taken together
+    dom = "conv" if conv_ms >= m_ms else "marcher"
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get(dom)
-    roof = {k2: v for k2, v in stages[dom].items() if k2 in ("bound", "achieved", "peak", "unit", "frac")}
-    roof.update(traffic=traffic, kernel=("march_kernel" if dom == "march" else "W-Net forward (tcgen05 convs)"),
-                peak_source=f"{src} ({'sustained' if dom == 'reconstruct' else 'copy'})")
+        traffic = json.loads(tp.read_text()).get(dom, {}).get("dram_bytes_per_launch")
+    if dom == "conv":
+        roof = {"bound": "tensor", "achieved": conv_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": conv_tf / tf_sus,
+                "traffic": traffic, "kernel": "conv3x3_tc_kernel (all W-Net convs of a frame)",
+                "launches_per_frame": conv_n / k,
+                "how": "sum of algorithmic conv FLOPs / sum of launch durations (CUDA events per launch)",
+                "peak_source": f"{src} (sustained dense fp16/bf16)"}
+    else:
+        roof = dict(marcher, traffic=traffic, kernel="march_wave_{main,shadow,composite}_kernel",
+                    how=f"({BYTES_PER_SAMPLE} B/sample + 20 B/ray) / summed launch durations",
+                    peak_source=f"{src} (copy bandwidth)")
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         sec, desc, threads = cpu_frame_estimate(cfg)
@@ -338,7 +367,7 @@ def run_ours(args, cfg):
                    "serial_fps": whole_job_rate(k, world, serial_ms / 1e3),
                    "how": "value = K frames pipelined over two streams (render t+1 || reconstruct t), "
                           "CUDA events on the pipeline stream; phase_ms from the same frames serialised"},
-        "roofline": roof, "stages": stages,
+        "roofline": roof, "stages": stages, "kernels": kernels, "marcher": marcher,
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": h * w * 3 * 4,
                 "how": "fv_frame C-ABI call per frame (camera/fovea by value, pinned host RGB out, sync)"},

@@ -117,6 +117,23 @@ FV_API int fv_stats_read(fv_ctx* ctx, fv_stats* out_host);
 FV_API int fv_stats_reset(fv_ctx* ctx);
 /* number of library kernels launched on this ctx since creation */
 FV_API uint64_t fv_launch_count(fv_ctx* ctx);
+/* Per-kernel-class device timing: while enabled, every library launch on the context's stream is
+ * bracketed by a pair of CUDA events; fv_ctx_kernel_time() synchronises on them and returns the
+ * summed launch durations (ms), the summed algorithmic work of the class (FLOPs for FV_KC_CONV,
+ * 0 elsewhere) and the launch count since timing was (re-)enabled. Costs an event pair per launch:
+ * for measurement runs, not for the headline timed region. */
+enum {
+  FV_KC_MASK = 0,            /* mask_compact / tau */
+  FV_KC_MARCH_MAIN = 1,      /* primary-ray march (wavefront main pass, or the fused single-pass tiers) */
+  FV_KC_MARCH_SHADOW = 2,    /* wavefront shadow pass */
+  FV_KC_MARCH_COMPOSITE = 3, /* wavefront composite pass */
+  FV_KC_CONV = 4,            /* tcgen05 implicit-GEMM convolutions (W-Net D and K stages) */
+  FV_KC_NETOPS = 5,          /* upsample / K filter application / pack / finalize */
+  FV_KC_OTHER = 6,           /* volume bricking, procedural volumes */
+  FV_KC_COUNT = 7
+};
+FV_API int fv_ctx_set_kernel_timing(fv_ctx* ctx, int enable);
+FV_API int fv_ctx_kernel_time(fv_ctx* ctx, int kernel_class, double* ms, double* work, uint64_t* launches);
 
 /* ---- foveated mask + compaction (device outputs) ------------------------ */
 /* pb_map_dev: nullable (H,W) float64 per-pixel base density; bits_dev: nullable (H,W) uint8;

@@ -20,6 +20,12 @@ FV_E_NOMEM = -3
 FV_E_STATE = -4
 FV_E_UNSUPPORTED = -5
 
+# kernel classes of fv_ctx_kernel_time (include/fovnet.h)
+FV_KC_MASK, FV_KC_MARCH_MAIN, FV_KC_MARCH_SHADOW, FV_KC_MARCH_COMPOSITE, FV_KC_CONV, FV_KC_NETOPS, FV_KC_OTHER = range(7)
+KERNEL_CLASSES = {"mask": FV_KC_MASK, "march_main": FV_KC_MARCH_MAIN, "march_shadow": FV_KC_MARCH_SHADOW,
+                  "march_composite": FV_KC_MARCH_COMPOSITE, "conv": FV_KC_CONV, "netops": FV_KC_NETOPS,
+                  "other": FV_KC_OTHER}
+
 LIGHT_NONE, LIGHT_DIRECTIONAL, LIGHT_POINT = 0, 1, 2
 PREC_FP32, PREC_FP64 = 0, 1
 
@@ -68,6 +74,8 @@ _SIGS = {
     "fv_stats_read": (I, [P, C.POINTER(FvStats)]),
     "fv_stats_reset": (I, [P]),
     "fv_launch_count": (C.c_uint64, [P]),
+    "fv_ctx_set_kernel_timing": (I, [P, I]),
+    "fv_ctx_kernel_time": (I, [P, I, C.POINTER(D), C.POINTER(D), C.POINTER(C.c_uint64)]),
     "fv_mask_compact": (I, [P, I, I, I, C.POINTER(FvFovea), P, P, P, P, P]),
     "fv_mask_compact_tau": (I, [P, I, I, I, P, P, P, P, P]),
     "fv_tau_map": (I, [P, I, I, C.POINTER(FvFovea), P, P]),
@@ -176,6 +184,16 @@ class Context:
 
     def reset_stats(self) -> None:
         check(self.lib.fv_stats_reset(self.h))
+
+    def set_kernel_timing(self, enable: bool) -> None:
+        """Bracket every library launch with CUDA events (totals reset on each call)."""
+        check(self.lib.fv_ctx_set_kernel_timing(self.h, 1 if enable else 0))
+
+    def kernel_time(self, kernel_class: int) -> tuple[float, float, int]:
+        """(summed launch ms, summed algorithmic work, launches) of one FV_KC_* class."""
+        ms, work, n = C.c_double(), C.c_double(), C.c_uint64()
+        check(self.lib.fv_ctx_kernel_time(self.h, kernel_class, C.byref(ms), C.byref(work), C.byref(n)))
+        return ms.value, work.value, int(n.value)
 
     def ensure_noise(self, stack) -> None:
         """Upload a NoiseStack once per context (keyed by object identity + shape)."""

@@ -28,6 +28,34 @@ int pack_input(fv_ctx* ctx, fv_state* st, const float* rgba, const uint8_t* bits
 
 using namespace fv;
 
+namespace fv {
+static cudaEvent_t kpool_get(fv_ctx* ctx) {
+  if (ctx->kpool.empty()) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+  }
+  cudaEvent_t e = ctx->kpool.back();
+  ctx->kpool.pop_back();
+  return e;
+}
+
+void ktime_begin(fv_ctx* ctx) {
+  if (!ctx->ktiming) return;
+  if (!ctx->kopen) ctx->kopen = kpool_get(ctx);
+  if (ctx->kopen) cudaEventRecord(ctx->kopen, ctx->stream);
+}
+
+void ktime_end(fv_ctx* ctx, int cls, double work) {
+  if (!ctx->ktiming || !ctx->kopen) return;
+  cudaEvent_t b = kpool_get(ctx);
+  if (!b) return;
+  cudaEventRecord(b, ctx->stream);
+  ctx->kspans.push_back({ctx->kopen, b, cls, work});
+  ctx->kopen = nullptr;
+}
+}  // namespace fv
+
 extern "C" {
 
 const char* fv_last_error(void) { return g_err; }
@@ -66,6 +94,9 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   if (ctx->idx_scratch) cudaFree(ctx->idx_scratch);
   if (ctx->rgb_scratch) cudaFree(ctx->rgb_scratch);
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
+  for (auto& sp : ctx->kspans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
+  for (auto& ev : ctx->kpool) cudaEventDestroy(ev);
+  if (ctx->kopen) cudaEventDestroy(ctx->kopen);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;
@@ -92,6 +123,43 @@ int fv_sync(fv_ctx* ctx) {
 }
 
 uint64_t fv_launch_count(fv_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int fv_ctx_set_kernel_timing(fv_ctx* ctx, int enable) {
+  FV_REQUIRE(ctx, "null context");
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (auto& sp : ctx->kspans) {
+    ctx->kpool.push_back(sp.a);
+    ctx->kpool.push_back(sp.b);
+  }
+  ctx->kspans.clear();
+  for (int c = 0; c < FV_KC_COUNT; ++c) {
+    ctx->k_ms[c] = ctx->k_work[c] = 0.0;
+    ctx->k_n[c] = 0;
+  }
+  ctx->ktiming = enable != 0;
+  return 0;
+}
+
+int fv_ctx_kernel_time(fv_ctx* ctx, int cls, double* ms, double* work, uint64_t* launches) {
+  FV_REQUIRE(ctx, "null context");
+  FV_REQUIRE(cls >= 0 && cls < FV_KC_COUNT, "kernel class %d out of range", cls);
+  // fold the pending spans into the totals
+  for (auto& sp : ctx->kspans) {
+    FV_CUDA(cudaEventSynchronize(sp.b));
+    float t = 0.f;
+    FV_CUDA(cudaEventElapsedTime(&t, sp.a, sp.b));
+    ctx->k_ms[sp.cls] += t;
+    ctx->k_work[sp.cls] += sp.work;
+    ctx->k_n[sp.cls] += 1;
+    ctx->kpool.push_back(sp.a);
+    ctx->kpool.push_back(sp.b);
+  }
+  ctx->kspans.clear();
+  if (ms) *ms = ctx->k_ms[cls];
+  if (work) *work = ctx->k_work[cls];
+  if (launches) *launches = ctx->k_n[cls];
+  return 0;
+}
 
 int fv_noise_upload(fv_ctx* ctx, const float* vals, int T, int H, int W) {
   FV_REQUIRE(ctx && vals, "null argument");

@@ -56,6 +56,7 @@ struct ConvArgs {
   int kcol[2];         // first logit column of each K block
   int center_only;     // 1x1 conv: only the centre tap's MMAs are issued
   int tiles_x, tiles_y;
+  double flops;        // host-side: algorithmic FLOPs of the launch (kernel timing)
 };
 
 // R output rows per tile, N output channels (MMA N), S pipeline stages; BRES: the whole weight
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
 #pragma unroll
               for (int s = 0; s < 2; ++s) {
                 if (!a.kw[s]) continue;
-                const int c0 = a.kcol[s];
+                const int c0 = logit_col(s);  // compile-time: keeps v[] in registers
                 float l[9], m = -INFINITY;
 #pragma unroll
                 for (int j = 0; j < 9; ++j) {
@@ -331,11 +332,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
                 float sum = 0.f;
 #pragma unroll
                 for (int j = 0; j < 9; ++j) {
-                  l[j] = expf(l[j] - m);
+                  l[j] = __expf(l[j] - m);  // arguments <= 0: ex2.approx, rel. error ~1e-7
                   sum += l[j];
                 }
+                const float inv = __frcp_rn(sum);
 #pragma unroll
-                for (int j = 0; j < 9; ++j) a.kw[s][j * hw + pix] = l[j] / sum;
+                for (int j = 0; j < 9; ++j) a.kw[s][j * hw + pix] = l[j] * inv;
               }
             }
           }
@@ -431,7 +433,9 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   a.tiles_y = (a.H + R - 1) / R;
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
+  ktime_begin(ctx);
   conv3x3_tc_kernel<R, N, S, BRES, FUSED><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
+  ktime_end(ctx, FV_KC_CONV, a.flops);
   FV_CHECK_LAUNCH("conv3x3_tc_kernel");
   ctx->launches += 1;
   return 0;
@@ -514,6 +518,8 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   a.dst = dst ? dst->p : nullptr;
   a.pool_dst = pool_dst ? pool_dst->p : nullptr;
   a.relu = relu ? 1 : 0;
+  a.flops = 2.0 * a.H * a.W *
+            (cp.macs_per_px > 0 ? cp.macs_per_px : (double)cp.cin * cp.cout * cp.ksize * cp.ksize);
   if (aux) {
     a.head = 1;
     a.od = aux->od;
@@ -523,6 +529,8 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
       a.kcol[s] = aux->kcol[s];
     }
     a.center_only = aux->center_only ? 1 : 0;
+    FV_REQUIRE((!aux->kw[0] || aux->kcol[0] == kLogitCol[0]) && (!aux->kw[1] || aux->kcol[1] == kLogitCol[1]),
+               "conv %s: K-stage logits must sit at columns %d and %d", cp.name.c_str(), kLogitCol[0], kLogitCol[1]);
     FV_REQUIRE(aux->center_only == cp.center_only, "conv %s: 1x1 use needs a center-only weight image",
                cp.name.c_str());
     FV_REQUIRE(!(aux->kw[0] || aux->kw[1]) || cp.n_pad >= 32, "conv %s: logits need N >= 32", cp.name.c_str());

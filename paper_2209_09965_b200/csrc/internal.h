@@ -44,6 +44,22 @@ struct DevCounters {
   unsigned int pad[4];
 };
 
+// Per-launch timing spans (fv_ctx_set_kernel_timing).
+struct KSpan {
+  cudaEvent_t a, b;
+  int cls;
+  double work;
+};
+void ktime_begin(fv_ctx* ctx);
+void ktime_end(fv_ctx* ctx, int cls, double work = 0.0);
+// Launch statement bracketed by the context's kernel-timing events (no-ops unless enabled).
+#define FV_TIMED(ctx_, cls_, ...)     \
+  do {                                \
+    fv::ktime_begin(ctx_);            \
+    __VA_ARGS__;                      \
+    fv::ktime_end(ctx_, cls_);        \
+  } while (0)
+
 }  // namespace fv
 
 struct fv_ctx {
@@ -71,6 +87,13 @@ struct fv_ctx {
   void* wave_ray = nullptr;   // int4 per compacted ray
   int64_t wave_ray_cap = 0;
   unsigned long long launches = 0;
+  // kernel timing (off by default)
+  bool ktiming = false;
+  cudaEvent_t kopen = nullptr;
+  std::vector<cudaEvent_t> kpool;
+  std::vector<fv::KSpan> kspans;
+  double k_ms[FV_KC_COUNT] = {}, k_work[FV_KC_COUNT] = {};
+  uint64_t k_n[FV_KC_COUNT] = {};
 };
 
 struct fv_volume {
@@ -100,6 +123,7 @@ struct ConvParam {
   float* b_dev = nullptr;   // bias (n_pad) fp32
   bool center_only = false;   // used as a 1x1 conv (K-stage logits at levels > 0)
   bool row_fused = false;     // B image stacked by dy for row-fused MMAs (conv_tc.cu)
+  double macs_per_px = 0;     // algorithmic MACs per output pixel (0: cin * cout * ksize^2)
   std::vector<float> w_host;  // reference layout (oc,ic,kh,kw), fp16-rounded values
   std::vector<float> b_host;
   bool w_set = false, b_set = false;
@@ -109,6 +133,10 @@ struct ConvParam {
 
 namespace fv {
 // Auxiliary epilogue of a conv: D.head outputs and/or K-stage logits -> softmax filter weights.
+// First logit column of the s-th K block in a K-stage conv (columns 0..2 = D.head); the conv
+// epilogue indexes its TMEM registers with these, so they are compile-time constants.
+constexpr int kLogitCol[2] = {4, 13};
+__host__ __device__ constexpr int logit_col(int s) { return s == 0 ? 4 : 13; }
 struct ConvAux {
   float* od = nullptr;         // (3,H,W) fp32, columns 0..2
   __half* feedback = nullptr;  // NHWC8 input channels 5..7

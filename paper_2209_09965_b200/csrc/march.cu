@@ -1227,8 +1227,8 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
   FV_REQUIRE(n < (1ll << 31), "volume too large for 32-bit brick addressing");
   if (!vol->bricks) FV_CUDA(cudaMalloc(&vol->bricks, sizeof(float4) * n));
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
-  brick_kernel<<<blocks, 256, 0, ctx->stream>>>(vol->data, reinterpret_cast<float4*>(vol->bricks), vol->nx,
-                                                vol->ny, vol->nz, nbx, nby, nbz);
+  FV_TIMED(ctx, FV_KC_OTHER, brick_kernel<<<blocks, 256, 0, ctx->stream>>>(vol->data, reinterpret_cast<float4*>(vol->bricks), vol->nx,
+                                                vol->ny, vol->nz, nbx, nby, nbz));
   FV_CHECK_LAUNCH("brick_kernel");
   ctx->launches += 1;
   vol->bricks_version = vol->version;
@@ -1299,7 +1299,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
   const int threads = 128;
   const int blocks = (k_max + threads - 1) / threads;
   if (s->precision == FV_PREC_FP64) {
-    march_kernel<double><<<blocks, threads, 0, ctx->stream>>>(P);
+    FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_kernel<double><<<blocks, threads, 0, ctx->stream>>>(P));
   } else {
     fv_volume* mv = const_cast<fv_volume*>(vol);  // the brick copy is a cache of the grid
     int rc = volume_bricks(ctx, mv);
@@ -1376,16 +1376,16 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 3 * sizeof(unsigned int), ctx->stream));
       const int mgrid = std::min(blocks, ctx->num_sms * per_sm_main);
       if (main_u == 8)
-        march_wave_main_kernel<8><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next);
+        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<8><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
       else
-        march_wave_main_kernel<4><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next);
+        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<4><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
       if (P.light_kind != FV_LIGHT_NONE) {
-        march_wave_shadow_kernel<<<ctx->num_sms * per_sm_sh, threads, 0, ctx->stream>>>(F, B);
-        march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B);
+        FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<<<ctx->num_sms * per_sm_sh, threads, 0, ctx->stream>>>(F, B));
+        FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;
       }
     } else if (variant == 2) {
-      march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F);
+      FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F));
     } else {
       static int per_sm[2] = {0, 0};
       if (!per_sm[variant]) {
@@ -1398,9 +1398,9 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       const int pgrid = std::min(blocks, ctx->num_sms * per_sm[variant]);
       FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, sizeof(unsigned int), ctx->stream));
       if (variant == 1)
-        march_persist_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next);
+        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_persist_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next));
       else
-        march_refill_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next);
+        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_refill_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next));
     }
   }
   FV_CHECK_LAUNCH("march_kernel");

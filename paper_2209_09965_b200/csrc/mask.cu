@@ -187,7 +187,7 @@ int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
   p.epoch = ctx->epoch;
   p.tile_counter = &ctx->counters->scan_tile;
   FV_CUDA(cudaMemsetAsync(&ctx->counters->scan_tile, 0, sizeof(unsigned int), ctx->stream));
-  mask_compact_kernel<<<ntiles, kThreads, 0, ctx->stream>>>(p);
+  FV_TIMED(ctx, FV_KC_MASK, mask_compact_kernel<<<ntiles, kThreads, 0, ctx->stream>>>(p));
   FV_CHECK_LAUNCH("mask_compact_kernel");
   ctx->launches += 1;
   return 0;
@@ -197,7 +197,7 @@ int launch_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* p
                    double* tau) {
   MaskParams p = make_params(ctx, 0, H, W, f, pb_map);
   const int64_t n = (int64_t)H * W;
-  tau_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(p, tau);
+  FV_TIMED(ctx, FV_KC_MASK, tau_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(p, tau));
   FV_CHECK_LAUNCH("tau_kernel");
   ctx->launches += 1;
   return 0;

@@ -22,7 +22,6 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
             fv_act* pool_dst, bool relu, const ConvAux* aux);
 int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out);
 int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w);
-constexpr int kLogitCol[2] = {4, 13};
 int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out);
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in);
 int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw);
@@ -109,6 +108,7 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
     }
     cp.w_set = cp.b_set = true;
     cp.center_only = L > 0;
+    cp.macs_per_px = (L == 0 ? 27.0 * cin : 0.0) + 9.0 * cin * s;  // D.head 3x3 + s 1x1 logit convs
     const int rc = conv_prepare(ctx, cp);
     if (rc) return rc;
   }

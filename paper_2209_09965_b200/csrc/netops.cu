@@ -231,7 +231,7 @@ inline int grid_for(fv_ctx* ctx, int64_t n, int threads = 256) {
 
 int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
   const dim3 grid((in.W + 127) / 128, in.H, in.C / 8);
-  upsample2_nc8_kernel<<<grid, 128, 0, ctx->stream>>>(in.p, out.p, in.H, in.W);
+  FV_TIMED(ctx, FV_KC_NETOPS, upsample2_nc8_kernel<<<grid, 128, 0, ctx->stream>>>(in.p, out.p, in.H, in.W));
   FV_CHECK_LAUNCH("upsample2_nc8_kernel");
   ctx->launches += 1;
   return 0;
@@ -239,21 +239,21 @@ int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
 
 int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w) {
   const dim3 g((w + 127) / 128, h);
-  kapply_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w);
+  FV_TIMED(ctx, FV_KC_NETOPS, kapply_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
   FV_CHECK_LAUNCH("kapply_kernel");
   ctx->launches += 1;
   return 0;
 }
 
 int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out) {
-  pool3_kernel<<<dim3((w_out + 127) / 128, h_out, 3), 128, 0, ctx->stream>>>(in, out, h_out, w_out);
+  FV_TIMED(ctx, FV_KC_NETOPS, pool3_kernel<<<dim3((w_out + 127) / 128, h_out, 3), 128, 0, ctx->stream>>>(in, out, h_out, w_out));
   FV_CHECK_LAUNCH("pool3_kernel");
   ctx->launches += 1;
   return 0;
 }
 
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in) {
-  up3_kernel<<<dim3((w_in + 127) / 128, h_in, 3), 128, 0, ctx->stream>>>(in, out, h_in, w_in);
+  FV_TIMED(ctx, FV_KC_NETOPS, up3_kernel<<<dim3((w_in + 127) / 128, h_in, 3), 128, 0, ctx->stream>>>(in, out, h_in, w_in));
   FV_CHECK_LAUNCH("up3_kernel");
   ctx->launches += 1;
   return 0;
@@ -261,7 +261,7 @@ int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in) {
 
 int pack_input(fv_ctx* ctx, fv_state* st, const float* rgba, const uint8_t* bits) {
   const int64_t n = (int64_t)st->H * st->W;
-  pack_input_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(rgba, bits, st->x.p, st->H, st->W, st->Wp);
+  FV_TIMED(ctx, FV_KC_NETOPS, pack_input_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(rgba, bits, st->x.p, st->H, st->W, st->Wp));
   FV_CHECK_LAUNCH("pack_input_kernel");
   ctx->launches += 1;
   return 0;
@@ -269,7 +269,7 @@ int pack_input(fv_ctx* ctx, fv_state* st, const float* rgba, const uint8_t* bits
 
 int set_input(fv_ctx* ctx, fv_state* st, const float* xin, int C) {
   const int64_t n = (int64_t)st->H * st->W;
-  set_input_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(xin, C, st->x.p, st->H, st->W, st->Wp);
+  FV_TIMED(ctx, FV_KC_NETOPS, set_input_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(xin, C, st->x.p, st->H, st->W, st->Wp));
   FV_CHECK_LAUNCH("set_input_kernel");
   ctx->launches += 1;
   return 0;
@@ -277,8 +277,8 @@ int set_input(fv_ctx* ctx, fv_state* st, const float* xin, int C) {
 
 int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw) {
   const int64_t n = (int64_t)st->H * st->W;
-  finalize_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(img, st->od, st->H, st->W, st->Hp, st->Wp,
-                                                              rgb, o_raw, od_raw);
+  FV_TIMED(ctx, FV_KC_NETOPS, finalize_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(img, st->od, st->H, st->W, st->Hp, st->Wp,
+                                                              rgb, o_raw, od_raw));
   FV_CHECK_LAUNCH("finalize_kernel");
   ctx->launches += 1;
   return 0;
@@ -286,7 +286,7 @@ int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_r
 
 int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out) {
   const int64_t n = (int64_t)a.C * a.H * a.W;
-  nc8_to_nchw_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(a.p, out, a.C, a.H, a.W);
+  FV_TIMED(ctx, FV_KC_NETOPS, nc8_to_nchw_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(a.p, out, a.C, a.H, a.W));
   FV_CHECK_LAUNCH("nc8_to_nchw_kernel");
   ctx->launches += 1;
   return 0;
@@ -294,7 +294,7 @@ int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out) {
 
 int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a) {
   const int64_t n = (int64_t)a.C * a.H * a.W;
-  nchw_to_nc8_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(in, a.p, a.C, a.H, a.W);
+  FV_TIMED(ctx, FV_KC_NETOPS, nchw_to_nc8_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(in, a.p, a.C, a.H, a.W));
   FV_CHECK_LAUNCH("nchw_to_nc8_kernel");
   ctx->launches += 1;
   return 0;
@@ -302,7 +302,7 @@ int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a) {
 
 int od_to_feedback(fv_ctx* ctx, fv_state* st) {
   const int64_t n = (int64_t)st->Hp * st->Wp;
-  od_to_feedback_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(st->od, st->x.p, st->Hp, st->Wp);
+  FV_TIMED(ctx, FV_KC_NETOPS, od_to_feedback_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(st->od, st->x.p, st->Hp, st->Wp));
   FV_CHECK_LAUNCH("od_to_feedback_kernel");
   ctx->launches += 1;
   return 0;

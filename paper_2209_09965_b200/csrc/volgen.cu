@@ -92,9 +92,9 @@ int launch_volume_procedural(fv_ctx* ctx, fv_volume* vol, int kind, double* rang
   const int blocks = ctx->num_sms * 8;
   double* tmp = nullptr;
   FV_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (2 * blocks + 2), ctx->stream));
-  minmax_kernel<<<blocks, 256, 0, ctx->stream>>>(kind, vol->nx, vol->ny, vol->nz, tmp + 2);
-  minmax_final<<<1, 32, 0, ctx->stream>>>(tmp + 2, blocks, tmp);
-  normalize_kernel<<<blocks, 256, 0, ctx->stream>>>(kind, vol->nx, vol->ny, vol->nz, tmp, vol->data);
+  FV_TIMED(ctx, FV_KC_OTHER, minmax_kernel<<<blocks, 256, 0, ctx->stream>>>(kind, vol->nx, vol->ny, vol->nz, tmp + 2));
+  FV_TIMED(ctx, FV_KC_OTHER, minmax_final<<<1, 32, 0, ctx->stream>>>(tmp + 2, blocks, tmp));
+  FV_TIMED(ctx, FV_KC_OTHER, normalize_kernel<<<blocks, 256, 0, ctx->stream>>>(kind, vol->nx, vol->ny, vol->nz, tmp, vol->data));
   FV_CHECK_LAUNCH("procedural volume kernels");
   ctx->launches += 3;
   double r[2];

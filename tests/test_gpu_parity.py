@@ -382,3 +382,33 @@ def test_pipelined_frames_equal_serial_frames(stack):
         pipe.run_pipelined(frames[i:i + 1])
         torch.cuda.synchronize()
         assert torch.equal(pipe.rgb, outs[i]), i
+
+
+def test_kernel_timing_counts_algorithmic_conv_flops(stack):
+    """Per-launch kernel timing: the conv class sums exactly 2 x 275,071.5 MAC/pixel (SURVEY 8(a)
+    a20) over one FULL_BLOCKS frame, every class has positive time, and timing leaves frames unchanged."""
+    from paper_2209_09965_b200 import _lib
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    h, w = 184, 320
+    spec = ExperimentSpec(mode="hifi", width=w, height=h)
+    scene = default_scene("sphere_shells", (96, 96, 96))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, w, h)
+    pipe = FramePipeline(scene, net, (h, w), stack)
+    pipe.step(cams[0], spec.fovea(), 0)
+    ref = pipe.rgb.clone()
+    pipe.reset()
+    pipe.ctx.set_kernel_timing(True)
+    pipe.step(cams[0], spec.fovea(), 0)
+    torch.cuda.synchronize()
+    t = {k: pipe.ctx.kernel_time(c) for k, c in _lib.KERNEL_CLASSES.items()}
+    pipe.ctx.set_kernel_timing(False)
+    assert torch.equal(pipe.rgb, ref)
+    ms, flops, n = t["conv"]
+    assert n == 14 + 4 and ms > 0  # 7 blocks x 2 convs + one K-stage conv per level
+    assert flops == pytest.approx(2 * 275071.5 * h * w, rel=1e-12)
+    for k in ("mask", "march_main", "march_shadow", "march_composite", "netops"):
+        assert t[k][2] >= 1 and t[k][0] > 0, k
