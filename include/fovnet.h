@@ -220,6 +220,15 @@ FV_API int fv_debug_conv3x3(fv_ctx* ctx, int cin, int cout, int H, int W, const 
                             void* pool_nc8, int relu);
 
 /* ---- whole frame ---------------------------------------------------------- */
+/* A camera path of n frames (bench.cmd_bench_throughput's loop, bench.py:194-209) with host
+ * outputs: frame t+1's mask + march run on a second stream while frame t reconstructs, and frame
+ * t's image is copied into host_rgb_out[t] on a third stream while later frames compute. Every
+ * frame equals the corresponding fv_frame call. cams, foveas, frame_ids: n entries each;
+ * host_rgb_out: n pointers to (H,W,3) f32 host buffers (pinned for overlap; entries may repeat
+ * when the caller only needs the last image). Returns once every copy has landed. */
+FV_API int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, int n,
+                     const fv_camera* cams, const fv_light* light, const fv_settings* settings,
+                     const fv_fovea* foveas, const int* frame_ids, float* const* host_rgb_out);
 /* mask -> compact -> march -> reconstruct for one frame; host_rgb_out (H,W,3) f32 host (pinned
  * recommended) receives the clipped image; the copy is synchronous. timings_ms (nullable, 4
  * doubles) receives mask/render/reconstruct/total device times from CUDA events. */

@@ -106,6 +106,8 @@ _SIGS = {
     "fv_debug_conv3x3": (I, [P, I, I, I, I, P, P, P, P, P, I]),
     "fv_frame": (I, [P, P, P, P, C.POINTER(FvCamera), C.POINTER(FvLight), C.POINTER(FvSettings),
                      C.POINTER(FvFovea), I, P, C.POINTER(D)]),
+    "fv_frames": (I, [P, P, P, P, I, C.POINTER(FvCamera), C.POINTER(FvLight), C.POINTER(FvSettings),
+                      C.POINTER(FvFovea), C.POINTER(I), C.POINTER(P)]),
 }
 
 EXPORTED = tuple(_SIGS)

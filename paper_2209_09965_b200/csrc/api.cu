@@ -97,6 +97,8 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   for (auto& sp : ctx->kspans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
   for (auto& ev : ctx->kpool) cudaEventDestroy(ev);
   if (ctx->kopen) cudaEventDestroy(ctx->kopen);
+  for (auto& e : ctx->fev) if (e) cudaEventDestroy(e);
+  for (auto& s : ctx->fstream) if (s) cudaStreamDestroy(s);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;
@@ -402,6 +404,94 @@ int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st,
     cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
     timings_ms[0] = a; timings_ms[1] = b; timings_ms[2] = c; timings_ms[3] = a + b + c;
   }
+  return 0;
+}
+
+// A path of frames with host outputs, pipelined over three streams:
+//   render stream : mask + compaction + march of frame t (waits for frame t-2's network, the last
+//                   reader of the input buffer it overwrites -- the state alternates two buffers)
+//   network stream: reconstruction of frame t into device image t%2 (waits for render t and for
+//                   the copy of frame t-2, the last reader of that image)
+//   copy stream   : device image t%2 -> host_rgb_out[t]
+// The host enqueues in frame order, so every kernel sees exactly the buffers fv_frame would.
+int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, int n,
+              const fv_camera* cams, const fv_light* light, const fv_settings* settings,
+              const fv_fovea* foveas, const int* frame_ids, float* const* host_rgb_out) {
+  FV_REQUIRE(ctx && vol && net && st && cams && settings && foveas && frame_ids && host_rgb_out,
+             "null argument");
+  FV_REQUIRE(n >= 0, "frame count must be >= 0 (got %d)", n);
+  if (n == 0) return 0;
+  const int H = st->H, W = st->W;
+  for (int t = 0; t < n; ++t) {
+    FV_REQUIRE(host_rgb_out[t], "host_rgb_out[%d] is null", t);
+    if (cams[t].height != H || cams[t].width != W) {
+      set_error("carried state is for (%d, %d), input is (%d, %d); reset the state", H, W, cams[t].height,
+                cams[t].width);
+      return FV_E_STATE;
+    }
+    const int rc = check_fovea(&foveas[t]);
+    if (rc) return rc;
+  }
+  const int64_t npix = (int64_t)H * W;
+  if (npix > ctx->idx_cap) {
+    if (ctx->idx_scratch) cudaFree(ctx->idx_scratch);
+    ctx->idx_scratch = nullptr;
+    FV_CUDA(cudaMalloc(&ctx->idx_scratch, sizeof(int32_t) * npix));
+    ctx->idx_cap = npix;
+  }
+  if (!ctx->k_scratch) FV_CUDA(cudaMalloc(&ctx->k_scratch, sizeof(int32_t) * 4));
+  if (6 * npix > ctx->rgb_cap) {
+    if (ctx->rgb_scratch) cudaFree(ctx->rgb_scratch);
+    ctx->rgb_scratch = nullptr;
+    FV_CUDA(cudaMalloc(&ctx->rgb_scratch, sizeof(float) * 6 * npix));
+    ctx->rgb_cap = 6 * npix;
+  }
+  for (auto& s : ctx->fstream)
+    if (!s) FV_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  for (auto& e : ctx->fev)
+    if (!e) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaStream_t s_r = ctx->fstream[0], s_n = ctx->fstream[1], s_c = ctx->fstream[2];
+  cudaEvent_t* rendered = ctx->fev;      // [2]
+  cudaEvent_t* net_done = ctx->fev + 2;  // [2]
+  cudaEvent_t* copied = ctx->fev + 4;    // [2]
+  cudaEvent_t start = ctx->fev[6];
+  const cudaStream_t own = ctx->stream;
+  FV_CUDA(cudaEventRecord(start, own));
+  for (cudaStream_t s : {s_r, s_n, s_c}) FV_CUDA(cudaStreamWaitEvent(s, start, 0));
+  int rc = 0;
+  for (int t = 0; t < n && !rc; ++t) {
+    const int b = t & 1;
+    float* img = ctx->rgb_scratch + (int64_t)b * 3 * npix;
+    // render
+    if (t >= 2) FV_CUDA(cudaStreamWaitEvent(s_r, net_done[b], 0));
+    ctx->stream = s_r;
+    rc = launch_mask_compact(ctx, frame_ids[t], H, W, &foveas[t], nullptr, nullptr, ctx->idx_scratch,
+                             ctx->k_scratch, st->x.p, st->Wp);
+    if (!rc)
+      rc = launch_render(ctx, vol, &cams[t], light, settings, ctx->idx_scratch, ctx->k_scratch, (int)npix,
+                         nullptr, nullptr, st->x.p, st->Wp);
+    if (rc) break;
+    FV_CUDA(cudaEventRecord(rendered[b], s_r));
+    // network
+    FV_CUDA(cudaStreamWaitEvent(s_n, rendered[b], 0));
+    if (t >= 2) FV_CUDA(cudaStreamWaitEvent(s_n, copied[b], 0));
+    ctx->stream = s_n;
+    rc = reconstruct(ctx, net, st, 1, img, nullptr, nullptr);
+    if (rc) break;
+    FV_CUDA(cudaEventRecord(net_done[b], s_n));
+    // copy out
+    FV_CUDA(cudaStreamWaitEvent(s_c, net_done[b], 0));
+    FV_CUDA(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, s_c));
+    FV_CUDA(cudaEventRecord(copied[b], s_c));
+  }
+  ctx->stream = own;
+  // rejoin: the context's own stream continues after every frame and copy
+  for (cudaStream_t s : {s_r, s_n, s_c}) {
+    FV_CUDA(cudaEventRecord(ctx->fev[7], s));
+    FV_CUDA(cudaStreamWaitEvent(own, ctx->fev[7], 0));
+  }
+  if (rc) return rc;
+  FV_CUDA(cudaStreamSynchronize(s_c));
   return 0;
 }
 

@@ -87,6 +87,9 @@ struct fv_ctx {
   void* wave_ray = nullptr;   // int4 per compacted ray
   int64_t wave_ray_cap = 0;
   unsigned long long launches = 0;
+  // fv_frames: render / network / copy streams and their event rings (created on first use)
+  cudaStream_t fstream[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fev[8] = {};
   // kernel timing (off by default)
   bool ktiming = false;
   cudaEvent_t kopen = nullptr;

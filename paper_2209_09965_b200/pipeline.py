@@ -158,3 +158,22 @@ class FramePipeline:
                                          C.c_void_p(host_rgb.ctypes.data if isinstance(host_rgb, np.ndarray)
                                                     else host_rgb.data_ptr()), t))
         return tuple(t)
+
+    def frames_to_host(self, frames, host_rgb) -> None:
+        """A camera path through the C ABI's fv_frames: `frames` is a sequence of (camera, fovea,
+        frame index); frame t's (H,W,3) float32 image lands in host_rgb[t % len(host_rgb)] (pinned
+        torch tensors or NumPy arrays). Render t+1, reconstruct t and the copy of t-1 overlap on
+        three streams; returns once every copy has landed."""
+        n = len(frames)
+        if n == 0:
+            return
+        cams = (_lib.FvCamera * n)(*[c.c_struct() for c, _, _ in frames])
+        fovs = (_lib.FvFovea * n)(*[f.c_struct() for _, f, _ in frames])
+        ids = (C.c_int * n)(*[int(j) for _, _, j in frames])
+
+        def addr(b):
+            return b.ctypes.data if isinstance(b, np.ndarray) else b.data_ptr()
+
+        outs = (C.c_void_p * n)(*[addr(host_rgb[t % len(host_rgb)]) for t in range(n)])
+        _lib.check(self.ctx.lib.fv_frames(self.ctx.h, self.vol, self.net_h, self.state.h, n, cams,
+                                          self._light_ref(), C.byref(self._set), fovs, ids, outs))

@@ -412,3 +412,30 @@ def test_kernel_timing_counts_algorithmic_conv_flops(stack):
     assert flops == pytest.approx(2 * 275071.5 * h * w, rel=1e-12)
     for k in ("mask", "march_main", "march_shadow", "march_composite", "netops"):
         assert t[k][2] >= 1 and t[k][0] > 0, k
+
+
+def test_frames_to_host_equals_frame_by_frame(stack):
+    """fv_frames (render t+1 || reconstruct t || copy t-1, three streams) must produce exactly the
+    images of successive fv_frame calls, each in its own host buffer."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    h, w = 184, 320
+    spec = ExperimentSpec(mode="hifi", width=w, height=h)
+    scene = default_scene("sphere_shells", (96, 96, 96))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, w, h)
+    pipe = FramePipeline(scene, net, (h, w), stack)
+    frames = [(cams[3 * i], spec.fovea(), i) for i in range(5)]
+    ref = []
+    for c, f, j in frames:
+        out = np.zeros((h, w, 3), np.float32)
+        pipe.frame_to_host(c, f, j, out)
+        ref.append(out)
+    pipe.reset()
+    outs = [torch.zeros((h, w, 3), dtype=torch.float32).pin_memory() for _ in frames]
+    pipe.frames_to_host(frames, outs)
+    for i, (a, b) in enumerate(zip(outs, ref)):
+        assert np.array_equal(a.numpy(), b), i
+    assert float(np.abs(ref[-1]).sum()) > 0
