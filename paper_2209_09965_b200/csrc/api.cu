@@ -2,6 +2,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -446,8 +447,17 @@ int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st
     FV_CUDA(cudaMalloc(&ctx->rgb_scratch, sizeof(float) * 6 * npix));
     ctx->rgb_cap = 6 * npix;
   }
-  for (auto& s : ctx->fstream)
-    if (!s) FV_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  if (!ctx->fstream[0]) {
+    // the network is the critical path: its stream gets the highest priority, so the marcher's
+    // blocks fill the SMs the convs leave idle instead of delaying them
+    int lo = 0, hi = 0;
+    FV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* e = getenv("FV_PIPE_PRIORITY");
+    const bool prio = !(e && atoi(e) == 0);
+    FV_CUDA(cudaStreamCreateWithPriority(&ctx->fstream[0], cudaStreamNonBlocking, lo));
+    FV_CUDA(cudaStreamCreateWithPriority(&ctx->fstream[1], cudaStreamNonBlocking, prio ? hi : lo));
+    FV_CUDA(cudaStreamCreateWithPriority(&ctx->fstream[2], cudaStreamNonBlocking, lo));
+  }
   for (auto& e : ctx->fev)
     if (!e) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cudaStream_t s_r = ctx->fstream[0], s_n = ctx->fstream[1], s_c = ctx->fstream[2];

@@ -10,6 +10,7 @@ it, and the D.head epilogue writes next frame's O_d feedback into channels 5..7.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -98,8 +99,11 @@ class FramePipeline:
         import torch
 
         if getattr(self, "_rctx", None) is None:
-            self._s_render = torch.cuda.Stream(device=self.ctx.device)
-            self._s_net = torch.cuda.Stream(device=self.ctx.device)
+            # the network is the critical path: its stream gets the higher priority, so the marcher's
+            # blocks fill the SMs the convs leave idle instead of delaying them
+            prio = int(os.environ.get("FV_PIPE_PRIORITY", "1"))
+            self._s_render = torch.cuda.Stream(device=self.ctx.device, priority=0)
+            self._s_net = torch.cuda.Stream(device=self.ctx.device, priority=-1 if prio else 0)
             self._rctx = _lib.Context(self.ctx.device, stream=self._s_render)
             self._nctx = _lib.Context(self.ctx.device, stream=self._s_net)
             self._rctx.ensure_noise(self.ctx._noise_ref)
