@@ -19,8 +19,11 @@
 //   warp 0     producer: cp.async.bulk of A halo rows + the stage's B (weight) image
 //   warp 1     MMA issuer: tcgen05.mma 128 x N x 16, accumulators in TMEM (R x N columns,
 //              double-buffered across tiles), tcgen05.commit to release smem / publish TMEM
-//   warps 2-5  epilogue: tcgen05.ld -> +bias, ReLU -> fp16 NC8HW8 store, fused 2x2 average pool,
+//   warps 2-9  epilogue (two per TMEM lane quarter): tcgen05.ld -> +bias, ReLU -> fp16 NC8HW8 store, fused 2x2 average pool,
 //              or the D.head mode (fp32 O_d planes + the next frame's feedback channels)
+#include <cstdio>
+#include <cstdlib>
+
 #include "internal.h"
 #include "sm100.cuh"
 
@@ -57,7 +60,22 @@ struct ConvArgs {
   int center_only;     // 1x1 conv: only the centre tap's MMAs are issued
   int tiles_x, tiles_y;
   double flops;        // host-side: algorithmic FLOPs of the launch (kernel timing)
+  unsigned long long* prof;  // nullable (FV_CONV_PROF=1): per-CTA wait-cycle counters, kProfSlots each
+  int mma_test;              // FV_CONV_MMA_TEST timing probe (0 = off)
+  int dx_outer;              // row-fused MMA order (FV_CONV_DXOUTER, A/B)
 };
+constexpr int kProfSlots = 6;  // producer empty-wait, MMA full-wait, MMA tempty-wait, epilogue tfull-wait, MMA total, tiles
+
+// mbarrier wait that adds the cycles spent to *acc when profiling
+__device__ __forceinline__ void pwait(uint32_t bar, uint32_t parity, bool prof, unsigned long long& acc) {
+  if (!prof) {
+    sm100::mbar_wait(bar, parity);
+    return;
+  }
+  const unsigned long long t0 = clock64();
+  sm100::mbar_wait(bar, parity);
+  acc += clock64() - t0;
+}
 
 // R output rows per tile, N output channels (MMA N), S pipeline stages; BRES: the whole weight
 // image (<= kBResStages stages, i.e. cin <= 64) is loaded once per CTA and stays in smem, so
@@ -100,18 +118,19 @@ __device__ __forceinline__ void issue_stage(uint64_t a0, uint64_t b0, uint32_t d
 // instead of three times -- at N = 64 the A reads alone otherwise saturate the SM's operand
 // bandwidth (ncu: L1/TEX 86% busy, tensor pipe 57%). In the first K-stage the dy = 0 slice (the
 // row's first contribution) is issued separately without accumulate.
-template <int R, int N>
+template <int R, int N, bool kDxOuter>
 __device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint32_t d_base, bool first_stage) {
   using C = Cfg<R, N>;
 #pragma unroll
-  for (int h = 0; h < R + 2; ++h) {
-    constexpr int dummy = 0;
-    (void)dummy;
+  for (int it = 0; it < 3 * (R + 2); ++it) {
+    // kDxOuter: dx-major order (consecutive MMAs hit different accumulator rows); else h-major.
+    // Either way row r is first written by (h = r, dx = 0, dy = 0) before any other MMA touches it.
+    const int h = kDxOuter ? it % (R + 2) : it / 3;
+    const int dx = kDxOuter ? it / (R + 2) : it % 3;
     const int dy_lo = h - R + 1 > 0 ? h - R + 1 : 0;
     const int dy_hi = h < 2 ? h : 2;
     const int r_first = h - dy_lo;
-#pragma unroll
-    for (int dx = 0; dx < 3; ++dx) {
+    {
       const uint64_t ad = a0 + (uint64_t)(((h * kHaloW + dx) * 16) >> 4);
       const uint64_t bdx = b0 + (uint64_t)((dx * 2 * 3 * N * 16) >> 4);
       const uint32_t d0 = d_base + (R - 1 - r_first) * N;
@@ -166,6 +185,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_tiles = a.tiles_x * a.tiles_y;
+  const bool prof = a.prof != nullptr;
+  unsigned long long w_empty = 0, w_full = 0, w_tempty = 0, w_tfull = 0;
+  const unsigned long long t_start = prof ? clock64() : 0ull;
+  int n_my_tiles = 0;
 
   if (warp == 0) {
     // ---------------- producer ----------------
@@ -181,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
         const int st = it % kStages;
         const uint32_t round = it / kStages;
-        sm100::mbar_wait(bar_empty + 8 * st, (round & 1) ^ 1);
+        pwait(bar_empty + 8 * st, (round & 1) ^ 1, prof, w_empty);
         const int g0 = ks * kStageGroups;
         int gs = a.groups - g0;
         if (gs > kStageGroups) gs = kStageGroups;
@@ -240,15 +263,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     if (BRES) sm100::mbar_wait(bar_bres, 0);
     int it = 0, lt = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
+      ++n_my_tiles;
       const int acc = lt % C::kAcc;
       const uint32_t acc_round = lt / C::kAcc;
-      sm100::mbar_wait(bar_tempty + 8 * acc, (acc_round & 1) ^ 1);
+      pwait(bar_tempty + 8 * acc, (acc_round & 1) ^ 1, prof, w_tempty);
       sm100::tc_fence_after();
       const uint32_t d_base = tmem_base + acc * R * N;
       for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
         const int st = it % kStages;
         const uint32_t round = it / kStages;
-        sm100::mbar_wait(bar_full + 8 * st, round & 1);
+        pwait(bar_full + 8 * st, round & 1, prof, w_full);
         sm100::tc_fence_after();
         int gs = a.groups - ks * kStageGroups;
         if (gs > kStageGroups) gs = kStageGroups;
@@ -260,11 +284,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + (BRES ? ks : st) * C::kBBytes),
                                              (FUSED && !a.center_only ? 3 : 1) * N * 16, 128);
         (void)nk;  // one 16-channel MMA K-step per stage
-        if (sm100::elect_one()) {
+        const bool leader = sm100::elect_one();
+        if (a.mma_test && leader) {
+          // timing probe (FV_CONV_MMA_TEST, results are garbage): the same MMA work per stage
+          // (128 x 2304 x 16) as 9 x N256, 18 x N128 or 36 x N64 dispatches
+          const uint64_t bt = sm100::smem_desc(sm100::smem_u32(sB + (BRES ? ks : st) * C::kBBytes), 16 * 16, 128);
+          if (a.mma_test == 1) {
+#pragma unroll
+            for (int i = 0; i < 9; ++i)
+              sm100::mma_f16(d_base, a0 + (uint64_t)((i * 16) >> 4), bt, sm100::idesc_f16(128, 256), 1u);
+          } else if (a.mma_test == 2) {
+#pragma unroll
+            for (int i = 0; i < 18; ++i)
+              sm100::mma_f16(d_base + (i & 1) * 128, a0 + (uint64_t)((i * 16) >> 4), bt, sm100::idesc_f16(128, 128), 1u);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 36; ++i)
+              sm100::mma_f16(d_base + (i & 3) * 64, a0 + (uint64_t)((i * 16) >> 4), bt, sm100::idesc_f16(128, 64), 1u);
+          }
+        } else if (!a.mma_test && leader) {
           if (a.center_only)
             issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
           else
-            FUSED ? issue_stage_rows<R, N>(a0, b0, d_base, ks == 0)
+            FUSED ? (a.dx_outer ? issue_stage_rows<R, N, true>(a0, b0, d_base, ks == 0)
+                                : issue_stage_rows<R, N, false>(a0, b0, d_base, ks == 0))
                   : issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
         }
         __syncwarp();
@@ -287,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       const uint32_t acc_round = lt / C::kAcc;
       const int x0 = (tile % a.tiles_x) * kTileW;
       const int y0 = (tile / a.tiles_x) * R;
-      sm100::mbar_wait(bar_tfull + 8 * acc, acc_round & 1);
+      pwait(bar_tfull + 8 * acc, acc_round & 1, prof, w_tfull);
       sm100::tc_fence_after();
       const int x = x0 + 32 * q + lane;
       const bool xin = x < a.W;
@@ -411,6 +454,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       if (lane == 0) sm100::mbar_arrive(bar_tempty + 8 * acc);
     }
   }
+  if (prof && lane == 0) {
+    unsigned long long* o = a.prof + (int64_t)blockIdx.x * kProfSlots;
+    if (warp == 0) atomicAdd(o + 0, w_empty);
+    if (warp == 1) {
+      atomicAdd(o + 1, w_full);
+      atomicAdd(o + 2, w_tempty);
+      atomicAdd(o + 4, clock64() - t_start);
+      atomicAdd(o + 5, (unsigned long long)n_my_tiles);
+    }
+    if (warp >= 2) atomicAdd(o + 3, w_tfull / kEpiWarps);
+  }
   __syncthreads();
   if (warp == 1) {
     sm100::tc_fence_after();
@@ -436,6 +490,18 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   ktime_begin(ctx);
   conv3x3_tc_kernel<R, N, S, BRES, FUSED><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
   ktime_end(ctx, FV_KC_CONV, a.flops);
+  if (a.prof) {
+    std::vector<unsigned long long> h((size_t)grid * kProfSlots);
+    FV_CUDA(cudaMemcpyAsync(h.data(), a.prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    FV_CUDA(cudaStreamSynchronize(ctx->stream));
+    double s[kProfSlots] = {};
+    for (int b = 0; b < grid; ++b)
+      for (int k = 0; k < kProfSlots; ++k) s[k] += (double)h[(size_t)b * kProfSlots + k] / grid;
+    fprintf(stderr,
+            "[conv prof] R=%d N=%d S=%d bres=%d fused=%d %dx%d groups=%d: per CTA %.1f tiles, total %.0f cyc; "
+            "MMA waits full %.0f tempty %.0f; producer empty-wait %.0f; epilogue tfull-wait %.0f\n",
+            R, N, S, (int)BRES, (int)FUSED, a.H, a.W, a.groups, s[5], s[4], s[1], s[2], s[0], s[3]);
+  }
   FV_CHECK_LAUNCH("conv3x3_tc_kernel");
   ctx->launches += 1;
   return 0;
@@ -448,7 +514,8 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
 int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
   const int groups = (cp.cin + 7) / 8;
   const int N = cp.n_pad;
-  cp.row_fused = !cp.center_only && 3 * N <= 256;
+  static const bool no_fuse = getenv("FV_CONV_FUSE") && atoi(getenv("FV_CONV_FUSE")) == 0;  // A/B runs
+  cp.row_fused = !no_fuse && !cp.center_only && 3 * N <= 256;
   cp.n_stages = (groups + kStageGroups - 1) / kStageGroups;
   cp.stage_groups.clear();
   cp.stage_off.clear();
@@ -518,6 +585,17 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   a.dst = dst ? dst->p : nullptr;
   a.pool_dst = pool_dst ? pool_dst->p : nullptr;
   a.relu = relu ? 1 : 0;
+  static const int mma_test = getenv("FV_CONV_MMA_TEST") ? atoi(getenv("FV_CONV_MMA_TEST")) : 0;
+  a.mma_test = mma_test;
+  static const int dx_outer = getenv("FV_CONV_DXOUTER") ? atoi(getenv("FV_CONV_DXOUTER")) : 1;
+  a.dx_outer = dx_outer;
+  static unsigned long long* prof_buf = nullptr;
+  static const bool want_prof = getenv("FV_CONV_PROF") != nullptr;
+  if (want_prof) {
+    if (!prof_buf) FV_CUDA(cudaMalloc(&prof_buf, sizeof(unsigned long long) * kProfSlots * 1024));
+    FV_CUDA(cudaMemsetAsync(prof_buf, 0, sizeof(unsigned long long) * kProfSlots * 1024, ctx->stream));
+    a.prof = prof_buf;
+  }
   a.flops = 2.0 * a.H * a.W *
             (cp.macs_per_px > 0 ? cp.macs_per_px : (double)cp.cin * cp.cout * cp.ksize * cp.ksize);
   if (aux) {
@@ -539,6 +617,7 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   // row-fused MMAs whenever 3N <= 256 (the B image was laid out for it in conv_prepare)
   const bool res = cp.n_stages <= kBResStages;
   const bool fu = cp.row_fused;
+  static const int r8 = getenv("FV_CONV_R8") ? atoi(getenv("FV_CONV_R8")) : 0;  // A/B: 8-row tiles at N=64
 #define FV_LAUNCH(R_, N_, S_) \
   (res ? (fu ? launch<R_, N_, S_, true, true>(ctx, a) : launch<R_, N_, S_, true, false>(ctx, a)) \
        : (fu ? launch<R_, N_, S_, false, true>(ctx, a) : launch<R_, N_, S_, false, false>(ctx, a)))
@@ -546,7 +625,9 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
     case 16: return FV_LAUNCH(4, 16, 6);
     case 32: return FV_LAUNCH(4, 32, 5);
     case 48: return FV_LAUNCH(4, 48, 4);
-    case 64: return res ? (fu ? launch<4, 64, 5, true, true>(ctx, a) : launch<4, 64, 5, true, false>(ctx, a))
+    case 64:
+      if (r8 && fu) return res ? launch<8, 64, 3, true, true>(ctx, a) : launch<8, 64, 3, false, true>(ctx, a);
+      return res ? (fu ? launch<4, 64, 5, true, true>(ctx, a) : launch<4, 64, 5, true, false>(ctx, a))
                         : (fu ? launch<4, 64, 4, false, true>(ctx, a) : launch<4, 64, 4, false, false>(ctx, a));
     case 80: return res ? (fu ? launch<2, 80, 5, true, true>(ctx, a) : launch<2, 80, 5, true, false>(ctx, a))
                         : (fu ? launch<2, 80, 4, false, true>(ctx, a) : launch<2, 80, 4, false, false>(ctx, a));
