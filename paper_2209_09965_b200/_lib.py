@@ -12,7 +12,8 @@ import threading
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libfovnet.so"
+# FV_LIBFOVNET: alternative build of the same library (A/B runs of tools/probes; never set in tests)
+LIB_PATH = Path(os.environ["FV_LIBFOVNET"]) if os.environ.get("FV_LIBFOVNET") else _HERE / "libfovnet.so"
 
 FV_E_INVALID = -1
 FV_E_CUDA = -2

@@ -369,12 +369,17 @@ __device__ __forceinline__ float tri_fast(const FastVol& V, float px, float py, 
   return c0 * (1.f - tz) + c1 * tz;
 }
 
+// (1-a)^(dt/ref) of a ray's last, partial step (and of unusual full-step exponents). Not inlined:
+// the call forces a real branch -- inlined, the compiler evaluated powf for every sample and
+// selected (ncu: 26% of the shadow pass's instructions on that line).
+__device__ __noinline__ float keep_partial(float x, float e) { return powf(x, e); }
+
 // exponent classes of (1-a)^(dt/ref) on full steps: 0 sqrt, 1 identity, 2 square, 3 general
 __device__ __forceinline__ float keep_cls(float x, int cls, float e) {
   if (cls == 0) return sqrtf(x);
   if (cls == 1) return x;
   if (cls == 2) return x * x;
-  return powf(x, e);
+  return keep_partial(x, e);
 }
 
 struct FastParams {
@@ -445,8 +450,105 @@ __device__ float shadow_fast(const FastParams& F, const float* lut, float px, fl
     for (int j = 0; j < kShadowU; ++j) {
       const float dt = dts[j];
       const float a = tf_alpha<float>(lut, P.K, tri_finish(f[j]));
-      const float keep = dt == step ? keep_cls(1.f - a, F.cls_sh, F.e_sh) : powf(1.f - a, dt * F.inv_ref);
+      const float keep = dt == step ? keep_cls(1.f - a, F.cls_sh, F.e_sh) : keep_partial(1.f - a, dt * F.inv_ref);
       trans = trans * (1.f - (1.f - keep));
+      ++nsamp;
+      t = t + dt;
+      if (!(t < tend) || !(trans > mt)) { stop = true; break; }
+    }
+    if (stop) break;
+  }
+  return trans;
+}
+
+// ---- shadow pass fast path ---------------------------------------------------------------------
+// The wavefront shadow pass is issue-bound (ncu: 78% issue slots, ~140 instructions per sample), so
+// its per-sample path is specialised: the full-step exponent class is a template parameter (no
+// per-sample switch), lerps are single FMAs, and the TF alpha comes from a (a_i, a_{i+1} - a_i)
+// float2 table in shared memory (one LDS.64). All fp32-tier rounding changes (~1e-7).
+__device__ __forceinline__ float lerp_fma(float a, float b, float t) { return fmaf(t, b - a, a); }
+
+__device__ __forceinline__ float tri_finish_fma(const TriFetch& f) {
+  if (!f.inside) return 0.f;
+  const float c00 = lerp_fma(f.A.x, f.A.y, f.tx), c10 = lerp_fma(f.A.z, f.A.w, f.tx);
+  const float c01 = lerp_fma(f.B.x, f.B.y, f.tx), c11 = lerp_fma(f.B.z, f.B.w, f.tx);
+  return lerp_fma(lerp_fma(c00, c10, f.ty), lerp_fma(c01, c11, f.ty), f.tz);
+}
+
+// alpha LUT: lut2[i] = (a_i, a_{i+1} - a_i), i < K-1
+__device__ __forceinline__ float tf_alpha2(const float2* lut2, int K, float s) {
+  s = fminf(fmaxf(s, 0.f), 1.f);
+  const float x = s * (float)(K - 1);
+  const int i0 = min((int)x, K - 2);  // x >= 0: truncation == floor
+  const float2 v = lut2[i0];
+  return fmaf(x - (float)i0, v.y, v.x);
+}
+
+template <int CLS>
+__device__ __forceinline__ float keep_t(float x, float e) {
+  if constexpr (CLS == 0) return sqrtf(x);
+  else if constexpr (CLS == 1) return x;
+  else if constexpr (CLS == 2) return x * x;
+  else return keep_partial(x, e);
+}
+
+template <int CLS>
+__device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px, float py, float pz,
+                               unsigned int& nsamp) {
+  const MarchParams& P = F.P;
+  float dir[3], inv[3], dist = INFINITY;
+  if (P.light_kind == FV_LIGHT_DIRECTIONAL) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { dir[a] = F.ld[a]; inv[a] = F.ld_inv[a]; }
+  } else {
+    const float dx = F.lpos[0] - px, dy = F.lpos[1] - py, dz = F.lpos[2] - pz;
+    dist = sqrtf(dx * dx + dy * dy + dz * dz);
+    const float m = fmaxf(dist, 1e-30f);
+    dir[0] = dx / m; dir[1] = dy / m; dir[2] = dz / m;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float s = dir[a];
+      if (fabsf(s) < 1e-30f) s = s < 0.f ? -1e-30f : 1e-30f;
+      inv[a] = 1.f / s;
+    }
+  }
+  const float p[3] = {px, py, pz};
+  float tmin = -INFINITY, tmax = INFINITY;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float ta = (0.f - p[a]) * inv[a], tb = (F.V.ext[a] - p[a]) * inv[a];
+    tmin = fmaxf(tmin, fminf(ta, tb));
+    tmax = fminf(tmax, fmaxf(ta, tb));
+  }
+  const float t0 = fmaxf(tmin, 0.f);
+  const float tend = fminf(tmax, dist);
+  float trans = 1.f;
+  if (!(tmax > t0 && tend > t0)) return trans;
+  const float step = (float)P.step_sh, mt = (float)P.min_trans;
+  constexpr int kU = 4;
+  const float q0x = px * F.V.inv_sp[0] - 0.5f, q0y = py * F.V.inv_sp[1] - 0.5f, q0z = pz * F.V.inv_sp[2] - 0.5f;
+  const float qdx = dir[0] * F.V.inv_sp[0], qdy = dir[1] * F.V.inv_sp[1], qdz = dir[2] * F.V.inv_sp[2];
+  float t = t0;
+#pragma unroll 1
+  while (true) {
+    TriFetch f[kU];
+    float dts[kU];
+    float tj = t;
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const float dt = fminf(step, tend - tj);
+      const float mid = tj + 0.5f * dt;
+      dts[j] = dt;
+      f[j] = tri_issue_q(F.V, fmaf(qdx, mid, q0x), fmaf(qdy, mid, q0y), fmaf(qdz, mid, q0z));
+      tj = tj + dt;
+    }
+    bool stop = false;
+#pragma unroll
+    for (int j = 0; j < kU; ++j) {
+      const float dt = dts[j];
+      const float om = 1.f - tf_alpha2(lut2, P.K, tri_finish_fma(f[j]));
+      const float keep = dt == step ? keep_t<CLS>(om, F.e_sh) : keep_partial(om, dt * F.inv_ref);
+      trans = trans * keep;
       ++nsamp;
       t = t + dt;
       if (!(t < tend) || !(trans > mt)) { stop = true; break; }
@@ -504,7 +606,7 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
         float c[4];
         tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
         ++n_main;
-        const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+        const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
         const float a_step = 1.f - keep;
         float shade = 1.f;
         if (lit && a_step > 0.f) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
@@ -669,7 +771,7 @@ __global__ void __launch_bounds__(128) march_persist_kernel(FastParams F, unsign
     float shade = -1.f;  // >= 0: composite the pending main sample with this shade
     if (in_shadow) {
       ++n_shadow;
-      const float keep = dt == step_sh ? keep_cls(1.f - c[3], F.cls_sh, F.e_sh) : powf(1.f - c[3], dt * F.inv_ref);
+      const float keep = dt == step_sh ? keep_cls(1.f - c[3], F.cls_sh, F.e_sh) : keep_partial(1.f - c[3], dt * F.inv_ref);
       strans = strans * (1.f - (1.f - keep));
       st = st + dt;
       if (!(st < stend) || !(strans > mt)) {
@@ -678,7 +780,7 @@ __global__ void __launch_bounds__(128) march_persist_kernel(FastParams F, unsign
       }
     } else {
       ++n_main;
-      const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+      const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
       pc0 = c[0]; pc1 = c[1]; pc2 = c[2];
       pa = 1.f - keep;
       shade = 1.f;
@@ -843,7 +945,7 @@ __global__ void __launch_bounds__(128) march_refill_kernel(FastParams F, unsigne
         float c[4];
         tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
         ++n_main;
-        const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+        const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
         const float a_step = 1.f - keep;
         float shade = 1.f;
         if (lit && a_step > 0.f) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
@@ -1025,7 +1127,7 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, W
       const float mid = (float)s * stepf + 0.5f * dt;
       float c[4];
       tf_apply<float>(lut, P.K, tri_finish(f[u]), c);
-      const float keep = last ? powf(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+      const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
       const float a_step = 1.f - keep;
       const bool needs_shadow = lit && a_step > 0.f;
       bool restart = false;
@@ -1107,10 +1209,12 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, W
 
 // One shadow ray per record slot (empty tail slots of a ray's last chunk are skipped); lanes
 // refill from a work counter so long shadow rays do not idle their warp's neighbours.
+template <int CLS>
 __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
-  __shared__ float lut[4 * 256];
-  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __shared__ float2 lut2[256];
+  for (int i = threadIdx.x; i < P.K - 1; i += blockDim.x)
+    lut2[i] = make_float2(P.lut[4 * i + 3], P.lut[4 * (i + 1) + 3] - P.lut[4 * i + 3]);
   __syncthreads();
   const int nslots = (int)min(*B.chunk_count, (unsigned)B.n_chunks_cap) * kChunk;
   const int lane = threadIdx.x & 31;
@@ -1138,7 +1242,7 @@ __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, Wa
     if (!__any_sync(0xffffffffu, my >= 0)) break;
     if (my >= 0) {
       const float4 r0 = B.rec0[my];
-      const float ts = shadow_fast(F, lut, r0.x, r0.y, r0.z, n_shadow);
+      const float ts = shadow_fast_t<CLS>(F, lut2, r0.x, r0.y, r0.z, n_shadow);
       B.shade[my] = amb + (1.f - amb) * ts;
       my = -1;
     }
@@ -1370,7 +1474,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<8>, threads, 0));
         else
           FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<4>, threads, 0));
-        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sh, march_wave_shadow_kernel, threads, 0));
+        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sh, march_wave_shadow_kernel<2>, threads, 0));
         per_sm_main = std::max(per_sm_main, 1);
         per_sm_sh = std::max(per_sm_sh, 1);
       }
@@ -1382,7 +1486,13 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       else
         FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<4><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
       if (P.light_kind != FV_LIGHT_NONE) {
-        FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<<<ctx->num_sms * per_sm_sh, threads, 0, ctx->stream>>>(F, B));
+        const int sgrid = ctx->num_sms * per_sm_sh;
+        switch (F.cls_sh) {
+          case 0: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<0><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
+          case 1: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<1><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
+          case 2: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<2><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
+          default: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<3><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
+        }
         FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;
       }
