@@ -41,7 +41,8 @@ struct DevCounters {
   unsigned int ray_next;   // work counter of the persistent marcher
   unsigned int wave_rec;   // wavefront marcher: records allocated
   unsigned int wave_next;  // wavefront marcher: shadow-pass work counter
-  unsigned int pad[4];
+  unsigned int wave_ord;   // wavefront marcher: chunks listed in ray order
+  unsigned int pad[3];
 };
 
 // Per-launch timing spans (fv_ctx_set_kernel_timing).

@@ -1012,6 +1012,13 @@ struct WaveBufs {
   unsigned int* chunk_count;
   unsigned int* next;      // work counter of the shadow pass
   int4* ray;               // per compacted ray: (first chunk, record count, trans, depth) bits
+  unsigned chunk_perm;     // shadow pass chunk visiting order: 0 = in order, else a prime multiplier
+  int* ord;                // nullable: chunk ids in shadow-pass visiting order (order_*_kernel)
+  unsigned int* ord_count;
+  unsigned int* seg;       // kSegs per-segment counts / cursors
+  int cap_a;               // > 0 (warp main pass): chunk r < cap_a is the FIRST chunk of ray r; later
+                           // chunks come from pools at ids cap_a + counter (see march_wave_shadow_kernel)
+  int chunk_pool;          // warp main pass: chunks claimed per counter round trip
 };
 
 __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float r0, float r1, float r2,
@@ -1207,6 +1214,376 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, W
   }
 }
 
+// ---- main pass, warp per ray -------------------------------------------------------------------
+// The samples of a primary ray do not depend on the data, so a warp marches one ray 32 x kU samples
+// at a time: lane l evaluates samples s0 + u*32 + l (all loads issued first), the transmittance in
+// front of each sample is an inclusive product scan over the lanes, and early termination cuts the
+// block after the first sample whose accumulated opacity reaches early_term_alpha -- the samples the
+// sequential loop would have evaluated, with the products associated differently (fp32 rounding).
+// Records of the lit samples are compacted into the ray's 32-slot chunks with ballot/popc, so all
+// chunks but the last are full (what the shadow and composite passes expect). Rays are claimed 32 at a
+// time; their fp64 setup runs one ray per lane, then the warp walks the hitting rays one by one.
+// (The per-lane state machine it replaces left ~half the lanes idle: rays are 0..~1000 samples long.)
+template <int kU>
+__global__ void __launch_bounds__(128, 4) march_wave_main_warp_kernel(FastParams F, WaveBufs B,
+                                                                      unsigned int* ray_counter) {
+  const MarchParams& P = F.P;
+  __shared__ float lut[4 * 256];
+  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __syncthreads();
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool lit = P.light_kind != FV_LIGHT_NONE;
+  const float amb = lit ? (float)P.ambient : 1.f;
+  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
+  const float early = (float)P.early, stepf = (float)P.step;
+  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
+  // Chunk pool: chunks are claimed kPool at a time and the next pool is claimed (lane 0) when the
+  // current one is opened, so the contended counter's round trip is off the critical path (ncu:
+  // one atomic per chunk was a third of the stalls). Unused pool chunks get fill 0 at exit.
+  const int kPool = B.chunk_pool;
+  int pool_cur = 0, pool_end = 0;  // warp-uniform
+  unsigned int pool_pref = 0;      // lane 0: base of the prefetched pool
+  if (lit && lane == 0) pool_pref = atomicAdd(B.chunk_count, (unsigned)kPool);
+  while (true) {
+    unsigned int base = 0;
+    if (lane == 0) base = atomicAdd(ray_counter, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((int)base >= k) break;
+    // ---- per-lane ray setup (fp64, as the reference) ----
+    const int r = (int)base + lane;
+    bool hit = false;
+    int pix = 0, n = 0;
+    float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0;
+    double t0 = 0.0;
+    if (r < k) {
+      pix = P.idx ? P.idx[r] : r;
+      ++nrays;
+      const int u = pix % P.W, v = pix / P.W;
+      const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
+      const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+      double d[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+      const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+      d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
+      double tend;
+      ray_box(P.pos, d, P.ext, t0, tend, hit);
+      if (!hit) {
+        write_pixel(P, pix, 0.f, 0.f, 0.f, 1.f, 0.f);
+        B.ray[r] = make_int4(-1, 0, 0, 0);
+        if (r < B.cap_a) B.chunk_fill[r] = 0;
+      } else {
+        ++hitc;
+        const double L = tend - t0;
+        n = (int)ceil((L - 1e-12) / P.step);
+        if (n < 1) n = 1;
+        last_dt = (float)(L - (double)(n - 1) * P.step);
+        ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
+        ez = (float)(P.pos[2] + d[2] * t0);
+        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
+      }
+    }
+    unsigned hit_mask = __ballot_sync(0xffffffffu, hit);
+    // ---- march the hitting rays one at a time, the whole warp on each ----
+    while (hit_mask) {
+      const int src = __ffs(hit_mask) - 1;
+      hit_mask &= hit_mask - 1;
+      const int rn = __shfl_sync(0xffffffffu, n, src);
+      const float rl = __shfl_sync(0xffffffffu, last_dt, src);
+      const float rex = __shfl_sync(0xffffffffu, ex, src), rey = __shfl_sync(0xffffffffu, ey, src),
+                  rez = __shfl_sync(0xffffffffu, ez, src);
+      const float rdx = __shfl_sync(0xffffffffu, dx, src), rdy = __shfl_sync(0xffffffffu, dy, src),
+                  rdz = __shfl_sync(0xffffffffu, dz, src);
+      const double rt0 = __shfl_sync(0xffffffffu, t0, src);
+      const int rpix = __shfl_sync(0xffffffffu, pix, src);
+      const int rray = (int)base + src;
+      // pass 0 defers shadows to records; pass 1 (record buffer full) marches them inline
+      for (int fused = 0; fused < 2; ++fused) {
+        float trans = 1.f, depth = 0.f;
+        float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;  // per-lane partial sums
+        int first = -1, chunk = -1, fill = kChunk, m = 0;
+        bool overflow = false;
+        unsigned int n_main_ray = 0, n_shadow_ray = 0;
+        for (int s0 = 0; s0 < rn; s0 += 32 * kU) {
+          TriFetch f[kU];
+#pragma unroll
+          for (int uu = 0; uu < kU; ++uu) {
+            const int s = s0 + uu * 32 + lane;
+            const float dt = s == rn - 1 ? rl : stepf;
+            const float mid = (float)s * stepf + 0.5f * dt;
+            f[uu] = tri_issue(F.V, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid);
+          }
+          bool done = false;
+#pragma unroll
+          for (int uu = 0; uu < kU; ++uu) {
+            const int s = s0 + uu * 32 + lane;
+            const bool active = s < rn;
+            const unsigned act = __ballot_sync(0xffffffffu, active);
+            if (!act) { done = true; break; }
+            const bool last = s == rn - 1;
+            const float dt = last ? rl : stepf;
+            const float mid = (float)s * stepf + 0.5f * dt;
+            float c[4];
+            tf_apply<float>(lut, P.K, tri_finish(f[uu]), c);
+            const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+            const float a_step = active ? 1.f - keep : 0.f;
+            // transmittance in front of / behind each sample: product scan of (1 - a_step)
+            const float om = 1.f - a_step;
+            float incl = om;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const float v = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl *= v;
+            }
+            float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 1.f;
+            const float t_in = trans * excl, t_out = trans * incl;
+            const float acc = 1.f - t_out;
+            // the sequential loop stops after the first sample with !(acc < early) (or the last)
+            const unsigned term = __ballot_sync(0xffffffffu, active && !(acc < early));
+            const int stop_lane = term ? __ffs(term) - 1 : 31 - __clz(act);
+            const bool use = active && lane <= stop_lane;
+            if (depth == 0.f) {
+              const unsigned dm = __ballot_sync(0xffffffffu, use && acc >= 0.5f);
+              if (dm) {
+                const int dl = __ffs(dm) - 1;
+                const float mid_d = __shfl_sync(0xffffffffu, mid, dl);
+                depth = (float)(rt0 + (double)mid_d);
+              }
+            }
+            const float contrib = t_in * a_step;
+            const bool needs_shadow = use && lit && a_step > 0.f;
+            if (!lit) {
+              if (use) {
+                rgb0 += contrib * (c[0] * I0);
+                rgb1 += contrib * (c[1] * I1);
+                rgb2 += contrib * (c[2] * I2);
+              }
+            } else if (fused) {
+              if (use) {
+                float shade = 1.f;
+                if (needs_shadow)
+                  shade = amb + (1.f - amb) * shadow_fast(F, lut, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid,
+                                                          n_shadow_ray);
+                rgb0 += contrib * (c[0] * (shade * I0));
+                rgb1 += contrib * (c[1] * (shade * I1));
+                rgb2 += contrib * (c[2] * (shade * I2));
+              }
+            } else {
+              const unsigned lm = __ballot_sync(0xffffffffu, needs_shadow);
+              const int cnt = __popc(lm);
+              if (cnt) {
+                const int room = kChunk - fill;
+                int nc = -1;
+                if (cnt > room) {
+                  if (chunk < 0 && rray < B.cap_a) {
+                    nc = rray;  // the ray's first chunk: fixed id, so the shadow pass meets first chunks in ray order
+                  } else {
+                    if (pool_cur >= pool_end) {
+                      pool_cur = B.cap_a + (int)__shfl_sync(0xffffffffu, pool_pref, 0);
+                      pool_end = pool_cur + kPool;
+                      if (lane == 0) pool_pref = atomicAdd(B.chunk_count, (unsigned)kPool);
+                    }
+                    nc = pool_cur++;
+                    if (nc >= B.n_chunks_cap) overflow = true;
+                  }
+                }
+                if (!overflow) {
+                  const int rank = __popc(lm & lt_mask);
+                  if (needs_shadow) {
+                    const int slot = rank < room ? chunk * kChunk + fill + rank : nc * kChunk + (rank - room);
+                    B.rec0[slot] = make_float4(rex + rdx * mid, rey + rdy * mid, rez + rdz * mid, 0.f);
+                    B.rec1[slot] = make_float4(c[0], c[1], c[2], contrib);
+                  }
+                  if (nc >= 0) {
+                    if (lane == 0) {
+                      if (chunk >= 0) { B.chunk_fill[chunk] = kChunk; B.chunk_next[chunk] = nc; }
+                    }
+                    if (chunk < 0) first = nc;
+                    chunk = nc;
+                    fill = cnt - room;
+                  } else {
+                    fill += cnt;
+                  }
+                  m += cnt;
+                }
+              }
+            }
+            n_main_ray += __popc(__ballot_sync(0xffffffffu, use));
+            trans = __shfl_sync(0xffffffffu, t_out, stop_lane);
+            if (term || overflow) { done = true; break; }
+          }
+          if (done) break;
+        }
+        if (overflow) {
+          // release this ray's chunks and march it again with inline shadows
+          if (lane == 0)
+            for (int cc = first; cc >= 0; cc = (cc == chunk) ? -1 : B.chunk_next[cc]) B.chunk_fill[cc] = 0;
+          continue;
+        }
+        n_main += n_main_ray;
+        n_shadow += n_shadow_ray;
+        if (lit && !fused && m > 0) {
+          if (lane == 0) {
+            B.chunk_fill[chunk] = fill;
+            B.chunk_next[chunk] = -1;
+            B.ray[rray] = make_int4(first, m, __float_as_int(trans), __float_as_int(depth));
+          }
+        } else {
+          if (lane == 0 && rray < B.cap_a) B.chunk_fill[rray] = 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            rgb0 += __shfl_xor_sync(0xffffffffu, rgb0, o);
+            rgb1 += __shfl_xor_sync(0xffffffffu, rgb1, o);
+            rgb2 += __shfl_xor_sync(0xffffffffu, rgb2, o);
+          }
+          if (lane == 0) {
+            write_pixel(P, rpix, rgb0, rgb1, rgb2, trans, depth);
+            B.ray[rray] = make_int4(-1, 0, 0, 0);
+          }
+        }
+        break;
+      }
+    }
+  }
+  // release the unused chunks of the open pool and of the prefetched one (the shadow pass skips
+  // chunks whose fill is 0)
+  if (lit) {
+    const int pref = B.cap_a + (int)__shfl_sync(0xffffffffu, pool_pref, 0);
+    for (int c = pool_cur + lane; c < pool_end; c += 32)
+      if (c < B.n_chunks_cap) B.chunk_fill[c] = 0;
+    for (int c = lane; c < kPool; c += 32)
+      if (pref + c < B.n_chunks_cap) B.chunk_fill[pref + c] = 0;
+  }
+  // n_main is warp-uniform (popc of ballots); nrays, hitc and n_shadow (inline shadows) are per lane
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
+    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
+    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  }
+  if (lane == 0 && nrays) {
+    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
+    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
+    if (n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+  }
+}
+
+// Shadow-pass visiting order: chunk j of every ray, rays in (roughly) image order, then chunk j+1
+// ... ("depth-major"). Chunk j of neighbouring pixels holds samples at similar depth, so their light
+// rays start close together and overlap in the volume -- that is what makes the L1/L2 hit rates of
+// the shadow pass (A/B: allocation order of the warp-per-ray main pass 488 us, this order ~440).
+// Three small passes: count chunks per segment, scan the counts, scatter chunk ids.
+constexpr int kSegs = 64;  // segments >= kSegs-1 share the last bucket
+
+__global__ void __launch_bounds__(256) order_count_kernel(FastParams F, WaveBufs B) {
+  const MarchParams& P = F.P;
+  __shared__ unsigned cnt[kSegs];
+  for (int i = threadIdx.x; i < kSegs; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k; r += gridDim.x * blockDim.x) {
+    const int4 v = B.ray[r];
+    if (v.x < 0) continue;
+    const int nch = (v.y + kChunk - 1) / kChunk;
+    for (int j = 0; j < min(nch, kSegs - 1); ++j) atomicAdd(&cnt[j], 1u);
+    if (nch > kSegs - 1) atomicAdd(&cnt[kSegs - 1], (unsigned)(nch - (kSegs - 1)));
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kSegs; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&B.seg[i], cnt[i]);
+}
+
+__global__ void order_scan_kernel(WaveBufs B) {  // one warp: seg[j] <- exclusive prefix; total -> ord_count
+  const int lane = threadIdx.x;
+  unsigned a = B.seg[2 * lane], b = B.seg[2 * lane + 1];
+  unsigned incl = a + b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const unsigned excl = incl - (a + b);
+  B.seg[2 * lane] = excl;
+  B.seg[2 * lane + 1] = excl + a;
+  if (lane == 31) *B.ord_count = incl;
+}
+
+// One atomic per block and segment (per-warp atomics on the few hot segment cursors cost 16 us).
+__global__ void __launch_bounds__(256) order_scatter_kernel(FastParams F, WaveBufs B) {
+  const MarchParams& P = F.P;
+  __shared__ int s_cnt[8], s_pre[8], s_max[8];
+  __shared__ unsigned s_base;
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int r0 = blockIdx.x * blockDim.x; r0 < k; r0 += gridDim.x * blockDim.x) {
+    const int r = r0 + threadIdx.x;
+    int4 v = make_int4(-1, 0, 0, 0);
+    if (r < k) v = B.ray[r];
+    const int nch = v.x >= 0 ? (v.y + kChunk - 1) / kChunk : 0;
+    int wmax = nch;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+    if (lane == 0) s_max[warp] = wmax;
+    __syncthreads();
+    int bmax = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) bmax = max(bmax, s_max[w]);
+    int c = v.x;
+    for (int j = 0; j < bmax; ++j) {
+      const bool has = j < nch;
+      const unsigned m = __ballot_sync(0xffffffffu, has);
+      if (lane == 0) s_cnt[warp] = __popc(m);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) { s_pre[w] = t; t += s_cnt[w]; }
+        s_base = t ? atomicAdd(&B.seg[min(j, kSegs - 1)], (unsigned)t) : 0u;
+      }
+      __syncthreads();
+      if (has) {
+        const unsigned pos = s_base + s_pre[warp] + __popc(m & lt_mask);
+        if (pos < (unsigned)B.n_chunks_cap) B.ord[pos] = c;
+        c = B.chunk_next[c];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// With cap_a: list the rays whose first chunk (id = ray index) holds records, in ray order (one
+// atomic per block; blocks cover consecutive rays) -- the shadow pass visits these first, then the
+// pooled later chunks. No chain walks, so this is a few microseconds.
+__global__ void __launch_bounds__(256) first_list_kernel(FastParams F, WaveBufs B) {
+  const MarchParams& P = F.P;
+  __shared__ int s_cnt[8], s_pre[8];
+  __shared__ unsigned s_base;
+  const int n = min(P.k_dev ? *P.k_dev : P.k_max, B.cap_a);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int r0 = blockIdx.x * blockDim.x; r0 < n; r0 += gridDim.x * blockDim.x) {
+    const int r = r0 + threadIdx.x;
+    const bool has = r < n && B.chunk_fill[r] > 0;
+    const unsigned m = __ballot_sync(0xffffffffu, has);
+    if (lane == 0) s_cnt[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) { s_pre[w] = t; t += s_cnt[w]; }
+      s_base = t ? atomicAdd(B.ord_count, (unsigned)t) : 0u;
+    }
+    __syncthreads();
+    if (has) B.ord[s_base + s_pre[warp] + __popc(m & lt_mask)] = r;
+    __syncthreads();
+  }
+}
+
 // One shadow ray per record slot (empty tail slots of a ray's last chunk are skipped); lanes
 // refill from a work counter so long shadow rays do not idle their warp's neighbours.
 template <int CLS>
@@ -1216,7 +1593,11 @@ __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, Wa
   for (int i = threadIdx.x; i < P.K - 1; i += blockDim.x)
     lut2[i] = make_float2(P.lut[4 * i + 3], P.lut[4 * (i + 1) + 3] - P.lut[4 * i + 3]);
   __syncthreads();
-  const int nslots = (int)min(*B.chunk_count, (unsigned)B.n_chunks_cap) * kChunk;
+  // chunks to visit: with cap_a, first the listed non-empty first chunks (ord) then the pooled ones
+  const int n_a = B.cap_a > 0 ? (int)*B.ord_count : 0;
+  const int n_b = B.cap_a > 0 ? (int)min(*B.chunk_count, (unsigned)(B.n_chunks_cap - B.cap_a))
+                              : (int)min(B.ord ? *B.ord_count : *B.chunk_count, (unsigned)B.n_chunks_cap);
+  const int nslots = (n_a + n_b) * kChunk;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const float amb = (float)P.ambient;
@@ -1234,9 +1615,21 @@ __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, Wa
       if (lane == leader) base = atomicAdd(B.next, (unsigned)__popc(msk));
       base = __shfl_sync(0xffffffffu, base, leader);
       if (need) {
-        const int i = (int)(base + __popc(msk & lt_mask));
-        if (i >= nslots) exhausted = true;
-        else if ((i % kChunk) < B.chunk_fill[i / kChunk]) my = i;
+        int i = (int)(base + __popc(msk & lt_mask));
+        if (i >= nslots) {
+          exhausted = true;
+        } else {
+          if (B.cap_a > 0) {
+            const int q = i / kChunk;
+            i = (q < n_a ? B.ord[q] : B.cap_a + q - n_a) * kChunk + (i % kChunk);
+          } else if (B.ord) {
+            i = B.ord[i / kChunk] * kChunk + (i % kChunk);
+          } else if (B.chunk_perm) {  // visit chunks in a scattered order (bijection: perm is prime, > nchunks)
+            const unsigned nch = (unsigned)(nslots / kChunk);
+            i = (int)(((unsigned long long)(i / kChunk) * B.chunk_perm % nch) * kChunk + (i % kChunk));
+          }
+          if ((i % kChunk) < B.chunk_fill[i / kChunk]) my = i;
+        }
       }
     }
     if (!__any_sync(0xffffffffu, my >= 0)) break;
@@ -1447,7 +1840,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         if (ctx->wave_rec) cudaFree(ctx->wave_rec);
         ctx->wave_rec = nullptr;
         FV_CUDA(cudaMalloc(&ctx->wave_rec, (sizeof(float4) * 2 + sizeof(float)) * rec_cap +
-                                               2 * sizeof(int) * (rec_cap / kChunk)));
+                                               3 * sizeof(int) * (rec_cap / kChunk) + 64 * sizeof(int)));
         ctx->wave_cap = rec_cap;
       }
       if (k_max > ctx->wave_ray_cap) {
@@ -1466,6 +1859,14 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.chunk_count = &ctx->counters->wave_rec;
       B.next = &ctx->counters->wave_next;
       B.ray = reinterpret_cast<int4*>(ctx->wave_ray);
+      static const unsigned chunk_perm = getenv("FV_SHADOW_PERM") ? (unsigned)atol(getenv("FV_SHADOW_PERM")) : 0u;
+      B.chunk_perm = chunk_perm;
+      static const int chunk_pool = getenv("FV_CHUNK_POOL") ? std::max(1, atoi(getenv("FV_CHUNK_POOL"))) : 8;
+      B.chunk_pool = chunk_pool;
+      static const bool shadow_order = getenv("FV_SHADOW_ORDER") && atoi(getenv("FV_SHADOW_ORDER")) == 1;
+      B.ord = shadow_order ? B.chunk_fill + ctx->wave_cap / kChunk : nullptr;
+      B.ord_count = &ctx->counters->wave_ord;
+      B.seg = reinterpret_cast<unsigned int*>(B.chunk_fill + 2 * (ctx->wave_cap / kChunk));
       static int main_u = 0, per_sm_main = 0, per_sm_sh = 0;
       if (!per_sm_main) {
         const char* e = getenv("FV_MAIN_U");  // main-sample prefetch depth (A/B runs): 4 or 8
@@ -1478,14 +1879,42 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         per_sm_main = std::max(per_sm_main, 1);
         per_sm_sh = std::max(per_sm_sh, 1);
       }
-      // ray_next, wave_rec, wave_next are consecutive counters
-      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 3 * sizeof(unsigned int), ctx->stream));
+      // ray_next, wave_rec, wave_next, wave_ord are consecutive counters
+      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 4 * sizeof(unsigned int), ctx->stream));
       const int mgrid = std::min(blocks, ctx->num_sms * per_sm_main);
-      if (main_u == 8)
+      static const int main_warp = getenv("FV_MAIN_WARP") ? atoi(getenv("FV_MAIN_WARP")) : 2;  // 0: per-lane rays
+      // warp main pass: half the chunk space holds first chunks at id = ray index (k_max may exceed it:
+      // later rays then take pooled first chunks)
+      static const bool direct_first = !(getenv("FV_FIRST_DIRECT") && atoi(getenv("FV_FIRST_DIRECT")) == 0);
+      B.cap_a = (main_warp && direct_first) ? B.n_chunks_cap / 2 : 0;
+      if (B.cap_a > 0) B.ord = B.chunk_fill + ctx->wave_cap / kChunk;  // the first-chunk list
+      static int per_sm_warp = 0;
+      if (main_warp && !per_sm_warp) {
+        if (main_warp == 1)
+          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_warp, march_wave_main_warp_kernel<1>, threads, 0));
+        else
+          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_warp, march_wave_main_warp_kernel<2>, threads, 0));
+        per_sm_warp = std::max(per_sm_warp, 1);
+      }
+      if (main_warp == 1)
+        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<1><<<ctx->num_sms * per_sm_warp, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
+      else if (main_warp)
+        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<2><<<ctx->num_sms * per_sm_warp, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
+      else if (main_u == 8)
         FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<8><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
       else
         FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<4><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
       if (P.light_kind != FV_LIGHT_NONE) {
+        if (B.cap_a > 0) {
+          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, first_list_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
+          ctx->launches += 1;
+        } else if (B.ord) {
+          FV_CUDA(cudaMemsetAsync(B.seg, 0, kSegs * sizeof(unsigned int), ctx->stream));
+          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_count_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
+          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_scan_kernel<<<1, 32, 0, ctx->stream>>>(B));
+          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_scatter_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
+          ctx->launches += 3;
+        }
         const int sgrid = ctx->num_sms * per_sm_sh;
         switch (F.cls_sh) {
           case 0: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<0><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
