@@ -25,6 +25,9 @@ int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, in
 int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out);
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in);
 int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw);
+int kapply_pool(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w);
+int kapply_final(fv_ctx* ctx, fv_state* st, const float* kw, const float* img, float* rgb, float* o_raw,
+                 float* od_raw);
 int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out);
 int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a);
 int od_to_feedback(fv_ctx* ctx, fv_state* st);
@@ -185,30 +188,36 @@ int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float*
     rc = conv3x3(ctx, net->kconv[L], &st->hidden[newp][ne - L], 1, nullptr, nullptr, false, &aux);
     if (rc) return rc;
   }
-  const float* final_img = st->od;
   if (use_k) {
+    // forward_K (network.py:280-293): encoder levels fuse the filter with the following pool, the
+    // last block (level 0) with the output stage
     const float* img = st->od;
     for (int i = 0; i < nb; ++i) {
       const int L = lv[i];
-      float* out = st->img2[L];
-      rc = kapply(ctx, st->kw[i], img, out, st->Hp >> L, st->Wp >> L);
-      if (rc) return rc;
       if (net->blocks[i].first == 'e') {
-        rc = pool3(ctx, out, st->img[L + 1], st->Hp >> (L + 1), st->Wp >> (L + 1));
+        rc = kapply_pool(ctx, st->kw[i], img, st->img[L + 1], st->Hp >> L, st->Wp >> L);
         if (rc) return rc;
         img = st->img[L + 1];
       } else if (i < nb - 1) {
+        float* out = st->img2[L];
+        rc = kapply(ctx, st->kw[i], img, out, st->Hp >> L, st->Wp >> L);
+        if (rc) return rc;
         rc = up3(ctx, out, st->img[L - 1], st->Hp >> L, st->Wp >> L);
         if (rc) return rc;
         img = st->img[L - 1];
+      } else if (L == 0) {
+        rc = kapply_final(ctx, st, st->kw[i], img, out_rgb, out_o, out_od);
+        if (rc) return rc;
+        img = nullptr;
       } else {
-        img = out;
+        set_error("the last K block must be at level 0 (got level %d)", L);
+        return FV_E_INVALID;
       }
     }
-    final_img = img;
+  } else {
+    rc = finalize(ctx, st, st->od, out_rgb, out_o, out_od);
+    if (rc) return rc;
   }
-  rc = finalize(ctx, st, final_img, out_rgb, out_o, out_od);
-  if (rc) return rc;
   std::swap(st->x, st->xalt);
   st->parity = newp;
   st->fresh = false;

@@ -99,6 +99,65 @@ __global__ void __launch_bounds__(128) kapply_kernel(const float* __restrict__ k
   }
 }
 
+// One pixel of apply_kernel_field for the 3 channels (same tap order and zero padding as above).
+__device__ __forceinline__ void kapply_px(const float* __restrict__ kw, const float* __restrict__ img, int h, int w,
+                                          int y, int x, float (&o)[3]) {
+  const int64_t n = (int64_t)h * w, pix = (int64_t)y * w + x;
+  float k[9];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) k[j] = __ldg(kw + j * n + pix);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const float* pl = img + (int64_t)c * n;
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const int yy = y + j / 3 - 1, xx = x + j % 3 - 1;
+      const float v = (yy >= 0 && yy < h && xx >= 0 && xx < w) ? __ldg(pl + (int64_t)yy * w + xx) : 0.f;
+      acc = acc + k[j] * v;
+    }
+    o[c] = acc;
+  }
+}
+
+// K block on an encoder level fused with the avg_pool2 that follows it (forward_K, network.py:280-293):
+// one thread per POOLED pixel computes the 2x2 filtered pixels and averages them, so the level-L
+// filtered image is never written. h, w: level-L dims (even).
+__global__ void __launch_bounds__(128) kapply_pool_kernel(const float* __restrict__ kw, const float* __restrict__ img,
+                                                          float* __restrict__ out, int h, int w) {
+  const int ho = h >> 1, wo = w >> 1;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= wo) return;
+  float p00[3], p10[3], p01[3], p11[3];
+  kapply_px(kw, img, h, w, 2 * y, 2 * x, p00);
+  kapply_px(kw, img, h, w, 2 * y + 1, 2 * x, p10);
+  kapply_px(kw, img, h, w, 2 * y, 2 * x + 1, p01);
+  kapply_px(kw, img, h, w, 2 * y + 1, 2 * x + 1, p11);
+  const int64_t no = (int64_t)ho * wo;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)  // 0.25 * (p00 + p10 + p01 + p11), left to right as autograd.avg_pool2
+    out[c * no + (int64_t)y * wo + x] = 0.25f * (((p00[c] + p10[c]) + p01[c]) + p11[c]);
+}
+
+// Last K block (level 0) fused with the output stage: crop, clip to [0,1] and interleave (rgb), plus
+// the optional raw outputs (bench._reconstruct_frame, bench.py:166-175).
+__global__ void __launch_bounds__(128) kapply_final_kernel(const float* __restrict__ kw, const float* __restrict__ img,
+                                                           const float* __restrict__ od, int H, int W, int Hp, int Wp,
+                                                           float* __restrict__ rgb, float* __restrict__ o_raw,
+                                                           float* __restrict__ od_raw) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
+  if (u >= W) return;
+  float o[3];
+  kapply_px(kw, img, Hp, Wp, v, u, o);
+  const int64_t n = (int64_t)H * W, i = (int64_t)v * W + u, pp = (int64_t)Hp * Wp, j = (int64_t)v * Wp + u;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (rgb) rgb[i * 3 + c] = fminf(fmaxf(o[c], 0.f), 1.f);
+    if (o_raw) o_raw[c * n + i] = o[c];
+    if (od_raw) od_raw[c * n + i] = od[c * pp + j];
+  }
+}
+
 // 3-channel fp32 avg_pool2; grid (ceil(w/128), h, 3), h, w the OUTPUT dims
 __global__ void __launch_bounds__(128) pool3_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                     int h, int w) {
@@ -241,6 +300,24 @@ int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, in
   const dim3 g((w + 127) / 128, h);
   FV_TIMED(ctx, FV_KC_NETOPS, kapply_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
   FV_CHECK_LAUNCH("kapply_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int kapply_pool(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w) {
+  const dim3 g(((w >> 1) + 127) / 128, h >> 1);
+  FV_TIMED(ctx, FV_KC_NETOPS, kapply_pool_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
+  FV_CHECK_LAUNCH("kapply_pool_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int kapply_final(fv_ctx* ctx, fv_state* st, const float* kw, const float* img, float* rgb, float* o_raw,
+                 float* od_raw) {
+  const dim3 g((st->W + 127) / 128, st->H);
+  FV_TIMED(ctx, FV_KC_NETOPS, kapply_final_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, st->od, st->H, st->W, st->Hp,
+                                                                          st->Wp, rgb, o_raw, od_raw));
+  FV_CHECK_LAUNCH("kapply_final_kernel");
   ctx->launches += 1;
   return 0;
 }
