@@ -55,7 +55,7 @@ struct ConvArgs {
   int head;            // 1: aux epilogue (D.head and/or K-stage logits)
   float* od;           // head: (3, H, W) fp32 (nullable)
   __half* feedback;    // head: NHWC8 net input, channels 5..7 (nullable)
-  float* kw[2];        // K-stage filter weights (9, H, W) fp32 per K block (nullable)
+  kw_t* kw[2];         // K-stage filter weights (9, H, W) per K block (nullable)
   int kcol[2];         // first logit column of each K block
   int center_only;     // 1x1 conv: only the centre tap's MMAs are issued
   int tiles_x, tiles_y;

@@ -21,12 +21,12 @@ namespace fv {
 int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_act* dst,
             fv_act* pool_dst, bool relu, const ConvAux* aux);
 int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out);
-int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w);
+int kapply(fv_ctx* ctx, const kw_t* kw, const float* img, float* out, int h, int w);
 int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out);
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in);
 int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw);
-int kapply_pool(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w);
-int kapply_final(fv_ctx* ctx, fv_state* st, const float* kw, const float* img, float* rgb, float* o_raw,
+int kapply_pool(fv_ctx* ctx, const kw_t* kw, const float* img, float* out, int h, int w);
+int kapply_final(fv_ctx* ctx, fv_state* st, const kw_t* kw, const float* img, float* rgb, float* o_raw,
                  float* od_raw);
 int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out);
 int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a);
@@ -413,7 +413,7 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
   std::vector<int64_t> kw_off;
   for (int L : lv) {
     kw_off.push_back(bytes);
-    bytes += align_up((int64_t)9 * (st->Hp >> L) * (st->Wp >> L) * 4, 256);
+    bytes += align_up((int64_t)9 * (st->Hp >> L) * (st->Wp >> L) * (int64_t)sizeof(kw_t), 256);
   }
   if (cudaMalloc(&st->arena, bytes) != cudaSuccess) {
     delete st;
@@ -433,7 +433,7 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
     st->img.push_back(reinterpret_cast<float*>(base + img_off[L]));
     st->img2.push_back(reinterpret_cast<float*>(base + img2_off[L]));
   }
-  for (int64_t o : kw_off) st->kw.push_back(reinterpret_cast<float*>(base + o));
+  for (int64_t o : kw_off) st->kw.push_back(reinterpret_cast<kw_t*>(base + o));
   if (cudaMemsetAsync(st->arena, 0, bytes, ctx->stream) != cudaSuccess) {
     cudaFree(st->arena);
     delete st;

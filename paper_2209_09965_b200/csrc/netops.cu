@@ -77,14 +77,14 @@ __global__ void __launch_bounds__(128) upsample2_nc8_kernel(const __half* __rest
 // out[c,y,x] = sum_j k[j,y,x] * img[c, y+j/3-1, x+j%3-1], zero padding, taps in order
 // (apply_kernel_field, autograd.py:332-359). The softmax-normalised weights k come from the
 // tcgen05 logits conv's epilogue (conv_tc.cu), so this pass only streams 9 + 3 planes.
-__global__ void __launch_bounds__(128) kapply_kernel(const float* __restrict__ kw, const float* __restrict__ img,
+__global__ void __launch_bounds__(128) kapply_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
                                                      float* __restrict__ out, int h, int w) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
   if (x >= w) return;
   const int64_t n = (int64_t)h * w, pix = (int64_t)y * w + x;
   float k[9];
 #pragma unroll
-  for (int j = 0; j < 9; ++j) k[j] = __ldg(kw + j * n + pix);
+  for (int j = 0; j < 9; ++j) k[j] = kw_load(kw + j * n + pix);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float* pl = img + (int64_t)c * n;
@@ -100,12 +100,12 @@ __global__ void __launch_bounds__(128) kapply_kernel(const float* __restrict__ k
 }
 
 // One pixel of apply_kernel_field for the 3 channels (same tap order and zero padding as above).
-__device__ __forceinline__ void kapply_px(const float* __restrict__ kw, const float* __restrict__ img, int h, int w,
+__device__ __forceinline__ void kapply_px(const kw_t* __restrict__ kw, const float* __restrict__ img, int h, int w,
                                           int y, int x, float (&o)[3]) {
   const int64_t n = (int64_t)h * w, pix = (int64_t)y * w + x;
   float k[9];
 #pragma unroll
-  for (int j = 0; j < 9; ++j) k[j] = __ldg(kw + j * n + pix);
+  for (int j = 0; j < 9; ++j) k[j] = kw_load(kw + j * n + pix);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     const float* pl = img + (int64_t)c * n;
@@ -123,7 +123,7 @@ __device__ __forceinline__ void kapply_px(const float* __restrict__ kw, const fl
 // K block on an encoder level fused with the avg_pool2 that follows it (forward_K, network.py:280-293):
 // one thread per POOLED pixel computes the 2x2 filtered pixels and averages them, so the level-L
 // filtered image is never written. h, w: level-L dims (even).
-__global__ void __launch_bounds__(128) kapply_pool_kernel(const float* __restrict__ kw, const float* __restrict__ img,
+__global__ void __launch_bounds__(128) kapply_pool_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
                                                           float* __restrict__ out, int h, int w) {
   const int ho = h >> 1, wo = w >> 1;
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(128) kapply_pool_kernel(const float* __restric
 
 // Last K block (level 0) fused with the output stage: crop, clip to [0,1] and interleave (rgb), plus
 // the optional raw outputs (bench._reconstruct_frame, bench.py:166-175).
-__global__ void __launch_bounds__(128) kapply_final_kernel(const float* __restrict__ kw, const float* __restrict__ img,
+__global__ void __launch_bounds__(128) kapply_final_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
                                                            const float* __restrict__ od, int H, int W, int Hp, int Wp,
                                                            float* __restrict__ rgb, float* __restrict__ o_raw,
                                                            float* __restrict__ od_raw) {
@@ -296,7 +296,7 @@ int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
   return 0;
 }
 
-int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w) {
+int kapply(fv_ctx* ctx, const kw_t* kw, const float* img, float* out, int h, int w) {
   const dim3 g((w + 127) / 128, h);
   FV_TIMED(ctx, FV_KC_NETOPS, kapply_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
   FV_CHECK_LAUNCH("kapply_kernel");
@@ -304,7 +304,7 @@ int kapply(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, in
   return 0;
 }
 
-int kapply_pool(fv_ctx* ctx, const float* kw, const float* img, float* out, int h, int w) {
+int kapply_pool(fv_ctx* ctx, const kw_t* kw, const float* img, float* out, int h, int w) {
   const dim3 g(((w >> 1) + 127) / 128, h >> 1);
   FV_TIMED(ctx, FV_KC_NETOPS, kapply_pool_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
   FV_CHECK_LAUNCH("kapply_pool_kernel");
@@ -312,7 +312,7 @@ int kapply_pool(fv_ctx* ctx, const float* kw, const float* img, float* out, int 
   return 0;
 }
 
-int kapply_final(fv_ctx* ctx, fv_state* st, const float* kw, const float* img, float* rgb, float* o_raw,
+int kapply_final(fv_ctx* ctx, fv_state* st, const kw_t* kw, const float* img, float* rgb, float* o_raw,
                  float* od_raw) {
   const dim3 g((st->W + 127) / 128, st->H);
   FV_TIMED(ctx, FV_KC_NETOPS, kapply_final_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, st->od, st->H, st->W, st->Hp,
