@@ -141,7 +141,7 @@ namespace fv {
 // filter pass). fp32: measured A/B with fp16 storage saved only ~8 us per 1080p frame (the filter
 // pass is not bound by these bytes) for a 100 -> 91 dB PSNR drop against the reference.
 using kw_t = float;
-__host__ __device__ __forceinline__ float kw_load(const kw_t* p) { return __ldg(p); }
+__device__ __forceinline__ float kw_load(const kw_t* p) { return __ldg(p); }
 
 // First logit column of the s-th K block in a K-stage conv (columns 0..2 = D.head); the conv
 // epilogue indexes its TMEM registers with these, so they are compile-time constants.
