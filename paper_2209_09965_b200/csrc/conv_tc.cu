@@ -118,8 +118,12 @@ __device__ __forceinline__ void issue_stage(uint64_t a0, uint64_t b0, uint32_t d
 // instead of three times -- at N = 64 the A reads alone otherwise saturate the SM's operand
 // bandwidth (ncu: L1/TEX 86% busy, tensor pipe 57%). In the first K-stage the dy = 0 slice (the
 // row's first contribution) is issued separately without accumulate.
-template <int R, int N, bool kDxOuter>
-__device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint32_t d_base, bool first_stage) {
+// kPairWait (single accumulator): before the first write of output rows (2p, 2p+1) in a tile's first
+// K-stage, wait until the epilogue has drained that row pair of the previous tile (bar_pair + 8p,
+// parity pair_par), so the next tile's MMAs start while the epilogue is still draining.
+template <int R, int N, bool kDxOuter, bool kPairWait = false>
+__device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint32_t d_base, bool first_stage,
+                                                 uint32_t bar_pair = 0, uint32_t pair_par = 0) {
   using C = Cfg<R, N>;
 #pragma unroll
   for (int it = 0; it < 3 * (R + 2); ++it) {
@@ -127,6 +131,10 @@ __device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint3
     // Either way row r is first written by (h = r, dx = 0, dy = 0) before any other MMA touches it.
     const int h = kDxOuter ? it % (R + 2) : it / 3;
     const int dx = kDxOuter ? it / (R + 2) : it % 3;
+    if (kPairWait && first_stage && dx == 0 && (h & 1) == 0 && h < R) {
+      sm100::mbar_wait(bar_pair + 8 * (h >> 1), pair_par);
+      sm100::tc_fence_after();
+    }
     const int dy_lo = h - R + 1 > 0 ? h - R + 1 : 0;
     const int dy_hi = h < 2 ? h : 2;
     const int r_first = h - dy_lo;
@@ -155,13 +163,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * C::kABytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::kBSlots * C::kBBytes);
-  // bars: full[kStages], empty[kStages], tfull[2], tempty[2], weights-resident
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
+  // bars: full[kStages], empty[kStages], tfull[2], tempty[2], weights-resident, row-pair free[R/2]
+  constexpr bool kPairs = C::kAcc == 1 && FUSED;  // single accumulator: release it row pair by row pair
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5 + (kPairs ? R / 2 : 0));
   const uint32_t bar_full = sm100::smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * kStages;
   const uint32_t bar_tfull = bar_empty + 8 * kStages;
   const uint32_t bar_tempty = bar_tfull + 16;
   const uint32_t bar_bres = bar_tempty + 16;
+  const uint32_t bar_pair = bar_bres + 8;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -176,6 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       sm100::mbar_init(bar_tempty + 8 * s, kEpiWarps);
     }
     sm100::mbar_init(bar_bres, 1);
+    if (kPairs)
+      for (int p = 0; p < R / 2; ++p) sm100::mbar_init(bar_pair + 8 * p, kEpiWarps);
     sm100::fence_mbar_init();
   }
   if (warp == 1) sm100::tmem_alloc<512>(sm100::smem_u32(tmem_slot));
@@ -266,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       ++n_my_tiles;
       const int acc = lt % C::kAcc;
       const uint32_t acc_round = lt / C::kAcc;
-      pwait(bar_tempty + 8 * acc, (acc_round & 1) ^ 1, prof, w_tempty);
+      if (!kPairs) pwait(bar_tempty + 8 * acc, (acc_round & 1) ^ 1, prof, w_tempty);
       sm100::tc_fence_after();
       const uint32_t d_base = tmem_base + acc * R * N;
       for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
@@ -306,8 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
           if (a.center_only)
             issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
           else
-            FUSED ? (a.dx_outer ? issue_stage_rows<R, N, true>(a0, b0, d_base, ks == 0)
-                                : issue_stage_rows<R, N, false>(a0, b0, d_base, ks == 0))
+            FUSED ? (a.dx_outer ? issue_stage_rows<R, N, true, kPairs>(a0, b0, d_base, ks == 0, bar_pair,
+                                                                       (acc_round & 1) ^ 1)
+                                : issue_stage_rows<R, N, false, kPairs>(a0, b0, d_base, ks == 0, bar_pair,
+                                                                        (acc_round & 1) ^ 1))
                   : issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
         }
         __syncwarp();
@@ -447,11 +461,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
               }
             }
           }
+          if constexpr (kPairs) {
+            // last item of this row pair for this warp: release the pair to the next tile's MMAs
+            if (item + 2 >= (R / 2) * kCb || (item + 2) / kCb != item / kCb) {
+              sm100::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) sm100::mbar_arrive(bar_pair + 8 * (item / kCb));
+            }
+          }
         }
       }
       sm100::tc_fence_before();
       __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(bar_tempty + 8 * acc);
+      if (!kPairs && lane == 0) sm100::mbar_arrive(bar_tempty + 8 * acc);
     }
   }
   if (prof && lane == 0) {
@@ -617,7 +639,6 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   // row-fused MMAs whenever 3N <= 256 (the B image was laid out for it in conv_prepare)
   const bool res = cp.n_stages <= kBResStages;
   const bool fu = cp.row_fused;
-  static const int r8 = getenv("FV_CONV_R8") ? atoi(getenv("FV_CONV_R8")) : 0;  // A/B: 8-row tiles at N=64
 #define FV_LAUNCH(R_, N_, S_) \
   (res ? (fu ? launch<R_, N_, S_, true, true>(ctx, a) : launch<R_, N_, S_, true, false>(ctx, a)) \
        : (fu ? launch<R_, N_, S_, false, true>(ctx, a) : launch<R_, N_, S_, false, false>(ctx, a)))
@@ -626,7 +647,6 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
     case 32: return FV_LAUNCH(4, 32, 5);
     case 48: return FV_LAUNCH(4, 48, 4);
     case 64:
-      if (r8 && fu) return res ? launch<8, 64, 3, true, true>(ctx, a) : launch<8, 64, 3, false, true>(ctx, a);
       return res ? (fu ? launch<4, 64, 5, true, true>(ctx, a) : launch<4, 64, 5, true, false>(ctx, a))
                         : (fu ? launch<4, 64, 4, false, true>(ctx, a) : launch<4, 64, 4, false, false>(ctx, a));
     case 80: return res ? (fu ? launch<2, 80, 5, true, true>(ctx, a) : launch<2, 80, 5, true, false>(ctx, a))
