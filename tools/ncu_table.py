@@ -40,7 +40,11 @@ def rows(report):
             if i is None or not d[i]:
                 e[k] = None
                 continue
-            v = float(d[i].replace(",", ""))
+            try:
+                v = float(d[i].replace(",", ""))
+            except ValueError:  # "no data" / "n/a"
+                e[k] = None
+                continue
             if k.startswith("dram_") or k == "us":
                 v *= SCALE.get(units[i], 1.0)
             e[k] = v
