@@ -177,6 +177,15 @@ FV_API int fv_render_sparse(fv_ctx* ctx, const fv_volume* vol, const fv_camera* 
                      const fv_light* light, const fv_settings* settings,
                      const int32_t* idx_dev, const int32_t* k_dev, int k_max,
                      float* rgba_dev, float* depth_dev, fv_state* net_state, fv_stats* stats_out);
+/* renderer.render_sparse_naive (renderer.py:225-259): every pixel of each occupied 64-pixel chunk of
+ * bits_dev ((H,W) uint8, device) is a lane of the thread-per-pixel marcher; lanes whose bit is clear
+ * idle and receive zeros. idx_dev: (H*W) int32 device scratch receiving the lane list (idle lanes
+ * as -(pix+1)); k_dev: one int32 on device receiving the lane count (= work_items). Pixels outside
+ * occupied chunks are left untouched (the caller zero-fills the frame). */
+FV_API int fv_render_sparse_naive(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam,
+                                  const fv_light* light, const fv_settings* settings,
+                                  const uint8_t* bits_dev, int32_t* idx_dev, int32_t* k_dev,
+                                  float* rgba_dev, float* depth_dev, fv_stats* stats_out);
 FV_API int fv_render_full(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam,
                    const fv_light* light, const fv_settings* settings, float* rgba_dev,
                    float* depth_dev, fv_stats* stats_out);

@@ -67,6 +67,39 @@ def compact(bits: np.ndarray) -> np.ndarray:
     return np.flatnonzero(bits.reshape(-1)).astype(np.int64)
 
 
+def uniform_noise(h: int, w: int, t: int = 1, seed: int = 0) -> np.ndarray:
+    """gen_uniform_noise (noise.py:60-75): per frame an independent rank permutation from NumPy's
+    PCG64 stream, value (r+0.5)/n as float32 -> (t, h, w)."""
+    rng = np.random.default_rng(seed)
+    n = h * w
+    out = np.empty((t, h, w), np.float32)
+    for k in range(t):
+        out[k] = ((rng.permutation(n).astype(np.float64) + 0.5) / n).reshape(h, w).astype(np.float32)
+    return out
+
+
+def naive_lanes(bits: np.ndarray, chunk: int = 64) -> np.ndarray:
+    """render_sparse_naive's lane set (renderer.py:225-245): flat indices of every pixel of each
+    `chunk`-pixel row-major group holding at least one set bit."""
+    b = np.asarray(bits, bool).ravel()
+    n = b.size
+    nc = (n + chunk - 1) // chunk
+    pad = np.zeros(nc * chunk, bool)
+    pad[:n] = b
+    occ = pad.reshape(nc, chunk).any(axis=1)
+    return np.flatnonzero(np.repeat(occ, chunk)[:n])
+
+
+def direct_samples(tau: np.ndarray, count: int, rng: np.random.Generator) -> np.ndarray:
+    """draw_direct_samples (sample_maps.py:181-198): inverse-CDF draws over the fp64 tau map ->
+    (count, 2) int64 (u, v); duplicates allowed."""
+    h, w = tau.shape
+    cdf = np.cumsum(tau.ravel())
+    cdf /= cdf[-1]
+    idx = np.minimum(np.searchsorted(cdf, rng.random(count), side="right"), h * w - 1)
+    return np.stack([idx % w, idx // w], axis=1).astype(np.int64)
+
+
 def load_rnkstack(path) -> np.ndarray:
     import struct
 

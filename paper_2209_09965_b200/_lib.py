@@ -91,6 +91,8 @@ _SIGS = {
                              P, P, I, P, P, P, C.POINTER(FvStats)]),
     "fv_render_full": (I, [P, P, C.POINTER(FvCamera), C.POINTER(FvLight), C.POINTER(FvSettings),
                            P, P, C.POINTER(FvStats)]),
+    "fv_render_sparse_naive": (I, [P, P, C.POINTER(FvCamera), C.POINTER(FvLight), C.POINTER(FvSettings),
+                                   P, P, P, P, P, C.POINTER(FvStats)]),
     "fv_net_create": (I, [P, C.c_char_p, I, I, I, C.POINTER(P)]),
     "fv_net_destroy": (I, [P]),
     "fv_net_set_param": (I, [P, P, C.c_char_p, P, I64]),

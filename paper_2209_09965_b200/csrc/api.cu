@@ -341,6 +341,21 @@ int fv_render_sparse(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, co
   return finish_stats(ctx, stats_out, &before);
 }
 
+int fv_render_sparse_naive(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
+                           const fv_settings* settings, const uint8_t* bits_dev, int32_t* idx_dev,
+                           int32_t* k_dev, float* rgba_dev, float* depth_dev, fv_stats* stats_out) {
+  FV_REQUIRE(ctx && vol && cam && settings && bits_dev && idx_dev && k_dev, "null argument");
+  DevCounters before{};
+  int rc = snapshot(ctx, stats_out, &before);
+  if (rc) return rc;
+  rc = launch_naive_list(ctx, bits_dev, cam->height, cam->width, idx_dev, k_dev);
+  if (rc) return rc;
+  rc = launch_render(ctx, vol, cam, light, settings, idx_dev, k_dev, cam->width * cam->height, rgba_dev,
+                     depth_dev, nullptr, cam->width, /*force_variant=*/2);
+  if (rc) return rc;
+  return finish_stats(ctx, stats_out, &before);
+}
+
 int fv_render_full(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
                    const fv_settings* settings, float* rgba_dev, float* depth_dev, fv_stats* stats_out) {
   FV_REQUIRE(ctx && vol && cam && settings, "null argument");

@@ -209,7 +209,11 @@ int launch_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* p
                    double* tau);
 int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
                   const fv_settings* settings, const int32_t* idx, const int32_t* k, int k_max,
-                  float* rgba, float* depth, __half* net_in, int net_wp);
+                  float* rgba, float* depth, __half* net_in, int net_wp, int force_variant = -1);
+// naive renderer's lane list: every pixel of each occupied kChunkNaive-pixel chunk, idle lanes as
+// -(pix+1); returns the entry count in *k_dev
+constexpr int kChunkNaive = 64;  // WARP_CHUNK (renderer.py:34)
+int launch_naive_list(fv_ctx* ctx, const uint8_t* bits, int H, int W, int32_t* idx, int32_t* k_dev);
 int launch_volume_procedural(fv_ctx* ctx, fv_volume* vol, int kind, double* range);
 int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* out_rgb,
                 float* out_o, float* out_od);

@@ -183,8 +183,15 @@ __global__ void __launch_bounds__(128) march_kernel(MarchParams P) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = P.k_dev ? *P.k_dev : P.k_max;
   unsigned int n_main = 0, n_shadow = 0, hitc = 0;
-  if (i < k) {
-    const int pix = P.idx ? P.idx[i] : i;
+  // naive renderer lists idle lanes of occupied chunks as -(pix+1): out[~active] = 0 (renderer.py:195-197)
+  const int raw = (i < k) ? (P.idx ? P.idx[i] : i) : 0;
+  if (i < k && raw < 0) {
+    const int q = -raw - 1;
+    if (P.rgba) *reinterpret_cast<float4*>(P.rgba + (int64_t)q * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (P.depth) P.depth[q] = 0.f;
+  }
+  if (i < k && raw >= 0) {
+    const int pix = raw;
     const int u = pix % P.W, v = pix / P.W;
     // generate_rays (volume.py:293-303)
     const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(128) march_kernel(MarchParams P) {
     }
   }
   // counters: warp reduce, one atomic per warp
-  unsigned int r = (i < k) ? 1u : 0u;
+  unsigned int r = (i < k && raw >= 0) ? 1u : 0u;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     r += __shfl_xor_sync(0xffffffffu, r, o);
@@ -566,8 +573,15 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = P.k_dev ? *P.k_dev : P.k_max;
   unsigned int n_main = 0, n_shadow = 0, hitc = 0;
-  if (i < k) {
-    const int pix = P.idx ? P.idx[i] : i;
+  // naive renderer lists idle lanes of occupied chunks as -(pix+1): out[~active] = 0 (renderer.py:195-197)
+  const int raw = (i < k) ? (P.idx ? P.idx[i] : i) : 0;
+  if (i < k && raw < 0) {
+    const int q = -raw - 1;
+    if (P.rgba) *reinterpret_cast<float4*>(P.rgba + (int64_t)q * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (P.depth) P.depth[q] = 0.f;
+  }
+  if (i < k && raw >= 0) {
+    const int pix = raw;
     const int u = pix % P.W, v = pix / P.W;
     const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
     const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
@@ -634,7 +648,7 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
       px[1] = __floats2half2_rn(out[2], out[3]);
     }
   }
-  unsigned int r = (i < k) ? 1u : 0u;
+  unsigned int r = (i < k && raw >= 0) ? 1u : 0u;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     r += __shfl_xor_sync(0xffffffffu, r, o);
@@ -1736,7 +1750,7 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
 
 int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
                   const fv_settings* s, const int32_t* idx, const int32_t* k, int k_max,
-                  float* rgba, float* depth, __half* net_in, int net_wp) {
+                  float* rgba, float* depth, __half* net_in, int net_wp, int force_variant) {
   FV_REQUIRE(vol && vol->data, "volume has no data");
   FV_REQUIRE(vol->K >= 2, "transfer function not set");
   FV_REQUIRE(cam->width >= 1 && cam->height >= 1, "film dims must be positive");
@@ -1826,12 +1840,14 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     F.cls_sh = exp_class(P.step_sh / P.ref);
     F.inv_ref = (float)(1.0 / P.ref);
     // FV_MARCH_KERNEL=wave (default) | refill | ray | persist -- variants kept for A/B runs
-    static int variant = -1;
-    if (variant < 0) {
+    static int env_variant = -1;
+    if (env_variant < 0) {
       const char* e = getenv("FV_MARCH_KERNEL");
-      variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2
-              : (e && strcmp(e, "refill") == 0) ? 0 : 3;
+      env_variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2
+                  : (e && strcmp(e, "refill") == 0) ? 0 : 3;
     }
+    // the naive renderer forces the thread-per-lane kernel (idle lanes are its point)
+    const int variant = force_variant >= 0 ? force_variant : env_variant;
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
       // record slots: 16 per compacted ray (C3 needs ~12 incl. chunk tails), at least 4M

@@ -15,6 +15,8 @@
 // (dynamic tile index => tiles retire in order), publishes its aggregate, looks back over its
 // predecessors' epoch-tagged status words and writes its indices. Status words carry the
 // call's epoch, so they never need clearing between calls.
+#include <algorithm>
+
 #include "internal.h"
 
 namespace fv {
@@ -199,6 +201,39 @@ int launch_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* p
   const int64_t n = (int64_t)H * W;
   FV_TIMED(ctx, FV_KC_MASK, tau_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(p, tau));
   FV_CHECK_LAUNCH("tau_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+// Naive renderer lane list (render_sparse_naive, renderer.py:225-259): one warp per 64-pixel chunk;
+// an occupied chunk appends all its pixels (idle ones as -(pix+1)), contiguous in the list so each
+// chunk still maps onto two warps of the thread-per-lane marcher.
+__global__ void naive_list_kernel(const uint8_t* __restrict__ bits, int64_t n, int32_t* __restrict__ idx,
+                                  int32_t* __restrict__ k_dev) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_chunks = (n + kChunkNaive - 1) / kChunkNaive;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n_chunks; c += warps) {
+    const int64_t p0 = c * kChunkNaive + lane, p1 = p0 + 32;
+    const bool b0 = p0 < n && bits[p0], b1 = p1 < n && bits[p1];
+    if (!__any_sync(0xffffffffu, b0 || b1)) continue;
+    const int64_t rem = n - c * kChunkNaive;
+    const int len = rem < kChunkNaive ? (int)rem : kChunkNaive;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(k_dev, len);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (p0 < n) idx[base + lane] = b0 ? (int32_t)p0 : -(int32_t)p0 - 1;
+    if (p1 < n) idx[base + 32 + lane] = b1 ? (int32_t)p1 : -(int32_t)p1 - 1;
+  }
+}
+
+int launch_naive_list(fv_ctx* ctx, const uint8_t* bits, int H, int W, int32_t* idx, int32_t* k_dev) {
+  const int64_t n = (int64_t)H * W;
+  FV_CUDA(cudaMemsetAsync(k_dev, 0, sizeof(int32_t), ctx->stream));
+  const int64_t chunks = (n + kChunkNaive - 1) / kChunkNaive;
+  const int blocks = (int)std::min<int64_t>((chunks * 32 + 255) / 256, (int64_t)ctx->num_sms * 8);
+  FV_TIMED(ctx, FV_KC_MASK, naive_list_kernel<<<blocks, 256, 0, ctx->stream>>>(bits, n, idx, k_dev));
+  FV_CHECK_LAUNCH("naive_list_kernel");
   ctx->launches += 1;
   return 0;
 }

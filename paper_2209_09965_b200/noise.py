@@ -52,6 +52,25 @@ class NoiseStack:
         return self.values.shape[1], self.values.shape[2]
 
 
+def _rank_values(order_r: np.ndarray, n: int, shape: tuple[int, int]) -> np.ndarray:
+    """rank-per-site array -> values (r+0.5)/n reshaped to (H, W) (noise.py:60-62)."""
+    return ((order_r.astype(np.float64) + 0.5) / n).reshape(shape).astype(np.float32)
+
+
+def gen_uniform_noise(h: int, w: int, t: int = 1, seed: int = 0) -> NoiseStack:
+    """Independent random rank permutation per frame (noise.py:65-75): the film-sized white-noise
+    stack of the compression sweep. Host-side input generation (NumPy's PCG64 stream, as the
+    reference), uploaded by the mask kernel like any stack."""
+    if h < 8 or w < 8:
+        raise ValueError(f"noise dims must be >= 8, got {h}x{w}")
+    rng = np.random.default_rng(seed)
+    n = h * w
+    frames = np.empty((t, h, w), dtype=np.float32)
+    for k in range(t):
+        frames[k] = _rank_values(rng.permutation(n), n, (h, w))
+    return NoiseStack(values=frames, seed=seed)
+
+
 def save_stack(stack: NoiseStack, path: str | Path) -> None:
     """RNKSTACK cache: magic, (H, W, T, seed, sigma_s, sigma_t), float32 payload."""
     t = stack.values.shape[0]

@@ -178,6 +178,78 @@ def render_sparse_compact(scene: Scene, cam: Camera, compact: CompactIndexList,
                        mask=scatter(compact), stats=st)
 
 
+WARP_CHUNK = 64  # lanes per naive-mode execution group (renderer.py:34)
+
+
+def render_sparse_naive(scene: Scene, cam: Camera, mask: SampleMask,
+                        settings: RenderSettings = RenderSettings(), stats: bool = False) -> SparseFrame:
+    """Thread-per-pixel march over every pixel of each occupied WARP_CHUNK-pixel chunk; lanes whose
+    bit is clear idle and stay zero (renderer.py:225-259). Cost tracks occupied chunks, not set bits:
+    the uncompacted baseline of the compression sweep."""
+    import torch
+
+    if mask.dims != (cam.height, cam.width):
+        raise ValueError(f"mask dims {mask.dims} != film {cam.height}x{cam.width}")
+    ctx = _lib.context()
+    vol = scene.volume.handle(ctx, scene.tf)
+    h, w = cam.height, cam.width
+    rgba = torch.zeros((h, w, 4), dtype=torch.float32, device="cuda")
+    depth = torch.zeros((h, w), dtype=torch.float32, device="cuda")
+    idx = torch.empty((h * w,), dtype=torch.int32, device="cuda")
+    k = torch.empty((1,), dtype=torch.int32, device="cuda")
+    st = _lib.FvStats() if stats else None
+    camc, setc = cam.c_struct(), settings.c_struct()
+    lightc = scene.light.c_struct() if scene.light is not None else None
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(ctx.stream)
+    _lib.check(ctx.lib.fv_render_sparse_naive(
+        ctx.h, vol, C.byref(camc), C.byref(lightc) if lightc else None, C.byref(setc),
+        _lib.ptr(mask.bits_dev.contiguous()), _lib.ptr(idx), _lib.ptr(k), _lib.ptr(rgba), _lib.ptr(depth),
+        C.byref(st) if st is not None else None))
+    ev1.record(ctx.stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    return SparseFrame(rgba, depth, render_ms=ms, total_ms=ms, work_items=int(k.item()), mask=mask,
+                       stats=st)
+
+
+def render_sparse_direct(scene: Scene, cam: Camera, positions,
+                         settings: RenderSettings = RenderSettings(), stats: bool = False) -> SparseFrame:
+    """Render stochastically drawn (u, v) positions; duplicates are recomputed (renderer.py:291-314)."""
+    import torch
+
+    pos = np.asarray(positions, dtype=np.int64).reshape(-1, 2)
+    h, w = cam.height, cam.width
+    if pos.size and (pos[:, 0].min() < 0 or pos[:, 1].min() < 0 or pos[:, 0].max() >= w
+                     or pos[:, 1].max() >= h):
+        raise IndexError("direct sample positions out of film range")
+    ctx = _lib.context()
+    vol = scene.volume.handle(ctx, scene.tf)
+    rgba = torch.zeros((h, w, 4), dtype=torch.float32, device="cuda")
+    depth = torch.zeros((h, w), dtype=torch.float32, device="cuda")
+    n = int(pos.shape[0])
+    idx = torch.as_tensor((pos[:, 1] * w + pos[:, 0]).astype(np.int32), device="cuda")
+    k = torch.tensor([n], dtype=torch.int32, device="cuda")
+    st = _lib.FvStats() if stats else None
+    camc, setc = cam.c_struct(), settings.c_struct()
+    lightc = scene.light.c_struct() if scene.light is not None else None
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(ctx.stream)
+    if n:
+        _lib.check(ctx.lib.fv_render_sparse(
+            ctx.h, vol, C.byref(camc), C.byref(lightc) if lightc else None, C.byref(setc),
+            _lib.ptr(idx), _lib.ptr(k), n, _lib.ptr(rgba), _lib.ptr(depth), None,
+            C.byref(st) if st is not None else None))
+    ev1.record(ctx.stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    bits = np.zeros((h, w), dtype=bool)
+    if n:
+        bits[pos[:, 1], pos[:, 0]] = True
+    return SparseFrame(rgba, depth, render_ms=ms, total_ms=ms, work_items=n, mask=SampleMask(bits=bits),
+                       stats=st)
+
+
 @dataclass(frozen=True)
 class OrbitPathSpec:
     """Oscillating-zoom orbit around the volume centre (renderer.py:317-339)."""

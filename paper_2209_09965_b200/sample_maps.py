@@ -115,7 +115,7 @@ class TauMap:
 
         if self._dev is None:
             if self._host is not None:
-                self._dev = torch.as_tensor(self._host, device="cuda")
+                self._dev = torch.as_tensor(np.array(self._host), device="cuda")  # writable copy
             else:
                 ctx = _lib.context()
                 h, w = self.dims
@@ -184,7 +184,8 @@ class SampleMask:
         return self._host
 
     def density(self) -> float:
-        return float(self._dev.float().mean().item())
+        """Fraction of set bits: exact count / pixels in fp64, as numpy's bool mean."""
+        return int(self._dev.sum(dtype=__import__("torch").int64).item()) / self._dev.numel()
 
 
 def build_sample_mask(noise: NoiseStack, frame: int, tau: TauMap) -> SampleMask:
@@ -298,3 +299,37 @@ def scatter(compact: CompactIndexList, frame: int = 0) -> SampleMask:
     if k:
         bits[compact.idx_dev[:k].long()] = 1
     return SampleMask(frame=frame, bits_dev=bits.reshape(h, w), compact=compact)
+
+
+def draw_direct_samples(cfg: FoveaConfig, noise_frame, count: int, rng: np.random.Generator) -> np.ndarray:
+    """Stochastic pixel positions with probability proportional to tau (sample_maps.py:181-198).
+
+    Inverse-CDF sampling over the fp64 tau map (computed on the GPU, fv_tau_map) with NumPy's
+    generator on the host, so the draws follow the reference's random stream. Duplicates are
+    expected: that is direct sampling's documented weakness versus compaction. Returns (count, 2)
+    int64 (u, v)."""
+    if count < 1:
+        raise ValueError(f"count must be >= 1, got {count}")
+    h, w = np.asarray(noise_frame).shape
+    tau = build_tau_map(cfg, (h, w)).values.ravel()
+    cdf = np.cumsum(tau)
+    cdf /= cdf[-1]
+    idx = np.searchsorted(cdf, rng.random(count), side="right")
+    idx = np.minimum(idx, h * w - 1)
+    return np.stack([idx % w, idx // w], axis=1).astype(np.int64)
+
+
+def cmax_sweep_rows(settings: list[tuple[float, float]], noise: NoiseStack, dims: tuple[int, int],
+                    focus: tuple[float, float] | None = None) -> list[tuple]:
+    """(P_b, sigma, c_max, measured_density) rows over the noise loop (sample_maps.py:209-223); the
+    masks come from the fused mask kernel."""
+    h, w = dims
+    if focus is None:
+        focus = ((w - 1) / 2.0, (h - 1) / 2.0)
+    rows = []
+    for pb, sigma in settings:
+        cfg = FoveaConfig(focus=focus, sigma=sigma, base_density=pb)
+        tau = build_tau_map(cfg, dims)
+        dens = np.mean([build_sample_mask(noise, f, tau).density() for f in range(noise.frames)])
+        rows.append((pb, sigma, c_max(tau), float(dens)))
+    return rows

@@ -18,9 +18,9 @@ from . import _lib
 from .network import WNetParams, load_network, quantized_net
 from .noise import NoiseStack, default_stack
 from .pipeline import FramePipeline
-from .renderer import OrbitPathSpec, RenderSettings, Scene, orbit_cameras
+from .renderer import OrbitPathSpec, RenderSettings, Scene, orbit_cameras, render_full, render_sparse_compact
 from .sample_maps import FAST_PRESET, HIFI_PRESET, FoveaConfig, pixel_scale_for_film
-from .volume import Light, TransferFunction, make_procedural_volume
+from .volume import Camera, Light, TransferFunction, make_procedural_volume
 
 DATASETS = ("sphere_shells", "vortex_field", "box_lattice")
 MODES = ("ovr", "fast", "hifi")
@@ -124,6 +124,59 @@ def cmd_bench_throughput(spec: ExperimentSpec, checkpoint=None, noise: NoiseStac
         _write_csv(out / f"{spec.dataset}_{spec.mode}_summary.csv",
                    ["dataset", "mode", "mean_total_ms", "std_total_ms"],
                    [(spec.dataset, spec.mode, float(np.mean(totals)), float(np.std(totals)))], echo)
+    return rows
+
+
+def cmd_bench_cmax(taus=(0.01, 0.03, 0.05, 0.1, 0.2, 0.5, 1.0), dims: tuple[int, int] = (180, 320),
+                   repeats: int = 3, dataset: str = "vortex_field", out_dir: str | Path | None = "bench_out",
+                   volume_dims: tuple[int, int, int] = (48, 48, 48), seed: int = 0) -> list[tuple]:
+    """Frame time vs uniform threshold for the naive and compacted renderers (bench.py:111-163).
+
+    Film-sized uniform rank noise, so the work-item count is round(tau*H*W) up to rounding. Each
+    render is timed on the device (CUDA events, median of warm repeats). Returns the CSV rows
+    (tau, t_naive_ms, t_compact_ms, c_max, t_full_ms, work_items, mean_compact_ms, std_compact_ms);
+    with out_dir, writes cmax/cmax_sweep.csv and cmax/cmax_settings.csv as the reference does.
+    """
+    from .noise import gen_uniform_noise
+    from .renderer import render_sparse_naive
+    from .sample_maps import TauMap, build_sample_mask, c_max, cmax_sweep_rows, compact_mask
+
+    if min(taus) <= 0 or max(taus) > 1:
+        raise ValueError("taus must lie in (0, 1]")
+    h, w = dims
+    scene = default_scene(dataset, volume_dims)
+    center = scene.volume.center()
+    diag = float(np.linalg.norm(scene.volume.extent))
+    cam = Camera(position=tuple(center + diag * np.array([1.0, 0.7, 1.2])), look_at=tuple(center),
+                 fov_y=40.0, width=w, height=h)
+    noise = gen_uniform_noise(h, w, 2, seed=seed)
+    settings = RenderSettings()
+    render_full(scene, cam, settings)  # warm-up (brick cache, context)
+    t_full = min(render_full(scene, cam, settings).render_ms for _ in range(repeats))
+    rows = []
+    for tau in taus:
+        tmap = TauMap(values=np.full((h, w), float(tau)))
+        mask = build_sample_mask(noise, 0, tmap)
+        comp = compact_mask(mask)
+        render_sparse_naive(scene, cam, mask, settings)
+        render_sparse_compact(scene, cam, comp, settings)
+        naive_ts = [render_sparse_naive(scene, cam, mask, settings).render_ms for _ in range(repeats)]
+        compact_ts = [render_sparse_compact(scene, cam, comp, settings).render_ms for _ in range(repeats)]
+        rows.append((tau, float(np.median(naive_ts)), float(np.median(compact_ts)), c_max(tmap), t_full,
+                     comp.count, float(np.mean(compact_ts)), float(np.std(compact_ts))))
+    if out_dir is not None:
+        echo = {"taus": list(taus), "dims": list(dims), "repeats": repeats, "dataset": dataset,
+                "volume_dims": list(volume_dims), "seed": seed, "device": "cuda",
+                "timing": "median of warm repeats, CUDA events around each render, ms"}
+        out = Path(out_dir) / "cmax"
+        _write_csv(out / "cmax_sweep.csv",
+                   ["tau", "t_naive_ms", "t_compact_ms", "c_max", "t_full_ms", "work_items",
+                    "mean_compact_ms", "std_compact_ms"], rows, echo)
+        settings_rows = cmax_sweep_rows(
+            [(FAST_PRESET["base_density"], FAST_PRESET["sigma"]),
+             (HIFI_PRESET["base_density"], HIFI_PRESET["sigma"]), (0.01, 0.02), (0.10, 0.02)],
+            default_stack(), dims)
+        _write_csv(out / "cmax_settings.csv", ["p_b", "sigma", "c_max", "measured_density"], settings_rows, echo)
     return rows
 
 

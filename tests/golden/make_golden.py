@@ -18,6 +18,8 @@ Outputs (all under tests/golden/ unless noted):
   render_small.npz      render_full / render_sparse_compact outputs on small scenes
   net_small.npz         forward_full outputs (desk + paper nets, carried state)
   e2e_c1.npz            config C1 (64^3, 256x256, fast) mask -> march -> fp16 net, 2 frames
+  sweep_small.npz       compression sweep pieces: uniform noise, direct draws, naive/direct
+                        renders, foveated-settings density rows
 """
 from __future__ import annotations
 
@@ -186,6 +188,35 @@ def gen_renders(stack):
     print("renders done")
 
 
+def gen_sweep(stack):
+    """Compression-sweep inputs and outputs: uniform noise, direct draws, naive/direct renders,
+    foveated-settings density rows (bench.cmd_bench_cmax's building blocks)."""
+    out = {}
+    un = rn.gen_uniform_noise(12, 16, 2, seed=5)
+    out["uniform_12x16_s5"] = un.values
+    cfg = rsm.FoveaConfig(focus=(20.0, 11.0), sigma=0.06, base_density=0.07, pixel_scale=0.125)
+    out["direct_pos"] = rsm.draw_direct_samples(cfg, np.zeros((24, 40)), 400, np.random.default_rng(11))
+    scene = test_scene()
+    cam = rv.Camera(position=(80.0, 60.0, 90.0), look_at=(16.0, 16.0, 16.0), fov_y=40.0,
+                    width=64, height=36)
+    un2 = rn.gen_uniform_noise(36, 64, 1, seed=2)
+    for tau in (0.02, 0.2):
+        mask = rsm.build_sample_mask(un2, 0, rsm.TauMap(values=np.full((36, 64), tau)))
+        nv = rr.render_sparse_naive(scene, cam, mask)
+        key = f"naive{int(tau * 100)}"
+        out[key + "_rgba"], out[key + "_depth"], out[key + "_bits"] = nv.rgba, nv.depth, mask.bits
+        out[key + "_work"] = np.array(nv.work_items)
+    pos = rsm.draw_direct_samples(rsm.FoveaConfig(focus=(32.0, 18.0), sigma=0.3, base_density=0.1,
+                                                  pixel_scale=0.2), np.zeros((36, 64)), 300,
+                                  np.random.default_rng(3))
+    dr = rr.render_sparse_direct(scene, cam, pos)
+    out["direct64_pos"], out["direct64_rgba"], out["direct64_depth"] = pos, dr.rgba, dr.depth
+    rows = rsm.cmax_sweep_rows([(0.03, 0.02), (0.07, 0.06), (0.01, 0.02), (0.10, 0.02)], stack, (90, 160))
+    out["cmax_rows"] = np.array(rows, dtype=np.float64)
+    np.savez_compressed(HERE / "sweep_small.npz", **out)
+    print("sweep done")
+
+
 def gen_net():
     out = {}
     rng = np.random.default_rng(77)
@@ -250,7 +281,7 @@ def main():
     stack = rn.default_stack()
     rn.save_stack(stack, DATA / "stbn_64x64x8_s1.noise")
     print(f"stbn sha {sha(stack.values.astype('<f4').tobytes())}")
-    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1"}
+    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep"}
     if "masks" in which:
         gen_masks(stack)
     if "volumes" in which:
@@ -261,6 +292,8 @@ def main():
         gen_net()
     if "c1" in which:
         gen_c1(stack)
+    if "sweep" in which:
+        gen_sweep(stack)
     print(f"done in {time.perf_counter() - t0:.1f}s")
 
 

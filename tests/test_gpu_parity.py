@@ -439,3 +439,55 @@ def test_frames_to_host_equals_frame_by_frame(stack):
     for i, (a, b) in enumerate(zip(outs, ref)):
         assert np.array_equal(a.numpy(), b), i
     assert float(np.abs(ref[-1]).sum()) > 0
+
+
+# ---------------------------------------------------------------- compression sweep
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_render_sparse_naive_vs_reference_golden(golden, scene32, prec):
+    """Naive renderer: same pixels as compaction, zeros elsewhere, work = lanes of occupied
+    64-pixel chunks (renderer.py:225-259)."""
+    from paper_2209_09965_b200.renderer import render_sparse_naive
+
+    g = np.load(golden / "sweep_small.npz")
+    for key in ("naive2", "naive20"):
+        bits = g[key + "_bits"]
+        fr = render_sparse_naive(scene32, Camera(**CAM), S.SampleMask(bits=bits), RenderSettings(precision=prec))
+        if prec == "fp64":
+            assert np.abs(fr.rgba - g[key + "_rgba"]).max() <= 1e-9
+            assert np.abs(fr.depth - g[key + "_depth"]).max() <= 1e-6
+        else:
+            check_fp32(fr.rgba, g[key + "_rgba"])
+        assert np.all(fr.rgba[~bits] == 0)
+        assert fr.work_items == int(g[key + "_work"])
+
+
+def test_render_sparse_direct_and_draws_vs_reference_golden(golden, scene32):
+    from paper_2209_09965_b200.renderer import render_sparse_direct
+
+    g = np.load(golden / "sweep_small.npz")
+    cfg = S.FoveaConfig(focus=(20.0, 11.0), sigma=0.06, base_density=0.07, pixel_scale=0.125)
+    pos = S.draw_direct_samples(cfg, np.zeros((24, 40)), 400, np.random.default_rng(11))
+    assert np.array_equal(pos, g["direct_pos"])
+    fr = render_sparse_direct(scene32, Camera(**CAM), g["direct64_pos"], RenderSettings(precision="fp64"))
+    assert np.abs(fr.rgba - g["direct64_rgba"]).max() <= 1e-9
+    assert fr.work_items == g["direct64_pos"].shape[0]
+
+
+def test_cmax_rows_and_sweep(golden, stack, tmp_path):
+    from paper_2209_09965_b200.noise import gen_uniform_noise
+    from paper_2209_09965_b200.throughput import cmd_bench_cmax
+
+    g = np.load(golden / "sweep_small.npz")
+    assert np.array_equal(gen_uniform_noise(12, 16, 2, seed=5).values, g["uniform_12x16_s5"])
+    rows = S.cmax_sweep_rows([(0.03, 0.02), (0.07, 0.06), (0.01, 0.02), (0.10, 0.02)], stack, (90, 160))
+    for got, ref in zip(rows, g["cmax_rows"]):
+        assert got[0] == ref[0] and got[1] == ref[1] and got[3] == ref[3]
+        assert abs(got[2] - ref[2]) <= 1e-12
+    taus = (0.05, 0.5, 1.0)
+    out = cmd_bench_cmax(taus=taus, dims=(36, 64), repeats=1, dataset="sphere_shells", out_dir=tmp_path,
+                         volume_dims=(32, 32, 32), seed=0)
+    noise = gen_uniform_noise(36, 64, 2, seed=0).values[0].astype(np.float64)
+    for tau, row in zip(taus, out):
+        assert row[0] == tau and row[5] == int((noise < tau).sum())
+        assert row[1] > 0 and row[2] > 0 and row[4] > 0
+    assert (tmp_path / "cmax" / "cmax_sweep.csv").exists() and (tmp_path / "cmax" / "cmax_settings.csv").exists()

@@ -134,3 +134,37 @@ def test_psnr_ssim_identity():
     a = np.random.default_rng(0).random((32, 32, 3))
     assert O.psnr(a, a) == 100.0
     assert O.ssim(a, a) == pytest.approx(1.0)
+
+
+# ---------------------------------------------------------------- compression sweep pieces
+def test_uniform_noise_and_direct_draws_match_reference(golden):
+    g = np.load(golden / "sweep_small.npz")
+    assert np.array_equal(O.uniform_noise(12, 16, 2, seed=5), g["uniform_12x16_s5"])
+    tau = O.tau_map(24, 40, (20.0, 11.0), 0.06, 0.07, 0.125)
+    assert np.array_equal(O.direct_samples(tau, 400, np.random.default_rng(11)), g["direct_pos"])
+
+
+def test_naive_and_direct_renders_match_reference(golden):
+    g = np.load(golden / "sweep_small.npz")
+    for key in ("naive2", "naive20"):
+        bits = g[key + "_bits"]
+        rgba, depth = O.render_image(_scene32(), (1, 1, 1), O.DEFAULT_LUT, LIGHT, CAM, bits=bits)
+        assert np.array_equal(rgba, g[key + "_rgba"]) and np.array_equal(depth, g[key + "_depth"])
+        assert O.naive_lanes(bits).size == int(g[key + "_work"])
+    pos = g["direct64_pos"]
+    flat = np.unique(pos[:, 1] * CAM["width"] + pos[:, 0])
+    bits = np.zeros(CAM["height"] * CAM["width"], bool)
+    bits[flat] = True
+    rgba, depth = O.render_image(_scene32(), (1, 1, 1), O.DEFAULT_LUT, LIGHT, CAM,
+                                 bits=bits.reshape(CAM["height"], CAM["width"]))
+    assert np.array_equal(rgba, g["direct64_rgba"]) and np.array_equal(depth, g["direct64_depth"])
+
+
+def test_cmax_settings_rows_match_reference(golden, stack_values):
+    g = np.load(golden / "sweep_small.npz")
+    h, w = 90, 160
+    for pb, sigma, cm, dens in g["cmax_rows"]:
+        tau = O.tau_map(h, w, ((w - 1) / 2.0, (h - 1) / 2.0), sigma, pb, 1.0 / 32.0)
+        d = np.mean([O.sample_mask(stack_values, h, w, f, tau).mean() for f in range(stack_values.shape[0])])
+        assert d == dens
+        assert abs(float(np.mean(tau)) - cm) <= 1e-12
