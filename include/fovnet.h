@@ -245,6 +245,18 @@ FV_API int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_sta
              const fv_camera* cam, const fv_light* light, const fv_settings* settings,
              const fv_fovea* fovea, int frame, float* host_rgb_out, double* timings_ms);
 
+/* ---- quality metrics on the device (metrics.py:40-148), fp64 ---------------------------- */
+/* Images are (H,W,C) float64 device arrays, C >= 3 (RGB = channels 0..2; SSIM also takes C == 1
+ * luma). fv_metric_sqdiff: sum over pixels and RGB of (a-b)^2 -> *sum_out (host); with a_prev and
+ * b_prev it sums the tPSNR differences ((a-a_prev+1)/2 - (b-b_prev+1)/2)^2 (metrics.py:133-148).
+ * fv_metric_ssim: mode 0 = mean SSIM over valid 11x11 windows of Rec.601 luma (metrics.py:74-87);
+ * mode 1 = MS-SSIM over `scales` scales with the given renormalised weights (metrics.py:104-130).
+ * Reductions are deterministic (fixed block partials summed in order). */
+FV_API int fv_metric_sqdiff(fv_ctx* ctx, const double* a, const double* b, const double* a_prev,
+                            const double* b_prev, int H, int W, int ca, int cb, double* sum_out);
+FV_API int fv_metric_ssim(fv_ctx* ctx, const double* a, const double* b, int H, int W, int ca, int cb,
+                          int mode, int scales, const double* weights, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -417,5 +417,68 @@ def ssim(a, b) -> float:
     return float(s.mean())
 
 
+def _ssim_maps(la, lb):
+    from numpy.lib.stride_tricks import sliding_window_view
+
+    d = np.arange(11, dtype=np.float64) - 5.0
+    k = np.exp(-(d * d) / (2 * 1.5 * 1.5))
+    k /= k.sum()
+
+    def filt(im):
+        rows = sliding_window_view(im, 11, axis=0) @ k
+        return sliding_window_view(rows, 11, axis=1) @ k
+
+    mu_a, mu_b = filt(la), filt(lb)
+    va = filt(la * la) - mu_a * mu_a
+    vb = filt(lb * lb) - mu_b * mu_b
+    cov = filt(la * lb) - mu_a * mu_b
+    c1, c2 = 0.01 ** 2, 0.03 ** 2
+    cs = (2 * cov + c2) / (va + vb + c2)
+    lum = (2 * mu_a * mu_b + c1) / (mu_a * mu_a + mu_b * mu_b + c1)
+    return lum, cs
+
+
+def _luma(img):
+    img = np.asarray(img, np.float64)
+    if img.ndim == 2:
+        return img
+    return 0.299 * img[..., 0] + 0.587 * img[..., 1] + 0.114 * img[..., 2]
+
+
+def msssim(a, b) -> float:
+    """metrics.msssim (metrics.py:96-130): scales while the coarse image keeps an 11px window,
+    weights renormalised, contrast-structure means clamped at 0, 2x2 mean downsampling."""
+    wts_all = (0.0448, 0.2856, 0.3001, 0.2363, 0.1333)
+    la, lb = _luma(a), _luma(b)
+    m, size = 1, min(la.shape)
+    while m < len(wts_all) and size // 2 >= 11:
+        size //= 2
+        m += 1
+    wts = np.asarray(wts_all[:m])
+    wts = wts / wts.sum()
+    value = 1.0
+    for j in range(m):
+        lum, cs = _ssim_maps(la, lb)
+        stat = float((lum * cs).mean()) if j == m - 1 else float(cs.mean())
+        value *= max(stat, 0.0) ** wts[j]
+        if j < m - 1:
+            h, w = la.shape
+            la = la[: h // 2 * 2, : w // 2 * 2]
+            lb = lb[: h // 2 * 2, : w // 2 * 2]
+            la = 0.25 * (la[0::2, 0::2] + la[1::2, 0::2] + la[0::2, 1::2] + la[1::2, 1::2])
+            lb = 0.25 * (lb[0::2, 0::2] + lb[1::2, 0::2] + lb[0::2, 1::2] + lb[1::2, 1::2])
+    return float(value)
+
+
+def tpsnr(seq_a, seq_b) -> np.ndarray:
+    """metrics.tpsnr (metrics.py:133-148): PSNR of (d+1)/2 temporal differences."""
+    out = np.empty(len(seq_a) - 1)
+    for i in range(1, len(seq_a)):
+        da = (np.asarray(seq_a[i], np.float64)[..., :3] - np.asarray(seq_a[i - 1], np.float64)[..., :3] + 1.0) / 2.0
+        db = (np.asarray(seq_b[i], np.float64)[..., :3] - np.asarray(seq_b[i - 1], np.float64)[..., :3] + 1.0) / 2.0
+        out[i - 1] = psnr(da, db)
+    return out
+
+
 def threads() -> int:
     return len(os.sched_getaffinity(0))

@@ -162,9 +162,9 @@ class SampleMask:
             if b.ndim != 2 or b.dtype != np.bool_:
                 raise ValueError("mask bits must be a 2D bool array")
             b = b.copy()
+            self._dev = torch.as_tensor(b.view(np.uint8), device="cuda")
             b.setflags(write=False)
             self._host = b
-            self._dev = torch.as_tensor(b.view(np.uint8), device="cuda")
 
     @property
     def dims(self) -> tuple[int, int]:

@@ -18,6 +18,7 @@ Outputs (all under tests/golden/ unless noted):
   render_small.npz      render_full / render_sparse_compact outputs on small scenes
   net_small.npz         forward_full outputs (desk + paper nets, carried state)
   e2e_c1.npz            config C1 (64^3, 256x256, fast) mask -> march -> fp16 net, 2 frames
+  metrics_small.npz     PSNR / SSIM / MS-SSIM / tPSNR / quality-report values on seeded images
   sweep_small.npz       compression sweep pieces: uniform noise, direct draws, naive/direct
                         renders, foveated-settings density rows
 """
@@ -217,6 +218,34 @@ def gen_sweep(stack):
     print("sweep done")
 
 
+def metrics_inputs():
+    """Seeded inputs of the metric fixtures (rebuilt identically by the tests: PCG64 streams)."""
+    rng = np.random.default_rng(21)
+    a = rng.random((64, 80, 3))
+    b = np.clip(a + 0.05 * rng.standard_normal(a.shape), 0, 1)
+    yy, xx = np.mgrid[0:192, 0:256]
+    big_a = np.stack([np.exp(-((xx - 90 - 20 * c) ** 2 + (yy - 100) ** 2) / 3000.0) for c in range(3)], -1)
+    big_b = np.clip(big_a + 0.02 * rng.standard_normal(big_a.shape), 0, 1)
+    s = a[:32, :40]
+    seq_p = [np.clip(s + 0.03 * k + 0.02 * rng.standard_normal(s.shape), 0, 1) for k in range(4)]
+    seq_g = [np.clip(s + 0.03 * k, 0, 1) for k in range(4)]
+    return a, b, big_a, big_b, seq_p, seq_g
+
+
+def gen_metrics():
+    """metrics.psnr / ssim / msssim / tpsnr / build_quality_report on seeded images."""
+    from fovray import metrics as rm
+
+    a, b, big_a, big_b, seq_p, seq_g = metrics_inputs()
+    vals = [rm.psnr(a, b), rm.ssim(a, b), rm.msssim(a, b), rm.psnr(big_a, big_b), rm.ssim(big_a, big_b),
+            rm.msssim(big_a, big_b), rm.psnr(a, a), rm.ssim(a, a), rm.msssim(a, 1.0 - a),
+            rm.ssim(a[..., 0], b[..., 0]), rm.psnr(a, b, peak=2.0)]
+    rep = rm.build_quality_report(seq_p, seq_g)
+    np.savez_compressed(HERE / "metrics_small.npz", values=np.array(vals),
+                        rep=np.stack([rep.psnr, rep.ssim, rep.msssim, rep.tpsnr]))
+    print("metrics done")
+
+
 def gen_net():
     out = {}
     rng = np.random.default_rng(77)
@@ -281,7 +310,7 @@ def main():
     stack = rn.default_stack()
     rn.save_stack(stack, DATA / "stbn_64x64x8_s1.noise")
     print(f"stbn sha {sha(stack.values.astype('<f4').tobytes())}")
-    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep"}
+    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep", "metrics"}
     if "masks" in which:
         gen_masks(stack)
     if "volumes" in which:
@@ -294,6 +323,8 @@ def main():
         gen_c1(stack)
     if "sweep" in which:
         gen_sweep(stack)
+    if "metrics" in which:
+        gen_metrics()
     print(f"done in {time.perf_counter() - t0:.1f}s")
 
 

@@ -491,3 +491,28 @@ def test_cmax_rows_and_sweep(golden, stack, tmp_path):
         assert row[0] == tau and row[5] == int((noise < tau).sum())
         assert row[1] > 0 and row[2] > 0 and row[4] > 0
     assert (tmp_path / "cmax" / "cmax_sweep.csv").exists() and (tmp_path / "cmax" / "cmax_settings.csv").exists()
+
+
+# ---------------------------------------------------------------- quality metrics
+def test_device_metrics_vs_reference_golden(golden):
+    from conftest import metrics_inputs
+    from paper_2209_09965_b200 import metrics as M
+
+    g = np.load(golden / "metrics_small.npz")
+    a, b, big_a, big_b, seq_p, seq_g = metrics_inputs()
+    got = [M.psnr(a, b), M.ssim(a, b), M.msssim(a, b), M.psnr(big_a, big_b), M.ssim(big_a, big_b),
+           M.msssim(big_a, big_b), M.psnr(a, a), M.ssim(a, a), M.msssim(a, 1.0 - a),
+           M.ssim(a[..., 0], b[..., 0]), M.psnr(a, b, peak=2.0)]
+    np.testing.assert_allclose(got, g["values"], rtol=1e-10, atol=1e-12)
+    assert got[6] == 100.0
+    rep = M.build_quality_report(seq_p, [torch.as_tensor(x, device="cuda") for x in seq_g])
+    ref = g["rep"]
+    np.testing.assert_allclose(rep.psnr, ref[0], rtol=1e-10)
+    np.testing.assert_allclose(rep.ssim, ref[1], rtol=1e-10)
+    np.testing.assert_allclose(rep.msssim, ref[2], rtol=1e-10)
+    assert np.isnan(rep.tpsnr[0]) and np.isnan(ref[3][0])
+    np.testing.assert_allclose(rep.tpsnr[1:], ref[3][1:], rtol=1e-10)
+    with pytest.raises(ValueError):
+        M.ssim(a[:8], b[:8])
+    with pytest.raises(ValueError):
+        M.psnr(a, b[:10])

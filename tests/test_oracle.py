@@ -168,3 +168,16 @@ def test_cmax_settings_rows_match_reference(golden, stack_values):
         d = np.mean([O.sample_mask(stack_values, h, w, f, tau).mean() for f in range(stack_values.shape[0])])
         assert d == dens
         assert abs(float(np.mean(tau)) - cm) <= 1e-12
+
+
+# ---------------------------------------------------------------- quality metrics
+def test_metric_restatements_match_reference(golden):
+    from conftest import metrics_inputs
+
+    g = np.load(golden / "metrics_small.npz")
+    a, b, big_a, big_b, seq_p, seq_g = metrics_inputs()
+    got = [O.psnr(a, b), O.ssim(a, b), O.msssim(a, b), O.psnr(big_a, big_b), O.ssim(big_a, big_b),
+           O.msssim(big_a, big_b), O.psnr(a, a), O.ssim(a, a), O.msssim(a, 1.0 - a),
+           O.ssim(np.stack([a[..., 0]] * 3, -1), np.stack([b[..., 0]] * 3, -1)), O.psnr(a, b, peak=2.0)]
+    np.testing.assert_allclose(got, g["values"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(O.tpsnr(seq_p, seq_g), g["rep"][3, 1:], rtol=1e-12)
