@@ -245,6 +245,11 @@ FV_API int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_sta
              const fv_camera* cam, const fv_light* light, const fv_settings* settings,
              const fv_fovea* fovea, int frame, float* host_rgb_out, double* timings_ms);
 
+/* pngio.to_uint8 (pngio.py:11-12) on the device: (clip(x,0,1)*255 + 0.5) truncated, fp32 without FMA
+ * contraction; in_dev addressed by element strides (HWC RGB/RGBA or CHW), out_dev (H,W,3) uint8. */
+FV_API int fv_pack_rgb8(fv_ctx* ctx, const float* in_dev, int H, int W, int64_t stride_y, int64_t stride_x,
+                        int64_t stride_c, uint8_t* out_dev);
+
 /* ---- quality metrics on the device (metrics.py:40-148), fp64 ---------------------------- */
 /* Images are (H,W,C) float64 device arrays, C >= 3 (RGB = channels 0..2; SSIM also takes C == 1
  * luma). fv_metric_sqdiff: sum over pixels and RGB of (a-b)^2 -> *sum_out (host); with a_prev and

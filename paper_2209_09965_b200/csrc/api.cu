@@ -24,6 +24,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 int pack_input(fv_ctx* ctx, fv_state* st, const float* rgba, const uint8_t* bits);
+int pack_rgb8(fv_ctx* ctx, const float* in, int h, int w, int64_t sy, int64_t sx, int64_t sc, uint8_t* out);
 
 }  // namespace fv
 
@@ -366,6 +367,13 @@ int fv_render_full(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, cons
                      rgba_dev, depth_dev, nullptr, cam->width);
   if (rc) return rc;
   return finish_stats(ctx, stats_out, &before);
+}
+
+int fv_pack_rgb8(fv_ctx* ctx, const float* in_dev, int H, int W, int64_t stride_y, int64_t stride_x,
+                 int64_t stride_c, uint8_t* out_dev) {
+  FV_REQUIRE(ctx && in_dev && out_dev, "null argument");
+  FV_REQUIRE(H > 0 && W > 0, "dims must be positive, got (%d, %d)", H, W);
+  return pack_rgb8(ctx, in_dev, H, W, stride_y, stride_x, stride_c, out_dev);
 }
 
 int fv_pack_input(fv_ctx* ctx, fv_state* st, const float* rgba_dev, const uint8_t* bits_dev) {

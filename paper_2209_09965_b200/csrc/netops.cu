@@ -158,6 +158,21 @@ __global__ void __launch_bounds__(128) kapply_final_kernel(const kw_t* __restric
   }
 }
 
+// pngio.to_uint8 (pngio.py:11-12): (clip(x, 0, 1) * 255 + 0.5) truncated, in fp32 without FMA
+// contraction like NumPy; input addressed by element strides so HWC (RGB / RGBA) and CHW both work.
+__global__ void rgb8_kernel(const float* __restrict__ in, int h, int w, int64_t sy, int64_t sx, int64_t sc,
+                            uint8_t* __restrict__ out) {
+  const int64_t n = (int64_t)h * w;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = p / w, x = p % w;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float v = fminf(fmaxf(in[y * sy + x * sx + c * sc], 0.f), 1.f);
+      out[p * 3 + c] = (uint8_t)__float2uint_rz(__fadd_rn(__fmul_rn(v, 255.f), 0.5f));
+    }
+  }
+}
+
 // 3-channel fp32 avg_pool2; grid (ceil(w/128), h, 3), h, w the OUTPUT dims
 __global__ void __launch_bounds__(128) pool3_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                     int h, int w) {
@@ -318,6 +333,14 @@ int kapply_final(fv_ctx* ctx, fv_state* st, const kw_t* kw, const float* img, fl
   FV_TIMED(ctx, FV_KC_NETOPS, kapply_final_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, st->od, st->H, st->W, st->Hp,
                                                                           st->Wp, rgb, o_raw, od_raw));
   FV_CHECK_LAUNCH("kapply_final_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int pack_rgb8(fv_ctx* ctx, const float* in, int h, int w, int64_t sy, int64_t sx, int64_t sc, uint8_t* out) {
+  const int64_t n = (int64_t)h * w;
+  FV_TIMED(ctx, FV_KC_NETOPS, rgb8_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(in, h, w, sy, sx, sc, out));
+  FV_CHECK_LAUNCH("rgb8_kernel");
   ctx->launches += 1;
   return 0;
 }

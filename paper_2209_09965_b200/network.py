@@ -313,6 +313,35 @@ def forward_full(net: WNetParams, sparse_input, state: RecurrentState, use_kerne
     return DeviceTensor(o[None]), DeviceTensor(od[None]), new
 
 
+def forward_sparse(net: WNetParams, rgba, bits, state: RecurrentState, use_kernel_stage: bool = True):
+    """_reconstruct_frame (bench.py:166-175) on device buffers: the input packing x = rgba*m ++ m
+    runs in fv_pack_input straight into the network's NHWC8 input, then the W-Net, and the clipped
+    (H, W, 3) image is written by the output stage. rgba: (H, W, 4) float32 CUDA tensor; bits:
+    (H, W) uint8 CUDA tensor. Returns (rgb (H, W, 3) CUDA tensor in [0, 1], O, O_d, state')."""
+    import torch
+
+    cfg = net.config
+    if not cfg.include_mask_channel:
+        raise ValueError("forward_sparse packs the mask channel; this network has none")
+    h, w = int(rgba.shape[0]), int(rgba.shape[1])
+    if state.film_dims != (h, w):
+        raise ValueError(f"carried state is for {state.film_dims}, input is {(h, w)}; reset the state")
+    ctx = _lib.context()
+    handle = net.handle(ctx)
+    dev = _bind_state(net, state, ctx, handle)
+    rgba = rgba.to(device="cuda", dtype=torch.float32).contiguous()
+    bits = bits.to(device="cuda", dtype=torch.uint8).contiguous()
+    _lib.check(ctx.lib.fv_pack_input(ctx.h, dev.h, _lib.ptr(rgba), _lib.ptr(bits)))
+    rgb = torch.empty((h, w, 3), dtype=torch.float32, device="cuda")
+    o = torch.empty((3, h, w), dtype=torch.float32, device="cuda")
+    od = torch.empty((3, h, w), dtype=torch.float32, device="cuda")
+    _lib.check(ctx.lib.fv_reconstruct(ctx.h, handle, dev.h, int(bool(use_kernel_stage)), _lib.ptr(rgb),
+                                      _lib.ptr(o), _lib.ptr(od)))
+    state._consumed = True
+    new = RecurrentState(film_dims=(h, w), _dev=dev, _config=cfg)
+    return rgb, DeviceTensor(o[None]), DeviceTensor(od[None]), new
+
+
 def detach_state(state: RecurrentState) -> RecurrentState:
     return state
 

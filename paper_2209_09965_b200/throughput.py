@@ -67,8 +67,14 @@ def _reconstruct_frame(net: WNetParams, sparse_rgba, mask_bits, state):
 
     rgba = torch.as_tensor(np.asarray(getattr(sparse_rgba, "rgba", sparse_rgba), dtype=np.float32)
                            if not isinstance(sparse_rgba, torch.Tensor) else sparse_rgba, device="cuda")
-    m = torch.as_tensor(np.asarray(mask_bits) if not isinstance(mask_bits, torch.Tensor) else mask_bits,
-                        device="cuda").to(torch.float32)
+    mb = torch.as_tensor(np.asarray(mask_bits) if not isinstance(mask_bits, torch.Tensor) else mask_bits,
+                         device="cuda")
+    if net.config.include_mask_channel:  # packing + clip on the device (fv_pack_input, output stage)
+        from .network import forward_sparse
+
+        rgb, _, _, state = forward_sparse(net, rgba, mb.to(torch.uint8), state)
+        return rgb.cpu().numpy(), state
+    m = mb.to(torch.float32)
     x = rgba.permute(2, 0, 1)[None] * m[None, None]
     if net.config.include_mask_channel:
         x = torch.cat([x, m[None, None]], dim=1)

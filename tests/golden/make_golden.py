@@ -18,6 +18,7 @@ Outputs (all under tests/golden/ unless noted):
   render_small.npz      render_full / render_sparse_compact outputs on small scenes
   net_small.npz         forward_full outputs (desk + paper nets, carried state)
   e2e_c1.npz            config C1 (64^3, 256x256, fast) mask -> march -> fp16 net, 2 frames
+  viewer_small.npz      viewer.RenderService.render_frame: decoded PNGs + headers, every mode
   metrics_small.npz     PSNR / SSIM / MS-SSIM / tPSNR / quality-report values on seeded images
   sweep_small.npz       compression sweep pieces: uniform noise, direct draws, naive/direct
                         renders, foveated-settings density rows
@@ -246,6 +247,35 @@ def gen_metrics():
     print("metrics done")
 
 
+def gen_viewer(stack):
+    """viewer.RenderService.render_frame messages (decoded PNGs + headers) for every mode."""
+    import io as _io
+
+    from PIL import Image
+    from fovray import bench as rbench
+    from fovray import viewer as rview
+
+    scene = test_scene()
+    net = rbench._quantized_net(rnet.init_network(rnet.NetConfig.from_string(rnet.DESK_BLOCKS), seed=7), "fp16")
+    cam = rv.Camera(position=(80.0, 60.0, 90.0), look_at=(16.0, 16.0, 16.0), fov_y=40.0, width=64, height=36)
+    svc = rview.RenderService(scene, film=(64, 36), checkpoint=net, noise=stack,
+                              settings=rr.RenderSettings(step_size=1.0), camera=cam)
+    out = {}
+    state = rview.default_session((64, 36))
+    plan = [("sparse_raw", {}), ("reconstructed", {}), ("reconstructed", {"focus": [10.0, 30.0], "p_b": 0.2}),
+            ("ground_truth", {}), ("side_by_side", {"sigma": 0.5})]
+    for i, (mode, ctl) in enumerate(plan):
+        msg = dict(ctl, mode=mode)
+        state = rview.handle_control(state, msg, svc.film, has_checkpoint=True)
+        blob, state = svc.render_frame(state)
+        d = rview.parse_frame_message(blob)
+        out[f"img{i}"] = np.asarray(Image.open(_io.BytesIO(d["png"])))
+        out[f"hdr{i}"] = np.array([d["frame_id"], d["width"], d["height"], rview.MODES.index(d["mode"]),
+                                   d["focus"][0], d["focus"][1], d["p_b"], d["sigma"]], dtype=np.float64)
+    np.savez_compressed(HERE / "viewer_small.npz", **out)
+    print("viewer done")
+
+
 def gen_net():
     out = {}
     rng = np.random.default_rng(77)
@@ -310,7 +340,7 @@ def main():
     stack = rn.default_stack()
     rn.save_stack(stack, DATA / "stbn_64x64x8_s1.noise")
     print(f"stbn sha {sha(stack.values.astype('<f4').tobytes())}")
-    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep", "metrics"}
+    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep", "metrics", "viewer"}
     if "masks" in which:
         gen_masks(stack)
     if "volumes" in which:
@@ -325,6 +355,8 @@ def main():
         gen_sweep(stack)
     if "metrics" in which:
         gen_metrics()
+    if "viewer" in which:
+        gen_viewer(stack)
     print(f"done in {time.perf_counter() - t0:.1f}s")
 
 
