@@ -34,6 +34,10 @@ CONFIGS = {
                name="512^3 sphere_shells, 1920x1080, hifi (P_b=0.07, sigma=0.06), FULL_BLOCKS fp16 net"),
     "c2": dict(vol=256, width=1920, height=1080, mode="fast", pb=0.03, sigma=0.02,
                name="256^3 sphere_shells, 1920x1080, fast (P_b=0.03, sigma=0.02), FULL_BLOCKS fp16 net"),
+    "c1": dict(vol=64, width=256, height=256, mode="fast", pb=0.03, sigma=0.02,
+               name="64^3 sphere_shells, 256x256, fast (P_b=0.03, sigma=0.02), FULL_BLOCKS fp16 net"),
+    "c5": dict(vol=1024, width=3840, height=2160, mode="fast", pb=0.03, sigma=0.02,
+               name="1024^3 sphere_shells, 3840x2160, fast (P_b=0.03, sigma=0.02), FULL_BLOCKS fp16 net"),
 }
 PATH_FRAMES = 500
 MAC_PER_PX = 275071.5  # FULL_BLOCKS multiply-accumulates per output pixel
@@ -388,6 +392,90 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+def run_sharded(args, cfg):
+    """One frame stream split across the ranks (config 5: --config c5 --shard): every rank marches
+    its packets of each frame, the records are all-gathered over NCCL, every rank reconstructs.
+    Strong scaling: the job renders K frames whatever N is; time = max over ranks."""
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2209_09965_b200 import _lib
+    from paper_2209_09965_b200 import network as N
+    from paper_2209_09965_b200.noise import default_stack
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, RenderSettings, orbit_cameras
+    from paper_2209_09965_b200.sample_maps import FoveaConfig, pixel_scale_for_film
+    from paper_2209_09965_b200.sharded import ShardedFramePipeline
+    from paper_2209_09965_b200.throughput import default_scene
+
+    h, w, n = cfg["height"], cfg["width"], cfg["vol"]
+    scene = default_scene("sphere_shells", (n, n, n))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=PATH_FRAMES), scene.volume, w, h)
+    fovea = FoveaConfig(focus=((w - 1) / 2.0, (h - 1) / 2.0), sigma=cfg["sigma"], base_density=cfg["pb"],
+                        pixel_scale=pixel_scale_for_film((h, w)))
+    pipe = ShardedFramePipeline(scene, net, (h, w), default_stack(), RenderSettings(), rank=rank, world=world,
+                                group=group)
+    ctx = pipe.pipe.ctx
+    k, wu = args.steps, args.warmup
+    clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_r{rank}.csv") if rank == 0 else None
+    for j in range(wu):
+        pipe.step(cams[j % PATH_FRAMES], fovea, j)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    ctx.reset_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for j in range(wu, wu + k):  # the same frames on every rank: each marches its share
+        pipe.step(cams[j % PATH_FRAMES], fovea, j)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world, device="cuda")
+    launches = ctx.launches() - l0
+    st = ctx.stats()
+    # end to end: frame -> host image on rank 0 (pinned), wall clock, max over ranks
+    host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for j in range(wu + k, wu + 2 * k):
+        pipe.step(cams[j % PATH_FRAMES], fovea, j)
+        if rank == 0:
+            host.copy_(pipe.rgb, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world, device="cuda")
+    clk = clocks.stop() if clocks else None
+    if rank == 0:
+        hbm, tf_burst, tf_sus, src = load_peaks()
+        samples = (st.samples_main + st.samples_shadow) / k  # this rank's share
+        line = {
+            "metric": METRIC, "value": k / (ms / 1e3), "unit": "frames/s", "n_gpus": world, "steps": k,
+            "warmup": wu, "ms_per_step": ms / k, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp16 net (fp32 acc) / fp32 march", "data": "synthetic",
+            "config": {"workload": cfg["name"], "film": [w, h], "volume": [n, n, n], "path_frames": PATH_FRAMES,
+                       "parallelism": f"one frame stream, march sharded in 32-ray packets over {world} GPUs, "
+                                      "record all-gather (NCCL), replicated reconstruction",
+                       "l2": "inputs larger than L2"},
+            "samples_per_frame_rank0": samples,
+            "e2e": {"value": k / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": h * w * 3 * 4,
+                    "how": "ShardedFramePipeline.step per frame + pinned D2H of the image on rank 0, wall clock"},
+            "gpu_launches": launches, "clocks": clk,
+            "roofline": None, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -396,6 +484,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="split each frame's march across the ranks (config 5) instead of independent frame streams")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -403,6 +493,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.shard:
+        run_sharded(args, cfg)
     else:
         run_ours(args, cfg)
 

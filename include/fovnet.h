@@ -262,6 +262,20 @@ FV_API int fv_metric_sqdiff(fv_ctx* ctx, const double* a, const double* b, const
 FV_API int fv_metric_ssim(fv_ctx* ctx, const double* a, const double* b, int H, int W, int ca, int cb,
                           int mode, int scales, const double* weights, double* out);
 
+/* ---- one frame across GPUs (config 5) ------------------------------------------- */
+/* fv_shard_rays: the rank's share of the compacted ray list -- 32-ray packets dealt round-robin
+ * (packet p belongs to rank p % world) -> out_idx_dev (capacity k_max), count -> out_k_dev.
+ * fv_pack_records: (pixel, RGBA) records of the rays in idx_dev[0, *k_dev) read from the (H,W,4)
+ * framebuffer into [0, cap) (pixel -1 past the count) -- the all-gather payload.
+ * fv_scatter_records: n gathered records -> the network input channels 0..3 of st (fp16, exactly
+ * as the marcher writes them) and/or an (H,W,4) framebuffer; records with pixel < 0 are skipped. */
+FV_API int fv_shard_rays(fv_ctx* ctx, const int32_t* idx_dev, const int32_t* k_dev, int k_max, int rank,
+                         int world, int32_t* out_idx_dev, int32_t* out_k_dev);
+FV_API int fv_pack_records(fv_ctx* ctx, const float* rgba_dev, const int32_t* idx_dev, const int32_t* k_dev,
+                           int cap, int32_t* rec_pix_dev, float* rec_rgba_dev);
+FV_API int fv_scatter_records(fv_ctx* ctx, fv_state* st, const int32_t* rec_pix_dev, const float* rec_rgba_dev,
+                              int64_t n, int W, float* rgba_out_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,9 @@ _SIGS = {
                              P, P, I, P, P, P, C.POINTER(FvStats)]),
     "fv_render_full": (I, [P, P, C.POINTER(FvCamera), C.POINTER(FvLight), C.POINTER(FvSettings),
                            P, P, C.POINTER(FvStats)]),
+    "fv_shard_rays": (I, [P, P, P, I, I, I, P, P]),
+    "fv_pack_records": (I, [P, P, P, P, I, P, P]),
+    "fv_scatter_records": (I, [P, P, P, P, I64, I, P]),
     "fv_pack_rgb8": (I, [P, P, I, I, I64, I64, I64, P]),
     "fv_metric_sqdiff": (I, [P, P, P, P, P, I, I, I, I, C.POINTER(D)]),
     "fv_metric_ssim": (I, [P, P, P, I, I, I, I, I, I, C.POINTER(D), C.POINTER(D)]),

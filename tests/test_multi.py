@@ -58,3 +58,50 @@ def test_single_rank_helpers():
     assert bench.max_over_ranks(3.5, 1) == 3.5
     assert bench.rank_frames(0, 2, 3) == [2, 3, 4]
     assert bench.whole_job_rate(10, 1, 0.5) == 20.0
+
+
+def _shard_worker(rank, world, port, q):
+    import numpy as np
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2209_09965_b200 import sharded as SH
+
+    # a synthetic sparse frame: the same compacted list on every rank, each rank "marches" its packets
+    h, w = 23, 37
+    rng = np.random.default_rng(4)
+    active = np.flatnonzero(rng.random(h * w) < 0.3).astype(np.int32)
+    frame = rng.random((h * w, 4)).astype(np.float32)
+    mine = active[SH.packet_owner(active.size, world) == rank]
+    cap = SH.record_capacity(h * w, world)
+    pix = torch.full((cap,), -1, dtype=torch.int32)
+    pix[: mine.size] = torch.from_numpy(mine)
+    rgba = torch.zeros((cap, 4), dtype=torch.float32)
+    rgba[: mine.size] = torch.from_numpy(frame[mine])
+    gp, gr = SH.all_gather_records(pix, rgba, world)
+    full = SH.scatter_records_host(gp.numpy(), gr.numpy(), h, w)
+    expect = np.zeros((h * w, 4), np.float32)
+    expect[active] = frame[active]
+    ok = bool(np.array_equal(full, expect.reshape(h, w, 4))) and gp.numel() == world * cap
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, ok, int(mine.size)))
+
+
+@pytest.mark.timeout(120)
+def test_two_rank_ray_sharding_exchange():
+    """Packet-interleaved ray shards + fixed-capacity record all-gather rebuild the whole sparse
+    frame on every rank (the host side of sharded.ShardedFramePipeline, over gloo)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=100) for _ in procs]
+    for p in procs:
+        p.join(timeout=30)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(ok for _, ok, _ in res)
+    counts = sorted(n for _, _, n in res)
+    assert abs(counts[0] - counts[1]) <= 32  # packets dealt round-robin
