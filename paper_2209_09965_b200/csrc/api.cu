@@ -272,6 +272,8 @@ int fv_volume_destroy(fv_volume* v) {
   if (v->data && v->owns_data) cudaFree(v->data);
   if (v->lut_dev) cudaFree(v->lut_dev);
   if (v->bricks) cudaFree(v->bricks);
+  if (v->qtex) cudaDestroyTextureObject((cudaTextureObject_t)v->qtex);
+  if (v->qarr) cudaFreeArray(v->qarr);
   delete v;
   return 0;
 }

@@ -108,6 +108,10 @@ struct fv_volume {
   float* lut_dev = nullptr;  // (K,4) float32, K <= 256
   float* bricks = nullptr;   // 8^3-bricked copy used by the fp32 marcher
   uint64_t version = 1, bricks_version = 0;
+  // the same quads as a point-sampled 3D texture (block-linear layout; FV_VOL_TEX=1, A/B)
+  cudaArray_t qarr = nullptr;
+  unsigned long long qtex = 0;  // cudaTextureObject_t
+  uint64_t tex_version = 0;
   int K = 0;
   double value_range[2] = {0, 0};
 };

@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(128) march_kernel(MarchParams P) {
 // Quads are stored in 8x8x8 bricks (8 KB, z-y-x inside a brick) so consecutive samples of a ray
 // in any direction -- shadow rays run diagonally toward the light -- stay in the same lines.
 struct FastVol {
+  cudaTextureObject_t tex;  // non-zero: fetch quads from the 3D texture (unnormalised, point, clamp)
   const float4* quads;
   int nx, ny, nz;
   int sby, sbz;        // brick strides (quads) in y and z
@@ -313,12 +314,20 @@ struct TriFetch {
 
 // Same, from continuous voxel coordinates q = p/spacing - 0.5 (rays stepped directly in q-space;
 // p in [0, ext] <=> q in [-0.5, n-0.5]).
+template <bool TEX = false>
 __device__ __forceinline__ TriFetch tri_issue_q(const FastVol& V, float qx, float qy, float qz) {
   TriFetch f;
   f.inside = qx >= -0.5f && qx <= V.qmax[0] && qy >= -0.5f && qy <= V.qmax[1] && qz >= -0.5f &&
              qz <= V.qmax[2];
   const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
   f.tx = qx - fx; f.ty = qy - fy; f.tz = qz - fz;
+  if constexpr (TEX) {
+    // texel (i, j, k) is sampled at (i + .5, j + .5, k + .5); clamp addressing = the reference's
+    // clamped i0; the second plane is clamp(max(floor, 0) + 1) as the reference's i1
+    f.A = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fz + 0.5f);
+    f.B = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fmaxf(fz, 0.f) + 1.5f);
+    return f;
+  }
   const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
             z0 = min(max((int)fz, 0), V.nz - 1);
   const int z1 = min(z0 + 1, V.nz - 1);
@@ -328,12 +337,18 @@ __device__ __forceinline__ TriFetch tri_issue_q(const FastVol& V, float qx, floa
   return f;
 }
 
+template <bool TEX = false>
 __device__ __forceinline__ TriFetch tri_issue(const FastVol& V, float px, float py, float pz) {
   TriFetch f;
   f.inside = px >= 0.f && px <= V.ext[0] && py >= 0.f && py <= V.ext[1] && pz >= 0.f && pz <= V.ext[2];
   const float qx = px * V.inv_sp[0] - 0.5f, qy = py * V.inv_sp[1] - 0.5f, qz = pz * V.inv_sp[2] - 0.5f;
   const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
   f.tx = qx - fx; f.ty = qy - fy; f.tz = qz - fz;
+  if constexpr (TEX) {
+    f.A = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fz + 0.5f);
+    f.B = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fmaxf(fz, 0.f) + 1.5f);
+    return f;
+  }
   const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
             z0 = min(max((int)fz, 0), V.nz - 1);
   const int z1 = min(z0 + 1, V.nz - 1);
@@ -499,7 +514,7 @@ __device__ __forceinline__ float keep_t(float x, float e) {
   else return keep_partial(x, e);
 }
 
-template <int CLS>
+template <int CLS, bool TEX>
 __device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px, float py, float pz,
                                unsigned int& nsamp) {
   const MarchParams& P = F.P;
@@ -546,7 +561,7 @@ __device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px
       const float dt = fminf(step, tend - tj);
       const float mid = tj + 0.5f * dt;
       dts[j] = dt;
-      f[j] = tri_issue_q(F.V, fmaf(qdx, mid, q0x), fmaf(qdy, mid, q0y), fmaf(qdz, mid, q0z));
+      f[j] = tri_issue_q<TEX>(F.V, fmaf(qdx, mid, q0x), fmaf(qdy, mid, q0y), fmaf(qdz, mid, q0z));
       tj = tj + dt;
     }
     bool stop = false;
@@ -1238,7 +1253,7 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, W
 // chunks but the last are full (what the shadow and composite passes expect). Rays are claimed 32 at a
 // time; their fp64 setup runs one ray per lane, then the warp walks the hitting rays one by one.
 // (The per-lane state machine it replaces left ~half the lanes idle: rays are 0..~1000 samples long.)
-template <int kU>
+template <int kU, bool TEX>
 __global__ void __launch_bounds__(128, 4) march_wave_main_warp_kernel(FastParams F, WaveBufs B,
                                                                       unsigned int* ray_counter) {
   const MarchParams& P = F.P;
@@ -1327,7 +1342,7 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_warp_kernel(FastParams
             const int s = s0 + uu * 32 + lane;
             const float dt = s == rn - 1 ? rl : stepf;
             const float mid = (float)s * stepf + 0.5f * dt;
-            f[uu] = tri_issue(F.V, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid);
+            f[uu] = tri_issue<TEX>(F.V, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid);
           }
           bool done = false;
 #pragma unroll
@@ -1600,8 +1615,8 @@ __global__ void __launch_bounds__(256) first_list_kernel(FastParams F, WaveBufs 
 
 // One shadow ray per record slot (empty tail slots of a ray's last chunk are skipped); lanes
 // refill from a work counter so long shadow rays do not idle their warp's neighbours.
-template <int CLS>
-__global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
+template <int CLS, bool TEX>
+__global__ void __launch_bounds__(128, 7) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
   __shared__ float2 lut2[256];
   for (int i = threadIdx.x; i < P.K - 1; i += blockDim.x)
@@ -1649,7 +1664,7 @@ __global__ void __launch_bounds__(128) march_wave_shadow_kernel(FastParams F, Wa
     if (!__any_sync(0xffffffffu, my >= 0)) break;
     if (my >= 0) {
       const float4 r0 = B.rec0[my];
-      const float ts = shadow_fast_t<CLS>(F, lut2, r0.x, r0.y, r0.z, n_shadow);
+      const float ts = shadow_fast_t<CLS, TEX>(F, lut2, r0.x, r0.y, r0.z, n_shadow);
       B.shade[my] = amb + (1.f - amb) * ts;
       my = -1;
     }
@@ -1733,6 +1748,51 @@ void normalize3(double v[3]) {
 
 }  // namespace
 
+// quads -> 3D surface (texel (x,y,z) = the float4 quad of voxel (x,y,z), as brick_kernel)
+__global__ void quad_surface_kernel(const float* __restrict__ lin, cudaSurfaceObject_t surf, int nx, int ny, int nz) {
+  const int64_t n = (int64_t)nx * ny * nz;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((int64_t)nx * ny));
+    const int x1 = min(x + 1, nx - 1), y1 = min(y + 1, ny - 1);
+    const float* pl = lin + (int64_t)z * ny * nx;
+    const float4 q = make_float4(pl[(int64_t)y * nx + x], pl[(int64_t)y * nx + x1], pl[(int64_t)y1 * nx + x],
+                                 pl[(int64_t)y1 * nx + x1]);
+    surf3Dwrite(q, surf, x * (int)sizeof(float4), y, z);
+  }
+}
+
+int volume_texture(fv_ctx* ctx, fv_volume* vol) {
+  if (vol->qtex && vol->tex_version == vol->version) return 0;
+  if (!vol->qarr) {
+    const cudaChannelFormatDesc fd = cudaCreateChannelDesc<float4>();
+    FV_CUDA(cudaMalloc3DArray(&vol->qarr, &fd, make_cudaExtent(vol->nx, vol->ny, vol->nz), cudaArraySurfaceLoadStore));
+  }
+  cudaResourceDesc rd{};
+  rd.resType = cudaResourceTypeArray;
+  rd.res.array.array = vol->qarr;
+  cudaSurfaceObject_t surf = 0;
+  FV_CUDA(cudaCreateSurfaceObject(&surf, &rd));
+  const int64_t n = (int64_t)vol->nx * vol->ny * vol->nz;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16);
+  FV_TIMED(ctx, FV_KC_OTHER, quad_surface_kernel<<<blocks, 256, 0, ctx->stream>>>(vol->data, surf, vol->nx, vol->ny, vol->nz));
+  FV_CHECK_LAUNCH("quad_surface_kernel");
+  ctx->launches += 1;
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaDestroySurfaceObject(surf);
+  if (!vol->qtex) {
+    cudaTextureDesc td{};
+    td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModePoint;
+    td.readMode = cudaReadModeElementType;
+    td.normalizedCoords = 0;
+    cudaTextureObject_t t = 0;
+    FV_CUDA(cudaCreateTextureObject(&t, &rd, &td, nullptr));
+    vol->qtex = (unsigned long long)t;
+  }
+  vol->tex_version = vol->version;
+  return 0;
+}
+
 int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
   if (vol->bricks && vol->bricks_version == vol->version) return 0;
   const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8, nbz = (vol->nz + 7) / 8;
@@ -1745,6 +1805,36 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
   FV_CHECK_LAUNCH("brick_kernel");
   ctx->launches += 1;
   vol->bricks_version = vol->version;
+  return 0;
+}
+
+// wavefront passes, instantiated for quads from the bricked buffer (TEX = false) or the texture
+template <bool TEX>
+int launch_main_warp(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_warp_kernel<2, TEX>, threads, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<2, TEX><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(
+                                      F, B, &ctx->counters->ray_next));
+  return 0;
+}
+
+template <bool TEX>
+int launch_shadow(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_shadow_kernel<2, TEX>, threads, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  const int g = ctx->num_sms * per_sm;
+  switch (F.cls_sh) {
+    case 0: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<0, TEX><<<g, threads, 0, ctx->stream>>>(F, B)); break;
+    case 1: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<1, TEX><<<g, threads, 0, ctx->stream>>>(F, B)); break;
+    case 2: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<2, TEX><<<g, threads, 0, ctx->stream>>>(F, B)); break;
+    default: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<3, TEX><<<g, threads, 0, ctx->stream>>>(F, B)); break;
+  }
   return 0;
 }
 
@@ -1814,12 +1904,27 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
   if (s->precision == FV_PREC_FP64) {
     FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_kernel<double><<<blocks, threads, 0, ctx->stream>>>(P));
   } else {
-    fv_volume* mv = const_cast<fv_volume*>(vol);  // the brick copy is a cache of the grid
-    int rc = volume_bricks(ctx, mv);
+    fv_volume* mv = const_cast<fv_volume*>(vol);  // the quad copy is a cache of the grid
+    // FV_MARCH_KERNEL=wave (default) | refill | ray | persist -- variants kept for A/B runs
+    static int env_variant = -1;
+    if (env_variant < 0) {
+      const char* e = getenv("FV_MARCH_KERNEL");
+      env_variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2
+                  : (e && strcmp(e, "refill") == 0) ? 0 : 3;
+    }
+    // the naive renderer forces the thread-per-lane kernel (idle lanes are its point)
+    const int variant = force_variant >= 0 ? force_variant : env_variant;
+    // Quads come from a point-sampled 3D texture (block-linear layout, hardware clamp addressing:
+    // A/B -43 us per C3 frame versus the bricked buffer, which the thread-per-ray variants and
+    // FV_VOL_TEX=0 still use).
+    static const bool use_tex = !(getenv("FV_VOL_TEX") && atoi(getenv("FV_VOL_TEX")) == 0);
+    const bool tex_path = use_tex && variant == 3;
+    int rc = tex_path ? volume_texture(ctx, mv) : volume_bricks(ctx, mv);
     if (rc) return rc;
     FastParams F;
     F.P = P;
     F.V.quads = reinterpret_cast<const float4*>(mv->bricks);
+    F.V.tex = tex_path ? (cudaTextureObject_t)mv->qtex : 0;
     F.V.nx = vol->nx; F.V.ny = vol->ny; F.V.nz = vol->nz;
     const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8;
     F.V.sby = nbx * 512;
@@ -1839,15 +1944,6 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     F.cls_main = exp_class(P.step / P.ref);
     F.cls_sh = exp_class(P.step_sh / P.ref);
     F.inv_ref = (float)(1.0 / P.ref);
-    // FV_MARCH_KERNEL=wave (default) | refill | ray | persist -- variants kept for A/B runs
-    static int env_variant = -1;
-    if (env_variant < 0) {
-      const char* e = getenv("FV_MARCH_KERNEL");
-      env_variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2
-                  : (e && strcmp(e, "refill") == 0) ? 0 : 3;
-    }
-    // the naive renderer forces the thread-per-lane kernel (idle lanes are its point)
-    const int variant = force_variant >= 0 ? force_variant : env_variant;
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
       // record slots: 16 per compacted ray (C3 needs ~12 incl. chunk tails), at least 4M
@@ -1883,7 +1979,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.ord = shadow_order ? B.chunk_fill + ctx->wave_cap / kChunk : nullptr;
       B.ord_count = &ctx->counters->wave_ord;
       B.seg = reinterpret_cast<unsigned int*>(B.chunk_fill + 2 * (ctx->wave_cap / kChunk));
-      static int main_u = 0, per_sm_main = 0, per_sm_sh = 0;
+      static int main_u = 0, per_sm_main = 0;
       if (!per_sm_main) {
         const char* e = getenv("FV_MAIN_U");  // main-sample prefetch depth (A/B runs): 4 or 8
         main_u = (e && atoi(e) == 8) ? 8 : 4;
@@ -1891,9 +1987,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<8>, threads, 0));
         else
           FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<4>, threads, 0));
-        FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sh, march_wave_shadow_kernel<2>, threads, 0));
         per_sm_main = std::max(per_sm_main, 1);
-        per_sm_sh = std::max(per_sm_sh, 1);
       }
       // ray_next, wave_rec, wave_next, wave_ord are consecutive counters
       FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 4 * sizeof(unsigned int), ctx->stream));
@@ -1904,18 +1998,10 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       static const bool direct_first = !(getenv("FV_FIRST_DIRECT") && atoi(getenv("FV_FIRST_DIRECT")) == 0);
       B.cap_a = (main_warp && direct_first) ? B.n_chunks_cap / 2 : 0;
       if (B.cap_a > 0) B.ord = B.chunk_fill + ctx->wave_cap / kChunk;  // the first-chunk list
-      static int per_sm_warp = 0;
-      if (main_warp && !per_sm_warp) {
-        if (main_warp == 1)
-          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_warp, march_wave_main_warp_kernel<1>, threads, 0));
-        else
-          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_warp, march_wave_main_warp_kernel<2>, threads, 0));
-        per_sm_warp = std::max(per_sm_warp, 1);
+      if (main_warp) {
+        rc = F.V.tex ? launch_main_warp<true>(ctx, F, B, threads) : launch_main_warp<false>(ctx, F, B, threads);
+        if (rc) return rc;
       }
-      if (main_warp == 1)
-        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<1><<<ctx->num_sms * per_sm_warp, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
-      else if (main_warp)
-        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<2><<<ctx->num_sms * per_sm_warp, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
       else if (main_u == 8)
         FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<8><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
       else
@@ -1931,13 +2017,8 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_scatter_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
           ctx->launches += 3;
         }
-        const int sgrid = ctx->num_sms * per_sm_sh;
-        switch (F.cls_sh) {
-          case 0: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<0><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
-          case 1: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<1><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
-          case 2: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<2><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
-          default: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<3><<<sgrid, threads, 0, ctx->stream>>>(F, B)); break;
-        }
+        rc = F.V.tex ? launch_shadow<true>(ctx, F, B, threads) : launch_shadow<false>(ctx, F, B, threads);
+        if (rc) return rc;
         FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;
       }
