@@ -164,6 +164,12 @@ FV_API int fv_volume_upload(fv_ctx* ctx, fv_volume* vol, const float* data, int 
  * kind 0 sphere_shells, 1 vortex_field, 2 box_lattice; value_range_out: nullable host double[2] */
 FV_API int fv_volume_procedural(fv_ctx* ctx, fv_volume* vol, int kind, double* value_range_out);
 /* TransferFunction lut (K,4) float32 host */
+/* load_raw_volume's normalisation (volume.py:75-109) on the device: raw_dev holds nx*ny*nz values
+ * (dtype 0 = uint8, 1 = float32, x fastest); the volume's data receives (raw - lo) / (hi - lo) in fp64
+ * cast to float32 (zeros when hi == lo); range = (lo, hi). Float data with a NaN fails with the
+ * reference's message and *first_nan (nullable) = the first NaN's flat index (else -1). */
+FV_API int fv_volume_from_raw(fv_ctx* ctx, fv_volume* vol, const void* raw_dev, int dtype, double* range,
+                              int64_t* first_nan);
 FV_API int fv_volume_set_tf(fv_ctx* ctx, fv_volume* vol, const float* lut_host, int K);
 /* device pointer to the (nz,ny,nx) float32 grid */
 FV_API float* fv_volume_data(fv_volume* vol);

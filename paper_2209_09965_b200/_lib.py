@@ -85,6 +85,7 @@ _SIGS = {
     "fv_volume_destroy": (I, [P]),
     "fv_volume_upload": (I, [P, P, P, I]),
     "fv_volume_procedural": (I, [P, P, I, C.POINTER(D)]),
+    "fv_volume_from_raw": (I, [P, P, P, I, C.POINTER(D), C.POINTER(I64)]),
     "fv_volume_set_tf": (I, [P, P, P, I]),
     "fv_volume_data": (P, [P]),
     "fv_render_sparse": (I, [P, P, C.POINTER(FvCamera), C.POINTER(FvLight), C.POINTER(FvSettings),

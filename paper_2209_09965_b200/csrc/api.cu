@@ -294,6 +294,12 @@ int fv_volume_procedural(fv_ctx* ctx, fv_volume* v, int kind, double* range) {
   return launch_volume_procedural(ctx, v, kind, range);
 }
 
+int fv_volume_from_raw(fv_ctx* ctx, fv_volume* v, const void* raw_dev, int dtype, double* range,
+                       int64_t* first_nan) {
+  FV_REQUIRE(ctx && v && v->data && raw_dev, "null argument");
+  return launch_volume_from_raw(ctx, v, raw_dev, dtype, range, first_nan);
+}
+
 int fv_volume_set_tf(fv_ctx* ctx, fv_volume* v, const float* lut, int K) {
   FV_REQUIRE(ctx && v && lut, "null argument");
   FV_REQUIRE(K >= 2 && K <= 256, "transfer function lut must be (K>=2, 4) with K <= 256, got K=%d", K);

@@ -219,6 +219,8 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
 constexpr int kChunkNaive = 64;  // WARP_CHUNK (renderer.py:34)
 int launch_naive_list(fv_ctx* ctx, const uint8_t* bits, int H, int W, int32_t* idx, int32_t* k_dev);
 int launch_volume_procedural(fv_ctx* ctx, fv_volume* vol, int kind, double* range);
+int launch_volume_from_raw(fv_ctx* ctx, fv_volume* vol, const void* raw, int dtype, double* range_out,
+                           int64_t* first_nan_out);
 int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* out_rgb,
                 float* out_o, float* out_od);
 int conv_prepare(fv_ctx* ctx, ConvParam& cp);

@@ -100,19 +100,6 @@ class VolumeGrid:
                 pass
 
 
-def _normalize_dev(raw):
-    """(raw - lo) / (hi - lo) in fp64 -> float32 (volume.py:75-81), on the device."""
-    import torch
-
-    r = raw.to(torch.float64)
-    lo, hi = float(r.min()), float(r.max())
-    if hi > lo:
-        data = ((r - lo) / (hi - lo)).to(torch.float32)
-    else:
-        data = torch.zeros_like(r, dtype=torch.float32)
-    return data, (lo, hi)
-
-
 def load_raw_volume(path: str | Path, meta: VolumeMeta) -> VolumeGrid:
     """Load a little-endian raw volume and min-max normalise it (volume.py:84-109)."""
     import torch
@@ -126,15 +113,21 @@ def load_raw_volume(path: str | Path, meta: VolumeMeta) -> VolumeGrid:
     if len(blob) != expected:
         raise ValueError(f"size mismatch for {path}: expected {expected} bytes "
                          f"({nx}x{ny}x{nz} {meta.dtype}), got {len(blob)}")
-    raw = torch.as_tensor(np.frombuffer(blob, dtype=elem).reshape(nz, ny, nx).copy(), device="cuda")
-    if raw.is_floating_point():
-        bad = torch.nonzero(torch.isnan(raw.reshape(-1)))
-        if bad.numel():
-            i = int(bad[0])
-            z, y, x = np.unravel_index(i, (nz, ny, nx))
-            raise ValueError(f"NaN in volume data at flat index {i} (voxel x={x}, y={y}, z={z})")
-    data, vr = _normalize_dev(raw)
-    return VolumeGrid(meta.dims, meta.spacing, data, vr, _validated=True)
+    raw = torch.as_tensor(np.frombuffer(blob, dtype=elem).copy(), device="cuda")
+    # NaN scan, global min/max and the fp64 normalisation run in libfovnet (fv_volume_from_raw)
+    ctx = _lib.context()
+    out = torch.empty((nz, ny, nx), dtype=torch.float32, device="cuda")
+    h = C.c_void_p()
+    sp = (C.c_double * 3)(*meta.spacing)
+    _lib.check(ctx.lib.fv_volume_wrap(ctx.h, nx, ny, nz, sp, _lib.ptr(out), C.byref(h)))
+    try:
+        vr = (C.c_double * 2)()
+        nan_at = C.c_int64()
+        _lib.check(ctx.lib.fv_volume_from_raw(ctx.h, h, _lib.ptr(raw), 0 if meta.dtype == "uint8" else 1, vr,
+                                              C.byref(nan_at)))
+    finally:
+        ctx.lib.fv_volume_destroy(h)
+    return VolumeGrid(meta.dims, meta.spacing, out, (vr[0], vr[1]), _validated=True)
 
 
 def make_procedural_volume(kind: str, dims: tuple[int, int, int],

@@ -18,6 +18,7 @@ Outputs (all under tests/golden/ unless noted):
   render_small.npz      render_full / render_sparse_compact outputs on small scenes
   net_small.npz         forward_full outputs (desk + paper nets, carried state)
   e2e_c1.npz            config C1 (64^3, 256x256, fast) mask -> march -> fp16 net, 2 frames
+  rawvol_small.npz      load_raw_volume on uint8 / float32 / constant / NaN raw files
   viewer_small.npz      viewer.RenderService.render_frame: decoded PNGs + headers, every mode
   metrics_small.npz     PSNR / SSIM / MS-SSIM / tPSNR / quality-report values on seeded images
   sweep_small.npz       compression sweep pieces: uniform noise, direct draws, naive/direct
@@ -276,6 +277,36 @@ def gen_viewer(stack):
     print("viewer done")
 
 
+def gen_rawvol():
+    """volume.load_raw_volume on small raw files (uint8, float32, constant, NaN)."""
+    import tempfile
+
+    rng = np.random.default_rng(9)
+    out = {}
+    cases = {"u8": (rng.integers(0, 256, size=(9, 10, 12), dtype=np.uint8), "uint8"),
+             "f32": ((rng.standard_normal((9, 10, 12)) * 3.7 + 1.1).astype("<f4"), "float32"),
+             "const": (np.full((9, 10, 12), 2.5, dtype="<f4"), "float32")}
+    with tempfile.TemporaryDirectory() as d:
+        for key, (arr, dt) in cases.items():
+            path = Path(d) / f"{key}.raw"
+            path.write_bytes(arr.tobytes())
+            vg = rv.load_raw_volume(path, rv.VolumeMeta(dims=(12, 10, 9), dtype=dt, spacing=(1.0, 2.0, 0.5)))
+            out[key + "_raw"] = arr
+            out[key + "_data"] = vg.data
+            out[key + "_range"] = np.array(vg.value_range)
+        bad = cases["f32"][0].copy()
+        bad.reshape(-1)[437] = np.nan
+        path = Path(d) / "nan.raw"
+        path.write_bytes(bad.tobytes())
+        try:
+            rv.load_raw_volume(path, rv.VolumeMeta(dims=(12, 10, 9), dtype="float32"))
+        except ValueError as e:
+            out["nan_msg"] = np.array(str(e))
+        out["nan_raw"] = bad
+    np.savez_compressed(HERE / "rawvol_small.npz", **out)
+    print("rawvol done")
+
+
 def gen_net():
     out = {}
     rng = np.random.default_rng(77)
@@ -340,7 +371,7 @@ def main():
     stack = rn.default_stack()
     rn.save_stack(stack, DATA / "stbn_64x64x8_s1.noise")
     print(f"stbn sha {sha(stack.values.astype('<f4').tobytes())}")
-    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep", "metrics", "viewer"}
+    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep", "metrics", "viewer", "rawvol"}
     if "masks" in which:
         gen_masks(stack)
     if "volumes" in which:
@@ -357,6 +388,8 @@ def main():
         gen_metrics()
     if "viewer" in which:
         gen_viewer(stack)
+    if "rawvol" in which:
+        gen_rawvol()
     print(f"done in {time.perf_counter() - t0:.1f}s")
 
 

@@ -562,3 +562,24 @@ def test_sharded_frames_equal_unsharded_frames(stack, world):
         sh.step_emulated(cams[5 * i], spec.fovea(), i)
         torch.cuda.synchronize()
         assert torch.equal(sh.rgb, ref.rgb), i
+
+
+# ---------------------------------------------------------------- input formats
+def test_load_raw_volume_on_device_vs_reference(golden, tmp_path):
+    """load_raw_volume: NaN scan, min/max and fp64 normalisation in libfovnet, bit-exact."""
+    from paper_2209_09965_b200.volume import VolumeMeta, load_raw_volume
+
+    g = np.load(golden / "rawvol_small.npz")
+    for key, dt in (("u8", "uint8"), ("f32", "float32"), ("const", "float32")):
+        p = tmp_path / f"{key}.raw"
+        p.write_bytes(g[key + "_raw"].tobytes())
+        vg = load_raw_volume(p, VolumeMeta(dims=(12, 10, 9), dtype=dt, spacing=(1.0, 2.0, 0.5)))
+        assert np.array_equal(vg.data, g[key + "_data"]), key
+        assert tuple(vg.value_range) == tuple(g[key + "_range"]), key
+    p = tmp_path / "nan.raw"
+    p.write_bytes(g["nan_raw"].tobytes())
+    with pytest.raises(ValueError) as e:
+        load_raw_volume(p, VolumeMeta(dims=(12, 10, 9), dtype="float32"))
+    assert str(e.value) == str(g["nan_msg"])
+    with pytest.raises(ValueError, match="size mismatch"):
+        load_raw_volume(p, VolumeMeta(dims=(12, 10, 8), dtype="float32"))
