@@ -583,3 +583,30 @@ def test_load_raw_volume_on_device_vs_reference(golden, tmp_path):
     assert str(e.value) == str(g["nan_msg"])
     with pytest.raises(ValueError, match="size mismatch"):
         load_raw_volume(p, VolumeMeta(dims=(12, 10, 8), dtype="float32"))
+
+
+@pytest.mark.parametrize("h,w", [(97, 131), (200, 257)])
+def test_fused_pipeline_equals_separate_calls_on_padded_films(stack, h, w):
+    """Films not divisible by 8 (network padding, partial conv tiles, cropped output stage): the
+    fused device pipeline (mask kernel + marcher write the network input) equals the separate
+    public calls (render_sparse_compact -> _reconstruct_frame), which are pinned to the reference."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, _reconstruct_frame, default_scene
+
+    spec = ExperimentSpec(mode="hifi", width=w, height=h)
+    scene = default_scene("sphere_shells", (48, 48, 48))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=1), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, w, h)
+    pipe = FramePipeline(scene, net, (h, w), stack)
+    state = N.reset_state(net.config, (h, w))
+    for i in range(3):
+        fov = spec.fovea()
+        pipe.step(cams[7 * i], fov, i)
+        mask = S.build_sample_mask(stack, i, S.build_tau_map(fov, (h, w)))
+        fr = render_sparse_compact(scene, cams[7 * i], S.compact_mask(mask), RenderSettings())
+        img, state = _reconstruct_frame(net, fr.rgba_dev, mask.bits_dev, state)
+        torch.cuda.synchronize()
+        got = pipe.rgb.cpu().numpy()
+        assert got.shape == (h, w, 3)
+        assert np.array_equal(got, img), (i, np.abs(got - img).max())
