@@ -1254,7 +1254,7 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, W
 // time; their fp64 setup runs one ray per lane, then the warp walks the hitting rays one by one.
 // (The per-lane state machine it replaces left ~half the lanes idle: rays are 0..~1000 samples long.)
 template <int kU, bool TEX>
-__global__ void __launch_bounds__(128, 4) march_wave_main_warp_kernel(FastParams F, WaveBufs B,
+__global__ void __launch_bounds__(128, 5) march_wave_main_warp_kernel(FastParams F, WaveBufs B,
                                                                       unsigned int* ray_counter) {
   const MarchParams& P = F.P;
   __shared__ float lut[4 * 256];
@@ -1616,7 +1616,7 @@ __global__ void __launch_bounds__(256) first_list_kernel(FastParams F, WaveBufs 
 // One shadow ray per record slot (empty tail slots of a ray's last chunk are skipped); lanes
 // refill from a work counter so long shadow rays do not idle their warp's neighbours.
 template <int CLS, bool TEX>
-__global__ void __launch_bounds__(128, 7) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
+__global__ void __launch_bounds__(128, 8) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
   __shared__ float2 lut2[256];
   for (int i = threadIdx.x; i < P.K - 1; i += blockDim.x)
