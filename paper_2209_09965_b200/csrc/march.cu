@@ -305,6 +305,13 @@ __host__ __device__ __forceinline__ int morton_xy(int x, int y) {
 }
 __host__ __device__ __forceinline__ int morton_z(int z) { return FV_BRICK_MORTON ? (spread3(z) << 2) : (z << 6); }
 
+// Texel coordinate offset of the point-sampled quad texture: texel i is returned for any coordinate
+// in [i, i+1); floor(q) is an exact integer, so it addresses texel floor(q) itself (no +0.5 add).
+#ifndef FV_TEX_OFF
+#define FV_TEX_OFF 0.0f
+#endif
+constexpr float kTexOff = FV_TEX_OFF;
+
 // Two-phase trilinear: tri_issue computes the weights and issues both loads, tri_finish blends.
 struct TriFetch {
   float4 A, B;
@@ -324,8 +331,13 @@ __device__ __forceinline__ TriFetch tri_issue_q(const FastVol& V, float qx, floa
   if constexpr (TEX) {
     // texel (i, j, k) is sampled at (i + .5, j + .5, k + .5); clamp addressing = the reference's
     // clamped i0; the second plane is clamp(max(floor, 0) + 1) as the reference's i1
-    f.A = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fz + 0.5f);
-    f.B = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fmaxf(fz, 0.f) + 1.5f);
+    if constexpr (kTexOff == 0.f) {
+      f.A = tex3D<float4>(V.tex, fx, fy, fz);
+      f.B = tex3D<float4>(V.tex, fx, fy, fmaxf(fz, 0.f) + 1.f);
+    } else {
+      f.A = tex3D<float4>(V.tex, fx + kTexOff, fy + kTexOff, fz + kTexOff);
+      f.B = tex3D<float4>(V.tex, fx + kTexOff, fy + kTexOff, fmaxf(fz, 0.f) + (1.f + kTexOff));
+    }
     return f;
   }
   const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
@@ -345,8 +357,13 @@ __device__ __forceinline__ TriFetch tri_issue(const FastVol& V, float px, float 
   const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
   f.tx = qx - fx; f.ty = qy - fy; f.tz = qz - fz;
   if constexpr (TEX) {
-    f.A = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fz + 0.5f);
-    f.B = tex3D<float4>(V.tex, fx + 0.5f, fy + 0.5f, fmaxf(fz, 0.f) + 1.5f);
+    if constexpr (kTexOff == 0.f) {
+      f.A = tex3D<float4>(V.tex, fx, fy, fz);
+      f.B = tex3D<float4>(V.tex, fx, fy, fmaxf(fz, 0.f) + 1.f);
+    } else {
+      f.A = tex3D<float4>(V.tex, fx + kTexOff, fy + kTexOff, fz + kTexOff);
+      f.B = tex3D<float4>(V.tex, fx + kTexOff, fy + kTexOff, fmaxf(fz, 0.f) + (1.f + kTexOff));
+    }
     return f;
   }
   const int x0 = min(max((int)fx, 0), V.nx - 1), y0 = min(max((int)fy, 0), V.ny - 1),
@@ -368,6 +385,20 @@ __device__ __forceinline__ float tri_finish(const TriFetch& f) {
   const float c0 = c00 * (1.f - ty) + c10 * ty;
   const float c1 = c01 * (1.f - ty) + c11 * ty;
   return c0 * (1.f - tz) + c1 * tz;
+}
+
+// texture quads hold (v00, v01 - v00, v10, v11 - v10) per plane
+template <bool TEX>
+__device__ __forceinline__ float tri_finish_t(const TriFetch& f) {
+  if constexpr (!TEX) {
+    return tri_finish(f);
+  } else {
+    if (!f.inside) return 0.f;
+    const float c00 = fmaf(f.tx, f.A.y, f.A.x), c10 = fmaf(f.tx, f.A.w, f.A.z);
+    const float c01 = fmaf(f.tx, f.B.y, f.B.x), c11 = fmaf(f.tx, f.B.w, f.B.z);
+    const float c0 = fmaf(f.ty, c10 - c00, c00), c1 = fmaf(f.ty, c11 - c01, c01);
+    return fmaf(f.tz, c1 - c0, c0);
+  }
 }
 
 __device__ __forceinline__ float tri_fast(const FastVol& V, float px, float py, float pz) {
@@ -411,8 +442,12 @@ struct FastParams {
   float lpos[3];
   int cls_main, cls_sh;
   float e_main, e_sh, inv_ref;
+  // shadow pass (directional light): q-space step toward the light, fp32 copies of the settings
+  float qs_sh[3];
+  float step_sh, inv_step_sh, min_trans, ambient;
 };
 
+template <bool TEX = false>
 __device__ float shadow_fast(const FastParams& F, const float* lut, float px, float py, float pz,
                              unsigned int& nsamp) {
   const MarchParams& P = F.P;
@@ -464,14 +499,14 @@ __device__ float shadow_fast(const FastParams& F, const float* lut, float px, fl
       const float dt = fminf(step, tend - tj);
       const float mid = tj + 0.5f * dt;
       dts[j] = dt;
-      f[j] = tri_issue_q(F.V, q0x + qdx * mid, q0y + qdy * mid, q0z + qdz * mid);
+      f[j] = tri_issue_q<TEX>(F.V, q0x + qdx * mid, q0y + qdy * mid, q0z + qdz * mid);
       tj = tj + dt;
     }
     bool stop = false;
 #pragma unroll
     for (int j = 0; j < kShadowU; ++j) {
       const float dt = dts[j];
-      const float a = tf_alpha<float>(lut, P.K, tri_finish(f[j]));
+      const float a = tf_alpha<float>(lut, P.K, tri_finish_t<TEX>(f[j]));
       const float keep = dt == step ? keep_cls(1.f - a, F.cls_sh, F.e_sh) : keep_partial(1.f - a, dt * F.inv_ref);
       trans = trans * (1.f - (1.f - keep));
       ++nsamp;
@@ -568,7 +603,7 @@ __device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px
 #pragma unroll
     for (int j = 0; j < kU; ++j) {
       const float dt = dts[j];
-      const float om = 1.f - tf_alpha2(lut2, P.K, tri_finish_fma(f[j]));
+      const float om = 1.f - tf_alpha2(lut2, P.K, TEX ? tri_finish_t<true>(f[j]) : tri_finish_fma(f[j]));
       const float keep = dt == step ? keep_t<CLS>(om, F.e_sh) : keep_partial(om, dt * F.inv_ref);
       trans = trans * keep;
       ++nsamp;
@@ -1253,9 +1288,9 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, W
 // chunks but the last are full (what the shadow and composite passes expect). Rays are claimed 32 at a
 // time; their fp64 setup runs one ray per lane, then the warp walks the hitting rays one by one.
 // (The per-lane state machine it replaces left ~half the lanes idle: rays are 0..~1000 samples long.)
-template <int kU, bool TEX>
-__global__ void __launch_bounds__(128, 5) march_wave_main_warp_kernel(FastParams F, WaveBufs B,
-                                                                      unsigned int* ray_counter) {
+template <int kU, bool TEX, int MINB = 5>
+__global__ void __launch_bounds__(128, MINB) march_wave_main_warp_kernel(FastParams F, WaveBufs B,
+                                                                         unsigned int* ray_counter) {
   const MarchParams& P = F.P;
   __shared__ float lut[4 * 256];
   for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
@@ -1355,7 +1390,7 @@ __global__ void __launch_bounds__(128, 5) march_wave_main_warp_kernel(FastParams
             const float dt = last ? rl : stepf;
             const float mid = (float)s * stepf + 0.5f * dt;
             float c[4];
-            tf_apply<float>(lut, P.K, tri_finish(f[uu]), c);
+            tf_apply<float>(lut, P.K, tri_finish_t<TEX>(f[uu]), c);
             const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
             const float a_step = active ? 1.f - keep : 0.f;
             // transmittance in front of / behind each sample: product scan of (1 - a_step)
@@ -1394,8 +1429,8 @@ __global__ void __launch_bounds__(128, 5) march_wave_main_warp_kernel(FastParams
               if (use) {
                 float shade = 1.f;
                 if (needs_shadow)
-                  shade = amb + (1.f - amb) * shadow_fast(F, lut, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid,
-                                                          n_shadow_ray);
+                  shade = amb + (1.f - amb) * shadow_fast<TEX>(F, lut, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid,
+                                                               n_shadow_ray);
                 rgb0 += contrib * (c[0] * (shade * I0));
                 rgb1 += contrib * (c[1] * (shade * I1));
                 rgb2 += contrib * (c[2] * (shade * I2));
@@ -1674,6 +1709,165 @@ __global__ void __launch_bounds__(128, 8) march_wave_shadow_kernel(FastParams F,
   if (lane == 0 && n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
 }
 
+// ---- shadow pass, directional light, partial refill ------------------------------------------
+// The pass above marches all 32 lanes' shadow rays to the end of the longest before it refills
+// (ncu: 17 of 32 lanes active) and pays ~76 instructions per sample. This version:
+//  * steps by sample index: sample s < last sits at q = qa + qs*s (qs = the warp-uniform q-space
+//    step toward the light), the final partial sample at q = qa + qs*fl with its own exponent --
+//    no per-sample dt/min/compare chain, no fp64->fp32 parameter conversions in the loop;
+//  * drops the inside-the-box test: the shadow ray is clipped to the box, so every midpoint lies
+//    inside it in exact arithmetic (the fp64 reference never sees an outside sample there); the
+//    texture's clamp addressing gives the edge value for the fp32 points that land a rounding
+//    error outside;
+//  * marches U samples per lane per round and, between rounds, hands a finished lane the next
+//    record slot once at least `refill_min` lanes of the warp are free -- refilled lanes take
+//    consecutive slots (neighbouring samples of one primary ray, whose light rays overlap), so the
+//    coherence that made all-lane refills win over per-lane ones is kept.
+// Results match march_wave_shadow_kernel to fp32 rounding (same samples, same termination rule).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int U, int MINB>
+__global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastParams F, WaveBufs B, int refill_min) {
+  const MarchParams& P = F.P;
+  // om table: (1 - a_i, -(a_{i+1} - a_i)), padded with (1 - a_{K-1}, 0) so that the index may
+  // round to K-1 at s = 1 (w = 0 there)
+  __shared__ float2 lut_om[257];
+  for (int i = threadIdx.x; i < P.K; i += blockDim.x)
+    lut_om[i] = i < P.K - 1 ? make_float2(1.f - P.lut[4 * i + 3], -(P.lut[4 * (i + 1) + 3] - P.lut[4 * i + 3]))
+                            : make_float2(1.f - P.lut[4 * i + 3], 0.f);
+  __syncthreads();
+  const int n_a = B.cap_a > 0 ? (int)*B.ord_count : 0;
+  const int n_b = B.cap_a > 0 ? (int)min(*B.chunk_count, (unsigned)(B.n_chunks_cap - B.cap_a))
+                              : (int)min(B.ord ? *B.ord_count : *B.chunk_count, (unsigned)B.n_chunks_cap);
+  const int nslots = (n_a + n_b) * kChunk;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const float amb = F.ambient;
+  const float step = F.step_sh, inv_step = F.inv_step_sh, mt = F.min_trans;
+  const float qsx = F.qs_sh[0], qsy = F.qs_sh[1], qsz = F.qs_sh[2];
+  const float kscale = (float)(P.K - 1), e_full = F.e_sh;
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
+  unsigned int n_shadow = 0;
+  bool exhausted = false;
+  int my = -1, s = 0, last = -1;  // free lanes keep last = -1, so none of their samples is live
+  float qax = 0.f, qay = 0.f, qaz = 0.f, fl = 0.f, el = 0.f, trans = 1.f;
+  while (true) {
+    while (true) {
+      const bool need = my < 0 && !exhausted;
+      const unsigned msk = __ballot_sync(0xffffffffu, need);
+      const unsigned busy = __ballot_sync(0xffffffffu, my >= 0);
+      if (!msk || (busy && __popc(msk) < refill_min)) break;
+      const int leader = __ffs(msk) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(B.next, (unsigned)__popc(msk));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (need) {
+        int i = (int)(base + __popc(msk & lt_mask));
+        if (i >= nslots) {
+          exhausted = true;
+        } else {
+          if (B.cap_a > 0) {
+            const int q = i / kChunk;
+            i = (q < n_a ? B.ord[q] : B.cap_a + q - n_a) * kChunk + (i % kChunk);
+          } else if (B.ord) {
+            i = B.ord[i / kChunk] * kChunk + (i % kChunk);
+          }
+          if ((i % kChunk) < B.chunk_fill[i / kChunk]) {
+            const float4 r0 = B.rec0[i];
+            const float p[3] = {r0.x, r0.y, r0.z};
+            float tmin = -INFINITY, tmax = INFINITY;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+              const float ta = (0.f - p[a]) * F.ld_inv[a], tb = (F.V.ext[a] - p[a]) * F.ld_inv[a];
+              tmin = fmaxf(tmin, fminf(ta, tb));
+              tmax = fminf(tmax, fmaxf(ta, tb));
+            }
+            const float t0 = fmaxf(tmin, 0.f);
+            if (!(tmax > t0)) {
+              B.shade[i] = amb + (1.f - amb) * 1.f;
+            } else {
+              const float L = tmax - t0;
+              int n = max(1, (int)ceilf(L * inv_step));
+              float ldt = L - (float)(n - 1) * step;
+              if (ldt <= 0.f && n > 1) { --n; ldt += step; }
+              ldt = fminf(ldt, step);
+              const float m0 = t0 + 0.5f * step;
+              qax = fmaf(F.ld[0] * F.V.inv_sp[0], m0, fmaf(p[0], F.V.inv_sp[0], -0.5f));
+              qay = fmaf(F.ld[1] * F.V.inv_sp[1], m0, fmaf(p[1], F.V.inv_sp[1], -0.5f));
+              qaz = fmaf(F.ld[2] * F.V.inv_sp[2], m0, fmaf(p[2], F.V.inv_sp[2], -0.5f));
+              last = n - 1;
+              fl = (float)(n - 1) + 0.5f * (ldt - step) * inv_step;
+              el = ldt * F.inv_ref;
+              s = 0;
+              trans = 1.f;
+              my = i;
+            }
+          }
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, my >= 0)) break;
+    // U samples per lane: positions first (all texture loads in flight), then the products
+    float4 A[U], Bq[U];
+    float tx[U], ty[U], tz[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int si = s + u;
+      const float fs = si == last ? fl : (float)si;
+      const float qx = fmaf(qsx, fs, qax), qy = fmaf(qsy, fs, qay), qz = fmaf(qsz, fs, qaz);
+      const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+      tx[u] = qx - fx; ty[u] = qy - fy; tz[u] = qz - fz;
+      if constexpr (kTexOff == 0.f) {
+        A[u] = tex3D<float4>(F.V.tex, fx, fy, fz);
+        Bq[u] = tex3D<float4>(F.V.tex, fx, fy, fmaxf(fz, 0.f) + 1.f);
+      } else {
+        A[u] = tex3D<float4>(F.V.tex, fx + kTexOff, fy + kTexOff, fz + kTexOff);
+        Bq[u] = tex3D<float4>(F.V.tex, fx + kTexOff, fy + kTexOff, fmaxf(fz, 0.f) + (1.f + kTexOff));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int si = s + u;
+      // quads hold (v00, v01 - v00, v10, v11 - v10)
+      const float c00 = fmaf(tx[u], A[u].y, A[u].x), c10 = fmaf(tx[u], A[u].w, A[u].z);
+      const float c01 = fmaf(tx[u], Bq[u].y, Bq[u].x), c11 = fmaf(tx[u], Bq[u].w, Bq[u].z);
+      const float c0 = fmaf(ty[u], c10 - c00, c00), c1 = fmaf(ty[u], c11 - c01, c01);
+      const float v = __saturatef(fmaf(tz[u], c1 - c0, c0));
+      // TF alpha: x = v (K-1); i = rint(x - 1/2) in [0, K-1], w = x - i in [0, 1]
+      const float xh = fmaf(v, kscale, -0.5f);
+      const float r = xh + kMagic;
+      const int i0 = __float_as_int(r) - __float_as_int(kMagic);
+      const float w = fmaf(v, kscale, -(r - kMagic));
+      const float2 lv = lut_om[i0];
+      const float om = fmaf(w, lv.y, lv.x);
+      // (1 - a)^(dt/ref): e = e_full on full steps, dt_last/ref on the final partial one
+      const float keep = ex2_approx((si == last ? el : e_full) * lg2_approx(om));
+      if (si <= last && trans > mt) {
+        trans *= keep;
+        ++n_shadow;
+      }
+    }
+    s += U;
+    if (my >= 0 && (s > last || !(trans > mt))) {
+      B.shade[my] = amb + (1.f - amb) * trans;
+      my = -1;
+      last = -1;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  if (lane == 0 && n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+}
+
 // rgb = sum_j contrib_j * (c_j * (shade_j * I)), then the background blend. One warp per ray,
 // one chunk (32 records) per step of the chain; lane sums then a fixed xor tree -- deterministic;
 // the reordering versus the reference's sequential sum is an fp32 rounding effect (~1e-7).
@@ -1748,15 +1942,18 @@ void normalize3(double v[3]) {
 
 }  // namespace
 
-// quads -> 3D surface (texel (x,y,z) = the float4 quad of voxel (x,y,z), as brick_kernel)
+// quads -> 3D surface (texel (x,y,z) = the quad of voxel (x,y,z) as brick_kernel's, x pairs stored
+// as value + difference)
 __global__ void quad_surface_kernel(const float* __restrict__ lin, cudaSurfaceObject_t surf, int nx, int ny, int nz) {
   const int64_t n = (int64_t)nx * ny * nz;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int x = (int)(i % nx), y = (int)((i / nx) % ny), z = (int)(i / ((int64_t)nx * ny));
     const int x1 = min(x + 1, nx - 1), y1 = min(y + 1, ny - 1);
     const float* pl = lin + (int64_t)z * ny * nx;
-    const float4 q = make_float4(pl[(int64_t)y * nx + x], pl[(int64_t)y * nx + x1], pl[(int64_t)y1 * nx + x],
-                                 pl[(int64_t)y1 * nx + x1]);
+    // (v00, v01 - v00, v10, v11 - v10): the x lerps become one FMA each (tri_finish_t<true>)
+    const float v00 = pl[(int64_t)y * nx + x], v01 = pl[(int64_t)y * nx + x1];
+    const float v10 = pl[(int64_t)y1 * nx + x], v11 = pl[(int64_t)y1 * nx + x1];
+    const float4 q = make_float4(v00, v01 - v00, v10, v11 - v10);
     surf3Dwrite(q, surf, x * (int)sizeof(float4), y, z);
   }
 }
@@ -1809,16 +2006,26 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
 }
 
 // wavefront passes, instantiated for quads from the bricked buffer (TEX = false) or the texture
-template <bool TEX>
-int launch_main_warp(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+template <int MINB, bool TEX>
+int launch_main_warp_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
   static int per_sm = 0;
   if (!per_sm) {
-    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_warp_kernel<2, TEX>, threads, 0));
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_warp_kernel<2, TEX, MINB>, threads, 0));
     per_sm = std::max(per_sm, 1);
   }
-  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<2, TEX><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(
+  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<2, TEX, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(
                                       F, B, &ctx->counters->ray_next));
   return 0;
+}
+
+// FV_MAIN_MINB: resident-block target of the register allocation (A/B runs)
+// FV_MAIN_MINB: resident-block target of the register allocation (A/B runs)
+template <bool TEX>
+int launch_main_warp(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+  static const int minb = getenv("FV_MAIN_MINB") ? atoi(getenv("FV_MAIN_MINB")) : 5;
+  if (minb == 6) return launch_main_warp_t<6, TEX>(ctx, F, B, threads);
+  if (minb == 8) return launch_main_warp_t<8, TEX>(ctx, F, B, threads);
+  return launch_main_warp_t<5, TEX>(ctx, F, B, threads);
 }
 
 template <bool TEX>
@@ -1836,6 +2043,27 @@ int launch_shadow(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threa
     default: FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_kernel<3, TEX><<<g, threads, 0, ctx->stream>>>(F, B)); break;
   }
   return 0;
+}
+
+// directional light on the texture path: the partial-refill pass (FV_SHADOW_V=1 keeps the
+// all-lane-refill pass for A/B runs; FV_SHADOW_REFILL tunes it)
+template <int U, int MINB>
+int launch_shadow_dir_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads, int refill) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_shadow_dir_kernel<U, MINB>, threads, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_dir_kernel<U, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B, refill));
+  return 0;
+}
+
+// refill threshold: A/B on B200 at C3, 1 / 4 / 8 / 16 / 24 / 32 free lanes: 632 / 517 / 434 / 372 /
+// 359 / 376 us (a refill costs the warp a chain of dependent loads; fewer lanes per refill pay it
+// more often). 4 samples per round and 8 blocks/SM beat 2 samples and 6 blocks/SM (+37% / +17%).
+int launch_shadow_dir(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+  static const int refill = getenv("FV_SHADOW_REFILL") ? std::min(32, std::max(1, atoi(getenv("FV_SHADOW_REFILL")))) : 24;
+  return launch_shadow_dir_t<4, 8>(ctx, F, B, threads, refill);
 }
 
 int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,
@@ -1944,6 +2172,11 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     F.cls_main = exp_class(P.step / P.ref);
     F.cls_sh = exp_class(P.step_sh / P.ref);
     F.inv_ref = (float)(1.0 / P.ref);
+    F.step_sh = (float)P.step_sh;
+    F.inv_step_sh = 1.f / F.step_sh;
+    F.min_trans = (float)P.min_trans;
+    F.ambient = (float)P.ambient;
+    for (int a = 0; a < 3; ++a) F.qs_sh[a] = F.ld[a] * F.V.inv_sp[a] * F.step_sh;
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
       // record slots: 16 per compacted ray (C3 needs ~12 incl. chunk tails), at least 4M
@@ -2017,7 +2250,11 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_scatter_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
           ctx->launches += 3;
         }
-        rc = F.V.tex ? launch_shadow<true>(ctx, F, B, threads) : launch_shadow<false>(ctx, F, B, threads);
+        static const int shadow_v = getenv("FV_SHADOW_V") ? atoi(getenv("FV_SHADOW_V")) : 2;
+        if (F.V.tex && P.light_kind == FV_LIGHT_DIRECTIONAL && shadow_v == 2)
+          rc = launch_shadow_dir(ctx, F, B, threads);
+        else
+          rc = F.V.tex ? launch_shadow<true>(ctx, F, B, threads) : launch_shadow<false>(ctx, F, B, threads);
         if (rc) return rc;
         FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;

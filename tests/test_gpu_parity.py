@@ -254,6 +254,9 @@ def test_sample_counts_match_oracle_512_subset(stack):
     assert fr.stats.samples_shadow == counts[:, 1].sum()
     fr32 = render_sparse_compact(sc, cam, comp, RenderSettings(), stats=True)
     check_fp32(fr32.rgba.reshape(-1, 4)[pix], ref)
+    # the fp32 tier takes the same samples up to step-count rounding at ray ends
+    assert abs(int(fr32.stats.samples_main) - int(counts[:, 0].sum())) <= 1e-3 * counts[:, 0].sum()
+    assert abs(int(fr32.stats.samples_shadow) - int(counts[:, 1].sum())) <= 1e-3 * counts[:, 1].sum()
 
 
 # ---------------------------------------------------------------- network
