@@ -95,6 +95,9 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   if (ctx->k_scratch) cudaFree(ctx->k_scratch);
   if (ctx->idx_scratch) cudaFree(ctx->idx_scratch);
   if (ctx->rgb_scratch) cudaFree(ctx->rgb_scratch);
+  if (ctx->wave_rec) cudaFree(ctx->wave_rec);
+  if (ctx->wave_ray) cudaFree(ctx->wave_ray);
+  if (ctx->wave_hits) cudaFree(ctx->wave_hits);
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   for (auto& sp : ctx->kspans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
   for (auto& ev : ctx->kpool) cudaEventDestroy(ev);

@@ -42,7 +42,9 @@ struct DevCounters {
   unsigned int wave_rec;   // wavefront marcher: records allocated
   unsigned int wave_next;  // wavefront marcher: shadow-pass work counter
   unsigned int wave_ord;   // wavefront marcher: chunks listed in ray order
-  unsigned int pad[3];
+  unsigned int hit_count;  // wavefront marcher: hitting rays listed by the setup pass
+  unsigned int hit_next;   // wavefront marcher: work counter of the main pass over that list
+  unsigned int pad[1];
 };
 
 // Per-launch timing spans (fv_ctx_set_kernel_timing).
@@ -87,6 +89,8 @@ struct fv_ctx {
   int64_t wave_cap = 0;
   void* wave_ray = nullptr;   // int4 per compacted ray
   int64_t wave_ray_cap = 0;
+  void* wave_hits = nullptr;  // 3 float4 per hitting ray (setup pass -> main pass)
+  int64_t wave_hits_cap = 0;
   unsigned long long launches = 0;
   // fv_frames: render / network / copy streams and their event rings (created on first use)
   cudaStream_t fstream[3] = {nullptr, nullptr, nullptr};

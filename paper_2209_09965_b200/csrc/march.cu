@@ -1083,6 +1083,10 @@ struct WaveBufs {
   int cap_a;               // > 0 (warp main pass): chunk r < cap_a is the FIRST chunk of ray r; later
                            // chunks come from pools at ids cap_a + counter (see march_wave_shadow_kernel)
   int chunk_pool;          // warp main pass: chunks claimed per counter round trip
+  int claim;               // main pass: rays claimed per counter round trip (<= 32)
+  float4* hits;            // setup pass -> main pass: 3 float4 per hitting ray
+  unsigned int* hit_count;
+  unsigned int* hit_next;
 };
 
 __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float r0, float r1, float r2,
@@ -1278,6 +1282,185 @@ __global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, W
   }
 }
 
+// March the hitting rays of a claimed set (one ray's setup per lane, hit_mask = lanes holding a
+// hitting ray) one at a time, the whole warp on each (see march_wave_main_warp_kernel).
+template <int kU, bool TEX>
+__device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& B, const float* lut,
+                                           unsigned hit_mask, int n, float last_dt, float ex, float ey,
+                                           float ez, float dx, float dy, float dz, double t0, int pix,
+                                           int rid, int& pool_cur, int& pool_end, unsigned int& pool_pref,
+                                           unsigned int& n_main, unsigned int& n_shadow) {
+  const MarchParams& P = F.P;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool lit = P.light_kind != FV_LIGHT_NONE;
+  const float amb = lit ? (float)P.ambient : 1.f;
+  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
+  const float early = (float)P.early, stepf = (float)P.step;
+  const int kPool = B.chunk_pool;
+  // ---- march the hitting rays one at a time, the whole warp on each ----
+  while (hit_mask) {
+    const int src = __ffs(hit_mask) - 1;
+    hit_mask &= hit_mask - 1;
+    const int rn = __shfl_sync(0xffffffffu, n, src);
+    const float rl = __shfl_sync(0xffffffffu, last_dt, src);
+    const float rex = __shfl_sync(0xffffffffu, ex, src), rey = __shfl_sync(0xffffffffu, ey, src),
+                rez = __shfl_sync(0xffffffffu, ez, src);
+    const float rdx = __shfl_sync(0xffffffffu, dx, src), rdy = __shfl_sync(0xffffffffu, dy, src),
+                rdz = __shfl_sync(0xffffffffu, dz, src);
+    const double rt0 = __shfl_sync(0xffffffffu, t0, src);
+    const int rpix = __shfl_sync(0xffffffffu, pix, src);
+    const int rray = __shfl_sync(0xffffffffu, rid, src);
+    // pass 0 defers shadows to records; pass 1 (record buffer full) marches them inline
+    for (int fused = 0; fused < 2; ++fused) {
+      float trans = 1.f, depth = 0.f;
+      float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;  // per-lane partial sums
+      int first = -1, chunk = -1, fill = kChunk, m = 0;
+      bool overflow = false;
+      unsigned int n_main_ray = 0, n_shadow_ray = 0;
+      for (int s0 = 0; s0 < rn; s0 += 32 * kU) {
+        TriFetch f[kU];
+#pragma unroll
+        for (int uu = 0; uu < kU; ++uu) {
+          const int s = s0 + uu * 32 + lane;
+          const float dt = s == rn - 1 ? rl : stepf;
+          const float mid = (float)s * stepf + 0.5f * dt;
+          f[uu] = tri_issue<TEX>(F.V, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid);
+        }
+        bool done = false;
+#pragma unroll
+        for (int uu = 0; uu < kU; ++uu) {
+          const int s = s0 + uu * 32 + lane;
+          const bool active = s < rn;
+          const unsigned act = __ballot_sync(0xffffffffu, active);
+          if (!act) { done = true; break; }
+          const bool last = s == rn - 1;
+          const float dt = last ? rl : stepf;
+          const float mid = (float)s * stepf + 0.5f * dt;
+          float c[4];
+          tf_apply<float>(lut, P.K, tri_finish_t<TEX>(f[uu]), c);
+          const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
+          const float a_step = active ? 1.f - keep : 0.f;
+          // transmittance in front of / behind each sample: product scan of (1 - a_step)
+          const float om = 1.f - a_step;
+          float incl = om;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const float v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl *= v;
+          }
+          float excl = __shfl_up_sync(0xffffffffu, incl, 1);
+          if (lane == 0) excl = 1.f;
+          const float t_in = trans * excl, t_out = trans * incl;
+          const float acc = 1.f - t_out;
+          // the sequential loop stops after the first sample with !(acc < early) (or the last)
+          const unsigned term = __ballot_sync(0xffffffffu, active && !(acc < early));
+          const int stop_lane = term ? __ffs(term) - 1 : 31 - __clz(act);
+          const bool use = active && lane <= stop_lane;
+          if (depth == 0.f) {
+            const unsigned dm = __ballot_sync(0xffffffffu, use && acc >= 0.5f);
+            if (dm) {
+              const int dl = __ffs(dm) - 1;
+              const float mid_d = __shfl_sync(0xffffffffu, mid, dl);
+              depth = (float)(rt0 + (double)mid_d);
+            }
+          }
+          const float contrib = t_in * a_step;
+          const bool needs_shadow = use && lit && a_step > 0.f;
+          if (!lit) {
+            if (use) {
+              rgb0 += contrib * (c[0] * I0);
+              rgb1 += contrib * (c[1] * I1);
+              rgb2 += contrib * (c[2] * I2);
+            }
+          } else if (fused) {
+            if (use) {
+              float shade = 1.f;
+              if (needs_shadow)
+                shade = amb + (1.f - amb) * shadow_fast<TEX>(F, lut, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid,
+                                                             n_shadow_ray);
+              rgb0 += contrib * (c[0] * (shade * I0));
+              rgb1 += contrib * (c[1] * (shade * I1));
+              rgb2 += contrib * (c[2] * (shade * I2));
+            }
+          } else {
+            const unsigned lm = __ballot_sync(0xffffffffu, needs_shadow);
+            const int cnt = __popc(lm);
+            if (cnt) {
+              const int room = kChunk - fill;
+              int nc = -1;
+              if (cnt > room) {
+                if (chunk < 0 && rray < B.cap_a) {
+                  nc = rray;  // the ray's first chunk: fixed id, so the shadow pass meets first chunks in ray order
+                } else {
+                  if (pool_cur >= pool_end) {
+                    pool_cur = B.cap_a + (int)__shfl_sync(0xffffffffu, pool_pref, 0);
+                    pool_end = pool_cur + kPool;
+                    if (lane == 0) pool_pref = atomicAdd(B.chunk_count, (unsigned)kPool);
+                  }
+                  nc = pool_cur++;
+                  if (nc >= B.n_chunks_cap) overflow = true;
+                }
+              }
+              if (!overflow) {
+                const int rank = __popc(lm & lt_mask);
+                if (needs_shadow) {
+                  const int slot = rank < room ? chunk * kChunk + fill + rank : nc * kChunk + (rank - room);
+                  B.rec0[slot] = make_float4(rex + rdx * mid, rey + rdy * mid, rez + rdz * mid, 0.f);
+                  B.rec1[slot] = make_float4(c[0], c[1], c[2], contrib);
+                }
+                if (nc >= 0) {
+                  if (lane == 0) {
+                    if (chunk >= 0) { B.chunk_fill[chunk] = kChunk; B.chunk_next[chunk] = nc; }
+                  }
+                  if (chunk < 0) first = nc;
+                  chunk = nc;
+                  fill = cnt - room;
+                } else {
+                  fill += cnt;
+                }
+                m += cnt;
+              }
+            }
+          }
+          n_main_ray += __popc(__ballot_sync(0xffffffffu, use));
+          trans = __shfl_sync(0xffffffffu, t_out, stop_lane);
+          if (term || overflow) { done = true; break; }
+        }
+        if (done) break;
+      }
+      if (overflow) {
+        // release this ray's chunks and march it again with inline shadows
+        if (lane == 0)
+          for (int cc = first; cc >= 0; cc = (cc == chunk) ? -1 : B.chunk_next[cc]) B.chunk_fill[cc] = 0;
+        continue;
+      }
+      n_main += n_main_ray;
+      n_shadow += n_shadow_ray;
+      if (lit && !fused && m > 0) {
+        if (lane == 0) {
+          B.chunk_fill[chunk] = fill;
+          B.chunk_next[chunk] = -1;
+          B.ray[rray] = make_int4(first, m, __float_as_int(trans), __float_as_int(depth));
+        }
+      } else {
+        if (lane == 0 && rray < B.cap_a) B.chunk_fill[rray] = 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          rgb0 += __shfl_xor_sync(0xffffffffu, rgb0, o);
+          rgb1 += __shfl_xor_sync(0xffffffffu, rgb1, o);
+          rgb2 += __shfl_xor_sync(0xffffffffu, rgb2, o);
+        }
+        if (lane == 0) {
+          write_pixel(P, rpix, rgb0, rgb1, rgb2, trans, depth);
+          B.ray[rray] = make_int4(-1, 0, 0, 0);
+        }
+      }
+      break;
+    }
+  }
+}
+
 // ---- main pass, warp per ray -------------------------------------------------------------------
 // The samples of a primary ray do not depend on the data, so a warp marches one ray 32 x kU samples
 // at a time: lane l evaluates samples s0 + u*32 + l (all loads issued first), the transmittance in
@@ -1312,7 +1495,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_warp_kernel(FastPar
   if (lit && lane == 0) pool_pref = atomicAdd(B.chunk_count, (unsigned)kPool);
   while (true) {
     unsigned int base = 0;
-    if (lane == 0) base = atomicAdd(ray_counter, 32u);
+    if (lane == 0) base = atomicAdd(ray_counter, (unsigned)B.claim);
     base = __shfl_sync(0xffffffffu, base, 0);
     if ((int)base >= k) break;
     // ---- per-lane ray setup (fp64, as the reference) ----
@@ -1321,7 +1504,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_warp_kernel(FastPar
     int pix = 0, n = 0;
     float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0;
     double t0 = 0.0;
-    if (r < k) {
+    if (r < k && lane < B.claim) {
       pix = P.idx ? P.idx[r] : r;
       ++nrays;
       const int u = pix % P.W, v = pix / P.W;
@@ -1350,167 +1533,8 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_warp_kernel(FastPar
       }
     }
     unsigned hit_mask = __ballot_sync(0xffffffffu, hit);
-    // ---- march the hitting rays one at a time, the whole warp on each ----
-    while (hit_mask) {
-      const int src = __ffs(hit_mask) - 1;
-      hit_mask &= hit_mask - 1;
-      const int rn = __shfl_sync(0xffffffffu, n, src);
-      const float rl = __shfl_sync(0xffffffffu, last_dt, src);
-      const float rex = __shfl_sync(0xffffffffu, ex, src), rey = __shfl_sync(0xffffffffu, ey, src),
-                  rez = __shfl_sync(0xffffffffu, ez, src);
-      const float rdx = __shfl_sync(0xffffffffu, dx, src), rdy = __shfl_sync(0xffffffffu, dy, src),
-                  rdz = __shfl_sync(0xffffffffu, dz, src);
-      const double rt0 = __shfl_sync(0xffffffffu, t0, src);
-      const int rpix = __shfl_sync(0xffffffffu, pix, src);
-      const int rray = (int)base + src;
-      // pass 0 defers shadows to records; pass 1 (record buffer full) marches them inline
-      for (int fused = 0; fused < 2; ++fused) {
-        float trans = 1.f, depth = 0.f;
-        float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;  // per-lane partial sums
-        int first = -1, chunk = -1, fill = kChunk, m = 0;
-        bool overflow = false;
-        unsigned int n_main_ray = 0, n_shadow_ray = 0;
-        for (int s0 = 0; s0 < rn; s0 += 32 * kU) {
-          TriFetch f[kU];
-#pragma unroll
-          for (int uu = 0; uu < kU; ++uu) {
-            const int s = s0 + uu * 32 + lane;
-            const float dt = s == rn - 1 ? rl : stepf;
-            const float mid = (float)s * stepf + 0.5f * dt;
-            f[uu] = tri_issue<TEX>(F.V, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid);
-          }
-          bool done = false;
-#pragma unroll
-          for (int uu = 0; uu < kU; ++uu) {
-            const int s = s0 + uu * 32 + lane;
-            const bool active = s < rn;
-            const unsigned act = __ballot_sync(0xffffffffu, active);
-            if (!act) { done = true; break; }
-            const bool last = s == rn - 1;
-            const float dt = last ? rl : stepf;
-            const float mid = (float)s * stepf + 0.5f * dt;
-            float c[4];
-            tf_apply<float>(lut, P.K, tri_finish_t<TEX>(f[uu]), c);
-            const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
-            const float a_step = active ? 1.f - keep : 0.f;
-            // transmittance in front of / behind each sample: product scan of (1 - a_step)
-            const float om = 1.f - a_step;
-            float incl = om;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const float v = __shfl_up_sync(0xffffffffu, incl, o);
-              if (lane >= o) incl *= v;
-            }
-            float excl = __shfl_up_sync(0xffffffffu, incl, 1);
-            if (lane == 0) excl = 1.f;
-            const float t_in = trans * excl, t_out = trans * incl;
-            const float acc = 1.f - t_out;
-            // the sequential loop stops after the first sample with !(acc < early) (or the last)
-            const unsigned term = __ballot_sync(0xffffffffu, active && !(acc < early));
-            const int stop_lane = term ? __ffs(term) - 1 : 31 - __clz(act);
-            const bool use = active && lane <= stop_lane;
-            if (depth == 0.f) {
-              const unsigned dm = __ballot_sync(0xffffffffu, use && acc >= 0.5f);
-              if (dm) {
-                const int dl = __ffs(dm) - 1;
-                const float mid_d = __shfl_sync(0xffffffffu, mid, dl);
-                depth = (float)(rt0 + (double)mid_d);
-              }
-            }
-            const float contrib = t_in * a_step;
-            const bool needs_shadow = use && lit && a_step > 0.f;
-            if (!lit) {
-              if (use) {
-                rgb0 += contrib * (c[0] * I0);
-                rgb1 += contrib * (c[1] * I1);
-                rgb2 += contrib * (c[2] * I2);
-              }
-            } else if (fused) {
-              if (use) {
-                float shade = 1.f;
-                if (needs_shadow)
-                  shade = amb + (1.f - amb) * shadow_fast<TEX>(F, lut, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid,
-                                                               n_shadow_ray);
-                rgb0 += contrib * (c[0] * (shade * I0));
-                rgb1 += contrib * (c[1] * (shade * I1));
-                rgb2 += contrib * (c[2] * (shade * I2));
-              }
-            } else {
-              const unsigned lm = __ballot_sync(0xffffffffu, needs_shadow);
-              const int cnt = __popc(lm);
-              if (cnt) {
-                const int room = kChunk - fill;
-                int nc = -1;
-                if (cnt > room) {
-                  if (chunk < 0 && rray < B.cap_a) {
-                    nc = rray;  // the ray's first chunk: fixed id, so the shadow pass meets first chunks in ray order
-                  } else {
-                    if (pool_cur >= pool_end) {
-                      pool_cur = B.cap_a + (int)__shfl_sync(0xffffffffu, pool_pref, 0);
-                      pool_end = pool_cur + kPool;
-                      if (lane == 0) pool_pref = atomicAdd(B.chunk_count, (unsigned)kPool);
-                    }
-                    nc = pool_cur++;
-                    if (nc >= B.n_chunks_cap) overflow = true;
-                  }
-                }
-                if (!overflow) {
-                  const int rank = __popc(lm & lt_mask);
-                  if (needs_shadow) {
-                    const int slot = rank < room ? chunk * kChunk + fill + rank : nc * kChunk + (rank - room);
-                    B.rec0[slot] = make_float4(rex + rdx * mid, rey + rdy * mid, rez + rdz * mid, 0.f);
-                    B.rec1[slot] = make_float4(c[0], c[1], c[2], contrib);
-                  }
-                  if (nc >= 0) {
-                    if (lane == 0) {
-                      if (chunk >= 0) { B.chunk_fill[chunk] = kChunk; B.chunk_next[chunk] = nc; }
-                    }
-                    if (chunk < 0) first = nc;
-                    chunk = nc;
-                    fill = cnt - room;
-                  } else {
-                    fill += cnt;
-                  }
-                  m += cnt;
-                }
-              }
-            }
-            n_main_ray += __popc(__ballot_sync(0xffffffffu, use));
-            trans = __shfl_sync(0xffffffffu, t_out, stop_lane);
-            if (term || overflow) { done = true; break; }
-          }
-          if (done) break;
-        }
-        if (overflow) {
-          // release this ray's chunks and march it again with inline shadows
-          if (lane == 0)
-            for (int cc = first; cc >= 0; cc = (cc == chunk) ? -1 : B.chunk_next[cc]) B.chunk_fill[cc] = 0;
-          continue;
-        }
-        n_main += n_main_ray;
-        n_shadow += n_shadow_ray;
-        if (lit && !fused && m > 0) {
-          if (lane == 0) {
-            B.chunk_fill[chunk] = fill;
-            B.chunk_next[chunk] = -1;
-            B.ray[rray] = make_int4(first, m, __float_as_int(trans), __float_as_int(depth));
-          }
-        } else {
-          if (lane == 0 && rray < B.cap_a) B.chunk_fill[rray] = 0;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            rgb0 += __shfl_xor_sync(0xffffffffu, rgb0, o);
-            rgb1 += __shfl_xor_sync(0xffffffffu, rgb1, o);
-            rgb2 += __shfl_xor_sync(0xffffffffu, rgb2, o);
-          }
-          if (lane == 0) {
-            write_pixel(P, rpix, rgb0, rgb1, rgb2, trans, depth);
-            B.ray[rray] = make_int4(-1, 0, 0, 0);
-          }
-        }
-        break;
-      }
-    }
+    march_hits<kU, TEX>(F, B, lut, hit_mask, n, last_dt, ex, ey, ez, dx, dy, dz, t0, pix, (int)base + lane,
+                        pool_cur, pool_end, pool_pref, n_main, n_shadow);
   }
   // release the unused chunks of the open pool and of the prefetched one (the shadow pass skips
   // chunks whose fill is 0)
@@ -1531,6 +1555,126 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_warp_kernel(FastPar
   if (lane == 0 && nrays) {
     atomicAdd(&P.counters->rays, (unsigned long long)nrays);
     atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
+    if (n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
+  }
+}
+
+// ---- ray setup pass + main pass over the list of hitting rays ------------------------------------
+// With the setup inside the main pass, a warp claims 32 compacted rays, sets them up one per lane and
+// then marches the ~10 that hit the volume one by one: per-warp work comes in lumps of 32 rays, and
+// the last lumps leave a tail in which most warps have exited (ncu: 19% achieved occupancy against
+// 31% theoretical; claiming 4 rays per round trip cut the pass 262 -> 185 us, but then 28 of 32 lanes
+// idle through every fp64 setup). Here a thread-per-ray pass does the fp64 setup (ray through the
+// pixel centre, slab test, step count), writes the pixels of missing rays, and lists the hitting rays
+// (warp-aggregated appends, so the list keeps the compacted order within each warp); the main pass
+// then claims hitting rays a few at a time. A/B on B200 at C3 (main pass incl. setup, us):
+// in-kernel setup 262; list with 1 / 2 / 4 / 8 rays per claim: 171 / 168 / 180 / 211. Two per claim
+// also gave the best pipelined frame rate (the pass then co-runs with the network's convs).
+__global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B) {
+  const MarchParams& P = F.P;
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned int nrays = 0, hitc = 0;
+  for (int r0 = blockIdx.x * blockDim.x; r0 < k; r0 += gridDim.x * blockDim.x) {
+    const int r = r0 + threadIdx.x;
+    bool hit = false;
+    int pix = 0, n = 0;
+    float4 h0, h1;
+    double t0 = 0.0;
+    if (r < k) {
+      pix = P.idx ? P.idx[r] : r;
+      ++nrays;
+      const int u = pix % P.W, v = pix / P.W;
+      const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
+      const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+      double d[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+      const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+      d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
+      double tend;
+      ray_box(P.pos, d, P.ext, t0, tend, hit);
+      if (!hit) {
+        write_pixel(P, pix, 0.f, 0.f, 0.f, 1.f, 0.f);
+        B.ray[r] = make_int4(-1, 0, 0, 0);
+        if (r < B.cap_a) B.chunk_fill[r] = 0;
+      } else {
+        ++hitc;
+        const double L = tend - t0;
+        n = (int)ceil((L - 1e-12) / P.step);
+        if (n < 1) n = 1;
+        const float last_dt = (float)(L - (double)(n - 1) * P.step);
+        h0 = make_float4((float)(P.pos[0] + d[0] * t0), (float)(P.pos[1] + d[1] * t0),
+                         (float)(P.pos[2] + d[2] * t0), (float)d[0]);
+        h1 = make_float4((float)d[1], (float)d[2], last_dt, __int_as_float(n));
+      }
+    }
+    const unsigned hm = __ballot_sync(0xffffffffu, hit);
+    unsigned base = 0;
+    if (lane == 0 && hm) base = atomicAdd(B.hit_count, (unsigned)__popc(hm));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hit) {
+      float4* e = B.hits + 3 * (int64_t)(base + __popc(hm & lt_mask));
+      e[0] = h0;
+      e[1] = h1;
+      e[2] = make_float4(__int_as_float(__double2loint(t0)), __int_as_float(__double2hiint(t0)),
+                         __int_as_float(r), __int_as_float(pix));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
+    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
+  }
+  if (lane == 0 && nrays) {
+    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
+    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+  }
+}
+
+template <int kU, bool TEX, int MINB>
+__global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastParams F, WaveBufs B) {
+  const MarchParams& P = F.P;
+  __shared__ float lut[4 * 256];
+  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
+  __syncthreads();
+  const int nhit = (int)*B.hit_count;
+  const int lane = threadIdx.x & 31;
+  const bool lit = P.light_kind != FV_LIGHT_NONE;
+  unsigned int n_main = 0, n_shadow = 0;
+  const int kPool = B.chunk_pool;
+  int pool_cur = 0, pool_end = 0;  // warp-uniform
+  unsigned int pool_pref = 0;      // lane 0: base of the prefetched pool
+  if (lit && lane == 0) pool_pref = atomicAdd(B.chunk_count, (unsigned)kPool);
+  while (true) {
+    unsigned int base = 0;
+    if (lane == 0) base = atomicAdd(B.hit_next, (unsigned)B.claim);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if ((int)base >= nhit) break;
+    const int i = (int)base + lane;
+    const bool valid = lane < B.claim && i < nhit;
+    float4 h0 = make_float4(0.f, 0.f, 0.f, 0.f), h1 = h0, h2 = h0;
+    if (valid) {
+      const float4* e = B.hits + 3 * (int64_t)i;
+      h0 = e[0]; h1 = e[1]; h2 = e[2];
+    }
+    const double t0 = __hiloint2double(__float_as_int(h2.y), __float_as_int(h2.x));
+    march_hits<kU, TEX>(F, B, lut, __ballot_sync(0xffffffffu, valid), __float_as_int(h1.w), h1.z, h0.x, h0.y,
+                        h0.z, h0.w, h1.x, h1.y, t0, __float_as_int(h2.w), __float_as_int(h2.z), pool_cur,
+                        pool_end, pool_pref, n_main, n_shadow);
+  }
+  if (lit) {
+    const int pref = B.cap_a + (int)__shfl_sync(0xffffffffu, pool_pref, 0);
+    for (int c = pool_cur + lane; c < pool_end; c += 32)
+      if (c < B.n_chunks_cap) B.chunk_fill[c] = 0;
+    for (int c = lane; c < kPool; c += 32)
+      if (pref + c < B.n_chunks_cap) B.chunk_fill[pref + c] = 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
+  if (lane == 0 && (n_main || n_shadow)) {
     atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
     if (n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
   }
@@ -2019,9 +2163,29 @@ int launch_main_warp_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int 
 }
 
 // FV_MAIN_MINB: resident-block target of the register allocation (A/B runs)
-// FV_MAIN_MINB: resident-block target of the register allocation (A/B runs)
+template <int MINB, bool TEX>
+int launch_main_list_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_list_kernel<2, TEX, MINB>, threads, 0));
+    per_sm = std::max(per_sm, 1);
+  }
+  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<2, TEX, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B));
+  return 0;
+}
+
+// FV_MAIN_MINB: resident-block target of the register allocation (A/B runs); FV_MAIN_LIST=0: the
+// setup runs inside the main pass (32 rays per claim)
 template <bool TEX>
 int launch_main_warp(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+  static const bool use_list = !(getenv("FV_MAIN_LIST") && atoi(getenv("FV_MAIN_LIST")) == 0);
+  if (use_list && B.hits) {
+    const int k_max = F.P.k_max;
+    const int blocks = std::max(1, std::min((k_max + 255) / 256, ctx->num_sms * 8));
+    FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<<<blocks, 256, 0, ctx->stream>>>(F, B));
+    ctx->launches += 1;
+    return launch_main_list_t<5, TEX>(ctx, F, B, threads);
+  }
   static const int minb = getenv("FV_MAIN_MINB") ? atoi(getenv("FV_MAIN_MINB")) : 5;
   if (minb == 6) return launch_main_warp_t<6, TEX>(ctx, F, B, threads);
   if (minb == 8) return launch_main_warp_t<8, TEX>(ctx, F, B, threads);
@@ -2208,6 +2372,23 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.chunk_perm = chunk_perm;
       static const int chunk_pool = getenv("FV_CHUNK_POOL") ? std::max(1, atoi(getenv("FV_CHUNK_POOL"))) : 8;
       B.chunk_pool = chunk_pool;
+      static const bool use_list = !(getenv("FV_MAIN_LIST") && atoi(getenv("FV_MAIN_LIST")) == 0);
+      static const int claim = getenv("FV_MAIN_CLAIM") ? std::min(32, std::max(1, atoi(getenv("FV_MAIN_CLAIM"))))
+                                                       : (use_list ? 2 : 32);
+      B.claim = claim;
+      B.hits = nullptr;
+      B.hit_count = &ctx->counters->hit_count;
+      B.hit_next = &ctx->counters->hit_next;
+      static const bool warp_main = !(getenv("FV_MAIN_WARP") && atoi(getenv("FV_MAIN_WARP")) == 0);
+      if (use_list && warp_main) {
+        if (k_max > ctx->wave_hits_cap) {
+          if (ctx->wave_hits) cudaFree(ctx->wave_hits);
+          ctx->wave_hits = nullptr;
+          FV_CUDA(cudaMalloc(&ctx->wave_hits, 3 * sizeof(float4) * (size_t)k_max));
+          ctx->wave_hits_cap = k_max;
+        }
+        B.hits = reinterpret_cast<float4*>(ctx->wave_hits);
+      }
       static const bool shadow_order = getenv("FV_SHADOW_ORDER") && atoi(getenv("FV_SHADOW_ORDER")) == 1;
       B.ord = shadow_order ? B.chunk_fill + ctx->wave_cap / kChunk : nullptr;
       B.ord_count = &ctx->counters->wave_ord;
@@ -2222,8 +2403,8 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<4>, threads, 0));
         per_sm_main = std::max(per_sm_main, 1);
       }
-      // ray_next, wave_rec, wave_next, wave_ord are consecutive counters
-      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 4 * sizeof(unsigned int), ctx->stream));
+      // ray_next, wave_rec, wave_next, wave_ord, hit_count, hit_next are consecutive counters
+      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 6 * sizeof(unsigned int), ctx->stream));
       const int mgrid = std::min(blocks, ctx->num_sms * per_sm_main);
       static const int main_warp = getenv("FV_MAIN_WARP") ? atoi(getenv("FV_MAIN_WARP")) : 2;  // 0: per-lane rays
       // warp main pass: half the chunk space holds first chunks at id = ray index (k_max may exceed it:
