@@ -2021,12 +2021,18 @@ __global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F,
   const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  // Latency-bound: a chain of dependent loads per ray, one warp per ray and many warps in flight
+  // (A/B: a warp walking 32 rays' records in turn took 143 us against 65). All of a ray's chunks but
+  // the last are full (the main pass compacts records with ballots), so the fill of chunk j is
+  // min(32, records - 32 j): chunk_fill is not read, and a chunk's records, shades and successor
+  // link come back in one round trip.
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < k; r += warps) {
     const int4 v = B.ray[r];
     if (v.x < 0) continue;
     float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;
-    for (int c = v.x, j = 0; j < v.y; j += kChunk) {
-      if (lane < B.chunk_fill[c]) {
+    for (int c = v.x, jj = 0; jj < v.y; jj += kChunk) {
+      const int nxt = jj + kChunk < v.y ? B.chunk_next[c] : -1;
+      if (lane < v.y - jj) {
         const int slot = c * kChunk + lane;
         const float4 q = B.rec1[slot];
         const float sh = B.shade[slot];
@@ -2034,7 +2040,7 @@ __global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F,
         rgb1 += q.w * (q.y * (sh * I1));
         rgb2 += q.w * (q.z * (sh * I2));
       }
-      c = B.chunk_next[c];
+      c = nxt;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -2437,7 +2443,8 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         else
           rc = F.V.tex ? launch_shadow<true>(ctx, F, B, threads) : launch_shadow<false>(ctx, F, B, threads);
         if (rc) return rc;
-        FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
+        static const int comp_blocks = getenv("FV_COMP_BLOCKS") ? atoi(getenv("FV_COMP_BLOCKS")) : 16;
+        FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * comp_blocks, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;
       }
     } else if (variant == 2) {
