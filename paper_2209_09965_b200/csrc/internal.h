@@ -177,6 +177,7 @@ struct fv_net {
   // K stage as tcgen05 convs, one per level: D.head (level 0) + the logits of the K blocks there
   std::vector<fv::ConvParam> kconv;
   bool kstage_dirty = true;
+  uint64_t version = 1;  // bumped by every parameter change (captured frame graphs key on it)
 };
 
 // Activation tensor in "NC8HW8" layout: C/8 planes of (H, W, 8) fp16.
@@ -206,6 +207,20 @@ struct fv_state {
   std::vector<fv::kw_t*> kw;        // per K block: softmax filter weights (9,HL,WL)
   void* arena = nullptr;
   int64_t arena_bytes = 0;
+  // reconstruct() as captured CUDA graphs, one per launch configuration (the two input / hidden
+  // buffer parities, output pointers, network version); captured on the configuration's second use
+  struct Graph {
+    const fv_net* net = nullptr;
+    uint64_t version = 0;
+    const void* x = nullptr;
+    int parity = 0, use_k = 0;
+    const float *rgb = nullptr, *o = nullptr, *od = nullptr;
+    int uses = 0;
+    unsigned long long n_launches = 0;  // kernels in the graph (ctx->launches accounting)
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<Graph> graphs;
+  cudaStream_t capture_stream = nullptr;
 };
 
 namespace fv {

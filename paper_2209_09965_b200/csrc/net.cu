@@ -119,18 +119,9 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
   return 0;
 }
 
-int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float* out_rgb,
-                float* out_o, float* out_od) {
-  fv_net* net = const_cast<fv_net*>(cnet);  // the fused K-stage convs are a cache of the params
-  for (const auto& cp : net->convs)
-    if (!(cp.w_set && cp.b_set)) {
-      set_error("network parameter %s not set", cp.name.c_str());
-      return FV_E_INVALID;
-    }
-  if (net->kstage_dirty) {
-    const int rc0 = build_kstage(ctx, net);
-    if (rc0) return rc0;
-  }
+// The launches of one reconstruction (no host-side state change: see reconstruct()).
+static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb,
+                                float* out_o, float* out_od) {
   const int ne = net->n_enc, nd = net->n_dec;
   int rc;
   const fv_act* cur = &st->x;
@@ -218,8 +209,80 @@ int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float*
     rc = finalize(ctx, st, st->od, out_rgb, out_o, out_od);
     if (rc) return rc;
   }
+  return 0;
+}
+
+static bool graphs_enabled(const fv_ctx* ctx) {
+  static const bool off = (getenv("FV_GRAPH") && atoi(getenv("FV_GRAPH")) == 0) || getenv("FV_CONV_PROF");
+  return !off && !ctx->ktiming;
+}
+
+// One frame of the W-Net. A configuration's first run is eager (it sets kernel attributes and
+// allocates lazily); from its second run on the ~31 launches are replayed as one CUDA graph.
+int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float* out_rgb,
+                float* out_o, float* out_od) {
+  fv_net* net = const_cast<fv_net*>(cnet);  // the fused K-stage convs are a cache of the params
+  for (const auto& cp : net->convs)
+    if (!(cp.w_set && cp.b_set)) {
+      set_error("network parameter %s not set", cp.name.c_str());
+      return FV_E_INVALID;
+    }
+  if (net->kstage_dirty) {
+    const int rc0 = build_kstage(ctx, net);
+    if (rc0) return rc0;
+  }
+  int rc = 0;
+  fv_state::Graph* g = nullptr;
+  if (graphs_enabled(ctx)) {
+    for (auto& e : st->graphs)
+      if (e.net == net && e.version == net->version && e.x == st->x.p && e.parity == st->parity &&
+          e.use_k == use_k && e.rgb == out_rgb && e.o == out_o && e.od == out_od) {
+        g = &e;
+        break;
+      }
+    if (!g) {
+      if (st->graphs.size() >= 8) {  // configurations changed (new outputs / weights): start over
+        for (auto& e : st->graphs)
+          if (e.exec) cudaGraphExecDestroy(e.exec);
+        st->graphs.clear();
+      }
+      fv_state::Graph e;
+      e.net = net; e.version = net->version; e.x = st->x.p; e.parity = st->parity; e.use_k = use_k;
+      e.rgb = out_rgb; e.o = out_o; e.od = out_od;
+      st->graphs.push_back(e);
+      g = &st->graphs.back();
+    }
+  }
+  if (g && g->uses >= 1 && !g->exec) {
+    // record on a private stream (the context's may be the legacy default stream, which cannot
+    // capture); the graph is then launched on the context's stream
+    if (!st->capture_stream) FV_CUDA(cudaStreamCreateWithFlags(&st->capture_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    const cudaStream_t own = ctx->stream;
+    ctx->stream = st->capture_stream;
+    cudaError_t e0 = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal);
+    if (e0 != cudaSuccess) { ctx->stream = own; return cuda_fail(e0, "cudaStreamBeginCapture (reconstruct)"); }
+    rc = reconstruct_launches(ctx, net, st, use_k, out_rgb, out_o, out_od);
+    const cudaError_t e1 = cudaStreamEndCapture(ctx->stream, &graph);
+    ctx->stream = own;
+    if (rc) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (e1 != cudaSuccess) return cuda_fail(e1, "cudaStreamEndCapture (reconstruct)");
+    const cudaError_t e2 = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e2 != cudaSuccess) { g->exec = nullptr; return cuda_fail(e2, "cudaGraphInstantiate (reconstruct)"); }
+  }
+  if (g && g->exec) {
+    FV_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
+    ctx->launches += g->n_launches;
+  } else {
+    const unsigned long long before = ctx->launches;
+    rc = reconstruct_launches(ctx, net, st, use_k, out_rgb, out_o, out_od);
+    if (rc) return rc;
+    if (g) g->n_launches = ctx->launches - before;
+  }
+  if (g) ++g->uses;
   std::swap(st->x, st->xalt);
-  st->parity = newp;
+  st->parity ^= 1;
   st->fresh = false;
   return 0;
 }
@@ -355,6 +418,7 @@ int fv_net_set_param(fv_ctx* ctx, fv_net* net, const char* name, const float* ho
     cp.b_host.assign(host, host + count);
     cp.b_set = true;
   }
+  ++net->version;
   if (idx == net->head_index || cp.ksize == 1) net->kstage_dirty = true;  // folded into kconv
   if (!(cp.w_set && cp.b_set) || cp.ksize == 1 || idx == net->head_index) return 0;
   return conv_prepare(ctx, cp);
@@ -454,6 +518,9 @@ int fv_state_reset(fv_ctx* ctx, fv_state* st) {
 
 int fv_state_destroy(fv_state* st) {
   if (!st) return 0;
+  for (auto& e : st->graphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  if (st->capture_stream) cudaStreamDestroy(st->capture_stream);
   if (st->arena) cudaFree(st->arena);
   delete st;
   return 0;
