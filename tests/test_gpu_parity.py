@@ -613,3 +613,41 @@ def test_fused_pipeline_equals_separate_calls_on_padded_films(stack, h, w):
         got = pipe.rgb.cpu().numpy()
         assert got.shape == (h, w, 3)
         assert np.array_equal(got, img), (i, np.abs(got - img).max())
+
+
+_GRAPH_PROBE = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2209_09965_b200 import network as N
+from paper_2209_09965_b200.noise import default_stack
+from paper_2209_09965_b200.pipeline import FramePipeline
+from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+spec = ExperimentSpec(mode="hifi", width=320, height=184)
+scene = default_scene("sphere_shells", (96, 96, 96))
+net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, 320, 184)
+pipe = FramePipeline(scene, net, (184, 320), default_stack())
+outs = []
+for i in range(6):
+    pipe.step(cams[i], spec.fovea(), i)
+    outs.append(pipe.rgb.cpu().numpy())
+np.save(sys.argv[2], np.stack(outs))
+"""
+
+
+def test_graph_replay_equals_eager_launches(tmp_path):
+    """reconstruct() replayed from captured CUDA graphs (frames 2+) == the same frames launched eagerly."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    outs = {}
+    for flag in ("0", "1"):
+        out = tmp_path / f"frames_{flag}.npy"
+        env = dict(os.environ, FV_GRAPH=flag)
+        subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out)], env=env, check=True, timeout=300)
+        outs[flag] = np.load(out)
+    assert np.array_equal(outs["0"], outs["1"])
