@@ -1865,8 +1865,8 @@ __global__ void __launch_bounds__(128, 8) march_wave_shadow_kernel(FastParams F,
 //    error outside;
 //  * marches U samples per lane per round and, between rounds, hands a finished lane the next
 //    record slot once at least `refill_min` lanes of the warp are free -- refilled lanes take
-//    consecutive slots (neighbouring samples of one primary ray, whose light rays overlap), so the
-//    coherence that made all-lane refills win over per-lane ones is kept.
+//    consecutive slots (neighbouring samples of one primary ray, whose light rays overlap) from a
+//    warp-private range, so refills neither lose that coherence nor wait on a shared counter.
 // Results match march_wave_shadow_kernel to fp32 rounding (same samples, same termination rule).
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
@@ -1880,7 +1880,8 @@ __device__ __forceinline__ float lg2_approx(float x) {
 }
 
 template <int U, int MINB>
-__global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastParams F, WaveBufs B, int refill_min) {
+__global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastParams F, WaveBufs B, int refill_min,
+                                                                          unsigned claim_blk) {
   const MarchParams& P = F.P;
   // om table: (1 - a_i, -(a_{i+1} - a_i)), padded with (1 - a_{K-1}, 0) so that the index may
   // round to K-1 at s = 1 (w = 0 there)
@@ -1904,18 +1905,30 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
   bool exhausted = false;
   int my = -1, s = 0, last = -1;  // free lanes keep last = -1, so none of their samples is live
   float qax = 0.f, qay = 0.f, qaz = 0.f, fl = 0.f, el = 0.f, trans = 1.f;
+  // Record slots come from a warp-private range [lb, le) of claim_blk slots; the next range is
+  // claimed (lane 0) when the current one opens, so a refill never waits on the shared counter
+  // (one contended atomic per claim_blk slots instead of one per refill).
+  unsigned lb = 0, le = 0, pend = 0;
+  if (lane == 0) pend = atomicAdd(B.next, claim_blk);
   while (true) {
     while (true) {
       const bool need = my < 0 && !exhausted;
       const unsigned msk = __ballot_sync(0xffffffffu, need);
       const unsigned busy = __ballot_sync(0xffffffffu, my >= 0);
       if (!msk || (busy && __popc(msk) < refill_min)) break;
-      const int leader = __ffs(msk) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(B.next, (unsigned)__popc(msk));
-      base = __shfl_sync(0xffffffffu, base, leader);
+      const unsigned cnt = (unsigned)__popc(msk), rank = (unsigned)__popc(msk & lt_mask);
+      const unsigned take = min(cnt, le - lb);
+      unsigned slot = lb + rank;
+      lb += take;
+      if (take < cnt) {
+        const unsigned nb = __shfl_sync(0xffffffffu, pend, 0);
+        if (lane == 0) pend = atomicAdd(B.next, claim_blk);
+        if (rank >= take) slot = nb + (rank - take);
+        lb = nb + (cnt - take);
+        le = nb + claim_blk;
+      }
       if (need) {
-        int i = (int)(base + __popc(msk & lt_mask));
+        int i = slot < (unsigned)nslots ? (int)slot : nslots;
         if (i >= nslots) {
           exhausted = true;
         } else {
@@ -2224,15 +2237,19 @@ int launch_shadow_dir_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int
     FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_shadow_dir_kernel<U, MINB>, threads, 0));
     per_sm = std::max(per_sm, 1);
   }
-  FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_dir_kernel<U, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B, refill));
+  static const unsigned blk = getenv("FV_SHADOW_CLAIM") ? (unsigned)std::max(32, atoi(getenv("FV_SHADOW_CLAIM"))) : 64u;
+  FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_dir_kernel<U, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B, refill, blk));
   return 0;
 }
 
-// refill threshold: A/B on B200 at C3, 1 / 4 / 8 / 16 / 24 / 32 free lanes: 632 / 517 / 434 / 372 /
-// 359 / 376 us (a refill costs the warp a chain of dependent loads; fewer lanes per refill pay it
-// more often). 4 samples per round and 8 blocks/SM beat 2 samples and 6 blocks/SM (+37% / +17%).
+// Refill threshold (free lanes) and private slot-range size, A/B on B200 at C3 (shadow pass, us):
+// with one shared-counter atomic per refill, 1 / 4 / 8 / 16 / 24 / 32 free lanes gave 632 / 517 /
+// 434 / 372 / 359 / 376 (each refill waited on the contended counter); with warp-private ranges of
+// 64 slots, 1 / 2 / 4 / 8 / 16 / 24 gave 386 / 364 / 345 / 335 / 371 / 395, ranges of 32 / 48 / 128 /
+// 256 slots at 8 free lanes 345 / 335 / 374 / 441. 4 samples per round and 8 blocks/SM beat 2
+// samples and 6 blocks/SM (+37% / +17%).
 int launch_shadow_dir(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
-  static const int refill = getenv("FV_SHADOW_REFILL") ? std::min(32, std::max(1, atoi(getenv("FV_SHADOW_REFILL")))) : 24;
+  static const int refill = getenv("FV_SHADOW_REFILL") ? std::min(32, std::max(1, atoi(getenv("FV_SHADOW_REFILL")))) : 8;
   return launch_shadow_dir_t<4, 8>(ctx, F, B, threads, refill);
 }
 
