@@ -13,8 +13,9 @@
 //
 // Compaction is a single-pass decoupled look-back scan: each CTA takes a 2048-pixel tile
 // (dynamic tile index => tiles retire in order), publishes its aggregate, looks back over its
-// predecessors' epoch-tagged status words and writes its indices. Status words carry the
-// call's epoch, so they never need clearing between calls.
+// predecessors' epoch-tagged status words -- 32 at a time, one per lane of the first warp -- and
+// writes its indices. Status words carry the call's epoch, so they never need clearing between
+// calls.
 #include <algorithm>
 
 #include "internal.h"
@@ -111,29 +112,44 @@ __global__ void __launch_bounds__(kThreads) mask_compact_kernel(MaskParams p) {
     }
     if (lane < kThreads / 32) s_warp[lane] = wi - w;  // exclusive per warp
     const unsigned int aggregate = __shfl_sync(0xffffffffu, wi, kThreads / 32 - 1);
-    // decoupled look-back (lane 0)
-    if (lane == 0) {
-      volatile unsigned long long* st = p.status;
-      unsigned int excl = 0;
-      if (tile == 0) {
+    // decoupled look-back, a warp-wide window of 32 predecessors per step (lane l reads tile
+    // j - l): one memory round trip covers 32 tiles instead of one
+    volatile unsigned long long* st = p.status;
+    if (tile == 0) {
+      if (lane == 0) {
         st[0] = pack_status(p.epoch, 2u, aggregate);
-      } else {
+        s_prefix = 0;
+      }
+    } else {
+      if (lane == 0) {
         st[tile] = pack_status(p.epoch, 1u, aggregate);
         __threadfence();
-        int j = (int)tile - 1;
-        while (true) {
-          unsigned long long s = st[j];
-          if ((unsigned int)(s >> 32) != p.epoch || ((s >> 30) & 3u) == 0u) continue;
-          excl += (unsigned int)(s & 0x3fffffffu);
-          if (((s >> 30) & 3u) == 2u) break;
-          --j;
+      }
+      __syncwarp();
+      unsigned int excl = 0;
+      for (int j = (int)tile - 1;; j -= 32) {
+        const int t = j - lane;
+        unsigned long long s = pack_status(p.epoch, 2u, 0u);  // before tile 0: an inclusive 0
+        if (t >= 0) {
+          do { s = st[t]; } while ((unsigned int)(s >> 32) != p.epoch || ((s >> 30) & 3u) == 0u);
         }
+        const unsigned inc = __ballot_sync(0xffffffffu, ((s >> 30) & 3u) == 2u);
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        unsigned int v = lane <= stop ? (unsigned int)(s & 0x3fffffffu) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+      }
+      if (lane == 0) {
         __threadfence();
         st[tile] = pack_status(p.epoch, 2u, excl + aggregate);
+        s_prefix = excl;
       }
-      s_prefix = excl;
+    }
+    if (lane == 0) {
       const int64_t ntiles = (npix + kTile - 1) / kTile;
-      if ((int64_t)tile == ntiles - 1) *p.k_out = (int32_t)(excl + aggregate);
+      if ((int64_t)tile == ntiles - 1) *p.k_out = (int32_t)(s_prefix + aggregate);
     }
   }
   __syncthreads();
