@@ -494,7 +494,12 @@ int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st
   }
   for (auto& e : ctx->fev)
     if (!e) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  cudaStream_t s_r = ctx->fstream[0], s_n = ctx->fstream[1], s_c = ctx->fstream[2];
+  // FV_PIPE_OVERLAP=1: render t+1 on its own stream next to reconstruct t; by default both run
+  // in order on the network stream (only the copy-out overlaps): the marcher's persistent grids
+  // and the convs' persistent CTAs do not share SMs well (C5: 71 frames/s overlapped against 95
+  // in order), and the two barely overlap at C3
+  static const bool overlap = getenv("FV_PIPE_OVERLAP") && atoi(getenv("FV_PIPE_OVERLAP")) == 1;
+  cudaStream_t s_r = overlap ? ctx->fstream[0] : ctx->fstream[1], s_n = ctx->fstream[1], s_c = ctx->fstream[2];
   cudaEvent_t* rendered = ctx->fev;      // [2]
   cudaEvent_t* net_done = ctx->fev + 2;  // [2]
   cudaEvent_t* copied = ctx->fev + 4;    // [2]

@@ -221,6 +221,7 @@ struct fv_state {
   };
   std::vector<Graph> graphs;
   cudaStream_t capture_stream = nullptr;
+  int capture_prio = 0;
 };
 
 namespace fv {

@@ -256,7 +256,18 @@ int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float*
   if (g && g->uses >= 1 && !g->exec) {
     // record on a private stream (the context's may be the legacy default stream, which cannot
     // capture); the graph is then launched on the context's stream
-    if (!st->capture_stream) FV_CUDA(cudaStreamCreateWithFlags(&st->capture_stream, cudaStreamNonBlocking));
+    // (with the context stream's priority: captured kernel nodes keep the capturing stream's
+    // priority, and the network's high priority is what lets it win SMs over the marcher)
+    int prio = 0;
+    if (ctx->stream) FV_CUDA(cudaStreamGetPriority(ctx->stream, &prio));
+    if (st->capture_stream && st->capture_prio != prio) {
+      cudaStreamDestroy(st->capture_stream);
+      st->capture_stream = nullptr;
+    }
+    if (!st->capture_stream) {
+      FV_CUDA(cudaStreamCreateWithPriority(&st->capture_stream, cudaStreamNonBlocking, prio));
+      st->capture_prio = prio;
+    }
     cudaGraph_t graph = nullptr;
     const cudaStream_t own = ctx->stream;
     ctx->stream = st->capture_stream;

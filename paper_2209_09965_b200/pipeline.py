@@ -102,8 +102,11 @@ class FramePipeline:
             # the network is the critical path: its stream gets the higher priority, so the marcher's
             # blocks fill the SMs the convs leave idle instead of delaying them
             prio = int(os.environ.get("FV_PIPE_PRIORITY", "1"))
-            self._s_render = torch.cuda.Stream(device=self.ctx.device, priority=0)
             self._s_net = torch.cuda.Stream(device=self.ctx.device, priority=-1 if prio else 0)
+            # FV_PIPE_OVERLAP=1: the render of frame t+1 on its own stream next to frame t's
+            # network; by default one stream in frame order (see fv_frames in csrc/api.cu)
+            overlap = os.environ.get("FV_PIPE_OVERLAP", "0") == "1"
+            self._s_render = torch.cuda.Stream(device=self.ctx.device, priority=0) if overlap else self._s_net
             self._rctx = _lib.Context(self.ctx.device, stream=self._s_render)
             self._nctx = _lib.Context(self.ctx.device, stream=self._s_net)
             self._rctx.ensure_noise(self.ctx._noise_ref)

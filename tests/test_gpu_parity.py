@@ -359,8 +359,11 @@ def test_end_to_end_c1_against_reference(golden, stack):
     assert O.psnr(host, g["img1"]) >= 55.0
 
 
-def test_pipelined_frames_equal_serial_frames(stack):
-    """Two-stream pipelining (render t+1 during reconstruct t) must not change any frame."""
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_pipelined_frames_equal_serial_frames(stack, overlap, monkeypatch):
+    """The pipelined frame loop -- one stream in frame order, or (FV_PIPE_OVERLAP=1) render t+1 on a
+    second stream during reconstruct t -- must not change any frame."""
+    monkeypatch.setenv("FV_PIPE_OVERLAP", overlap)
     from paper_2209_09965_b200.pipeline import FramePipeline
     from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
     from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene

@@ -1,0 +1,6 @@
+# frame loop on one stream (default) vs render t+1 || network t (FV_PIPE_OVERLAP=1), C5 and C3
+for cfg in "FV_PIPE_OVERLAP=0" "FV_PIPE_OVERLAP=1"; do
+  env $cfg timeout 600 python bench.py --config c5 --steps 6 --warmup 3 --no-cpu-baseline > gpurun_out/p.log 2>&1
+  tail -1 gpurun_out/p.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']; print('c5 $cfg', round(d['value'],1), 'serial', round(d['timing']['serial_ms_per_frame'],3), 'e2e', round(d['e2e']['value'],1))" | tee -a gpurun_out/ab_results.txt
+done
+bash tools/probes/ab_env.sh "FV_PIPE_OVERLAP=0" "FV_PIPE_OVERLAP=1" "FV_PIPE_OVERLAP=0" "FV_PIPE_OVERLAP=1"
