@@ -247,7 +247,7 @@ def run_ours(args, cfg):
     pipe.run_pipelined([(cams[j % PATH_FRAMES], fovea, j) for j in rank_frames(rank, 0, wu)])
     torch.cuda.synchronize()
     timed_frames = rank_frames(rank, wu, k)
-    # --- device-resident timed region 1: the headline, frames pipelined over two streams ---
+    # --- device-resident timed region 1: the headline, the frame loop (run_pipelined) ---
     # (mask + march of frame t+1 on one stream while frame t reconstructs on the other)
     if world > 1:
         torch.distributed.barrier()
@@ -378,14 +378,16 @@ def run_ours(args, cfg):
         "phase_ms": {"mask": mask_ms, "march": march_ms, "reconstruct": net_ms},
         "timing": {"pipelined_ms_per_frame": pipe_ms / k, "serial_ms_per_frame": serial_ms / k,
                    "serial_fps": whole_job_rate(k, world, serial_ms / 1e3),
-                   "how": "value = K frames pipelined over two streams (render t+1 || reconstruct t), "
-                          "CUDA events on the pipeline stream; phase_ms from the same frames serialised"},
+                   "how": "value = K frames through the frame loop (FramePipeline.run_pipelined: mask, march "
+                          "and network in frame order on one stream, the network replayed as a CUDA graph; "
+                          "FV_PIPE_OVERLAP=1 renders t+1 on a second stream), CUDA events on the pipeline "
+                          "stream; phase_ms from the same frames with events between the phases"},
         "roofline": roof, "stages": stages, "kernels": kernels, "marcher": marcher,
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": h * w * 3 * 4, "serial_fv_frame_fps": e2e_serial_fps,
                 "how": f"fv_frames C-ABI call over {ke} frames, wall clock: per frame camera + fovea by value "
-                       "(H2D as kernel parameters), (H,W,3) f32 image D2H into pinned host memory; render t+1, "
-                       "reconstruct t and the copy of t-1 overlap on three streams"},
+                       "(H2D as kernel parameters), (H,W,3) f32 image D2H into pinned host memory; the copy of "
+                       "frame t-1 overlaps the compute of frame t (copy stream)"},
         "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
