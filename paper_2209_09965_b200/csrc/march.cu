@@ -1573,6 +1573,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_warp_kernel(FastPar
 // also gave the best pipelined frame rate (the pass then co-runs with the network's convs).
 __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
+  __shared__ unsigned s_cnt[8], s_off[8], s_base;
   const int k = P.k_dev ? *P.k_dev : P.k_max;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -1611,10 +1612,19 @@ __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B
         h1 = make_float4((float)d[1], (float)d[2], last_dt, __int_as_float(n));
       }
     }
+    // one append per block (the shared list counter is contended: one atomic per warp cost ~2x)
     const unsigned hm = __ballot_sync(0xffffffffu, hit);
-    unsigned base = 0;
-    if (lane == 0 && hm) base = atomicAdd(B.hit_count, (unsigned)__popc(hm));
-    base = __shfl_sync(0xffffffffu, base, 0);
+    const int warp = threadIdx.x >> 5;
+    if (lane == 0) s_cnt[warp] = __popc(hm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned t = 0;
+      for (int w2 = 0; w2 < 8; ++w2) { s_off[w2] = t; t += s_cnt[w2]; }
+      s_base = t ? atomicAdd(B.hit_count, t) : 0u;
+    }
+    __syncthreads();
+    const unsigned base = s_base + s_off[warp];
+    __syncthreads();  // (s_cnt / s_off / s_base are rewritten by the next iteration)
     if (hit) {
       float4* e = B.hits + 3 * (int64_t)(base + __popc(hm & lt_mask));
       e[0] = h0;
