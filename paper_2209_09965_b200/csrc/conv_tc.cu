@@ -155,7 +155,7 @@ __device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint3
   }
 }
 
-template <int R, int N, int kStages, bool BRES, bool FUSED>
+template <int R, int N, int kStages, bool BRES, bool FUSED, bool CO = false>
 __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   using C = Cfg<R, N, kStages, BRES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -224,11 +224,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         const int n_items = gs_fill * (R + 2);
         // bytes this lane will copy
         uint32_t my_bytes = 0;
+        // CO (1x1 convs): only halo rows 1..R and columns 1..128 are read (the centre tap), so the
+        // rest of the halo is neither loaded nor zero-filled
+        constexpr int co = CO ? 1 : 0;
         for (int item = lane; item < n_items; item += 32) {
           const int g = item / (R + 2), row = item % (R + 2);
           const int y = y0 - 1 + row;
+          if (CO && (row == 0 || row == R + 1)) continue;
           if (g0 + g < a.groups && y >= 0 && y < a.H) {
-            const int lo = max(x0 - 1, 0), hi = min(x0 + kTileW + 1, a.W);
+            const int lo = max(x0 - 1 + co, 0), hi = min(x0 + kTileW + 1 - co, a.W);
             if (hi > lo) my_bytes += (uint32_t)(hi - lo) * 16u;
           }
         }
@@ -248,8 +252,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
           const int y = y0 - 1 + row;
           const uint32_t row_addr = a_st + g * C::kPlaneBytes + row * kRowBytes;
           const int gg = g0 + g;
+          if (CO && (row == 0 || row == R + 1)) continue;
           if (gg < a.groups && y >= 0 && y < a.H) {
-            const int lo = max(x0 - 1, 0), hi = min(x0 + kTileW + 1, a.W);
+            const int lo = max(x0 - 1 + co, 0), hi = min(x0 + kTileW + 1 - co, a.W);
             // locate the source tensor of this channel group (concat folded into the loader)
             int s = 0, gl = gg;
             while (s + 1 < a.n_src && gl >= a.src_groups[s]) { gl -= a.src_groups[s]; ++s; }
@@ -258,10 +263,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
             if (hi > lo)
               sm100::bulk_g2s(row_addr + c_lo * 16, plane + ((int64_t)y * a.W + lo) * 8,
                               (uint32_t)(hi - lo) * 16u, bar_full + 8 * st);
-            for (int c = 0; c < c_lo; ++c) sm100::st_shared_zero16(row_addr + c * 16);
-            for (int c = max(c_hi, 0); c < kHaloW; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+            for (int c = co; c < c_lo; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+            for (int c = max(c_hi, 0); c < kHaloW - co; ++c) sm100::st_shared_zero16(row_addr + c * 16);
           } else {
-            for (int c = 0; c < kHaloW; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+            for (int c = co; c < kHaloW - co; ++c) sm100::st_shared_zero16(row_addr + c * 16);
           }
         }
         sm100::fence_proxy_async_smem();
@@ -494,13 +499,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   }
 }
 
-template <int R, int N, int S, bool BRES, bool FUSED>
+template <int R, int N, int S, bool BRES, bool FUSED, bool CO = false>
 int launch(fv_ctx* ctx, const ConvArgs& args) {
   using C = Cfg<R, N, S, BRES>;
   static_assert(C::kSmem <= 227 * 1024, "conv tile configuration exceeds shared memory");
   static bool attr_set = false;
   if (!attr_set) {
-    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  C::kSmem));
     attr_set = true;
   }
@@ -510,7 +515,7 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
   ktime_begin(ctx);
-  conv3x3_tc_kernel<R, N, S, BRES, FUSED><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
+  conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
   ktime_end(ctx, FV_KC_CONV, a.flops);
   if (a.prof) {
     std::vector<unsigned long long> h((size_t)grid * kProfSlots);
@@ -642,6 +647,7 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
 #define FV_LAUNCH(R_, N_, S_) \
   (res ? (fu ? launch<R_, N_, S_, true, true>(ctx, a) : launch<R_, N_, S_, true, false>(ctx, a)) \
        : (fu ? launch<R_, N_, S_, false, true>(ctx, a) : launch<R_, N_, S_, false, false>(ctx, a)))
+  if (a.center_only && cp.n_pad == 32 && res && !fu) return launch<4, 32, 5, true, false, true>(ctx, a);
   switch (cp.n_pad) {
     case 16: return FV_LAUNCH(4, 16, 6);
     case 32: return FV_LAUNCH(4, 32, 5);
