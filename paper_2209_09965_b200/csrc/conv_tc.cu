@@ -213,6 +213,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int x0 = (tile % a.tiles_x) * kTileW;
       const int y0 = (tile / a.tiles_x) * R;
+      uint32_t tile_bytes_per_group;
+      {
+        const int r_lo = CO ? 1 : 0, r_hi = CO ? R : R + 1;  // halo rows loaded
+        const int rows_in = max(0, min(r_hi, a.H - y0) - max(r_lo, 1 - y0) + 1);
+        const int lo = max(x0 - 1 + (CO ? 1 : 0), 0), hi = min(x0 + kTileW + 1 - (CO ? 1 : 0), a.W);
+        tile_bytes_per_group = hi > lo ? (uint32_t)(rows_in * (hi - lo) * 16) : 0u;
+      }
       for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
         const int st = it % kStages;
         const uint32_t round = it / kStages;
@@ -222,23 +229,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         if (gs > kStageGroups) gs = kStageGroups;
         const int gs_fill = (gs + 1) & ~1;  // odd group count: one zero group
         const int n_items = gs_fill * (R + 2);
-        // bytes this lane will copy
-        uint32_t my_bytes = 0;
         // CO (1x1 convs): only halo rows 1..R and columns 1..128 are read (the centre tap), so the
         // rest of the halo is neither loaded nor zero-filled
         constexpr int co = CO ? 1 : 0;
-        for (int item = lane; item < n_items; item += 32) {
-          const int g = item / (R + 2), row = item % (R + 2);
-          const int y = y0 - 1 + row;
-          if (CO && (row == 0 || row == R + 1)) continue;
-          if (g0 + g < a.groups && y >= 0 && y < a.H) {
-            const int lo = max(x0 - 1 + co, 0), hi = min(x0 + kTileW + 1 - co, a.W);
-            if (hi > lo) my_bytes += (uint32_t)(hi - lo) * 16u;
-          }
-        }
-        uint32_t tot = my_bytes;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        // bytes the stage's bulk copies deliver: every real group copies the same in-image rows and
+        // column span of the tile (no per-item pass and warp reduction on the producer's path)
+        const uint32_t tot = (uint32_t)gs * tile_bytes_per_group;
         const uint32_t b_bytes = BRES ? 0u : (uint32_t)(9 * gs_fill * N * 16);
         if (lane == 0) sm100::mbar_arrive_expect_tx(bar_full + 8 * st, tot + b_bytes);
         __syncwarp();
