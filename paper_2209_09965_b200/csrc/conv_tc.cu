@@ -643,7 +643,8 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
 #define FV_LAUNCH(R_, N_, S_) \
   (res ? (fu ? launch<R_, N_, S_, true, true>(ctx, a) : launch<R_, N_, S_, true, false>(ctx, a)) \
        : (fu ? launch<R_, N_, S_, false, true>(ctx, a) : launch<R_, N_, S_, false, false>(ctx, a)))
-  if (a.center_only && cp.n_pad == 32 && res && !fu) return launch<4, 32, 5, true, false, true>(ctx, a);
+  if (a.center_only && cp.n_pad == 32 && !fu)
+    return res ? launch<4, 32, 5, true, false, true>(ctx, a) : launch<4, 32, 5, false, false, true>(ctx, a);
   switch (cp.n_pad) {
     case 16: return FV_LAUNCH(4, 16, 6);
     case 32: return FV_LAUNCH(4, 32, 5);
