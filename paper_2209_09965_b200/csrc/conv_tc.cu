@@ -236,8 +236,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         // column span of the tile (no per-item pass and warp reduction on the producer's path)
         const uint32_t tot = (uint32_t)gs * tile_bytes_per_group;
         const uint32_t b_bytes = BRES ? 0u : (uint32_t)(9 * gs_fill * N * 16);
+        // (no warp sync before the copies: a copy completing ahead of the expect-tx only takes the
+        // barrier's tx-count below zero for a while; the phase still needs the final arrival below)
         if (lane == 0) sm100::mbar_arrive_expect_tx(bar_full + 8 * st, tot + b_bytes);
-        __syncwarp();
         const uint32_t a_st = sm100::smem_u32(sA + st * C::kABytes);
         if (!BRES && lane == 0)
           sm100::bulk_g2s(sm100::smem_u32(sB + st * C::kBBytes),
