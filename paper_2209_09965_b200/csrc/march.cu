@@ -2377,7 +2377,11 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
       // record slots: 16 per compacted ray (C3 needs ~12 incl. chunk tails), at least 4M
-      const int64_t rec_cap = std::max<int64_t>(4 << 20, 16ll * k_max) / kChunk * kChunk;
+      // FV_WAVE_REC_PER_RAY (default 16): record slots per compacted ray; FV_WAVE_REC_CAP: an
+      // absolute capacity (tests force the record-overflow fallback with a tiny one)
+      static const int64_t per_ray = getenv("FV_WAVE_REC_PER_RAY") ? std::max(1, atoi(getenv("FV_WAVE_REC_PER_RAY"))) : 16;
+      static const int64_t cap_env = getenv("FV_WAVE_REC_CAP") ? std::max(2 * kChunk, atoi(getenv("FV_WAVE_REC_CAP"))) : 0;
+      const int64_t rec_cap = (cap_env ? cap_env : std::max<int64_t>(4 << 20, per_ray * k_max)) / kChunk * kChunk;
       if (rec_cap > ctx->wave_cap) {
         if (ctx->wave_rec) cudaFree(ctx->wave_rec);
         ctx->wave_rec = nullptr;

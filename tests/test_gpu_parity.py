@@ -654,3 +654,20 @@ def test_graph_replay_equals_eager_launches(tmp_path):
         subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out)], env=env, check=True, timeout=300)
         outs[flag] = np.load(out)
     assert np.array_equal(outs["0"], outs["1"])
+
+
+def test_record_overflow_falls_back_to_inline_shadows():
+    """With a tiny shadow-record buffer (FV_WAVE_REC_CAP) most rays overflow it and are re-marched
+    with inline shadow rays: the renders must still meet the same golden tolerances and the fp32
+    sample counts. Runs the render tests in a subprocess (the capacity is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    here = Path(__file__).resolve()
+    env = dict(os.environ, FV_WAVE_REC_CAP="2048")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(here), "-q", "-p", "no:cacheprovider", "-k",
+                        "render_full or render_sparse_compact or c1_orbit or anisotropic or sample_counts"],
+                       env=env, cwd=here.parents[1], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
