@@ -715,345 +715,6 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Persistent fast-tier marcher: one trilinear sample per lane per loop iteration.
-//
-// The inline-shadow kernel above nests a variable-length shadow march inside a variable-length
-// main march, so lanes of a warp idle while their neighbours finish (ncu: 14 of 32 threads
-// active, 15% achieved occupancy from the ray-length tail). Here every lane runs a small state
-// machine -- MAIN sample, SHADOW sample, or fetch a new ray -- and each iteration of the warp
-// loop takes exactly one volume sample per busy lane, whichever ray it belongs to. Lanes refill
-// from a global ray counter with one warp-aggregated atomic, so warps stay full until the list
-// runs dry. Each ray is still marched start to finish by one lane in the reference's order, so
-// the results are those of the per-ray kernel.
-__global__ void __launch_bounds__(128) march_persist_kernel(FastParams F, unsigned int* ray_counter) {
-  const MarchParams& P = F.P;
-  __shared__ float lut[4 * 256];
-  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
-  __syncthreads();
-  const int k = P.k_dev ? *P.k_dev : P.k_max;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const bool lit = P.light_kind != FV_LIGHT_NONE;
-  const float amb = lit ? (float)P.ambient : 1.f;
-  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
-  const float early = (float)P.early, stepf = (float)P.step, step_sh = (float)P.step_sh;
-  const float mt = (float)P.min_trans;
-  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
-
-  // per-lane ray state
-  int pix = -1;            // -1: no ray
-  bool exhausted = false;
-  float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0;
-  int s = 0, n = 0;
-  float last_dt = 0.f;
-  double t0 = 0.0;
-  float rgb0 = 0, rgb1 = 0, rgb2 = 0, trans = 1.f, depth = 0.f;
-  bool in_shadow = false;
-  float pc0 = 0, pc1 = 0, pc2 = 0, pa = 0;          // pending main sample awaiting its shade
-  float spx = 0, spy = 0, spz = 0, sdx = 0, sdy = 0, sdz = 0, st = 0, stend = 0, strans = 1.f;
-
-  auto finish = [&](int p) {
-    const float bga = (float)P.bg[3];
-    const float o0 = rgb0 + (trans * bga) * (float)P.bg[0], o1 = rgb1 + (trans * bga) * (float)P.bg[1],
-                o2 = rgb2 + (trans * bga) * (float)P.bg[2], o3 = (1.f - trans) + trans * bga;
-    if (P.rgba) *reinterpret_cast<float4*>(P.rgba + (int64_t)p * 4) = make_float4(o0, o1, o2, o3);
-    if (P.depth) P.depth[p] = depth;
-    if (P.net_in) {
-      const int u = p % P.W, v = p / P.W;
-      __half2* px = reinterpret_cast<__half2*>(P.net_in + ((int64_t)v * P.net_wp + u) * 8);
-      px[0] = __floats2half2_rn(o0, o1);
-      px[1] = __floats2half2_rn(o2, o3);
-    }
-  };
-
-  while (true) {
-    // ---- refill lanes without a ray (rays that miss the box are finished right here) ----
-    while (true) {
-      const bool need = pix < 0 && !exhausted;
-      const unsigned m = __ballot_sync(0xffffffffu, need);
-      if (!m) break;
-      const int leader = __ffs(m) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(ray_counter, (unsigned)__popc(m));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (need) {
-        const int r = (int)(base + __popc(m & lt_mask));
-        if (r >= k) {
-          exhausted = true;
-        } else {
-          const int p = P.idx ? P.idx[r] : r;
-          ++nrays;
-          const int u = p % P.W, v = p / P.W;
-          const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
-          const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
-          double d[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
-          const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-          d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
-          double tend;
-          bool hit;
-          ray_box(P.pos, d, P.ext, t0, tend, hit);
-          rgb0 = rgb1 = rgb2 = 0.f;
-          trans = 1.f;
-          depth = 0.f;
-          if (!hit) {
-            finish(p);
-          } else {
-            ++hitc;
-            const double L = tend - t0;
-            n = (int)ceil((L - 1e-12) / P.step);
-            if (n < 1) n = 1;
-            last_dt = (float)(L - (double)(n - 1) * P.step);
-            ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
-            ez = (float)(P.pos[2] + d[2] * t0);
-            dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-            s = 0;
-            in_shadow = false;
-            pix = p;
-          }
-        }
-      }
-    }
-    if (!__any_sync(0xffffffffu, pix >= 0)) break;
-    if (pix < 0) continue;
-
-    // ---- one sample ----
-    float px, py, pz, dt, mid;
-    const bool last = s == n - 1;
-    if (in_shadow) {
-      dt = fminf(step_sh, stend - st);
-      mid = st + 0.5f * dt;
-      px = spx + sdx * mid; py = spy + sdy * mid; pz = spz + sdz * mid;
-    } else {
-      dt = last ? last_dt : stepf;
-      mid = (float)s * stepf + 0.5f * dt;
-      px = ex + dx * mid; py = ey + dy * mid; pz = ez + dz * mid;
-    }
-    float c[4];
-    tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
-    float shade = -1.f;  // >= 0: composite the pending main sample with this shade
-    if (in_shadow) {
-      ++n_shadow;
-      const float keep = dt == step_sh ? keep_cls(1.f - c[3], F.cls_sh, F.e_sh) : keep_partial(1.f - c[3], dt * F.inv_ref);
-      strans = strans * (1.f - (1.f - keep));
-      st = st + dt;
-      if (!(st < stend) || !(strans > mt)) {
-        shade = amb + (1.f - amb) * strans;
-        in_shadow = false;
-      }
-    } else {
-      ++n_main;
-      const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
-      pc0 = c[0]; pc1 = c[1]; pc2 = c[2];
-      pa = 1.f - keep;
-      shade = 1.f;
-      if (lit && pa > 0.f) {
-        // shadow ray from this sample toward the light (renderer.py:109-147)
-        float dir[3], inv[3], dist = INFINITY;
-        if (P.light_kind == FV_LIGHT_DIRECTIONAL) {
-          dir[0] = F.ld[0]; dir[1] = F.ld[1]; dir[2] = F.ld[2];
-          inv[0] = F.ld_inv[0]; inv[1] = F.ld_inv[1]; inv[2] = F.ld_inv[2];
-        } else {
-          const float lx = F.lpos[0] - px, ly = F.lpos[1] - py, lz = F.lpos[2] - pz;
-          dist = sqrtf(lx * lx + ly * ly + lz * lz);
-          const float mm = fmaxf(dist, 1e-30f);
-          dir[0] = lx / mm; dir[1] = ly / mm; dir[2] = lz / mm;
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            float sd = dir[a];
-            if (fabsf(sd) < 1e-30f) sd = sd < 0.f ? -1e-30f : 1e-30f;
-            inv[a] = 1.f / sd;
-          }
-        }
-        const float pp[3] = {px, py, pz};
-        float tmin = -INFINITY, tmax = INFINITY;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const float ta = (0.f - pp[a]) * inv[a], tb = (F.V.ext[a] - pp[a]) * inv[a];
-          tmin = fmaxf(tmin, fminf(ta, tb));
-          tmax = fminf(tmax, fmaxf(ta, tb));
-        }
-        const float ts0 = fmaxf(tmin, 0.f);
-        const float te = fminf(tmax, dist);
-        if (tmax > ts0 && te > ts0) {
-          in_shadow = true;
-          spx = px; spy = py; spz = pz;
-          sdx = dir[0]; sdy = dir[1]; sdz = dir[2];
-          st = ts0;
-          stend = te;
-          strans = 1.f;
-          shade = -1.f;
-        }
-      }
-    }
-    if (shade >= 0.f) {
-      const float contrib = trans * pa;
-      rgb0 += contrib * (pc0 * (shade * I0));
-      rgb1 += contrib * (pc1 * (shade * I1));
-      rgb2 += contrib * (pc2 * (shade * I2));
-      trans = trans * (1.f - pa);
-      const float acc = 1.f - trans;
-      const float mid_main = (float)s * stepf + 0.5f * (s == n - 1 ? last_dt : stepf);
-      if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid_main);
-      ++s;
-      if (s >= n || !(acc < early)) {
-        finish(pix);
-        pix = -1;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
-    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
-    n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
-    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
-  }
-  if (lane == 0 && nrays) {
-    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
-    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
-    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
-    atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Persistent per-lane-refill marcher (default fast tier).
-//
-// ncu on the one-ray-per-thread kernel: 12.7% achieved occupancy against 44% theoretical -- a
-// 128-thread block holds its slot until its slowest ray (thousands of shadow samples) is done,
-// and most of the 373k compacted rays miss the volume or stop early. Here a grid of
-// (SMs x resident blocks) warps loops over the compacted list: whenever a lane's ray finishes,
-// the lane takes the next ray index from a global counter (one warp-aggregated atomic per
-// refill), so warps stay full until the list drains. A loop iteration is one main sample plus
-// its inline shadow ray. Each ray is still marched start to finish by one lane in the
-// reference's order, so results equal the per-ray kernel's bit for bit.
-__global__ void __launch_bounds__(128) march_refill_kernel(FastParams F, unsigned int* ray_counter) {
-  const MarchParams& P = F.P;
-  __shared__ float lut[4 * 256];
-  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
-  __syncthreads();
-  const int k = P.k_dev ? *P.k_dev : P.k_max;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const bool lit = P.light_kind != FV_LIGHT_NONE;
-  const float amb = lit ? (float)P.ambient : 1.f;
-  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
-  const float early = (float)P.early, stepf = (float)P.step;
-  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
-  int pix = -1;
-  bool exhausted = false;
-  float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0.f;
-  int s = 0, n = 0;
-  double t0 = 0.0;
-  float rgb0 = 0, rgb1 = 0, rgb2 = 0, trans = 1.f, depth = 0.f;
-  const float bga = (float)P.bg[3];
-
-  while (true) {
-    while (true) {
-      const bool need = pix < 0 && !exhausted;
-      const unsigned m = __ballot_sync(0xffffffffu, need);
-      if (!m) break;
-      const int leader = __ffs(m) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(ray_counter, (unsigned)__popc(m));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (need) {
-        const int r = (int)(base + __popc(m & lt_mask));
-        if (r >= k) {
-          exhausted = true;
-        } else {
-          const int p = P.idx ? P.idx[r] : r;
-          ++nrays;
-          const int u = p % P.W, v = p / P.W;
-          const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
-          const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
-          double d[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
-          const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-          d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
-          double tend;
-          bool hit;
-          ray_box(P.pos, d, P.ext, t0, tend, hit);
-          rgb0 = rgb1 = rgb2 = 0.f;
-          trans = 1.f;
-          depth = 0.f;
-          if (hit) {
-            ++hitc;
-            const double L = tend - t0;
-            n = (int)ceil((L - 1e-12) / P.step);
-            if (n < 1) n = 1;
-            last_dt = (float)(L - (double)(n - 1) * P.step);
-            ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
-            ez = (float)(P.pos[2] + d[2] * t0);
-            dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-            s = 0;
-            pix = p;
-          } else {
-            pix = p;
-            n = 0;  // finished below without samples
-          }
-        }
-      }
-    }
-    if (!__any_sync(0xffffffffu, pix >= 0)) break;
-    if (pix >= 0) {
-      bool done = s >= n;
-      if (!done) {
-        const bool last = s == n - 1;
-        const float dt = last ? last_dt : stepf;
-        const float mid = (float)s * stepf + 0.5f * dt;
-        const float px = ex + dx * mid, py = ey + dy * mid, pz = ez + dz * mid;
-        float c[4];
-        tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
-        ++n_main;
-        const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
-        const float a_step = 1.f - keep;
-        float shade = 1.f;
-        if (lit && a_step > 0.f) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
-        const float contrib = trans * a_step;
-        rgb0 += contrib * (c[0] * (shade * I0));
-        rgb1 += contrib * (c[1] * (shade * I1));
-        rgb2 += contrib * (c[2] * (shade * I2));
-        trans = trans * (1.f - a_step);
-        const float acc = 1.f - trans;
-        if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid);
-        ++s;
-        done = s >= n || !(acc < early);
-      }
-      if (done) {
-        const float o0 = rgb0 + (trans * bga) * (float)P.bg[0], o1 = rgb1 + (trans * bga) * (float)P.bg[1],
-                    o2 = rgb2 + (trans * bga) * (float)P.bg[2], o3 = (1.f - trans) + trans * bga;
-        if (P.rgba) *reinterpret_cast<float4*>(P.rgba + (int64_t)pix * 4) = make_float4(o0, o1, o2, o3);
-        if (P.depth) P.depth[pix] = depth;
-        if (P.net_in) {
-          const int u = pix % P.W, v = pix / P.W;
-          __half2* hp = reinterpret_cast<__half2*>(P.net_in + ((int64_t)v * P.net_wp + u) * 8);
-          hp[0] = __floats2half2_rn(o0, o1);
-          hp[1] = __floats2half2_rn(o2, o3);
-        }
-        pix = -1;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
-    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
-    n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
-    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
-  }
-  if (lane == 0 && nrays) {
-    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
-    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
-    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
-    atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
 // Wavefront marcher (default fast tier): main rays, shadow rays and compositing as three passes.
 //
 // In _march the shade of a sample enters only the colour sum (renderer.py:181-182); opacity,
@@ -1076,10 +737,8 @@ struct WaveBufs {
   unsigned int* chunk_count;
   unsigned int* next;      // work counter of the shadow pass
   int4* ray;               // per compacted ray: (first chunk, record count, trans, depth) bits
-  unsigned chunk_perm;     // shadow pass chunk visiting order: 0 = in order, else a prime multiplier
   int* ord;                // nullable: chunk ids in shadow-pass visiting order (order_*_kernel)
   unsigned int* ord_count;
-  unsigned int* seg;       // kSegs per-segment counts / cursors
   int cap_a;               // > 0 (warp main pass): chunk r < cap_a is the FIRST chunk of ray r; later
                            // chunks come from pools at ids cap_a + counter (see march_wave_shadow_kernel)
   int chunk_pool;          // warp main pass: chunks claimed per counter round trip
@@ -1104,186 +763,17 @@ __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float
   }
 }
 
-// (128, 4): register cap for 4 resident blocks per SM -- the pass is load-latency bound, so the
-// extra warps beat the few spilled bytes (A/B on B200: -8% time versus 152 registers / 3 blocks).
-template <int kMainU>
-__global__ void __launch_bounds__(128, 4) march_wave_main_kernel(FastParams F, WaveBufs B, unsigned int* ray_counter) {
-  const MarchParams& P = F.P;
-  __shared__ float lut[4 * 256];
-  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
-  __syncthreads();
-  const int k = P.k_dev ? *P.k_dev : P.k_max;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const bool lit = P.light_kind != FV_LIGHT_NONE;
-  const float amb = lit ? (float)P.ambient : 1.f;
-  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
-  const float early = (float)P.early, stepf = (float)P.step;
-  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
-  int pix = -1, ray = -1;
-  bool exhausted = false;
-  float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0.f;
-  int s = 0, n = 0, m = 0;
-  bool fused = false;           // inline-shadow fallback for this ray
-  int first = -1, chunk = -1, fill = 0;
-  double t0 = 0.0;
-  float rgb0 = 0, rgb1 = 0, rgb2 = 0, trans = 1.f, depth = 0.f;
-
-  while (true) {
-    while (true) {
-      const bool need = pix < 0 && !exhausted;
-      const unsigned msk = __ballot_sync(0xffffffffu, need);
-      if (!msk) break;
-      const int leader = __ffs(msk) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(ray_counter, (unsigned)__popc(msk));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (need) {
-        const int r = (int)(base + __popc(msk & lt_mask));
-        if (r >= k) {
-          exhausted = true;
-        } else {
-          const int p = P.idx ? P.idx[r] : r;
-          ++nrays;
-          const int u = p % P.W, v = p / P.W;
-          const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
-          const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
-          double d[3];
-#pragma unroll
-          for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
-          const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-          d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
-          double tend;
-          bool hit;
-          ray_box(P.pos, d, P.ext, t0, tend, hit);
-          rgb0 = rgb1 = rgb2 = 0.f;
-          trans = 1.f;
-          depth = 0.f;
-          if (!hit) {
-            write_pixel(P, p, 0.f, 0.f, 0.f, 1.f, 0.f);
-            B.ray[r] = make_int4(-1, 0, 0, 0);
-          } else {
-            ++hitc;
-            const double L = tend - t0;
-            n = (int)ceil((L - 1e-12) / P.step);
-            if (n < 1) n = 1;
-            last_dt = (float)(L - (double)(n - 1) * P.step);
-            ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
-            ez = (float)(P.pos[2] + d[2] * t0);
-            dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-            s = 0; m = 0;
-            fused = false;
-            first = chunk = -1;
-            fill = kChunk;
-            pix = p;
-            ray = r;
-          }
-        }
-      }
-    }
-    if (!__any_sync(0xffffffffu, pix >= 0)) break;
-    if (pix < 0) continue;
-
-    // Up to kMainU samples per iteration: their positions do not depend on the data, so all
-    // loads are issued before the first sample is consumed (the longest main rays are ~1000
-    // samples; a serial chain of L2 round trips would set the kernel's tail).
-    TriFetch f[kMainU];
-#pragma unroll
-    for (int u = 0; u < kMainU; ++u) {
-      const int si = s + u;
-      const float dt = si == n - 1 ? last_dt : stepf;
-      const float mid = (float)si * stepf + 0.5f * dt;
-      f[u] = tri_issue(F.V, ex + dx * mid, ey + dy * mid, ez + dz * mid);
-    }
-#pragma unroll
-    for (int u = 0; u < kMainU; ++u) {
-      const bool last = s == n - 1;
-      const float dt = last ? last_dt : stepf;
-      const float mid = (float)s * stepf + 0.5f * dt;
-      float c[4];
-      tf_apply<float>(lut, P.K, tri_finish(f[u]), c);
-      const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
-      const float a_step = 1.f - keep;
-      const bool needs_shadow = lit && a_step > 0.f;
-      bool restart = false;
-      if (!fused) ++n_main;
-      if (!lit) {
-        const float contrib = trans * a_step;
-        rgb0 += contrib * (c[0] * I0);
-        rgb1 += contrib * (c[1] * I1);
-        rgb2 += contrib * (c[2] * I2);
-      } else if (fused) {
-        float shade = 1.f;
-        if (needs_shadow)
-          shade = amb + (1.f - amb) * shadow_fast(F, lut, ex + dx * mid, ey + dy * mid, ez + dz * mid, n_shadow);
-        const float contrib = trans * a_step;
-        rgb0 += contrib * (c[0] * (shade * I0));
-        rgb1 += contrib * (c[1] * (shade * I1));
-        rgb2 += contrib * (c[2] * (shade * I2));
-      } else if (needs_shadow) {
-        if (fill == kChunk) {
-          const int nc = (int)atomicAdd(B.chunk_count, 1u);
-          if (nc >= B.n_chunks_cap) {
-            restart = true;  // buffer full: discard this ray's records, march it fused
-          } else {
-            if (chunk >= 0) { B.chunk_fill[chunk] = kChunk; B.chunk_next[chunk] = nc; }
-            else first = nc;
-            chunk = nc;
-            fill = 0;
-          }
-        }
-        if (!restart) {
-          const int slot = chunk * kChunk + fill;
-          B.rec0[slot] = make_float4(ex + dx * mid, ey + dy * mid, ez + dz * mid, 0.f);
-          B.rec1[slot] = make_float4(c[0], c[1], c[2], trans * a_step);
-          ++fill;
-          ++m;
-        }
-      }
-      if (restart) {
-        for (int cc = first; cc >= 0; cc = (cc == chunk) ? -1 : B.chunk_next[cc]) B.chunk_fill[cc] = 0;
-        fused = true;
-        s = 0; m = 0;
-        first = chunk = -1;
-        trans = 1.f; depth = 0.f;
-        rgb0 = rgb1 = rgb2 = 0.f;
-        break;
-      }
-      trans = trans * (1.f - a_step);
-      const float acc = 1.f - trans;
-      if (depth == 0.f && acc >= 0.5f) depth = (float)(t0 + (double)mid);
-      ++s;
-      if (s >= n || !(acc < early)) {
-        if (lit && !fused && m > 0) {
-          B.chunk_fill[chunk] = fill;
-          B.chunk_next[chunk] = -1;
-          B.ray[ray] = make_int4(first, m, __float_as_int(trans), __float_as_int(depth));
-        } else {
-          write_pixel(P, pix, rgb0, rgb1, rgb2, trans, depth);
-          B.ray[ray] = make_int4(-1, 0, 0, 0);
-        }
-        pix = -1;
-        break;
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
-    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
-    n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
-    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
-  }
-  if (lane == 0 && nrays) {
-    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
-    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
-    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
-    atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
-  }
-}
-
 // March the hitting rays of a claimed set (one ray's setup per lane, hit_mask = lanes holding a
-// hitting ray) one at a time, the whole warp on each (see march_wave_main_warp_kernel).
+// hitting ray) one at a time, the whole warp on each. The samples of a primary ray do not depend on
+// the data, so lane l evaluates samples s0 + u*32 + l (all texture loads issued first); the
+// transmittance in front of each sample is an inclusive product scan over the lanes, and early
+// termination cuts the block after the first sample whose accumulated opacity reaches
+// early_term_alpha -- the samples the sequential loop evaluates, with the products associated
+// differently (fp32 rounding). Records of the lit samples are compacted into the ray's 32-slot chunks
+// with ballot/popc, so all chunks but the last are full (the composite pass relies on it). The
+// first chunk of ray r is chunk r (first_list_kernel); later ones come from per-warp pools of
+// chunk_pool chunks, the next pool claimed when the current one opens. A ray that finds the record
+// buffer full releases its chunks and is marched again with inline shadow rays (fused).
 template <int kU, bool TEX>
 __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& B, const float* lut,
                                            unsigned hit_mask, int n, float last_dt, float ex, float ey,
@@ -1461,105 +951,6 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
   }
 }
 
-// ---- main pass, warp per ray -------------------------------------------------------------------
-// The samples of a primary ray do not depend on the data, so a warp marches one ray 32 x kU samples
-// at a time: lane l evaluates samples s0 + u*32 + l (all loads issued first), the transmittance in
-// front of each sample is an inclusive product scan over the lanes, and early termination cuts the
-// block after the first sample whose accumulated opacity reaches early_term_alpha -- the samples the
-// sequential loop would have evaluated, with the products associated differently (fp32 rounding).
-// Records of the lit samples are compacted into the ray's 32-slot chunks with ballot/popc, so all
-// chunks but the last are full (what the shadow and composite passes expect). Rays are claimed 32 at a
-// time; their fp64 setup runs one ray per lane, then the warp walks the hitting rays one by one.
-// (The per-lane state machine it replaces left ~half the lanes idle: rays are 0..~1000 samples long.)
-template <int kU, bool TEX, int MINB = 5>
-__global__ void __launch_bounds__(128, MINB) march_wave_main_warp_kernel(FastParams F, WaveBufs B,
-                                                                         unsigned int* ray_counter) {
-  const MarchParams& P = F.P;
-  __shared__ float lut[4 * 256];
-  for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
-  __syncthreads();
-  const int k = P.k_dev ? *P.k_dev : P.k_max;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const bool lit = P.light_kind != FV_LIGHT_NONE;
-  const float amb = lit ? (float)P.ambient : 1.f;
-  const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
-  const float early = (float)P.early, stepf = (float)P.step;
-  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nrays = 0;
-  // Chunk pool: chunks are claimed kPool at a time and the next pool is claimed (lane 0) when the
-  // current one is opened, so the contended counter's round trip is off the critical path (ncu:
-  // one atomic per chunk was a third of the stalls). Unused pool chunks get fill 0 at exit.
-  const int kPool = B.chunk_pool;
-  int pool_cur = 0, pool_end = 0;  // warp-uniform
-  unsigned int pool_pref = 0;      // lane 0: base of the prefetched pool
-  if (lit && lane == 0) pool_pref = atomicAdd(B.chunk_count, (unsigned)kPool);
-  while (true) {
-    unsigned int base = 0;
-    if (lane == 0) base = atomicAdd(ray_counter, (unsigned)B.claim);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if ((int)base >= k) break;
-    // ---- per-lane ray setup (fp64, as the reference) ----
-    const int r = (int)base + lane;
-    bool hit = false;
-    int pix = 0, n = 0;
-    float ex = 0, ey = 0, ez = 0, dx = 0, dy = 0, dz = 0, last_dt = 0;
-    double t0 = 0.0;
-    if (r < k && lane < B.claim) {
-      pix = P.idx ? P.idx[r] : r;
-      ++nrays;
-      const int u = pix % P.W, v = pix / P.W;
-      const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
-      const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
-      double d[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
-      const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-      d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
-      double tend;
-      ray_box(P.pos, d, P.ext, t0, tend, hit);
-      if (!hit) {
-        write_pixel(P, pix, 0.f, 0.f, 0.f, 1.f, 0.f);
-        B.ray[r] = make_int4(-1, 0, 0, 0);
-        if (r < B.cap_a) B.chunk_fill[r] = 0;
-      } else {
-        ++hitc;
-        const double L = tend - t0;
-        n = (int)ceil((L - 1e-12) / P.step);
-        if (n < 1) n = 1;
-        last_dt = (float)(L - (double)(n - 1) * P.step);
-        ex = (float)(P.pos[0] + d[0] * t0); ey = (float)(P.pos[1] + d[1] * t0);
-        ez = (float)(P.pos[2] + d[2] * t0);
-        dx = (float)d[0]; dy = (float)d[1]; dz = (float)d[2];
-      }
-    }
-    unsigned hit_mask = __ballot_sync(0xffffffffu, hit);
-    march_hits<kU, TEX>(F, B, lut, hit_mask, n, last_dt, ex, ey, ez, dx, dy, dz, t0, pix, (int)base + lane,
-                        pool_cur, pool_end, pool_pref, n_main, n_shadow);
-  }
-  // release the unused chunks of the open pool and of the prefetched one (the shadow pass skips
-  // chunks whose fill is 0)
-  if (lit) {
-    const int pref = B.cap_a + (int)__shfl_sync(0xffffffffu, pool_pref, 0);
-    for (int c = pool_cur + lane; c < pool_end; c += 32)
-      if (c < B.n_chunks_cap) B.chunk_fill[c] = 0;
-    for (int c = lane; c < kPool; c += 32)
-      if (pref + c < B.n_chunks_cap) B.chunk_fill[pref + c] = 0;
-  }
-  // n_main is warp-uniform (popc of ballots); nrays, hitc and n_shadow (inline shadows) are per lane
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nrays += __shfl_xor_sync(0xffffffffu, nrays, o);
-    hitc += __shfl_xor_sync(0xffffffffu, hitc, o);
-    n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
-  }
-  if (lane == 0 && nrays) {
-    atomicAdd(&P.counters->rays, (unsigned long long)nrays);
-    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
-    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
-    if (n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
-  }
-}
-
 // ---- ray setup pass + main pass over the list of hitting rays ------------------------------------
 // With the setup inside the main pass, a warp claims 32 compacted rays, sets them up one per lane and
 // then marches the ~10 that hit the volume one by one: per-warp work comes in lumps of 32 rays, and
@@ -1690,90 +1081,6 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastPar
   }
 }
 
-// Shadow-pass visiting order: chunk j of every ray, rays in (roughly) image order, then chunk j+1
-// ... ("depth-major"). Chunk j of neighbouring pixels holds samples at similar depth, so their light
-// rays start close together and overlap in the volume -- that is what makes the L1/L2 hit rates of
-// the shadow pass (A/B: allocation order of the warp-per-ray main pass 488 us, this order ~440).
-// Three small passes: count chunks per segment, scan the counts, scatter chunk ids.
-constexpr int kSegs = 64;  // segments >= kSegs-1 share the last bucket
-
-__global__ void __launch_bounds__(256) order_count_kernel(FastParams F, WaveBufs B) {
-  const MarchParams& P = F.P;
-  __shared__ unsigned cnt[kSegs];
-  for (int i = threadIdx.x; i < kSegs; i += blockDim.x) cnt[i] = 0;
-  __syncthreads();
-  const int k = P.k_dev ? *P.k_dev : P.k_max;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k; r += gridDim.x * blockDim.x) {
-    const int4 v = B.ray[r];
-    if (v.x < 0) continue;
-    const int nch = (v.y + kChunk - 1) / kChunk;
-    for (int j = 0; j < min(nch, kSegs - 1); ++j) atomicAdd(&cnt[j], 1u);
-    if (nch > kSegs - 1) atomicAdd(&cnt[kSegs - 1], (unsigned)(nch - (kSegs - 1)));
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kSegs; i += blockDim.x)
-    if (cnt[i]) atomicAdd(&B.seg[i], cnt[i]);
-}
-
-__global__ void order_scan_kernel(WaveBufs B) {  // one warp: seg[j] <- exclusive prefix; total -> ord_count
-  const int lane = threadIdx.x;
-  unsigned a = B.seg[2 * lane], b = B.seg[2 * lane + 1];
-  unsigned incl = a + b;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const unsigned excl = incl - (a + b);
-  B.seg[2 * lane] = excl;
-  B.seg[2 * lane + 1] = excl + a;
-  if (lane == 31) *B.ord_count = incl;
-}
-
-// One atomic per block and segment (per-warp atomics on the few hot segment cursors cost 16 us).
-__global__ void __launch_bounds__(256) order_scatter_kernel(FastParams F, WaveBufs B) {
-  const MarchParams& P = F.P;
-  __shared__ int s_cnt[8], s_pre[8], s_max[8];
-  __shared__ unsigned s_base;
-  const int k = P.k_dev ? *P.k_dev : P.k_max;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt_mask = (1u << lane) - 1u;
-  for (int r0 = blockIdx.x * blockDim.x; r0 < k; r0 += gridDim.x * blockDim.x) {
-    const int r = r0 + threadIdx.x;
-    int4 v = make_int4(-1, 0, 0, 0);
-    if (r < k) v = B.ray[r];
-    const int nch = v.x >= 0 ? (v.y + kChunk - 1) / kChunk : 0;
-    int wmax = nch;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
-    if (lane == 0) s_max[warp] = wmax;
-    __syncthreads();
-    int bmax = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) bmax = max(bmax, s_max[w]);
-    int c = v.x;
-    for (int j = 0; j < bmax; ++j) {
-      const bool has = j < nch;
-      const unsigned m = __ballot_sync(0xffffffffu, has);
-      if (lane == 0) s_cnt[warp] = __popc(m);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int t = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) { s_pre[w] = t; t += s_cnt[w]; }
-        s_base = t ? atomicAdd(&B.seg[min(j, kSegs - 1)], (unsigned)t) : 0u;
-      }
-      __syncthreads();
-      if (has) {
-        const unsigned pos = s_base + s_pre[warp] + __popc(m & lt_mask);
-        if (pos < (unsigned)B.n_chunks_cap) B.ord[pos] = c;
-        c = B.chunk_next[c];
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // With cap_a: list the rays whose first chunk (id = ray index) holds records, in ray order (one
 // atomic per block; blocks cover consecutive rays) -- the shadow pass visits these first, then the
 // pooled later chunks. No chain walks, so this is a few microseconds.
@@ -1812,9 +1119,9 @@ __global__ void __launch_bounds__(128, 8) march_wave_shadow_kernel(FastParams F,
     lut2[i] = make_float2(P.lut[4 * i + 3], P.lut[4 * (i + 1) + 3] - P.lut[4 * i + 3]);
   __syncthreads();
   // chunks to visit: with cap_a, first the listed non-empty first chunks (ord) then the pooled ones
-  const int n_a = B.cap_a > 0 ? (int)*B.ord_count : 0;
-  const int n_b = B.cap_a > 0 ? (int)min(*B.chunk_count, (unsigned)(B.n_chunks_cap - B.cap_a))
-                              : (int)min(B.ord ? *B.ord_count : *B.chunk_count, (unsigned)B.n_chunks_cap);
+  // slots: first the listed non-empty first chunks (ord), then the pooled chunks
+  const int n_a = (int)*B.ord_count;
+  const int n_b = (int)min(*B.chunk_count, (unsigned)(B.n_chunks_cap - B.cap_a));
   const int nslots = (n_a + n_b) * kChunk;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -1837,14 +1144,9 @@ __global__ void __launch_bounds__(128, 8) march_wave_shadow_kernel(FastParams F,
         if (i >= nslots) {
           exhausted = true;
         } else {
-          if (B.cap_a > 0) {
+          {
             const int q = i / kChunk;
             i = (q < n_a ? B.ord[q] : B.cap_a + q - n_a) * kChunk + (i % kChunk);
-          } else if (B.ord) {
-            i = B.ord[i / kChunk] * kChunk + (i % kChunk);
-          } else if (B.chunk_perm) {  // visit chunks in a scattered order (bijection: perm is prime, > nchunks)
-            const unsigned nch = (unsigned)(nslots / kChunk);
-            i = (int)(((unsigned long long)(i / kChunk) * B.chunk_perm % nch) * kChunk + (i % kChunk));
           }
           if ((i % kChunk) < B.chunk_fill[i / kChunk]) my = i;
         }
@@ -1900,9 +1202,9 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
     lut_om[i] = i < P.K - 1 ? make_float2(1.f - P.lut[4 * i + 3], -(P.lut[4 * (i + 1) + 3] - P.lut[4 * i + 3]))
                             : make_float2(1.f - P.lut[4 * i + 3], 0.f);
   __syncthreads();
-  const int n_a = B.cap_a > 0 ? (int)*B.ord_count : 0;
-  const int n_b = B.cap_a > 0 ? (int)min(*B.chunk_count, (unsigned)(B.n_chunks_cap - B.cap_a))
-                              : (int)min(B.ord ? *B.ord_count : *B.chunk_count, (unsigned)B.n_chunks_cap);
+  // slots: first the listed non-empty first chunks (ord), then the pooled chunks
+  const int n_a = (int)*B.ord_count;
+  const int n_b = (int)min(*B.chunk_count, (unsigned)(B.n_chunks_cap - B.cap_a));
   const int nslots = (n_a + n_b) * kChunk;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -1942,11 +1244,9 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
         if (i >= nslots) {
           exhausted = true;
         } else {
-          if (B.cap_a > 0) {
+          {
             const int q = i / kChunk;
             i = (q < n_a ? B.ord[q] : B.cap_a + q - n_a) * kChunk + (i % kChunk);
-          } else if (B.ord) {
-            i = B.ord[i / kChunk] * kChunk + (i % kChunk);
           }
           if ((i % kChunk) < B.chunk_fill[i / kChunk]) {
             const float4 r0 = B.rec0[i];
@@ -2179,46 +1479,18 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
 }
 
 // wavefront passes, instantiated for quads from the bricked buffer (TEX = false) or the texture
-template <int MINB, bool TEX>
-int launch_main_warp_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_warp_kernel<2, TEX, MINB>, threads, 0));
-    per_sm = std::max(per_sm, 1);
-  }
-  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_warp_kernel<2, TEX, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(
-                                      F, B, &ctx->counters->ray_next));
-  return 0;
-}
-
-// FV_MAIN_MINB: resident-block target of the register allocation (A/B runs)
-template <int MINB, bool TEX>
-int launch_main_list_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_list_kernel<2, TEX, MINB>, threads, 0));
-    per_sm = std::max(per_sm, 1);
-  }
-  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<2, TEX, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B));
-  return 0;
-}
-
-// FV_MAIN_MINB: resident-block target of the register allocation (A/B runs); FV_MAIN_LIST=0: the
-// setup runs inside the main pass (32 rays per claim)
 template <bool TEX>
-int launch_main_warp(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
-  static const bool use_list = !(getenv("FV_MAIN_LIST") && atoi(getenv("FV_MAIN_LIST")) == 0);
-  if (use_list && B.hits) {
-    const int k_max = F.P.k_max;
-    const int blocks = std::max(1, std::min((k_max + 255) / 256, ctx->num_sms * 8));
-    FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<<<blocks, 256, 0, ctx->stream>>>(F, B));
-    ctx->launches += 1;
-    return launch_main_list_t<5, TEX>(ctx, F, B, threads);
+int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
+  const int blocks = std::max(1, std::min((F.P.k_max + 255) / 256, ctx->num_sms * 8));
+  FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<<<blocks, 256, 0, ctx->stream>>>(F, B));
+  ctx->launches += 1;
+  static int per_sm = 0;
+  if (!per_sm) {
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_list_kernel<2, TEX, 5>, threads, 0));
+    per_sm = std::max(per_sm, 1);
   }
-  static const int minb = getenv("FV_MAIN_MINB") ? atoi(getenv("FV_MAIN_MINB")) : 5;
-  if (minb == 6) return launch_main_warp_t<6, TEX>(ctx, F, B, threads);
-  if (minb == 8) return launch_main_warp_t<8, TEX>(ctx, F, B, threads);
-  return launch_main_warp_t<5, TEX>(ctx, F, B, threads);
+  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<2, TEX, 5><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B));
+  return 0;
 }
 
 template <bool TEX>
@@ -2330,15 +1602,10 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_kernel<double><<<blocks, threads, 0, ctx->stream>>>(P));
   } else {
     fv_volume* mv = const_cast<fv_volume*>(vol);  // the quad copy is a cache of the grid
-    // FV_MARCH_KERNEL=wave (default) | refill | ray | persist -- variants kept for A/B runs
-    static int env_variant = -1;
-    if (env_variant < 0) {
-      const char* e = getenv("FV_MARCH_KERNEL");
-      env_variant = (e && strcmp(e, "persist") == 0) ? 1 : (e && strcmp(e, "ray") == 0) ? 2
-                  : (e && strcmp(e, "refill") == 0) ? 0 : 3;
-    }
-    // the naive renderer forces the thread-per-lane kernel (idle lanes are its point)
-    const int variant = force_variant >= 0 ? force_variant : env_variant;
+    // variant 3: the wavefront passes; 2: one thread per ray (march_fast_kernel), which the naive
+    // renderer forces (its idle lanes are the point) and FV_MARCH_KERNEL=ray selects everywhere
+    static const bool env_ray = getenv("FV_MARCH_KERNEL") && strcmp(getenv("FV_MARCH_KERNEL"), "ray") == 0;
+    const int variant = force_variant >= 0 ? force_variant : env_ray ? 2 : 3;
     // Quads come from a point-sampled 3D texture (block-linear layout, hardware clamp addressing:
     // A/B -43 us per C3 frame versus the bricked buffer, which the thread-per-ray variants and
     // FV_VOL_TEX=0 still use).
@@ -2405,96 +1672,44 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.chunk_count = &ctx->counters->wave_rec;
       B.next = &ctx->counters->wave_next;
       B.ray = reinterpret_cast<int4*>(ctx->wave_ray);
-      static const unsigned chunk_perm = getenv("FV_SHADOW_PERM") ? (unsigned)atol(getenv("FV_SHADOW_PERM")) : 0u;
-      B.chunk_perm = chunk_perm;
       static const int chunk_pool = getenv("FV_CHUNK_POOL") ? std::max(1, atoi(getenv("FV_CHUNK_POOL"))) : 8;
       B.chunk_pool = chunk_pool;
-      static const bool use_list = !(getenv("FV_MAIN_LIST") && atoi(getenv("FV_MAIN_LIST")) == 0);
-      static const int claim = getenv("FV_MAIN_CLAIM") ? std::min(32, std::max(1, atoi(getenv("FV_MAIN_CLAIM"))))
-                                                       : (use_list ? 2 : 32);
+      static const int claim = getenv("FV_MAIN_CLAIM") ? std::min(32, std::max(1, atoi(getenv("FV_MAIN_CLAIM")))) : 2;
       B.claim = claim;
-      B.hits = nullptr;
+      if (k_max > ctx->wave_hits_cap) {
+        if (ctx->wave_hits) cudaFree(ctx->wave_hits);
+        ctx->wave_hits = nullptr;
+        FV_CUDA(cudaMalloc(&ctx->wave_hits, 3 * sizeof(float4) * (size_t)k_max));
+        ctx->wave_hits_cap = k_max;
+      }
+      B.hits = reinterpret_cast<float4*>(ctx->wave_hits);
       B.hit_count = &ctx->counters->hit_count;
       B.hit_next = &ctx->counters->hit_next;
-      static const bool warp_main = !(getenv("FV_MAIN_WARP") && atoi(getenv("FV_MAIN_WARP")) == 0);
-      if (use_list && warp_main) {
-        if (k_max > ctx->wave_hits_cap) {
-          if (ctx->wave_hits) cudaFree(ctx->wave_hits);
-          ctx->wave_hits = nullptr;
-          FV_CUDA(cudaMalloc(&ctx->wave_hits, 3 * sizeof(float4) * (size_t)k_max));
-          ctx->wave_hits_cap = k_max;
-        }
-        B.hits = reinterpret_cast<float4*>(ctx->wave_hits);
-      }
-      static const bool shadow_order = getenv("FV_SHADOW_ORDER") && atoi(getenv("FV_SHADOW_ORDER")) == 1;
-      B.ord = shadow_order ? B.chunk_fill + ctx->wave_cap / kChunk : nullptr;
+      // half of the chunk space holds first chunks at id = ray index (k_max may exceed it: later
+      // rays then take pooled first chunks); ord lists the non-empty ones in ray order
+      B.cap_a = B.n_chunks_cap / 2;
+      B.ord = B.chunk_fill + ctx->wave_cap / kChunk;
       B.ord_count = &ctx->counters->wave_ord;
-      B.seg = reinterpret_cast<unsigned int*>(B.chunk_fill + 2 * (ctx->wave_cap / kChunk));
-      static int main_u = 0, per_sm_main = 0;
-      if (!per_sm_main) {
-        const char* e = getenv("FV_MAIN_U");  // main-sample prefetch depth (A/B runs): 4 or 8
-        main_u = (e && atoi(e) == 8) ? 8 : 4;
-        if (main_u == 8)
-          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<8>, threads, 0));
-        else
-          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_main, march_wave_main_kernel<4>, threads, 0));
-        per_sm_main = std::max(per_sm_main, 1);
-      }
       // ray_next, wave_rec, wave_next, wave_ord, hit_count, hit_next are consecutive counters
       FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 6 * sizeof(unsigned int), ctx->stream));
-      const int mgrid = std::min(blocks, ctx->num_sms * per_sm_main);
-      static const int main_warp = getenv("FV_MAIN_WARP") ? atoi(getenv("FV_MAIN_WARP")) : 2;  // 0: per-lane rays
-      // warp main pass: half the chunk space holds first chunks at id = ray index (k_max may exceed it:
-      // later rays then take pooled first chunks)
-      static const bool direct_first = !(getenv("FV_FIRST_DIRECT") && atoi(getenv("FV_FIRST_DIRECT")) == 0);
-      B.cap_a = (main_warp && direct_first) ? B.n_chunks_cap / 2 : 0;
-      if (B.cap_a > 0) B.ord = B.chunk_fill + ctx->wave_cap / kChunk;  // the first-chunk list
-      if (main_warp) {
-        rc = F.V.tex ? launch_main_warp<true>(ctx, F, B, threads) : launch_main_warp<false>(ctx, F, B, threads);
-        if (rc) return rc;
-      }
-      else if (main_u == 8)
-        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<8><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
-      else
-        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_kernel<4><<<mgrid, threads, 0, ctx->stream>>>(F, B, &ctx->counters->ray_next));
+      rc = F.V.tex ? launch_main<true>(ctx, F, B, threads) : launch_main<false>(ctx, F, B, threads);
+      if (rc) return rc;
       if (P.light_kind != FV_LIGHT_NONE) {
-        if (B.cap_a > 0) {
-          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, first_list_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
-          ctx->launches += 1;
-        } else if (B.ord) {
-          FV_CUDA(cudaMemsetAsync(B.seg, 0, kSegs * sizeof(unsigned int), ctx->stream));
-          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_count_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
-          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_scan_kernel<<<1, 32, 0, ctx->stream>>>(B));
-          FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, order_scatter_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
-          ctx->launches += 3;
-        }
+        FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, first_list_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
+        ctx->launches += 1;
+        // directional lights on the texture path: the partial-refill pass (FV_SHADOW_V=1: the
+        // all-lane-refill pass, which point lights and the bricked path use)
         static const int shadow_v = getenv("FV_SHADOW_V") ? atoi(getenv("FV_SHADOW_V")) : 2;
         if (F.V.tex && P.light_kind == FV_LIGHT_DIRECTIONAL && shadow_v == 2)
           rc = launch_shadow_dir(ctx, F, B, threads);
         else
           rc = F.V.tex ? launch_shadow<true>(ctx, F, B, threads) : launch_shadow<false>(ctx, F, B, threads);
         if (rc) return rc;
-        static const int comp_blocks = getenv("FV_COMP_BLOCKS") ? atoi(getenv("FV_COMP_BLOCKS")) : 16;
-        FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * comp_blocks, threads, 0, ctx->stream>>>(F, B));
+        FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;
       }
-    } else if (variant == 2) {
-      FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F));
     } else {
-      static int per_sm[2] = {0, 0};
-      if (!per_sm[variant]) {
-        if (variant == 1)
-          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[1], march_persist_kernel, threads, 0));
-        else
-          FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[0], march_refill_kernel, threads, 0));
-        if (per_sm[variant] < 1) per_sm[variant] = 1;
-      }
-      const int pgrid = std::min(blocks, ctx->num_sms * per_sm[variant]);
-      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, sizeof(unsigned int), ctx->stream));
-      if (variant == 1)
-        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_persist_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next));
-      else
-        FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_refill_kernel<<<pgrid, threads, 0, ctx->stream>>>(F, &ctx->counters->ray_next));
+      FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F));
     }
   }
   FV_CHECK_LAUNCH("march_kernel");
