@@ -61,8 +61,6 @@ struct ConvArgs {
   int tiles_x, tiles_y;
   double flops;        // host-side: algorithmic FLOPs of the launch (kernel timing)
   unsigned long long* prof;  // nullable (FV_CONV_PROF=1): per-CTA wait-cycle counters, kProfSlots each
-  int mma_test;              // FV_CONV_MMA_TEST timing probe (0 = off)
-  int dx_outer;              // row-fused MMA order (FV_CONV_DXOUTER, A/B)
 };
 constexpr int kProfSlots = 6;  // producer empty-wait, MMA full-wait, MMA tempty-wait, epilogue tfull-wait, MMA total, tiles
 
@@ -299,32 +297,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
                                              (FUSED && !a.center_only ? 3 : 1) * N * 16, 128);
         (void)nk;  // one 16-channel MMA K-step per stage
         const bool leader = sm100::elect_one();
-        if (a.mma_test && leader) {
-          // timing probe (FV_CONV_MMA_TEST, results are garbage): the same MMA work per stage
-          // (128 x 2304 x 16) as 9 x N256, 18 x N128 or 36 x N64 dispatches
-          const uint64_t bt = sm100::smem_desc(sm100::smem_u32(sB + (BRES ? ks : st) * C::kBBytes), 16 * 16, 128);
-          if (a.mma_test == 1) {
-#pragma unroll
-            for (int i = 0; i < 9; ++i)
-              sm100::mma_f16(d_base, a0 + (uint64_t)((i * 16) >> 4), bt, sm100::idesc_f16(128, 256), 1u);
-          } else if (a.mma_test == 2) {
-#pragma unroll
-            for (int i = 0; i < 18; ++i)
-              sm100::mma_f16(d_base + (i & 1) * 128, a0 + (uint64_t)((i * 16) >> 4), bt, sm100::idesc_f16(128, 128), 1u);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 36; ++i)
-              sm100::mma_f16(d_base + (i & 3) * 64, a0 + (uint64_t)((i * 16) >> 4), bt, sm100::idesc_f16(128, 64), 1u);
-          }
-        } else if (!a.mma_test && leader) {
-          if (a.center_only)
+        // (the dispatch-cost probe of round 1 -- the same MMA work per stage as 9 x N256, 18 x N128 or
+        // 36 x N64 dispatches: 1054 / 1398 / 2085 cycles -- is summarised in profiles/r01_summary.md)
+        if (leader) {
+          if (CO || a.center_only)
             issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
+          else if constexpr (FUSED)
+            issue_stage_rows<R, N, true, kPairs>(a0, b0, d_base, ks == 0, bar_pair, (acc_round & 1) ^ 1);
           else
-            FUSED ? (a.dx_outer ? issue_stage_rows<R, N, true, kPairs>(a0, b0, d_base, ks == 0, bar_pair,
-                                                                       (acc_round & 1) ^ 1)
-                                : issue_stage_rows<R, N, false, kPairs>(a0, b0, d_base, ks == 0, bar_pair,
-                                                                        (acc_round & 1) ^ 1))
-                  : issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
+            issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
         }
         __syncwarp();
         sm100::mma_commit_elect(bar_empty + 8 * st);
@@ -609,10 +590,6 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   a.dst = dst ? dst->p : nullptr;
   a.pool_dst = pool_dst ? pool_dst->p : nullptr;
   a.relu = relu ? 1 : 0;
-  static const int mma_test = getenv("FV_CONV_MMA_TEST") ? atoi(getenv("FV_CONV_MMA_TEST")) : 0;
-  a.mma_test = mma_test;
-  static const int dx_outer = getenv("FV_CONV_DXOUTER") ? atoi(getenv("FV_CONV_DXOUTER")) : 1;
-  a.dx_outer = dx_outer;
   static unsigned long long* prof_buf = nullptr;
   static const bool want_prof = getenv("FV_CONV_PROF") != nullptr;
   if (want_prof) {
