@@ -294,16 +294,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         // a base plus a 16-byte-unit offset in the start-address field.
         const uint64_t a0 = sm100::smem_desc(sm100::smem_u32(sA + st * C::kABytes), C::kPlaneBytes, 128);
         const uint64_t b0 = sm100::smem_desc(sm100::smem_u32(sB + (BRES ? ks : st) * C::kBBytes),
-                                             (FUSED && !a.center_only ? 3 : 1) * N * 16, 128);
+                                             (FUSED ? 3 : 1) * N * 16, 128);
         (void)nk;  // one 16-channel MMA K-step per stage
         const bool leader = sm100::elect_one();
         // (the dispatch-cost probe of round 1 -- the same MMA work per stage as 9 x N256, 18 x N128 or
         // 36 x N64 dispatches: 1054 / 1398 / 2085 cycles -- is summarised in profiles/r01_summary.md)
+        // (row-fused weight images exist only for 3x3 convs: FUSED implies not centre-only)
         if (leader) {
-          if (CO || a.center_only)
-            issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
-          else if constexpr (FUSED)
+          if constexpr (FUSED)
             issue_stage_rows<R, N, true, kPairs>(a0, b0, d_base, ks == 0, bar_pair, (acc_round & 1) ^ 1);
+          else if (CO || a.center_only)
+            issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
           else
             issue_stage<R, N, 1>(a0, b0, d_base, idesc, ks == 0);
         }
