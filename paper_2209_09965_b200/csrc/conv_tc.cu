@@ -62,6 +62,10 @@ struct ConvArgs {
   double flops;        // host-side: algorithmic FLOPs of the launch (kernel timing)
   unsigned long long* prof;  // nullable (FV_CONV_PROF=1): per-CTA wait-cycle counters, kProfSlots each
 };
+#ifndef FV_CONV_PROFILE
+#define FV_CONV_PROFILE 0
+#endif
+constexpr bool kProfileBuild = FV_CONV_PROFILE != 0;
 constexpr int kProfSlots = 6;  // producer empty-wait, MMA full-wait, MMA tempty-wait, epilogue tfull-wait, MMA total, tiles
 
 // mbarrier wait that adds the cycles spent to *acc when profiling
@@ -195,7 +199,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   const uint32_t tmem_base = *tmem_slot;
 
   const int n_tiles = a.tiles_x * a.tiles_y;
-  const bool prof = a.prof != nullptr;
+  // wait-cycle counters only in a profiling build (make EXTRA=-DFV_CONV_PROFILE=1, then
+  // FV_CONV_PROF=1): every wait sits on a role's critical path, so the default build has none
+  const bool prof = kProfileBuild && a.prof != nullptr;
   unsigned long long w_empty = 0, w_full = 0, w_tempty = 0, w_tfull = 0;
   const unsigned long long t_start = prof ? clock64() : 0ull;
   int n_my_tiles = 0;
@@ -592,7 +598,7 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   a.pool_dst = pool_dst ? pool_dst->p : nullptr;
   a.relu = relu ? 1 : 0;
   static unsigned long long* prof_buf = nullptr;
-  static const bool want_prof = getenv("FV_CONV_PROF") != nullptr;
+  static const bool want_prof = kProfileBuild && getenv("FV_CONV_PROF") != nullptr;
   if (want_prof) {
     if (!prof_buf) FV_CUDA(cudaMalloc(&prof_buf, sizeof(unsigned long long) * kProfSlots * 1024));
     FV_CUDA(cudaMemsetAsync(prof_buf, 0, sizeof(unsigned long long) * kProfSlots * 1024, ctx->stream));
