@@ -98,6 +98,7 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   if (ctx->wave_rec) cudaFree(ctx->wave_rec);
   if (ctx->wave_ray) cudaFree(ctx->wave_ray);
   if (ctx->wave_hits) cudaFree(ctx->wave_hits);
+  if (ctx->wave_ovf) cudaFree(ctx->wave_ovf);
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   for (auto& sp : ctx->kspans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
   for (auto& ev : ctx->kpool) cudaEventDestroy(ev);

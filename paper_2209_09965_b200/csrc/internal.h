@@ -44,7 +44,7 @@ struct DevCounters {
   unsigned int wave_ord;   // wavefront marcher: chunks listed in ray order
   unsigned int hit_count;  // wavefront marcher: hitting rays listed by the setup pass
   unsigned int hit_next;   // wavefront marcher: work counter of the main pass over that list
-  unsigned int pad[1];
+  unsigned int ovf_count;  // wavefront marcher: rays that found the record buffer full
 };
 
 // Per-launch timing spans (fv_ctx_set_kernel_timing).
@@ -91,6 +91,8 @@ struct fv_ctx {
   int64_t wave_ray_cap = 0;
   void* wave_hits = nullptr;  // 3 float4 per hitting ray (setup pass -> main pass)
   int64_t wave_hits_cap = 0;
+  void* wave_ovf = nullptr;   // int per compacted ray: the record-overflow list
+  int64_t wave_ovf_cap = 0;
   unsigned long long launches = 0;
   // fv_frames: render / network / copy streams and their event rings (created on first use)
   cudaStream_t fstream[3] = {nullptr, nullptr, nullptr};

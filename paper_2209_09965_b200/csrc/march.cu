@@ -615,14 +615,19 @@ __device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px
   return trans;
 }
 
-__global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
+// One thread per ray, shadows inline; grid-stride over the list. Used by the naive renderer (bricks)
+// and, on the texture path, for the rays the wavefront main pass could not record (count_rays =
+// false: the setup pass counted them already).
+template <bool TEX>
+__global__ void __launch_bounds__(128) march_fast_kernel(FastParams F, bool count_rays) {
   const MarchParams& P = F.P;
   __shared__ float lut[4 * 256];
   for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = P.k_dev ? *P.k_dev : P.k_max;
-  unsigned int n_main = 0, n_shadow = 0, hitc = 0;
+  unsigned int n_main = 0, n_shadow = 0, hitc = 0, nr = 0;
+  for (int i0 = blockIdx.x * blockDim.x; i0 < k; i0 += gridDim.x * blockDim.x) {
+  const int i = i0 + threadIdx.x;
   // naive renderer lists idle lanes of occupied chunks as -(pix+1): out[~active] = 0 (renderer.py:195-197)
   const int raw = (i < k) ? (P.idx ? P.idx[i] : i) : 0;
   if (i < k && raw < 0) {
@@ -651,7 +656,7 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
     const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
     const float early = (float)P.early;
     if (hit) {
-      hitc = 1;
+      ++hitc;
       // iterations of the reference loop: t_{i+1} = t0 + (i+1)*step, stop once >= t_end - 1e-12
       const double L = t_end - t0;
       int n = (int)ceil((L - 1e-12) / P.step);
@@ -668,12 +673,12 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
         const float mid = (float)s * stepf + 0.5f * dt;
         const float px = ex + dx * mid, py = ey + dy * mid, pz = ez + dz * mid;
         float c[4];
-        tf_apply<float>(lut, P.K, tri_fast(F.V, px, py, pz), c);
+        tf_apply<float>(lut, P.K, TEX ? tri_finish_t<true>(tri_issue<true>(F.V, px, py, pz)) : tri_fast(F.V, px, py, pz), c);
         ++n_main;
         const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
         const float a_step = 1.f - keep;
         float shade = 1.f;
-        if (lit && a_step > 0.f) shade = amb + (1.f - amb) * shadow_fast(F, lut, px, py, pz, n_shadow);
+        if (lit && a_step > 0.f) shade = amb + (1.f - amb) * shadow_fast<TEX>(F, lut, px, py, pz, n_shadow);
         const float contrib = trans * a_step;
         rgb[0] += contrib * (c[0] * (shade * I0));
         rgb[1] += contrib * (c[1] * (shade * I1));
@@ -698,7 +703,10 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
       px[1] = __floats2half2_rn(out[2], out[3]);
     }
   }
-  unsigned int r = (i < k && raw >= 0) ? 1u : 0u;
+  nr += (i < k && raw >= 0) ? 1u : 0u;
+  }
+  unsigned int r = count_rays ? nr : 0u;
+  if (!count_rays) hitc = 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     r += __shfl_xor_sync(0xffffffffu, r, o);
@@ -706,9 +714,9 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
     n_main += __shfl_xor_sync(0xffffffffu, n_main, o);
     n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
   }
-  if ((threadIdx.x & 31) == 0 && r) {
-    atomicAdd(&P.counters->rays, (unsigned long long)r);
-    atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
+  if ((threadIdx.x & 31) == 0 && (r || n_main)) {
+    if (r) atomicAdd(&P.counters->rays, (unsigned long long)r);
+    if (hitc) atomicAdd(&P.counters->hit_rays, (unsigned long long)hitc);
     atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
     atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
   }
@@ -724,7 +732,8 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F) {
 // work items (4.6M per C3 frame instead of 117k hit rays, so no ray's serial chain sets the
 // tail); the composite pass sums contrib*(c*(shade*I)) per ray. Records are appended to 32-slot
 // chunks taken from a global counter (a ray's chunks form a linked list), so one march suffices.
-// A ray that cannot get a chunk (buffer full) is re-marched fused, with inline shadows.
+// A ray that cannot get a chunk (buffer full) is listed and re-marched by march_fast_kernel with
+// inline shadows after the main pass.
 constexpr int kChunk = 32;
 
 struct WaveBufs {
@@ -744,6 +753,8 @@ struct WaveBufs {
   int chunk_pool;          // warp main pass: chunks claimed per counter round trip
   int claim;               // main pass: rays claimed per counter round trip (<= 32)
   float4* hits;            // setup pass -> main pass: 3 float4 per hitting ray
+  int* ovf;                // pixels of the rays that found the record buffer full
+  unsigned int* ovf_count;
   unsigned int* hit_count;
   unsigned int* hit_next;
 };
@@ -773,13 +784,14 @@ __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float
 // with ballot/popc, so all chunks but the last are full (the composite pass relies on it). The
 // first chunk of ray r is chunk r (first_list_kernel); later ones come from per-warp pools of
 // chunk_pool chunks, the next pool claimed when the current one opens. A ray that finds the record
-// buffer full releases its chunks and is marched again with inline shadow rays (fused).
+// buffer full releases its chunks and goes to the overflow list (march_fast_kernel marches those
+// with inline shadow rays afterwards): keeping that code out of this pass leaves it at 64 registers.
 template <int kU, bool TEX>
 __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& B, const float* lut,
                                            unsigned hit_mask, int n, float last_dt, float ex, float ey,
                                            float ez, float dx, float dy, float dz, double t0, int pix,
                                            int rid, int& pool_cur, int& pool_end, unsigned int& pool_pref,
-                                           unsigned int& n_main, unsigned int& n_shadow) {
+                                           unsigned int& n_main) {
   const MarchParams& P = F.P;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -801,13 +813,13 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
     const double rt0 = __shfl_sync(0xffffffffu, t0, src);
     const int rpix = __shfl_sync(0xffffffffu, pix, src);
     const int rray = __shfl_sync(0xffffffffu, rid, src);
-    // pass 0 defers shadows to records; pass 1 (record buffer full) marches them inline
-    for (int fused = 0; fused < 2; ++fused) {
+    // (a loop of one pass: `continue` below abandons the ray when the record buffer is full)
+    for (int pass = 0; pass < 1; ++pass) {
       float trans = 1.f, depth = 0.f;
       float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;  // per-lane partial sums
       int first = -1, chunk = -1, fill = kChunk, m = 0;
       bool overflow = false;
-      unsigned int n_main_ray = 0, n_shadow_ray = 0;
+      unsigned int n_main_ray = 0;
       for (int s0 = 0; s0 < rn; s0 += 32 * kU) {
         TriFetch f[kU];
 #pragma unroll
@@ -863,16 +875,6 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
               rgb1 += contrib * (c[1] * I1);
               rgb2 += contrib * (c[2] * I2);
             }
-          } else if (fused) {
-            if (use) {
-              float shade = 1.f;
-              if (needs_shadow)
-                shade = amb + (1.f - amb) * shadow_fast<TEX>(F, lut, rex + rdx * mid, rey + rdy * mid, rez + rdz * mid,
-                                                             n_shadow_ray);
-              rgb0 += contrib * (c[0] * (shade * I0));
-              rgb1 += contrib * (c[1] * (shade * I1));
-              rgb2 += contrib * (c[2] * (shade * I2));
-            }
           } else {
             const unsigned lm = __ballot_sync(0xffffffffu, needs_shadow);
             const int cnt = __popc(lm);
@@ -920,14 +922,17 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
         if (done) break;
       }
       if (overflow) {
-        // release this ray's chunks and march it again with inline shadows
-        if (lane == 0)
+        // release this ray's chunks; march_fast_kernel re-marches it with inline shadow rays after
+        // this pass (the overflow list), so neither this pass's samples nor its pixel count
+        if (lane == 0) {
           for (int cc = first; cc >= 0; cc = (cc == chunk) ? -1 : B.chunk_next[cc]) B.chunk_fill[cc] = 0;
+          B.ray[rray] = make_int4(-1, 0, 0, 0);
+          B.ovf[atomicAdd(B.ovf_count, 1u)] = rpix;
+        }
         continue;
       }
       n_main += n_main_ray;
-      n_shadow += n_shadow_ray;
-      if (lit && !fused && m > 0) {
+      if (lit && m > 0) {
         if (lane == 0) {
           B.chunk_fill[chunk] = fill;
           B.chunk_next[chunk] = -1;
@@ -1044,7 +1049,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastPar
   const int nhit = (int)*B.hit_count;
   const int lane = threadIdx.x & 31;
   const bool lit = P.light_kind != FV_LIGHT_NONE;
-  unsigned int n_main = 0, n_shadow = 0;
+  unsigned int n_main = 0;
   const int kPool = B.chunk_pool;
   int pool_cur = 0, pool_end = 0;  // warp-uniform
   unsigned int pool_pref = 0;      // lane 0: base of the prefetched pool
@@ -1064,7 +1069,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastPar
     const double t0 = __hiloint2double(__float_as_int(h2.y), __float_as_int(h2.x));
     march_hits<kU, TEX>(F, B, lut, __ballot_sync(0xffffffffu, valid), __float_as_int(h1.w), h1.z, h0.x, h0.y,
                         h0.z, h0.w, h1.x, h1.y, t0, __float_as_int(h2.w), __float_as_int(h2.z), pool_cur,
-                        pool_end, pool_pref, n_main, n_shadow);
+                        pool_end, pool_pref, n_main);
   }
   if (lit) {
     const int pref = B.cap_a + (int)__shfl_sync(0xffffffffu, pool_pref, 0);
@@ -1074,11 +1079,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastPar
       if (pref + c < B.n_chunks_cap) B.chunk_fill[pref + c] = 0;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) n_shadow += __shfl_xor_sync(0xffffffffu, n_shadow, o);
-  if (lane == 0 && (n_main || n_shadow)) {
-    atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
-    if (n_shadow) atomicAdd(&P.counters->samples_shadow, (unsigned long long)n_shadow);
-  }
+  if (lane == 0 && n_main) atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
 }
 
 // With cap_a: list the rays whose first chunk (id = ray index) holds records, in ray order (one
@@ -1478,6 +1479,11 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
   return 0;
 }
 
+// resident blocks per SM the main pass's registers are capped for (A/B on B200 at C3)
+#ifndef FV_MAIN_MINB
+#define FV_MAIN_MINB 6
+#endif
+
 // wavefront passes, instantiated for quads from the bricked buffer (TEX = false) or the texture
 template <bool TEX>
 int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
@@ -1486,10 +1492,10 @@ int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads
   ctx->launches += 1;
   static int per_sm = 0;
   if (!per_sm) {
-    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_list_kernel<2, TEX, 5>, threads, 0));
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB>, threads, 0));
     per_sm = std::max(per_sm, 1);
   }
-  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<2, TEX, 5><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B));
+  FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B));
   return 0;
 }
 
@@ -1685,15 +1691,35 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.hits = reinterpret_cast<float4*>(ctx->wave_hits);
       B.hit_count = &ctx->counters->hit_count;
       B.hit_next = &ctx->counters->hit_next;
+      if (k_max > ctx->wave_ovf_cap) {
+        if (ctx->wave_ovf) cudaFree(ctx->wave_ovf);
+        ctx->wave_ovf = nullptr;
+        FV_CUDA(cudaMalloc(&ctx->wave_ovf, sizeof(int) * (size_t)k_max));
+        ctx->wave_ovf_cap = k_max;
+      }
+      B.ovf = reinterpret_cast<int*>(ctx->wave_ovf);
+      B.ovf_count = &ctx->counters->ovf_count;
       // half of the chunk space holds first chunks at id = ray index (k_max may exceed it: later
       // rays then take pooled first chunks); ord lists the non-empty ones in ray order
       B.cap_a = B.n_chunks_cap / 2;
       B.ord = B.chunk_fill + ctx->wave_cap / kChunk;
       B.ord_count = &ctx->counters->wave_ord;
-      // ray_next, wave_rec, wave_next, wave_ord, hit_count, hit_next are consecutive counters
-      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 6 * sizeof(unsigned int), ctx->stream));
+      // ray_next, wave_rec, wave_next, wave_ord, hit_count, hit_next, ovf_count are consecutive
+      FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 7 * sizeof(unsigned int), ctx->stream));
       rc = F.V.tex ? launch_main<true>(ctx, F, B, threads) : launch_main<false>(ctx, F, B, threads);
       if (rc) return rc;
+      if (P.light_kind != FV_LIGHT_NONE) {
+        // rays that found the record buffer full: inline shadows, one thread per ray (a grid that
+        // exits at once when the list is empty)
+        FastParams Fo = F;
+        Fo.P.idx = B.ovf;
+        Fo.P.k_dev = reinterpret_cast<const int32_t*>(B.ovf_count);
+        if (F.V.tex)
+          FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<true><<<ctx->num_sms, threads, 0, ctx->stream>>>(Fo, false));
+        else
+          FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<false><<<ctx->num_sms, threads, 0, ctx->stream>>>(Fo, false));
+        ctx->launches += 1;
+      }
       if (P.light_kind != FV_LIGHT_NONE) {
         FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, first_list_kernel<<<ctx->num_sms * 2, 256, 0, ctx->stream>>>(F, B));
         ctx->launches += 1;
@@ -1709,7 +1735,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         ctx->launches += 2;
       }
     } else {
-      FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<<<blocks, threads, 0, ctx->stream>>>(F));
+      FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<false><<<blocks, threads, 0, ctx->stream>>>(F, true));
     }
   }
   FV_CHECK_LAUNCH("march_kernel");
