@@ -57,6 +57,27 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+# FV_DIST_BACKEND=gloo: a functional check of the torchrun path on a box with fewer GPUs than ranks
+# (ranks share devices round-robin, timing all-reduces go through host tensors). Never for numbers.
+DIST_BACKEND = os.environ.get("FV_DIST_BACKEND", "nccl")
+
+
+def init_rank_device(local: int, world: int):
+    """Bind this rank's GPU and join the process group; returns the device for timing all-reduces."""
+    import torch
+
+    dev = local % torch.cuda.device_count() if DIST_BACKEND == "gloo" else local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        if DIST_BACKEND == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    return "cuda" if DIST_BACKEND == "nccl" else None
+
+
 RANK_STRIDE = 977  # each rank's session starts at its own point of the camera path / noise loop
 
 
@@ -217,11 +238,7 @@ def run_ours(args, cfg):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tdev = init_rank_device(local, world)
     from paper_2209_09965_b200 import _lib
     from paper_2209_09965_b200 import network as N
     from paper_2209_09965_b200.noise import default_stack
@@ -260,7 +277,7 @@ def run_ours(args, cfg):
     p_end.record(stream)
     torch.cuda.synchronize()
     launches = sum(c.launches() for c in pipe.pipelined_contexts()) - lp0
-    pipe_ms = max_over_ranks(p_start.elapsed_time(p_end), world, device="cuda")
+    pipe_ms = max_over_ranks(p_start.elapsed_time(p_end), world, device=tdev)
     # --- timed region 2: the same frames serialised on one stream, with per-phase events ---
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(k)]
     if world > 1:
@@ -281,7 +298,7 @@ def run_ours(args, cfg):
         e[3].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
-    serial_ms = max_over_ranks(t_start.elapsed_time(t_end), world, device="cuda")
+    serial_ms = max_over_ranks(t_start.elapsed_time(t_end), world, device=tdev)
     st = ctx.stats()  # work counters of region 2 only
     # --- timed region 3: the same frames again with CUDA events around every library launch
     # (per-kernel-class launch durations for the roofline; kept out of regions 1 and 2) ---
@@ -312,14 +329,14 @@ def run_ours(args, cfg):
         torch.distributed.barrier()
     t0 = time.perf_counter()
     pipe.frames_to_host(e2e_frames, host)
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world, device="cuda")
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world, device=tdev)
     e2e_fps = whole_job_rate(ke, world, e2e_s)
     # the same frames one blocking fv_frame call at a time (no overlap of copy and compute)
     t0 = time.perf_counter()
     for c, f, j in e2e_frames[: max(3, ke // 2)]:
         pipe.frame_to_host(c, f, j, host[0])
     e2e_serial_fps = whole_job_rate(max(3, ke // 2), world, max_over_ranks(time.perf_counter() - t0, world,
-                                                                           device="cuda"))
+                                                                           device=tdev))
     h2d = C.sizeof(_lib.FvCamera) + C.sizeof(_lib.FvFovea) + C.sizeof(C.c_int)
     if rank != 0:
         if world > 1:
@@ -402,12 +419,8 @@ def run_sharded(args, cfg):
     import torch
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
+    tdev = init_rank_device(local, world)
     group = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2209_09965_b200 import _lib
     from paper_2209_09965_b200 import network as N
     from paper_2209_09965_b200.noise import default_stack
@@ -441,7 +454,7 @@ def run_sharded(args, cfg):
         pipe.step(cams[j % PATH_FRAMES], fovea, j)
     e1.record()
     torch.cuda.synchronize()
-    ms = max_over_ranks(e0.elapsed_time(e1), world, device="cuda")
+    ms = max_over_ranks(e0.elapsed_time(e1), world, device=tdev)
     launches = ctx.launches() - l0
     st = ctx.stats()
     # end to end: frame -> host image on rank 0 (pinned), wall clock, max over ranks
@@ -454,7 +467,7 @@ def run_sharded(args, cfg):
         if rank == 0:
             host.copy_(pipe.rgb, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world, device="cuda")
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world, device=tdev)
     clk = clocks.stop() if clocks else None
     if rank == 0:
         hbm, tf_burst, tf_sus, src = load_peaks()

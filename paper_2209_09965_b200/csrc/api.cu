@@ -42,6 +42,11 @@ static cudaEvent_t kpool_get(fv_ctx* ctx) {
   return e;
 }
 
+bool pdl_enabled() {
+  static const bool on = !(getenv("FV_PDL") && atoi(getenv("FV_PDL")) == 0);
+  return on;
+}
+
 void ktime_begin(fv_ctx* ctx) {
   if (!ctx->ktiming) return;
   if (!ctx->kopen) ctx->kopen = kpool_get(ctx);

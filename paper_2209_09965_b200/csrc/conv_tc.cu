@@ -191,12 +191,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     if (kPairs)
       for (int p = 0; p < R / 2; ++p) sm100::mbar_init(bar_pair + 8 * p, kEpiWarps);
     sm100::fence_mbar_init();
+    if (BRES) {
+      // resident weights: constant for the whole graph, so copied before the dependency wait
+      const uint32_t wb = (uint32_t)(a.n_kstages * C::kBBytes);
+      sm100::mbar_arrive_expect_tx(bar_bres, wb);
+      sm100::bulk_g2s(sm100::smem_u32(sB), a.wimg, wb, bar_bres);
+    }
   }
   if (warp == 1) sm100::tmem_alloc<512>(sm100::smem_u32(tmem_slot));
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: everything above overlapped the previous kernel's tail; activations only after it is done
+  fv::pdl_wait();
 
   const int n_tiles = a.tiles_x * a.tiles_y;
   // wait-cycle counters only in a profiling build (make EXTRA=-DFV_CONV_PROFILE=1, then
@@ -208,11 +216,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
 
   if (warp == 0) {
     // ---------------- producer ----------------
-    if (BRES && lane == 0) {
-      const uint32_t wb = (uint32_t)(a.n_kstages * C::kBBytes);
-      sm100::mbar_arrive_expect_tx(bar_bres, wb);
-      sm100::bulk_g2s(sm100::smem_u32(sB), a.wimg, wb, bar_bres);
-    }
     int it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int x0 = (tile % a.tiles_x) * kTileW;
@@ -500,7 +503,7 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
   ktime_begin(ctx);
-  conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO><<<grid, kThreads, C::kSmem, ctx->stream>>>(a);
+  fv::launch_pdl(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO>, grid, kThreads, C::kSmem, ctx->stream, a);
   ktime_end(ctx, FV_KC_CONV, a.flops);
   if (a.prof) {
     std::vector<unsigned long long> h((size_t)grid * kProfSlots);

@@ -31,6 +31,33 @@ int cuda_fail(cudaError_t e, const char* what);
     if (!(cond)) { fv::set_error(__VA_ARGS__); return FV_E_INVALID; } \
   } while (0)
 
+// Programmatic dependent launch (PDL) for the reconstruction's launch chain: a kernel launched
+// with launch_pdl may start (prologue: barrier init, TMEM alloc, resident-weight copies) while the
+// previous kernel on the stream drains; its pdl_wait() (griddepcontrol.wait) holds every access to
+// activations until that kernel has completed and flushed, so the order of reads and writes is
+// the plain stream order. No kernel triggers its dependents early (griddepcontrol.launch_dependents
+// at block start measured -0.6% frames/s: the waiting blocks of the next kernel crowd the SMs);
+// they launch as the blocks exit. FV_PDL=0 launches without the attribute (pdl_wait is a no-op).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+
 // Device-side counters (one cache line each to avoid false sharing).
 struct DevCounters {
   unsigned long long rays;

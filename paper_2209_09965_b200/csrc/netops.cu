@@ -31,6 +31,7 @@ __device__ __forceinline__ void load8(const __half* p, float (&v)[8]) {
 
 __global__ void __launch_bounds__(128) upsample2_nc8_kernel(const __half* __restrict__ in,
                                                             __half* __restrict__ out, int h, int w) {
+  fv::pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y, g = blockIdx.z;
   if (j >= w) return;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(128) upsample2_nc8_kernel(const __half* __rest
 // tcgen05 logits conv's epilogue (conv_tc.cu), so this pass only streams 9 + 3 planes.
 __global__ void __launch_bounds__(128) kapply_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
                                                      float* __restrict__ out, int h, int w) {
+  fv::pdl_wait();
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
   if (x >= w) return;
   const int64_t n = (int64_t)h * w, pix = (int64_t)y * w + x;
@@ -125,6 +127,7 @@ __device__ __forceinline__ void kapply_px(const kw_t* __restrict__ kw, const flo
 // filtered image is never written. h, w: level-L dims (even).
 __global__ void __launch_bounds__(128) kapply_pool_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
                                                           float* __restrict__ out, int h, int w) {
+  fv::pdl_wait();
   const int ho = h >> 1, wo = w >> 1;
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
   if (x >= wo) return;
@@ -145,6 +148,7 @@ __global__ void __launch_bounds__(128) kapply_final_kernel(const kw_t* __restric
                                                            const float* __restrict__ od, int H, int W, int Hp, int Wp,
                                                            float* __restrict__ rgb, float* __restrict__ o_raw,
                                                            float* __restrict__ od_raw) {
+  fv::pdl_wait();
   const int u = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
   if (u >= W) return;
   float o[3];
@@ -185,6 +189,7 @@ __device__ __forceinline__ void load_win(const float* pl, int h, int w, int y0, 
 // grid (ceil(w/2/128), h/2): one thread per POOLED pixel = the 2x2 filtered pixels (2x .. 2x+1)
 __global__ void __launch_bounds__(128) kapply_pool2_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
                                                            float* __restrict__ out, int h, int w) {
+  fv::pdl_wait();
   const int ho = h >> 1, wo = w >> 1;
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
   if (x >= wo) return;
@@ -220,6 +225,7 @@ __global__ void __launch_bounds__(128) kapply_final2_kernel(const kw_t* __restri
                                                             const float* __restrict__ od, int H, int W, int Hp, int Wp,
                                                             float* __restrict__ rgb, float* __restrict__ o_raw,
                                                             float* __restrict__ od_raw) {
+  fv::pdl_wait();
   const int x = blockIdx.x * blockDim.x + threadIdx.x, v = blockIdx.y;
   const int u0 = 2 * x;
   if (u0 >= W) return;
@@ -286,6 +292,7 @@ __global__ void __launch_bounds__(128) pool3_kernel(const float* __restrict__ in
 // writes the 2x2 output block of one input pixel
 __global__ void __launch_bounds__(128) up3_kernel(const float* __restrict__ in, float* __restrict__ out,
                                                   int h, int w) {
+  fv::pdl_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y, c = blockIdx.z;
   if (j >= w) return;
   const float* p = in + (int64_t)c * h * w;
@@ -340,6 +347,7 @@ __global__ void set_input_kernel(const float* __restrict__ xin, int C, __half* _
 __global__ void finalize_kernel(const float* __restrict__ img, const float* __restrict__ od, int H,
                                 int W, int Hp, int Wp, float* __restrict__ rgb, float* __restrict__ o_raw,
                                 float* __restrict__ od_raw) {
+  fv::pdl_wait();
   const int64_t n = (int64_t)H * W;
   const int64_t pp = (int64_t)Hp * Wp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -401,7 +409,7 @@ inline int grid_for(fv_ctx* ctx, int64_t n, int threads = 256) {
 
 int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
   const dim3 grid((in.W + 127) / 128, in.H, in.C / 8);
-  FV_TIMED(ctx, FV_KC_NETOPS, upsample2_nc8_kernel<<<grid, 128, 0, ctx->stream>>>(in.p, out.p, in.H, in.W));
+  FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(upsample2_nc8_kernel, grid, 128, 0, ctx->stream, in.p, out.p, in.H, in.W));
   FV_CHECK_LAUNCH("upsample2_nc8_kernel");
   ctx->launches += 1;
   return 0;
@@ -409,7 +417,7 @@ int upsample2_nc8(fv_ctx* ctx, const fv_act& in, fv_act& out) {
 
 int kapply(fv_ctx* ctx, const kw_t* kw, const float* img, float* out, int h, int w) {
   const dim3 g((w + 127) / 128, h);
-  FV_TIMED(ctx, FV_KC_NETOPS, kapply_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
+  FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(kapply_kernel, g, 128, 0, ctx->stream, kw, img, out, h, w));
   FV_CHECK_LAUNCH("kapply_kernel");
   ctx->launches += 1;
   return 0;
@@ -423,9 +431,9 @@ static bool kapply_v1() {  // FV_KAPPLY_V=1: the per-pixel kernels (A/B)
 int kapply_pool(fv_ctx* ctx, const kw_t* kw, const float* img, float* out, int h, int w) {
   const dim3 g(((w >> 1) + 127) / 128, h >> 1);
   if (kapply_v1() || (w & 1))
-    FV_TIMED(ctx, FV_KC_NETOPS, kapply_pool_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
+    FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(kapply_pool_kernel, g, 128, 0, ctx->stream, kw, img, out, h, w));
   else
-    FV_TIMED(ctx, FV_KC_NETOPS, kapply_pool2_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, out, h, w));
+    FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(kapply_pool2_kernel, g, 128, 0, ctx->stream, kw, img, out, h, w));
   FV_CHECK_LAUNCH("kapply_pool_kernel");
   ctx->launches += 1;
   return 0;
@@ -435,11 +443,11 @@ int kapply_final(fv_ctx* ctx, fv_state* st, const kw_t* kw, const float* img, fl
                  float* od_raw) {
   if (kapply_v1() || (st->Wp & 1)) {
     const dim3 g((st->W + 127) / 128, st->H);
-    FV_TIMED(ctx, FV_KC_NETOPS, kapply_final_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, st->od, st->H, st->W, st->Hp,
+    FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(kapply_final_kernel, g, 128, 0, ctx->stream, kw, img, st->od, st->H, st->W, st->Hp,
                                                                             st->Wp, rgb, o_raw, od_raw));
   } else {
     const dim3 g(((st->W + 1) / 2 + 127) / 128, st->H);
-    FV_TIMED(ctx, FV_KC_NETOPS, kapply_final2_kernel<<<g, 128, 0, ctx->stream>>>(kw, img, st->od, st->H, st->W, st->Hp,
+    FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(kapply_final2_kernel, g, 128, 0, ctx->stream, kw, img, st->od, st->H, st->W, st->Hp,
                                                                              st->Wp, rgb, o_raw, od_raw));
   }
   FV_CHECK_LAUNCH("kapply_final_kernel");
@@ -463,7 +471,7 @@ int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out) {
 }
 
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in) {
-  FV_TIMED(ctx, FV_KC_NETOPS, up3_kernel<<<dim3((w_in + 127) / 128, h_in, 3), 128, 0, ctx->stream>>>(in, out, h_in, w_in));
+  FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(up3_kernel, dim3((w_in + 127) / 128, h_in, 3), 128, 0, ctx->stream, in, out, h_in, w_in));
   FV_CHECK_LAUNCH("up3_kernel");
   ctx->launches += 1;
   return 0;
@@ -487,7 +495,7 @@ int set_input(fv_ctx* ctx, fv_state* st, const float* xin, int C) {
 
 int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw) {
   const int64_t n = (int64_t)st->H * st->W;
-  FV_TIMED(ctx, FV_KC_NETOPS, finalize_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(img, st->od, st->H, st->W, st->Hp, st->Wp,
+  FV_TIMED(ctx, FV_KC_NETOPS, fv::launch_pdl(finalize_kernel, grid_for(ctx, n), 256, 0, ctx->stream, img, st->od, st->H, st->W, st->Hp, st->Wp,
                                                               rgb, o_raw, od_raw));
   FV_CHECK_LAUNCH("finalize_kernel");
   ctx->launches += 1;
