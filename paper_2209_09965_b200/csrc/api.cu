@@ -156,11 +156,14 @@ int fv_ctx_set_kernel_timing(fv_ctx* ctx, int enable) {
 int fv_ctx_kernel_time(fv_ctx* ctx, int cls, double* ms, double* work, uint64_t* launches) {
   FV_REQUIRE(ctx, "null context");
   FV_REQUIRE(cls >= 0 && cls < FV_KC_COUNT, "kernel class %d out of range", cls);
-  // fold the pending spans into the totals
+  // fold the pending spans into the totals (FV_KTIME_LOG=1: each span to stderr, for
+  // tools/probes/launch_times.py)
+  static const bool log = getenv("FV_KTIME_LOG") && atoi(getenv("FV_KTIME_LOG")) == 1;
   for (auto& sp : ctx->kspans) {
     FV_CUDA(cudaEventSynchronize(sp.b));
     float t = 0.f;
     FV_CUDA(cudaEventElapsedTime(&t, sp.a, sp.b));
+    if (log) fprintf(stderr, "[kspan] %d %.0f %.5f\n", sp.cls, sp.work, t);
     ctx->k_ms[sp.cls] += t;
     ctx->k_work[sp.cls] += sp.work;
     ctx->k_n[sp.cls] += 1;

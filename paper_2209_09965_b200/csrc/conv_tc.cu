@@ -89,7 +89,8 @@ struct Cfg {
   static constexpr int kPlaneBytes = (R + 2) * kRowBytes;
   static constexpr int kAcc = (2 * R * N <= 512) ? 2 : 1;
   static constexpr int kBSlots = BRES ? kBResStages : S;
-  static constexpr int kSmem = S * kABytes + kBSlots * kBBytes + 1024 + 256;
+  static constexpr int kBiasBytes = N * 4;  // the epilogue's bias copy
+  static constexpr int kSmem = S * kABytes + kBSlots * kBBytes + 1024 + 256 + kBiasBytes;
 };
 
 // All MMAs of one K-stage: R output rows x 9 taps x NK k-steps, offsets folded at compile time.
@@ -168,6 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   // bars: full[kStages], empty[kStages], tfull[2], tempty[2], weights-resident, row-pair free[R/2]
   constexpr bool kPairs = C::kAcc == 1 && FUSED;  // single accumulator: release it row pair by row pair
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5 + (kPairs ? R / 2 : 0));
+  float* s_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // N floats
   const uint32_t bar_full = sm100::smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * kStages;
   const uint32_t bar_tfull = bar_empty + 8 * kStages;
@@ -326,6 +328,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     }
   } else {
     // ---------------- epilogue ----------------
+    // bias once per CTA into smem (broadcast reads, off the per-item dependency chain)
+    for (int i = threadIdx.x - 64; i < N; i += kEpiWarps * 32) s_bias[i] = __ldg(a.bias + i);
+    sm100::named_bar_sync(1, kEpiWarps * 32);
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int half = (warp - 2) >> 2;  // the two warps of a quarter split the tile's rows/columns
     int lt = 0;
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
               float o[3];
 #pragma unroll
               for (int c = 0; c < 3; ++c) {
-                o[c] = v[c] + __ldg(a.bias + c);
+                o[c] = v[c] + s_bias[c];
                 a.od[c * hw + pix] = o[c];
               }
               if (a.feedback) {
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
                 float l[9], m = -INFINITY;
 #pragma unroll
                 for (int j = 0; j < 9; ++j) {
-                  l[j] = v[c0 + j] + __ldg(a.bias + c0 + j);
+                  l[j] = v[c0 + j] + s_bias[c0 + j];
                   m = fmaxf(m, l[j]);
                 }
                 float sum = 0.f;
@@ -401,11 +406,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
           const int y = y0 + r;
           {
             float v0[16], v1[16];
-            sm100::tmem_ld16(t_row0 + (R - 1 - r) * N + cb, v0);
-            sm100::tmem_ld16(t_row0 + (R - 2 - r) * N + cb, v1);
+            {
+              uint32_t r0[16], r1[16];
+              sm100::tmem_ld16_nowait(t_row0 + (R - 1 - r) * N + cb, r0);
+              sm100::tmem_ld16_nowait(t_row0 + (R - 2 - r) * N + cb, r1);
+              sm100::tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) { v0[j] = __uint_as_float(r0[j]); v1[j] = __uint_as_float(r1[j]); }
+            }
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const float b = __ldg(a.bias + cb + j);
+              const float b = s_bias[cb + j];
               v0[j] += b;
               v1[j] += b;
               if (a.relu) { v0[j] = fmaxf(v0[j], 0.f); v1[j] = fmaxf(v1[j], 0.f); }
