@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
               uint32_t r0[16], r1[16];
               sm100::tmem_ld16_nowait(t_row0 + (R - 1 - r) * N + cb, r0);
               sm100::tmem_ld16_nowait(t_row0 + (R - 2 - r) * N + cb, r1);
-              sm100::tmem_wait_ld();
+              sm100::tmem_wait_ld_regs(r0, r1);
 #pragma unroll
               for (int j = 0; j < 16; ++j) { v0[j] = __uint_as_float(r0[j]); v1[j] = __uint_as_float(r1[j]); }
             }

@@ -58,6 +58,20 @@ inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 #endif
 
+// One stage of the fused K-stage chain (netops.cu kchain_kernel): op 0 = filter + 2x2 pool
+// (encoder block), 1 = filter, 2 = 3-channel 2x upsample; h, w = the stage's input dims.
+struct KChainStage {
+  int op;
+  int h, w;
+  const float* kw;
+  const float* in;
+  float* out;
+};
+struct KChain {
+  int n = 0;
+  KChainStage s[16];
+};
+
 // Device-side counters (one cache line each to avoid false sharing).
 struct DevCounters {
   unsigned long long rays;

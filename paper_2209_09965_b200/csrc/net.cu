@@ -26,6 +26,8 @@ int pool3(fv_ctx* ctx, const float* in, float* out, int h_out, int w_out);
 int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in);
 int finalize(fv_ctx* ctx, fv_state* st, const float* img, float* rgb, float* o_raw, float* od_raw);
 int kapply_pool(fv_ctx* ctx, const kw_t* kw, const float* img, float* out, int h, int w);
+int kchain(fv_ctx* ctx, const KChain& ch);
+bool kchain_enabled();
 int kapply_final(fv_ctx* ctx, fv_state* st, const kw_t* kw, const float* img, float* rgb, float* o_raw,
                  float* od_raw);
 int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out);
@@ -183,8 +185,30 @@ static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_
     // forward_K (network.py:280-293): encoder levels fuse the filter with the following pool, the
     // last block (level 0) with the output stage
     const float* img = st->od;
+    // blocks 1 .. nb-2 (the small levels) as one cooperative launch when every encoder level there
+    // has even width (the paired-pixel filter + pool)
+    KChain ch;
+    bool chain = kchain_enabled() && nb >= 3 && nb - 2 <= 8 && net->blocks[0].first == 'e';
+    for (int i = 1; chain && i < nb - 1; ++i)
+      if (net->blocks[i].first == 'e' && (((st->Wp >> lv[i]) & 1) || ((st->Hp >> lv[i]) & 1))) chain = false;
     for (int i = 0; i < nb; ++i) {
       const int L = lv[i];
+      if (chain && i >= 1 && i < nb - 1) {
+        const int h = st->Hp >> L, w = st->Wp >> L;
+        if (net->blocks[i].first == 'e') {
+          ch.s[ch.n++] = {0, h, w, st->kw[i], img, st->img[L + 1]};
+          img = st->img[L + 1];
+        } else {
+          ch.s[ch.n++] = {1, h, w, st->kw[i], img, st->img2[L]};
+          ch.s[ch.n++] = {2, h, w, nullptr, st->img2[L], st->img[L - 1]};
+          img = st->img[L - 1];
+        }
+        if (i == nb - 2) {
+          rc = kchain(ctx, ch);
+          if (rc) return rc;
+        }
+        continue;
+      }
       if (net->blocks[i].first == 'e') {
         rc = kapply_pool(ctx, st->kw[i], img, st->img[L + 1], st->Hp >> L, st->Wp >> L);
         if (rc) return rc;

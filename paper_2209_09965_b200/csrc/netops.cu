@@ -9,7 +9,11 @@
 //   predict_kernel_fields network.py:268-277 (1x1 conv of the decoder hidden state)
 //   forward_K            network.py:280-293 (pool after e-blocks, upsample after d-blocks)
 //   _reconstruct_frame   bench.py:166-175   (x = rgba*m ++ m; output clipped to [0,1])
+#include <cooperative_groups.h>
+
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace fv {
 
@@ -78,11 +82,8 @@ __global__ void __launch_bounds__(128) upsample2_nc8_kernel(const __half* __rest
 // out[c,y,x] = sum_j k[j,y,x] * img[c, y+j/3-1, x+j%3-1], zero padding, taps in order
 // (apply_kernel_field, autograd.py:332-359). The softmax-normalised weights k come from the
 // tcgen05 logits conv's epilogue (conv_tc.cu), so this pass only streams 9 + 3 planes.
-__global__ void __launch_bounds__(128) kapply_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
-                                                     float* __restrict__ out, int h, int w) {
-  fv::pdl_wait();
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-  if (x >= w) return;
+__device__ __forceinline__ void kapply_at(const kw_t* __restrict__ kw, const float* __restrict__ img,
+                                          float* __restrict__ out, int h, int w, int x, int y) {
   const int64_t n = (int64_t)h * w, pix = (int64_t)y * w + x;
   float k[9];
 #pragma unroll
@@ -99,6 +100,14 @@ __global__ void __launch_bounds__(128) kapply_kernel(const kw_t* __restrict__ kw
     }
     out[(int64_t)c * n + pix] = acc;
   }
+}
+
+__global__ void __launch_bounds__(128) kapply_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
+                                                     float* __restrict__ out, int h, int w) {
+  fv::pdl_wait();
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= w) return;
+  kapply_at(kw, img, out, h, w, x, y);
 }
 
 // One pixel of apply_kernel_field for the 3 channels (same tap order and zero padding as above).
@@ -187,12 +196,9 @@ __device__ __forceinline__ void load_win(const float* pl, int h, int w, int y0, 
 }
 
 // grid (ceil(w/2/128), h/2): one thread per POOLED pixel = the 2x2 filtered pixels (2x .. 2x+1)
-__global__ void __launch_bounds__(128) kapply_pool2_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
-                                                           float* __restrict__ out, int h, int w) {
-  fv::pdl_wait();
+__device__ __forceinline__ void kapply_pool2_at(const kw_t* __restrict__ kw, const float* __restrict__ img,
+                                                float* __restrict__ out, int h, int w, int x, int y) {
   const int ho = h >> 1, wo = w >> 1;
-  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
-  if (x >= wo) return;
   const int X0 = 2 * x, Y0 = 2 * y;
   const int64_t n = (int64_t)h * w;
   float2 k[9][2];
@@ -218,6 +224,14 @@ __global__ void __launch_bounds__(128) kapply_pool2_kernel(const kw_t* __restric
     // 0.25 * (p00 + p10 + p01 + p11), left to right as autograd.avg_pool2
     out[c * no + (int64_t)y * wo + x] = 0.25f * (((p[0][0] + p[1][0]) + p[0][1]) + p[1][1]);
   }
+}
+
+__global__ void __launch_bounds__(128) kapply_pool2_kernel(const kw_t* __restrict__ kw, const float* __restrict__ img,
+                                                           float* __restrict__ out, int h, int w) {
+  fv::pdl_wait();
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= (w >> 1)) return;
+  kapply_pool2_at(kw, img, out, h, w, x, y);
 }
 
 // grid (ceil(W/2/128), H): pixels (2x, 2x+1) of row v of the cropped film
@@ -290,11 +304,8 @@ __global__ void __launch_bounds__(128) pool3_kernel(const float* __restrict__ in
 
 // 3-channel fp32 2x bilinear upsample; grid (ceil(w/128), h, 3), h, w the INPUT dims; one thread
 // writes the 2x2 output block of one input pixel
-__global__ void __launch_bounds__(128) up3_kernel(const float* __restrict__ in, float* __restrict__ out,
-                                                  int h, int w) {
-  fv::pdl_wait();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y, c = blockIdx.z;
-  if (j >= w) return;
+__device__ __forceinline__ void up3_at(const float* __restrict__ in, float* __restrict__ out, int h, int w,
+                                       int j, int i, int c) {
   const float* p = in + (int64_t)c * h * w;
   const int rows[3] = {max(i - 1, 0), i, min(i + 1, h - 1)};
   const int cols[3] = {max(j - 1, 0), j, min(j + 1, w - 1)};
@@ -312,6 +323,42 @@ __global__ void __launch_bounds__(128) up3_kernel(const float* __restrict__ in, 
       make_float2(0.25f * re[0] + 0.75f * re[1], 0.75f * re[1] + 0.25f * re[2]);
   *reinterpret_cast<float2*>(o + (int64_t)(2 * i + 1) * W2 + 2 * j) =
       make_float2(0.25f * ro[0] + 0.75f * ro[1], 0.75f * ro[1] + 0.25f * ro[2]);
+}
+
+__global__ void __launch_bounds__(128) up3_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                  int h, int w) {
+  fv::pdl_wait();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x, i = blockIdx.y, c = blockIdx.z;
+  if (j >= w) return;
+  up3_at(in, out, h, w, j, i, c);
+}
+
+// The K stage between its first and last block (forward_K, network.py:280-293) in ONE cooperative
+// launch: the small levels' filter / pool / upsample passes (each a few us of work at L1..L3, but
+// a launch and a ramp apiece) run as grid-stride loops separated by grid-wide barriers. Every
+// element is computed by the same device function as the separate kernels, so results are identical.
+__global__ void __launch_bounds__(128) kchain_kernel(KChain ch) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int s = 0; s < ch.n; ++s) {
+    const KChainStage st = ch.s[s];
+    if (st.op == 0) {
+      const int wo = st.w >> 1;
+      const int64_t n = (int64_t)(st.h >> 1) * wo;
+      for (int64_t i = tid; i < n; i += nthr) kapply_pool2_at(st.kw, st.in, st.out, st.h, st.w, (int)(i % wo), (int)(i / wo));
+    } else if (st.op == 1) {
+      const int64_t n = (int64_t)st.h * st.w;
+      for (int64_t i = tid; i < n; i += nthr) kapply_at(st.kw, st.in, st.out, st.h, st.w, (int)(i % st.w), (int)(i / st.w));
+    } else {
+      const int64_t hw = (int64_t)st.h * st.w;
+      for (int64_t i = tid; i < 3 * hw; i += nthr) {
+        const int c = (int)(i / hw);
+        const int64_t r = i - c * hw;
+        up3_at(st.in, st.out, st.h, st.w, (int)(r % st.w), (int)(r / st.w), c);
+      }
+    }
+    if (s + 1 < ch.n) grid.sync();
+  }
 }
 
 // x = rgba*m ++ m into channels 0..4 of the NHWC8 input (film region only)
@@ -475,6 +522,39 @@ int up3(fv_ctx* ctx, const float* in, float* out, int h_in, int w_in) {
   FV_CHECK_LAUNCH("up3_kernel");
   ctx->launches += 1;
   return 0;
+}
+
+int kchain(fv_ctx* ctx, const KChain& ch) {
+  if (ch.n == 0) return 0;
+  static int per_sm = 0;
+  if (!per_sm) {
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kchain_kernel, 128, 0));
+    const char* e = getenv("FV_KCHAIN_BPS");  // blocks per SM cap (A/B)
+    const int cap = e ? atoi(e) : 4;
+    if (per_sm > cap) per_sm = cap;
+    if (per_sm < 1) per_sm = 1;
+  }
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctx->num_sms * per_sm);
+  cfg.blockDim = dim3(128);
+  cfg.stream = ctx->stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  FV_TIMED(ctx, FV_KC_NETOPS, cudaLaunchKernelEx(&cfg, kchain_kernel, ch));
+  FV_CHECK_LAUNCH("kchain_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+// opt-in (FV_KCHAIN=1): measured -1.2% frames/s at C3 against the separate launches replayed from
+// the graph (the grid-stride loops with index divisions and 6 grid barriers take 62 us; the ten
+// separate launches cost less than that inside the graph)
+bool kchain_enabled() {
+  static const bool on = getenv("FV_KCHAIN") && atoi(getenv("FV_KCHAIN")) == 1 && !kapply_v1();
+  return on;
 }
 
 int pack_input(fv_ctx* ctx, fv_state* st, const float* rgba, const uint8_t* bits) {

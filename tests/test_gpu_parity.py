@@ -656,6 +656,26 @@ def test_graph_replay_equals_eager_launches(tmp_path):
     assert np.array_equal(outs["0"], outs["1"])
 
 
+@pytest.mark.parametrize("knob", ["FV_KCHAIN", "FV_PDL"])
+def test_launch_variants_give_identical_frames(tmp_path, knob):
+    """The fused K-stage chain (one cooperative launch for the levels between the first and last K
+    block) and the programmatic-dependent launches leave every frame bit-identical: the same
+    frames with the knob off (separate launches / plain stream order) and on (the default)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    outs = {}
+    for flag in ("0", "1"):
+        out = tmp_path / f"frames_{flag}.npy"
+        env = dict(os.environ, **{knob: flag})
+        subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out)], env=env, check=True, timeout=300)
+        outs[flag] = np.load(out)
+    assert np.array_equal(outs["0"], outs["1"])
+
+
 def test_record_overflow_falls_back_to_inline_shadows():
     """With a tiny shadow-record buffer (FV_WAVE_REC_CAP) most rays overflow it and are re-marched
     with inline shadow rays: the renders must still meet the same golden tolerances and the fp32
