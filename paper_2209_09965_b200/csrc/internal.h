@@ -136,8 +136,8 @@ struct fv_ctx {
   int64_t wave_ovf_cap = 0;
   unsigned long long launches = 0;
   // fv_frames: render / network / copy streams and their event rings (created on first use)
-  cudaStream_t fstream[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t fev[8] = {};
+  cudaStream_t fstream[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t fev[10] = {};
   // kernel timing (off by default)
   bool ktiming = false;
   cudaEvent_t kopen = nullptr;

@@ -1649,11 +1649,15 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     for (int a = 0; a < 3; ++a) F.qs_sh[a] = F.ld[a] * F.V.inv_sp[a] * F.step_sh;
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
-      // record slots: 16 per compacted ray (C3 needs ~12 incl. chunk tails), at least 4M
-      // FV_WAVE_REC_PER_RAY (default 16): record slots per compacted ray; FV_WAVE_REC_CAP: an
-      // absolute capacity (tests force the record-overflow fallback with a tiny one)
-      static const int64_t per_ray = getenv("FV_WAVE_REC_PER_RAY") ? std::max(1, atoi(getenv("FV_WAVE_REC_PER_RAY"))) : 16;
+      // record slots per compacted ray: 64 up to 4M rays, so the first-chunk half of the chunk space
+      // (chunk id = ray index) covers every ray and only second and later chunks are pooled (36 B
+      // per slot: 4.8 GB at 1080p); 32 beyond (4K: 9.6 GB). With 16 per ray the dense 1080p orbit
+      // (C4) overflowed on its zoomed-in frames and re-marched those rays one thread per ray:
+      // 12.6 ms against 1.56 ms per dense frame. FV_WAVE_REC_PER_RAY overrides the count;
+      // FV_WAVE_REC_CAP sets an absolute capacity (tests force the overflow fallback with a tiny one)
+      static const int64_t per_ray_env = getenv("FV_WAVE_REC_PER_RAY") ? std::max(1, atoi(getenv("FV_WAVE_REC_PER_RAY"))) : 0;
       static const int64_t cap_env = getenv("FV_WAVE_REC_CAP") ? std::max(2 * kChunk, atoi(getenv("FV_WAVE_REC_CAP"))) : 0;
+      const int64_t per_ray = per_ray_env ? per_ray_env : (k_max <= (4 << 20) ? 64 : 32);
       const int64_t rec_cap = (cap_env ? cap_env : std::max<int64_t>(4 << 20, per_ray * k_max)) / kChunk * kChunk;
       if (rec_cap > ctx->wave_cap) {
         if (ctx->wave_rec) cudaFree(ctx->wave_rec);

@@ -111,6 +111,13 @@ class FramePipeline:
             self._nctx = _lib.Context(self.ctx.device, stream=self._s_net)
             self._rctx.ensure_noise(self.ctx._noise_ref)
             self._vol_r = self.scene.volume.handle(self._rctx, self.scene.tf)
+            # frame t+1's mask + compaction on a third (low-priority) stream as soon as frame t's march
+            # has consumed the ray list, i.e. next to frame t's network (FV_MASK_AHEAD=0: in line)
+            self._mask_ahead = os.environ.get("FV_MASK_AHEAD", "1") == "1"
+            if self._mask_ahead:
+                self._s_mask = torch.cuda.Stream(device=self.ctx.device, priority=0)
+                self._mctx = _lib.Context(self.ctx.device, stream=self._s_mask)
+                self._mctx.ensure_noise(self.ctx._noise_ref)
         s_r, s_n = self._s_render, self._s_net
         # both streams start after everything already queued on the pipeline's own stream
         start = torch.cuda.Event()
@@ -118,12 +125,18 @@ class FramePipeline:
         s_r.wait_event(start)
         s_n.wait_event(start)
         net_done = []
+        ahead = self._mask_ahead
+        masked = None
+        if ahead:
+            self._s_mask.wait_event(start)
+            masked = self._mask_on(self._mctx, frames[0])
         for t, (cam, fovea, j) in enumerate(frames):
             if t >= 2:
                 s_r.wait_event(net_done[t - 2])
-            f = fovea.c_struct()
-            _lib.check(self._rctx.lib.fv_mask_compact(self._rctx.h, int(j), self.h, self.w, C.byref(f), None, None,
-                                                      _lib.ptr(self.idx), _lib.ptr(self.k), self.state.h))
+            if ahead:
+                s_r.wait_event(masked)
+            else:
+                self._mask_on(self._rctx, (cam, fovea, j))
             camc = cam.c_struct()
             _lib.check(self._rctx.lib.fv_render_sparse(
                 self._rctx.h, self._vol_r, C.byref(camc), self._light_ref(), C.byref(self._set),
@@ -136,14 +149,35 @@ class FramePipeline:
             done = torch.cuda.Event()
             done.record(s_n)
             net_done.append(done)
+            if ahead and t + 1 < len(frames):
+                # after frame t's reconstruct was enqueued: the state now points at frame t+1's input
+                # buffer; the mask waits for frame t's march (the last reader of the ray list) and
+                # frame t-1's network (the last reader of that buffer)
+                self._s_mask.wait_event(rendered)
+                if t >= 1:  # frame t-1's network read this input buffer (implied unless FV_PIPE_OVERLAP)
+                    self._s_mask.wait_event(net_done[t - 1])
+                masked = self._mask_on(self._mctx, frames[t + 1])
         # rejoin the pipeline's own stream
         self.ctx.stream.wait_event(net_done[-1])
         rj = torch.cuda.Event()
         rj.record(s_r)
         self.ctx.stream.wait_event(rj)
 
+    def _mask_on(self, ctx, frame):
+        """Enqueue one frame's mask + compaction on ctx's stream; returns the event after it."""
+        import torch
+
+        _, fovea, j = frame
+        f = fovea.c_struct()
+        _lib.check(ctx.lib.fv_mask_compact(ctx.h, int(j), self.h, self.w, C.byref(f), None, None,
+                                           _lib.ptr(self.idx), _lib.ptr(self.k), self.state.h))
+        ev = torch.cuda.Event()
+        ev.record(ctx.stream)
+        return ev
+
     def pipelined_contexts(self):
-        return [c for c in (getattr(self, "_rctx", None), getattr(self, "_nctx", None)) if c is not None]
+        return [c for c in (getattr(self, "_rctx", None), getattr(self, "_nctx", None), getattr(self, "_mctx", None))
+                if c is not None]
 
     def dense(self, cam: Camera):
         """Dense baseline frame (render_full, renderer.py:211-222) into a device buffer."""

@@ -359,11 +359,13 @@ def test_end_to_end_c1_against_reference(golden, stack):
     assert O.psnr(host, g["img1"]) >= 55.0
 
 
-@pytest.mark.parametrize("overlap", ["0", "1"])
-def test_pipelined_frames_equal_serial_frames(stack, overlap, monkeypatch):
+@pytest.mark.parametrize("overlap,ahead", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
+def test_pipelined_frames_equal_serial_frames(stack, overlap, ahead, monkeypatch):
     """The pipelined frame loop -- one stream in frame order, or (FV_PIPE_OVERLAP=1) render t+1 on a
-    second stream during reconstruct t -- must not change any frame."""
+    second stream during reconstruct t, with (FV_MASK_AHEAD=1) or without the next frame's mask on a
+    third stream -- must not change any frame."""
     monkeypatch.setenv("FV_PIPE_OVERLAP", overlap)
+    monkeypatch.setenv("FV_MASK_AHEAD", ahead)
     from paper_2209_09965_b200.pipeline import FramePipeline
     from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
     from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
@@ -635,6 +637,16 @@ outs = []
 for i in range(6):
     pipe.step(cams[i], spec.fovea(), i)
     outs.append(pipe.rgb.cpu().numpy())
+if len(sys.argv) > 3:  # also the pipelined loop and the C ABI's fv_frames over the same frames
+    frames = [(cams[i], spec.fovea(), i) for i in range(6)]
+    pipe.reset()
+    pipe.run_pipelined(frames)
+    torch.cuda.synchronize()
+    outs.append(pipe.rgb.cpu().numpy())
+    pipe.reset()
+    host = [np.zeros((184, 320, 3), np.float32) for _ in range(6)]
+    pipe.frames_to_host(frames, host)
+    outs.extend(host)
 np.save(sys.argv[2], np.stack(outs))
 """
 
@@ -656,7 +668,7 @@ def test_graph_replay_equals_eager_launches(tmp_path):
     assert np.array_equal(outs["0"], outs["1"])
 
 
-@pytest.mark.parametrize("knob", ["FV_KCHAIN", "FV_PDL"])
+@pytest.mark.parametrize("knob", ["FV_KCHAIN", "FV_PDL", "FV_MASK_AHEAD"])
 def test_launch_variants_give_identical_frames(tmp_path, knob):
     """The fused K-stage chain (one cooperative launch for the levels between the first and last K
     block) and the programmatic-dependent launches leave every frame bit-identical: the same
@@ -671,9 +683,13 @@ def test_launch_variants_give_identical_frames(tmp_path, knob):
     for flag in ("0", "1"):
         out = tmp_path / f"frames_{flag}.npy"
         env = dict(os.environ, **{knob: flag})
-        subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out)], env=env, check=True, timeout=300)
+        subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out), "loops"], env=env, check=True,
+                       timeout=300)
         outs[flag] = np.load(out)
     assert np.array_equal(outs["0"], outs["1"])
+    # the pipelined loop ends on frame 5, fv_frames returns frames 0..5: all equal to the stepped ones
+    assert np.array_equal(outs["1"][6], outs["1"][5])
+    assert np.array_equal(outs["1"][7:], outs["1"][:6])
 
 
 def test_record_overflow_falls_back_to_inline_shadows():
