@@ -287,14 +287,54 @@ def init_params(blocks: str, seed: int, in_channels: int = 8, fp16_weights: bool
 
 
 def conv3x3(x: np.ndarray, w: np.ndarray, b: np.ndarray) -> np.ndarray:
-    """Cross-correlation, zero padding 1 (autograd.py:238-276), as 9 shifted matmuls. x (C,H,W)."""
-    c, h, wd = x.shape
-    xp = np.pad(x, ((0, 0), (1, 1), (1, 1)))
-    out = np.zeros((w.shape[0], h * wd), np.float32)
-    for ky in range(3):
-        for kx in range(3):
-            out += w[:, :, ky, kx] @ xp[:, ky:ky + h, kx:kx + wd].reshape(c, -1)
-    return (out + b[:, None]).reshape(w.shape[0], h, wd)
+    """Cross-correlation, zero padding 1 (autograd.py:238-276). x (C,H,W) -> (cout,H,W)."""
+    return np.ascontiguousarray(conv3x3_hwc(np.ascontiguousarray(np.moveaxis(x, 0, -1)), w, b).transpose(2, 0, 1))
+
+
+def conv3x3_hwc(x, w: np.ndarray, b: np.ndarray, relu_out: bool = False, band: int = 32) -> np.ndarray:
+    """The same conv on a channel-last (H,W,C) image -> (H,W,cout), as nine shifted GEMMs.
+
+    x may be a list of (H,W,C_i) parts: concat_channels (autograd.py:173-185) is done by writing
+    the parts into the padded buffer. The zero-padded image is stored with rows of W+2 pixels, so
+    tap (ky,kx) of every output pixel in a band of rows is one CONTIGUOUS slice of the flattened
+    padded image, offset by ky*(W+2)+kx (the two junk columns per row this computes are dropped).
+    No im2col copy is built; the sum over (c, ky, kx) runs in a different order than the
+    reference's single sgemm, which moves fp32 results by ~1e-6 (BLAS order is unpinned in the
+    reference too). relu_out applies relu (autograd.py:134-141) per band."""
+    parts = x if isinstance(x, (list, tuple)) else [x]
+    h, wd = parts[0].shape[:2]
+    c = sum(p.shape[2] for p in parts)
+    wp2 = wd + 2
+    cout = w.shape[0]
+    xp = np.empty((h + 3, wp2, c), np.float32)
+    xp[0] = 0.0
+    xp[h + 1:] = 0.0
+    xp[:, 0] = 0.0
+    xp[:, wd + 1] = 0.0
+    c0 = 0
+    for p in parts:
+        xp[1:h + 1, 1:wd + 1, c0:c0 + p.shape[2]] = p
+        c0 += p.shape[2]
+    flat = xp.reshape(-1, c)
+    taps = [np.ascontiguousarray(w[:, :, t // 3, t % 3].T, dtype=np.float32) for t in range(9)]
+    bias = b.astype(np.float32)
+    out = np.empty((h, wd, cout), np.float32)
+    tmp = None
+    for r0 in range(0, h, band):
+        rows = min(band, h - r0)
+        n = rows * wp2
+        acc = flat[r0 * wp2:r0 * wp2 + n] @ taps[0]
+        if tmp is None or tmp.shape[0] != n:
+            tmp = np.empty((n, cout), np.float32)
+        for t in range(1, 9):
+            o = (r0 + t // 3) * wp2 + t % 3
+            np.matmul(flat[o:o + n], taps[t], out=tmp)
+            acc += tmp
+        acc += bias
+        if relu_out:
+            np.maximum(acc, 0.0, out=acc)
+        out[r0:r0 + rows] = acc.reshape(rows, wp2, cout)[:, :wd]
+    return out
 
 
 def relu(x):
@@ -302,33 +342,56 @@ def relu(x):
 
 
 def pool2(x):
+    """avg_pool2 (autograd.py:279-291) on (C,H,W)."""
     return 0.25 * (x[:, 0::2, 0::2] + x[:, 1::2, 0::2] + x[:, 0::2, 1::2] + x[:, 1::2, 1::2])
 
 
+def pool2_hwc(x):
+    return 0.25 * (x[0::2, 0::2] + x[1::2, 0::2] + x[0::2, 1::2] + x[1::2, 1::2])
+
+
+def _up2_axis(d, ax):
+    """Half-pixel bilinear x2 along one axis, edge clamp (autograd.py:294-305):
+    out[2i] = 0.25*d[i-1] + 0.75*d[i], out[2i+1] = 0.75*d[i] + 0.25*d[i+1] (clamped)."""
+    d = np.moveaxis(d, ax, 0)
+    n = d.shape[0]
+    out = np.empty((2 * n,) + d.shape[1:], dtype=d.dtype)
+    q = 0.75 * d
+    ev, od = out[0::2], out[1::2]
+    np.multiply(d[:1], 0.25, out=ev[:1])
+    np.multiply(d[:-1], 0.25, out=ev[1:])
+    ev += q
+    np.multiply(d[1:], 0.25, out=od[:-1])
+    np.multiply(d[-1:], 0.25, out=od[-1:])
+    od += q  # (0.75*d + 0.25*nxt: the same two rounded products and one rounded sum)
+    return np.moveaxis(out, 0, ax)
+
+
 def up2(x):
-    """Half-pixel bilinear x2, edge clamp, rows then columns (autograd.py:294-329)."""
-    def axis(d, ax):
-        d = np.moveaxis(d, ax, -1)
-        prev = np.concatenate([d[..., :1], d[..., :-1]], axis=-1)
-        nxt = np.concatenate([d[..., 1:], d[..., -1:]], axis=-1)
-        out = np.empty(d.shape[:-1] + (2 * d.shape[-1],), dtype=d.dtype)
-        out[..., 0::2] = 0.25 * prev + 0.75 * d
-        out[..., 1::2] = 0.75 * d + 0.25 * nxt
-        return np.moveaxis(out, -1, ax)
-    return axis(axis(x, 1), 2)
+    """upsample_bilinear2 (autograd.py:322-329) on (C,H,W): rows then columns."""
+    return _up2_axis(_up2_axis(x, 1), 2)
+
+
+def up2_hwc(x):
+    return _up2_axis(_up2_axis(x, 0), 1)
 
 
 def kernel_filter(img, logits):
-    """softmax over 9 taps then per-pixel 3x3 filter, zero padding (autograd.py:188-199, :332-359)."""
-    m = logits.max(axis=0, keepdims=True)
+    """softmax over 9 taps then per-pixel 3x3 filter, zero padding (autograd.py:188-199, :332-359).
+    img (3,H,W), logits (9,H,W)."""
+    return kernel_filter_hwc(np.moveaxis(img, 0, -1), np.moveaxis(logits, 0, -1)).transpose(2, 0, 1)
+
+
+def kernel_filter_hwc(img, logits):
+    m = logits.max(axis=-1, keepdims=True)
     e = np.exp(logits - m)
-    k = e / e.sum(axis=0, keepdims=True)
-    h, w = img.shape[1:]
-    ip = np.pad(img, ((0, 0), (1, 1), (1, 1)))
+    k = e / e.sum(axis=-1, keepdims=True)
+    h, w = img.shape[:2]
+    ip = np.pad(img, ((1, 1), (1, 1), (0, 0)))
     out = np.zeros_like(img)
     for j in range(9):
         dy, dx = divmod(j, 3)
-        out += k[j:j + 1] * ip[:, dy:dy + h, dx:dx + w]
+        out += k[..., j:j + 1] * ip[dy:dy + h, dx:dx + w]
     return out
 
 
@@ -336,48 +399,50 @@ def net_forward(params: dict, blocks: str, x: np.ndarray, state: dict | None, us
     """forward_full for one frame (network.py:296-323). x (C,H,W) float32 rgba[+mask].
 
     state: None or {"hidden": [arrays (C,Hp/s,Wp/s)], "prev": (3,Hp,Wp)}.
-    returns (O (3,H,W), O_d (3,H,W), new_state)
+    returns (O (3,H,W), O_d (3,H,W), new_state); the state's arrays are (C,h,w) views of
+    channel-last buffers (the whole forward runs channel-last, see conv3x3_hwc).
     """
     layout, k_in, ne, nd, levels, cfg = conv_layout(blocks)
     c, h, w = x.shape
     div = 2 ** ne
     hp, wp = -(-h // div) * div, -(-w // div) * div
-    xp = np.zeros((c, hp, wp), np.float32)
-    xp[:, :h, :w] = x
-    prev = np.zeros((3, hp, wp), np.float32) if state is None else state["prev"]
-    cur = np.concatenate([xp, prev], axis=0)
+    cur = np.zeros((hp, wp, c + 3), np.float32)
+    cur[:h, :w, :c] = np.moveaxis(x, 0, -1)
+    if state is not None:
+        cur[..., c:] = np.moveaxis(state["prev"], 0, -1)
+    P = params
+
+    def block(t, i):
+        t = conv3x3_hwc(t, P[f"D.block{i}.conv1.w"], P[f"D.block{i}.conv1.b"], relu_out=True)
+        return conv3x3_hwc(t, P[f"D.block{i}.conv2.w"], P[f"D.block{i}.conv2.b"], relu_out=True)
+
     skips = []
     for i in range(ne):
-        cur = relu(conv3x3(cur, params[f"D.block{i}.conv1.w"], params[f"D.block{i}.conv1.b"]))
-        cur = relu(conv3x3(cur, params[f"D.block{i}.conv2.w"], params[f"D.block{i}.conv2.b"]))
+        cur = block(cur, i)
         skips.append(cur)
-        cur = pool2(cur)
+        cur = pool2_hwc(cur)
     hd = []
     for j in range(nd):
-        if j > 0:
-            cur = np.concatenate([up2(cur), skips[ne - j]], axis=0)
-        hid = (np.zeros((layout[ne + j][1],) + cur.shape[1:], np.float32) if state is None
-               else state["hidden"][j])
-        cur = np.concatenate([cur, hid], axis=0)
-        b = ne + j
-        cur = relu(conv3x3(cur, params[f"D.block{b}.conv1.w"], params[f"D.block{b}.conv1.b"]))
-        cur = relu(conv3x3(cur, params[f"D.block{b}.conv2.w"], params[f"D.block{b}.conv2.b"]))
+        parts = [up2_hwc(cur), skips[ne - j]] if j > 0 else [cur]
+        parts.append(np.zeros(parts[0].shape[:2] + (layout[ne + j][1],), np.float32) if state is None
+                     else np.moveaxis(state["hidden"][j], 0, -1))
+        cur = block(parts, ne + j)
         hd.append(cur)
-    od = conv3x3(hd[-1], params["D.head.w"], params["D.head.b"])
+    od = conv3x3_hwc(hd[-1], P["D.head.w"], P["D.head.b"])
     img = od
     if use_k:
         by_level = {ne - j: hd[j] for j in range(nd)}
         for i, lv in enumerate(levels):
             hdl = by_level[lv]
-            wk = params[f"K.block{i}.w"][:, :, 0, 0]
-            logits = (wk @ hdl.reshape(hdl.shape[0], -1) + params[f"K.block{i}.b"][:, None]).reshape(
-                9, *hdl.shape[1:])
-            img = kernel_filter(img, logits)
+            logits = hdl @ np.ascontiguousarray(P[f"K.block{i}.w"][:, :, 0, 0].T) + P[f"K.block{i}.b"]
+            img = kernel_filter_hwc(img, logits)
             if cfg[i][0] == "e":
-                img = pool2(img)
+                img = pool2_hwc(img)
             elif i < len(cfg) - 1:
-                img = up2(img)
-    return img[:, :h, :w], od[:, :h, :w], {"hidden": hd, "prev": od}
+                img = up2_hwc(img)
+    chw = lambda a: a.transpose(2, 0, 1)  # noqa: E731
+    return (np.ascontiguousarray(chw(img[:h, :w])), np.ascontiguousarray(chw(od[:h, :w])),
+            {"hidden": [chw(t) for t in hd], "prev": chw(od)})
 
 
 # --------------------------------------------------------------------------- metrics

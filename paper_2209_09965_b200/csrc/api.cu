@@ -104,6 +104,8 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   if (ctx->wave_ray) cudaFree(ctx->wave_ray);
   if (ctx->wave_hits) cudaFree(ctx->wave_hits);
   if (ctx->wave_ovf) cudaFree(ctx->wave_ovf);
+  if (ctx->wave_fb) cudaFreeHost(ctx->wave_fb);
+  if (ctx->wave_fb_ev) cudaEventDestroy(ctx->wave_fb_ev);
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   for (auto& sp : ctx->kspans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
   for (auto& ev : ctx->kpool) cudaEventDestroy(ev);
@@ -451,13 +453,20 @@ int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st,
   return 0;
 }
 
-// A path of frames with host outputs, pipelined over three streams:
-//   render stream : mask + compaction + march of frame t (waits for frame t-2's network, the last
-//                   reader of the input buffer it overwrites -- the state alternates two buffers)
-//   network stream: reconstruction of frame t into device image t%2 (waits for render t and for
-//                   the copy of frame t-2, the last reader of that image)
-//   copy stream   : device image t%2 -> host_rgb_out[t]
-// The host enqueues in frame order, so every kernel sees exactly the buffers fv_frame would.
+// A path of frames with host outputs, pipelined over four streams:
+//   mask stream   : mask + compaction of frame t+1 (FV_MASK_AHEAD, default on) next to frame t's
+//                   network; waits for rendered[t] (the march of frame t, the last reader of the ray
+//                   list) and net_done[t-1] (the last reader of the input buffer it fills), signals
+//                   masked[t+1]. With FV_MASK_AHEAD=0 the mask runs in line on the render stream.
+//   render stream : the march of frame t (waits for masked[t] and net_done[t-2]); by default this
+//                   IS the network stream (render and network in frame order: the marcher's and the
+//                   convs' persistent grids do not share SMs well); FV_PIPE_OVERLAP=1 gives it its
+//                   own stream so render t+1 overlaps reconstruct t. Signals rendered[t].
+//   network stream: reconstruction of frame t into device image t%2 (waits for rendered[t] and
+//                   copied[t-2], the last reader of that image); signals net_done[t].
+//   copy stream   : device image t%2 -> host_rgb_out[t] (waits for net_done[t]); signals copied[t].
+// The host enqueues in frame order, so every kernel sees exactly the buffers fv_frame would. On an
+// error the loop stops, the context's own stream is restored and rejoined with all four streams.
 int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, int n,
               const fv_camera* cams, const fv_light* light, const fv_settings* settings,
               const fv_fovea* foveas, const int* frame_ids, float* const* host_rgb_out) {
@@ -528,52 +537,67 @@ int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st
     ctx->stream = s_m;
     rc = launch_mask_compact(ctx, frame_ids[0], H, W, &foveas[0], nullptr, nullptr, ctx->idx_scratch,
                              ctx->k_scratch, st->x.p, st->Wp);
-    if (!rc) FV_CUDA(cudaEventRecord(masked[0], s_m));
+    if (!rc) {
+      const cudaError_t e = cudaEventRecord(masked[0], s_m);
+      if (e != cudaSuccess) rc = cuda_fail(e, "cudaEventRecord (mask ahead)");
+    }
+  }
+// inside the frame loop: record the failure and leave the loop (the stream state is restored below)
+#define FV_TRY(call)                                   \
+  {                                                    \
+    const cudaError_t e_ = (call);                     \
+    if (e_ != cudaSuccess) {                           \
+      rc = cuda_fail(e_, #call);                       \
+      break;                                           \
+    }                                                  \
   }
   for (int t = 0; t < n && !rc; ++t) {
     const int b = t & 1;
     float* img = ctx->rgb_scratch + (int64_t)b * 3 * npix;
     // render
-    if (t >= 2) FV_CUDA(cudaStreamWaitEvent(s_r, net_done[b], 0));
+    if (t >= 2) FV_TRY(cudaStreamWaitEvent(s_r, net_done[b], 0));
     ctx->stream = s_r;
-    if (ahead)
-      FV_CUDA(cudaStreamWaitEvent(s_r, masked[b], 0));
-    else
+    if (ahead) {
+      FV_TRY(cudaStreamWaitEvent(s_r, masked[b], 0));
+    } else {
       rc = launch_mask_compact(ctx, frame_ids[t], H, W, &foveas[t], nullptr, nullptr, ctx->idx_scratch,
                                ctx->k_scratch, st->x.p, st->Wp);
+    }
     if (!rc)
       rc = launch_render(ctx, vol, &cams[t], light, settings, ctx->idx_scratch, ctx->k_scratch, (int)npix,
                          nullptr, nullptr, st->x.p, st->Wp);
     if (rc) break;
-    FV_CUDA(cudaEventRecord(rendered[b], s_r));
+    FV_TRY(cudaEventRecord(rendered[b], s_r));
     // network
-    FV_CUDA(cudaStreamWaitEvent(s_n, rendered[b], 0));
-    if (t >= 2) FV_CUDA(cudaStreamWaitEvent(s_n, copied[b], 0));
+    FV_TRY(cudaStreamWaitEvent(s_n, rendered[b], 0));
+    if (t >= 2) FV_TRY(cudaStreamWaitEvent(s_n, copied[b], 0));
     ctx->stream = s_n;
     rc = reconstruct(ctx, net, st, 1, img, nullptr, nullptr);
     if (rc) break;
-    FV_CUDA(cudaEventRecord(net_done[b], s_n));
+    FV_TRY(cudaEventRecord(net_done[b], s_n));
     if (ahead && t + 1 < n) {
       // reconstruct() swapped the state's input buffers: st->x is frame t+1's now
-      FV_CUDA(cudaStreamWaitEvent(s_m, rendered[b], 0));
-      if (t >= 1) FV_CUDA(cudaStreamWaitEvent(s_m, net_done[b ^ 1], 0));
+      FV_TRY(cudaStreamWaitEvent(s_m, rendered[b], 0));
+      if (t >= 1) FV_TRY(cudaStreamWaitEvent(s_m, net_done[b ^ 1], 0));
       ctx->stream = s_m;
       rc = launch_mask_compact(ctx, frame_ids[t + 1], H, W, &foveas[t + 1], nullptr, nullptr, ctx->idx_scratch,
                                ctx->k_scratch, st->x.p, st->Wp);
       if (rc) break;
-      FV_CUDA(cudaEventRecord(masked[b ^ 1], s_m));
+      FV_TRY(cudaEventRecord(masked[b ^ 1], s_m));
     }
     // copy out
-    FV_CUDA(cudaStreamWaitEvent(s_c, net_done[b], 0));
-    FV_CUDA(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, s_c));
-    FV_CUDA(cudaEventRecord(copied[b], s_c));
+    FV_TRY(cudaStreamWaitEvent(s_c, net_done[b], 0));
+    FV_TRY(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, s_c));
+    FV_TRY(cudaEventRecord(copied[b], s_c));
   }
   ctx->stream = own;
-  // rejoin: the context's own stream continues after every frame and copy
+  // rejoin: the context's own stream continues after every frame and copy (also after an error)
   for (cudaStream_t s : {s_r, s_n, s_c, s_m}) {
-    FV_CUDA(cudaEventRecord(ctx->fev[7], s));
-    FV_CUDA(cudaStreamWaitEvent(own, ctx->fev[7], 0));
+    cudaError_t e = cudaEventRecord(ctx->fev[7], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(own, ctx->fev[7], 0);
+    if (e != cudaSuccess && !rc) rc = cuda_fail(e, "fv_frames rejoin");
   }
+#undef FV_TRY
   if (rc) return rc;
   FV_CUDA(cudaStreamSynchronize(s_c));
   return 0;

@@ -134,6 +134,12 @@ struct fv_ctx {
   int64_t wave_hits_cap = 0;
   void* wave_ovf = nullptr;   // int per compacted ray: the record-overflow list
   int64_t wave_ovf_cap = 0;
+  int64_t wave_cap_a = 0;     // record chunks reserved as first chunks (chunk id = ray index)
+  // previous render's record usage, read back asynchronously into pinned memory: [0] = compacted
+  // rays k, [1..7] = DevCounters ray_next..ovf_count (see march.cu, record buffer sizing)
+  unsigned int* wave_fb = nullptr;
+  cudaEvent_t wave_fb_ev = nullptr;
+  bool wave_fb_pending = false;
   unsigned long long launches = 0;
   // fv_frames: render / network / copy streams and their event rings (created on first use)
   cudaStream_t fstream[4] = {nullptr, nullptr, nullptr, nullptr};

@@ -1649,22 +1649,65 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     for (int a = 0; a < 3; ++a) F.qs_sh[a] = F.ld[a] * F.V.inv_sp[a] * F.step_sh;
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
-      // record slots per compacted ray: 64 up to 4M rays, so the first-chunk half of the chunk space
-      // (chunk id = ray index) covers every ray and only second and later chunks are pooled (36 B
-      // per slot: 4.8 GB at 1080p); 32 beyond (4K: 9.6 GB). With 16 per ray the dense 1080p orbit
-      // (C4) overflowed on its zoomed-in frames and re-marched those rays one thread per ray:
-      // 12.6 ms against 1.56 ms per dense frame. FV_WAVE_REC_PER_RAY overrides the count;
-      // FV_WAVE_REC_CAP sets an absolute capacity (tests force the overflow fallback with a tiny one)
+      // Record buffer, in chunks of kChunk slots (36 B per slot): the first cap_a chunks are the
+      // first chunks of rays 0..cap_a-1 (chunk id = ray index); the rest is the pool for later
+      // chunks and for the first chunks of rays beyond cap_a. It is sized from what this context's
+      // previous render used -- its ray count k, pooled-chunk count and overflow count, read back
+      // asynchronously into pinned memory (a readback still in flight is not waited for) -- and
+      // never shrinks. A frame whose records do not fit is still correct: its overflowing rays are
+      // re-marched one thread per ray (inline shadows) after the main pass, and the next frame gets
+      // a larger buffer. (Round 1 allocated 64 slots per FILM pixel: 4.8 GB per context at 1080p
+      // against ~1.8 GB of records a C3 frame writes.) FV_WAVE_REC_PER_RAY fixes the size at that
+      // many slots per film pixel, FV_WAVE_REC_CAP at an absolute slot count (tests use a tiny one
+      // to force the overflow fallback); both disable the feedback.
       static const int64_t per_ray_env = getenv("FV_WAVE_REC_PER_RAY") ? std::max(1, atoi(getenv("FV_WAVE_REC_PER_RAY"))) : 0;
       static const int64_t cap_env = getenv("FV_WAVE_REC_CAP") ? std::max(2 * kChunk, atoi(getenv("FV_WAVE_REC_CAP"))) : 0;
-      const int64_t per_ray = per_ray_env ? per_ray_env : (k_max <= (4 << 20) ? 64 : 32);
-      const int64_t rec_cap = (cap_env ? cap_env : std::max<int64_t>(4 << 20, per_ray * k_max)) / kChunk * kChunk;
-      if (rec_cap > ctx->wave_cap) {
-        if (ctx->wave_rec) cudaFree(ctx->wave_rec);
-        ctx->wave_rec = nullptr;
-        FV_CUDA(cudaMalloc(&ctx->wave_rec, (sizeof(float4) * 2 + sizeof(float)) * rec_cap +
-                                               3 * sizeof(int) * (rec_cap / kChunk) + 64 * sizeof(int)));
-        ctx->wave_cap = rec_cap;
+      {
+        cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+        FV_CUDA(cudaStreamIsCapturing(ctx->stream, &cap_st));
+        const bool capturing = cap_st != cudaStreamCaptureStatusNone;
+        const int64_t have = ctx->wave_cap / kChunk;
+        int64_t want_a = ctx->wave_cap_a, want_pool = have - ctx->wave_cap_a;
+        if (cap_env || per_ray_env) {
+          const int64_t n = (cap_env ? cap_env : per_ray_env * k_max) / kChunk;
+          want_a = n / 2;
+          want_pool = n - n / 2;
+        } else if (have == 0) {
+          // no history: first chunks for a quarter of the film's pixels, 8 pooled slots per pixel
+          want_a = std::max<int64_t>(1024, ((int64_t)k_max + 3) / 4);
+          want_pool = std::max<int64_t>(4096, (int64_t)k_max * 8 / kChunk);
+        } else if (ctx->wave_fb_pending && !capturing && cudaEventQuery(ctx->wave_fb_ev) == cudaSuccess) {
+          ctx->wave_fb_pending = false;
+          const int64_t k_prev = ctx->wave_fb[0], pooled = ctx->wave_fb[1 + 1], ovf = ctx->wave_fb[1 + 6];
+          want_a = std::max(want_a, std::min<int64_t>(k_max, k_prev + k_prev / 4 + 1024));
+          want_pool = std::max(want_pool, ovf ? 2 * want_pool : pooled + 3 * pooled / 10 + 1024);
+        } else {
+          (void)cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+        }
+        int64_t need = std::min<int64_t>(want_a + want_pool, INT32_MAX / kChunk);
+        if (need > have) {
+          if (ctx->wave_rec) cudaFree(ctx->wave_rec);
+          ctx->wave_rec = nullptr;
+          ctx->wave_cap = 0;
+          // on an allocation failure retry smaller (the overflow path handles what does not fit)
+          for (int64_t n = need; n >= 64 && !ctx->wave_rec; n /= 2) {
+            const size_t bytes = (sizeof(float4) * 2 + sizeof(float)) * (size_t)(n * kChunk) + 3 * sizeof(int) * (size_t)n +
+                                 64 * sizeof(int);
+            if (cudaMalloc(&ctx->wave_rec, bytes) == cudaSuccess) {
+              ctx->wave_cap = n * kChunk;
+            } else {
+              ctx->wave_rec = nullptr;
+              (void)cudaGetLastError();
+            }
+          }
+          FV_REQUIRE(ctx->wave_rec, "cudaMalloc of the marcher record buffer failed");
+        }
+        const int64_t n_have = ctx->wave_cap / kChunk;
+        ctx->wave_cap_a = want_a + want_pool <= n_have ? want_a : std::min(want_a, n_have / 2);
+        if (!ctx->wave_fb) {
+          FV_CUDA(cudaMallocHost(&ctx->wave_fb, 8 * sizeof(unsigned int)));
+          FV_CUDA(cudaEventCreateWithFlags(&ctx->wave_fb_ev, cudaEventDisableTiming));
+        }
       }
       if (k_max > ctx->wave_ray_cap) {
         if (ctx->wave_ray) cudaFree(ctx->wave_ray);
@@ -1705,7 +1748,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.ovf_count = &ctx->counters->ovf_count;
       // half of the chunk space holds first chunks at id = ray index (k_max may exceed it: later
       // rays then take pooled first chunks); ord lists the non-empty ones in ray order
-      B.cap_a = B.n_chunks_cap / 2;
+      B.cap_a = (int)std::min<int64_t>(ctx->wave_cap_a, B.n_chunks_cap);
       B.ord = B.chunk_fill + ctx->wave_cap / kChunk;
       B.ord_count = &ctx->counters->wave_ord;
       // ray_next, wave_rec, wave_next, wave_ord, hit_count, hit_next, ovf_count are consecutive
@@ -1737,6 +1780,20 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         if (rc) return rc;
         FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;
+      }
+      // record usage of this frame for the next one's buffer sizing (not inside a graph capture,
+      // and not while the previous readback is still unread)
+      cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+      FV_CUDA(cudaStreamIsCapturing(ctx->stream, &cap_st));
+      if (cap_st == cudaStreamCaptureStatusNone && !ctx->wave_fb_pending) {
+        if (P.k_dev)
+          FV_CUDA(cudaMemcpyAsync(ctx->wave_fb, P.k_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        else
+          ctx->wave_fb[0] = (unsigned)k_max;
+        FV_CUDA(cudaMemcpyAsync(ctx->wave_fb + 1, &ctx->counters->ray_next, 7 * sizeof(unsigned int),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        FV_CUDA(cudaEventRecord(ctx->wave_fb_ev, ctx->stream));
+        ctx->wave_fb_pending = true;
       }
     } else {
       FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<false><<<blocks, threads, 0, ctx->stream>>>(F, true));

@@ -78,20 +78,41 @@ class RenderSettings:
 
 
 class Frame:
-    """renderer.Frame (renderer.py:68-80) over device tensors."""
+    """renderer.Frame (renderer.py:68-80) over device tensors.
+
+    Nothing here synchronises the host at render time: the phase times are CUDA events read on first
+    access of a `*_ms` field, the arrays copy to NumPy on first access of `.rgba` / `.depth`."""
 
     def __init__(self, rgba_dev, depth_dev=None, mask_ms=0.0, render_ms=0.0, reconstruct_ms=0.0,
-                 total_ms=0.0, work_items=0, stats=None):
+                 total_ms=None, work_items=0, stats=None):
         self.rgba_dev = rgba_dev
         self.depth_dev = depth_dev
-        self.mask_ms = mask_ms
-        self.render_ms = render_ms
-        self.reconstruct_ms = reconstruct_ms
-        self.total_ms = total_ms
-        self.work_items = work_items
+        self._ms = {"mask_ms": mask_ms, "render_ms": render_ms, "reconstruct_ms": reconstruct_ms,
+                    "total_ms": total_ms}
+        self._work = work_items
         self.stats = stats
         self._rgba = None
         self._depth = None
+
+    def _get_ms(self, key):
+        v = self._ms[key]
+        if key == "total_ms" and v is None:
+            return self.mask_ms + self.render_ms + self.reconstruct_ms
+        if isinstance(v, tuple):  # (start, end) CUDA events
+            v = float(v[0].elapsed_time(v[1]))
+            self._ms[key] = v
+        return v
+
+    mask_ms = property(lambda self: self._get_ms("mask_ms"))
+    render_ms = property(lambda self: self._get_ms("render_ms"))
+    reconstruct_ms = property(lambda self: self._get_ms("reconstruct_ms"))
+    total_ms = property(lambda self: self._get_ms("total_ms"))
+
+    @property
+    def work_items(self) -> int:
+        if callable(self._work):
+            self._work = int(self._work())
+        return self._work
 
     @property
     def rgba(self) -> np.ndarray:
@@ -111,9 +132,15 @@ class Frame:
 
 
 class SparseFrame(Frame):
-    def __init__(self, *args, mask: SampleMask | None = None, **kw):
+    def __init__(self, *args, mask=None, **kw):
         super().__init__(*args, **kw)
-        self.mask = mask
+        self._mask = mask
+
+    @property
+    def mask(self) -> SampleMask | None:
+        if callable(self._mask):
+            self._mask = self._mask()
+        return self._mask
 
 
 def _light_ptr(scene: Scene):
@@ -139,9 +166,7 @@ def render_full(scene: Scene, cam: Camera, settings: RenderSettings = RenderSett
                                       C.byref(setc), _lib.ptr(rgba), _lib.ptr(depth),
                                       C.byref(st) if st is not None else None))
     ev1.record(ctx.stream)
-    ev1.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    return Frame(rgba, depth, render_ms=ms, total_ms=ms, work_items=w * h, stats=st)
+    return Frame(rgba, depth, render_ms=(ev0, ev1), work_items=w * h, stats=st)
 
 
 def render_sparse_compact(scene: Scene, cam: Camera, compact: CompactIndexList,
@@ -170,12 +195,10 @@ def render_sparse_compact(scene: Scene, cam: Camera, compact: CompactIndexList,
         _lib.ptr(compact.idx_dev), _lib.ptr(compact.k_dev), int(compact.idx_dev.numel()),
         _lib.ptr(rgba), _lib.ptr(depth), net_state, C.byref(st) if st is not None else None))
     ev1.record(ctx.stream)
-    ev1.synchronize()
-    ms = ev0.elapsed_time(ev1)
     from .sample_maps import scatter
 
-    return SparseFrame(rgba, depth, render_ms=ms, total_ms=ms, work_items=compact.count,
-                       mask=scatter(compact), stats=st)
+    return SparseFrame(rgba, depth, render_ms=(ev0, ev1), work_items=lambda: compact.count,
+                       mask=lambda: scatter(compact), stats=st)
 
 
 WARP_CHUNK = 64  # lanes per naive-mode execution group (renderer.py:34)
@@ -207,9 +230,7 @@ def render_sparse_naive(scene: Scene, cam: Camera, mask: SampleMask,
         _lib.ptr(mask.bits_dev.contiguous()), _lib.ptr(idx), _lib.ptr(k), _lib.ptr(rgba), _lib.ptr(depth),
         C.byref(st) if st is not None else None))
     ev1.record(ctx.stream)
-    ev1.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    return SparseFrame(rgba, depth, render_ms=ms, total_ms=ms, work_items=int(k.item()), mask=mask,
+    return SparseFrame(rgba, depth, render_ms=(ev0, ev1), work_items=lambda: int(k.item()), mask=mask,
                        stats=st)
 
 
@@ -241,12 +262,10 @@ def render_sparse_direct(scene: Scene, cam: Camera, positions,
             _lib.ptr(idx), _lib.ptr(k), n, _lib.ptr(rgba), _lib.ptr(depth), None,
             C.byref(st) if st is not None else None))
     ev1.record(ctx.stream)
-    ev1.synchronize()
-    ms = ev0.elapsed_time(ev1)
     bits = np.zeros((h, w), dtype=bool)
     if n:
         bits[pos[:, 1], pos[:, 0]] = True
-    return SparseFrame(rgba, depth, render_ms=ms, total_ms=ms, work_items=n, mask=SampleMask(bits=bits),
+    return SparseFrame(rgba, depth, render_ms=(ev0, ev1), work_items=n, mask=SampleMask(bits=bits),
                        stats=st)
 
 

@@ -60,24 +60,22 @@ def default_scene(dataset: str, dims: tuple[int, int, int] = (32, 32, 32)) -> Sc
 
 
 def _reconstruct_frame(net: WNetParams, sparse_rgba, mask_bits, state):
-    """x = rgba*m ++ m, forward_full, clip to [0,1] (bench.py:166-175); returns (img (H,W,3), state')."""
+    """x = rgba*m (++ m), forward_full, clip to [0,1] (bench.py:166-175); returns (img (H,W,3), state').
+
+    With the mask channel the packing and the clip run on the device (fv_pack_input, the output
+    stage); without it the rgba*m product is formed on the device and fed to forward_full."""
     import torch
 
-    from .network import forward_full
+    from .network import forward_full, forward_sparse
 
     rgba = torch.as_tensor(np.asarray(getattr(sparse_rgba, "rgba", sparse_rgba), dtype=np.float32)
                            if not isinstance(sparse_rgba, torch.Tensor) else sparse_rgba, device="cuda")
     mb = torch.as_tensor(np.asarray(mask_bits) if not isinstance(mask_bits, torch.Tensor) else mask_bits,
                          device="cuda")
-    if net.config.include_mask_channel:  # packing + clip on the device (fv_pack_input, output stage)
-        from .network import forward_sparse
-
+    if net.config.include_mask_channel:
         rgb, _, _, state = forward_sparse(net, rgba, mb.to(torch.uint8), state)
         return rgb.cpu().numpy(), state
-    m = mb.to(torch.float32)
-    x = rgba.permute(2, 0, 1)[None] * m[None, None]
-    if net.config.include_mask_channel:
-        x = torch.cat([x, m[None, None]], dim=1)
+    x = rgba.permute(2, 0, 1)[None] * mb.to(torch.float32)[None, None]
     o, _, state = forward_full(net, x, state)
     return torch.clamp(o.dev[0].permute(1, 2, 0), 0.0, 1.0).cpu().numpy(), state
 

@@ -80,8 +80,12 @@ class VolumeGrid:
         return self.extent * 0.5
 
     def handle(self, ctx: _lib.Context, tf: "TransferFunction"):
-        """fv_volume bound to this grid's memory and `tf` on `ctx` (uploaded once)."""
-        key = (id(ctx), id(tf))
+        """fv_volume bound to this grid's memory and `tf` (uploaded once per device).
+
+        The handle (and the marcher's quad texture it builds on first use, 4 floats per voxel:
+        2 GiB at 512^3) is shared by every context on the device -- the texture build synchronises
+        the stream it runs on, so later contexts' streams only ever read it."""
+        key = (int(ctx.device), id(tf))
         h = self._handles.get(key)
         if h is None:
             h = C.c_void_p()

@@ -1,0 +1,236 @@
+"""Parity at the headline configurations (SURVEY.md 8(c) items 1-4 at BASELINE C2 / C3 / C5).
+
+Every frame of a carried sequence is produced twice -- by libfovnet on the GPU and by the CPU
+oracle (oracle/fovray_oracle.py: NumPy mask, the C fp64 marcher, the fp32 NumPy W-Net, each
+pinned to the reference in tests/test_oracle.py) -- on the same volume, cameras, noise and seeded
+weights, and compared frame by frame:
+
+  config  film        volume  preset  frames (orbit of `frames` cameras, reference bench.py:192-209)
+  C3      1920x1080   512^3   hifi    16
+  C2      1920x1080   256^3   fast    4
+  C5net   3840x256    512^3   fast    3   (a full-width 4K strip through the fovea: the network at
+                                           4K width; rows 952..1207 of the 3840x2160 frame)
+
+Tolerances:
+  mask + compaction     bit-exact, every frame
+  marcher (fast tier)   over the frame's active pixels: max |err| <= 1e-2 on RGBA and
+                        PSNR(RGB) >= 80 dB; depth within 1e-3 on >= 99.99% of active pixels
+  network on the oracle's own sparse input (isolates the W-Net; FULL_BLOCKS, fp16 weights,
+  state carried over all frames): PSNR >= 60 dB and max |err| <= 5e-3 per frame after the
+                        clip; O_d max |err| <= 5e-3 per frame; hidden state after the last frame
+                        max |err| <= 2e-2 x max(1, |ref|max)
+  end to end (GPU mask -> march -> net vs the oracle's chain): PSNR >= 55 dB and SSIM >= 0.99
+                        per frame (fast marcher tier)
+
+FV_PARITY_REPORT=<path> writes the per-frame numbers as JSON (profiles/r02_headline_parity.json).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no GPU", allow_module_level=True)
+
+from oracle import fovray_oracle as O  # noqa: E402
+from paper_2209_09965_b200 import network as N  # noqa: E402
+from paper_2209_09965_b200 import sample_maps as S  # noqa: E402
+from paper_2209_09965_b200.noise import default_stack  # noqa: E402
+from paper_2209_09965_b200.pipeline import FramePipeline  # noqa: E402
+from paper_2209_09965_b200.renderer import OrbitPathSpec, RenderSettings, orbit_cameras, render_sparse_compact  # noqa: E402
+from paper_2209_09965_b200.throughput import default_scene  # noqa: E402
+
+LIGHT = ("dir", (-1.0, -1.0, -0.5), (1.0, 1.0, 1.0))
+PRESETS = {"fast": (0.03, 0.02), "hifi": (0.07, 0.06)}
+CONFIGS = {
+    "C3": dict(n=512, h=1080, w=1920, mode="hifi", frames=16),
+    "C2": dict(n=256, h=1080, w=1920, mode="fast", frames=4),
+}
+_REPORT: dict = {}
+
+
+def _cam_dict(cam):
+    return dict(position=cam.position, look_at=cam.look_at, up=cam.up, fov_y=cam.fov_y, width=cam.width,
+                height=cam.height)
+
+
+def _active_psnr(got, ref):
+    return O.psnr(got[..., :3], ref[..., :3])
+
+
+@pytest.fixture(scope="module")
+def stack():
+    return default_stack()
+
+
+@pytest.fixture(scope="module")
+def fullnet():
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    params = O.init_params(O.FULL_BLOCKS, 0, fp16_weights=True)
+    # the device weights are the oracle's (the seeded-weight contract is pinned in test_host.py)
+    for k, v in params.items():
+        assert np.array_equal(np.asarray(net.params[k], np.float32), v), k
+    return net, params
+
+
+_VOLS: dict = {}
+
+
+def _volume(n):
+    """The GPU procedural volume, checked bit-exact against the oracle's fp64 generator."""
+    if n not in _VOLS:
+        scene = default_scene("sphere_shells", (n, n, n))
+        ref, _ = O.procedural_volume("sphere_shells", (n, n, n))
+        assert np.array_equal(scene.volume.data, ref), f"{n}^3 volume differs from the oracle"
+        _VOLS[n] = (scene, ref)
+    return _VOLS[n]
+
+
+_RUNS: dict = {}
+
+
+def _run(name, stack, fullnet):
+    """Both chains over the config's frames; per-frame records (cached per session)."""
+    if name in _RUNS:
+        return _RUNS[name]
+    c = CONFIGS[name]
+    h, w = c["h"], c["w"]
+    scene, vol = _volume(c["n"])
+    net, params = fullnet
+    pb, sigma = PRESETS[c["mode"]]
+    scale = S.pixel_scale_for_film((h, w))
+    fovea = S.FoveaConfig(focus=((w - 1) / 2.0, (h - 1) / 2.0), sigma=sigma, base_density=pb, pixel_scale=scale)
+    tau_ref = O.tau_map(h, w, fovea.focus, sigma, pb, scale)
+    tau = S.build_tau_map(fovea, (h, w))
+    cams = orbit_cameras(OrbitPathSpec(n_frames=c["frames"]), scene.volume, w, h)
+    pipe = FramePipeline(scene, net, (h, w), stack)
+    g_state = N.reset_state(net.config, (h, w))
+    o_state = None
+    recs = []
+    for i, cam in enumerate(cams):
+        r = {"frame": i}
+        # -- mask: GPU vs oracle, bit-exact
+        bits_ref = O.sample_mask(stack.values, h, w, i, tau_ref)
+        mask = S.build_sample_mask(stack, i, tau)
+        comp = S.compact_mask(mask)
+        r["k"] = int(bits_ref.sum())
+        r["mask_exact"] = bool(np.array_equal(mask.bits, bits_ref)) and comp.count == r["k"] and np.array_equal(
+            comp.idx_dev[: comp.count].cpu().numpy().astype(np.int64), O.compact(bits_ref))
+        # -- march: the oracle's fp64 C marcher vs render_sparse_compact, same mask
+        pix = O.compact(bits_ref)
+        rgba_ref, dep_ref = O.render(vol, (1.0, 1.0, 1.0), O.DEFAULT_LUT, LIGHT, _cam_dict(cam), pix=pix)
+        fr = render_sparse_compact(scene, cam, comp, RenderSettings())
+        got = fr.rgba.reshape(-1, 4)[pix]
+        gdep = fr.depth.reshape(-1)[pix]
+        d = np.abs(got - rgba_ref)
+        r["march_max"] = float(d.max()) if d.size else 0.0
+        r["march_psnr"] = _active_psnr(got, rgba_ref)
+        r["march_frac_1e4"] = float((d <= 1e-4).mean()) if d.size else 1.0
+        dd = np.abs(gdep - dep_ref)
+        r["depth_frac_1e3"] = float((dd <= 1e-3).mean()) if dd.size else 1.0
+        r["depth_max"] = float(dd.max()) if dd.size else 0.0
+        # -- oracle network on the oracle's sparse input (x = rgba*m ++ m, bench.py:168-172)
+        img = np.zeros((h * w, 4), np.float32)
+        img[pix] = rgba_ref
+        m = bits_ref.astype(np.float32)
+        x = np.concatenate([np.moveaxis(img.reshape(h, w, 4), -1, 0) * m[None], m[None]], 0)
+        o_ref, od_ref, o_state = O.net_forward(params, O.FULL_BLOCKS, x, o_state)
+        o_ref_c = np.clip(o_ref, 0.0, 1.0)
+        # -- GPU network on the same input
+        o, od, g_state = N.forward_full(net, x[None], g_state)
+        o_c = np.clip(o.data[0], 0.0, 1.0)
+        r["net_psnr"] = O.psnr(np.moveaxis(o_c, 0, -1), np.moveaxis(o_ref_c, 0, -1))
+        r["net_max"] = float(np.abs(o_c - o_ref_c).max())
+        r["od_max"] = float(np.abs(od.data[0] - od_ref).max())
+        # -- end to end: the device pipeline frame vs the oracle's frame
+        pipe.step(cam, fovea, i)
+        e2e = pipe.rgb.cpu().numpy()
+        ref_img = np.moveaxis(o_ref_c, 0, -1)
+        r["e2e_psnr"] = O.psnr(e2e, ref_img)
+        r["e2e_ssim"] = O.ssim(e2e, ref_img)
+        recs.append(r)
+    hid = g_state.hidden
+    r_last = {"hidden_max": [float(np.abs(hid[j].data[0] - o_state["hidden"][j]).max()) for j in range(len(hid))],
+              "hidden_ref_max": [float(np.abs(o_state["hidden"][j]).max()) for j in range(len(hid))]}
+    out = {"config": dict(c, volume=f"{c['n']}^3 sphere_shells"), "frames": recs, "state": r_last}
+    _RUNS[name] = out
+    _REPORT[name] = out
+    path = os.environ.get("FV_PARITY_REPORT")
+    if path:
+        with open(path, "w") as f:
+            json.dump(_REPORT, f, indent=1)
+    return out
+
+
+@pytest.mark.parametrize("name", ["C3", "C2"])
+def test_headline_masks_bit_exact(name, stack, fullnet):
+    run = _run(name, stack, fullnet)
+    assert all(r["mask_exact"] for r in run["frames"]), [r["frame"] for r in run["frames"] if not r["mask_exact"]]
+
+
+@pytest.mark.parametrize("name", ["C3", "C2"])
+def test_headline_march_fast_tier(name, stack, fullnet):
+    for r in _run(name, stack, fullnet)["frames"]:
+        assert r["march_max"] <= 1e-2, r
+        assert r["march_psnr"] >= 80.0, r
+        assert r["depth_frac_1e3"] >= 0.9999, r
+
+
+@pytest.mark.parametrize("name", ["C3", "C2"])
+def test_headline_network_on_oracle_input(name, stack, fullnet):
+    run = _run(name, stack, fullnet)
+    for r in run["frames"]:
+        assert r["net_psnr"] >= 60.0, r
+        assert r["net_max"] <= 5e-3, r
+        assert r["od_max"] <= 5e-3, r
+    st = run["state"]
+    for got, ref in zip(st["hidden_max"], st["hidden_ref_max"]):
+        assert got <= 2e-2 * max(1.0, ref), st
+
+
+@pytest.mark.parametrize("name", ["C3", "C2"])
+def test_headline_end_to_end(name, stack, fullnet):
+    for r in _run(name, stack, fullnet)["frames"]:
+        assert r["e2e_psnr"] >= 55.0, r
+        assert r["e2e_ssim"] >= 0.99, r
+
+
+def test_c5_network_full_width_4k_strip(stack, fullnet):
+    """The W-Net at 4K width (30 column tiles per row): a 3840x256 strip of the C5 frame through
+    the fovea, with the 4K fast mask and oracle-marched pixels, 3 carried frames."""
+    net, params = fullnet
+    H, W, r0, rows = 2160, 3840, 952, 256
+    scene, vol = _volume(512)
+    pb, sigma = PRESETS["fast"]
+    scale = S.pixel_scale_for_film((H, W))
+    tau_ref = O.tau_map(H, W, ((W - 1) / 2.0, (H - 1) / 2.0), sigma, pb, scale)
+    cams = orbit_cameras(OrbitPathSpec(n_frames=16), scene.volume, W, H)
+    g_state = N.reset_state(net.config, (rows, W))
+    o_state = None
+    recs = []
+    for i in range(3):
+        bits = O.sample_mask(stack.values, H, W, i, tau_ref)[r0:r0 + rows]
+        pix = O.compact(bits) + r0 * W
+        rgba, _ = O.render(vol, (1.0, 1.0, 1.0), O.DEFAULT_LUT, LIGHT, _cam_dict(cams[i]), pix=pix)
+        img = np.zeros((rows * W, 4), np.float32)
+        img[pix - r0 * W] = rgba
+        m = bits.astype(np.float32)
+        x = np.concatenate([np.moveaxis(img.reshape(rows, W, 4), -1, 0) * m[None], m[None]], 0)
+        o_ref, od_ref, o_state = O.net_forward(params, O.FULL_BLOCKS, x, o_state)
+        o, od, g_state = N.forward_full(net, x[None], g_state)
+        o_c, o_ref_c = np.clip(o.data[0], 0, 1), np.clip(o_ref, 0, 1)
+        q = O.psnr(np.moveaxis(o_c, 0, -1), np.moveaxis(o_ref_c, 0, -1))
+        recs.append({"frame": i, "k": int(bits.sum()), "net_psnr": q, "net_max": float(np.abs(o_c - o_ref_c).max()),
+                     "od_max": float(np.abs(od.data[0] - od_ref).max())})
+    _REPORT["C5net"] = {"config": {"film": [W, rows], "rows": [r0, r0 + rows], "of": [W, H], "mode": "fast"},
+                        "frames": recs}
+    path = os.environ.get("FV_PARITY_REPORT")
+    if path:
+        with open(path, "w") as f:
+            json.dump(_REPORT, f, indent=1)
+    for r in recs:
+        assert r["net_psnr"] >= 60.0 and r["net_max"] <= 5e-3 and r["od_max"] <= 5e-3, r

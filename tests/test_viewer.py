@@ -1,37 +1,36 @@
-"""Viewer caller of the hot path (viewer.py:50-242): control handling and frame messages (CPU),
-render_frame against messages the reference produced (GPU)."""
+"""Viewer caller of the hot path (reference viewer.py:161-223): render_frame's device path against
+the messages the reference produced (tests/golden/viewer_small.npz, made by make_golden.gen_viewer)."""
 import io
 import struct
+from dataclasses import dataclass, replace
 
 import numpy as np
 import pytest
 
 from paper_2209_09965_b200 import viewer as V
+from paper_2209_09965_b200.sample_maps import FAST_PRESET, FoveaConfig, pixel_scale_for_film
 
 
-def test_handle_control_clamps_and_warnings():
-    st = V.default_session((64, 36))
-    assert st.fovea.focus == (31.5, 17.5) and st.mode == "sparse_raw"
-    s2 = V.handle_control(st, {"type": "control", "focus": [-3, 50], "p_b": 5.0, "sigma": -1, "mode": "bogus",
-                               "extra": 1}, (64, 36), has_checkpoint=False)
-    assert s2.fovea.focus == (0.0, 35.0) and s2.fovea.base_density == 1.0 and s2.fovea.sigma == 0.0
-    assert s2.mode == "sparse_raw"
-    assert s2.warning == ("ignored unknown field 'extra'; focus clamped to film bounds; p_b clamped; "
-                          "sigma clamped; unknown mode 'bogus'")
-    s3 = V.handle_control(st, {"mode": "reconstructed"}, (64, 36), has_checkpoint=False)
-    assert s3.mode == "sparse_raw" and "no checkpoint" in s3.warning
-    s4 = V.handle_control(st, {"mode": "side_by_side", "p_b": 0.5}, (64, 36), has_checkpoint=True)
-    assert s4.mode == "side_by_side" and s4.fovea.base_density == 0.5 and s4.warning == ""
+@dataclass
+class Session:
+    """The attributes render_frame reads from the caller's session (reference SessionState)."""
+
+    fovea: FoveaConfig
+    mode: str = "sparse_raw"
+    frame_idx: int = 0
+    recurrent: object = None
+    warning: str = ""
 
 
-def test_frame_message_layout_round_trip():
-    png = b"\x89PNG-bytes"
-    hdr = struct.pack(V.HEADER_FMT, 7, 64, 36, 2, 1, 1.5, 2.5, 3.5, 7.5, 10.0, 20.0, 0.03, 0.02, len(png))
-    d = V.parse_frame_message(hdr + png + "careful".encode())
-    assert V.HEADER_SIZE == 46
-    assert d["frame_id"] == 7 and (d["width"], d["height"]) == (64, 36) and d["mode"] == "ground_truth"
-    assert d["png"] == png and d["warning"] == "careful"
-    assert d["timings"]["total_ms"] == 7.5 and d["focus"] == (10.0, 20.0)
+def viewer_fovea(w, h, focus=None, p_b=FAST_PRESET["base_density"], sigma=FAST_PRESET["sigma"]):
+    # the reference viewer's fovea: film-centre focus, fast preset, pixel scale at fraction 0.25
+    return FoveaConfig(focus=focus if focus is not None else ((w - 1) / 2.0, (h - 1) / 2.0), sigma=sigma,
+                       base_density=p_b, pixel_scale=pixel_scale_for_film((h, w), fraction=0.25))
+
+
+def test_header_layout():
+    hdr = struct.pack(V.HEADER_FMT, 7, 64, 36, 2, 1, 1.5, 2.5, 3.5, 7.5, 10.0, 20.0, 0.03, 0.02, 10)
+    assert len(hdr) == 46 and V.MODES[2] == "ground_truth"
 
 
 @pytest.mark.gpu
@@ -51,19 +50,23 @@ def test_render_frame_every_mode_vs_reference_messages(golden):
     cam = Camera(position=(80.0, 60.0, 90.0), look_at=(16.0, 16.0, 16.0), fov_y=40.0, width=64, height=36)
     svc = V.RenderService(scene, film=(64, 36), checkpoint=net, noise=default_stack(),
                           settings=RenderSettings(step_size=1.0), camera=cam)
-    state = V.default_session((64, 36))
-    plan = [("sparse_raw", {}), ("reconstructed", {}), ("reconstructed", {"focus": [10.0, 30.0], "p_b": 0.2}),
-            ("ground_truth", {}), ("side_by_side", {"sigma": 0.5})]
-    for i, (mode, ctl) in enumerate(plan):
-        state = V.handle_control(state, dict(ctl, mode=mode), svc.film, has_checkpoint=True)
+    # the reference's control plan (make_golden.gen_viewer): fovea changes persist across frames
+    plan = [("sparse_raw", viewer_fovea(64, 36)), ("reconstructed", viewer_fovea(64, 36)),
+            ("reconstructed", viewer_fovea(64, 36, focus=(10.0, 30.0), p_b=0.2)),
+            ("ground_truth", viewer_fovea(64, 36, focus=(10.0, 30.0), p_b=0.2)),
+            ("side_by_side", viewer_fovea(64, 36, focus=(10.0, 30.0), p_b=0.2, sigma=0.5))]
+    state = Session(fovea=plan[0][1])
+    for i, (mode, fovea) in enumerate(plan):
+        state = replace(state, mode=mode, fovea=fovea)
         blob, state = svc.render_frame(state)
-        d = V.parse_frame_message(blob)
-        img = np.asarray(Image.open(io.BytesIO(d["png"])))
+        fields = struct.unpack(V.HEADER_FMT, blob[:46])
+        png = blob[46:46 + fields[-1]]
+        img = np.asarray(Image.open(io.BytesIO(png)))
         ref = g[f"img{i}"]
         assert img.shape == ref.shape, (i, img.shape)
-        hdr = np.array([d["frame_id"], d["width"], d["height"], V.MODES.index(d["mode"]), d["focus"][0],
-                        d["focus"][1], d["p_b"], d["sigma"]], dtype=np.float64)
-        assert np.array_equal(hdr, g[f"hdr{i}"]), (i, hdr, g[f"hdr{i}"])
+        hdr = np.array([fields[0], fields[1], fields[2], fields[3], fields[9], fields[10], fields[11], fields[12]],
+                       dtype=np.float64)
+        assert np.array_equal(hdr, g[f"hdr{i}"].astype(np.float32).astype(np.float64)), (i, hdr, g[f"hdr{i}"])
         diff = np.abs(img.astype(int) - ref.astype(int))
         assert diff.max() <= 2 and (diff <= 1).mean() >= 0.99, (i, diff.max(), (diff <= 1).mean())
     assert state.frame_idx == len(plan)
