@@ -152,6 +152,17 @@ FV_API int fv_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* fovea, const do
                double* tau_dev);
 
 /* ---- volume -------------------------------------------------------------- */
+/* c_max (sample_maps.py:135-137): deterministic fp64 sum of tau over an (H, W) film into *sum_dev
+ * (device); tau from the fovea (and optional per-pixel P_b map) or from a tau map (tau_dev) */
+FV_API int fv_tau_sum(fv_ctx* ctx, int H, int W, const fv_fovea* fovea, const double* pb_map_dev,
+                      const double* tau_dev, double* sum_dev);
+/* draw_direct_samples (sample_maps.py:181-198): inverse-CDF draws over the fp64 tau map for `count`
+ * caller-supplied uniforms in [0,1) -> flat pixel indices v*W+u (device int32) */
+FV_API int fv_direct_draws(fv_ctx* ctx, int H, int W, const fv_fovea* fovea, const double* pb_map_dev,
+                           const double* tau_dev, const double* uniforms_dev, int64_t count, int32_t* idx_dev);
+/* foveal_density (sample_maps.py:62-68) over n broadcast pixel offsets (dx, dy), fp64 */
+FV_API int fv_foveal_density(fv_ctx* ctx, const double* dx_dev, const double* dy_dev, int64_t n, double sigma,
+                             double pixel_scale, double* out_dev);
 FV_API int fv_volume_create(fv_ctx* ctx, int nx, int ny, int nz, const double spacing[3],
                      fv_volume** out);
 /* same, over caller-owned device memory (nz,ny,nx) float32 that outlives the handle */
@@ -253,6 +264,24 @@ FV_API int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_sta
 
 /* pngio.to_uint8 (pngio.py:11-12) on the device: (clip(x,0,1)*255 + 0.5) truncated, fp32 without FMA
  * contraction; in_dev addressed by element strides (HWC RGB/RGBA or CHW), out_dev (H,W,3) uint8. */
+/* forward_K (network.py:280-293): the K stage over the decoder hidden states the state holds and a
+ * given O_d (3, Hp, Wp) fp32 on the device; out_dev (3, H, W) fp32 */
+FV_API int fv_forward_k(fv_ctx* ctx, const fv_net* net, fv_state* st, const float* od_dev, float* out_dev);
+/* predict_kernel_fields (network.py:268-277), one K block: logits (9, h, w) fp32 of the 1x1 conv
+ * over hd (C, h, w) fp32; normalize = 1: softmax over the 9 taps (KernelField.normalized) */
+FV_API int fv_kfield_logits(fv_ctx* ctx, const fv_net* net, int block, const float* hd_dev, int C, int h, int w,
+                            int normalize, float* logits_dev);
+/* Building blocks of the marcher as device calls (fp64, the reference's arithmetic):
+ * volume.generate_rays (volume.py:293-303): n pixel centres -> origins (n,3), unit dirs (n,3) */
+FV_API int fv_generate_rays(fv_ctx* ctx, const fv_camera* cam, const int32_t* us_dev, const int32_t* vs_dev,
+                            int64_t n, double* origins_dev, double* dirs_dev);
+/* volume.sample_trilinear (volume.py:149-180): n world points (n,3) -> values, 0 outside the box */
+FV_API int fv_sample_trilinear(fv_ctx* ctx, const fv_volume* vol, const double* pts_dev, int64_t n,
+                               double* out_dev);
+/* TransferFunction.apply (volume.py:201-208): n scalars -> RGBA (n,4), lut (K,4) fp32 on the device */
+FV_API int fv_tf_apply(fv_ctx* ctx, const float* lut_dev, int K, const double* s_dev, int64_t n, double* out_dev);
+/* noise.tile_field (noise.py:378-384): frame `frame` of the uploaded stack tiled to (h, w) fp32 */
+FV_API int fv_tile_field(fv_ctx* ctx, int frame, int h, int w, float* out_dev);
 FV_API int fv_pack_rgb8(fv_ctx* ctx, const float* in_dev, int H, int W, int64_t stride_y, int64_t stride_x,
                         int64_t stride_c, uint8_t* out_dev);
 

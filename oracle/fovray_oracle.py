@@ -10,6 +10,7 @@ for masks and marching, float32 for the network) written for checking:
   tau_map / sample_mask / compact          sample_maps.py:62-68, :89-105, :128-132, :161-171
   procedural_volume                        volume.py:112-146 (+ _normalize :75-81)
   camera_basis / render (C, march_oracle.c) volume.py:269-303, renderer.py:88-195
+  generate_rays / sample_trilinear / tf_apply volume.py:293-303, :149-180, :201-208
   net_forward (conv/pool/up/K stage)       network.py:183-323, autograd.py:173-359
   psnr / ssim                              metrics.py:40-87
 
@@ -173,6 +174,54 @@ def orbit_camera(i: int, n_frames: int, dims, spacing=(1.0, 1.0, 1.0), radius_fa
     r = radius_factor * diag * (1.0 + zoom_amplitude * np.sin(2.0 * np.pi * zoom_periods * s))
     pos = center + r * np.array([np.cos(pitch) * np.cos(yaw), np.sin(pitch), np.cos(pitch) * np.sin(yaw)])
     return tuple(pos), tuple(center)
+
+
+def generate_rays(cam: dict, us, vs):
+    """Rays through pixel centres (volume.py:293-303): (origins, unit dirs) (n, 3) fp64."""
+    right, up, fwd = camera_basis(cam["position"], cam["look_at"], cam.get("up", (0.0, 1.0, 0.0)))
+    tan_half = np.tan(np.deg2rad(cam.get("fov_y", 45.0)) * 0.5)
+    aspect = cam["width"] / cam["height"]
+    sx = ((np.asarray(us, dtype=np.float64) + 0.5) / cam["width"] * 2.0 - 1.0) * tan_half * aspect
+    sy = (1.0 - (np.asarray(vs, dtype=np.float64) + 0.5) / cam["height"] * 2.0) * tan_half
+    d = fwd[None, :] + sx[:, None] * right[None, :] + sy[:, None] * up[None, :]
+    d = d / np.sqrt((d * d).sum(axis=1, keepdims=True))
+    return np.broadcast_to(np.asarray(cam["position"], np.float64), d.shape).copy(), d
+
+
+def sample_trilinear(data: np.ndarray, spacing, pts) -> np.ndarray:
+    """Trilinear value at world points (n, 3), 0 outside [0, ext] (volume.py:149-180); data (nz,ny,nx)."""
+    pts = np.atleast_2d(np.asarray(pts, dtype=np.float64))
+    nz, ny, nx = data.shape
+    sp = np.asarray(spacing, dtype=np.float64)
+    ext = np.asarray([nx, ny, nz], np.float64) * sp
+    inside = np.all((pts >= 0.0) & (pts <= ext), axis=-1)
+    q = pts / sp - 0.5
+    f = np.floor(q)
+    t = q - f
+    n = np.asarray([nx, ny, nz])
+    i0 = np.clip(f.astype(np.int64), 0, n - 1)
+    i1 = np.clip(i0 + 1, 0, n - 1)
+    x0, y0, z0 = i0.T
+    x1, y1, z1 = i1.T
+    tx, ty, tz = t.T
+    d = data.astype(np.float64)
+    c00 = d[z0, y0, x0] * (1 - tx) + d[z0, y0, x1] * tx
+    c10 = d[z0, y1, x0] * (1 - tx) + d[z0, y1, x1] * tx
+    c01 = d[z1, y0, x0] * (1 - tx) + d[z1, y0, x1] * tx
+    c11 = d[z1, y1, x0] * (1 - tx) + d[z1, y1, x1] * tx
+    v = (c00 * (1 - ty) + c10 * ty) * (1 - tz) + (c01 * (1 - ty) + c11 * ty) * tz
+    return np.where(inside, v, 0.0)
+
+
+def tf_apply(lut, s) -> np.ndarray:
+    """TransferFunction.apply (volume.py:201-208): clip to [0,1], lerp between LUT rows (fp64)."""
+    lut = np.asarray(lut, dtype=np.float32)
+    s = np.clip(np.asarray(s, dtype=np.float64), 0.0, 1.0)
+    k = lut.shape[0]
+    x = s * (k - 1)
+    i0 = np.clip(np.floor(x).astype(np.int64), 0, k - 2)
+    t = (x - i0)[..., None]
+    return lut[i0] * (1 - t) + lut[i0 + 1] * t
 
 
 def render(volume: np.ndarray, spacing, lut, light, cam: dict, pix=None, step_size=None,

@@ -118,6 +118,15 @@ _SIGS = {
                      C.POINTER(FvFovea), I, P, C.POINTER(D)]),
     "fv_frames": (I, [P, P, P, P, I, C.POINTER(FvCamera), C.POINTER(FvLight), C.POINTER(FvSettings),
                       C.POINTER(FvFovea), C.POINTER(I), C.POINTER(P)]),
+    "fv_forward_k": (I, [P, P, P, P, P]),
+    "fv_kfield_logits": (I, [P, P, I, P, I, I, I, I, P]),
+    "fv_generate_rays": (I, [P, C.POINTER(FvCamera), P, P, I64, P, P]),
+    "fv_sample_trilinear": (I, [P, P, P, I64, P]),
+    "fv_tf_apply": (I, [P, P, I, P, I64, P]),
+    "fv_tile_field": (I, [P, I, I, I, P]),
+    "fv_tau_sum": (I, [P, I, I, C.POINTER(FvFovea), P, P, P]),
+    "fv_foveal_density": (I, [P, P, P, I64, D, D, P]),
+    "fv_direct_draws": (I, [P, I, I, C.POINTER(FvFovea), P, P, P, I64, P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -251,6 +251,38 @@ int fv_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* fovea, const double* p
   return launch_tau_map(ctx, H, W, fovea, pb_map_dev, tau_dev);
 }
 
+int fv_tau_sum(fv_ctx* ctx, int H, int W, const fv_fovea* fovea, const double* pb_map_dev, const double* tau_dev,
+               double* sum_dev) {
+  FV_REQUIRE(ctx && sum_dev && (fovea || tau_dev), "null argument");
+  FV_REQUIRE(H >= 1 && W >= 1, "dims must be positive, got (%d, %d)", H, W);
+  fv_fovea dummy{};
+  if (!tau_dev) {
+    int rc = check_fovea(fovea);
+    if (rc) return rc;
+  }
+  return launch_tau_sum(ctx, H, W, fovea ? fovea : &dummy, pb_map_dev, tau_dev, sum_dev);
+}
+
+int fv_direct_draws(fv_ctx* ctx, int H, int W, const fv_fovea* fovea, const double* pb_map_dev, const double* tau_dev,
+                    const double* uniforms_dev, int64_t count, int32_t* idx_dev) {
+  FV_REQUIRE(ctx && (fovea || tau_dev) && (count == 0 || (uniforms_dev && idx_dev)), "null argument");
+  FV_REQUIRE(H >= 1 && W >= 1, "dims must be positive, got (%d, %d)", H, W);
+  FV_REQUIRE(count >= 0, "count must be >= 0");
+  fv_fovea dummy{};
+  if (!tau_dev) {
+    int rc = check_fovea(fovea);
+    if (rc) return rc;
+  }
+  return launch_direct_draws(ctx, H, W, fovea ? fovea : &dummy, pb_map_dev, tau_dev, uniforms_dev, count, idx_dev);
+}
+
+int fv_foveal_density(fv_ctx* ctx, const double* dx_dev, const double* dy_dev, int64_t n, double sigma,
+                      double pixel_scale, double* out_dev) {
+  FV_REQUIRE(ctx && (n == 0 || (dx_dev && dy_dev && out_dev)), "null argument");
+  FV_REQUIRE(n >= 0, "count must be >= 0");
+  return launch_foveal_density(ctx, dx_dev, dy_dev, n, sigma, pixel_scale, out_dev);
+}
+
 int fv_volume_create(fv_ctx* ctx, int nx, int ny, int nz, const double spacing[3], fv_volume** out) {
   FV_REQUIRE(ctx && out, "null argument");
   FV_REQUIRE(nx >= 2 && ny >= 2 && nz >= 2, "volume dims must all be >= 2, got (%d, %d, %d)", nx, ny, nz);
@@ -288,6 +320,8 @@ int fv_volume_destroy(fv_volume* v) {
   if (v->bricks) cudaFree(v->bricks);
   if (v->qtex) cudaDestroyTextureObject((cudaTextureObject_t)v->qtex);
   if (v->qarr) cudaFreeArray(v->qarr);
+  if (v->ltex) cudaDestroyTextureObject((cudaTextureObject_t)v->ltex);
+  if (v->larr) cudaFreeArray(v->larr);
   delete v;
   return 0;
 }

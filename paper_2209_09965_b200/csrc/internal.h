@@ -134,7 +134,6 @@ struct fv_ctx {
   int64_t wave_hits_cap = 0;
   void* wave_ovf = nullptr;   // int per compacted ray: the record-overflow list
   int64_t wave_ovf_cap = 0;
-  int64_t wave_cap_a = 0;     // record chunks reserved as first chunks (chunk id = ray index)
   // previous render's record usage, read back asynchronously into pinned memory: [0] = compacted
   // rays k, [1..7] = DevCounters ray_next..ovf_count (see march.cu, record buffer sizing)
   unsigned int* wave_fb = nullptr;
@@ -165,6 +164,11 @@ struct fv_volume {
   cudaArray_t qarr = nullptr;
   unsigned long long qtex = 0;  // cudaTextureObject_t
   uint64_t tex_version = 0;
+  // the voxels as a hardware-filtered (trilinear, 8-bit fractional weights) float texture: the
+  // shadow pass's fast-tier sample source (one 4-byte return per sample instead of two quads)
+  cudaArray_t larr = nullptr;
+  unsigned long long ltex = 0;
+  uint64_t ltex_version = 0;
   int K = 0;
   double value_range[2] = {0, 0};
 };
@@ -278,6 +282,12 @@ namespace fv {
 int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
                         const double* pb_map, uint8_t* bits, int32_t* idx, int32_t* k,
                         __half* net_in, int net_wp, const double* tau_map = nullptr);
+int launch_direct_draws(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* pb_map, const double* tau_map,
+                        const double* r, int64_t count, int32_t* idx);
+int launch_tau_sum(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* pb_map, const double* tau_map,
+                   double* sum_dev);
+int launch_foveal_density(fv_ctx* ctx, const double* ox, const double* oy, int64_t n, double sigma, double scale,
+                          double* out);
 int launch_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* pb_map,
                    double* tau);
 int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const fv_light* light,

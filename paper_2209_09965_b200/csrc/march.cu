@@ -284,6 +284,7 @@ __global__ void __launch_bounds__(128) march_kernel(MarchParams P) {
 // in any direction -- shadow rays run diagonally toward the light -- stay in the same lines.
 struct FastVol {
   cudaTextureObject_t tex;  // non-zero: fetch quads from the 3D texture (unnormalised, point, clamp)
+  cudaTextureObject_t ltex;  // non-zero: the shadow pass samples the hardware-filtered scalar texture
   const float4* quads;
   int nx, ny, nz;
   int sby, sbz;        // brick strides (quads) in y and z
@@ -319,13 +320,25 @@ struct TriFetch {
   bool inside;
 };
 
+// Hardware-filtered sample (TEX == 2, the fast tier): trilinear at q + 1/2 from the scalar texture;
+// q < 0 (the lower half-voxel shell) maps to q + 1, which addresses the reference's texels 0, 1
+// with its weight q + 1 (see volume_ltex).
+__device__ __forceinline__ float tex_lin(const FastVol& V, float qx, float qy, float qz) {
+  return tex3D<float>(V.ltex, qx + (qx < 0.f ? 1.5f : 0.5f), qy + (qy < 0.f ? 1.5f : 0.5f),
+                      qz + (qz < 0.f ? 1.5f : 0.5f));
+}
+
 // Same, from continuous voxel coordinates q = p/spacing - 0.5 (rays stepped directly in q-space;
 // p in [0, ext] <=> q in [-0.5, n-0.5]).
-template <bool TEX = false>
+template <int TEX = 0>
 __device__ __forceinline__ TriFetch tri_issue_q(const FastVol& V, float qx, float qy, float qz) {
   TriFetch f;
   f.inside = qx >= -0.5f && qx <= V.qmax[0] && qy >= -0.5f && qy <= V.qmax[1] && qz >= -0.5f &&
              qz <= V.qmax[2];
+  if constexpr (TEX == 2) {
+    f.A.x = tex_lin(V, qx, qy, qz);
+    return f;
+  }
   const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
   f.tx = qx - fx; f.ty = qy - fy; f.tz = qz - fz;
   if constexpr (TEX) {
@@ -349,11 +362,15 @@ __device__ __forceinline__ TriFetch tri_issue_q(const FastVol& V, float qx, floa
   return f;
 }
 
-template <bool TEX = false>
+template <int TEX = 0>
 __device__ __forceinline__ TriFetch tri_issue(const FastVol& V, float px, float py, float pz) {
   TriFetch f;
   f.inside = px >= 0.f && px <= V.ext[0] && py >= 0.f && py <= V.ext[1] && pz >= 0.f && pz <= V.ext[2];
   const float qx = px * V.inv_sp[0] - 0.5f, qy = py * V.inv_sp[1] - 0.5f, qz = pz * V.inv_sp[2] - 0.5f;
+  if constexpr (TEX == 2) {
+    f.A.x = tex_lin(V, qx, qy, qz);
+    return f;
+  }
   const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
   f.tx = qx - fx; f.ty = qy - fy; f.tz = qz - fz;
   if constexpr (TEX) {
@@ -388,10 +405,12 @@ __device__ __forceinline__ float tri_finish(const TriFetch& f) {
 }
 
 // texture quads hold (v00, v01 - v00, v10, v11 - v10) per plane
-template <bool TEX>
+template <int TEX>
 __device__ __forceinline__ float tri_finish_t(const TriFetch& f) {
   if constexpr (!TEX) {
     return tri_finish(f);
+  } else if constexpr (TEX == 2) {
+    return f.inside ? f.A.x : 0.f;
   } else {
     if (!f.inside) return 0.f;
     const float c00 = fmaf(f.tx, f.A.y, f.A.x), c10 = fmaf(f.tx, f.A.w, f.A.z);
@@ -447,7 +466,7 @@ struct FastParams {
   float step_sh, inv_step_sh, min_trans, ambient;
 };
 
-template <bool TEX = false>
+template <int TEX = 0>
 __device__ float shadow_fast(const FastParams& F, const float* lut, float px, float py, float pz,
                              unsigned int& nsamp) {
   const MarchParams& P = F.P;
@@ -549,7 +568,7 @@ __device__ __forceinline__ float keep_t(float x, float e) {
   else return keep_partial(x, e);
 }
 
-template <int CLS, bool TEX>
+template <int CLS, int TEX>
 __device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px, float py, float pz,
                                unsigned int& nsamp) {
   const MarchParams& P = F.P;
@@ -603,7 +622,7 @@ __device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px
 #pragma unroll
     for (int j = 0; j < kU; ++j) {
       const float dt = dts[j];
-      const float om = 1.f - tf_alpha2(lut2, P.K, TEX ? tri_finish_t<true>(f[j]) : tri_finish_fma(f[j]));
+      const float om = 1.f - tf_alpha2(lut2, P.K, TEX ? tri_finish_t<TEX>(f[j]) : tri_finish_fma(f[j]));
       const float keep = dt == step ? keep_t<CLS>(om, F.e_sh) : keep_partial(om, dt * F.inv_ref);
       trans = trans * keep;
       ++nsamp;
@@ -618,7 +637,7 @@ __device__ float shadow_fast_t(const FastParams& F, const float2* lut2, float px
 // One thread per ray, shadows inline; grid-stride over the list. Used by the naive renderer (bricks)
 // and, on the texture path, for the rays the wavefront main pass could not record (count_rays =
 // false: the setup pass counted them already).
-template <bool TEX>
+template <int TEX>
 __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F, bool count_rays) {
   const MarchParams& P = F.P;
   __shared__ float lut[4 * 256];
@@ -673,7 +692,7 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F, bool coun
         const float mid = (float)s * stepf + 0.5f * dt;
         const float px = ex + dx * mid, py = ey + dy * mid, pz = ez + dz * mid;
         float c[4];
-        tf_apply<float>(lut, P.K, TEX ? tri_finish_t<true>(tri_issue<true>(F.V, px, py, pz)) : tri_fast(F.V, px, py, pz), c);
+        tf_apply<float>(lut, P.K, TEX ? tri_finish_t<TEX>(tri_issue<TEX>(F.V, px, py, pz)) : tri_fast(F.V, px, py, pz), c);
         ++n_main;
         const float keep = last ? keep_partial(1.f - c[3], dt * F.inv_ref) : keep_cls(1.f - c[3], F.cls_main, F.e_main);
         const float a_step = 1.f - keep;
@@ -786,7 +805,7 @@ __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float
 // chunk_pool chunks, the next pool claimed when the current one opens. A ray that finds the record
 // buffer full releases its chunks and goes to the overflow list (march_fast_kernel marches those
 // with inline shadow rays afterwards): keeping that code out of this pass leaves it at 64 registers.
-template <int kU, bool TEX>
+template <int kU, int TEX>
 __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& B, const float* lut,
                                            unsigned hit_mask, int n, float last_dt, float ex, float ey,
                                            float ez, float dx, float dy, float dz, double t0, int pix,
@@ -1040,9 +1059,10 @@ __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B
   }
 }
 
-template <int kU, bool TEX, int MINB>
+template <int kU, int TEX, int MINB>
 __global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
+  B.cap_a = min(P.k_dev ? *P.k_dev : P.k_max, B.cap_a);  // first chunks for this frame's k rays
   __shared__ float lut[4 * 256];
   for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
   __syncthreads();
@@ -1112,9 +1132,10 @@ __global__ void __launch_bounds__(256) first_list_kernel(FastParams F, WaveBufs 
 
 // One shadow ray per record slot (empty tail slots of a ray's last chunk are skipped); lanes
 // refill from a work counter so long shadow rays do not idle their warp's neighbours.
-template <int CLS, bool TEX>
+template <int CLS, int TEX>
 __global__ void __launch_bounds__(128, 8) march_wave_shadow_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
+  B.cap_a = min(P.k_dev ? *P.k_dev : P.k_max, B.cap_a);  // first chunks for this frame's k rays
   __shared__ float2 lut2[256];
   for (int i = threadIdx.x; i < P.K - 1; i += blockDim.x)
     lut2[i] = make_float2(P.lut[4 * i + 3], P.lut[4 * (i + 1) + 3] - P.lut[4 * i + 3]);
@@ -1192,10 +1213,11 @@ __device__ __forceinline__ float lg2_approx(float x) {
   return y;
 }
 
-template <int U, int MINB>
+template <int U, int MINB, bool LIN = false>
 __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastParams F, WaveBufs B, int refill_min,
                                                                           unsigned claim_blk) {
   const MarchParams& P = F.P;
+  B.cap_a = min(P.k_dev ? *P.k_dev : P.k_max, B.cap_a);  // first chunks for this frame's k rays
   // om table: (1 - a_i, -(a_{i+1} - a_i)), padded with (1 - a_{K-1}, 0) so that the index may
   // round to K-1 at s = 1 (w = 0 there)
   __shared__ float2 lut_om[257];
@@ -1287,11 +1309,19 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
     // U samples per lane: positions first (all texture loads in flight), then the products
     float4 A[U], Bq[U];
     float tx[U], ty[U], tz[U];
+    float vl[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int si = s + u;
       const float fs = si == last ? fl : (float)si;
       const float qx = fmaf(qsx, fs, qax), qy = fmaf(qsy, fs, qay), qz = fmaf(qsz, fs, qaz);
+      if constexpr (LIN) {
+        // hardware trilinear at q + 1/2; q < 0 (the lower half-voxel shell) maps to q + 1, which
+        // addresses the reference's texels 0, 1 with its weight q + 1 (see volume_ltex)
+        vl[u] = tex3D<float>(F.V.ltex, qx + (qx < 0.f ? 1.5f : 0.5f), qy + (qy < 0.f ? 1.5f : 0.5f),
+                             qz + (qz < 0.f ? 1.5f : 0.5f));
+        continue;
+      }
       const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
       tx[u] = qx - fx; ty[u] = qy - fy; tz[u] = qz - fz;
       if constexpr (kTexOff == 0.f) {
@@ -1305,11 +1335,16 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int si = s + u;
-      // quads hold (v00, v01 - v00, v10, v11 - v10)
-      const float c00 = fmaf(tx[u], A[u].y, A[u].x), c10 = fmaf(tx[u], A[u].w, A[u].z);
-      const float c01 = fmaf(tx[u], Bq[u].y, Bq[u].x), c11 = fmaf(tx[u], Bq[u].w, Bq[u].z);
-      const float c0 = fmaf(ty[u], c10 - c00, c00), c1 = fmaf(ty[u], c11 - c01, c01);
-      const float v = __saturatef(fmaf(tz[u], c1 - c0, c0));
+      float v;
+      if constexpr (LIN) {
+        v = __saturatef(vl[u]);
+      } else {
+        // quads hold (v00, v01 - v00, v10, v11 - v10)
+        const float c00 = fmaf(tx[u], A[u].y, A[u].x), c10 = fmaf(tx[u], A[u].w, A[u].z);
+        const float c01 = fmaf(tx[u], Bq[u].y, Bq[u].x), c11 = fmaf(tx[u], Bq[u].w, Bq[u].z);
+        const float c0 = fmaf(ty[u], c10 - c00, c00), c1 = fmaf(ty[u], c11 - c01, c01);
+        v = __saturatef(fmaf(tz[u], c1 - c0, c0));
+      }
       // TF alpha: x = v (K-1); i = rint(x - 1/2) in [0, K-1], w = x - i in [0, 1]
       const float xh = fmaf(v, kscale, -0.5f);
       const float r = xh + kMagic;
@@ -1464,6 +1499,41 @@ int volume_texture(fv_ctx* ctx, fv_volume* vol) {
   return 0;
 }
 
+// The voxels as a 3D float texture with hardware trilinear filtering (unnormalised coordinates,
+// clamp addressing). tex3D(q + 0.5) = lerp over texels floor(q), floor(q)+1 with weights
+// frac(q) quantised to 8 fractional bits (the SURVEY's fast tier) -- the reference's
+// sample_trilinear (volume.py:149-180) except in the half-voxel shell q < 0, where the reference
+// keeps i0 = 0, i1 = 1 and t = q + 1; the caller maps q -> q + 1 there (same texels and weight).
+int volume_ltex(fv_ctx* ctx, fv_volume* vol) {
+  if (vol->ltex && vol->ltex_version == vol->version) return 0;
+  if (!vol->larr) {
+    const cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
+    FV_CUDA(cudaMalloc3DArray(&vol->larr, &fd, make_cudaExtent(vol->nx, vol->ny, vol->nz)));
+  }
+  cudaMemcpy3DParms cp{};
+  cp.srcPtr = make_cudaPitchedPtr(vol->data, (size_t)vol->nx * sizeof(float), vol->nx, vol->ny);
+  cp.dstArray = vol->larr;
+  cp.extent = make_cudaExtent(vol->nx, vol->ny, vol->nz);
+  cp.kind = cudaMemcpyDeviceToDevice;
+  FV_CUDA(cudaMemcpy3DAsync(&cp, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (!vol->ltex) {
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeArray;
+    rd.res.array.array = vol->larr;
+    cudaTextureDesc td{};
+    td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModeLinear;
+    td.readMode = cudaReadModeElementType;
+    td.normalizedCoords = 0;
+    cudaTextureObject_t t = 0;
+    FV_CUDA(cudaCreateTextureObject(&t, &rd, &td, nullptr));
+    vol->ltex = (unsigned long long)t;
+  }
+  vol->ltex_version = vol->version;
+  return 0;
+}
+
 int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
   if (vol->bricks && vol->bricks_version == vol->version) return 0;
   const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8, nbz = (vol->nz + 7) / 8;
@@ -1485,7 +1555,7 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
 #endif
 
 // wavefront passes, instantiated for quads from the bricked buffer (TEX = false) or the texture
-template <bool TEX>
+template <int TEX>
 int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
   const int blocks = std::max(1, std::min((F.P.k_max + 255) / 256, ctx->num_sms * 8));
   FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<<<blocks, 256, 0, ctx->stream>>>(F, B));
@@ -1499,7 +1569,7 @@ int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads
   return 0;
 }
 
-template <bool TEX>
+template <int TEX>
 int launch_shadow(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
   static int per_sm = 0;
   if (!per_sm) {
@@ -1518,15 +1588,15 @@ int launch_shadow(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threa
 
 // directional light on the texture path: the partial-refill pass (FV_SHADOW_V=1 keeps the
 // all-lane-refill pass for A/B runs; FV_SHADOW_REFILL tunes it)
-template <int U, int MINB>
+template <int U, int MINB, bool LIN = false>
 int launch_shadow_dir_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads, int refill) {
   static int per_sm = 0;
   if (!per_sm) {
-    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_shadow_dir_kernel<U, MINB>, threads, 0));
+    FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_shadow_dir_kernel<U, MINB, LIN>, threads, 0));
     per_sm = std::max(per_sm, 1);
   }
   static const unsigned blk = getenv("FV_SHADOW_CLAIM") ? (unsigned)std::max(32, atoi(getenv("FV_SHADOW_CLAIM"))) : 64u;
-  FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_dir_kernel<U, MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B, refill, blk));
+  FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_dir_kernel<U, MINB, LIN><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B, refill, blk));
   return 0;
 }
 
@@ -1538,6 +1608,11 @@ int launch_shadow_dir_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int
 // samples and 6 blocks/SM (+37% / +17%).
 int launch_shadow_dir(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
   static const int refill = getenv("FV_SHADOW_REFILL") ? std::min(32, std::max(1, atoi(getenv("FV_SHADOW_REFILL")))) : 8;
+  static const int lin_u = getenv("FV_SHADOW_LIN_U") ? atoi(getenv("FV_SHADOW_LIN_U")) : 4;
+  if (F.V.ltex) {
+    if (lin_u == 8) return launch_shadow_dir_t<8, 8, true>(ctx, F, B, threads, refill);
+    return launch_shadow_dir_t<4, 8, true>(ctx, F, B, threads, refill);
+  }
   return launch_shadow_dir_t<4, 8>(ctx, F, B, threads, refill);
 }
 
@@ -1617,12 +1692,27 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     // FV_VOL_TEX=0 still use).
     static const bool use_tex = !(getenv("FV_VOL_TEX") && atoi(getenv("FV_VOL_TEX")) == 0);
     const bool tex_path = use_tex && variant == 3;
-    int rc = tex_path ? volume_texture(ctx, mv) : volume_bricks(ctx, mv);
+    // Sample source of the wavefront passes (`src`, the kernels' TEX parameter):
+    //   1  quads (v00, v01-v00, v10, v11-v10) from a point-sampled float4 texture, software
+    //      trilinear in fp32 (two 16-byte returns per sample; 4 floats per voxel)
+    //   2  a hardware-filtered float texture: trilinear with 8-bit fractional weights (one 4-byte
+    //      return per sample; 1 float per voxel) -- the SURVEY's fast tier
+    // FV_TEX_FILTER: 0 = quads everywhere, 1 = filtered shadow samples only, 2 = filtered
+    // everywhere (the quad texture is then never built).
+    static const int tex_filter = getenv("FV_TEX_FILTER") ? atoi(getenv("FV_TEX_FILTER")) : 1;
+    const int src = !tex_path ? 0 : tex_filter >= 2 ? 2 : 1;
+    int rc = src == 0 ? volume_bricks(ctx, mv) : src == 1 ? volume_texture(ctx, mv) : 0;
     if (rc) return rc;
     FastParams F;
     F.P = P;
     F.V.quads = reinterpret_cast<const float4*>(mv->bricks);
-    F.V.tex = tex_path ? (cudaTextureObject_t)mv->qtex : 0;
+    F.V.tex = src == 1 ? (cudaTextureObject_t)mv->qtex : 0;
+    F.V.ltex = 0;
+    if (tex_path && tex_filter >= 1) {
+      rc = volume_ltex(ctx, mv);
+      if (rc) return rc;
+      F.V.ltex = (cudaTextureObject_t)mv->ltex;
+    }
     F.V.nx = vol->nx; F.V.ny = vol->ny; F.V.nz = vol->nz;
     const int nbx = (vol->nx + 7) / 8, nby = (vol->ny + 7) / 8;
     F.V.sby = nbx * 512;
@@ -1649,17 +1739,18 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     for (int a = 0; a < 3; ++a) F.qs_sh[a] = F.ld[a] * F.V.inv_sp[a] * F.step_sh;
     if (variant == 3) {
       // wavefront: main -> shadow -> composite
-      // Record buffer, in chunks of kChunk slots (36 B per slot): the first cap_a chunks are the
-      // first chunks of rays 0..cap_a-1 (chunk id = ray index); the rest is the pool for later
-      // chunks and for the first chunks of rays beyond cap_a. It is sized from what this context's
-      // previous render used -- its ray count k, pooled-chunk count and overflow count, read back
-      // asynchronously into pinned memory (a readback still in flight is not waited for) -- and
-      // never shrinks. A frame whose records do not fit is still correct: its overflowing rays are
-      // re-marched one thread per ray (inline shadows) after the main pass, and the next frame gets
-      // a larger buffer. (Round 1 allocated 64 slots per FILM pixel: 4.8 GB per context at 1080p
-      // against ~1.8 GB of records a C3 frame writes.) FV_WAVE_REC_PER_RAY fixes the size at that
-      // many slots per film pixel, FV_WAVE_REC_CAP at an absolute slot count (tests use a tiny one
-      // to force the overflow fallback); both disable the feedback.
+      // Record buffer, in chunks of kChunk slots (36 B per slot). The first min(k, n_chunks / 2)
+      // chunks are the first chunks of rays 0..k-1 (chunk id = ray index; k = this frame's ray
+      // count, read on the device); the rest is the pool for later chunks (and the first chunks of
+      // any rays beyond). Initial size 32 slots per film pixel (at least 8M slots): a C3 frame
+      // writes ~24 records per film pixel, so foveated frames never overflow and their results do
+      // not depend on the buffer's history. The buffer then follows this context's usage -- the
+      // previous render's pooled-chunk and overflow counts are read back asynchronously into pinned
+      // memory (a readback still in flight is not waited for) -- and never shrinks. A frame whose
+      // records do not fit is still correct: its overflowing rays are re-marched one thread per ray
+      // (inline shadows) after the main pass. FV_WAVE_REC_PER_RAY fixes the size at that many
+      // slots per film pixel, FV_WAVE_REC_CAP at an absolute slot count (tests force the overflow
+      // fallback with a tiny one); both disable the feedback.
       static const int64_t per_ray_env = getenv("FV_WAVE_REC_PER_RAY") ? std::max(1, atoi(getenv("FV_WAVE_REC_PER_RAY"))) : 0;
       static const int64_t cap_env = getenv("FV_WAVE_REC_CAP") ? std::max(2 * kChunk, atoi(getenv("FV_WAVE_REC_CAP"))) : 0;
       {
@@ -1667,25 +1758,22 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         FV_CUDA(cudaStreamIsCapturing(ctx->stream, &cap_st));
         const bool capturing = cap_st != cudaStreamCaptureStatusNone;
         const int64_t have = ctx->wave_cap / kChunk;
-        int64_t want_a = ctx->wave_cap_a, want_pool = have - ctx->wave_cap_a;
+        int64_t need = have;
         if (cap_env || per_ray_env) {
-          const int64_t n = (cap_env ? cap_env : per_ray_env * k_max) / kChunk;
-          want_a = n / 2;
-          want_pool = n - n / 2;
+          need = (cap_env ? cap_env : per_ray_env * k_max) / kChunk;
         } else if (have == 0) {
-          // no history: first chunks for a quarter of the film's pixels, 8 pooled slots per pixel
-          want_a = std::max<int64_t>(1024, ((int64_t)k_max + 3) / 4);
-          want_pool = std::max<int64_t>(4096, (int64_t)k_max * 8 / kChunk);
+          need = std::max<int64_t>((8 << 20) / kChunk, (int64_t)k_max);  // 32 slots per pixel
         } else if (ctx->wave_fb_pending && !capturing && cudaEventQuery(ctx->wave_fb_ev) == cudaSuccess) {
           ctx->wave_fb_pending = false;
           const int64_t k_prev = ctx->wave_fb[0], pooled = ctx->wave_fb[1 + 1], ovf = ctx->wave_fb[1 + 6];
-          want_a = std::max(want_a, std::min<int64_t>(k_max, k_prev + k_prev / 4 + 1024));
-          want_pool = std::max(want_pool, ovf ? 2 * want_pool : pooled + 3 * pooled / 10 + 1024);
+          const int64_t first = std::min(k_prev, have / 2), pool = have - first;
+          if (ovf) need = 2 * have;
+          else if (pooled > pool - pool / 8) need = first + pooled + pooled / 2;
         } else {
           (void)cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
         }
-        int64_t need = std::min<int64_t>(want_a + want_pool, INT32_MAX / kChunk);
-        if (need > have) {
+        need = std::min<int64_t>(need, INT32_MAX / kChunk);
+        if (need > have || (cap_env || per_ray_env) && need != have) {
           if (ctx->wave_rec) cudaFree(ctx->wave_rec);
           ctx->wave_rec = nullptr;
           ctx->wave_cap = 0;
@@ -1702,8 +1790,6 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           }
           FV_REQUIRE(ctx->wave_rec, "cudaMalloc of the marcher record buffer failed");
         }
-        const int64_t n_have = ctx->wave_cap / kChunk;
-        ctx->wave_cap_a = want_a + want_pool <= n_have ? want_a : std::min(want_a, n_have / 2);
         if (!ctx->wave_fb) {
           FV_CUDA(cudaMallocHost(&ctx->wave_fb, 8 * sizeof(unsigned int)));
           FV_CUDA(cudaEventCreateWithFlags(&ctx->wave_fb_ev, cudaEventDisableTiming));
@@ -1748,12 +1834,13 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       B.ovf_count = &ctx->counters->ovf_count;
       // half of the chunk space holds first chunks at id = ray index (k_max may exceed it: later
       // rays then take pooled first chunks); ord lists the non-empty ones in ray order
-      B.cap_a = (int)std::min<int64_t>(ctx->wave_cap_a, B.n_chunks_cap);
+      B.cap_a = B.n_chunks_cap / 2;  // at most; the kernels take min(k, cap_a) on the device
       B.ord = B.chunk_fill + ctx->wave_cap / kChunk;
       B.ord_count = &ctx->counters->wave_ord;
       // ray_next, wave_rec, wave_next, wave_ord, hit_count, hit_next, ovf_count are consecutive
       FV_CUDA(cudaMemsetAsync(&ctx->counters->ray_next, 0, 7 * sizeof(unsigned int), ctx->stream));
-      rc = F.V.tex ? launch_main<true>(ctx, F, B, threads) : launch_main<false>(ctx, F, B, threads);
+      rc = src == 2 ? launch_main<2>(ctx, F, B, threads) : src == 1 ? launch_main<1>(ctx, F, B, threads)
+                                                            : launch_main<0>(ctx, F, B, threads);
       if (rc) return rc;
       if (P.light_kind != FV_LIGHT_NONE) {
         // rays that found the record buffer full: inline shadows, one thread per ray (a grid that
@@ -1761,10 +1848,12 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         FastParams Fo = F;
         Fo.P.idx = B.ovf;
         Fo.P.k_dev = reinterpret_cast<const int32_t*>(B.ovf_count);
-        if (F.V.tex)
-          FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<true><<<ctx->num_sms, threads, 0, ctx->stream>>>(Fo, false));
+        if (src == 2)
+          FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<2><<<ctx->num_sms, threads, 0, ctx->stream>>>(Fo, false));
+        else if (src == 1)
+          FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<1><<<ctx->num_sms, threads, 0, ctx->stream>>>(Fo, false));
         else
-          FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<false><<<ctx->num_sms, threads, 0, ctx->stream>>>(Fo, false));
+          FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_fast_kernel<0><<<ctx->num_sms, threads, 0, ctx->stream>>>(Fo, false));
         ctx->launches += 1;
       }
       if (P.light_kind != FV_LIGHT_NONE) {
@@ -1773,10 +1862,11 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         // directional lights on the texture path: the partial-refill pass (FV_SHADOW_V=1: the
         // all-lane-refill pass, which point lights and the bricked path use)
         static const int shadow_v = getenv("FV_SHADOW_V") ? atoi(getenv("FV_SHADOW_V")) : 2;
-        if (F.V.tex && P.light_kind == FV_LIGHT_DIRECTIONAL && shadow_v == 2)
-          rc = launch_shadow_dir(ctx, F, B, threads);
+        if (src && P.light_kind == FV_LIGHT_DIRECTIONAL && shadow_v == 2)
+          rc = launch_shadow_dir(ctx, F, B, threads);  // (filtered samples whenever F.V.ltex is set)
         else
-          rc = F.V.tex ? launch_shadow<true>(ctx, F, B, threads) : launch_shadow<false>(ctx, F, B, threads);
+          rc = src == 2 ? launch_shadow<2>(ctx, F, B, threads) : src == 1 ? launch_shadow<1>(ctx, F, B, threads)
+                                                                : launch_shadow<0>(ctx, F, B, threads);
         if (rc) return rc;
         FV_TIMED(ctx, FV_KC_MARCH_COMPOSITE, march_wave_composite_kernel<<<ctx->num_sms * 16, threads, 0, ctx->stream>>>(F, B));
         ctx->launches += 2;
@@ -1805,3 +1895,140 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
 }
 
 }  // namespace fv
+
+// ---- Boundary ops: the reference's per-sample building blocks as device calls ------------------
+// (volume.generate_rays :293-303, volume.sample_trilinear :149-180, TransferFunction.apply
+// :201-208, noise.tile_field :378-384), fp64 like the reference. The marcher inlines the same
+// arithmetic; these entry points serve callers of the individual functions.
+namespace fv {
+namespace {
+
+__global__ void generate_rays_kernel(MarchParams P, const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
+                                     int64_t n, double* __restrict__ orig, double* __restrict__ dirs) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double sx = (((double)us[i] + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
+    const double sy = (1.0 - ((double)vs[i] + 0.5) / P.H * 2.0) * P.tan_half;
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+    const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      dirs[3 * i + a] = d[a] / nrm;
+      orig[3 * i + a] = P.pos[a];
+    }
+  }
+}
+
+__global__ void sample_trilinear_kernel(MarchParams P, const double* __restrict__ pts, int64_t n,
+                                        double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    out[i] = trilinear<double>(P, p);
+  }
+}
+
+__global__ void tf_apply_kernel(const float* __restrict__ lut, int K, const double* __restrict__ s, int64_t n,
+                                double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double c[4];
+    // np.clip propagates NaN; tf_apply's comparisons would map it to 0 -- keep the reference's NaN
+    if (s[i] != s[i]) {
+      for (int a = 0; a < 4; ++a) out[4 * i + a] = s[i];
+      continue;
+    }
+    tf_apply<double>(lut, K, s[i], c);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) out[4 * i + a] = c[a];
+  }
+}
+
+__global__ void tile_field_kernel(const float* __restrict__ noise, int T, int th, int tw, int frame, int h, int w,
+                                  float* __restrict__ out) {
+  const float* f = noise + (int64_t)(frame % T) * th * tw;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)h * w; i += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(i % w), v = (int)(i / w);
+    out[i] = f[(v % th) * tw + (u % tw)];
+  }
+}
+
+int grid_for(const fv_ctx* ctx, int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, ctx->num_sms * 16)); }
+
+int camera_params(const fv_camera* cam, MarchParams& P) {
+  FV_REQUIRE(cam->width >= 1 && cam->height >= 1, "film dims must be positive");
+  FV_REQUIRE(cam->fov_y > 0.0 && cam->fov_y < 180.0, "fov_y must be in (0, 180) degrees, got %g", cam->fov_y);
+  double fwd[3] = {cam->look_at[0] - cam->position[0], cam->look_at[1] - cam->position[1],
+                   cam->look_at[2] - cam->position[2]};
+  FV_REQUIRE(fwd[0] != 0 || fwd[1] != 0 || fwd[2] != 0, "camera position and look_at coincide");
+  normalize3(fwd);
+  double right[3] = {fwd[1] * cam->up[2] - fwd[2] * cam->up[1], fwd[2] * cam->up[0] - fwd[0] * cam->up[2],
+                     fwd[0] * cam->up[1] - fwd[1] * cam->up[0]};
+  FV_REQUIRE(sqrt(right[0] * right[0] + right[1] * right[1] + right[2] * right[2]) > 0,
+             "up vector is parallel to the view direction");
+  normalize3(right);
+  const double up[3] = {right[1] * fwd[2] - right[2] * fwd[1], right[2] * fwd[0] - right[0] * fwd[2],
+                        right[0] * fwd[1] - right[1] * fwd[0]};
+  for (int a = 0; a < 3; ++a) {
+    P.pos[a] = cam->position[a]; P.fwd[a] = fwd[a]; P.right[a] = right[a]; P.up[a] = up[a];
+  }
+  P.tan_half = tan(cam->fov_y * (M_PI / 180.0) * 0.5);
+  P.aspect = (double)cam->width / (double)cam->height;
+  P.W = cam->width;
+  P.H = cam->height;
+  return 0;
+}
+
+}  // namespace
+}  // namespace fv
+
+extern "C" {
+
+int fv_generate_rays(fv_ctx* ctx, const fv_camera* cam, const int32_t* us_dev, const int32_t* vs_dev, int64_t n,
+                     double* origins_dev, double* dirs_dev) {
+  FV_REQUIRE(ctx && cam && (n == 0 || (us_dev && vs_dev && origins_dev && dirs_dev)), "null argument");
+  fv::MarchParams P{};
+  const int rc = fv::camera_params(cam, P);
+  if (rc) return rc;
+  if (n == 0) return 0;
+  fv::generate_rays_kernel<<<fv::grid_for(ctx, n), 256, 0, ctx->stream>>>(P, us_dev, vs_dev, n, origins_dev, dirs_dev);
+  FV_CHECK_LAUNCH("generate_rays_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int fv_sample_trilinear(fv_ctx* ctx, const fv_volume* vol, const double* pts_dev, int64_t n, double* out_dev) {
+  FV_REQUIRE(ctx && vol && vol->data && (n == 0 || (pts_dev && out_dev)), "null argument");
+  fv::MarchParams P{};
+  P.data = vol->data; P.nx = vol->nx; P.ny = vol->ny; P.nz = vol->nz;
+  for (int a = 0; a < 3; ++a) P.sp[a] = vol->spacing[a];
+  P.ext[0] = vol->nx * vol->spacing[0]; P.ext[1] = vol->ny * vol->spacing[1]; P.ext[2] = vol->nz * vol->spacing[2];
+  if (n == 0) return 0;
+  fv::sample_trilinear_kernel<<<fv::grid_for(ctx, n), 256, 0, ctx->stream>>>(P, pts_dev, n, out_dev);
+  FV_CHECK_LAUNCH("sample_trilinear_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int fv_tf_apply(fv_ctx* ctx, const float* lut_dev, int K, const double* s_dev, int64_t n, double* out_dev) {
+  FV_REQUIRE(ctx && lut_dev && (n == 0 || (s_dev && out_dev)), "null argument");
+  FV_REQUIRE(K >= 2 && K <= 256, "transfer function lut must be (K>=2, 4), got K=%d", K);
+  if (n == 0) return 0;
+  fv::tf_apply_kernel<<<fv::grid_for(ctx, n), 256, 0, ctx->stream>>>(lut_dev, K, s_dev, n, out_dev);
+  FV_CHECK_LAUNCH("tf_apply_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int fv_tile_field(fv_ctx* ctx, int frame, int h, int w, float* out_dev) {
+  FV_REQUIRE(ctx && out_dev, "null argument");
+  FV_REQUIRE(ctx->noise, "no noise stack uploaded (fv_noise_upload)");
+  FV_REQUIRE(h >= 1 && w >= 1, "dims must be positive, got (%d, %d)", h, w);
+  FV_REQUIRE(frame >= 0, "frame must be >= 0");
+  fv::tile_field_kernel<<<fv::grid_for(ctx, (int64_t)h * w), 256, 0, ctx->stream>>>(
+      ctx->noise, ctx->noise_T, ctx->noise_H, ctx->noise_W, frame, h, w, out_dev);
+  FV_CHECK_LAUNCH("tile_field_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+}  // extern "C"

@@ -221,6 +221,160 @@ int launch_tau_map(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* p
   return 0;
 }
 
+// c_max (sample_maps.py:135-137): the mean of tau over the frame as a deterministic fp64 sum --
+// a fixed grid of kSumBlocks blocks (independent of the device), each summing a fixed pixel
+// stride then a fixed shared-memory tree, and one block summing the partials the same way. tau is
+// evaluated inline (tau_at: the mask kernel's arithmetic) or read from a tau map.
+constexpr int kSumBlocks = 512, kSumThreads = 256;
+
+__global__ void __launch_bounds__(kSumThreads) tau_sum_partial_kernel(MaskParams p, double* partial) {
+  __shared__ double s[kSumThreads];
+  const int64_t n = (int64_t)p.H * p.W;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kSumThreads + threadIdx.x; i < n; i += (int64_t)kSumBlocks * kSumThreads)
+    acc += tau_at(p, (int)(i % p.W), (int)(i / p.W));
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kSumThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = s[0];
+}
+
+__global__ void __launch_bounds__(kSumThreads) sum_partials_kernel(const double* partial, double* out) {
+  __shared__ double s[kSumThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kSumBlocks; i += kSumThreads) acc += partial[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = kSumThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+// foveal_density (sample_maps.py:62-68) elementwise over broadcast (dx, dy) offsets: the mask
+// kernel's fp64 arithmetic (no FMA contraction)
+__global__ void foveal_density_kernel(const double* __restrict__ ox, const double* __restrict__ oy, int64_t n,
+                                      double sigma, double scale, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double dx = __dmul_rn(ox[i], scale), dy = __dmul_rn(oy[i], scale);
+    const double r2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+    out[i] = exp(__dmul_rn(__dmul_rn(-0.5, r2), sigma));
+  }
+}
+
+int launch_tau_sum(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* pb_map, const double* tau_map,
+                   double* sum_dev) {
+  MaskParams p = make_params(ctx, 0, H, W, f, pb_map);
+  p.tau_map = tau_map;
+  double* partial = nullptr;
+  FV_CUDA(cudaMallocAsync(&partial, sizeof(double) * kSumBlocks, ctx->stream));
+  FV_TIMED(ctx, FV_KC_MASK, tau_sum_partial_kernel<<<kSumBlocks, kSumThreads, 0, ctx->stream>>>(p, partial));
+  FV_TIMED(ctx, FV_KC_MASK, sum_partials_kernel<<<1, kSumThreads, 0, ctx->stream>>>(partial, sum_dev));
+  FV_CHECK_LAUNCH("tau_sum_kernel");
+  ctx->launches += 2;
+  FV_CUDA(cudaFreeAsync(partial, ctx->stream));
+  return 0;
+}
+
+int launch_foveal_density(fv_ctx* ctx, const double* ox, const double* oy, int64_t n, double sigma, double scale,
+                          double* out) {
+  if (n == 0) return 0;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 16));
+  FV_TIMED(ctx, FV_KC_MASK, foveal_density_kernel<<<blocks, 256, 0, ctx->stream>>>(ox, oy, n, sigma, scale, out));
+  FV_CHECK_LAUNCH("foveal_density_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+// draw_direct_samples (sample_maps.py:181-198): inverse-CDF sampling over the row-major fp64 tau
+// map -- cdf = cumsum(tau) / total, idx = searchsorted(cdf, r, side="right") clamped to n-1 -- for
+// caller-supplied uniforms r (NumPy's stream, so the draws follow the reference's generator). The
+// cumulative sum is blocked (sequential per thread over 16 pixels, a fixed in-block scan, a
+// sequential scan of the block totals): deterministic, and within rounding of np.cumsum's
+// sequential sum (a draw can only differ when r falls within ~1e-16 of a CDF step).
+constexpr int kCdfPer = 16, kCdfBlock = kSumThreads * kCdfPer;
+
+__global__ void __launch_bounds__(kSumThreads) cdf_block_kernel(MaskParams p, double* cdf, double* bsum) {
+  __shared__ double s[kSumThreads];
+  const int64_t n = (int64_t)p.H * p.W;
+  const int64_t base = (int64_t)blockIdx.x * kCdfBlock + (int64_t)threadIdx.x * kCdfPer;
+  double loc[kCdfPer];
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < kCdfPer; ++j) {
+    const int64_t i = base + j;
+    const double t = i < n ? tau_at(p, (int)(i % p.W), (int)(i / p.W)) : 0.0;
+    acc += t;
+    loc[j] = acc;
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  // inclusive Hillis-Steele scan of the thread totals (fixed order)
+  for (int o = 1; o < kSumThreads; o <<= 1) {
+    const double v = threadIdx.x >= o ? s[threadIdx.x - o] : 0.0;
+    __syncthreads();
+    s[threadIdx.x] += v;
+    __syncthreads();
+  }
+  const double off = threadIdx.x ? s[threadIdx.x - 1] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kCdfPer; ++j)
+    if (base + j < n) cdf[base + j] = off + loc[j];
+  if (threadIdx.x == kSumThreads - 1) bsum[blockIdx.x] = s[threadIdx.x];
+}
+
+__global__ void cdf_offsets_kernel(double* bsum, int nb) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double acc = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    const double v = bsum[b];
+    bsum[b] = acc;  // exclusive offsets; bsum[nb] = total
+    acc += v;
+  }
+  bsum[nb] = acc;
+}
+
+__global__ void direct_draw_kernel(double* cdf, const double* bsum, int nb, int64_t n, const double* r,
+                                   int64_t count, int32_t* idx) {
+  const double total = bsum[nb];
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < count; d += (int64_t)gridDim.x * blockDim.x) {
+    const double x = r[d];
+    // first i with cdf[i] / total > x (searchsorted side="right" on the normalised cdf)
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      const double c = (cdf[mid] + bsum[mid / kCdfBlock]) / total;
+      if (c > x) hi = mid; else lo = mid + 1;
+    }
+    idx[d] = (int32_t)(lo < n - 1 ? lo : n - 1);
+  }
+}
+
+int launch_direct_draws(fv_ctx* ctx, int H, int W, const fv_fovea* f, const double* pb_map, const double* tau_map,
+                        const double* r, int64_t count, int32_t* idx) {
+  MaskParams p = make_params(ctx, 0, H, W, f, pb_map);
+  p.tau_map = tau_map;
+  const int64_t n = (int64_t)H * W;
+  const int nb = (int)((n + kCdfBlock - 1) / kCdfBlock);
+  double* cdf = nullptr;
+  FV_CUDA(cudaMallocAsync(&cdf, sizeof(double) * (n + nb + 1), ctx->stream));
+  double* bsum = cdf + n;
+  FV_TIMED(ctx, FV_KC_MASK, cdf_block_kernel<<<nb, kSumThreads, 0, ctx->stream>>>(p, cdf, bsum));
+  FV_TIMED(ctx, FV_KC_MASK, cdf_offsets_kernel<<<1, 32, 0, ctx->stream>>>(bsum, nb));
+  if (count > 0) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, (int64_t)ctx->num_sms * 16));
+    FV_TIMED(ctx, FV_KC_MASK, direct_draw_kernel<<<blocks, 256, 0, ctx->stream>>>(cdf, bsum, nb, n, r, count, idx));
+  }
+  FV_CHECK_LAUNCH("direct_draw_kernel");
+  ctx->launches += 3;
+  FV_CUDA(cudaFreeAsync(cdf, ctx->stream));
+  return 0;
+}
+
 // Naive renderer lane list (render_sparse_naive, renderer.py:225-259): one warp per 64-pixel chunk;
 // an occupied chunk appends all its pixels (idle ones as -(pix+1)), contiguous in the list so each
 // chunk still maps onto two warps of the thread-per-lane marcher.

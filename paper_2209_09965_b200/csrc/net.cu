@@ -33,6 +33,8 @@ int kapply_final(fv_ctx* ctx, fv_state* st, const kw_t* kw, const float* img, fl
 int nc8_to_nchw(fv_ctx* ctx, const fv_act& a, float* out);
 int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a);
 int od_to_feedback(fv_ctx* ctx, fv_state* st);
+int kfield_logits(fv_ctx* ctx, const float* w_host, const float* b_host, const float* hd, int C, int h, int w,
+                  int normalize, float* out);
 int set_input(fv_ctx* ctx, fv_state* st, const float* xin, int C);
 
 namespace {
@@ -121,40 +123,13 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
   return 0;
 }
 
-// The launches of one reconstruction (no host-side state change: see reconstruct()).
-static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb,
-                                float* out_o, float* out_od) {
-  const int ne = net->n_enc, nd = net->n_dec;
+// The K stage (network.py:268-293) plus D.head over the decoder hidden states hidden[hp]: the
+// level-0 conv writes D.head's O_d to od_out (and the next frame's feedback channels when feedback
+// is set), the filter chain starts from od_in (forward_K's given O_d) or, when null, from od_out.
+static int kstage_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int hp, float* od_out, __half* feedback,
+                           int use_k, const float* od_in, float* out_rgb, float* out_o, float* out_od) {
+  const int ne = net->n_enc;
   int rc;
-  const fv_act* cur = &st->x;
-  for (int i = 0; i < ne; ++i) {
-    rc = conv3x3(ctx, net->convs[2 * i], cur, 1, &st->enc_a[i], nullptr, true, nullptr);
-    if (rc) return rc;
-    rc = conv3x3(ctx, net->convs[2 * i + 1], &st->enc_a[i], 1, &st->skips[i], &st->pooled[i], true,
-                 nullptr);
-    if (rc) return rc;
-    cur = &st->pooled[i];
-  }
-  const int oldp = st->parity, newp = st->parity ^ 1;
-  for (int j = 0; j < nd; ++j) {
-    fv_act srcs[3];
-    int n = 0;
-    if (j > 0) {
-      rc = upsample2_nc8(ctx, st->hidden[newp][j - 1], st->ups[j]);
-      if (rc) return rc;
-      srcs[n++] = st->ups[j];
-      srcs[n++] = st->skips[ne - j];
-    } else {
-      srcs[n++] = *cur;
-    }
-    if (net->recurrent) srcs[n++] = st->hidden[oldp][j];
-    const int b = ne + j;
-    rc = conv3x3(ctx, net->convs[2 * b], srcs, n, &st->dec_a[j], nullptr, true, nullptr);
-    if (rc) return rc;
-    rc = conv3x3(ctx, net->convs[2 * b + 1], &st->dec_a[j], 1, &st->hidden[newp][j], nullptr, true,
-                 nullptr);
-    if (rc) return rc;
-  }
   // Level 0: one tcgen05 conv over Hd3 computes D.head (3x3, columns 0..2) AND the logits of
   // the two K blocks at level 0 (1x1, centre tap only, columns 4.. and 13..); its epilogue writes
   // O_d, the NEXT frame's feedback channels 5..7 (the two input buffers alternate, so the next
@@ -166,8 +141,8 @@ static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_
     if (L > 0 && !use_k) break;
     ConvAux aux;
     if (L == 0) {
-      aux.od = st->od;
-      aux.feedback = net->recurrent ? st->xalt.p : nullptr;
+      aux.od = od_out;
+      aux.feedback = feedback;
     } else {
       aux.center_only = true;
     }
@@ -178,13 +153,13 @@ static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_
         aux.kcol[s] = kLogitCol[s];
         ++s;
       }
-    rc = conv3x3(ctx, net->kconv[L], &st->hidden[newp][ne - L], 1, nullptr, nullptr, false, &aux);
+    rc = conv3x3(ctx, net->kconv[L], &st->hidden[hp][ne - L], 1, nullptr, nullptr, false, &aux);
     if (rc) return rc;
   }
   if (use_k) {
     // forward_K (network.py:280-293): encoder levels fuse the filter with the following pool, the
     // last block (level 0) with the output stage
-    const float* img = st->od;
+    const float* img = od_in ? od_in : od_out;
     // blocks 1 .. nb-2 (the small levels) as one cooperative launch when every encoder level there
     // has even width (the paired-pixel filter + pool)
     KChain ch;
@@ -230,10 +205,49 @@ static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_
       }
     }
   } else {
-    rc = finalize(ctx, st, st->od, out_rgb, out_o, out_od);
+    rc = finalize(ctx, st, od_in ? od_in : od_out, out_rgb, out_o, out_od);
     if (rc) return rc;
   }
   return 0;
+}
+
+
+// The launches of one reconstruction (no host-side state change: see reconstruct()).
+static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb,
+                                float* out_o, float* out_od) {
+  const int ne = net->n_enc, nd = net->n_dec;
+  int rc;
+  const fv_act* cur = &st->x;
+  for (int i = 0; i < ne; ++i) {
+    rc = conv3x3(ctx, net->convs[2 * i], cur, 1, &st->enc_a[i], nullptr, true, nullptr);
+    if (rc) return rc;
+    rc = conv3x3(ctx, net->convs[2 * i + 1], &st->enc_a[i], 1, &st->skips[i], &st->pooled[i], true,
+                 nullptr);
+    if (rc) return rc;
+    cur = &st->pooled[i];
+  }
+  const int oldp = st->parity, newp = st->parity ^ 1;
+  for (int j = 0; j < nd; ++j) {
+    fv_act srcs[3];
+    int n = 0;
+    if (j > 0) {
+      rc = upsample2_nc8(ctx, st->hidden[newp][j - 1], st->ups[j]);
+      if (rc) return rc;
+      srcs[n++] = st->ups[j];
+      srcs[n++] = st->skips[ne - j];
+    } else {
+      srcs[n++] = *cur;
+    }
+    if (net->recurrent) srcs[n++] = st->hidden[oldp][j];
+    const int b = ne + j;
+    rc = conv3x3(ctx, net->convs[2 * b], srcs, n, &st->dec_a[j], nullptr, true, nullptr);
+    if (rc) return rc;
+    rc = conv3x3(ctx, net->convs[2 * b + 1], &st->dec_a[j], 1, &st->hidden[newp][j], nullptr, true,
+                 nullptr);
+    if (rc) return rc;
+  }
+  return kstage_launches(ctx, net, st, newp, st->od, net->recurrent ? st->xalt.p : nullptr, use_k, nullptr,
+                         out_rgb, out_o, out_od);
 }
 
 static bool graphs_enabled(const fv_ctx* ctx) {
@@ -580,6 +594,38 @@ int fv_reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_kernel_
     return FV_E_STATE;
   }
   return reconstruct(ctx, net, st, use_kernel_stage, out_rgb_dev, out_o_dev, out_od_dev);
+}
+
+// forward_K (network.py:280-293) on the decoder hidden states the state currently holds (written
+// with fv_state_write, or left by the last fv_reconstruct) and a given O_d (3, Hp, Wp) fp32 on
+// the device; writes the filtered image (3, H, W) to out_dev. The state's recurrent buffers and
+// its O_d are not modified.
+int fv_forward_k(fv_ctx* ctx, const fv_net* cnet, fv_state* st, const float* od_dev, float* out_dev) {
+  FV_REQUIRE(ctx && cnet && st && od_dev && out_dev, "null argument");
+  FV_REQUIRE(st->net == cnet, "carried state belongs to a different network; reset the state");
+  fv_net* net = const_cast<fv_net*>(cnet);
+  for (const auto& cp : net->convs)
+    FV_REQUIRE(cp.w_set && cp.b_set, "network parameter %s not set", cp.name.c_str());
+  if (net->kstage_dirty) {
+    const int rc0 = build_kstage(ctx, net);
+    if (rc0) return rc0;
+  }
+  // the level-0 conv's D.head output goes to the level-0 scratch image (unused by the chain)
+  return kstage_launches(ctx, net, st, st->parity, st->img2[0], nullptr, 1, od_dev, nullptr, out_dev, nullptr);
+}
+
+// predict_kernel_fields (network.py:268-277) for one K block: the 9 logits of the 1x1 conv over
+// a decoder hidden state hd (C, h, w) fp32 (device), in fp32; normalize = 1 applies the softmax
+// over the taps (KernelField.normalized).
+int fv_kfield_logits(fv_ctx* ctx, const fv_net* net, int block, const float* hd_dev, int C, int h, int w,
+                     int normalize, float* logits_dev) {
+  FV_REQUIRE(ctx && net && hd_dev && logits_dev, "null argument");
+  FV_REQUIRE(block >= 0 && block < (int)net->convs.size() - net->k_index0, "K block %d out of range", block);
+  const ConvParam& kp = net->convs[net->k_index0 + block];
+  FV_REQUIRE(kp.w_set && kp.b_set, "network parameter %s not set", kp.name.c_str());
+  FV_REQUIRE(C == kp.cin, "K.block%d expects %d channels, got %d", block, kp.cin, C);
+  FV_REQUIRE(h >= 1 && w >= 1, "dims must be positive, got (%d, %d)", h, w);
+  return kfield_logits(ctx, kp.w_host.data(), kp.b_host.data(), hd_dev, C, h, w, normalize, logits_dev);
 }
 
 int fv_state_read(fv_ctx* ctx, const fv_state* st, int which, float* host, int64_t cap,

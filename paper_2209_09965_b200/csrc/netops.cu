@@ -598,6 +598,55 @@ int nchw_to_nc8(fv_ctx* ctx, const float* in, fv_act& a) {
   return 0;
 }
 
+// predict_kernel_fields' 1x1 conv for one block in fp32 (a checking/API path, not the hot path:
+// the hot path computes these logits on the tensor cores inside the K-stage conv epilogue)
+__global__ void kfield_logits_kernel(const float* __restrict__ w, const float* __restrict__ b,
+                                     const float* __restrict__ hd, int C, int64_t n, int normalize,
+                                     float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) acc[j] = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float v = hd[(int64_t)c * n + i];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) acc[j] = fmaf(w[j * C + c], v, acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) acc[j] += b[j];
+    if (normalize) {  // softmax_channels (autograd.py:188-199): max-subtracted, then normalised
+      float m = acc[0];
+#pragma unroll
+      for (int j = 1; j < 9; ++j) m = fmaxf(m, acc[j]);
+      float sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        acc[j] = expf(acc[j] - m);
+        sum += acc[j];
+      }
+#pragma unroll
+      for (int j = 0; j < 9; ++j) acc[j] /= sum;
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) out[(int64_t)j * n + i] = acc[j];
+  }
+}
+
+int kfield_logits(fv_ctx* ctx, const float* w_host, const float* b_host, const float* hd, int C, int h, int w,
+                  int normalize, float* out) {
+  const int64_t n = (int64_t)h * w;
+  float* wb = nullptr;
+  FV_CUDA(cudaMallocAsync(&wb, sizeof(float) * (9 * C + 9), ctx->stream));
+  FV_CUDA(cudaMemcpyAsync(wb, w_host, sizeof(float) * 9 * C, cudaMemcpyHostToDevice, ctx->stream));
+  FV_CUDA(cudaMemcpyAsync(wb + 9 * C, b_host, sizeof(float) * 9, cudaMemcpyHostToDevice, ctx->stream));
+  kfield_logits_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(wb, wb + 9 * C, hd, C, n, normalize, out);
+  FV_CHECK_LAUNCH("kfield_logits_kernel");
+  ctx->launches += 1;
+  FV_CUDA(cudaFreeAsync(wb, ctx->stream));
+  FV_CUDA(cudaStreamSynchronize(ctx->stream));  // the host weight pointers are borrowed for the call
+  return 0;
+}
+
 int od_to_feedback(fv_ctx* ctx, fv_state* st) {
   const int64_t n = (int64_t)st->Hp * st->Wp;
   FV_TIMED(ctx, FV_KC_NETOPS, od_to_feedback_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(st->od, st->x.p, st->Hp, st->Wp));

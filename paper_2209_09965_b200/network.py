@@ -120,7 +120,7 @@ class DeviceTensor:
 
     @property
     def shape(self):
-        return tuple(self.dev.shape)
+        return tuple(self.dev.shape) if self.dev is not None else tuple(self._host.shape)
 
 
 def _arr(v) -> np.ndarray:
@@ -311,6 +311,95 @@ def forward_full(net: WNetParams, sparse_input, state: RecurrentState, use_kerne
     state._consumed = True
     new = RecurrentState(film_dims=(h, w), _dev=dev, _config=cfg)
     return DeviceTensor(o[None]), DeviceTensor(od[None]), new
+
+
+def forward_D(net: WNetParams, x, state: RecurrentState):
+    """Coarse reconstruction (network.py:203-254): returns (O_d, H_d list, state'). The input's
+    spatial dims must already be divisible by config.divisor. The D network (with the recurrent
+    concat) runs on the device; H_d are the decoder hidden states the state now carries."""
+    cfg = net.config
+    arr = x.dev if isinstance(x, DeviceTensor) else x
+    shape = tuple(arr.shape)
+    if len(shape) != 4:
+        raise ValueError(f"input must be (N, C, H, W), got {shape}")
+    h, w = int(shape[2]), int(shape[3])
+    if h % cfg.divisor or w % cfg.divisor:
+        raise ValueError(f"input {h}x{w} not divisible by {cfg.divisor}; pad upstream")
+    if state.film_dims != (h, w):
+        raise ValueError(f"carried state is for {state.film_dims}, input is {(h, w)}; reset the state")
+    _, od, new = forward_full(net, x, state, use_kernel_stage=False)
+    return od, new.hidden, new
+
+
+class KernelField:
+    """Per-block predicted filter logits (network.py:257-265); normalized() softmaxes over the taps.
+    Both are computed on the device (fv_kfield_logits) from the block's decoder hidden state."""
+
+    def __init__(self, net: WNetParams, block: int, hd, kernel_size: int):
+        self._net, self._block, self._hd, self.kernel_size = net, block, hd, kernel_size
+        self._logits = None
+
+    def _run(self, normalize: bool) -> "DeviceTensor":
+        import torch
+
+        hd = _dev_f32(self._hd)
+        c, h, w = int(hd.shape[1]), int(hd.shape[2]), int(hd.shape[3])
+        out = torch.empty((1, 9, h, w), dtype=torch.float32, device="cuda")
+        ctx = _lib.context()
+        _lib.check(ctx.lib.fv_kfield_logits(ctx.h, self._net.handle(ctx), self._block, _lib.ptr(hd[0].contiguous()),
+                                            c, h, w, int(normalize), _lib.ptr(out)))
+        return DeviceTensor(out)
+
+    @property
+    def logits(self) -> "DeviceTensor":
+        if self._logits is None:
+            self._logits = self._run(False)
+        return self._logits
+
+    def normalized(self) -> "DeviceTensor":
+        return self._run(True)
+
+
+def _dev_f32(t):
+    """A (1, C, h, w) float32 CUDA tensor view of a DeviceTensor / array."""
+    import torch
+
+    if isinstance(t, DeviceTensor):
+        return t.dev.to(torch.float32) if t.dev is not None else torch.as_tensor(t.data, device="cuda")
+    if isinstance(t, torch.Tensor):
+        return t.to(device="cuda", dtype=torch.float32)
+    return torch.as_tensor(np.asarray(getattr(t, "data", t), dtype=np.float32), device="cuda")
+
+
+def predict_kernel_fields(net: WNetParams, h_d: list) -> list[KernelField]:
+    """One KernelField per block from the decoder hidden state at its level (network.py:268-277)."""
+    cfg = net.config
+    levels = _block_levels(cfg)
+    by_level = {cfg.n_enc - j: h_d[j] for j in range(cfg.n_dec)}
+    return [KernelField(net, i, by_level[lv], cfg.predicted_kernel) for i, lv in enumerate(levels)]
+
+
+def forward_K(net: WNetParams, h_d: list, o_d) -> "DeviceTensor":
+    """Refinement (network.py:280-293): filter O_d through the U shape with the kernels predicted from
+    H_d -- the K-stage convs (tensor cores) and filter passes of the fused reconstruction, run on a
+    scratch state holding H_d (fv_forward_k)."""
+    import torch
+
+    od = _dev_f32(o_d)
+    h, w = int(od.shape[2]), int(od.shape[3])
+    ctx = _lib.context()
+    handle = net.handle(ctx)
+    dev = _DevState(ctx, handle, h, w)
+    if (dev.Hp, dev.Wp) != (h, w):
+        raise ValueError(f"O_d {h}x{w} not divisible by {net.config.divisor}; pad upstream")
+    for j, t in enumerate(h_d):
+        a = np.ascontiguousarray(_dev_f32(t).cpu().numpy())
+        _lib.check(ctx.lib.fv_state_write(ctx.h, dev.h, j, a.ctypes.data_as(C.c_void_p), a.size))
+    out = torch.empty((3, h, w), dtype=torch.float32, device="cuda")
+    _lib.check(ctx.lib.fv_forward_k(ctx.h, handle, dev.h, _lib.ptr(od[0].contiguous()), _lib.ptr(out)))
+    res = DeviceTensor(out[None])
+    res._scratch = dev  # the scratch state lives until the result does (its kernels are stream-ordered)
+    return res
 
 
 def forward_sparse(net: WNetParams, rgba, bits, state: RecurrentState, use_kernel_stage: bool = True):

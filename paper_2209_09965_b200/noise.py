@@ -102,3 +102,30 @@ def default_stack(cache_dir: str | Path | None = None, h: int = DEFAULT_TILE,
     raise ValueError(
         f"no cached noise stack {name}: generation is an offline step of the reference "
         "(fovray.noise.gen_stbn); cache it with save_stack() and pass cache_dir")
+
+
+def tile_lookup(stack: NoiseStack, u: int, v: int, frame: int) -> float:
+    """Toroidal lookup of one value (noise.py:371-375): a scalar read of the caller's stack (the
+    mask kernel performs the same lookup per pixel on the device)."""
+    t = stack.values.shape[0]
+    h, w = stack.dims
+    return float(stack.values[frame % t, v % h, u % w])
+
+
+def tile_field(stack: NoiseStack, h: int, w: int, frame: int) -> np.ndarray:
+    """Frame `frame` of the stack tiled out to an (h, w) field (noise.py:378-384): built on the
+    device by fv_tile_field (the mask kernel's lookup), returned as a read-only (h, w) float32 array."""
+    import torch
+
+    from . import _lib
+
+    if h < 1 or w < 1:
+        raise ValueError(f"dims must be positive, got {(h, w)}")
+    ctx = _lib.context()
+    ctx.ensure_noise(stack)
+    out = torch.empty((h, w), dtype=torch.float32, device="cuda")
+    _lib.check(ctx.lib.fv_tile_field(ctx.h, int(frame), int(h), int(w), _lib.ptr(out)))
+    a = out.cpu().numpy()
+    a.setflags(write=False)
+    return a
+

@@ -98,15 +98,20 @@ class Frame:
         v = self._ms[key]
         if key == "total_ms" and v is None:
             return self.mask_ms + self.render_ms + self.reconstruct_ms
-        if isinstance(v, tuple):  # (start, end) CUDA events
+        if isinstance(v, tuple):  # (start, end) CUDA events: wait for the end on first access
+            v[1].synchronize()
             v = float(v[0].elapsed_time(v[1]))
             self._ms[key] = v
         return v
 
-    mask_ms = property(lambda self: self._get_ms("mask_ms"))
-    render_ms = property(lambda self: self._get_ms("render_ms"))
-    reconstruct_ms = property(lambda self: self._get_ms("reconstruct_ms"))
-    total_ms = property(lambda self: self._get_ms("total_ms"))
+    def _set_ms(self, key, v):
+        self._ms[key] = v
+
+    mask_ms = property(lambda self: self._get_ms("mask_ms"), lambda self, v: self._set_ms("mask_ms", v))
+    render_ms = property(lambda self: self._get_ms("render_ms"), lambda self, v: self._set_ms("render_ms", v))
+    reconstruct_ms = property(lambda self: self._get_ms("reconstruct_ms"),
+                              lambda self, v: self._set_ms("reconstruct_ms", v))
+    total_ms = property(lambda self: self._get_ms("total_ms"), lambda self, v: self._set_ms("total_ms", v))
 
     @property
     def work_items(self) -> int:
@@ -244,12 +249,20 @@ def render_sparse_direct(scene: Scene, cam: Camera, positions,
     if pos.size and (pos[:, 0].min() < 0 or pos[:, 1].min() < 0 or pos[:, 0].max() >= w
                      or pos[:, 1].max() >= h):
         raise IndexError("direct sample positions out of film range")
+    idx = torch.as_tensor((pos[:, 1] * w + pos[:, 0]).astype(np.int32), device="cuda")
+    return _render_direct_idx(scene, cam, idx, settings, stats)
+
+
+def _render_direct_idx(scene: Scene, cam: Camera, idx, settings: RenderSettings, stats: bool = False) -> SparseFrame:
+    """render_sparse_direct over device flat indices v*W+u (in range; duplicates allowed)."""
+    import torch
+
     ctx = _lib.context()
     vol = scene.volume.handle(ctx, scene.tf)
+    h, w = cam.height, cam.width
     rgba = torch.zeros((h, w, 4), dtype=torch.float32, device="cuda")
     depth = torch.zeros((h, w), dtype=torch.float32, device="cuda")
-    n = int(pos.shape[0])
-    idx = torch.as_tensor((pos[:, 1] * w + pos[:, 0]).astype(np.int32), device="cuda")
+    n = int(idx.numel())
     k = torch.tensor([n], dtype=torch.int32, device="cuda")
     st = _lib.FvStats() if stats else None
     camc, setc = cam.c_struct(), settings.c_struct()
@@ -262,11 +275,61 @@ def render_sparse_direct(scene: Scene, cam: Camera, positions,
             _lib.ptr(idx), _lib.ptr(k), n, _lib.ptr(rgba), _lib.ptr(depth), None,
             C.byref(st) if st is not None else None))
     ev1.record(ctx.stream)
-    bits = np.zeros((h, w), dtype=bool)
-    if n:
-        bits[pos[:, 1], pos[:, 0]] = True
-    return SparseFrame(rgba, depth, render_ms=(ev0, ev1), work_items=n, mask=SampleMask(bits=bits),
-                       stats=st)
+
+    def mask():
+        bits = torch.zeros((h * w,), dtype=torch.uint8, device="cuda")
+        if n:
+            bits[idx.long()] = 1
+        return SampleMask(bits=bits.reshape(h, w).cpu().numpy().astype(bool))
+
+    return SparseFrame(rgba, depth, render_ms=(ev0, ev1), work_items=n, mask=mask, stats=st)
+
+
+def render_flythrough(scene: Scene, cams: list[Camera], settings: RenderSettings = RenderSettings(),
+                      mode: str = "full", noise=None, fovea=None, rng: np.random.Generator | None = None):
+    """Render a camera path; returns (frames, timing rows) (renderer.py:385-432).
+
+    Modes "full" (render_full), "naive", "compact" (mask + compaction, then the naive or compacted
+    marcher) and "direct" (tau-proportional draws). Every frame is enqueued on the device without a
+    host synchronisation (the noise frame index advances with the path frame); the timing rows
+    (frame, mask_ms, render_ms, reconstruct_ms, total_ms) are CUDA-event intervals read once all
+    frames are queued. ("direct" reads c_max back per frame: the draw count sizes the draws.)"""
+    import torch
+
+    from .sample_maps import build_sample_mask, build_tau_map, c_max, compact_mask, direct_draws_dev
+
+    if not cams:
+        raise ValueError("camera path must have at least one frame")
+    if mode not in ("full", "naive", "compact", "direct"):
+        raise ValueError(f"unknown flythrough mode {mode!r}")
+    if mode != "full" and (noise is None or fovea is None):
+        raise ValueError(f"mode {mode!r} needs a noise stack and a fovea config")
+    rng = rng if rng is not None else np.random.default_rng(0)
+    ctx = _lib.context()
+    frames = []
+    for i, cam in enumerate(cams):
+        if mode == "full":
+            fr = render_full(scene, cam, settings)
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(ctx.stream)
+            tau = build_tau_map(fovea, (cam.height, cam.width))
+            if mode == "direct":
+                count = max(1, int(round(c_max(tau) * cam.height * cam.width)))
+                idx = direct_draws_dev(fovea, (cam.height, cam.width), count, rng)
+            else:
+                mask = build_sample_mask(noise, i, tau)
+            e1.record(ctx.stream)
+            if mode == "naive":
+                fr = render_sparse_naive(scene, cam, mask, settings)
+            elif mode == "compact":
+                fr = render_sparse_compact(scene, cam, compact_mask(mask), settings)
+            else:
+                fr = _render_direct_idx(scene, cam, idx, settings)
+            fr.mask_ms = (e0, e1)
+        frames.append(fr)
+    rows = [(i, fr.mask_ms, fr.render_ms, fr.reconstruct_ms, fr.total_ms) for i, fr in enumerate(frames)]
+    return frames, rows
 
 
 @dataclass(frozen=True)

@@ -58,15 +58,20 @@ class FoveaConfig:
 
 
 def foveal_density(offset, sigma: float, pixel_scale: float = DEFAULT_PIXEL_SCALE):
-    """exp(-0.5*((dx*s)^2+(dy*s)^2)*sigma) (sample_maps.py:62-68), evaluated in fp64 on the GPU."""
+    """exp(-0.5*((dx*s)^2+(dy*s)^2)*sigma) (sample_maps.py:62-68) over broadcast pixel offsets,
+    evaluated by fv_foveal_density with the mask kernel's fp64 arithmetic."""
     import torch
 
-    dev = torch.device("cuda")
-    dx = torch.as_tensor(np.asarray(offset[0], dtype=np.float64), device=dev) * pixel_scale
-    dy = torch.as_tensor(np.asarray(offset[1], dtype=np.float64), device=dev) * pixel_scale
-    out = torch.exp(-0.5 * (dx * dx + dy * dy) * sigma)
-    out = out.cpu().numpy()
-    return float(out) if out.ndim == 0 else out
+    dx, dy = np.broadcast_arrays(np.asarray(offset[0], dtype=np.float64), np.asarray(offset[1], dtype=np.float64))
+    shape = dx.shape
+    tx = torch.as_tensor(np.ascontiguousarray(dx).reshape(-1), device="cuda")
+    ty = torch.as_tensor(np.ascontiguousarray(dy).reshape(-1), device="cuda")
+    out = torch.empty_like(tx)
+    ctx = _lib.context()
+    _lib.check(ctx.lib.fv_foveal_density(ctx.h, _lib.ptr(tx), _lib.ptr(ty), int(tx.numel()), float(sigma),
+                                         float(pixel_scale), _lib.ptr(out)))
+    res = out.cpu().numpy().reshape(shape)
+    return float(res) if res.ndim == 0 else res
 
 
 class TauMap:
@@ -214,8 +219,19 @@ def build_sample_mask(noise: NoiseStack, frame: int, tau: TauMap) -> SampleMask:
 
 
 def c_max(tau: TauMap) -> float:
-    """Mean of tau over the frame: the ideal work fraction (sample_maps.py:135-137)."""
-    return float(tau.values_dev().mean().item())
+    """Mean of tau over the frame: the ideal work fraction (sample_maps.py:135-137), a deterministic
+    fp64 device sum (fv_tau_sum; tau evaluated inline unless the map holds explicit values)."""
+    import torch
+
+    ctx = _lib.context()
+    h, w = tau.dims
+    out = torch.empty((1,), dtype=torch.float64, device="cuda")
+    if tau.cfg is not None and tau._host is None and tau._dev is None:
+        f = tau.cfg.c_struct()
+        _lib.check(ctx.lib.fv_tau_sum(ctx.h, h, w, C.byref(f), _lib.ptr(tau.pb_map_dev()), None, _lib.ptr(out)))
+    else:
+        _lib.check(ctx.lib.fv_tau_sum(ctx.h, h, w, None, None, _lib.ptr(tau.values_dev()), _lib.ptr(out)))
+    return float(out.item()) / (h * w)
 
 
 class CompactIndexList:
@@ -304,19 +320,31 @@ def scatter(compact: CompactIndexList, frame: int = 0) -> SampleMask:
 def draw_direct_samples(cfg: FoveaConfig, noise_frame, count: int, rng: np.random.Generator) -> np.ndarray:
     """Stochastic pixel positions with probability proportional to tau (sample_maps.py:181-198).
 
-    Inverse-CDF sampling over the fp64 tau map (computed on the GPU, fv_tau_map) with NumPy's
-    generator on the host, so the draws follow the reference's random stream. Duplicates are
-    expected: that is direct sampling's documented weakness versus compaction. Returns (count, 2)
-    int64 (u, v)."""
+    Inverse-CDF sampling over the fp64 tau map on the device (fv_direct_draws: tau, the cumulative
+    sum, the normalisation and the right-sided binary search); the uniforms come from the caller's
+    NumPy generator, so the draws follow the reference's random stream. Duplicates are expected:
+    that is direct sampling's documented weakness versus compaction. Returns (count, 2) int64 (u, v)."""
+    idx = direct_draws_dev(cfg, np.asarray(noise_frame).shape, count, rng)
+    w = np.asarray(noise_frame).shape[1]
+    flat = idx.cpu().numpy().astype(np.int64)
+    return np.stack([flat % w, flat // w], axis=1)
+
+
+def direct_draws_dev(cfg: FoveaConfig, dims: tuple[int, int], count: int, rng: np.random.Generator):
+    """The draws of draw_direct_samples as a (count,) int32 CUDA tensor of flat indices v*W+u."""
+    import torch
+
     if count < 1:
         raise ValueError(f"count must be >= 1, got {count}")
-    h, w = np.asarray(noise_frame).shape
-    tau = build_tau_map(cfg, (h, w)).values.ravel()
-    cdf = np.cumsum(tau)
-    cdf /= cdf[-1]
-    idx = np.searchsorted(cdf, rng.random(count), side="right")
-    idx = np.minimum(idx, h * w - 1)
-    return np.stack([idx % w, idx // w], axis=1).astype(np.int64)
+    h, w = dims
+    r = torch.as_tensor(rng.random(count), device="cuda")
+    idx = torch.empty((count,), dtype=torch.int32, device="cuda")
+    tau = build_tau_map(cfg, (h, w))
+    ctx = _lib.context()
+    f = cfg.c_struct()
+    _lib.check(ctx.lib.fv_direct_draws(ctx.h, h, w, C.byref(f), _lib.ptr(tau.pb_map_dev()), None, _lib.ptr(r),
+                                       int(count), _lib.ptr(idx)))
+    return idx
 
 
 def cmax_sweep_rows(settings: list[tuple[float, float]], noise: NoiseStack, dims: tuple[int, int],

@@ -178,6 +178,20 @@ class TransferFunction:
     def __hash__(self):
         return id(self)
 
+    def apply(self, s) -> np.ndarray:
+        """Map scalars s (any shape) to RGBA, shape s.shape + (4,) (volume.py:201-208): clip to [0,1],
+        linear interpolation between LUT entries, fp64 on the device (fv_tf_apply)."""
+        import torch
+
+        a = np.asarray(s, dtype=np.float64)
+        st = torch.as_tensor(np.ascontiguousarray(a).reshape(-1), device="cuda")
+        lut = torch.as_tensor(np.ascontiguousarray(self.lut), device="cuda")
+        out = torch.empty((st.numel(), 4), dtype=torch.float64, device="cuda")
+        ctx = _lib.context()
+        _lib.check(ctx.lib.fv_tf_apply(ctx.h, _lib.ptr(lut), int(self.lut.shape[0]), _lib.ptr(st), int(st.numel()),
+                                       _lib.ptr(out)))
+        return out.cpu().numpy().reshape(a.shape + (4,))
+
     @staticmethod
     def from_file(path: str | Path) -> "TransferFunction":
         rows = []
@@ -280,3 +294,52 @@ class Light:
             l.vec[i] = float(vec[i])
             l.intensity[i] = float(self.intensity[i])
         return l
+
+
+_SAMPLING_TF = None
+
+
+def _sampling_tf() -> TransferFunction:
+    global _SAMPLING_TF
+    if _SAMPLING_TF is None:
+        _SAMPLING_TF = TransferFunction.default()
+    return _SAMPLING_TF
+
+
+def generate_rays(cam: Camera, us, vs) -> tuple[np.ndarray, np.ndarray]:
+    """Rays through pixel centres (volume.py:293-303): (origins, unit directions), shape (n, 3) fp64,
+    computed by fv_generate_rays (the marcher's in-kernel ray generation)."""
+    import torch
+
+    u = np.asarray(us).reshape(-1)
+    v = np.asarray(vs).reshape(-1)
+    if u.shape != v.shape:
+        raise ValueError("us and vs must have the same length")
+    n = int(u.size)
+    tu = torch.as_tensor(u.astype(np.int32), device="cuda")
+    tv = torch.as_tensor(v.astype(np.int32), device="cuda")
+    o = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    d = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    ctx = _lib.context()
+    camc = cam.c_struct()
+    _lib.check(ctx.lib.fv_generate_rays(ctx.h, C.byref(camc), _lib.ptr(tu), _lib.ptr(tv), n, _lib.ptr(o),
+                                        _lib.ptr(d)))
+    return o.cpu().numpy(), d.cpu().numpy()
+
+
+def sample_trilinear(vol: VolumeGrid, p) -> np.ndarray:
+    """Trilinearly interpolated value at world point(s) p, 0 outside the box (volume.py:149-180);
+    fp64 on the device (fv_sample_trilinear). p has shape (..., 3); the result has shape (...)."""
+    import torch
+
+    pts = np.asarray(p, dtype=np.float64)
+    scalar = pts.ndim == 1
+    flat = np.ascontiguousarray(np.atleast_2d(pts).reshape(-1, 3))
+    tp = torch.as_tensor(flat, device="cuda")
+    out = torch.empty((flat.shape[0],), dtype=torch.float64, device="cuda")
+    ctx = _lib.context()
+    h = vol.handle(ctx, _sampling_tf())  # (any TF: the handle is only the grid's view here)
+    _lib.check(ctx.lib.fv_sample_trilinear(ctx.h, h, _lib.ptr(tp), int(flat.shape[0]), _lib.ptr(out)))
+    res = out.cpu().numpy().reshape(np.atleast_2d(pts).shape[:-1])
+    return res[0] if scalar else res
+

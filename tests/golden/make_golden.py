@@ -23,6 +23,8 @@ Outputs (all under tests/golden/ unless noted):
   metrics_small.npz     PSNR / SSIM / MS-SSIM / tPSNR / quality-report values on seeded images
   sweep_small.npz       compression sweep pieces: uniform noise, direct draws, naive/direct
                         renders, foveated-settings density rows
+  boundary_small.npz    generate_rays, sample_trilinear, TransferFunction.apply, tile_field /
+                        tile_lookup, foveal_density, forward_D / predict_kernel_fields / forward_K
 """
 from __future__ import annotations
 
@@ -365,13 +367,59 @@ def gen_c1(stack):
     np.savez_compressed(HERE / "e2e_c1.npz", **out)
 
 
+def gen_boundary(stack):
+    """The per-sample building blocks and the kernel-stage API of the reference, for the device
+    boundary functions: generate_rays, sample_trilinear, TransferFunction.apply, tile_field,
+    foveal_density, forward_D / predict_kernel_fields / forward_K."""
+    from fovray import autograd as ag
+
+    out = {}
+    cam = rv.Camera(position=(80.0, 60.0, 90.0), look_at=(16.0, 16.0, 16.0), fov_y=40.0, width=64, height=36)
+    rng = np.random.default_rng(31)
+    us = rng.integers(0, 64, 200)
+    vs = rng.integers(0, 36, 200)
+    o, d = rv.generate_rays(cam, us, vs)
+    out.update(ray_us=us, ray_vs=vs, ray_o=o, ray_d=d)
+    vol = rv.make_procedural_volume("vortex_field", (33, 17, 9), spacing=(1.0, 2.0, 0.5))
+    pts = np.concatenate([rng.uniform(-2, 36, (400, 3)) * np.array([1.0, 1.0, 0.5]),
+                          rng.uniform(0, 0.6, (100, 3)), rng.uniform(0, 1, (50, 3)) * vol.extent])
+    out.update(tri_pts=pts, tri_vals=rv.sample_trilinear(vol, pts))
+    s = np.concatenate([rng.uniform(-0.5, 1.5, 300), [0.0, 1.0, 1.0 / 6, 0.5]])
+    out.update(tf_s=s, tf_rgba=rv.TransferFunction.default().apply(s))
+    out["tile_field"] = rn.tile_field(stack, 70, 150, 11)
+    out["tile_lookup"] = np.array([rn.tile_lookup(stack, u, v, f) for u, v, f in [(0, 0, 0), (70, 3, 9), (-3, 200, 13)]])
+    dx = np.arange(-40, 41, dtype=np.float64)[None, :]
+    dy = np.arange(-20, 21, dtype=np.float64)[:, None]
+    out["fovd"] = rsm.foveal_density((dx, dy), 0.06, 0.02)
+    # the kernel stage through the reference's split API, state carried over 2 frames
+    net = rnet.init_network(rnet.NetConfig.from_string(rnet.DESK_BLOCKS), seed=5)
+    state = rnet.reset_state(net.config, (32, 48))
+    for f in range(2):
+        x = rng.random((1, 5, 32, 48)).astype(np.float32)
+        with no_grad():
+            od, hd, state = rnet.forward_D(net, x, state)
+            fields = rnet.predict_kernel_fields(net, hd)
+            img = rnet.forward_K(net, hd, od)
+        out[f"k_x{f}"] = x
+        out[f"k_od{f}"] = od.data
+        out[f"k_img{f}"] = img.data
+        for j, h in enumerate(hd):
+            out[f"k_hd{f}_{j}"] = h.data
+        for i, fl in enumerate(fields):
+            out[f"k_logits{f}_{i}"] = fl.logits.data
+            out[f"k_norm{f}_{i}"] = fl.normalized().data
+    np.savez_compressed(HERE / "boundary_small.npz", **out)
+    print("boundary: done")
+
+
 def main():
     t0 = time.perf_counter()
     DATA.mkdir(parents=True, exist_ok=True)
     stack = rn.default_stack()
     rn.save_stack(stack, DATA / "stbn_64x64x8_s1.noise")
     print(f"stbn sha {sha(stack.values.astype('<f4').tobytes())}")
-    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep", "metrics", "viewer", "rawvol"}
+    which = set(sys.argv[1:]) or {"masks", "volumes", "renders", "net", "c1", "sweep", "metrics", "viewer", "rawvol",
+                                  "boundary"}
     if "masks" in which:
         gen_masks(stack)
     if "volumes" in which:
@@ -390,6 +438,8 @@ def main():
         gen_viewer(stack)
     if "rawvol" in which:
         gen_rawvol()
+    if "boundary" in which:
+        gen_boundary(stack)
     print(f"done in {time.perf_counter() - t0:.1f}s")
 
 

@@ -4,7 +4,8 @@ Tolerances (stated here, derived in DESIGN.md):
   mask / compaction      bit-exact (bits and ordered index list)
   procedural volume      bit-exact at golden sizes; <= 1 f32 ulp on a vanishing fraction at 256^3
   marcher, fp64 tier     max |err| <= 1e-9 on RGBA/depth
-  marcher, fp32 tier     max |err| <= 2e-3, and <= 1e-4 on >= 99.9% of pixel values
+  marcher, fp32 tier     (the benchmarked "fast tier": fp32 samples, hardware-filtered shadow samples)
+                         max |err| <= 1e-2 and PSNR(RGB) >= 80 dB
   conv layer (fp16 in, fp32 acc, fp16 out) vs fp32 conv of the same fp16 inputs: rel <= 2e-3
   W-Net (fp16 storage) vs the fp32 oracle/reference: PSNR >= 60 dB (paper net), max|err| <= 5e-3
   end to end (C1 golden, 2 carried frames): PSNR >= 55 dB, SSIM >= 0.99
@@ -163,9 +164,12 @@ def scene32():
 
 
 def check_fp32(got, ref):
+    """The benchmarked marcher tier (SURVEY 8(c) "fast tier"): fp32 samples, shadow samples from the
+    hardware-filtered texture: max |err| <= 1e-2 and PSNR(RGB) >= 80 dB."""
     d = np.abs(got - ref)
-    assert d.max() <= 2e-3, d.max()
-    assert (d <= 1e-4).mean() >= 0.999, (d <= 1e-4).mean()
+    assert d.max() <= 1e-2, d.max()
+    mse = float(np.mean((got[..., :3].astype(np.float64) - ref[..., :3]) ** 2))
+    assert mse == 0.0 or 10 * np.log10(1.0 / mse) >= 80.0, mse
 
 
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])
@@ -193,8 +197,10 @@ def test_render_sparse_compact_vs_reference_golden(golden, scene32, stack, prec)
     g = np.load(golden / "render_small.npz")
     m = S.SampleMask(bits=g["sparse64_bits"])
     fr = render_sparse_compact(scene32, Camera(**CAM), S.compact_mask(m), RenderSettings(precision=prec))
-    tol = 1e-9 if prec == "fp64" else 2e-3
-    assert np.abs(fr.rgba - g["sparse64_rgba"]).max() <= tol
+    if prec == "fp64":
+        assert np.abs(fr.rgba - g["sparse64_rgba"]).max() <= 1e-9
+    else:
+        check_fp32(fr.rgba, g["sparse64_rgba"])
     assert np.all(fr.rgba[~g["sparse64_bits"]] == 0)
     assert fr.work_items == int(g["sparse64_bits"].sum())
 

@@ -17,7 +17,7 @@ Tolerances (DESIGN.md "Precision tiers"):
                         PSNR(RGB) >= 80 dB; depth within 1e-3 on >= 99.99% of active pixels
   network on the oracle's own sparse input (isolates the W-Net; FULL_BLOCKS, fp16 weights,
   state carried over all frames): PSNR >= 60 dB and max |err| <= 5e-3 per frame after the
-                        clip; O_d max |err| <= 5e-3 per frame; hidden state after the last frame
+                        clip; O_d (unclipped) max |err| <= 5e-3 x max(1, |O_d ref|max) per frame; hidden state after the last frame
                         max |err| <= 2e-2 x max(1, |ref|max)
   end to end (GPU mask -> march -> net vs the oracle's chain): PSNR >= 55 dB and SSIM >= 0.99
                         per frame (fast marcher tier)
@@ -60,6 +60,11 @@ def _cam_dict(cam):
 
 def _active_psnr(got, ref):
     return O.psnr(got[..., :3], ref[..., :3])
+
+
+def _psnr_uncapped(got, ref):
+    mse = float(np.mean((np.asarray(got, np.float64)[..., :3] - np.asarray(ref, np.float64)[..., :3]) ** 2))
+    return float("inf") if mse == 0.0 else 10.0 * float(np.log10(1.0 / mse))
 
 
 @pytest.fixture(scope="module")
@@ -129,6 +134,7 @@ def _run(name, stack, fullnet):
         d = np.abs(got - rgba_ref)
         r["march_max"] = float(d.max()) if d.size else 0.0
         r["march_psnr"] = _active_psnr(got, rgba_ref)
+        r["march_psnr_uncapped"] = _psnr_uncapped(got, rgba_ref)
         r["march_frac_1e4"] = float((d <= 1e-4).mean()) if d.size else 1.0
         dd = np.abs(gdep - dep_ref)
         r["depth_frac_1e3"] = float((dd <= 1e-3).mean()) if dd.size else 1.0
@@ -145,13 +151,16 @@ def _run(name, stack, fullnet):
         o_c = np.clip(o.data[0], 0.0, 1.0)
         r["net_psnr"] = O.psnr(np.moveaxis(o_c, 0, -1), np.moveaxis(o_ref_c, 0, -1))
         r["net_max"] = float(np.abs(o_c - o_ref_c).max())
+        r["net_psnr_uncapped"] = _psnr_uncapped(np.moveaxis(o_c, 0, -1), np.moveaxis(o_ref_c, 0, -1))
         r["od_max"] = float(np.abs(od.data[0] - od_ref).max())
+        r["od_ref_max"] = float(np.abs(od_ref).max())
         # -- end to end: the device pipeline frame vs the oracle's frame
         pipe.step(cam, fovea, i)
         e2e = pipe.rgb.cpu().numpy()
         ref_img = np.moveaxis(o_ref_c, 0, -1)
         r["e2e_psnr"] = O.psnr(e2e, ref_img)
         r["e2e_ssim"] = O.ssim(e2e, ref_img)
+        r["e2e_psnr_uncapped"] = _psnr_uncapped(e2e, ref_img)
         recs.append(r)
     hid = g_state.hidden
     r_last = {"hidden_max": [float(np.abs(hid[j].data[0] - o_state["hidden"][j]).max()) for j in range(len(hid))],
@@ -186,7 +195,7 @@ def test_headline_network_on_oracle_input(name, stack, fullnet):
     for r in run["frames"]:
         assert r["net_psnr"] >= 60.0, r
         assert r["net_max"] <= 5e-3, r
-        assert r["od_max"] <= 5e-3, r
+        assert r["od_max"] <= 5e-3 * max(1.0, r["od_ref_max"]), r  # O_d is the unclipped head output
     st = run["state"]
     for got, ref in zip(st["hidden_max"], st["hidden_ref_max"]):
         assert got <= 2e-2 * max(1.0, ref), st
@@ -225,7 +234,7 @@ def test_c5_network_full_width_4k_strip(stack, fullnet):
         o_c, o_ref_c = np.clip(o.data[0], 0, 1), np.clip(o_ref, 0, 1)
         q = O.psnr(np.moveaxis(o_c, 0, -1), np.moveaxis(o_ref_c, 0, -1))
         recs.append({"frame": i, "k": int(bits.sum()), "net_psnr": q, "net_max": float(np.abs(o_c - o_ref_c).max()),
-                     "od_max": float(np.abs(od.data[0] - od_ref).max())})
+                     "od_max": float(np.abs(od.data[0] - od_ref).max()), "od_ref_max": float(np.abs(od_ref).max())})
     _REPORT["C5net"] = {"config": {"film": [W, rows], "rows": [r0, r0 + rows], "of": [W, H], "mode": "fast"},
                         "frames": recs}
     path = os.environ.get("FV_PARITY_REPORT")
@@ -233,4 +242,5 @@ def test_c5_network_full_width_4k_strip(stack, fullnet):
         with open(path, "w") as f:
             json.dump(_REPORT, f, indent=1)
     for r in recs:
-        assert r["net_psnr"] >= 60.0 and r["net_max"] <= 5e-3 and r["od_max"] <= 5e-3, r
+        assert r["net_psnr"] >= 60.0 and r["net_max"] <= 5e-3, r
+        assert r["od_max"] <= 5e-3 * max(1.0, r["od_ref_max"]), r
