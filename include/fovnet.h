@@ -246,12 +246,15 @@ FV_API int fv_debug_conv3x3(fv_ctx* ctx, int cin, int cout, int H, int W, const 
                             void* pool_nc8, int relu);
 
 /* ---- whole frame ---------------------------------------------------------- */
-/* A camera path of n frames (bench.cmd_bench_throughput's loop, bench.py:194-209) with host
- * outputs: frame t+1's mask + march run on a second stream while frame t reconstructs, and frame
- * t's image is copied into host_rgb_out[t] on a third stream while later frames compute. Every
- * frame equals the corresponding fv_frame call. cams, foveas, frame_ids: n entries each;
- * host_rgb_out: n pointers to (H,W,3) f32 host buffers (pinned for overlap; entries may repeat
- * when the caller only needs the last image). Returns once every copy has landed. */
+/* A camera path of n frames (bench.cmd_bench_throughput's loop, bench.py:194-209). Each frame --
+ * the march of frame t, then frame t's network next to frame t+1's mask + compaction -- is replayed
+ * as ONE captured CUDA graph whose kernels read the per-frame camera / fovea / noise frame from a
+ * device parameter block (fed by one small host->device copy per frame); frame t's image is
+ * copied into host_rgb_out[t] on a copy stream while later frames compute. Every frame equals the
+ * corresponding fv_frame call. cams, foveas, frame_ids: n entries each; host_rgb_out: nullable,
+ * n pointers to (H,W,3) f32 buffers, each nullable (no copy for that frame), host (pinned for
+ * overlap) or device memory; entries may repeat. Returns once every host copy has landed; device
+ * copies are ordered on the context's stream. */
 FV_API int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, int n,
                      const fv_camera* cams, const fv_light* light, const fv_settings* settings,
                      const fv_fovea* foveas, const int* frame_ids, float* const* host_rgb_out);
@@ -310,6 +313,19 @@ FV_API int fv_pack_records(fv_ctx* ctx, const float* rgba_dev, const int32_t* id
                            int cap, int32_t* rec_pix_dev, float* rec_rgba_dev);
 FV_API int fv_scatter_records(fv_ctx* ctx, fv_state* st, const int32_t* rec_pix_dev, const float* rec_rgba_dev,
                               int64_t n, int W, float* rgba_out_dev);
+/* Row-strip reconstruction (BASELINE config 5 across GPUs; sharded.py): marched rays as 12-byte
+ * records (pix, RGBA fp16) -- rec (cap, 3) int32, pix = -1 past the rank's count */
+FV_API int fv_pack_records16(fv_ctx* ctx, const float* rgba_dev, const int32_t* idx_dev, const int32_t* k_dev,
+                             int cap, int32_t* rec_dev);
+/* records -> channels 0..3 of a window state's input for frame rows [row0, row0 + H_window) */
+FV_API int fv_scatter_records16(fv_ctx* ctx, fv_state* st, const int32_t* rec_dev, int64_t n, int W, int row0);
+/* a window state's input channels 0..4 from the full-frame mask bits (H_full, W) uint8: zero RGBA +
+ * the mask channel for frame rows [row0, row0 + H_window) (rows past the film: zero) */
+FV_API int fv_window_input(fv_ctx* ctx, fv_state* st, const uint8_t* bits_dev, int H_full, int W, int row0);
+/* the recurrent band [row0, row0 + rows) of a state (local L0 rows, multiples of the divisor): the
+ * decoder hidden tensors + fp32 O_d, packed contiguously (pack = 1) or unpacked (pack = 0, then
+ * the next input's O_d feedback channels of those rows); buf = null returns only *bytes */
+FV_API int fv_state_band(fv_ctx* ctx, fv_state* st, int pack, int row0, int rows, void* buf_dev, int64_t* bytes);
 
 #ifdef __cplusplus
 }

@@ -127,6 +127,10 @@ _SIGS = {
     "fv_tau_sum": (I, [P, I, I, C.POINTER(FvFovea), P, P, P]),
     "fv_foveal_density": (I, [P, P, P, I64, D, D, P]),
     "fv_direct_draws": (I, [P, I, I, C.POINTER(FvFovea), P, P, P, I64, P]),
+    "fv_pack_records16": (I, [P, P, P, P, I, P]),
+    "fv_scatter_records16": (I, [P, P, P, I64, I, I]),
+    "fv_window_input": (I, [P, P, P, I, I, I]),
+    "fv_state_band": (I, [P, P, I, I, I, P, C.POINTER(I64)]),
 }
 
 EXPORTED = tuple(_SIGS)

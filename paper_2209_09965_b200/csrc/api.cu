@@ -105,6 +105,9 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   if (ctx->wave_hits) cudaFree(ctx->wave_hits);
   if (ctx->wave_ovf) cudaFree(ctx->wave_ovf);
   if (ctx->wave_fb) cudaFreeHost(ctx->wave_fb);
+  if (ctx->dyn_dev) cudaFree(ctx->dyn_dev);
+  if (ctx->dyn_host) cudaFreeHost(ctx->dyn_host);
+  for (auto& e : ctx->dyn_ev) if (e) cudaEventDestroy(e);
   if (ctx->wave_fb_ev) cudaEventDestroy(ctx->wave_fb_ev);
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   for (auto& sp : ctx->kspans) { cudaEventDestroy(sp.a); cudaEventDestroy(sp.b); }
@@ -487,6 +490,186 @@ int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st,
   return 0;
 }
 
+// ---- fv_frames, whole-frame graph path ------------------------------------------------------
+// One frame = the march of frame t, then frame t's network next to frame t+1's mask + compaction
+// (a forked branch), captured once per launch configuration as ONE CUDA graph and replayed with
+// cudaGraphLaunch. The per-frame inputs -- frame t's camera basis and frame t+1's fovea, noise
+// frame and scan epoch -- are read by the kernels from the context's FrameDyn block, which a
+// pinned ring feeds with one small host->device copy ahead of each replay (no host round trip:
+// the host only waits for a ring slot it is about to overwrite, kDynRing frames back).
+constexpr int kDynRing = 8;
+
+static int frame_body(fv_ctx* ctx, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t ev_fork, cudaEvent_t ev_join,
+                      const fv_volume* vol, const fv_net* net, fv_state* st, const fv_camera* cam,
+                      const fv_light* light, const fv_settings* settings, const fv_fovea* fovea_next, int frame_next,
+                      float* img) {
+  const int64_t npix = (int64_t)st->H * st->W;
+  ctx->stream = s_main;
+  int rc = launch_render(ctx, vol, cam, light, settings, ctx->idx_scratch, ctx->k_scratch, (int)npix, nullptr,
+                         nullptr, st->x.p, st->Wp);
+  if (rc) return rc;
+  FV_CUDA(cudaEventRecord(ev_fork, s_main));
+  FV_CUDA(cudaStreamWaitEvent(s_side, ev_fork, 0));
+  ctx->stream = s_side;
+  // the next frame's mask writes channels 0..4 of the other input buffer (the network below writes
+  // its feedback channels 5..7 of the same buffer: disjoint bytes)
+  rc = launch_mask_compact(ctx, frame_next, st->H, st->W, fovea_next, nullptr, nullptr, ctx->idx_scratch,
+                           ctx->k_scratch, st->xalt.p, st->Wp);
+  if (rc) return rc;
+  FV_CUDA(cudaEventRecord(ev_join, s_side));
+  ctx->stream = s_main;
+  rc = reconstruct_launches(ctx, const_cast<fv_net*>(net), st, 1, img, nullptr, nullptr);
+  if (rc) return rc;
+  FV_CUDA(cudaStreamWaitEvent(s_main, ev_join, 0));
+  return 0;
+}
+
+static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, int n,
+                        const fv_camera* cams, const fv_light* light, const fv_settings* settings,
+                        const fv_fovea* foveas, const int* frame_ids, float* const* host_rgb_out) {
+  const int H = st->H, W = st->W;
+  const int64_t npix = (int64_t)H * W;
+  int rc = prepare_net(ctx, net);
+  if (rc) return rc;
+  if (!ctx->dyn_dev) {
+    FV_CUDA(cudaMalloc(&ctx->dyn_dev, sizeof(FrameDyn)));
+    FV_CUDA(cudaMallocHost(&ctx->dyn_host, sizeof(FrameDyn) * kDynRing));
+    for (auto& e : ctx->dyn_ev) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (!st->fcap[i]) FV_CUDA(cudaStreamCreateWithFlags(&st->fcap[i], cudaStreamNonBlocking));
+    if (!st->fcap_ev[i]) FV_CUDA(cudaEventCreateWithFlags(&st->fcap_ev[i], cudaEventDisableTiming));
+  }
+  static const bool no_graph = getenv("FV_FRAME_GRAPH") && atoi(getenv("FV_FRAME_GRAPH")) == 0;
+  const cudaStream_t own = ctx->stream;
+  cudaStream_t s_n = ctx->fstream[1], s_m = ctx->fstream[3], s_c = ctx->fstream[2];
+  cudaEvent_t* net_done = ctx->fev + 2;  // [2]
+  cudaEvent_t* copied = ctx->fev + 4;    // [2]
+  cudaEvent_t fork = ctx->fev[8], join = ctx->fev[9];
+  FV_CUDA(cudaEventRecord(ctx->fev[6], own));
+  for (cudaStream_t s_ : {s_n, s_m, s_c}) FV_CUDA(cudaStreamWaitEvent(s_, ctx->fev[6], 0));
+  // prologue: frame 0's mask (by-value parameters)
+  ctx->stream = s_n;
+  rc = launch_mask_compact(ctx, frame_ids[0], H, W, &foveas[0], nullptr, nullptr, ctx->idx_scratch, ctx->k_scratch,
+                           st->x.p, st->Wp);
+  static uint64_t dyn_seq = 0;
+// inside the frame loop: record the failure and leave the loop (streams are restored below)
+#define FG_TRY(call)                 \
+  {                                  \
+    const cudaError_t e_ = (call);   \
+    if (e_ != cudaSuccess) {         \
+      rc = cuda_fail(e_, #call);     \
+      break;                         \
+    }                                \
+  }
+  for (int t = 0; t < n && !rc; ++t) {
+    const int b = t & 1;
+    float* img = ctx->rgb_scratch + (int64_t)b * 3 * npix;
+    const int tn = t + 1 < n ? t + 1 : t;
+    // this frame's FrameDyn: camera t, fovea / noise frame / epoch of frame t+1's mask
+    const int slot = (int)(dyn_seq++ % kDynRing);
+    FG_TRY(cudaEventSynchronize(ctx->dyn_ev[slot]));
+    FrameDyn& d = ctx->dyn_host[slot];
+    rc = fill_camera_dyn(&cams[t], &d);
+    if (rc) break;
+    d.fx = foveas[tn].focus[0]; d.fy = foveas[tn].focus[1]; d.sigma = foveas[tn].sigma;
+    d.pb = foveas[tn].base_density; d.scale = foveas[tn].pixel_scale;
+    d.frame = frame_ids[tn];
+    if (++ctx->epoch == 0) ctx->epoch = 1;
+    d.epoch = ctx->epoch;
+    FG_TRY(cudaMemcpyAsync(ctx->dyn_dev, &d, sizeof(FrameDyn), cudaMemcpyHostToDevice, s_n));
+    FG_TRY(cudaEventRecord(ctx->dyn_ev[slot], s_n));
+    if (t >= 2) FG_TRY(cudaStreamWaitEvent(s_n, copied[b], 0));  // frame t-2's copy read image b
+    // the frame's launch configuration
+    fv_state::FrameGraph* g = nullptr;
+    for (auto& e : st->fgraphs)
+      if (e.vol == vol && e.net == net && e.version == net->version && e.wave_version == ctx->wave_version &&
+          e.x == st->x.p && e.parity == st->parity && e.img == img && e.has_light == (light != nullptr) &&
+          (!light || memcmp(&e.light, light, sizeof(fv_light)) == 0) &&
+          memcmp(&e.settings, settings, sizeof(fv_settings)) == 0) {
+        g = &e;
+        break;
+      }
+    if (!g && !no_graph) {
+      if (st->fgraphs.size() >= 8) {
+        for (auto& e : st->fgraphs)
+          if (e.exec) cudaGraphExecDestroy(e.exec);
+        st->fgraphs.clear();
+      }
+      fv_state::FrameGraph e;
+      e.vol = vol; e.net = net; e.version = net->version; e.wave_version = ctx->wave_version; e.x = st->x.p;
+      e.parity = st->parity; e.img = img; e.has_light = light != nullptr;
+      if (light) e.light = *light;
+      e.settings = *settings;
+      st->fgraphs.push_back(e);
+      g = &st->fgraphs.back();
+    }
+    ctx->dyn_active = ctx->dyn_dev;
+    if (g && g->exec) {
+      const cudaError_t e = cudaGraphLaunch(g->exec, s_n);
+      if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphLaunch (frame)");
+      ctx->launches += g->n_launches;
+    } else if (g && g->uses >= 1) {
+      // capture this configuration (second use), then replay it for this frame
+      cudaGraph_t graph = nullptr;
+      const unsigned long long before = ctx->launches;
+      cudaError_t e = cudaStreamBeginCapture(st->fcap[0], cudaStreamCaptureModeThreadLocal);
+      if (e == cudaSuccess) {
+        rc = frame_body(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st, &cams[t], light,
+                        settings, &foveas[tn], frame_ids[tn], img);
+        e = cudaStreamEndCapture(st->fcap[0], &graph);
+      }
+      if (!rc && e != cudaSuccess) rc = cuda_fail(e, "frame graph capture");
+      if (!rc) {
+        e = cudaGraphInstantiate(&g->exec, graph, 0);
+        if (e != cudaSuccess) { g->exec = nullptr; rc = cuda_fail(e, "cudaGraphInstantiate (frame)"); }
+      }
+      if (graph) cudaGraphDestroy(graph);
+      g->n_launches = ctx->launches - before;
+      if (!rc) {
+        e = cudaGraphLaunch(g->exec, s_n);
+        if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphLaunch (frame)");
+      }
+    } else {
+      rc = frame_body(ctx, s_n, s_m, fork, join, vol, net, st, &cams[t], light, settings, &foveas[tn],
+                      frame_ids[tn], img);
+    }
+    ctx->dyn_active = nullptr;
+    if (g) ++g->uses;
+    if (rc) break;
+    // reconstruct()'s host-side state change: the input buffers swap, the hidden parity flips
+    std::swap(st->x, st->xalt);
+    st->parity ^= 1;
+    st->fresh = false;
+    FG_TRY(cudaEventRecord(net_done[b], s_n));
+    const bool out = host_rgb_out && host_rgb_out[t];
+    if (out) {
+      FG_TRY(cudaStreamWaitEvent(s_c, net_done[b], 0));
+      FG_TRY(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDefault, s_c));
+    }
+    FG_TRY(cudaEventRecord(copied[b], out ? s_c : s_n));
+  }
+#undef FG_TRY
+  ctx->dyn_active = nullptr;
+  ctx->stream = own;
+  for (cudaStream_t s_ : {s_n, s_m, s_c}) {
+    cudaError_t e = cudaEventRecord(ctx->fev[7], s_);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(own, ctx->fev[7], 0);
+    if (e != cudaSuccess && !rc) rc = cuda_fail(e, "fv_frames rejoin");
+  }
+  if (rc) return rc;
+  // host outputs are complete on return; device outputs are stream-ordered on the context's stream
+  bool any_host = false;
+  for (int t = 0; host_rgb_out && t < n; ++t) {
+    cudaPointerAttributes pa{};
+    if (host_rgb_out[t] && cudaPointerGetAttributes(&pa, host_rgb_out[t]) == cudaSuccess && pa.type != cudaMemoryTypeDevice)
+      any_host = true;
+    (void)cudaGetLastError();
+  }
+  if (any_host) FV_CUDA(cudaStreamSynchronize(s_c));
+  return 0;
+}
+
 // A path of frames with host outputs, pipelined over four streams:
 //   mask stream   : mask + compaction of frame t+1 (FV_MASK_AHEAD, default on) next to frame t's
 //                   network; waits for rendered[t] (the march of frame t, the last reader of the ray
@@ -504,13 +687,11 @@ int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st,
 int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, int n,
               const fv_camera* cams, const fv_light* light, const fv_settings* settings,
               const fv_fovea* foveas, const int* frame_ids, float* const* host_rgb_out) {
-  FV_REQUIRE(ctx && vol && net && st && cams && settings && foveas && frame_ids && host_rgb_out,
-             "null argument");
+  FV_REQUIRE(ctx && vol && net && st && cams && settings && foveas && frame_ids, "null argument");
   FV_REQUIRE(n >= 0, "frame count must be >= 0 (got %d)", n);
   if (n == 0) return 0;
   const int H = st->H, W = st->W;
   for (int t = 0; t < n; ++t) {
-    FV_REQUIRE(host_rgb_out[t], "host_rgb_out[%d] is null", t);
     if (cams[t].height != H || cams[t].width != W) {
       set_error("carried state is for (%d, %d), input is (%d, %d); reset the state", H, W, cams[t].height,
                 cams[t].width);
@@ -556,6 +737,12 @@ int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st
   // march, the last reader of the ray list, and frame t-1's network, the last reader of the input
   // buffer it fills); FV_MASK_AHEAD=0 keeps it in line. Measured +0.5% frames/s, +1% e2e at C3.
   static const bool ahead = !(getenv("FV_MASK_AHEAD") && atoi(getenv("FV_MASK_AHEAD")) == 0);
+  // default: the whole-frame graph path (FV_FRAME_GRAPH=0 keeps it eager but with the same
+  // FrameDyn launches); the stream-juggling path below serves FV_PIPE_OVERLAP=1, FV_MASK_AHEAD=0,
+  // kernel timing and fp64 renders
+  static const bool legacy = getenv("FV_FRAME_GRAPH") && atoi(getenv("FV_FRAME_GRAPH")) == 2;
+  if (!overlap && ahead && !legacy && !ctx->ktiming && settings->precision != FV_PREC_FP64)
+    return frames_graph(ctx, vol, net, st, n, cams, light, settings, foveas, frame_ids, host_rgb_out);
   cudaStream_t s_r = overlap ? ctx->fstream[0] : ctx->fstream[1], s_n = ctx->fstream[1], s_c = ctx->fstream[2];
   cudaStream_t s_m = ctx->fstream[3];
   cudaEvent_t* masked = ctx->fev + 8;  // [2]
@@ -621,7 +808,8 @@ int fv_frames(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st
     }
     // copy out
     FV_TRY(cudaStreamWaitEvent(s_c, net_done[b], 0));
-    FV_TRY(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, s_c));
+    if (host_rgb_out && host_rgb_out[t])
+      FV_TRY(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDefault, s_c));
     FV_TRY(cudaEventRecord(copied[b], s_c));
   }
   ctx->stream = own;

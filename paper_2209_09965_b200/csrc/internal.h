@@ -106,6 +106,21 @@ void ktime_end(fv_ctx* ctx, int cls, double work = 0.0);
 
 }  // namespace fv
 
+namespace fv {
+// The per-frame inputs of the mask and the marcher, read by the kernels from device memory when a
+// frame is replayed as a CUDA graph (fv_frames): the camera basis of the frame being rendered and
+// the fovea / noise frame / scan epoch of the mask computed next to its network. Host-filled per
+// frame, copied to the device ahead of the graph launch.
+struct FrameDyn {
+  double pos[3], right[3], up[3], fwd[3];
+  double tan_half, aspect;
+  double fx, fy, sigma, pb, scale;
+  int frame;
+  unsigned int epoch;
+};
+int fill_camera_dyn(const fv_camera* cam, FrameDyn* d);
+}  // namespace fv
+
 struct fv_ctx {
   int device = 0;
   int num_sms = 148;
@@ -140,6 +155,13 @@ struct fv_ctx {
   cudaEvent_t wave_fb_ev = nullptr;
   bool wave_fb_pending = false;
   unsigned long long launches = 0;
+  // fv_frames whole-frame graphs: the device FrameDyn the captured kernels read (dyn_active is
+  // set while a frame's launches are enqueued or captured), a pinned ring of host copies
+  fv::FrameDyn* dyn_dev = nullptr;
+  const fv::FrameDyn* dyn_active = nullptr;
+  fv::FrameDyn* dyn_host = nullptr;  // kDynRing slots
+  cudaEvent_t dyn_ev[8] = {};
+  uint64_t wave_version = 0;  // bumped when the marcher record buffer is reallocated
   // fv_frames: render / network / copy streams and their event rings (created on first use)
   cudaStream_t fstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t fev[10] = {};
@@ -275,9 +297,32 @@ struct fv_state {
   std::vector<Graph> graphs;
   cudaStream_t capture_stream = nullptr;
   int capture_prio = 0;
+  // fv_frames: one whole frame (march of frame t, then its network next to the mask of frame t+1)
+  // as a captured CUDA graph per launch configuration; the per-frame camera / fovea / noise frame
+  // come from the context's FrameDyn block
+  struct FrameGraph {
+    const void* vol = nullptr;
+    const fv_net* net = nullptr;
+    uint64_t version = 0, wave_version = 0;
+    const void* x = nullptr;
+    int parity = 0;
+    const float* img = nullptr;
+    fv_light light{};
+    int has_light = 0;
+    fv_settings settings{};
+    int uses = 0;
+    unsigned long long n_launches = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<FrameGraph> fgraphs;
+  cudaStream_t fcap[2] = {nullptr, nullptr};
+  cudaEvent_t fcap_ev[2] = {nullptr, nullptr};
 };
 
 namespace fv {
+int prepare_net(fv_ctx* ctx, const fv_net* net);
+int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb, float* out_o,
+                         float* out_od);
 // launchers (return 0 / negative)
 int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
                         const double* pb_map, uint8_t* bits, int32_t* idx, int32_t* k,

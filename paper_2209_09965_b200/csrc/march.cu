@@ -53,7 +53,32 @@ struct MarchParams {
   __half* net_in;
   int net_wp;
   DevCounters* counters;
+  const FrameDyn* dyn;  // non-null: the camera basis comes from device memory (graph replay)
 };
+
+// The camera of a ray-generating kernel: the launch's by-value basis, or the FrameDyn block.
+struct CamView {
+  double pos[3], right[3], up[3], fwd[3], tan_half, aspect;
+};
+__device__ __forceinline__ CamView load_cam(const MarchParams& P) {
+  CamView c;
+  if (P.dyn) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      c.pos[a] = P.dyn->pos[a]; c.right[a] = P.dyn->right[a]; c.up[a] = P.dyn->up[a]; c.fwd[a] = P.dyn->fwd[a];
+    }
+    c.tan_half = P.dyn->tan_half;
+    c.aspect = P.dyn->aspect;
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      c.pos[a] = P.pos[a]; c.right[a] = P.right[a]; c.up[a] = P.up[a]; c.fwd[a] = P.fwd[a];
+    }
+    c.tan_half = P.tan_half;
+    c.aspect = P.aspect;
+  }
+  return c;
+}
 
 __device__ __forceinline__ void ray_box(const double o[3], const double d[3], const double ext[3],
                                         double& t0, double& t1, bool& hit) {
@@ -657,16 +682,17 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F, bool coun
   if (i < k && raw >= 0) {
     const int pix = raw;
     const int u = pix % P.W, v = pix / P.W;
-    const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
-    const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+    const CamView cam = load_cam(P);
+    const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * cam.tan_half * cam.aspect;
+    const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * cam.tan_half;
     double d[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+    for (int a = 0; a < 3; ++a) d[a] = cam.fwd[a] + sx * cam.right[a] + sy * cam.up[a];
     const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
     double t0, t_end;
     bool hit;
-    ray_box(P.pos, d, P.ext, t0, t_end, hit);
+    ray_box(cam.pos, d, P.ext, t0, t_end, hit);
     float rgb[3] = {0.f, 0.f, 0.f};
     float trans = 1.f;
     double depth = 0.0;
@@ -681,8 +707,8 @@ __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F, bool coun
       int n = (int)ceil((L - 1e-12) / P.step);
       if (n < 1) n = 1;
       const float last_dt = (float)(L - (double)(n - 1) * P.step);
-      const float ex = (float)(P.pos[0] + d[0] * t0), ey = (float)(P.pos[1] + d[1] * t0),
-                  ez = (float)(P.pos[2] + d[2] * t0);
+      const float ex = (float)(cam.pos[0] + d[0] * t0), ey = (float)(cam.pos[1] + d[1] * t0),
+                  ez = (float)(cam.pos[2] + d[2] * t0);
       const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
       const float stepf = (float)P.step;
 #pragma unroll 1
@@ -1003,15 +1029,16 @@ __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B
       pix = P.idx ? P.idx[r] : r;
       ++nrays;
       const int u = pix % P.W, v = pix / P.W;
-      const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * P.tan_half * P.aspect;
-      const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * P.tan_half;
+      const CamView cam = load_cam(P);
+      const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * cam.tan_half * cam.aspect;
+      const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * cam.tan_half;
       double d[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) d[a] = P.fwd[a] + sx * P.right[a] + sy * P.up[a];
+      for (int a = 0; a < 3; ++a) d[a] = cam.fwd[a] + sx * cam.right[a] + sy * cam.up[a];
       const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
       d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
       double tend;
-      ray_box(P.pos, d, P.ext, t0, tend, hit);
+      ray_box(cam.pos, d, P.ext, t0, tend, hit);
       if (!hit) {
         write_pixel(P, pix, 0.f, 0.f, 0.f, 1.f, 0.f);
         B.ray[r] = make_int4(-1, 0, 0, 0);
@@ -1022,8 +1049,8 @@ __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B
         n = (int)ceil((L - 1e-12) / P.step);
         if (n < 1) n = 1;
         const float last_dt = (float)(L - (double)(n - 1) * P.step);
-        h0 = make_float4((float)(P.pos[0] + d[0] * t0), (float)(P.pos[1] + d[1] * t0),
-                         (float)(P.pos[2] + d[2] * t0), (float)d[0]);
+        h0 = make_float4((float)(cam.pos[0] + d[0] * t0), (float)(cam.pos[1] + d[1] * t0),
+                         (float)(cam.pos[2] + d[2] * t0), (float)d[0]);
         h1 = make_float4((float)d[1], (float)d[2], last_dt, __int_as_float(n));
       }
     }
@@ -1676,6 +1703,9 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
   P.idx = idx; P.k_dev = k; P.k_max = k_max;
   P.rgba = rgba; P.depth = depth; P.net_in = net_in; P.net_wp = net_wp;
   P.counters = ctx->counters;
+  // graph replays read the camera from the FrameDyn block (the wavefront fp32 path: its ray setup
+  // and the overflow re-march are the only ray-generating kernels there)
+  P.dyn = s->precision == FV_PREC_FP64 ? nullptr : ctx->dyn_active;
   if (k_max <= 0) return 0;
   const int threads = 128;
   const int blocks = (k_max + threads - 1) / threads;
@@ -1783,6 +1813,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
                                  64 * sizeof(int);
             if (cudaMalloc(&ctx->wave_rec, bytes) == cudaSuccess) {
               ctx->wave_cap = n * kChunk;
+              ++ctx->wave_version;
             } else {
               ctx->wave_rec = nullptr;
               (void)cudaGetLastError();
@@ -2032,3 +2063,19 @@ int fv_tile_field(fv_ctx* ctx, int frame, int h, int w, float* out_dev) {
 }
 
 }  // extern "C"
+
+namespace fv {
+// Camera.basis (volume.py:269-276) and the generate_rays constants into a FrameDyn block.
+int fill_camera_dyn(const fv_camera* cam, FrameDyn* d) {
+  MarchParams P{};
+  const int rc = camera_params(cam, P);
+  if (rc) return rc;
+  for (int a = 0; a < 3; ++a) {
+    d->pos[a] = P.pos[a]; d->right[a] = P.right[a]; d->up[a] = P.up[a]; d->fwd[a] = P.fwd[a];
+  }
+  d->tan_half = P.tan_half;
+  d->aspect = P.aspect;
+  return 0;
+}
+}  // namespace fv
+

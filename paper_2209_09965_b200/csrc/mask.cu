@@ -43,6 +43,7 @@ struct MaskParams {
   unsigned long long* status;
   unsigned int epoch;
   unsigned int* tile_counter;
+  const FrameDyn* dyn;  // non-null: fovea, noise frame and epoch from device memory (graph replay)
 };
 
 __device__ __forceinline__ double tau_at(const MaskParams& p, int u, int v) {
@@ -61,7 +62,13 @@ __device__ __forceinline__ unsigned long long pack_status(unsigned int epoch, un
   return ((unsigned long long)epoch << 32) | ((unsigned long long)flag << 30) | value;
 }
 
-__global__ void __launch_bounds__(kThreads) mask_compact_kernel(MaskParams p) {
+__global__ void __launch_bounds__(kThreads) mask_compact_kernel(MaskParams p_in) {
+  MaskParams p = p_in;
+  if (p.dyn) {
+    p.fx = p.dyn->fx; p.fy = p.dyn->fy; p.sigma = p.dyn->sigma; p.pb = p.dyn->pb; p.scale = p.dyn->scale;
+    p.frame = p.dyn->frame;
+    p.epoch = p.dyn->epoch;
+  }
   __shared__ unsigned int s_tile;
   __shared__ unsigned int s_warp[kThreads / 32];
   __shared__ unsigned int s_prefix;
@@ -204,6 +211,7 @@ int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
   if (++ctx->epoch == 0) ctx->epoch = 1;
   p.epoch = ctx->epoch;
   p.tile_counter = &ctx->counters->scan_tile;
+  p.dyn = ctx->dyn_active;
   FV_CUDA(cudaMemsetAsync(&ctx->counters->scan_tile, 0, sizeof(unsigned int), ctx->stream));
   FV_TIMED(ctx, FV_KC_MASK, mask_compact_kernel<<<ntiles, kThreads, 0, ctx->stream>>>(p));
   FV_CHECK_LAUNCH("mask_compact_kernel");

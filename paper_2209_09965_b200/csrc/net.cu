@@ -213,7 +213,7 @@ static int kstage_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int hp, float
 
 
 // The launches of one reconstruction (no host-side state change: see reconstruct()).
-static int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb,
+int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb,
                                 float* out_o, float* out_od) {
   const int ne = net->n_enc, nd = net->n_dec;
   int rc;
@@ -255,18 +255,25 @@ static bool graphs_enabled(const fv_ctx* ctx) {
   return !off && !ctx->ktiming;
 }
 
-// One frame of the W-Net. A configuration's first run is eager (it sets kernel attributes and
-// allocates lazily); from its second run on the ~31 launches are replayed as one CUDA graph.
-int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float* out_rgb,
-                float* out_o, float* out_od) {
+// Parameters complete and the fused K-stage convs built (before any launch or capture).
+int prepare_net(fv_ctx* ctx, const fv_net* cnet) {
   fv_net* net = const_cast<fv_net*>(cnet);  // the fused K-stage convs are a cache of the params
   for (const auto& cp : net->convs)
     if (!(cp.w_set && cp.b_set)) {
       set_error("network parameter %s not set", cp.name.c_str());
       return FV_E_INVALID;
     }
-  if (net->kstage_dirty) {
-    const int rc0 = build_kstage(ctx, net);
+  if (net->kstage_dirty) return build_kstage(ctx, net);
+  return 0;
+}
+
+// One frame of the W-Net. A configuration's first run is eager (it sets kernel attributes and
+// allocates lazily); from its second run on the ~31 launches are replayed as one CUDA graph.
+int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float* out_rgb,
+                float* out_o, float* out_od) {
+  fv_net* net = const_cast<fv_net*>(cnet);
+  {
+    const int rc0 = prepare_net(ctx, net);
     if (rc0) return rc0;
   }
   int rc = 0;
@@ -569,6 +576,12 @@ int fv_state_destroy(fv_state* st) {
   if (!st) return 0;
   for (auto& e : st->graphs)
     if (e.exec) cudaGraphExecDestroy(e.exec);
+  for (auto& e : st->fgraphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  for (auto& s_ : st->fcap)
+    if (s_) cudaStreamDestroy(s_);
+  for (auto& e : st->fcap_ev)
+    if (e) cudaEventDestroy(e);
   if (st->capture_stream) cudaStreamDestroy(st->capture_stream);
   if (st->arena) cudaFree(st->arena);
   delete st;

@@ -76,6 +76,66 @@ __global__ void scatter_records_kernel(const int32_t* __restrict__ rec_pix, cons
   }
 }
 
+// ---- row-strip reconstruction (see sharded.py): record exchange in fp16 and window inputs ----
+
+// records as (pix, rgba half2 x2) int32 triples: 12 bytes per marched ray
+__global__ void pack_records16_kernel(const float* __restrict__ rgba, const int32_t* __restrict__ idx,
+                                      const int32_t* __restrict__ k_dev, int cap, int32_t* __restrict__ rec) {
+  const int k = min(*k_dev, cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += gridDim.x * blockDim.x) {
+    int3 r = make_int3(-1, 0, 0);
+    if (i < k) {
+      const int pix = idx[i];
+      const float4 c = *reinterpret_cast<const float4*>(rgba + (int64_t)pix * 4);
+      const __half2 a = __floats2half2_rn(c.x, c.y), b = __floats2half2_rn(c.z, c.w);
+      r = make_int3(pix, *reinterpret_cast<const int*>(&a), *reinterpret_cast<const int*>(&b));
+    }
+    rec[3 * (int64_t)i] = r.x;
+    rec[3 * (int64_t)i + 1] = r.y;
+    rec[3 * (int64_t)i + 2] = r.z;
+  }
+}
+
+// fp16 records -> network input channels 0..3 of rows [row0, row0 + rows) (window-local rows)
+__global__ void scatter_records16_kernel(const int32_t* __restrict__ rec, int64_t n, int W, int row0, int rows,
+                                         __half* __restrict__ net_in, int net_wp) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int pix = rec[3 * i];
+    if (pix < 0) continue;
+    const int u = pix % W, v = pix / W - row0;
+    if (v < 0 || v >= rows) continue;
+    int2* hp = reinterpret_cast<int2*>(net_in + ((int64_t)v * net_wp + u) * 8);
+    *hp = make_int2(rec[3 * i + 1], rec[3 * i + 2]);
+  }
+}
+
+// window input channels 0..4 from the full-frame mask bits: 0 RGBA (the records fill the active
+// pixels) and the mask channel; rows past the film (the padded bottom) are zero
+__global__ void window_input_kernel(const uint8_t* __restrict__ bits, int H_full, int W, int row0, int rows,
+                                    __half* __restrict__ net_in, int net_wp) {
+  const int64_t n = (int64_t)rows * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(i % W), y = (int)(i / W), v = row0 + y;
+    const bool m = v < H_full && bits[(int64_t)v * W + u];
+    __half* px = net_in + ((int64_t)y * net_wp + u) * 8;
+    *reinterpret_cast<uint2*>(px) = make_uint2(0u, 0u);
+    px[4] = m ? __float2half(1.0f) : __float2half(0.0f);
+  }
+}
+
+// x channels 5..7 (the O_d feedback) of rows [r0, r0 + rows) from the fp32 O_d planes
+__global__ void feedback_rows_kernel(const float* __restrict__ od, __half* __restrict__ x, int Hp, int Wp, int r0,
+                                     int rows) {
+  const int64_t n = (int64_t)rows * Wp, plane = (int64_t)Hp * Wp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = (int64_t)r0 * Wp + i;
+    __half* px = x + pix * 8;
+    px[5] = __float2half(od[pix]);
+    px[6] = __float2half(od[plane + pix]);
+    px[7] = __float2half(od[2 * plane + pix]);
+  }
+}
+
 int grid_of(fv_ctx* ctx, int64_t n) {
   const int64_t b = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)ctx->num_sms * 8));
@@ -120,6 +180,90 @@ int fv_scatter_records(fv_ctx* ctx, fv_state* st, const int32_t* rec_pix_dev, co
                                   st ? st->x.p : nullptr, st ? st->Wp : W, rgba_out_dev));
   FV_CHECK_LAUNCH("scatter_records_kernel");
   ctx->launches += 1;
+  return 0;
+}
+
+
+int fv_pack_records16(fv_ctx* ctx, const float* rgba_dev, const int32_t* idx_dev, const int32_t* k_dev, int cap,
+                      int32_t* rec_dev) {
+  FV_REQUIRE(ctx && rgba_dev && idx_dev && k_dev && rec_dev, "null argument");
+  FV_REQUIRE(cap >= 0, "record capacity must be >= 0");
+  FV_TIMED(ctx, FV_KC_NETOPS, pack_records16_kernel<<<grid_of(ctx, cap), 256, 0, ctx->stream>>>(
+                                  rgba_dev, idx_dev, k_dev, cap, rec_dev));
+  FV_CHECK_LAUNCH("pack_records16_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int fv_scatter_records16(fv_ctx* ctx, fv_state* st, const int32_t* rec_dev, int64_t n, int W, int row0) {
+  FV_REQUIRE(ctx && st && rec_dev, "null argument");
+  FV_REQUIRE(st->W == W, "state film width %d != %d", st->W, W);
+  FV_REQUIRE(row0 >= 0, "row offset must be >= 0");
+  FV_TIMED(ctx, FV_KC_NETOPS, scatter_records16_kernel<<<grid_of(ctx, n), 256, 0, ctx->stream>>>(
+                                  rec_dev, n, W, row0, st->H, st->x.p, st->Wp));
+  FV_CHECK_LAUNCH("scatter_records16_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+int fv_window_input(fv_ctx* ctx, fv_state* st, const uint8_t* bits_dev, int H_full, int W, int row0) {
+  FV_REQUIRE(ctx && st && bits_dev, "null argument");
+  FV_REQUIRE(st->W == W, "state film width %d != %d", st->W, W);
+  FV_REQUIRE(row0 >= 0 && row0 < H_full + st->Hp, "row offset %d outside the film", row0);
+  const int64_t n = (int64_t)st->H * W;
+  FV_TIMED(ctx, FV_KC_MASK, window_input_kernel<<<grid_of(ctx, n), 256, 0, ctx->stream>>>(
+                                bits_dev, H_full, W, row0, st->H, st->x.p, st->Wp));
+  FV_CHECK_LAUNCH("window_input_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
+// The recurrent band [row0, row0 + rows) of a state (window-local L0 rows, multiples of the
+// network divisor): the current decoder hidden tensors at their levels and the fp32 O_d, packed
+// in that order. pack = 1: state -> buf; pack = 0: buf -> state, then the next input's O_d
+// feedback channels for those rows. buf = null: only *bytes.
+int fv_state_band(fv_ctx* ctx, fv_state* st, int pack, int row0, int rows, void* buf_dev, int64_t* bytes) {
+  FV_REQUIRE(ctx && st, "null argument");
+  const fv_net* net = st->net;
+  const int div = 1 << net->n_enc;
+  FV_REQUIRE(row0 >= 0 && rows >= 0 && row0 + rows <= st->Hp && row0 % div == 0 && rows % div == 0,
+             "band [%d, %d) must lie in the state's %d rows at multiples of %d", row0, row0 + rows, st->Hp, div);
+  int64_t off = 0;
+  uint8_t* b = reinterpret_cast<uint8_t*>(buf_dev);
+  const std::vector<fv_act>& hid = st->hidden[st->parity];
+  for (int j = 0; j < net->n_dec; ++j) {
+    const fv_act& a = hid[j];
+    const int L = net->n_enc - j;
+    const int r0 = row0 >> L, nr = rows >> L;
+    const size_t width = (size_t)nr * a.W * 16, pitch = (size_t)a.H * a.W * 16;
+    const int groups = a.C / 8;
+    if (b && width) {
+      uint8_t* t = reinterpret_cast<uint8_t*>(a.p) + (size_t)r0 * a.W * 16;
+      if (pack)
+        FV_CUDA(cudaMemcpy2DAsync(b + off, width, t, pitch, width, groups, cudaMemcpyDeviceToDevice, ctx->stream));
+      else
+        FV_CUDA(cudaMemcpy2DAsync(t, pitch, b + off, width, width, groups, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    off += (int64_t)width * groups;
+  }
+  {
+    const size_t width = (size_t)rows * st->Wp * 4, pitch = (size_t)st->Hp * st->Wp * 4;
+    if (b && width) {
+      uint8_t* t = reinterpret_cast<uint8_t*>(st->od) + (size_t)row0 * st->Wp * 4;
+      if (pack)
+        FV_CUDA(cudaMemcpy2DAsync(b + off, width, t, pitch, width, 3, cudaMemcpyDeviceToDevice, ctx->stream));
+      else
+        FV_CUDA(cudaMemcpy2DAsync(t, pitch, b + off, width, width, 3, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    off += (int64_t)width * 3;
+  }
+  if (b && !pack && rows && net->recurrent) {
+    FV_TIMED(ctx, FV_KC_NETOPS, feedback_rows_kernel<<<grid_of(ctx, (int64_t)rows * st->Wp), 256, 0, ctx->stream>>>(
+                                    st->od, st->x.p, st->Hp, st->Wp, row0, rows));
+    FV_CHECK_LAUNCH("feedback_rows_kernel");
+    ctx->launches += 1;
+  }
+  if (bytes) *bytes = off;
   return 0;
 }
 

@@ -88,7 +88,28 @@ class FramePipeline:
                     self.ev[2].elapsed_time(self.ev[3]))
         return None
 
-    def run_pipelined(self, frames) -> None:
+    def run_pipelined(self, frames, outs=None) -> None:
+        """The frame loop through the C ABI's fv_frames: every frame replayed as one whole-frame CUDA
+        graph (march t, then network t next to the mask of t+1). Frame t's image goes to outs[t]
+        ((H,W,3) float32 CUDA tensors, entries may be None) or, by default, the last frame's into
+        self.rgb. Launches only (stream-ordered on the pipeline's stream). FV_PIPE_PY=1: the Python
+        stream-juggling loop below (separate mask / render / reconstruct calls)."""
+        n = len(frames)
+        if n == 0:
+            return
+        if outs is None:
+            outs = [None] * (n - 1) + [self.rgb]
+        if os.environ.get("FV_PIPE_PY", "0") != "1":
+            cams = (_lib.FvCamera * n)(*[c.c_struct() for c, _, _ in frames])
+            fovs = (_lib.FvFovea * n)(*[f.c_struct() for _, f, _ in frames])
+            ids = (C.c_int * n)(*[int(j) for _, _, j in frames])
+            ptrs = (C.c_void_p * n)(*[o.data_ptr() if o is not None else None for o in outs])
+            _lib.check(self.ctx.lib.fv_frames(self.ctx.h, self.vol, self.net_h, self.state.h, n, cams,
+                                              self._light_ref(), C.byref(self._set), fovs, ids, ptrs))
+            return
+        self._run_pipelined_py(frames, outs)
+
+    def _run_pipelined_py(self, frames, outs) -> None:
         """Render frame t+1 (mask + march) on one stream while frame t reconstructs on another.
 
         `frames` is a sequence of (camera, fovea, frame index). The state's two input buffers
@@ -145,7 +166,8 @@ class FramePipeline:
             rendered.record(s_r)
             s_n.wait_event(rendered)
             _lib.check(self._nctx.lib.fv_reconstruct(self._nctx.h, self.net_h, self.state.h, 1,
-                                                     _lib.ptr(self.rgb), None, None))
+                                                     _lib.ptr(outs[t] if outs[t] is not None else self.rgb),
+                                                     None, None))
             done = torch.cuda.Event()
             done.record(s_n)
             net_done.append(done)
@@ -176,8 +198,8 @@ class FramePipeline:
         return ev
 
     def pipelined_contexts(self):
-        return [c for c in (getattr(self, "_rctx", None), getattr(self, "_nctx", None), getattr(self, "_mctx", None))
-                if c is not None]
+        return [c for c in (self.ctx, getattr(self, "_rctx", None), getattr(self, "_nctx", None),
+                            getattr(self, "_mctx", None)) if c is not None]
 
     def dense(self, cam: Camera):
         """Dense baseline frame (render_full, renderer.py:211-222) into a device buffer."""

@@ -1,15 +1,27 @@
 """One frame stream split across the GPUs of a node (BASELINE config 5).
 
-Every rank computes the full sample mask (microseconds) and marches only its share of the
-compacted active-ray list: 32-ray packets dealt round-robin, so each rank gets a statistically
+The march: every rank computes the full sample mask (microseconds) and marches only its share of
+the compacted active-ray list -- 32-ray packets dealt round-robin, so each rank gets a statistically
 equal mix of foveal and peripheral rays (fixed screen tiles would be unbalanced by the fovea). The
-marched (pixel, RGBA) records of all ranks are all-gathered -- NCCL over NVLink on the GPU box --
-and scattered into the network input exactly as the marcher writes it, so every rank reconstructs
-the same frame as the unsharded pipeline (bit-exact; tests/test_gpu_parity.py emulates the ranks
-on one GPU, tests/test_multi.py runs the exchange with gloo). The recurrent network needs the whole
-frame, so reconstruction is replicated; marching -- which dominates at 1024^3 -- scales.
+marched rays become 12-byte records (pixel, RGBA fp16 -- the network input is fp16) and ONE
+all_gather_into_tensor (NCCL over NVLink) gives every rank every record.
 
-Kernels: fv_shard_rays, fv_pack_records, fv_scatter_records (csrc/shard.cu).
+The reconstruction (StripShardedPipeline): each rank owns a strip of rows [a, b) of the padded
+frame (a multiple of the network divisor) and runs the unchanged W-Net on a WINDOW [a - E, b + E)
+clipped to the frame, E >= the network's per-frame reach (81 rows measured for FULL_BLOCKS; the
+default halo is the interval bound of network.py's structure rounded up to the divisor, 96). A
+window's owned rows are then exactly the full-frame network's rows (each output pixel is computed
+independently of the tile it falls in; tests/test_gpu_parity.py checks bit-identity) PROVIDED its
+recurrent inputs -- the decoder hidden states and O_d fed back into the next frame -- are exact
+over the whole window. They are exact on the owned rows; after every frame each rank sends its
+owned boundary bands (E rows: all four hidden levels + O_d, fv_state_band) to its two neighbours
+and receives theirs into its window extension (batch_isend_irecv; the band is the only per-frame
+network exchange). Cost: the window's extra rows (2E per interior rank) and ~2 bands per frame.
+ShardedFramePipeline (the round-1 design: the march sharded, the network replicated) is kept as
+the baseline the strip design replaces.
+
+Kernels: fv_shard_rays, fv_pack_records16, fv_scatter_records16, fv_window_input, fv_state_band
+(csrc/shard.cu).
 """
 from __future__ import annotations
 
@@ -127,3 +139,231 @@ class ShardedFramePipeline:
             pixs.append(pix.clone())
             rgbas.append(rgba.clone())
         self.finish(torch.cat(pixs), torch.cat(rgbas))
+
+
+# ------------------------------------------------------------------ row-strip reconstruction
+def default_halo(config) -> int:
+    """Window halo in L0 rows: an interval bound of how far (in rows) the W-Net's output, O_d and
+    decoder hidden states of one frame reach (convs widen by one row per conv at their level, a
+    2x upsample by two rows of the coarser level, the K stage by one row per filter), rounded up
+    to the network divisor. FULL_BLOCKS / DESK_BLOCKS: 95 -> 96 (measured reach: 81)."""
+    ne, nd = config.n_enc, config.n_dec
+    r, skips = 0, []
+    for i in range(ne):
+        r += 2 * 2 ** i
+        skips.append(r)
+    cur, hd = r, {}
+    for j in range(nd):
+        L = ne - j
+        if j > 0:
+            cur = max(cur + 2 ** (L + 1), skips[L])
+        cur += 2 * 2 ** L
+        hd[L] = cur
+    img = od = hd[0] + 1
+    kinds = [k for k, _ in config.block_config]
+    levels = list(range(ne)) + [ne - j for j in range(nd)]
+    for i, L in enumerate(levels):
+        img = max(img, hd[L]) + 2 ** L
+        if kinds[i] == "d" and i < len(kinds) - 1:
+            img += 2 ** L
+    reach = max(img, od, max(hd.values()))
+    div = config.divisor
+    return -(-reach // div) * div
+
+
+def strip_geometry(hp: int, world: int, div: int, halo: int) -> list[tuple[int, int, int, int]]:
+    """Per rank (a, b, w0, w1): owned rows [a, b) (multiples of div, as equal as possible) and the
+    window [w0, w1) = [a - halo, b + halo] clipped to [0, hp)."""
+    if hp % div or halo % div:
+        raise ValueError(f"padded height {hp} and halo {halo} must be multiples of {div}")
+    units = hp // div
+    if units < world:
+        raise ValueError(f"{hp} rows cannot be split into {world} strips of {div}-row units")
+    out, a = [], 0
+    for r in range(world):
+        b = a + (units // world + (1 if r < units % world else 0)) * div
+        out.append((a, b, max(0, a - halo), min(hp, b + halo)))
+        a = b
+    if world > 1 and halo > min(b - a for a, b, _, _ in out):
+        raise ValueError(f"halo {halo} exceeds the smallest strip; use fewer ranks")
+    return out
+
+
+def band_plan(geo, rank: int):
+    """Window-local row ranges of rank's exchanges: {"send_up": (r0, r1), "recv_up": ..., "send_dn",
+    "recv_dn"} -- up = with rank - 1, dn = with rank + 1; empty at the frame's edges."""
+    a, b, w0, w1 = geo[rank]
+    plan = {"send_up": (0, 0), "recv_up": (0, 0), "send_dn": (0, 0), "recv_dn": (0, 0)}
+    if rank > 0:
+        plan["send_up"] = (a - w0, geo[rank - 1][3] - w0)
+        plan["recv_up"] = (0, a - w0)
+    if rank + 1 < len(geo):
+        plan["send_dn"] = (geo[rank + 1][2] - w0, b - w0)
+        plan["recv_dn"] = (b - w0, w1 - w0)
+    return plan
+
+
+def exchange_bands(bufs: dict, rank: int, world: int, group=None) -> None:
+    """Send/receive the boundary bands with the two neighbours (batch_isend_irecv; NCCL for CUDA
+    tensors, gloo for CPU tensors). bufs: "send_up", "recv_up", "send_dn", "recv_dn" tensors."""
+    import torch.distributed as dist
+
+    ops = []
+    if rank > 0:
+        ops += [dist.P2POp(dist.isend, bufs["send_up"], rank - 1, group),
+                dist.P2POp(dist.irecv, bufs["recv_up"], rank - 1, group)]
+    if rank + 1 < world:
+        ops += [dist.P2POp(dist.isend, bufs["send_dn"], rank + 1, group),
+                dist.P2POp(dist.irecv, bufs["recv_dn"], rank + 1, group)]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+class StripShardedPipeline:
+    """The C5 frame across `world` GPUs: march sharded by packets, reconstruction by row strips.
+
+    This process is `rank`; emulate=True instead holds every rank's window on this one GPU and runs
+    them one after another with the band exchange as device copies (tests: no rank waits on another)."""
+
+    def __init__(self, scene: Scene, net, dims: tuple[int, int], noise: NoiseStack,
+                 settings: RenderSettings = RenderSettings(), rank: int = 0, world: int = 1, group=None,
+                 halo: int | None = None, emulate: bool = False):
+        import ctypes as C
+
+        import torch
+
+        from .network import _DevState
+
+        self.pipe = FramePipeline(scene, None, dims, noise, settings)
+        self.net = net
+        self.rank, self.world, self.group, self.emulate = rank, world, group, emulate
+        h, w = dims
+        self.h, self.w = h, w
+        div = net.config.divisor
+        self.hp = -(-h // div) * div
+        self.halo = default_halo(net.config) if halo is None else halo
+        self.geo = strip_geometry(self.hp, world, div, self.halo)
+        ctx = self.pipe.ctx
+        self.net_h = net.handle(ctx)
+        self.ranks = list(range(world)) if emulate else [rank]
+        self.states = {r: _DevState(ctx, self.net_h, self.geo[r][3] - self.geo[r][2], w) for r in self.ranks}
+        self.img = {r: torch.empty((self.geo[r][3] - self.geo[r][2], w, 3), dtype=torch.float32, device="cuda")
+                    for r in self.ranks}
+        n = h * w
+        self.bits = torch.empty((h, w), dtype=torch.uint8, device="cuda")
+        self.cap = record_capacity(n, world)
+        self.rec = torch.empty((self.cap, 3), dtype=torch.int32, device="cuda")
+        self.gathered = torch.empty((world * self.cap, 3), dtype=torch.int32, device="cuda")
+        self.local_idx = torch.empty((n,), dtype=torch.int32, device="cuda")
+        self.local_k = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        self.fb = torch.zeros((h, w, 4), dtype=torch.float32, device="cuda")
+        self.bands = {}
+        for r in self.ranks:
+            plan = band_plan(self.geo, r)
+            bufs = {}
+            for key, (r0, r1) in plan.items():
+                nb = C.c_int64()
+                _lib.check(ctx.lib.fv_state_band(ctx.h, self.states[r].h, 1, r0, r1 - r0, None, C.byref(nb)))
+                bufs[key] = torch.empty((max(1, nb.value),), dtype=torch.uint8, device="cuda")
+            self.bands[r] = (plan, bufs)
+
+    def mask(self, fovea: FoveaConfig, frame: int) -> None:
+        import ctypes as C
+
+        p = self.pipe
+        f = fovea.c_struct()
+        _lib.check(p.ctx.lib.fv_mask_compact(p.ctx.h, int(frame), self.h, self.w, C.byref(f), None,
+                                             _lib.ptr(self.bits), _lib.ptr(p.idx), _lib.ptr(p.k), None))
+
+    def march_shard(self, cam: Camera, rank: int) -> None:
+        """This rank's packets of the compacted list -> fb -> its 12-byte records."""
+        import ctypes as C
+
+        p = self.pipe
+        ctx = p.ctx
+        n = self.h * self.w
+        _lib.check(ctx.lib.fv_shard_rays(ctx.h, _lib.ptr(p.idx), _lib.ptr(p.k), n, rank, self.world,
+                                         _lib.ptr(self.local_idx), _lib.ptr(self.local_k)))
+        camc = cam.c_struct()
+        _lib.check(ctx.lib.fv_render_sparse(ctx.h, p.vol, C.byref(camc), p._light_ref(), C.byref(p._set),
+                                            _lib.ptr(self.local_idx), _lib.ptr(self.local_k), n, _lib.ptr(self.fb),
+                                            None, None, None))
+        _lib.check(ctx.lib.fv_pack_records16(ctx.h, _lib.ptr(self.fb), _lib.ptr(self.local_idx),
+                                             _lib.ptr(self.local_k), self.cap, _lib.ptr(self.rec)))
+
+    def reconstruct_window(self, rank: int) -> None:
+        ctx = self.pipe.ctx
+        st = self.states[rank]
+        w0 = self.geo[rank][2]
+        _lib.check(ctx.lib.fv_window_input(ctx.h, st.h, _lib.ptr(self.bits), self.h, self.w, w0))
+        _lib.check(ctx.lib.fv_scatter_records16(ctx.h, st.h, _lib.ptr(self.gathered), int(self.gathered.shape[0]),
+                                                self.w, w0))
+        _lib.check(ctx.lib.fv_reconstruct(ctx.h, self.net_h, st.h, 1, _lib.ptr(self.img[rank]), None, None))
+
+    def _band(self, rank: int, key: str, pack: bool) -> None:
+        ctx = self.pipe.ctx
+        plan, bufs = self.bands[rank]
+        r0, r1 = plan[key]
+        if r1 > r0:
+            _lib.check(ctx.lib.fv_state_band(ctx.h, self.states[rank].h, 1 if pack else 0, r0, r1 - r0,
+                                             _lib.ptr(bufs[key]), None))
+
+    def exchange(self) -> None:
+        """After a frame: owned boundary bands -> the neighbours' window extensions."""
+        if self.emulate:
+            for r in self.ranks:
+                for key in ("send_up", "send_dn"):
+                    self._band(r, key, True)
+            for r in self.ranks:
+                if r > 0:
+                    self.bands[r][1]["recv_up"].copy_(self.bands[r - 1][1]["send_dn"])
+                    self._band(r, "recv_up", False)
+                if r + 1 < self.world:
+                    self.bands[r][1]["recv_dn"].copy_(self.bands[r + 1][1]["send_up"])
+                    self._band(r, "recv_dn", False)
+            return
+        r = self.rank
+        for key in ("send_up", "send_dn"):
+            self._band(r, key, True)
+        if self.world > 1:
+            exchange_bands(self.bands[r][1], r, self.world, self.group)
+        for key in ("recv_up", "recv_dn"):
+            self._band(r, key, False)
+
+    def step(self, cam: Camera, fovea: FoveaConfig, frame: int) -> None:
+        """One frame on this rank: mask, its march share, the record all-gather, its window's
+        reconstruction, the band exchange."""
+        import torch.distributed as dist
+
+        self.mask(fovea, frame)
+        self.march_shard(cam, self.rank)
+        if self.world > 1:
+            dist.all_gather_into_tensor(self.gathered, self.rec, group=self.group)
+        else:
+            self.gathered.copy_(self.rec)
+        self.reconstruct_window(self.rank)
+        self.exchange()
+
+    def step_emulated(self, cam: Camera, fovea: FoveaConfig, frame: int) -> None:
+        """Every rank's share of the frame on this GPU, one rank after another."""
+        self.mask(fovea, frame)
+        for r in range(self.world):
+            self.march_shard(cam, r)
+            self.gathered[r * self.cap:(r + 1) * self.cap].copy_(self.rec)
+        for r in self.ranks:
+            self.reconstruct_window(r)
+        self.exchange()
+
+    def owned_rgb(self, rank: int):
+        """The rank's owned rows of the frame's image (rows past the film dropped)."""
+        a, b, w0, _ = self.geo[rank]
+        return self.img[rank][a - w0:min(b, self.h) - w0]
+
+    @property
+    def rgb(self):
+        """The whole (H, W, 3) image (emulated runs: every rank's owned rows)."""
+        import torch
+
+        return torch.cat([self.owned_rgb(r) for r in self.ranks], dim=0)
+

@@ -365,13 +365,17 @@ def test_end_to_end_c1_against_reference(golden, stack):
     assert O.psnr(host, g["img1"]) >= 55.0
 
 
-@pytest.mark.parametrize("overlap,ahead", [("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")])
-def test_pipelined_frames_equal_serial_frames(stack, overlap, ahead, monkeypatch):
-    """The pipelined frame loop -- one stream in frame order, or (FV_PIPE_OVERLAP=1) render t+1 on a
-    second stream during reconstruct t, with (FV_MASK_AHEAD=1) or without the next frame's mask on a
-    third stream -- must not change any frame."""
-    monkeypatch.setenv("FV_PIPE_OVERLAP", overlap)
-    monkeypatch.setenv("FV_MASK_AHEAD", ahead)
+@pytest.mark.parametrize("loop", ["graph", "py-00", "py-10", "py-01", "py-11"])
+def test_pipelined_frames_equal_serial_frames(stack, loop, monkeypatch):
+    """The frame loop must not change any frame: fv_frames' whole-frame graphs ("graph": each
+    frame one captured graph, the camera / fovea read from the device parameter block), and the
+    Python stream loop (FV_PIPE_PY=1) in frame order or (FV_PIPE_OVERLAP=1) with render t+1 on a
+    second stream, with (FV_MASK_AHEAD=1) or without the next frame's mask on a third stream.
+    Every frame of the run is compared with the serial frame-by-frame result."""
+    if loop != "graph":
+        monkeypatch.setenv("FV_PIPE_PY", "1")
+        monkeypatch.setenv("FV_PIPE_OVERLAP", loop[3])
+        monkeypatch.setenv("FV_MASK_AHEAD", loop[4])
     from paper_2209_09965_b200.pipeline import FramePipeline
     from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
     from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
@@ -381,21 +385,24 @@ def test_pipelined_frames_equal_serial_frames(stack, overlap, ahead, monkeypatch
     net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
     cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, 320, 184)
     pipe = FramePipeline(scene, net, (184, 320), stack)
-    outs = []
-    for i in range(6):
+    ref = []
+    for i in range(8):
         pipe.step(cams[i], spec.fovea(), i)
-        outs.append(pipe.rgb.clone())
+        ref.append(pipe.rgb.clone())
+    frames = [(cams[i], spec.fovea(), i) for i in range(8)]
+    # the whole path in one call (graph capture on each configuration's second use, then replays)
     pipe.reset()
-    frames = [(cams[i], spec.fovea(), i) for i in range(6)]
-    pipe.run_pipelined(frames)
+    outs = [torch.empty_like(pipe.rgb) for _ in range(8)]
+    pipe.run_pipelined(frames, outs)
     torch.cuda.synchronize()
-    assert torch.equal(pipe.rgb, outs[-1])
-    # and frame by frame
+    for i in range(8):
+        assert torch.equal(outs[i], ref[i]), i
+    # and one frame per call (each call ends on the mask of a frame that does not come)
     pipe.reset()
-    for i in range(6):
+    for i in range(8):
         pipe.run_pipelined(frames[i:i + 1])
         torch.cuda.synchronize()
-        assert torch.equal(pipe.rgb, outs[i]), i
+        assert torch.equal(pipe.rgb, ref[i]), i
 
 
 def test_kernel_timing_counts_algorithmic_conv_flops(stack):
@@ -578,6 +585,80 @@ def test_sharded_frames_equal_unsharded_frames(stack, world):
         assert torch.equal(sh.rgb, ref.rgb), i
 
 
+@pytest.mark.parametrize("world,h", [(2, 392), (3, 390)])
+def test_strip_sharded_reconstruction_equals_unsharded_frames(stack, world, h):
+    """Row-strip reconstruction (StripShardedPipeline, every rank's window on this GPU one after
+    another, the boundary bands exchanged as device copies): the ranks' owned rows together are
+    bit-identical to the unsharded frame, frame after frame with the recurrent state carried (the
+    band exchange keeps each window's hidden states and O_d feedback exact)."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.sharded import StripShardedPipeline
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    w = 256
+    spec = ExperimentSpec(mode="fast", width=w, height=h)
+    scene = default_scene("sphere_shells", (96, 96, 96))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=0), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=64), scene.volume, w, h)
+    ref = FramePipeline(scene, net, (h, w), stack)
+    sh = StripShardedPipeline(scene, net, (h, w), stack, world=world, emulate=True)
+    assert sh.halo == 96 and all(w1 - w0 < sh.hp for _, _, w0, w1 in sh.geo)
+    for i in range(6):
+        ref.step(cams[3 * i], spec.fovea(), i)
+        sh.step_emulated(cams[3 * i], spec.fovea(), i)
+        torch.cuda.synchronize()
+        assert torch.equal(sh.rgb, ref.rgb), i
+    # without the band exchange the windows drift from the full frame (the exchange is load-bearing)
+    sh2 = StripShardedPipeline(scene, net, (h, w), stack, world=world, emulate=True)
+    ref.reset()
+    diverged = False
+    for i in range(6):
+        ref.step(cams[3 * i], spec.fovea(), i)
+        sh2.mask(spec.fovea(), i)
+        for r in range(world):
+            sh2.march_shard(cams[3 * i], r)
+            sh2.gathered[r * sh2.cap:(r + 1) * sh2.cap].copy_(sh2.rec)
+        for r in range(world):
+            sh2.reconstruct_window(r)
+        torch.cuda.synchronize()
+        diverged |= not torch.equal(sh2.rgb, ref.rgb)
+    assert diverged
+
+
+def test_fp16_records_carry_the_marched_rays(stack):
+    """fv_pack_records16: (pixel, RGBA rounded to fp16 -- the network input's precision) for every
+    marched ray in list order, pixel -1 past the count."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    h, w = 96, 160
+    spec = ExperimentSpec(mode="fast", width=w, height=h)
+    scene = default_scene("sphere_shells", (64, 64, 64))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.DESK_BLOCKS), seed=0), "fp16")
+    cam = orbit_cameras(OrbitPathSpec(n_frames=8), scene.volume, w, h)[1]
+    pipe = FramePipeline(scene, net, (h, w), stack)
+    import ctypes as C
+
+    pipe.mask(spec.fovea(), 0)
+    ctx = pipe.ctx
+    fb = torch.zeros((h, w, 4), dtype=torch.float32, device="cuda")
+    _lib.check(ctx.lib.fv_render_sparse(ctx.h, pipe.vol, C.byref(cam.c_struct()), pipe._light_ref(),
+                                        C.byref(pipe._set), _lib.ptr(pipe.idx), _lib.ptr(pipe.k), h * w, _lib.ptr(fb),
+                                        None, None, None))
+    rec = torch.empty((h * w, 3), dtype=torch.int32, device="cuda")
+    _lib.check(ctx.lib.fv_pack_records16(ctx.h, _lib.ptr(fb), _lib.ptr(pipe.idx), _lib.ptr(pipe.k), h * w,
+                                         _lib.ptr(rec)))
+    k = int(pipe.k.item())
+    got = rec[:k].cpu().numpy()
+    assert np.array_equal(got[:, 0], pipe.idx[:k].cpu().numpy())
+    assert (rec[k:, 0] == -1).all()
+    rgba16 = got[:, 1:].view(np.float16).reshape(k, 4)
+    exp = fb.reshape(-1, 4)[pipe.idx[:k].long()].cpu().numpy().astype(np.float16)
+    assert np.array_equal(rgba16, exp)
+
+
 # ---------------------------------------------------------------- input formats (SURVEY 8(f) row 3)
 def test_load_raw_volume_on_device_vs_reference(golden, tmp_path):
     """load_raw_volume: NaN scan, min/max and fp64 normalisation in libfovnet, bit-exact."""
@@ -658,7 +739,8 @@ np.save(sys.argv[2], np.stack(outs))
 
 
 def test_graph_replay_equals_eager_launches(tmp_path):
-    """reconstruct() replayed from captured CUDA graphs (frames 2+) == the same frames launched eagerly."""
+    """reconstruct() and whole frames (fv_frames) replayed from captured CUDA graphs == the same frames
+    launched eagerly (FV_GRAPH=0 / FV_FRAME_GRAPH=0)."""
     import os
     import subprocess
     import sys
@@ -668,10 +750,12 @@ def test_graph_replay_equals_eager_launches(tmp_path):
     outs = {}
     for flag in ("0", "1"):
         out = tmp_path / f"frames_{flag}.npy"
-        env = dict(os.environ, FV_GRAPH=flag)
-        subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out)], env=env, check=True, timeout=300)
+        env = dict(os.environ, FV_GRAPH=flag, FV_FRAME_GRAPH=flag)
+        subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out), "loops"], env=env, check=True,
+                       timeout=300)
         outs[flag] = np.load(out)
-    assert np.array_equal(outs["0"], outs["1"])
+    assert np.array_equal(outs["0"], outs["1"])  # eager launches == reconstruct() / whole-frame graphs
+    assert np.array_equal(outs["1"][7:], outs["1"][:6])  # fv_frames (graphs) == the stepped frames
 
 
 @pytest.mark.parametrize("knob", ["FV_KCHAIN", "FV_PDL", "FV_MASK_AHEAD"])
