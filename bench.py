@@ -459,10 +459,45 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+def cpu_strip_sample(cfg, vol, rows=256, frames=1):
+    """cpu_baseline of the --shard line: the oracle on a full-width strip of `rows` rows through the
+    fovea (its mask, the C fp64 march of its active rays, the fp32 network on the strip), scaled to
+    the frame by rows; a whole 4K frame at 1024^3 would take minutes on the host."""
+    from oracle import fovray_oracle as O
+
+    h, w, n = cfg["height"], cfg["width"], cfg["vol"]
+    r0 = (h // 2 - rows // 2) // 8 * 8
+    stack = O.load_rnkstack(ROOT / "paper_2209_09965_b200" / "data" / "stbn_64x64x8_s1.noise")
+    tau = O.tau_map(h, w, ((w - 1) / 2, (h - 1) / 2), cfg["sigma"], cfg["pb"], O.pixel_scale_for_film(h, w))
+    params = O.init_params(O.FULL_BLOCKS, 0, fp16_weights=True)
+    state = None
+    secs = []
+    for i in range(frames):
+        t0 = time.perf_counter()
+        bits = O.sample_mask(stack, h, w, i, tau)[r0:r0 + rows]
+        pix = O.compact(bits) + r0 * w
+        pos, look = O.orbit_camera(i, PATH_FRAMES, (n, n, n))
+        rgba, _ = O.render(vol, (1, 1, 1), O.DEFAULT_LUT, ("dir", (-1.0, -1.0, -0.5), (1, 1, 1)),
+                           dict(position=pos, look_at=look, fov_y=45.0, width=w, height=h), pix=pix)
+        img = np.zeros((rows * w, 4), np.float32)
+        img[pix - r0 * w] = rgba
+        m = bits.astype(np.float32)
+        x = np.concatenate([np.moveaxis(img.reshape(rows, w, 4), -1, 0) * m[None], m[None]], 0)
+        _, _, state = O.net_forward(params, O.FULL_BLOCKS, x, state)
+        secs.append((time.perf_counter() - t0) * h / rows)
+    desc = (f"{frames} frame(s) of a {w}x{rows} strip through the fovea (rows {r0}..{r0 + rows}): oracle mask, C fp64 "
+            f"march of the strip's active rays on all {len(os.sched_getaffinity(0))} host threads, fp32 NumPy/BLAS "
+            f"FULL_BLOCKS net on the strip; per-frame time scaled by {h}/{rows} rows; CPU {cpu_model()}")
+    return float(np.mean(secs)), desc, len(os.sched_getaffinity(0))
+
+
 def run_sharded(args, cfg):
     """One frame stream split across the ranks (config 5: --config c5 --shard): every rank marches
-    its packets of each frame, the records are all-gathered over NCCL, every rank reconstructs.
-    Strong scaling: the job renders K frames whatever N is; time = max over ranks."""
+    its 32-ray packets of each frame, one all_gather_into_tensor of 12-byte records gives every
+    rank the frame's rays, and each rank reconstructs its row strip on a window (strip + halo),
+    exchanging the recurrent boundary bands with its neighbours after the frame
+    (sharded.StripShardedPipeline; --shard-replicated: the round-1 replicated network). Strong
+    scaling: the job renders K frames whatever N is; time = max over ranks."""
     import torch
 
     rank, world, local = dist_env()
@@ -473,7 +508,7 @@ def run_sharded(args, cfg):
     from paper_2209_09965_b200.noise import default_stack
     from paper_2209_09965_b200.renderer import OrbitPathSpec, RenderSettings, orbit_cameras
     from paper_2209_09965_b200.sample_maps import FoveaConfig, pixel_scale_for_film
-    from paper_2209_09965_b200.sharded import ShardedFramePipeline
+    from paper_2209_09965_b200.sharded import ShardedFramePipeline, StripShardedPipeline
     from paper_2209_09965_b200.throughput import default_scene
 
     h, w, n = cfg["height"], cfg["width"], cfg["vol"]
@@ -482,8 +517,9 @@ def run_sharded(args, cfg):
     cams = orbit_cameras(OrbitPathSpec(n_frames=PATH_FRAMES), scene.volume, w, h)
     fovea = FoveaConfig(focus=((w - 1) / 2.0, (h - 1) / 2.0), sigma=cfg["sigma"], base_density=cfg["pb"],
                         pixel_scale=pixel_scale_for_film((h, w)))
-    pipe = ShardedFramePipeline(scene, net, (h, w), default_stack(), RenderSettings(), rank=rank, world=world,
-                                group=group)
+    strip = not args.shard_replicated
+    cls = StripShardedPipeline if strip else ShardedFramePipeline
+    pipe = cls(scene, net, (h, w), default_stack(), RenderSettings(), rank=rank, world=world, group=group)
     ctx = pipe.pipe.ctx
     k, wu = args.steps, args.warmup
     clocks = ClockSampler(local, ROOT / "gpurun_out" / f"clocks_r{rank}.csv") if rank == 0 else None
@@ -504,35 +540,61 @@ def run_sharded(args, cfg):
     ms = max_over_ranks(e0.elapsed_time(e1), world, device=tdev)
     launches = ctx.launches() - l0
     st = ctx.stats()
-    # end to end: frame -> host image on rank 0 (pinned), wall clock, max over ranks
-    host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
+    # the conv roofline of this rank's network over the same frames, kernel timing on
+    ctx.set_kernel_timing(True)
+    for j in range(wu, wu + min(k, 4)):
+        pipe.step(cams[j % PATH_FRAMES], fovea, j)
+    torch.cuda.synchronize()
+    conv_ms, conv_flop, conv_n = ctx.kernel_time(_lib.KERNEL_CLASSES["conv"])
+    ctx.set_kernel_timing(False)
+    # end to end: every rank copies its part of each frame's image to pinned host memory (its owned
+    # strip; the replicated design: rank 0 the whole image); wall clock, max over ranks
+    part = pipe.owned_rgb(rank) if strip else pipe.rgb
+    host = torch.empty(tuple(part.shape), dtype=torch.float32).pin_memory()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for j in range(wu + k, wu + 2 * k):
         pipe.step(cams[j % PATH_FRAMES], fovea, j)
-        if rank == 0:
-            host.copy_(pipe.rgb, non_blocking=True)
+        if strip or rank == 0:
+            host.copy_(pipe.owned_rgb(rank) if strip else pipe.rgb, non_blocking=True)
         torch.cuda.current_stream().synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, world, device=tdev)
     clk = clocks.stop() if clocks else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sec, desc, thr = cpu_strip_sample(cfg, scene.volume.data)
+        cpu = {"value": 1.0 / sec, "unit": "frames/s", "cores": thr, "kind": "port", "sample": desc}
     if rank == 0:
         hbm, tf_burst, tf_sus, src = load_peaks()
+        at_max = bool(clk and clk.get("sm_mhz") and clk["sm_mhz"] >= 0.95 * clk.get("sm_max_mhz", 1e9))
+        peak = tf_burst if at_max else tf_sus
+        conv_tf = conv_flop / (conv_ms / 1e3) / 1e12 if conv_ms > 0 else 0.0
         samples = (st.samples_main + st.samples_shadow) / k  # this rank's share
+        geo = getattr(pipe, "geo", None)
         line = {
             "metric": METRIC, "value": k / (ms / 1e3), "unit": "frames/s", "n_gpus": world, "steps": k,
             "warmup": wu, "ms_per_step": ms / k, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp16 net (fp32 acc) / fp32 march", "data": "synthetic",
             "config": {"workload": cfg["name"], "film": [w, h], "volume": [n, n, n], "path_frames": PATH_FRAMES,
-                       "parallelism": f"one frame stream, march sharded in 32-ray packets over {world} GPUs, "
-                                      "record all-gather (NCCL), replicated reconstruction",
-                       "l2": "inputs larger than L2"},
+                       "parallelism": (f"one frame stream over {world} GPUs: march in 32-ray packets, record "
+                                       "all_gather_into_tensor (NCCL), reconstruction in row strips on windows of "
+                                       f"strip + {pipe.halo} rows with a per-frame band exchange" if strip else
+                                       f"one frame stream, march sharded in 32-ray packets over {world} GPUs, "
+                                       "record all-gather (NCCL), replicated reconstruction"),
+                       "strips": geo, "l2": "inputs larger than L2"},
             "samples_per_frame_rank0": samples,
             "e2e": {"value": k / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": h * w * 3 * 4,
-                    "how": "ShardedFramePipeline.step per frame + pinned D2H of the image on rank 0, wall clock"},
+                    "d2h_bytes_per_step": int(host.numel() * 4),
+                    "how": "pipe.step per frame + pinned D2H of the rank's part of the image, wall clock"},
             "gpu_launches": launches, "clocks": clk,
-            "roofline": None, "cpu_baseline": None,
+            "roofline": {"bound": "tensor", "achieved": conv_tf, "peak": peak, "unit": "TFLOP/s",
+                         "frac": conv_tf / peak, "traffic": None,
+                         "kernel": "conv3x3_tc_kernel (all W-Net convs of rank 0's window)",
+                         "launches_per_frame": conv_n / min(k, 4),
+                         "how": "algorithmic conv FLOPs of the window / summed launch durations (CUDA events)",
+                         "peak_source": f"{src} ({'burst' if at_max else 'sustained'} dense fp16/bf16)"},
+            "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -548,7 +610,10 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true",
-                    help="split each frame's march across the ranks (config 5) instead of independent frame streams")
+                    help="split each frame across the ranks (config 5: march by packets, network by row strips) "
+                         "instead of independent frame streams")
+    ap.add_argument("--shard-replicated", action="store_true",
+                    help="with --shard: the round-1 design (march split, network replicated on every rank)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -105,3 +105,73 @@ def test_two_rank_ray_sharding_exchange():
     assert all(ok for _, ok, _ in res)
     counts = sorted(n for _, _, n in res)
     assert abs(counts[0] - counts[1]) <= 32  # packets dealt round-robin
+
+
+def test_strip_geometry_and_band_plans():
+    """Row strips partition the padded frame; each window holds its strip plus up to `halo` rows on
+    either side; every band a rank receives is exactly the band its neighbour sends (global rows)."""
+    from paper_2209_09965_b200 import sharded as SH
+    from paper_2209_09965_b200.network import DESK_BLOCKS, FULL_BLOCKS, NetConfig
+
+    assert SH.default_halo(NetConfig.from_string(FULL_BLOCKS)) == 96
+    assert SH.default_halo(NetConfig.from_string(DESK_BLOCKS)) == 96
+    for hp, world in ((2160, 8), (2160, 2), (392, 3), (1088, 4), (96, 1)):
+        geo = SH.strip_geometry(hp, world, 8, 96)
+        assert geo[0][0] == 0 and geo[-1][1] == hp
+        for r, (a, b, w0, w1) in enumerate(geo):
+            assert a % 8 == 0 and b % 8 == 0 and w0 == max(0, a - 96) and w1 == min(hp, b + 96)
+            if r:
+                assert a == geo[r - 1][1]
+            plan = SH.band_plan(geo, r)
+            if r + 1 < world:
+                nxt = SH.band_plan(geo, r + 1)
+                s0, s1 = plan["send_dn"]
+                q0, q1 = nxt["recv_up"]
+                assert (s0 + w0, s1 + w0) == (q0 + geo[r + 1][2], q1 + geo[r + 1][2])
+                s0, s1 = nxt["send_up"]
+                q0, q1 = plan["recv_dn"]
+                assert (s0 + geo[r + 1][2], s1 + geo[r + 1][2]) == (q0 + w0, q1 + w0)
+                assert plan["recv_dn"][1] == w1 - w0 and plan["recv_up"][0] == 0
+    with pytest.raises(ValueError, match="halo"):
+        SH.strip_geometry(184, 3, 8, 96)
+
+
+def _band_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2209_09965_b200 import sharded as SH
+
+    n = 1000 + 10 * rank  # band sizes differ between rank pairs but match within a pair
+    bufs = {
+        "send_up": torch.full((1000 + 10 * (rank - 1) if rank else 1,), float(100 * rank + 1)),
+        "send_dn": torch.full((n,), float(100 * rank + 2)),
+        "recv_up": torch.zeros((1000 + 10 * (rank - 1) if rank else 1,)),
+        "recv_dn": torch.zeros((n,)),
+    }
+    SH.exchange_bands(bufs, rank, world)
+    ok = True
+    if rank > 0:
+        ok &= bool((bufs["recv_up"] == 100 * (rank - 1) + 2).all())
+    if rank + 1 < world:
+        ok &= bool((bufs["recv_dn"] == 100 * (rank + 1) + 1).all())
+    dist.barrier()
+    dist.destroy_process_group()
+    q.put((rank, ok))
+
+
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("world", [2, 3])
+def test_band_exchange_between_neighbour_strips(world):
+    """StripShardedPipeline's per-frame band exchange (batch_isend_irecv with the two neighbours)
+    over gloo: rank r's top extension receives rank r-1's bottom band and vice versa."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=100) for _ in procs]
+    for p in procs:
+        p.join(timeout=30)
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(ok for _, ok in res)
