@@ -82,16 +82,31 @@ __device__ __forceinline__ void pwait(uint32_t bar, uint32_t parity, bool prof, 
 // R output rows per tile, N output channels (MMA N), S pipeline stages; BRES: the whole weight
 // image (<= kBResStages stages, i.e. cin <= 64) is loaded once per CTA and stays in smem, so
 // only activations stream (the weights were ~40% of the L2->SM bytes of a 64->64 conv).
-template <int R, int N, int S = 2, bool BRES = false>
+template <int R, int N, int S = 2, bool BRES = false, bool TAPN = false>
 struct Cfg {
   static constexpr int kABytes = kStageGroups * (R + 2) * kRowBytes;
   static constexpr int kBBytes = 9 * kStageGroups * N * 16;
   static constexpr int kPlaneBytes = (R + 2) * kRowBytes;
-  static constexpr int kAcc = (2 * R * N <= 512) ? 2 : 1;
+  // TAPN: one accumulator block of N columns per HALO row (R + 2 of them), single-buffered
+  static constexpr int kAccCols = TAPN ? (R + 2) * N : R * N;
+  static constexpr int kAcc = (2 * kAccCols <= 512) ? 2 : 1;
   static constexpr int kBSlots = BRES ? kBResStages : S;
   static constexpr int kBiasBytes = N * 4;  // the epilogue's bias copy
-  static constexpr int kSmem = S * kABytes + kBSlots * kBBytes + 1024 + 256 + kBiasBytes;
+  static constexpr int kXchgBytes = TAPN ? 512 : 0;  // TAPN: cross-quarter partial sums
+  static constexpr int kSmem = S * kABytes + kBSlots * kBBytes + 1024 + 256 + kBiasBytes + kXchgBytes;
 };
+
+// TAPN (the K-stage level-0 conv): the nine 3x3 taps of D.head sit in N next to the two K blocks'
+// 1x1 logits -- column (dy*3 + dx)*3 + c is D.head output c's tap (dy, dx), columns 27.. and 36..
+// the logits -- so ONE 128 x 48 x 16 MMA per halo row and K-stage covers all of it (instead of 18
+// row-fused 128 x 96 x 16 dispatches, which left the launch MMA-issue bound at ~1280 cycles per
+// stage). Halo row h's accumulator holds, in TMEM lane m (input pixel x0 - 1 + m), the products of
+// that pixel with every tap's weights; the epilogue sums output pixel j = m - 1 over the 3 x 3
+// neighbourhood across halo rows (TMEM columns) and lanes (shuffles; smem across lane quarters).
+// Tiles therefore advance by 126 columns (lanes 1..126 are the valid outputs).
+constexpr int kTapnStride = kTileW - 2;
+constexpr int kTapnLogit[2] = {27, 36};
+__host__ __device__ constexpr int tapn_logit(int s) { return s == 0 ? 27 : 36; }
 
 // All MMAs of one K-stage: R output rows x 9 taps x NK k-steps, offsets folded at compile time.
 // kCenter: 1x1 convolution -- only tap 4 (dy = dx = 1) is issued.
@@ -158,9 +173,10 @@ __device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint3
   }
 }
 
-template <int R, int N, int kStages, bool BRES, bool FUSED, bool CO = false>
+template <int R, int N, int kStages, bool BRES, bool FUSED, bool CO = false, bool TAPN = false>
 __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
-  using C = Cfg<R, N, kStages, BRES>;
+  using C = Cfg<R, N, kStages, BRES, TAPN>;
+  constexpr int kStride = TAPN ? kTapnStride : kTileW;  // columns a tile advances by
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -170,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   constexpr bool kPairs = C::kAcc == 1 && FUSED;  // single accumulator: release it row pair by row pair
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5 + (kPairs ? R / 2 : 0));
   float* s_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // N floats
+  float* s_xchg = s_bias + N;  // TAPN: [half][quarter][left 3 | right 3]
   const uint32_t bar_full = sm100::smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * kStages;
   const uint32_t bar_tfull = bar_empty + 8 * kStages;
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     // ---------------- producer ----------------
     int it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int x0 = (tile % a.tiles_x) * kTileW;
+      const int x0 = (tile % a.tiles_x) * kStride;
       const int y0 = (tile / a.tiles_x) * R;
       uint32_t tile_bytes_per_group;
       {
@@ -291,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
       const uint32_t acc_round = lt / C::kAcc;
       if (!kPairs) pwait(bar_tempty + 8 * acc, (acc_round & 1) ^ 1, prof, w_tempty);
       sm100::tc_fence_after();
-      const uint32_t d_base = tmem_base + acc * R * N;
+      const uint32_t d_base = tmem_base + acc * C::kAccCols;
       for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
         const int st = it % kStages;
         const uint32_t round = it / kStages;
@@ -312,7 +329,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
         // 36 x N64 dispatches: 1054 / 1398 / 2085 cycles -- is summarised in profiles/r01_summary.md)
         // (row-fused weight images exist only for 3x3 convs: FUSED implies not centre-only)
         if (leader) {
-          if constexpr (FUSED)
+          if constexpr (TAPN) {
+            // one dispatch per halo row: A = the row from halo column 0 (pixel x0 - 1), all taps in N
+#pragma unroll
+            for (int h = 0; h < R + 2; ++h)
+              sm100::mma_f16(d_base + h * N, a0 + (uint64_t)((h * kRowBytes) >> 4), b0, idesc, ks == 0 ? 0u : 1u);
+          } else if constexpr (FUSED)
             issue_stage_rows<R, N, true, kPairs>(a0, b0, d_base, ks == 0, bar_pair, (acc_round & 1) ^ 1);
           else if (CO || a.center_only)
             issue_stage<R, N, 1, true>(a0, b0, d_base, idesc, ks == 0);
@@ -340,14 +362,113 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++lt) {
       const int acc = lt % C::kAcc;
       const uint32_t acc_round = lt / C::kAcc;
-      const int x0 = (tile % a.tiles_x) * kTileW;
+      const int x0 = (tile % a.tiles_x) * kStride;
       const int y0 = (tile / a.tiles_x) * R;
       pwait(bar_tfull + 8 * acc, acc_round & 1, prof, w_tfull);
       sm100::tc_fence_after();
       const int x = x0 + 32 * q + lane;
       const bool xin = x < a.W;
-      const uint32_t t_row0 = tmem_base + ((uint32_t)(32 * q) << 16) + acc * R * N;
-      if (a.head) {
+      const uint32_t t_row0 = tmem_base + ((uint32_t)(32 * q) << 16) + acc * C::kAccCols;
+      if constexpr (TAPN) {
+        // output pixel j = m - 1 (m = this thread's TMEM lane in the tile): D.head = sum over dy of
+        // L(m - 1) + M(m) + R(m + 1), L/M/R = the dx = 0/1/2 tap products of halo row r + dy in lane
+        // m; the logits are the centre row's columns in lane m itself. The two warps of a lane
+        // quarter take output rows {0, 1} and {2, 3}: each streams its four halo rows from TMEM once.
+        const int m = 32 * q + lane, xo = x0 + m - 1;
+        const bool valid = m >= 1 && m <= kTileW - 2 && xo < a.W;
+        const int64_t hw = (int64_t)a.H * a.W;
+        const int r0 = 2 * half;
+        float Ls[2][3] = {}, Ms[2][3] = {}, Rs[2][3] = {};
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          uint32_t u0[16], u1[16];
+          const uint32_t ta = t_row0 + (uint32_t)((r0 + hh) * N);
+          sm100::tmem_ld16_nowait(ta, u0);
+          sm100::tmem_ld16_nowait(ta + 16, u1);
+          sm100::tmem_wait_ld_regs(u0, u1);
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) { v[i] = __uint_as_float(u0[i]); v[16 + i] = __uint_as_float(u1[i]); }
+#pragma unroll
+          for (int o = 0; o < 2; ++o) {
+            const int dy = hh - o;
+            if (dy < 0 || dy > 2) continue;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              Ls[o][c] += v[(dy * 3 + 0) * 3 + c];
+              Ms[o][c] += v[(dy * 3 + 1) * 3 + c];
+              Rs[o][c] += v[(dy * 3 + 2) * 3 + c];
+            }
+          }
+          if (hh == 1 || hh == 2) {
+            // the centre row of output row r0 + hh - 1: its logits -> softmax -> filter weights
+            uint32_t u2[16];
+            sm100::tmem_ld16_nowait(ta + 32, u2);
+            sm100::tmem_wait_ld();
+            float lg[18];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) lg[i] = v[27 + i];
+#pragma unroll
+            for (int i = 0; i < 13; ++i) lg[5 + i] = __uint_as_float(u2[i]);
+            const int y = y0 + r0 + hh - 1;
+            if (valid && y < a.H) {
+              const int64_t pix = (int64_t)y * a.W + xo;
+#pragma unroll
+              for (int s_ = 0; s_ < 2; ++s_) {
+                if (!a.kw[s_]) continue;
+                float l[9], mx = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 9; ++j) {
+                  l[j] = lg[9 * s_ + j] + s_bias[logit_col(s_) + j];
+                  mx = fmaxf(mx, l[j]);
+                }
+                float sum = 0.f;
+#pragma unroll
+                for (int j = 0; j < 9; ++j) {
+                  l[j] = __expf(l[j] - mx);  // arguments <= 0: ex2.approx, rel. error ~1e-7
+                  sum += l[j];
+                }
+                const float inv = __frcp_rn(sum);
+#pragma unroll
+                for (int j = 0; j < 9; ++j) a.kw[s_][j * hw + pix] = l[j] * inv;
+              }
+            }
+          }
+        }
+        // neighbours' partial sums: inside the quarter by shuffles, across quarters through smem
+        float* xs = s_xchg + (half * 4 + q) * 12;
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          if (lane == 31) { xs[6 * o] = Ls[o][0]; xs[6 * o + 1] = Ls[o][1]; xs[6 * o + 2] = Ls[o][2]; }
+          if (lane == 0) { xs[6 * o + 3] = Rs[o][0]; xs[6 * o + 4] = Rs[o][1]; xs[6 * o + 5] = Rs[o][2]; }
+        }
+        sm100::named_bar_sync(2 + half, 128);
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          float od[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float left = __shfl_up_sync(0xffffffffu, Ls[o][c], 1);
+            float right = __shfl_down_sync(0xffffffffu, Rs[o][c], 1);
+            if (lane == 0) left = q > 0 ? s_xchg[(half * 4 + q - 1) * 12 + 6 * o + c] : 0.f;
+            if (lane == 31) right = q < 3 ? s_xchg[(half * 4 + q + 1) * 12 + 6 * o + 3 + c] : 0.f;
+            od[c] = ((left + Ms[o][c]) + right) + s_bias[c];
+          }
+          const int y = y0 + r0 + o;
+          if (valid && y < a.H && a.od) {
+            const int64_t pix = (int64_t)y * a.W + xo;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) a.od[c * hw + pix] = od[c];
+            if (a.feedback) {
+              __half* fb = a.feedback + pix * 8;
+              fb[5] = __float2half(od[0]);
+              fb[6] = __float2half(od[1]);
+              fb[7] = __float2half(od[2]);
+            }
+          }
+        }
+        sm100::named_bar_sync(2 + half, 128);  // the slots are rewritten by the next tile
+      } else if (a.head) {
         // D.head (cols 0..2) and/or K-stage logits (9 cols per K block): O_d in fp32 planes +
         // next frame's feedback channels; logits -> max-subtracted softmax (autograd.py:188-199)
         // -> 9 fp32 filter-weight planes per K block.
@@ -506,23 +627,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   }
 }
 
-template <int R, int N, int S, bool BRES, bool FUSED, bool CO = false>
+template <int R, int N, int S, bool BRES, bool FUSED, bool CO = false, bool TAPN = false>
 int launch(fv_ctx* ctx, const ConvArgs& args) {
-  using C = Cfg<R, N, S, BRES>;
+  using C = Cfg<R, N, S, BRES, TAPN>;
   static_assert(C::kSmem <= 227 * 1024, "conv tile configuration exceeds shared memory");
+  static_assert(!TAPN || (R == 4 && N >= 48 && !FUSED && !CO), "TAPN: 4-row tiles, 48 columns, plain issue");
   static bool attr_set = false;
   if (!attr_set) {
-    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 C::kSmem));
+    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
   ConvArgs a = args;
-  a.tiles_x = (a.W + kTileW - 1) / kTileW;
+  constexpr int kStride = TAPN ? kTapnStride : kTileW;
+  a.tiles_x = (a.W + kStride - 1) / kStride;
   a.tiles_y = (a.H + R - 1) / R;
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
   ktime_begin(ctx);
-  fv::launch_pdl(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO>, grid, kThreads, C::kSmem, ctx->stream, a);
+  fv::launch_pdl(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN>, grid, kThreads, C::kSmem, ctx->stream, a);
   ktime_end(ctx, FV_KC_CONV, a.flops);
   if (a.prof) {
     std::vector<unsigned long long> h((size_t)grid * kProfSlots);
@@ -549,7 +672,7 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
   const int groups = (cp.cin + 7) / 8;
   const int N = cp.n_pad;
   static const bool no_fuse = getenv("FV_CONV_FUSE") && atoi(getenv("FV_CONV_FUSE")) == 0;  // A/B runs
-  cp.row_fused = !no_fuse && !cp.center_only && 3 * N <= 256;
+  cp.row_fused = !no_fuse && !cp.center_only && !cp.tapn && 3 * N <= 256;
   cp.n_stages = (groups + kStageGroups - 1) / kStageGroups;
   cp.stage_groups.clear();
   cp.stage_off.clear();
@@ -564,7 +687,24 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
   }
   cp.wbytes = off;
   std::vector<__half> img(off / 2, __float2half(0.f));
-  for (int s = 0; s < cp.n_stages; ++s) {
+  for (int s = 0; s < cp.n_stages && cp.tapn; ++s) {
+    // TAPN: [kg][n][8] per stage; column n -> (output o, tap t) of the K-stage layout (D.head
+    // outputs 0..2 with their nine taps, the logits of the two K blocks at the centre tap)
+    __half* base = img.data() + cp.stage_off[s] / 2;
+    for (int kg = 0; kg < 2; ++kg)
+      for (int n = 0; n < N; ++n) {
+        int o = -1, t = 4;
+        if (n < 27) { o = n % 3; t = n / 3; }
+        else if (n < 36) o = kLogitCol[0] + (n - 27);
+        else if (n < 45) o = kLogitCol[1] + (n - 36);
+        for (int e = 0; e < 8; ++e) {
+          const int c = (s * kStageGroups + kg) * 8 + e;
+          const float w = (o >= 0 && o < cp.cout && c < cp.cin) ? cp.w_host[((int64_t)o * cp.cin + c) * 9 + t] : 0.f;
+          base[((int64_t)kg * N + n) * 8 + e] = __float2half(w);
+        }
+      }
+  }
+  for (int s = 0; s < cp.n_stages && !cp.tapn; ++s) {
     const int gs = cp.stage_groups[s];
     const int nk = gs / 2;
     __half* base = img.data() + cp.stage_off[s] / 2;
@@ -647,6 +787,11 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   // row-fused MMAs whenever 3N <= 256 (the B image was laid out for it in conv_prepare)
   const bool res = cp.n_stages <= kBResStages;
   const bool fu = cp.row_fused;
+  if (cp.tapn) {
+    FV_REQUIRE(res && cp.n_pad == 48 && aux, "conv %s: the taps-in-N K-stage conv needs cin <= 64 and 48 columns",
+               cp.name.c_str());
+    return launch<4, 48, 5, true, false, false, true>(ctx, a);
+  }
 #define FV_LAUNCH(R_, N_, S_) \
   (res ? (fu ? launch<R_, N_, S_, true, true>(ctx, a) : launch<R_, N_, S_, true, false>(ctx, a)) \
        : (fu ? launch<R_, N_, S_, false, true>(ctx, a) : launch<R_, N_, S_, false, false>(ctx, a)))

@@ -210,6 +210,7 @@ struct ConvParam {
   float* b_dev = nullptr;   // bias (n_pad) fp32
   bool center_only = false;   // used as a 1x1 conv (K-stage logits at levels > 0)
   bool row_fused = false;     // B image stacked by dy for row-fused MMAs (conv_tc.cu)
+  bool tapn = false;          // K-stage level 0: 3x3 taps of D.head in N, one MMA per halo row
   double macs_per_px = 0;     // algorithmic MACs per output pixel (0: cin * cout * ksize^2)
   std::vector<float> w_host;  // reference layout (oc,ic,kh,kw), fp16-rounded values
   std::vector<float> b_host;

@@ -1635,10 +1635,19 @@ int launch_shadow_dir_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int
 // samples and 6 blocks/SM (+37% / +17%).
 int launch_shadow_dir(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
   static const int refill = getenv("FV_SHADOW_REFILL") ? std::min(32, std::max(1, atoi(getenv("FV_SHADOW_REFILL")))) : 8;
-  static const int lin_u = getenv("FV_SHADOW_LIN_U") ? atoi(getenv("FV_SHADOW_LIN_U")) : 4;
+  // filtered samples: (samples in flight per lane, resident blocks per SM) -- FV_SHADOW_LIN=U,B (A/B)
+  static const int lin_cfg = getenv("FV_SHADOW_LIN") ? atoi(getenv("FV_SHADOW_LIN")) * 100 +
+                                                           atoi(strchr(getenv("FV_SHADOW_LIN"), ',') + 1)
+                                                     : 408;
   if (F.V.ltex) {
-    if (lin_u == 8) return launch_shadow_dir_t<8, 8, true>(ctx, F, B, threads, refill);
-    return launch_shadow_dir_t<4, 8, true>(ctx, F, B, threads, refill);
+    switch (lin_cfg) {
+      case 808: return launch_shadow_dir_t<8, 8, true>(ctx, F, B, threads, refill);
+      case 412: return launch_shadow_dir_t<4, 12, true>(ctx, F, B, threads, refill);
+      case 812: return launch_shadow_dir_t<8, 12, true>(ctx, F, B, threads, refill);
+      case 416: return launch_shadow_dir_t<4, 16, true>(ctx, F, B, threads, refill);
+      case 610: return launch_shadow_dir_t<6, 10, true>(ctx, F, B, threads, refill);
+      default: return launch_shadow_dir_t<4, 8, true>(ctx, F, B, threads, refill);
+    }
   }
   return launch_shadow_dir_t<4, 8>(ctx, F, B, threads, refill);
 }

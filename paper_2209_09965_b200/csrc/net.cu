@@ -115,6 +115,17 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
     }
     cp.w_set = cp.b_set = true;
     cp.center_only = L > 0;
+    // FV_K0_TAPN=1: level 0 with D.head's nine taps in N next to the logits (conv_tc.cu, TAPN).
+    // Measured at C3 (per-launch CUDA events, 8 frames): 124.3 us against 100.7 us for the default
+    // row-fused 32-column conv -- the MMA work drops ~4x but the launch is bound by its epilogue
+    // (three TMEM rows read per output row, 21 scattered stores per pixel) and the single-buffered
+    // 288-column accumulator; kept opt-in as the measured alternative.
+    static const bool tapn = getenv("FV_K0_TAPN") && atoi(getenv("FV_K0_TAPN")) == 1;
+    cp.tapn = L == 0 && tapn && cin <= 64;
+    if (cp.tapn) {
+      cp.n_pad = 48;
+      cp.b_host.resize(48, 0.f);
+    }
     cp.macs_per_px = (L == 0 ? 27.0 * cin : 0.0) + 9.0 * cin * s;  // D.head 3x3 + s 1x1 logit convs
     const int rc = conv_prepare(ctx, cp);
     if (rc) return rc;
