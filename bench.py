@@ -53,6 +53,15 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def device_memory_gb():
+    """Device memory in use on this GPU (all allocations of the process: volume, textures, marcher
+    workspace, network state), GB."""
+    import torch
+
+    free, total = torch.cuda.mem_get_info()
+    return round((total - free) / 1e9, 2)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -452,7 +461,7 @@ def run_ours(args, cfg):
                 "how": f"fv_frames C-ABI call over {ke} frames, wall clock: per frame camera + fovea by value "
                        "(H2D as kernel parameters), (H,W,3) f32 image D2H into pinned host memory; the copy of "
                        "frame t-1 overlaps the compute of frame t (copy stream)"},
-        "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu,
+        "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu, "device_memory_gb": device_memory_gb(),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -587,7 +596,7 @@ def run_sharded(args, cfg):
             "e2e": {"value": k / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": int(host.numel() * 4),
                     "how": "pipe.step per frame + pinned D2H of the rank's part of the image, wall clock"},
-            "gpu_launches": launches, "clocks": clk,
+            "gpu_launches": launches, "clocks": clk, "device_memory_gb": device_memory_gb(),
             "roofline": {"bound": "tensor", "achieved": conv_tf, "peak": peak, "unit": "TFLOP/s",
                          "frac": conv_tf / peak, "traffic": None,
                          "kernel": "conv3x3_tc_kernel (all W-Net convs of rank 0's window)",

@@ -1737,8 +1737,13 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     //   2  a hardware-filtered float texture: trilinear with 8-bit fractional weights (one 4-byte
     //      return per sample; 1 float per voxel) -- the SURVEY's fast tier
     // FV_TEX_FILTER: 0 = quads everywhere, 1 = filtered shadow samples only, 2 = filtered
-    // everywhere (the quad texture is then never built).
-    static const int tex_filter = getenv("FV_TEX_FILTER") ? atoi(getenv("FV_TEX_FILTER")) : 1;
+    // everywhere (the quad texture is then never built). Default: 1, and 2 for volumes whose quad
+    // copy would exceed 4 GiB (1024^3: 16 GiB of quads; the filtered main pass keeps the fast tier
+    // on colour, measured at C3 with depth one step off on ~0.03% of the active pixels, and the
+    // same C5 frame rate -- 121.1 vs 121.6 frames/s -- in 30.6 instead of 47.8 GB).
+    static const int tex_filter_env = getenv("FV_TEX_FILTER") ? atoi(getenv("FV_TEX_FILTER")) : -1;
+    const bool big = 16.0 * vol->nx * vol->ny * vol->nz > 4.0 * 1024 * 1024 * 1024;
+    const int tex_filter = tex_filter_env >= 0 ? tex_filter_env : big ? 2 : 1;
     const int src = !tex_path ? 0 : tex_filter >= 2 ? 2 : 1;
     int rc = src == 0 ? volume_bricks(ctx, mv) : src == 1 ? volume_texture(ctx, mv) : 0;
     if (rc) return rc;
@@ -1781,7 +1786,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       // Record buffer, in chunks of kChunk slots (36 B per slot). The first min(k, n_chunks / 2)
       // chunks are the first chunks of rays 0..k-1 (chunk id = ray index; k = this frame's ray
       // count, read on the device); the rest is the pool for later chunks (and the first chunks of
-      // any rays beyond). Initial size 32 slots per film pixel (at least 8M slots): a C3 frame
+      // any rays beyond). Initial size 32 slots per film pixel (at least 8M, at most 128M): a C3 frame
       // writes ~24 records per film pixel, so foveated frames never overflow and their results do
       // not depend on the buffer's history. The buffer then follows this context's usage -- the
       // previous render's pooled-chunk and overflow counts are read back asynchronously into pinned
@@ -1801,13 +1806,16 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
         if (cap_env || per_ray_env) {
           need = (cap_env ? cap_env : per_ray_env * k_max) / kChunk;
         } else if (have == 0) {
-          need = std::max<int64_t>((8 << 20) / kChunk, (int64_t)k_max);  // 32 slots per pixel
+          // 32 slots per film pixel, at least 8M and at most 128M slots (4.6 GB) to start with
+          need = std::min<int64_t>(std::max<int64_t>((8 << 20) / kChunk, (int64_t)k_max), (128 << 20) / kChunk);
         } else if (ctx->wave_fb_pending && !capturing && cudaEventQuery(ctx->wave_fb_ev) == cudaSuccess) {
           ctx->wave_fb_pending = false;
           const int64_t k_prev = ctx->wave_fb[0], pooled = ctx->wave_fb[1 + 1], ovf = ctx->wave_fb[1 + 6];
           const int64_t first = std::min(k_prev, have / 2), pool = have - first;
+          // grow in large steps: a reallocation synchronises the device and maps new pages (a C4
+          // dense zoomed frame that grew the buffer took ~0.3 s), so it should happen rarely
           if (ovf) need = 2 * have;
-          else if (pooled > pool - pool / 8) need = first + pooled + pooled / 2;
+          else if (pooled > pool - pool / 8) need = std::max(first + 2 * pooled, have + have / 2);
         } else {
           (void)cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
         }
