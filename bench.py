@@ -450,11 +450,12 @@ def run_ours(args, cfg):
         "phase_ms": {"mask": mask_ms, "march": march_ms, "reconstruct": net_ms},
         "timing": {"pipelined_ms_per_frame": pipe_ms / k, "serial_ms_per_frame": serial_ms / k,
                    "serial_fps": whole_job_rate(k, world, serial_ms / 1e3),
-                   "how": "value = K frames through the frame loop (FramePipeline.run_pipelined: march and "
-                          "network in frame order on one stream, the network replayed as a CUDA graph, frame "
-                          "t+1's mask on a side stream next to frame t's network; FV_PIPE_OVERLAP=1 renders "
-                          "t+1 on a second stream), CUDA events on the pipeline stream; phase_ms from the "
-                          "same frames in serial order with events between the phases"},
+                   "how": "value = K frames through the frame loop (FramePipeline.run_pipelined -> the C ABI's "
+                          "fv_frames: each frame one replayed CUDA graph -- frame t's network with frame t+1's "
+                          "mask + march forked off it after its first convs (FV_MARCH_AHEAD), the per-frame "
+                          "camera / fovea read from a device parameter block), CUDA events on the pipeline "
+                          "stream; phase_ms from the same frames in serial order with events between the "
+                          "phases"},
         "roofline": roof, "stages": stages, "kernels": kernels, "marcher": marcher,
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": h * w * 3 * 4, "serial_fv_frame_fps": e2e_serial_fps,

@@ -524,6 +524,38 @@ static int frame_body(fv_ctx* ctx, cudaStream_t s_main, cudaStream_t s_side, cud
   return 0;
 }
 
+// March-ahead variant (FV_MARCH_AHEAD=k): the graph of frame t holds frame t's network and, forked
+// after its k-th conv launch, frame t+1's mask + march into the other input buffer -- the render of
+// the next frame fills the SMs the network's small levels leave idle. (Both write disjoint bytes of
+// that buffer: the mask channels 0..4, the march channels 0..3 of active pixels, the network's
+// D.head feedback channels 5..7; the network reads only the current buffer.)
+static int frame_body_ahead(fv_ctx* ctx, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t ev_fork,
+                            cudaEvent_t ev_join, const fv_volume* vol, const fv_net* net, fv_state* st,
+                            const fv_camera* cam_next, const fv_light* light, const fv_settings* settings,
+                            const fv_fovea* fovea_next, int frame_next, float* img, int fork_at) {
+  const int64_t npix = (int64_t)st->H * st->W;
+  ctx->stream = s_main;
+  ctx->conv_fork_ev = ev_fork;
+  ctx->conv_fork_at = fork_at;
+  ctx->conv_count = 0;
+  int rc = reconstruct_launches(ctx, const_cast<fv_net*>(net), st, 1, img, nullptr, nullptr);
+  ctx->conv_fork_ev = nullptr;
+  if (rc) return rc;
+  if (ctx->conv_count < fork_at) FV_CUDA(cudaEventRecord(ev_fork, s_main));
+  FV_CUDA(cudaStreamWaitEvent(s_side, ev_fork, 0));
+  ctx->stream = s_side;
+  rc = launch_mask_compact(ctx, frame_next, st->H, st->W, fovea_next, nullptr, nullptr, ctx->idx_scratch,
+                           ctx->k_scratch, st->xalt.p, st->Wp);
+  if (!rc)
+    rc = launch_render(ctx, vol, cam_next, light, settings, ctx->idx_scratch, ctx->k_scratch, (int)npix, nullptr,
+                       nullptr, st->xalt.p, st->Wp);
+  if (rc) return rc;
+  FV_CUDA(cudaEventRecord(ev_join, s_side));
+  ctx->stream = s_main;
+  FV_CUDA(cudaStreamWaitEvent(s_main, ev_join, 0));
+  return 0;
+}
+
 static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st, int n,
                         const fv_camera* cams, const fv_light* light, const fv_settings* settings,
                         const fv_fovea* foveas, const int* frame_ids, float* const* host_rgb_out) {
@@ -548,10 +580,19 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   cudaEvent_t fork = ctx->fev[8], join = ctx->fev[9];
   FV_CUDA(cudaEventRecord(ctx->fev[6], own));
   for (cudaStream_t s_ : {s_n, s_m, s_c}) FV_CUDA(cudaStreamWaitEvent(s_, ctx->fev[6], 0));
-  // prologue: frame 0's mask (by-value parameters)
+  // frame t+1's mask + march forked off frame t's network after its 4th conv (E1.conv2: the march
+  // then runs next to the network's level 1-3 convs, which leave SMs idle). A/B at C3 (frames/s,
+  // e2e), fork after conv 0 (off) / 2 / 4 / 6 / 8: 547.8 / 559.6 / 579.1 / 583.0 / 585.4 and e2e
+  // 498 / 506 / 520 / 514 / 492 (later forks collide with the level-0 decoder convs); frames are
+  // bit-identical for every fork point. FV_MARCH_AHEAD=0: the march in line before the network.
+  static const int ahead = getenv("FV_MARCH_AHEAD") ? atoi(getenv("FV_MARCH_AHEAD")) : 4;
+  // prologue: frame 0's mask (and with march-ahead its march), by-value parameters
   ctx->stream = s_n;
   rc = launch_mask_compact(ctx, frame_ids[0], H, W, &foveas[0], nullptr, nullptr, ctx->idx_scratch, ctx->k_scratch,
                            st->x.p, st->Wp);
+  if (!rc && ahead > 0)
+    rc = launch_render(ctx, vol, &cams[0], light, settings, ctx->idx_scratch, ctx->k_scratch, (int)npix, nullptr,
+                       nullptr, st->x.p, st->Wp);
   static uint64_t dyn_seq = 0;
 // inside the frame loop: record the failure and leave the loop (streams are restored below)
 #define FG_TRY(call)                 \
@@ -570,7 +611,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     const int slot = (int)(dyn_seq++ % kDynRing);
     FG_TRY(cudaEventSynchronize(ctx->dyn_ev[slot]));
     FrameDyn& d = ctx->dyn_host[slot];
-    rc = fill_camera_dyn(&cams[t], &d);
+    rc = fill_camera_dyn(&cams[ahead > 0 ? tn : t], &d);
     if (rc) break;
     d.fx = foveas[tn].focus[0]; d.fy = foveas[tn].focus[1]; d.sigma = foveas[tn].sigma;
     d.pb = foveas[tn].base_density; d.scale = foveas[tn].pixel_scale;
@@ -584,7 +625,8 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     fv_state::FrameGraph* g = nullptr;
     for (auto& e : st->fgraphs)
       if (e.vol == vol && e.net == net && e.version == net->version && e.wave_version == ctx->wave_version &&
-          e.x == st->x.p && e.parity == st->parity && e.img == img && e.has_light == (light != nullptr) &&
+          e.x == st->x.p && e.parity == st->parity && e.ahead == ahead && e.img == img &&
+          e.has_light == (light != nullptr) &&
           (!light || memcmp(&e.light, light, sizeof(fv_light)) == 0) &&
           memcmp(&e.settings, settings, sizeof(fv_settings)) == 0) {
         g = &e;
@@ -598,7 +640,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       }
       fv_state::FrameGraph e;
       e.vol = vol; e.net = net; e.version = net->version; e.wave_version = ctx->wave_version; e.x = st->x.p;
-      e.parity = st->parity; e.img = img; e.has_light = light != nullptr;
+      e.parity = st->parity; e.ahead = ahead; e.img = img; e.has_light = light != nullptr;
       if (light) e.light = *light;
       e.settings = *settings;
       st->fgraphs.push_back(e);
@@ -615,8 +657,10 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       const unsigned long long before = ctx->launches;
       cudaError_t e = cudaStreamBeginCapture(st->fcap[0], cudaStreamCaptureModeThreadLocal);
       if (e == cudaSuccess) {
-        rc = frame_body(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st, &cams[t], light,
-                        settings, &foveas[tn], frame_ids[tn], img);
+        rc = ahead > 0 ? frame_body_ahead(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st,
+                                          &cams[tn], light, settings, &foveas[tn], frame_ids[tn], img, ahead)
+                       : frame_body(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st,
+                                    &cams[t], light, settings, &foveas[tn], frame_ids[tn], img);
         e = cudaStreamEndCapture(st->fcap[0], &graph);
       }
       if (!rc && e != cudaSuccess) rc = cuda_fail(e, "frame graph capture");
@@ -630,6 +674,9 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
         e = cudaGraphLaunch(g->exec, s_n);
         if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphLaunch (frame)");
       }
+    } else if (ahead > 0) {
+      rc = frame_body_ahead(ctx, s_n, s_m, fork, join, vol, net, st, &cams[tn], light, settings, &foveas[tn],
+                            frame_ids[tn], img, ahead);
     } else {
       rc = frame_body(ctx, s_n, s_m, fork, join, vol, net, st, &cams[t], light, settings, &foveas[tn],
                       frame_ids[tn], img);

@@ -647,6 +647,8 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   ktime_begin(ctx);
   fv::launch_pdl(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN>, grid, kThreads, C::kSmem, ctx->stream, a);
   ktime_end(ctx, FV_KC_CONV, a.flops);
+  if (ctx->conv_fork_ev && ++ctx->conv_count == ctx->conv_fork_at)
+    FV_CUDA(cudaEventRecord(ctx->conv_fork_ev, ctx->stream));
   if (a.prof) {
     std::vector<unsigned long long> h((size_t)grid * kProfSlots);
     FV_CUDA(cudaMemcpyAsync(h.data(), a.prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));

@@ -162,6 +162,9 @@ struct fv_ctx {
   fv::FrameDyn* dyn_host = nullptr;  // kDynRing slots
   cudaEvent_t dyn_ev[8] = {};
   uint64_t wave_version = 0;  // bumped when the marcher record buffer is reallocated
+  // march-ahead frames (fv_frames, FV_MARCH_AHEAD=k): record conv_fork_ev after the k-th conv launch
+  cudaEvent_t conv_fork_ev = nullptr;
+  int conv_fork_at = 0, conv_count = 0;
   // fv_frames: render / network / copy streams and their event rings (created on first use)
   cudaStream_t fstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t fev[10] = {};
@@ -306,7 +309,7 @@ struct fv_state {
     const fv_net* net = nullptr;
     uint64_t version = 0, wave_version = 0;
     const void* x = nullptr;
-    int parity = 0;
+    int parity = 0, ahead = 0;
     const float* img = nullptr;
     fv_light light{};
     int has_light = 0;

@@ -1815,7 +1815,7 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
           // grow in large steps: a reallocation synchronises the device and maps new pages (a C4
           // dense zoomed frame that grew the buffer took ~0.3 s), so it should happen rarely
           if (ovf) need = 2 * have;
-          else if (pooled > pool - pool / 8) need = std::max(first + 2 * pooled, have + have / 2);
+          else if (pooled > pool - pool / 8) need = std::max(first + 2 * pooled, 2 * have);
         } else {
           (void)cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
         }

@@ -758,11 +758,12 @@ def test_graph_replay_equals_eager_launches(tmp_path):
     assert np.array_equal(outs["1"][7:], outs["1"][:6])  # fv_frames (graphs) == the stepped frames
 
 
-@pytest.mark.parametrize("knob", ["FV_KCHAIN", "FV_PDL", "FV_MASK_AHEAD"])
+@pytest.mark.parametrize("knob", ["FV_KCHAIN", "FV_PDL", "FV_MASK_AHEAD", "FV_MARCH_AHEAD"])
 def test_launch_variants_give_identical_frames(tmp_path, knob):
     """The fused K-stage chain (one cooperative launch for the levels between the first and last K
-    block) and the programmatic-dependent launches leave every frame bit-identical: the same
-    frames with the knob off (separate launches / plain stream order) and on (the default)."""
+    block), the programmatic-dependent launches, the next frame's mask next to the network and the
+    next frame's march forked off the network (FV_MARCH_AHEAD: after its first conv here) leave
+    every frame bit-identical: the same frames with the knob off and on."""
     import os
     import subprocess
     import sys

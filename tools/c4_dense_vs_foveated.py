@@ -41,8 +41,8 @@ def gaze(i):
 ctx = pipe.ctx
 s = ctx.stream
 # warm-up: textures, workspaces, and the marcher's record buffer grown to the orbit's largest
-# frames (every 10th frame, dense and foveated) so the timed pass measures the steady state
-for i in range(0, frames, 10):
+# frames (every 5th frame, dense and foveated) so the timed pass measures the steady state
+for i in range(0, frames, 5):
     pipe.dense(cams[i])
     pipe.step(cams[i], gaze(i), i)
 torch.cuda.synchronize()
