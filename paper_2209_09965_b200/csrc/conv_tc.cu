@@ -627,6 +627,348 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
   }
 }
 
+// ---- CTA pairs (cta_group::2) for the cout = 64 row-fused convs -----------------------------------
+// A 2-CTA cluster runs one 128 x (2 x 4)-pixel tile pair: CTA c holds output rows [4c, 4c + 4) of the
+// pair's eight and its own A halo; the leader's elected thread issues tcgen05.mma.cta_group::2 with
+// M = 256 (each CTA's 128 pixels), and B's N columns are split between the two CTAs' shared memory.
+// Each CTA therefore streams HALF of the weight operand per MMA: the per-SM operand reads of a
+// K-stage drop from 72 KB A + 72 KB B to 72 KB + 36 KB (the single-CTA engine is bound by exactly
+// these reads at ~107 B/cycle). The row-fused windows ([dy_lo, dy_hi] x 64 columns) are the same in
+// both CTAs (the same relative halo row), so each CTA keeps, per dx, its half of each of the six
+// window types as a contiguous block ([n/8][k-half][8][8] fp16: LBO 128 B, SBO 256 B).
+// Synchronisation: each CTA's copies complete on its own full barrier; the peer's (idle) MMA warp
+// forwards its full / resident-weight phases to the leader with remote mbarrier arrivals; the
+// leader's commits multicast to both CTAs' empty and accumulator-full barriers; both CTAs'
+// epilogue warps release the accumulator on the leader's barrier.
+constexpr int kPairWinCols[6] = {32, 32, 32, 64, 64, 96};  // half-window widths: [0] [1] [2] [01] [12] [012]
+constexpr int kPairWinOff[6] = {0, 32, 64, 96, 160, 224};
+__host__ __device__ constexpr int pair_win_off(int wt) {
+  return wt == 0 ? 0 : wt == 1 ? 32 : wt == 2 ? 64 : wt == 3 ? 96 : wt == 4 ? 160 : 224;
+}
+constexpr int kPairDxCols = 320;
+constexpr int kPairStageBytes = 3 * kPairDxCols * 32;  // per CTA per K-stage: 30 KB
+__host__ __device__ constexpr int pair_win(int lo, int hi) {
+  return lo == hi ? lo : (hi - lo == 1 ? 3 + lo : 5);
+}
+
+template <int S, bool BRES>
+struct PairCfg {
+  static constexpr int R = 4, N = 64;
+  static constexpr int kABytes = kStageGroups * (R + 2) * kRowBytes;
+  static constexpr int kPlaneBytes = (R + 2) * kRowBytes;
+  static constexpr int kBSlots = BRES ? kBResStages : S;
+  static constexpr int kSmem = S * kABytes + kBSlots * kPairStageBytes + 1024 + 256 + N * 4;
+};
+
+template <int S, bool BRES>
+__global__ void __launch_bounds__(kThreads, 1) conv3x3_pair_kernel(ConvArgs a) {
+  using C = PairCfg<S, BRES>;
+  constexpr int R = 4, N = 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * C::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::kBSlots * kPairStageBytes);
+  // bars: full[S], empty[S], pairfull[S], tfull[2], tempty[2], bres, pairbres
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 6);
+  float* s_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
+  const uint32_t bar_full = sm100::smem_u32(bars);
+  const uint32_t bar_empty = bar_full + 8 * S;
+  const uint32_t bar_pfull = bar_empty + 8 * S;
+  const uint32_t bar_tfull = bar_pfull + 8 * S;
+  const uint32_t bar_tempty = bar_tfull + 16;
+  const uint32_t bar_bres = bar_tempty + 16;
+  const uint32_t bar_pbres = bar_bres + 8;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = sm100::cluster_ctarank();
+  const bool leader = rank == 0;
+
+  if (threadIdx.x == 0) {
+    for (int s_ = 0; s_ < S; ++s_) {
+      sm100::mbar_init(bar_full + 8 * s_, 2);
+      sm100::mbar_init(bar_empty + 8 * s_, 1);
+      sm100::mbar_init(bar_pfull + 8 * s_, 1);
+    }
+    for (int s_ = 0; s_ < 2; ++s_) {
+      sm100::mbar_init(bar_tfull + 8 * s_, 1);
+      sm100::mbar_init(bar_tempty + 8 * s_, 2 * kEpiWarps);
+    }
+    sm100::mbar_init(bar_bres, 1);
+    sm100::mbar_init(bar_pbres, 1);
+    sm100::fence_mbar_init();
+    if (BRES) {
+      const uint32_t wb = (uint32_t)(a.n_kstages * kPairStageBytes);
+      sm100::mbar_arrive_expect_tx(bar_bres, wb);
+      // this CTA's halves: stage s at image offset (2 s + rank) * kPairStageBytes
+      for (int s_ = 0; s_ < a.n_kstages; ++s_)
+        sm100::bulk_g2s(sm100::smem_u32(sB + s_ * kPairStageBytes),
+                        reinterpret_cast<const uint8_t*>(a.wimg) + (int64_t)(2 * s_ + rank) * kPairStageBytes,
+                        kPairStageBytes, bar_bres);
+    }
+  }
+  if (warp == 1) sm100::tmem_alloc_pair<512>(sm100::smem_u32(tmem_slot));
+  sm100::tc_fence_before();
+  sm100::cluster_sync();  // both CTAs' barriers initialised before any remote arrival
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  fv::pdl_wait();
+
+  const int pair_rows = 2 * R;
+  const int tiles_py = (a.H + pair_rows - 1) / pair_rows;
+  const int n_tiles = a.tiles_x * tiles_py;
+  const int cluster = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+
+  if (warp == 0) {
+    // ---------------- producer (both CTAs): this CTA's halo rows + (streamed) its B halves ----------------
+    int it = 0;
+    for (int tile = cluster; tile < n_tiles; tile += n_clusters) {
+      const int x0 = (tile % a.tiles_x) * kTileW;
+      const int y0 = (tile / a.tiles_x) * pair_rows + (int)rank * R;
+      const int rows_in = max(0, min(R + 1, a.H - y0) - max(0, 1 - y0) + 1);
+      const int lo = max(x0 - 1, 0), hi = min(x0 + kTileW + 1, a.W);
+      const uint32_t tile_bytes_per_group = hi > lo ? (uint32_t)(rows_in * (hi - lo) * 16) : 0u;
+      for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
+        const int st = it % S;
+        const uint32_t round = it / S;
+        sm100::mbar_wait(bar_empty + 8 * st, (round & 1) ^ 1);
+        const int g0 = ks * kStageGroups;
+        int gs = a.groups - g0;
+        if (gs > kStageGroups) gs = kStageGroups;
+        const int gs_fill = (gs + 1) & ~1;
+        const int n_items = gs_fill * (R + 2);
+        const uint32_t tot = (uint32_t)gs * tile_bytes_per_group;
+        const uint32_t b_bytes = BRES ? 0u : (uint32_t)kPairStageBytes;
+        if (lane == 0) sm100::mbar_arrive_expect_tx(bar_full + 8 * st, tot + b_bytes);
+        const uint32_t a_st = sm100::smem_u32(sA + st * C::kABytes);
+        if (!BRES && lane == 0)
+          sm100::bulk_g2s(sm100::smem_u32(sB + st * kPairStageBytes),
+                          reinterpret_cast<const uint8_t*>(a.wimg) + (int64_t)(2 * ks + rank) * kPairStageBytes,
+                          b_bytes, bar_full + 8 * st);
+        for (int item = lane; item < n_items; item += 32) {
+          const int g = item / (R + 2), row = item % (R + 2);
+          const int y = y0 - 1 + row;
+          const uint32_t row_addr = a_st + g * C::kPlaneBytes + row * kRowBytes;
+          const int gg = g0 + g;
+          if (gg < a.groups && y >= 0 && y < a.H) {
+            int s_ = 0, gl = gg;
+            while (s_ + 1 < a.n_src && gl >= a.src_groups[s_]) { gl -= a.src_groups[s_]; ++s_; }
+            const __half* plane = a.src[s_] + (int64_t)gl * a.H * a.W * 8;
+            const int c_lo = lo - (x0 - 1), c_hi = hi - (x0 - 1);
+            if (hi > lo)
+              sm100::bulk_g2s(row_addr + c_lo * 16, plane + ((int64_t)y * a.W + lo) * 8, (uint32_t)(hi - lo) * 16u,
+                              bar_full + 8 * st);
+            for (int c = 0; c < c_lo; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+            for (int c = max(c_hi, 0); c < kHaloW; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+          } else {
+            for (int c = 0; c < kHaloW; ++c) sm100::st_shared_zero16(row_addr + c * 16);
+          }
+        }
+        sm100::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(bar_full + 8 * st);
+      }
+    }
+  } else if (warp == 1 && !leader) {
+    // ---------------- peer: forward this CTA's operand phases to the leader ----------------
+    if (BRES) {
+      sm100::mbar_wait(bar_bres, 0);
+      if (lane == 0) sm100::mbar_arrive_cluster(sm100::mapa_shared(bar_pbres, 0));
+    }
+    int it = 0;
+    for (int tile = cluster; tile < n_tiles; tile += n_clusters)
+      for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
+        const int st = it % S;
+        sm100::mbar_wait(bar_full + 8 * st, (it / S) & 1);
+        if (lane == 0) sm100::mbar_arrive_cluster(sm100::mapa_shared(bar_pfull + 8 * st, 0));
+      }
+  } else if (warp == 1) {
+    // ---------------- leader: MMA issue for the pair ----------------
+    if (BRES) {
+      sm100::mbar_wait(bar_bres, 0);
+      sm100::mbar_wait(bar_pbres, 0);
+    }
+    int it = 0, lt = 0;
+    for (int tile = cluster; tile < n_tiles; tile += n_clusters, ++lt) {
+      const int acc = lt & 1;
+      sm100::mbar_wait(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
+      sm100::tc_fence_after();
+      const uint32_t d_base = tmem_base + acc * R * N;
+      for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
+        const int st = it % S;
+        const uint32_t par = (it / S) & 1;
+        sm100::mbar_wait(bar_full + 8 * st, par);
+        sm100::mbar_wait(bar_pfull + 8 * st, par);
+        sm100::tc_fence_after();
+        const uint64_t a0 = sm100::smem_desc(sm100::smem_u32(sA + st * C::kABytes), C::kPlaneBytes, 128);
+        const uint32_t b_stage = sm100::smem_u32(sB + (BRES ? ks : st) * kPairStageBytes);
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int it2 = 0; it2 < 3 * (R + 2); ++it2) {
+            const int h = it2 % (R + 2), dx = it2 / (R + 2);
+            const int dy_lo = h - R + 1 > 0 ? h - R + 1 : 0;
+            const int dy_hi = h < 2 ? h : 2;
+            const int r_first = h - dy_lo;
+            const uint64_t ad = a0 + (uint64_t)(((h * kHaloW + dx) * 16) >> 4);
+            const uint32_t d0 = d_base + (R - 1 - r_first) * N;
+            const uint32_t bdx = b_stage + dx * kPairDxCols * 32;
+            if (ks == 0 && dx == 0 && dy_lo == 0) {
+              // row h's first contribution (dy = 0) overwrites; the older rows accumulate
+              sm100::mma_f16_pair(d0, ad, sm100::smem_desc(bdx + pair_win_off(0) * 32, 128, 256),
+                                  sm100::idesc_f16(256, N), 0u);
+              if (dy_hi >= 1)
+                sm100::mma_f16_pair(d0 + N, ad,
+                                    sm100::smem_desc(bdx + pair_win_off(pair_win(1, dy_hi)) * 32, 128, 256),
+                                    sm100::idesc_f16(256, dy_hi * N), 1u);
+            } else {
+              sm100::mma_f16_pair(d0, ad, sm100::smem_desc(bdx + pair_win_off(pair_win(dy_lo, dy_hi)) * 32, 128, 256),
+                                  sm100::idesc_f16(256, (dy_hi - dy_lo + 1) * N), 1u);
+            }
+          }
+        }
+        __syncwarp();
+        sm100::mma_commit_pair_elect(bar_empty + 8 * st);
+        __syncwarp();
+      }
+      sm100::mma_commit_pair_elect(bar_tfull + 8 * acc);
+      __syncwarp();
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue (both CTAs): this CTA's 4 rows of the pair ----------------
+    for (int i = threadIdx.x - 64; i < N; i += kEpiWarps * 32) s_bias[i] = __ldg(a.bias + i);
+    sm100::named_bar_sync(1, kEpiWarps * 32);
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int64_t plane = (int64_t)a.H * a.W * 8;
+    const int Hp = a.H >> 1, Wp = a.W >> 1;
+    const int64_t pplane = (int64_t)Hp * Wp * 8;
+    const uint32_t tempty_leader = sm100::mapa_shared(bar_tempty, 0);
+    int lt = 0;
+    for (int tile = cluster; tile < n_tiles; tile += n_clusters, ++lt) {
+      const int acc = lt & 1;
+      const int x0 = (tile % a.tiles_x) * kTileW;
+      const int y0 = (tile / a.tiles_x) * pair_rows + (int)rank * R;
+      sm100::mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
+      sm100::tc_fence_after();
+      const int x = x0 + 32 * q + lane;
+      const bool xin = x < a.W;
+      const uint32_t t_row0 = tmem_base + ((uint32_t)(32 * q) << 16) + acc * R * N;
+      constexpr int kCb = N / 16;
+#pragma unroll 1
+      for (int item = half; item < (R / 2) * kCb; item += 2) {
+        const int r = 2 * (item / kCb);
+        const int cb = 16 * (item % kCb);
+        const int y = y0 + r;
+        float v0[16], v1[16];
+        {
+          uint32_t r0[16], r1[16];
+          sm100::tmem_ld16_nowait(t_row0 + (R - 1 - r) * N + cb, r0);
+          sm100::tmem_ld16_nowait(t_row0 + (R - 2 - r) * N + cb, r1);
+          sm100::tmem_wait_ld_regs(r0, r1);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) { v0[j] = __uint_as_float(r0[j]); v1[j] = __uint_as_float(r1[j]); }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float b = s_bias[cb + j];
+          v0[j] += b;
+          v1[j] += b;
+          if (a.relu) { v0[j] = fmaxf(v0[j], 0.f); v1[j] = fmaxf(v1[j], 0.f); }
+        }
+        if (xin) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int g = (cb >> 3) + hh;
+            if (8 * g >= a.cout) continue;
+            if (y < a.H) {
+              uint4 pk;
+              __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) p2[j] = __floats2half2_rn(v0[8 * hh + 2 * j], v0[8 * hh + 2 * j + 1]);
+              *reinterpret_cast<uint4*>(a.dst + g * plane + ((int64_t)y * a.W + x) * 8) = pk;
+            }
+            if (y + 1 < a.H) {
+              uint4 pk;
+              __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) p2[j] = __floats2half2_rn(v1[8 * hh + 2 * j], v1[8 * hh + 2 * j + 1]);
+              *reinterpret_cast<uint4*>(a.dst + g * plane + ((int64_t)(y + 1) * a.W + x) * 8) = pk;
+            }
+          }
+        }
+        if (a.pool_dst) {
+          float pv[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float nb0 = __shfl_xor_sync(0xffffffffu, v0[j], 1);
+            const float nb1 = __shfl_xor_sync(0xffffffffu, v1[j], 1);
+            pv[j] = 0.25f * (((v0[j] + v1[j]) + nb0) + nb1);
+          }
+          if (((lane & 1) == 0) && xin && y < a.H) {
+            const int px = x >> 1, py = y >> 1;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              if (cb + 8 * hh >= a.cout) continue;
+              uint4 pk;
+              __half2* p2 = reinterpret_cast<__half2*>(&pk);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) p2[j] = __floats2half2_rn(pv[8 * hh + 2 * j], pv[8 * hh + 2 * j + 1]);
+              *reinterpret_cast<uint4*>(a.pool_dst + ((cb >> 3) + hh) * pplane + ((int64_t)py * Wp + px) * 8) = pk;
+            }
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_cluster(tempty_leader + 8 * acc);
+    }
+  }
+  sm100::tc_fence_before();
+  sm100::cluster_sync();  // the pair's MMAs and both epilogues are done before the TMEM is freed
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
+template <int S, bool BRES>
+int launch_pair(fv_ctx* ctx, const ConvArgs& args) {
+  using C = PairCfg<S, BRES>;
+  static_assert(C::kSmem <= 227 * 1024, "pair conv configuration exceeds shared memory");
+  static bool attr_set = false;
+  if (!attr_set) {
+    FV_CUDA(cudaFuncSetAttribute(conv3x3_pair_kernel<S, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr_set = true;
+  }
+  ConvArgs a = args;
+  a.tiles_x = (a.W + kTileW - 1) / kTileW;
+  a.tiles_y = (a.H + 7) / 8;
+  const int n_pairs = a.tiles_x * a.tiles_y;
+  const int clusters = std::min(n_pairs, ctx->num_sms / 2);
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = fv::pdl_enabled() ? 1 : 0;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = 2;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = ctx->stream;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  ktime_begin(ctx);
+  FV_CUDA(cudaLaunchKernelEx(&cfg, conv3x3_pair_kernel<S, BRES>, a));
+  ktime_end(ctx, FV_KC_CONV, a.flops);
+  if (ctx->conv_fork_ev && ++ctx->conv_count == ctx->conv_fork_at)
+    FV_CUDA(cudaEventRecord(ctx->conv_fork_ev, ctx->stream));
+  FV_CHECK_LAUNCH("conv3x3_pair_kernel");
+  ctx->launches += 1;
+  return 0;
+}
+
 template <int R, int N, int S, bool BRES, bool FUSED, bool CO = false, bool TAPN = false>
 int launch(fv_ctx* ctx, const ConvArgs& args) {
   using C = Cfg<R, N, S, BRES, TAPN>;
@@ -675,6 +1017,9 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
   const int N = cp.n_pad;
   static const bool no_fuse = getenv("FV_CONV_FUSE") && atoi(getenv("FV_CONV_FUSE")) == 0;  // A/B runs
   cp.row_fused = !no_fuse && !cp.center_only && !cp.tapn && 3 * N <= 256;
+  // CTA pairs for the row-fused cout = 64 convs: opt-in FV_CONV_PAIR=1 (see conv3x3_pair_kernel)
+  static const bool pair_on = getenv("FV_CONV_PAIR") && atoi(getenv("FV_CONV_PAIR")) == 1;
+  cp.pair = pair_on && cp.row_fused && N == 64 && !cp.head_conv;
   cp.n_stages = (groups + kStageGroups - 1) / kStageGroups;
   cp.stage_groups.clear();
   cp.stage_off.clear();
@@ -687,8 +1032,29 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
     cp.stage_off.push_back(off);
     off += (int64_t)9 * kStageGroups * N * 16;  // stages strided at the full-stage size
   }
+  if (cp.pair) off = (int64_t)cp.n_stages * 2 * kPairStageBytes;  // [stage][rank][dx][320 cols][32 B]
   cp.wbytes = off;
   std::vector<__half> img(off / 2, __float2half(0.f));
+  for (int s = 0; s < cp.n_stages && cp.pair; ++s)
+    for (int rk = 0; rk < 2; ++rk)
+      for (int dx = 0; dx < 3; ++dx)
+        for (int wt = 0; wt < 6; ++wt) {
+          const int lo = wt < 3 ? wt : (wt == 3 ? 0 : (wt == 4 ? 1 : 0));
+          const int half_w = kPairWinCols[wt];
+          __half* base = img.data() + (((int64_t)(2 * s + rk) * 3 + dx) * kPairDxCols + kPairWinOff[wt]) * 16;
+          for (int j = 0; j < half_w; ++j) {
+            const int wj = rk * half_w + j;  // column of the full window
+            const int dy = lo + wj / 64, n = wj % 64;
+            const int t = dy * 3 + dx;
+            for (int kg = 0; kg < 2; ++kg)
+              for (int e = 0; e < 8; ++e) {
+                const int c = (s * kStageGroups + kg) * 8 + e;
+                const float w = (n < cp.cout && c < cp.cin) ? cp.w_host[((int64_t)n * cp.cin + c) * 9 + t] : 0.f;
+                // [n/8][kg][8 rows][8 elements]
+                base[((int64_t)(j / 8) * 2 + kg) * 64 + (j % 8) * 8 + e] = __float2half(w);
+              }
+          }
+        }
   for (int s = 0; s < cp.n_stages && cp.tapn; ++s) {
     // TAPN: [kg][n][8] per stage; column n -> (output o, tap t) of the K-stage layout (D.head
     // outputs 0..2 with their nine taps, the logits of the two K blocks at the centre tap)
@@ -706,7 +1072,7 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
         }
       }
   }
-  for (int s = 0; s < cp.n_stages && !cp.tapn; ++s) {
+  for (int s = 0; s < cp.n_stages && !cp.tapn && !cp.pair; ++s) {
     const int gs = cp.stage_groups[s];
     const int nk = gs / 2;
     __half* base = img.data() + cp.stage_off[s] / 2;
@@ -799,6 +1165,8 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
        : (fu ? launch<R_, N_, S_, false, true>(ctx, a) : launch<R_, N_, S_, false, false>(ctx, a)))
   if (a.center_only && cp.n_pad == 32 && !fu)  // (2-row tiles on the small levels: L2 16.9 -> 21.2 us, measured)
     return res ? launch<4, 32, 5, true, false, true>(ctx, a) : launch<4, 32, 5, false, false, true>(ctx, a);
+  if (cp.pair && !aux)
+    return res ? launch_pair<4, true>(ctx, a) : launch_pair<4, false>(ctx, a);
   switch (cp.n_pad) {
     case 16: return FV_LAUNCH(4, 16, 6);
     case 32: return FV_LAUNCH(4, 32, 5);

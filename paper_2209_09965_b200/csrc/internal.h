@@ -214,6 +214,8 @@ struct ConvParam {
   bool center_only = false;   // used as a 1x1 conv (K-stage logits at levels > 0)
   bool row_fused = false;     // B image stacked by dy for row-fused MMAs (conv_tc.cu)
   bool tapn = false;          // K-stage level 0: 3x3 taps of D.head in N, one MMA per halo row
+  bool pair = false;          // run as 2-CTA clusters with tcgen05 cta_group::2 (conv_tc.cu)
+  bool head_conv = false;     // a K-stage conv (auxiliary epilogue): never paired
   double macs_per_px = 0;     // algorithmic MACs per output pixel (0: cin * cout * ksize^2)
   std::vector<float> w_host;  // reference layout (oc,ic,kh,kw), fp16-rounded values
   std::vector<float> b_host;

@@ -115,6 +115,7 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
     }
     cp.w_set = cp.b_set = true;
     cp.center_only = L > 0;
+    cp.head_conv = true;
     // FV_K0_TAPN=1: level 0 with D.head's nine taps in N next to the logits (conv_tc.cu, TAPN).
     // Measured at C3 (per-launch CUDA events, 8 frames): 124.3 us against 100.7 us for the default
     // row-fused 32-column conv -- the MMA work drops ~4x but the launch is bound by its epilogue
