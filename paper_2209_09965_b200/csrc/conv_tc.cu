@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_pair_kernel(ConvArgs a) {
       for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
         const int st = it % S;
         const uint32_t round = it / S;
-        sm100::mbar_wait(bar_empty + 8 * st, (round & 1) ^ 1);
+        sm100::mbar_wait_cluster(bar_empty + 8 * st, (round & 1) ^ 1);  // released by the leader's commit
         const int g0 = ks * kStageGroups;
         int gs = a.groups - g0;
         if (gs > kStageGroups) gs = kStageGroups;
@@ -784,21 +784,32 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_pair_kernel(ConvArgs a) {
       }
   } else if (warp == 1) {
     // ---------------- leader: MMA issue for the pair ----------------
+    const bool prof = kProfileBuild && a.prof != nullptr;
+    unsigned long long w_full = 0, w_pfull = 0, w_tempty = 0;
+    const unsigned long long t_start = prof ? clock64() : 0ull;
     if (BRES) {
       sm100::mbar_wait(bar_bres, 0);
-      sm100::mbar_wait(bar_pbres, 0);
+      sm100::mbar_wait_cluster(bar_pbres, 0);
     }
     int it = 0, lt = 0;
     for (int tile = cluster; tile < n_tiles; tile += n_clusters, ++lt) {
       const int acc = lt & 1;
-      sm100::mbar_wait(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
+      {
+        const unsigned long long t0 = prof ? clock64() : 0ull;
+        sm100::mbar_wait_cluster(bar_tempty + 8 * acc, ((lt >> 1) & 1) ^ 1);
+        if (prof) w_tempty += clock64() - t0;
+      }
       sm100::tc_fence_after();
       const uint32_t d_base = tmem_base + acc * R * N;
       for (int ks = 0; ks < a.n_kstages; ++ks, ++it) {
         const int st = it % S;
         const uint32_t par = (it / S) & 1;
-        sm100::mbar_wait(bar_full + 8 * st, par);
-        sm100::mbar_wait(bar_pfull + 8 * st, par);
+        pwait(bar_full + 8 * st, par, prof, w_full);
+        {
+          const unsigned long long t0 = prof ? clock64() : 0ull;
+          sm100::mbar_wait_cluster(bar_pfull + 8 * st, par);
+          if (prof) w_pfull += clock64() - t0;
+        }
         sm100::tc_fence_after();
         const uint64_t a0 = sm100::smem_desc(sm100::smem_u32(sA + st * C::kABytes), C::kPlaneBytes, 128);
         const uint32_t b_stage = sm100::smem_u32(sB + (BRES ? ks : st) * kPairStageBytes);
@@ -833,6 +844,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_pair_kernel(ConvArgs a) {
       sm100::mma_commit_pair_elect(bar_tfull + 8 * acc);
       __syncwarp();
     }
+    if (prof && lane == 0) {
+      unsigned long long* o = a.prof + (int64_t)blockIdx.x * kProfSlots;
+      atomicAdd(o + 1, w_full);
+      atomicAdd(o + 0, w_pfull);  // (slot 0 = the peer-forward wait in the pair kernel)
+      atomicAdd(o + 2, w_tempty);
+      atomicAdd(o + 4, clock64() - t_start);
+      atomicAdd(o + 5, (unsigned long long)lt);
+    }
   } else if (warp >= 2) {
     // ---------------- epilogue (both CTAs): this CTA's 4 rows of the pair ----------------
     for (int i = threadIdx.x - 64; i < N; i += kEpiWarps * 32) s_bias[i] = __ldg(a.bias + i);
@@ -848,7 +867,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_pair_kernel(ConvArgs a) {
       const int acc = lt & 1;
       const int x0 = (tile % a.tiles_x) * kTileW;
       const int y0 = (tile / a.tiles_x) * pair_rows + (int)rank * R;
-      sm100::mbar_wait(bar_tfull + 8 * acc, (lt >> 1) & 1);
+      sm100::mbar_wait_cluster(bar_tfull + 8 * acc, (lt >> 1) & 1);  // the leader's commit
       sm100::tc_fence_after();
       const int x = x0 + 32 * q + lane;
       const bool xin = x < a.W;
@@ -962,6 +981,17 @@ int launch_pair(fv_ctx* ctx, const ConvArgs& args) {
   ktime_begin(ctx);
   FV_CUDA(cudaLaunchKernelEx(&cfg, conv3x3_pair_kernel<S, BRES>, a));
   ktime_end(ctx, FV_KC_CONV, a.flops);
+  if (a.prof) {
+    const int grid = 2 * clusters;
+    std::vector<unsigned long long> h((size_t)grid * kProfSlots);
+    FV_CUDA(cudaMemcpyAsync(h.data(), a.prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    FV_CUDA(cudaStreamSynchronize(ctx->stream));
+    double sm[kProfSlots] = {};
+    for (int b = 0; b < grid; b += 2)
+      for (int k = 0; k < kProfSlots; ++k) sm[k] += (double)h[(size_t)b * kProfSlots + k] / clusters;
+    fprintf(stderr, "[pair prof] %dx%d groups=%d: per leader %.1f tiles, total %.0f cyc; waits full %.0f peer %.0f tempty %.0f\n",
+            a.H, a.W, a.groups, sm[5], sm[4], sm[1], sm[0], sm[2]);
+  }
   if (ctx->conv_fork_ev && ++ctx->conv_count == ctx->conv_fork_at)
     FV_CUDA(cudaEventRecord(ctx->conv_fork_ev, ctx->stream));
   FV_CHECK_LAUNCH("conv3x3_pair_kernel");
