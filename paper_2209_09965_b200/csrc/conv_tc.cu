@@ -54,7 +54,7 @@ struct ConvArgs {
   int relu;
   int head;            // 1: aux epilogue (D.head and/or K-stage logits)
   float* od;           // head: (3, H, W) fp32 (nullable)
-  __half* feedback;    // head: NHWC8 net input, channels 5..7 (nullable)
+  __half* feedback;    // head: the next input's feedback group (internal.h kInGroups), nullable
   kw_t* kw[2];         // K-stage filter weights (9, H, W) per K block (nullable)
   int kcol[2];         // first logit column of each K block
   int center_only;     // 1x1 conv: only the centre tap's MMAs are issued
@@ -77,6 +77,17 @@ __device__ __forceinline__ void pwait(uint32_t bar, uint32_t parity, bool prof, 
   const unsigned long long t0 = clock64();
   sm100::mbar_wait(bar, parity);
   acc += clock64() - t0;
+}
+
+// one pixel of the input's feedback group: [O_d (3), 0 x 5], a whole 16-byte store
+__device__ __forceinline__ void feedback_store(__half* px, float o0, float o1, float o2) {
+  uint4 v;
+  __half2* h2 = reinterpret_cast<__half2*>(&v);
+  h2[0] = __floats2half2_rn(o0, o1);
+  h2[1] = __floats2half2_rn(o2, 0.f);
+  v.z = 0u;
+  v.w = 0u;
+  *reinterpret_cast<uint4*>(px) = v;
 }
 
 // R output rows per tile, N output channels (MMA N), S pipeline stages; BRES: the whole weight
@@ -459,12 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
             const int64_t pix = (int64_t)y * a.W + xo;
 #pragma unroll
             for (int c = 0; c < 3; ++c) a.od[c * hw + pix] = od[c];
-            if (a.feedback) {
-              __half* fb = a.feedback + pix * 8;
-              fb[5] = __float2half(od[0]);
-              fb[6] = __float2half(od[1]);
-              fb[7] = __float2half(od[2]);
-            }
+            if (a.feedback) feedback_store(a.feedback + pix * 8, od[0], od[1], od[2]);
           }
         }
         sm100::named_bar_sync(2 + half, 128);  // the slots are rewritten by the next tile
@@ -495,12 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
                 o[c] = v[c] + s_bias[c];
                 a.od[c * hw + pix] = o[c];
               }
-              if (a.feedback) {
-                __half* fb = a.feedback + pix * 8;
-                fb[5] = __float2half(o[0]);
-                fb[6] = __float2half(o[1]);
-                fb[7] = __float2half(o[2]);
-              }
+              if (a.feedback) feedback_store(a.feedback + pix * 8, o[0], o[1], o[2]);
             }
             if constexpr (N >= 32) {
 #pragma unroll

@@ -194,6 +194,7 @@ struct fv_volume {
   cudaArray_t larr = nullptr;
   unsigned long long ltex = 0;
   uint64_t ltex_version = 0;
+  int ltex_bits = 0;  // texel format of larr: 16 (unorm16, voxels in [0, 1]) or 32 (float)
   int K = 0;
   double value_range[2] = {0, 0};
 };
@@ -267,6 +268,14 @@ struct fv_act {
   int C = 0, H = 0, W = 0;
   int64_t plane() const { return (int64_t)H * W * 8; }
 };
+
+// The network input x (NC8HW8, two channel groups): group 0 = [r*m, g*m, b*m, a*m, m, 0, 0, 0]
+// (written whole by the mask, the march's records fill channels 0..3 of active pixels), group 1 =
+// [O_d feedback (3), 0 x 5] (written whole by the K-stage level-0 conv of the previous frame).
+// Separate groups keep every writer's stores full 16-byte pixels with no shared bytes, so the
+// next frame's mask and this frame's D.head can run concurrently on one buffer.
+constexpr int kInGroups = 2;
+inline __half* feedback_plane(const fv_act& x) { return x.p + x.plane(); }
 
 struct fv_state {
   const fv_net* net = nullptr;

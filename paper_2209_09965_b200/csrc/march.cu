@@ -1531,19 +1531,72 @@ int volume_texture(fv_ctx* ctx, fv_volume* vol) {
 // frac(q) quantised to 8 fractional bits (the SURVEY's fast tier) -- the reference's
 // sample_trilinear (volume.py:149-180) except in the half-voxel shell q < 0, where the reference
 // keeps i0 = 0, i1 = 1 and t = q + 1; the caller maps q -> q + 1 there (same texels and weight).
+// unorm16 texels of voxels in [0, 1] (round to nearest; *oob set when any voxel lies outside)
+__global__ void unorm16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n, int* oob) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = in[i];
+    if (!(v >= 0.f && v <= 1.f)) *oob = 1;
+    out[i] = (uint16_t)__float2uint_rn(__saturatef(v) * 65535.f);
+  }
+}
+
 int volume_ltex(fv_ctx* ctx, fv_volume* vol) {
   if (vol->ltex && vol->ltex_version == vol->version) return 0;
+  // Texel format (FV_LTEX_BITS, default 16): 16-bit texels filter at the texture unit's full rate
+  // (32-bit float texels at half rate); unorm16 holds a voxel in [0, 1] to 7.6e-6, far below the
+  // 8-bit fractional filter weights' 1/256. A volume with any voxel outside [0, 1] (the shadow
+  // pass clamps AFTER interpolation) keeps float texels.
+  static const int bits_env = getenv("FV_LTEX_BITS") ? atoi(getenv("FV_LTEX_BITS")) : 16;
+  const int64_t n = (int64_t)vol->nx * vol->ny * vol->nz;
+  const cudaExtent ext = make_cudaExtent(vol->nx, vol->ny, vol->nz);
+  int bits = 32;
+  uint16_t* u16 = nullptr;
+  if (bits_env == 16) {
+    int* oob = nullptr;
+    FV_CUDA(cudaMalloc(&u16, (size_t)n * sizeof(uint16_t) + 16));
+    oob = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(u16) + (((size_t)n * sizeof(uint16_t) + 7) & ~size_t(7)));
+    FV_CUDA(cudaMemsetAsync(oob, 0, sizeof(int), ctx->stream));
+    unorm16_kernel<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(vol->data, u16, n, oob);
+    FV_CHECK_LAUNCH("unorm16_kernel");
+    int h_oob = 1;
+    FV_CUDA(cudaMemcpyAsync(&h_oob, oob, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    FV_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!h_oob) bits = 16;
+  }
+  if (vol->larr && vol->ltex_bits != bits) {
+    if (vol->ltex) cudaDestroyTextureObject((cudaTextureObject_t)vol->ltex);
+    cudaFreeArray(vol->larr);
+    vol->ltex = 0;
+    vol->larr = nullptr;
+  }
+  int rc = 0;
   if (!vol->larr) {
-    const cudaChannelFormatDesc fd = cudaCreateChannelDesc<float>();
-    FV_CUDA(cudaMalloc3DArray(&vol->larr, &fd, make_cudaExtent(vol->nx, vol->ny, vol->nz)));
+    const cudaChannelFormatDesc fd =
+        bits == 16 ? cudaCreateChannelDesc<unsigned short>() : cudaCreateChannelDesc<float>();
+    const cudaError_t e = cudaMalloc3DArray(&vol->larr, &fd, ext);
+    if (e != cudaSuccess) {
+      vol->larr = nullptr;
+      cudaFree(u16);
+      set_error("cudaMalloc3DArray: %s", cudaGetErrorString(e));
+      return FV_E_CUDA;
+    }
+    vol->ltex_bits = bits;
   }
   cudaMemcpy3DParms cp{};
-  cp.srcPtr = make_cudaPitchedPtr(vol->data, (size_t)vol->nx * sizeof(float), vol->nx, vol->ny);
+  if (bits == 16)
+    cp.srcPtr = make_cudaPitchedPtr(u16, (size_t)vol->nx * sizeof(uint16_t), vol->nx, vol->ny);
+  else
+    cp.srcPtr = make_cudaPitchedPtr(vol->data, (size_t)vol->nx * sizeof(float), vol->nx, vol->ny);
   cp.dstArray = vol->larr;
-  cp.extent = make_cudaExtent(vol->nx, vol->ny, vol->nz);
+  cp.extent = ext;
   cp.kind = cudaMemcpyDeviceToDevice;
-  FV_CUDA(cudaMemcpy3DAsync(&cp, ctx->stream));
-  FV_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaError_t e = cudaMemcpy3DAsync(&cp, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(u16);
+  if (e != cudaSuccess) {
+    set_error("volume texture copy: %s", cudaGetErrorString(e));
+    return FV_E_CUDA;
+  }
   if (!vol->ltex) {
     cudaResourceDesc rd{};
     rd.resType = cudaResourceTypeArray;
@@ -1551,14 +1604,14 @@ int volume_ltex(fv_ctx* ctx, fv_volume* vol) {
     cudaTextureDesc td{};
     td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
     td.filterMode = cudaFilterModeLinear;
-    td.readMode = cudaReadModeElementType;
+    td.readMode = bits == 16 ? cudaReadModeNormalizedFloat : cudaReadModeElementType;
     td.normalizedCoords = 0;
     cudaTextureObject_t t = 0;
     FV_CUDA(cudaCreateTextureObject(&t, &rd, &td, nullptr));
     vol->ltex = (unsigned long long)t;
   }
   vol->ltex_version = vol->version;
-  return 0;
+  return rc;
 }
 
 int volume_bricks(fv_ctx* ctx, fv_volume* vol) {

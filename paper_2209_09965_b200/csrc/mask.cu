@@ -90,17 +90,30 @@ __global__ void __launch_bounds__(kThreads) mask_compact_kernel(MaskParams p_in)
       const bool m = n < tau_at(p, u, v);
       bits |= (unsigned)m << j;
       if (p.bits) p.bits[pix] = (uint8_t)m;
-      if (p.net_in) {
-        __half* px = p.net_in + ((int64_t)v * p.net_wp + u) * 8;
-        if (!m) *reinterpret_cast<uint2*>(px) = make_uint2(0u, 0u);
-        px[4] = m ? __float2half(1.0f) : __float2half(0.0f);
-      }
     }
     if (++u == p.W) { u = 0; ++v; }
   }
   const unsigned int cnt = __popc(bits);
-  // block-wide exclusive scan of cnt
   const int lane = tid & 31, warp = tid >> 5;
+  // the network input's group 0 ([0 x 4, m, 0 x 3]: the march's records fill channels 0..3 of the
+  // active pixels afterwards), whole 16-byte pixels, warp-coalesced: lane l writes pixel
+  // wbase + 32 j + l, whose bit lane (32 j + l) / 8 holds
+  if (p.net_in) {
+    const int64_t wbase = (int64_t)tile * kTile + (int64_t)warp * 32 * kPerThread;
+#pragma unroll
+    for (int j = 0; j < kPerThread; ++j) {
+      const int q = 32 * j + lane;
+      const unsigned b = __shfl_sync(0xffffffffu, bits, q >> 3);
+      const int64_t pix = wbase + q;
+      if (pix < npix) {
+        const unsigned vv = (unsigned)pix / (unsigned)p.W, uu = (unsigned)pix - vv * (unsigned)p.W;
+        const bool m = (b >> (q & 7)) & 1u;
+        *reinterpret_cast<uint4*>(p.net_in + ((int64_t)vv * p.net_wp + uu) * 8) =
+            make_uint4(0u, 0u, m ? 0x3c00u : 0u, 0u);  // 0x3c00: fp16 1.0 in channel 4
+      }
+    }
+  }
+  // block-wide exclusive scan of cnt
   unsigned int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {

@@ -258,7 +258,7 @@ int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, floa
                  nullptr);
     if (rc) return rc;
   }
-  return kstage_launches(ctx, net, st, newp, st->od, net->recurrent ? st->xalt.p : nullptr, use_k, nullptr,
+  return kstage_launches(ctx, net, st, newp, st->od, net->recurrent ? feedback_plane(st->xalt) : nullptr, use_k, nullptr,
                          out_rgb, out_o, out_od);
 }
 
@@ -395,7 +395,8 @@ int fv_net_create(fv_ctx* ctx, const char* blocks, int predicted_kernel, int rec
   std::vector<int> d_ch(ch.begin() + ne, ch.end());
   // _conv_channels (network.py:128-149)
   std::vector<std::pair<int, int>> io;
-  for (int i = 0; i < ne; ++i) io.push_back({i == 0 ? 8 : ch[i - 1], ch[i]});  // block0 input padded to 8 slots
+  // block0 input: 16 slots in two channel groups [rgba, m, 0 x 3 | prev(3), 0 x 5] (internal.h)
+  for (int i = 0; i < ne; ++i) io.push_back({i == 0 ? 8 * kInGroups : ch[i - 1], ch[i]});
   for (int j = 0; j < nd; ++j) {
     int inc = j == 0 ? ch[ne - 1] : d_ch[j - 1] + ch[ne - j];
     if (net->recurrent) inc += d_ch[j];
@@ -408,6 +409,8 @@ int fv_net_create(fv_ctx* ctx, const char* blocks, int predicted_kernel, int rec
       cp.cin = c == 1 ? io[i].first : io[i].second;
       cp.cout = io[i].second;
       cp.n_pad = (cp.cout + 15) / 16 * 16;
+      // algorithmic MACs of block0.conv1: the reference's in_channels, not the padded slots
+      if (i == 0 && c == 1) cp.macs_per_px = (double)net->in_channels * cp.cout * 9;
       net->convs.push_back(cp);
     }
   }
@@ -458,7 +461,7 @@ int fv_net_set_param(fv_ctx* ctx, fv_net* net, const char* name, const float* ho
   FV_REQUIRE(idx >= 0, "checkpoint parameter '%s' not in network", name);
   ConvParam& cp = net->convs[idx];
   const int ks = cp.ksize;
-  // reference cin of block0.conv1 is in_channels; device layout uses 8 slots [rgba, m, prev]
+  // reference cin of block0.conv1 is in_channels; device layout uses 16 slots [rgba, m, 0 x 3 | prev, 0 x 5]
   const bool first = base == "D.block0.conv1";
   const int ref_cin = first ? net->in_channels : cp.cin;
   const int64_t expect = is_w ? (int64_t)cp.cout * ref_cin * ks * ks : cp.cout;
@@ -475,7 +478,7 @@ int fv_net_set_param(fv_ctx* ctx, fv_net* net, const char* name, const float* ho
           // reference order: rgba(4), [mask], [prev(3)]
           if (c < 4) slot = c;
           else if (net->include_mask && c == 4) slot = 4;
-          else slot = 5 + (c - 4 - (net->include_mask ? 1 : 0));
+          else slot = 8 + (c - 4 - (net->include_mask ? 1 : 0));
         }
         for (int t = 0; t < ks * ks; ++t)
           cp.w_host[((size_t)o * cp.cin + slot) * ks * ks + t] =
@@ -511,8 +514,8 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
   std::vector<Req> reqs;
   st->enc_a.resize(ne); st->skips.resize(ne); st->pooled.resize(ne);
   st->dec_a.resize(nd); st->ups.resize(nd); st->hidden[0].resize(nd); st->hidden[1].resize(nd);
-  reqs.push_back({&st->x, 8, 0});
-  reqs.push_back({&st->xalt, 8, 0});
+  reqs.push_back({&st->x, 8 * kInGroups, 0});
+  reqs.push_back({&st->xalt, 8 * kInGroups, 0});
   for (int i = 0; i < ne; ++i) {
     reqs.push_back({&st->enc_a[i], ch[i], i});
     reqs.push_back({&st->skips[i], ch[i], i});

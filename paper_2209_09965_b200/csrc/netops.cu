@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(128) kchain_kernel(KChain ch) {
   }
 }
 
-// x = rgba*m ++ m into channels 0..4 of the NHWC8 input (film region only)
+// x = rgba*m ++ m: group 0 of the input (channels 0..4, film region only; internal.h kInGroups)
 __global__ void pack_input_kernel(const float* __restrict__ rgba, const uint8_t* __restrict__ bits,
                                   __half* __restrict__ x, int H, int W, int Wp) {
   const int64_t n = (int64_t)H * W;
@@ -370,23 +370,28 @@ __global__ void pack_input_kernel(const float* __restrict__ rgba, const uint8_t*
     const int u = (int)(i % W), v = (int)(i / W);
     const float m = bits[i] ? 1.f : 0.f;
     const float4 c = *reinterpret_cast<const float4*>(rgba + i * 4);
-    __half* px = x + ((int64_t)v * Wp + u) * 8;
-    __half2* p2 = reinterpret_cast<__half2*>(px);
+    uint4 q;
+    __half2* p2 = reinterpret_cast<__half2*>(&q);
     p2[0] = __floats2half2_rn(c.x * m, c.y * m);
     p2[1] = __floats2half2_rn(c.z * m, c.w * m);
-    px[4] = __float2half(m);
+    p2[2] = __floats2half2_rn(m, 0.f);
+    p2[3] = __floats2half2_rn(0.f, 0.f);
+    *reinterpret_cast<uint4*>(x + ((int64_t)v * Wp + u) * 8) = q;  // the whole group-0 pixel
   }
 }
 
-// forward_full input: NCHW (C,H,W) fp32 -> channels 0..C-1 of the NHWC8 input (C = 4 or 5)
+// forward_full input: NCHW (C,H,W) fp32 -> channels 0..C-1 of the input's group 0 (C = 4 or 5)
 __global__ void set_input_kernel(const float* __restrict__ xin, int C, __half* __restrict__ x, int H,
                                  int W, int Wp) {
   const int64_t n = (int64_t)H * W;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int u = (int)(i % W), v = (int)(i / W);
-    __half* px = x + ((int64_t)v * Wp + u) * 8;
-    for (int c = 0; c < 5; ++c) px[c] = __float2half_rn(c < C ? xin[c * n + i] : 0.f);
+    uint4 q;
+    __half* h = reinterpret_cast<__half*>(&q);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) h[c] = __float2half_rn(c < C && c < 5 ? xin[c * n + i] : 0.f);
+    *reinterpret_cast<uint4*>(x + ((int64_t)v * Wp + u) * 8) = q;
   }
 }
 
@@ -435,13 +440,17 @@ __global__ void nchw_to_nc8_kernel(const float* __restrict__ in, __half* __restr
   }
 }
 
-// O_d (3,H,W) fp32 -> feedback channels 5..7 of the NHWC8 input
-__global__ void od_to_feedback_kernel(const float* __restrict__ od, __half* __restrict__ x, int h, int w) {
+// O_d (3,H,W) fp32 -> the input's feedback group [O_d, 0 x 5] (fb = its base)
+__global__ void od_to_feedback_kernel(const float* __restrict__ od, __half* __restrict__ fb, int h, int w) {
   const int64_t n = (int64_t)h * w;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) x[i * 8 + 5 + c] = __float2half_rn(od[c * n + i]);
+    uint4 q;
+    __half2* p2 = reinterpret_cast<__half2*>(&q);
+    p2[0] = __floats2half2_rn(od[i], od[n + i]);
+    p2[1] = __floats2half2_rn(od[2 * n + i], 0.f);
+    q.z = q.w = 0u;
+    *reinterpret_cast<uint4*>(fb + i * 8) = q;
   }
 }
 
@@ -649,7 +658,7 @@ int kfield_logits(fv_ctx* ctx, const float* w_host, const float* b_host, const f
 
 int od_to_feedback(fv_ctx* ctx, fv_state* st) {
   const int64_t n = (int64_t)st->Hp * st->Wp;
-  FV_TIMED(ctx, FV_KC_NETOPS, od_to_feedback_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(st->od, st->x.p, st->Hp, st->Wp));
+  FV_TIMED(ctx, FV_KC_NETOPS, od_to_feedback_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(st->od, feedback_plane(st->x), st->Hp, st->Wp));
   FV_CHECK_LAUNCH("od_to_feedback_kernel");
   ctx->launches += 1;
   return 0;

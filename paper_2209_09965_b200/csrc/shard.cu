@@ -117,22 +117,23 @@ __global__ void window_input_kernel(const uint8_t* __restrict__ bits, int H_full
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int u = (int)(i % W), y = (int)(i / W), v = row0 + y;
     const bool m = v < H_full && bits[(int64_t)v * W + u];
-    __half* px = net_in + ((int64_t)y * net_wp + u) * 8;
-    *reinterpret_cast<uint2*>(px) = make_uint2(0u, 0u);
-    px[4] = m ? __float2half(1.0f) : __float2half(0.0f);
+    // the whole group-0 pixel [0 x 4, m, 0 x 3] (the records fill channels 0..3 afterwards)
+    *reinterpret_cast<uint4*>(net_in + ((int64_t)y * net_wp + u) * 8) = make_uint4(0u, 0u, m ? 0x3c00u : 0u, 0u);
   }
 }
 
-// x channels 5..7 (the O_d feedback) of rows [r0, r0 + rows) from the fp32 O_d planes
-__global__ void feedback_rows_kernel(const float* __restrict__ od, __half* __restrict__ x, int Hp, int Wp, int r0,
+// the input's feedback group (fb = its base: [O_d, 0 x 5]) for rows [r0, r0 + rows) from the fp32 O_d planes
+__global__ void feedback_rows_kernel(const float* __restrict__ od, __half* __restrict__ fb, int Hp, int Wp, int r0,
                                      int rows) {
   const int64_t n = (int64_t)rows * Wp, plane = (int64_t)Hp * Wp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pix = (int64_t)r0 * Wp + i;
-    __half* px = x + pix * 8;
-    px[5] = __float2half(od[pix]);
-    px[6] = __float2half(od[plane + pix]);
-    px[7] = __float2half(od[2 * plane + pix]);
+    uint4 q;
+    __half2* p2 = reinterpret_cast<__half2*>(&q);
+    p2[0] = __floats2half2_rn(od[pix], od[plane + pix]);
+    p2[1] = __floats2half2_rn(od[2 * plane + pix], 0.f);
+    q.z = q.w = 0u;
+    *reinterpret_cast<uint4*>(fb + pix * 8) = q;
   }
 }
 
@@ -259,7 +260,7 @@ int fv_state_band(fv_ctx* ctx, fv_state* st, int pack, int row0, int rows, void*
   }
   if (b && !pack && rows && net->recurrent) {
     FV_TIMED(ctx, FV_KC_NETOPS, feedback_rows_kernel<<<grid_of(ctx, (int64_t)rows * st->Wp), 256, 0, ctx->stream>>>(
-                                    st->od, st->x.p, st->Hp, st->Wp, row0, rows));
+                                    st->od, feedback_plane(st->x), st->Hp, st->Wp, row0, rows));
     FV_CHECK_LAUNCH("feedback_rows_kernel");
     ctx->launches += 1;
   }
