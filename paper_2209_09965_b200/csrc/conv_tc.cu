@@ -57,6 +57,9 @@ struct ConvArgs {
   __half* feedback;    // head: the next input's feedback group (internal.h kInGroups), nullable
   kw_t* kw[2];         // K-stage filter weights (9, H, W) per K block (nullable)
   int kcol[2];         // first logit column of each K block
+  const __half* lw;    // LG: the K-stage logits' 1x1 weight image [cout/8][32][8] fp16 (columns 9 s + j)
+  const float* lb;     // LG: their bias (32)
+  int lg;              // LG: K blocks at this level (1 or 2)
   int center_only;     // 1x1 conv: only the centre tap's MMAs are issued
   int tiles_x, tiles_y;
   double flops;        // host-side: algorithmic FLOPs of the launch (kernel timing)
@@ -93,7 +96,7 @@ __device__ __forceinline__ void feedback_store(__half* px, float o0, float o1, f
 // R output rows per tile, N output channels (MMA N), S pipeline stages; BRES: the whole weight
 // image (<= kBResStages stages, i.e. cin <= 64) is loaded once per CTA and stays in smem, so
 // only activations stream (the weights were ~40% of the L2->SM bytes of a 64->64 conv).
-template <int R, int N, int S = 2, bool BRES = false, bool TAPN = false>
+template <int R, int N, int S = 2, bool BRES = false, bool TAPN = false, bool LG = false>
 struct Cfg {
   static constexpr int kABytes = kStageGroups * (R + 2) * kRowBytes;
   static constexpr int kBBytes = 9 * kStageGroups * N * 16;
@@ -104,7 +107,13 @@ struct Cfg {
   static constexpr int kBSlots = BRES ? kBResStages : S;
   static constexpr int kBiasBytes = N * 4;  // the epilogue's bias copy
   static constexpr int kXchgBytes = TAPN ? 512 : 0;  // TAPN: cross-quarter partial sums
-  static constexpr int kSmem = S * kABytes + kBSlots * kBBytes + 1024 + 256 + kBiasBytes + kXchgBytes;
+  // LG: the tile's output rows staged as the logits GEMM's A operand ([row][g][128 px][8] fp16) and
+  // the logits' weight image, plus their bias
+  static constexpr int kStgBytes = LG ? R * N * 256 : 0;
+  static constexpr int kLWBytes = LG ? (N / 8) * 512 : 0;
+  static constexpr int kLBiasBytes = LG ? 128 : 0;
+  static constexpr int kSmem = S * kABytes + kBSlots * kBBytes + kStgBytes + kLWBytes + 1024 + 256 + kBiasBytes +
+                               kXchgBytes + kLBiasBytes;
 };
 
 // TAPN (the K-stage level-0 conv): the nine 3x3 taps of D.head sit in N next to the two K blocks'
@@ -184,26 +193,33 @@ __device__ __forceinline__ void issue_stage_rows(uint64_t a0, uint64_t b0, uint3
   }
 }
 
-template <int R, int N, int kStages, bool BRES, bool FUSED, bool CO = false, bool TAPN = false>
+template <int R, int N, int kStages, bool BRES, bool FUSED, bool CO = false, bool TAPN = false, bool LG = false>
 __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
-  using C = Cfg<R, N, kStages, BRES, TAPN>;
+  using C = Cfg<R, N, kStages, BRES, TAPN, LG>;
   constexpr int kStride = TAPN ? kTapnStride : kTileW;  // columns a tile advances by
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * C::kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + C::kBSlots * C::kBBytes);
-  // bars: full[kStages], empty[kStages], tfull[2], tempty[2], weights-resident, row-pair free[R/2]
+  uint8_t* sStg = sB + C::kBSlots * C::kBBytes;  // LG: staged output rows
+  uint8_t* sLW = sStg + C::kStgBytes;            // LG: logits weight image
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sLW + C::kLWBytes);
+  // bars: full[kStages], empty[kStages], tfull[2], tempty[2], weights-resident, row-pair free[R/2],
+  // LG: logits-done[R/2]
   constexpr bool kPairs = C::kAcc == 1 && FUSED;  // single accumulator: release it row pair by row pair
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5 + (kPairs ? R / 2 : 0));
+  static_assert(!(LG && (kPairs || TAPN || C::kAcc != 2)), "LG: double-buffered plain accumulators");
+  uint32_t* tmem_slot =
+      reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5 + (kPairs ? R / 2 : 0) + (LG ? R / 2 : 0));
   float* s_bias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // N floats
   float* s_xchg = s_bias + N;  // TAPN: [half][quarter][left 3 | right 3]
+  float* s_lbias = s_bias + N;  // LG: the logits' bias (32)
   const uint32_t bar_full = sm100::smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * kStages;
   const uint32_t bar_tfull = bar_empty + 8 * kStages;
   const uint32_t bar_tempty = bar_tfull + 16;
   const uint32_t bar_bres = bar_tempty + 16;
   const uint32_t bar_pair = bar_bres + 8;
+  const uint32_t bar_lfull = bar_pair + 8 * (kPairs ? R / 2 : 0);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -220,12 +236,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     sm100::mbar_init(bar_bres, 1);
     if (kPairs)
       for (int p = 0; p < R / 2; ++p) sm100::mbar_init(bar_pair + 8 * p, kEpiWarps);
+    if (LG)
+      for (int p = 0; p < R / 2; ++p) sm100::mbar_init(bar_lfull + 8 * p, 1);
     sm100::fence_mbar_init();
-    if (BRES) {
-      // resident weights: constant for the whole graph, so copied before the dependency wait
-      const uint32_t wb = (uint32_t)(a.n_kstages * C::kBBytes);
-      sm100::mbar_arrive_expect_tx(bar_bres, wb);
-      sm100::bulk_g2s(sm100::smem_u32(sB), a.wimg, wb, bar_bres);
+    if (BRES || LG) {
+      // resident weights (and the logits' weights): constant for the whole graph, so copied before
+      // the dependency wait
+      const uint32_t wb = BRES ? (uint32_t)(a.n_kstages * C::kBBytes) : 0u;
+      sm100::mbar_arrive_expect_tx(bar_bres, wb + (uint32_t)C::kLWBytes);
+      if (BRES) sm100::bulk_g2s(sm100::smem_u32(sB), a.wimg, wb, bar_bres);
+      if (LG) sm100::bulk_g2s(sm100::smem_u32(sLW), a.lw, (uint32_t)C::kLWBytes, bar_bres);
     }
   }
   if (warp == 1) sm100::tmem_alloc<512>(sm100::smem_u32(tmem_slot));
@@ -363,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
     // ---------------- epilogue ----------------
     // bias once per CTA into smem (broadcast reads, off the per-item dependency chain)
     for (int i = threadIdx.x - 64; i < N; i += kEpiWarps * 32) s_bias[i] = __ldg(a.bias + i);
+    if (LG && threadIdx.x - 64 < 32) s_lbias[threadIdx.x - 64] = __ldg(a.lb + threadIdx.x - 64);
     sm100::named_bar_sync(1, kEpiWarps * 32);
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int half = (warp - 2) >> 2;  // the two warps of a quarter split the tile's rows/columns
@@ -524,6 +545,110 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
 #pragma unroll
                 for (int j = 0; j < 9; ++j) a.kw[s][j * hw + pix] = l[j] * inv;
               }
+            }
+          }
+        }
+      } else if constexpr (LG) {
+        // Decoder conv2 with the K stage's logits fused (network.py:268-277): per row pair, the
+        // output rows go to HBM (the hidden state) AND, as fp16, to the staged A operand; then one
+        // elected epilogue thread runs the 1x1 logits GEMM (128 x 32 x cout) into the drained
+        // accumulator columns of those rows, and after the last row pair the epilogue turns them
+        // into the softmax filter weights (the separate level-L logits conv of the K stage).
+        constexpr int kCb = N / 16;
+        const int m = 32 * q + lane;  // TMEM lane = pixel of the tile
+#pragma unroll 1
+        for (int p = 0; p < R / 2; ++p) {
+          const int r = 2 * p;
+          const int y = y0 + r;
+#pragma unroll 1
+          for (int item = p * kCb + half; item < (p + 1) * kCb; item += 2) {
+            const int cb = 16 * (item - p * kCb);
+            float v0[16], v1[16];
+            {
+              uint32_t r0[16], r1[16];
+              sm100::tmem_ld16_nowait(t_row0 + (R - 1 - r) * N + cb, r0);
+              sm100::tmem_ld16_nowait(t_row0 + (R - 2 - r) * N + cb, r1);
+              sm100::tmem_wait_ld_regs(r0, r1);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) { v0[j] = __uint_as_float(r0[j]); v1[j] = __uint_as_float(r1[j]); }
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float b = s_bias[cb + j];
+              v0[j] += b;
+              v1[j] += b;
+              if (a.relu) { v0[j] = fmaxf(v0[j], 0.f); v1[j] = fmaxf(v1[j], 0.f); }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int g = (cb >> 3) + h;
+              uint4 pk0, pk1;
+              __half2* p0 = reinterpret_cast<__half2*>(&pk0);
+              __half2* p1 = reinterpret_cast<__half2*>(&pk1);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                p0[j] = __floats2half2_rn(v0[8 * h + 2 * j], v0[8 * h + 2 * j + 1]);
+                p1[j] = __floats2half2_rn(v1[8 * h + 2 * j], v1[8 * h + 2 * j + 1]);
+              }
+              *reinterpret_cast<uint4*>(sStg + (((int64_t)r * (N / 8) + g) * 128 + m) * 16) = pk0;
+              *reinterpret_cast<uint4*>(sStg + (((int64_t)(r + 1) * (N / 8) + g) * 128 + m) * 16) = pk1;
+              if (xin && 8 * g < a.cout) {
+                if (y < a.H) *reinterpret_cast<uint4*>(a.dst + g * plane + ((int64_t)y * a.W + x) * 8) = pk0;
+                if (y + 1 < a.H) *reinterpret_cast<uint4*>(a.dst + g * plane + ((int64_t)(y + 1) * a.W + x) * 8) = pk1;
+              }
+            }
+          }
+          // rows r, r + 1 staged and their accumulator columns read: the logits GEMM may overwrite them
+          sm100::fence_proxy_async_smem();
+          sm100::tc_fence_before();
+          sm100::named_bar_sync(1, kEpiWarps * 32);
+          if (threadIdx.x == 64) {
+            if (lt == 0 && p == 0) sm100::mbar_wait(bar_bres, 0);  // the logits' weight image
+            sm100::tc_fence_after();
+            constexpr uint32_t lidesc = sm100::idesc_f16(128, 32);
+#pragma unroll
+            for (int rr = r; rr < r + 2; ++rr)
+#pragma unroll
+              for (int k = 0; k < N / 16; ++k) {
+                const uint64_t ad = sm100::smem_desc(sm100::smem_u32(sStg + (rr * (N / 8) + 2 * k) * 2048), 2048, 128);
+                const uint64_t bd = sm100::smem_desc(sm100::smem_u32(sLW + 2 * k * 512), 512, 128);
+                sm100::mma_f16(tmem_base + acc * C::kAccCols + (R - 1 - rr) * N, ad, bd, lidesc, k ? 1u : 0u);
+              }
+            sm100::mma_commit(bar_lfull + 8 * p);
+          }
+        }
+        const int64_t hw = (int64_t)a.H * a.W;
+#pragma unroll 1
+        for (int p = 0; p < R / 2; ++p) {
+          sm100::mbar_wait(bar_lfull + 8 * p, lt & 1);  // completes once per tile
+          sm100::tc_fence_after();
+          const int rr = 2 * p + half;
+          uint32_t u0[16], u1[16];
+          sm100::tmem_ld16_nowait(t_row0 + (R - 1 - rr) * N, u0);
+          sm100::tmem_ld16_nowait(t_row0 + (R - 1 - rr) * N + 16, u1);
+          sm100::tmem_wait_ld_regs(u0, u1);
+          const int y = y0 + rr;
+          if (xin && y < a.H) {
+            const int64_t pix = (int64_t)y * a.W + x;
+#pragma unroll
+            for (int s_ = 0; s_ < 2; ++s_) {
+              if (s_ >= a.lg) break;
+              float l[9], mx = -INFINITY;
+#pragma unroll
+              for (int j = 0; j < 9; ++j) {
+                const int c = 9 * s_ + j;
+                l[j] = __uint_as_float(c < 16 ? u0[c] : u1[c - 16]) + s_lbias[c];
+                mx = fmaxf(mx, l[j]);
+              }
+              float sum = 0.f;
+#pragma unroll
+              for (int j = 0; j < 9; ++j) {
+                l[j] = __expf(l[j] - mx);  // arguments <= 0: ex2.approx, rel. error ~1e-7
+                sum += l[j];
+              }
+              const float inv = __frcp_rn(sum);
+#pragma unroll
+              for (int j = 0; j < 9; ++j) a.kw[s_][j * hw + pix] = l[j] * inv;
             }
           }
         }
@@ -1000,14 +1125,14 @@ int launch_pair(fv_ctx* ctx, const ConvArgs& args) {
   return 0;
 }
 
-template <int R, int N, int S, bool BRES, bool FUSED, bool CO = false, bool TAPN = false>
+template <int R, int N, int S, bool BRES, bool FUSED, bool CO = false, bool TAPN = false, bool LG = false>
 int launch(fv_ctx* ctx, const ConvArgs& args) {
-  using C = Cfg<R, N, S, BRES, TAPN>;
+  using C = Cfg<R, N, S, BRES, TAPN, LG>;
   static_assert(C::kSmem <= 227 * 1024, "conv tile configuration exceeds shared memory");
   static_assert(!TAPN || (R == 4 && N >= 48 && !FUSED && !CO), "TAPN: 4-row tiles, 48 columns, plain issue");
   static bool attr_set = false;
   if (!attr_set) {
-    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN>,
+    FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN, LG>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
@@ -1018,7 +1143,7 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   const int n_tiles = a.tiles_x * a.tiles_y;
   const int grid = n_tiles < ctx->num_sms ? n_tiles : ctx->num_sms;
   ktime_begin(ctx);
-  fv::launch_pdl(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN>, grid, kThreads, C::kSmem, ctx->stream, a);
+  fv::launch_pdl(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN, LG>, grid, kThreads, C::kSmem, ctx->stream, a);
   ktime_end(ctx, FV_KC_CONV, a.flops);
   if (ctx->conv_fork_ev && ++ctx->conv_count == ctx->conv_fork_at)
     FV_CUDA(cudaEventRecord(ctx->conv_fork_ev, ctx->stream));
@@ -1135,6 +1260,36 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
   return 0;
 }
 
+// Whether conv3x3 has a fused-logits (LG) variant for this conv's shape (see its dispatch)
+bool logits_fusable(const ConvParam& cp) {
+  const bool res = cp.n_stages <= kBResStages;
+  return (cp.n_pad == 64 && res && cp.row_fused) || (cp.n_pad == 80 && !res && cp.row_fused) ||
+         (cp.n_pad == 96 && !res && !cp.row_fused);
+}
+
+// The K stage's level logits as the LG epilogue's 1x1 GEMM B operand: w_host (cout = 9 x blocks,
+// cin) row-major -> [cin/8][32][8] fp16 (K-major, LBO 512 B, SBO 128 B), bias padded to 32.
+int logits_prepare(fv_ctx* ctx, ConvParam& cp) {
+  FV_REQUIRE(cp.cin % 8 == 0 && cp.cout <= 32, "logits %s: cin %d / cout %d", cp.name.c_str(), cp.cin, cp.cout);
+  cp.wbytes = (int64_t)(cp.cin / 8) * 512;
+  std::vector<__half> img(cp.wbytes / 2, __float2half(0.f));
+  for (int o = 0; o < cp.cout; ++o)
+    for (int c = 0; c < cp.cin; ++c)
+      img[((size_t)(c / 8) * 32 + o) * 8 + (c % 8)] = __float2half(cp.w_host[(size_t)o * cp.cin + c]);
+  if (cp.w_dev) cudaFree(cp.w_dev);
+  if (cp.b_dev) cudaFree(cp.b_dev);
+  cp.w_dev = nullptr;
+  cp.b_dev = nullptr;
+  FV_CUDA(cudaMalloc(&cp.w_dev, cp.wbytes));
+  FV_CUDA(cudaMemcpy(cp.w_dev, img.data(), cp.wbytes, cudaMemcpyHostToDevice));
+  std::vector<float> b(32, 0.f);
+  for (int n = 0; n < cp.cout; ++n) b[n] = cp.b_host[n];
+  FV_CUDA(cudaMalloc(&cp.b_dev, sizeof(float) * 32));
+  FV_CUDA(cudaMemcpy(cp.b_dev, b.data(), sizeof(float) * 32, cudaMemcpyHostToDevice));
+  (void)ctx;
+  return 0;
+}
+
 // Public-internal entry: run one 3x3 conv. srcs: up to 3 NC8HW8 tensors at the same level.
 int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_act* dst,
             fv_act* pool_dst, bool relu, const ConvAux* aux) {
@@ -1167,6 +1322,32 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   }
   a.flops = 2.0 * a.H * a.W *
             (cp.macs_per_px > 0 ? cp.macs_per_px : (double)cp.cin * cp.cout * cp.ksize * cp.ksize);
+  if (aux && aux->logits) {
+    // decoder conv2 with the K stage's level logits fused into its epilogue (LG)
+    const ConvParam& lp = *aux->logits;
+    FV_REQUIRE(!pool_dst && dst && lp.w_dev && lp.cin == cp.cout && (aux->kw[0] || aux->kw[1]),
+               "conv %s: fused logits need a plain output and the level's weight planes", cp.name.c_str());
+    a.lw = lp.w_dev;
+    a.lb = lp.b_dev;
+    a.lg = aux->kw[1] ? 2 : 1;
+    a.kw[0] = aux->kw[0];
+    a.kw[1] = aux->kw[1];
+    a.flops += 2.0 * a.H * a.W * (double)lp.cin * 9 * a.lg;
+    const bool res = cp.n_stages <= kBResStages;
+    switch (cp.n_pad) {
+      case 64:
+        if (res && cp.row_fused) return launch<4, 64, 3, true, true, false, false, true>(ctx, a);
+        break;
+      case 80:
+        if (!res && cp.row_fused) return launch<2, 80, 4, false, true, false, false, true>(ctx, a);
+        break;
+      case 96:
+        if (!res && !cp.row_fused) return launch<2, 96, 3, false, false, false, false, true>(ctx, a);
+        break;
+    }
+    set_error("conv %s: no fused-logits variant for %d columns", cp.name.c_str(), cp.n_pad);
+    return FV_E_UNSUPPORTED;
+  }
   if (aux) {
     a.head = 1;
     a.od = aux->od;

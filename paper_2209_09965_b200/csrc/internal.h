@@ -239,7 +239,8 @@ constexpr int kLogitCol[2] = {4, 13};
 __host__ __device__ constexpr int logit_col(int s) { return s == 0 ? 4 : 13; }
 struct ConvAux {
   float* od = nullptr;         // (3,H,W) fp32, columns 0..2
-  __half* feedback = nullptr;  // NHWC8 input channels 5..7
+  __half* feedback = nullptr;  // the next input's feedback group (kInGroups)
+  const ConvParam* logits = nullptr;  // non-null: a decoder conv2 with its level's K logits fused (LG)
   kw_t* kw[2] = {nullptr, nullptr};  // (9,H,W) per K block
   int kcol[2] = {0, 0};
   bool center_only = false;    // 1x1 conv (logits only)
@@ -258,6 +259,10 @@ struct fv_net {
   int k_index0 = -1;  // first K conv
   // K stage as tcgen05 convs, one per level: D.head (level 0) + the logits of the K blocks there
   std::vector<fv::ConvParam> kconv;
+  // fused K stage (FV_KFUSE, default on): D.head alone as the level-0 conv, and per level L the K
+  // blocks' 1x1 logits as a [cin/8][32][8] image for the decoder conv2 epilogue (conv_tc.cu LG)
+  fv::ConvParam khead;
+  std::vector<fv::ConvParam> klog;
   bool kstage_dirty = true;
   uint64_t version = 1;  // bumped by every parameter change (captured frame graphs key on it)
 };
@@ -274,6 +279,17 @@ struct fv_act {
 // [O_d feedback (3), 0 x 5] (written whole by the K-stage level-0 conv of the previous frame).
 // Separate groups keep every writer's stores full 16-byte pixels with no shared bytes, so the
 // next frame's mask and this frame's D.head can run concurrently on one buffer.
+// FV_MARCH_CARVEOUT (A/B knob): preferred shared-memory carveout (percent) of the render branch's
+// kernels, set once per kernel; FV_MARCH_OCC (percent): the persistent march passes' blocks per SM
+template <typename K>
+inline void render_carveout(K kernel) {
+  static const int pc = getenv("FV_MARCH_CARVEOUT") ? atoi(getenv("FV_MARCH_CARVEOUT")) : -1;
+  if (pc >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+}
+inline int render_occ(int per_sm) {
+  static const int occ = getenv("FV_MARCH_OCC") ? atoi(getenv("FV_MARCH_OCC")) : 100;
+  return per_sm * occ / 100 > 1 ? per_sm * occ / 100 : 1;
+}
 constexpr int kInGroups = 2;
 inline __half* feedback_plane(const fv_act& x) { return x.p + x.plane(); }
 
@@ -363,4 +379,6 @@ int launch_volume_from_raw(fv_ctx* ctx, fv_volume* vol, const void* raw, int dty
 int reconstruct(fv_ctx* ctx, const fv_net* net, fv_state* st, int use_k, float* out_rgb,
                 float* out_o, float* out_od);
 int conv_prepare(fv_ctx* ctx, ConvParam& cp);
+int logits_prepare(fv_ctx* ctx, ConvParam& cp);
+bool logits_fusable(const ConvParam& cp);
 }  // namespace fv

@@ -1638,12 +1638,20 @@ int volume_bricks(fv_ctx* ctx, fv_volume* vol) {
 template <int TEX>
 int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
   const int blocks = std::max(1, std::min((F.P.k_max + 255) / 256, ctx->num_sms * 8));
+  static bool co = false;
+  if (!co) {
+    render_carveout(ray_setup_kernel);
+    render_carveout(march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB>);
+    render_carveout(first_list_kernel);
+    render_carveout(march_wave_composite_kernel);
+    co = true;
+  }
   FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<<<blocks, 256, 0, ctx->stream>>>(F, B));
   ctx->launches += 1;
   static int per_sm = 0;
   if (!per_sm) {
     FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB>, threads, 0));
-    per_sm = std::max(per_sm, 1);
+    per_sm = render_occ(std::max(per_sm, 1));
   }
   FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B));
   return 0;
@@ -1673,7 +1681,8 @@ int launch_shadow_dir_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int
   static int per_sm = 0;
   if (!per_sm) {
     FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_shadow_dir_kernel<U, MINB, LIN>, threads, 0));
-    per_sm = std::max(per_sm, 1);
+    per_sm = render_occ(std::max(per_sm, 1));
+    render_carveout(march_wave_shadow_dir_kernel<U, MINB, LIN>);
   }
   static const unsigned blk = getenv("FV_SHADOW_CLAIM") ? (unsigned)std::max(32, atoi(getenv("FV_SHADOW_CLAIM"))) : 64u;
   FV_TIMED(ctx, FV_KC_MARCH_SHADOW, march_wave_shadow_dir_kernel<U, MINB, LIN><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B, refill, blk));

@@ -226,6 +226,11 @@ int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
   p.tile_counter = &ctx->counters->scan_tile;
   p.dyn = ctx->dyn_active;
   FV_CUDA(cudaMemsetAsync(&ctx->counters->scan_tile, 0, sizeof(unsigned int), ctx->stream));
+  static bool co = false;
+  if (!co) {
+    render_carveout(mask_compact_kernel);
+    co = true;
+  }
   FV_TIMED(ctx, FV_KC_MASK, mask_compact_kernel<<<ntiles, kThreads, 0, ctx->stream>>>(p));
   FV_CHECK_LAUNCH("mask_compact_kernel");
   ctx->launches += 1;

@@ -84,8 +84,18 @@ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 // Build the level convs of the K stage from D.head + K.block{i} parameters: conv L reads the
 // decoder hidden state at level L; columns 0..2 = D.head (level 0 only, all 9 taps), columns
 // kLogitCol[s].. = the 9 logits of the s-th K block at that level (1x1 = centre tap).
+static void free_conv_dev(ConvParam& cp) {
+  if (cp.w_dev) cudaFree(cp.w_dev);
+  if (cp.b_dev) cudaFree(cp.b_dev);
+  cp.w_dev = nullptr;
+  cp.b_dev = nullptr;
+}
+
 int build_kstage(fv_ctx* ctx, fv_net* net) {
   const int ne = net->n_enc;
+  for (auto& cp : net->kconv) free_conv_dev(cp);
+  for (auto& cp : net->klog) free_conv_dev(cp);
+  free_conv_dev(net->khead);
   const std::vector<int> lv = block_levels(net);
   const ConvParam& head = net->convs[net->head_index];
   net->kconv.assign(ne + 1, ConvParam());
@@ -131,15 +141,69 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
     const int rc = conv_prepare(ctx, cp);
     if (rc) return rc;
   }
+  // the fused K stage: D.head alone (3 of 16 columns) and the per-level logits images
+  {
+    ConvParam& cp = net->khead;
+    cp = ConvParam();
+    cp.name = "K.head";
+    cp.cin = head.cin;
+    cp.cout = 3;
+    cp.n_pad = 16;
+    cp.w_host = head.w_host;
+    cp.b_host = head.b_host;
+    cp.w_set = cp.b_set = true;
+    cp.head_conv = true;
+    cp.macs_per_px = 27.0 * cp.cin;
+    const int rc = conv_prepare(ctx, cp);
+    if (rc) return rc;
+  }
+  net->klog.assign(ne + 1, ConvParam());
+  for (int L = 0; L <= ne; ++L) {
+    ConvParam& cp = net->klog[L];
+    const int cin = net->blocks[ne + (ne - L)].second;
+    cp.name = "K.logits" + std::to_string(L);
+    cp.cin = cin;
+    cp.ksize = 1;
+    int s = 0;
+    for (size_t i = 0; i < lv.size(); ++i) {
+      if (lv[i] != L || s >= 2) continue;
+      const ConvParam& kp = net->convs[net->k_index0 + i];  // (9, cin, 1, 1)
+      for (int j = 0; j < 9; ++j) {
+        for (int c = 0; c < cin; ++c) cp.w_host.push_back(kp.w_host[(size_t)j * cin + c]);
+        cp.b_host.push_back(kp.b_host[j]);
+      }
+      ++s;
+    }
+    cp.cout = 9 * s;
+    cp.w_set = cp.b_set = true;
+    if (s == 0) continue;
+    const int rc = logits_prepare(ctx, cp);
+    if (rc) return rc;
+  }
   net->kstage_dirty = false;
   return 0;
+}
+
+// FV_KFUSE (default 1): the K stage's logits in the decoder conv2 epilogues, when every decoder
+// conv2 has a fused variant (conv_tc.cu LG); 0 = the separate level convs (A/B, and forward_K)
+static bool kfuse(const fv_net* net) {
+  static const bool off = getenv("FV_KFUSE") && atoi(getenv("FV_KFUSE")) == 0;
+  if (off) return false;
+  const std::vector<int> lv = block_levels(net);
+  for (int j = 0; j < net->n_dec; ++j) {
+    const int L = net->n_enc - j;
+    if (net->klog.size() <= (size_t)L || !net->klog[L].w_dev) return false;
+    if (!logits_fusable(net->convs[2 * (net->n_enc + j) + 1])) return false;
+  }
+  return true;
 }
 
 // The K stage (network.py:268-293) plus D.head over the decoder hidden states hidden[hp]: the
 // level-0 conv writes D.head's O_d to od_out (and the next frame's feedback channels when feedback
 // is set), the filter chain starts from od_in (forward_K's given O_d) or, when null, from od_out.
 static int kstage_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int hp, float* od_out, __half* feedback,
-                           int use_k, const float* od_in, float* out_rgb, float* out_o, float* out_od) {
+                           int use_k, const float* od_in, float* out_rgb, float* out_o, float* out_od,
+                           bool fused = false) {
   const int ne = net->n_enc;
   int rc;
   // Level 0: one tcgen05 conv over Hd3 computes D.head (3x3, columns 0..2) AND the logits of
@@ -149,7 +213,15 @@ static int kstage_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int hp, float
   // softmax-normalised 3x3 filter weights of both K blocks. Levels > 0: a 1x1 logits conv each.
   const std::vector<int> lv = block_levels(net);
   const int nb = (int)lv.size();
-  for (int L = 0; L <= ne; ++L) {
+  if (fused) {
+    // the logits came with the decoder conv2s (conv_tc.cu LG): only D.head here
+    ConvAux aux;
+    aux.od = od_out;
+    aux.feedback = feedback;
+    rc = conv3x3(ctx, net->khead, &st->hidden[hp][ne], 1, nullptr, nullptr, false, &aux);
+    if (rc) return rc;
+  }
+  for (int L = 0; L <= ne && !fused; ++L) {
     if (L > 0 && !use_k) break;
     ConvAux aux;
     if (L == 0) {
@@ -239,6 +311,8 @@ int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, floa
     cur = &st->pooled[i];
   }
   const int oldp = st->parity, newp = st->parity ^ 1;
+  const bool fused = use_k && kfuse(net);
+  const std::vector<int> lv = block_levels(net);
   for (int j = 0; j < nd; ++j) {
     fv_act srcs[3];
     int n = 0;
@@ -254,12 +328,20 @@ int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, floa
     const int b = ne + j;
     rc = conv3x3(ctx, net->convs[2 * b], srcs, n, &st->dec_a[j], nullptr, true, nullptr);
     if (rc) return rc;
+    ConvAux laux;
+    if (fused) {
+      const int L = ne - j;
+      laux.logits = &net->klog[L];
+      int s = 0;
+      for (size_t i = 0; i < lv.size(); ++i)
+        if (lv[i] == L && s < 2) laux.kw[s++] = st->kw[i];
+    }
     rc = conv3x3(ctx, net->convs[2 * b + 1], &st->dec_a[j], 1, &st->hidden[newp][j], nullptr, true,
-                 nullptr);
+                 fused ? &laux : nullptr);
     if (rc) return rc;
   }
   return kstage_launches(ctx, net, st, newp, st->od, net->recurrent ? feedback_plane(st->xalt) : nullptr, use_k, nullptr,
-                         out_rgb, out_o, out_od);
+                         out_rgb, out_o, out_od, fused);
 }
 
 static bool graphs_enabled(const fv_ctx* ctx) {
@@ -439,11 +521,9 @@ int fv_net_create(fv_ctx* ctx, const char* blocks, int predicted_kernel, int rec
 
 int fv_net_destroy(fv_net* net) {
   if (!net) return 0;
-  for (auto* v : {&net->convs, &net->kconv})
-    for (auto& cp : *v) {
-      if (cp.w_dev) cudaFree(cp.w_dev);
-      if (cp.b_dev) cudaFree(cp.b_dev);
-    }
+  for (auto* v : {&net->convs, &net->kconv, &net->klog})
+    for (auto& cp : *v) free_conv_dev(cp);
+  free_conv_dev(net->khead);
   delete net;
   return 0;
 }

@@ -24,15 +24,28 @@ for j in range(5):
     pipe.step(cams[j], fovea, j)
 pipe.run_pipelined([(cams[j], fovea, j) for j in range(5)])
 torch.cuda.synchronize()
-frames = [(cams[5 + j], fovea, 5 + j) for j in range(12)]
+frames = [(cams[5 + j], fovea, 5 + j) for j in range(16)]
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     pipe.run_pipelined(frames)
     torch.cuda.synchronize()
+import os
 out = Path("gpurun_out"); out.mkdir(exist_ok=True)
-prof.export_chrome_trace(str(out / "timeline_raw.json"))
+tag = os.environ.get("TL_TAG", "")
+prof.export_chrome_trace(str(out / f"timeline_raw{tag}.json"))
 ev = []
-for e in json.load(open(out / "timeline_raw.json"))["traceEvents"]:
+for e in json.load(open(out / f"timeline_raw{tag}.json"))["traceEvents"]:
     if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset") and "dur" in e:
         ev.append({"name": e["name"][:90], "stream": e.get("tid"), "ts": e["ts"], "dur": e["dur"], "cat": e["cat"]})
-json.dump(ev, open(out / "timeline.json", "w"))
-print(len(ev), "device events")
+json.dump(ev, open(out / f"timeline{tag}.json", "w"))
+os.remove(out / f"timeline_raw{tag}.json")
+# median frame period on the network stream (E0.conv1 starts)
+k = sorted((e for e in ev if e["cat"] == "kernel"), key=lambda e: e["ts"])
+net_s = max(set(e["stream"] for e in k), key=lambda s_: sum(1 for e in k if e["stream"] == s_))
+starts, prev = [], None
+for e in k:
+    if e["stream"] == net_s:
+        if prev is not None and "kapply_final" in prev["name"] and "conv3x3" in e["name"]:
+            starts.append(e["ts"])
+        prev = e
+per = sorted(b - a for a, b in zip(starts, starts[1:]))
+print(f"{tag}: {len(ev)} device events, median frame {per[len(per) // 2]:.1f} us", flush=True)
