@@ -114,6 +114,8 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   for (auto& ev : ctx->kpool) cudaEventDestroy(ev);
   if (ctx->kopen) cudaEventDestroy(ctx->kopen);
   for (auto& e : ctx->fev) if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->kev) if (e) cudaEventDestroy(e);
+  if (ctx->kstream) cudaStreamDestroy(ctx->kstream);
   for (auto& s : ctx->fstream) if (s) cudaStreamDestroy(s);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -578,8 +580,24 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   cudaEvent_t* net_done = ctx->fev + 2;  // [2]
   cudaEvent_t* copied = ctx->fev + 4;    // [2]
   cudaEvent_t fork = ctx->fev[8], join = ctx->fev[9];
+  // The K filter chain + output stage of frame t as its own graph on the chain stream (FV_KCHAIN_SPLIT,
+  // default on): it overlaps the start of frame t+1's network (which waits for it only before its
+  // first decoder conv2 rewrites the weight planes and O_d). FV_KCHAIN_SPLIT=0: in the frame graph.
+  static const bool split = !(getenv("FV_KCHAIN_SPLIT") && atoi(getenv("FV_KCHAIN_SPLIT")) == 0);
+  if (split && !ctx->kstream) {
+    int lo = 0, hi = 0;
+    FV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    int prio = 0;
+    FV_CUDA(cudaStreamGetPriority(s_n, &prio));
+    FV_CUDA(cudaStreamCreateWithPriority(&ctx->kstream, cudaStreamNonBlocking, prio));
+    for (auto& e : ctx->kev) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t s_k = split ? ctx->kstream : s_n;
+  cudaEvent_t* chain_done = ctx->kev;  // [2]
+  cudaEvent_t chain_last = ctx->kev[2];
   FV_CUDA(cudaEventRecord(ctx->fev[6], own));
-  for (cudaStream_t s_ : {s_n, s_m, s_c}) FV_CUDA(cudaStreamWaitEvent(s_, ctx->fev[6], 0));
+  for (cudaStream_t s_ : {s_n, s_m, s_c, s_k}) FV_CUDA(cudaStreamWaitEvent(s_, ctx->fev[6], 0));
+  if (split) FV_CUDA(cudaEventRecord(chain_last, s_k));  // nothing pending: the first network need not wait
   // frame t+1's mask + march forked off frame t's network after its 4th conv (E1.conv2: the march
   // then runs next to the network's level 1-3 convs, which leave SMs idle). A/B at C3 (frames/s,
   // e2e), fork after conv 0 (off) / 2 / 4 / 6 / 8: 547.8 / 559.6 / 579.1 / 583.0 / 585.4 and e2e
@@ -620,7 +638,9 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     d.epoch = ctx->epoch;
     FG_TRY(cudaMemcpyAsync(ctx->dyn_dev, &d, sizeof(FrameDyn), cudaMemcpyHostToDevice, s_n));
     FG_TRY(cudaEventRecord(ctx->dyn_ev[slot], s_n));
-    if (t >= 2) FG_TRY(cudaStreamWaitEvent(s_n, copied[b], 0));  // frame t-2's copy read image b
+    if (t >= 2) FG_TRY(cudaStreamWaitEvent(s_k, copied[b], 0));  // frame t-2's copy read image b
+    ctx->kchain_split = split;
+    ctx->kw_wait_ev = split ? chain_last : nullptr;
     // the frame's launch configuration
     fv_state::FrameGraph* g = nullptr;
     for (auto& e : st->fgraphs)
@@ -682,6 +702,8 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
                       frame_ids[tn], img);
     }
     ctx->dyn_active = nullptr;
+    ctx->kchain_split = false;
+    ctx->kw_wait_ev = nullptr;
     if (g) ++g->uses;
     if (rc) break;
     // reconstruct()'s host-side state change: the input buffers swap, the hidden parity flips
@@ -689,17 +711,67 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     st->parity ^= 1;
     st->fresh = false;
     FG_TRY(cudaEventRecord(net_done[b], s_n));
+    if (split) {
+      // the filter chain of frame t into image b (reads O_d and the weight planes of frame t)
+      FG_TRY(cudaStreamWaitEvent(s_k, net_done[b], 0));
+      fv_state::ChainGraph* cg = nullptr;
+      for (auto& e : st->cgraphs)
+        if (e.net == net && e.version == net->version && e.img == img) cg = &e;
+      if (!cg) {
+        fv_state::ChainGraph e;
+        e.net = net; e.version = net->version; e.img = img;
+        st->cgraphs.push_back(e);
+        cg = &st->cgraphs.back();
+      }
+      ctx->stream = s_k;
+      if (cg->exec) {
+        const cudaError_t e = cudaGraphLaunch(cg->exec, s_k);
+        if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphLaunch (filter chain)");
+        ctx->launches += cg->n_launches;
+      } else if (cg->uses >= 1 && !no_graph) {
+        cudaGraph_t graph = nullptr;
+        const unsigned long long before = ctx->launches;
+        cudaError_t e = cudaStreamBeginCapture(st->fcap[0], cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+          ctx->stream = st->fcap[0];
+          rc = kfilter_launches(ctx, const_cast<fv_net*>(net), st, 1, st->od, img, nullptr, nullptr);
+          ctx->stream = s_k;
+          e = cudaStreamEndCapture(st->fcap[0], &graph);
+        }
+        if (!rc && e != cudaSuccess) rc = cuda_fail(e, "filter chain graph capture");
+        if (!rc) {
+          e = cudaGraphInstantiate(&cg->exec, graph, 0);
+          if (e != cudaSuccess) { cg->exec = nullptr; rc = cuda_fail(e, "cudaGraphInstantiate (filter chain)"); }
+        }
+        if (graph) cudaGraphDestroy(graph);
+        cg->n_launches = ctx->launches - before;
+        if (!rc) {
+          e = cudaGraphLaunch(cg->exec, s_k);
+          if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphLaunch (filter chain)");
+        }
+      } else {
+        rc = kfilter_launches(ctx, const_cast<fv_net*>(net), st, 1, st->od, img, nullptr, nullptr);
+      }
+      ctx->stream = s_n;
+      ++cg->uses;
+      if (rc) break;
+      FG_TRY(cudaEventRecord(chain_done[b], s_k));
+      FG_TRY(cudaEventRecord(chain_last, s_k));
+    }
+    cudaEvent_t img_ready = split ? chain_done[b] : net_done[b];
     const bool out = host_rgb_out && host_rgb_out[t];
     if (out) {
-      FG_TRY(cudaStreamWaitEvent(s_c, net_done[b], 0));
+      FG_TRY(cudaStreamWaitEvent(s_c, img_ready, 0));
       FG_TRY(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDefault, s_c));
     }
-    FG_TRY(cudaEventRecord(copied[b], out ? s_c : s_n));
+    FG_TRY(cudaEventRecord(copied[b], out ? s_c : s_k));
   }
 #undef FG_TRY
   ctx->dyn_active = nullptr;
+  ctx->kchain_split = false;
+  ctx->kw_wait_ev = nullptr;
   ctx->stream = own;
-  for (cudaStream_t s_ : {s_n, s_m, s_c}) {
+  for (cudaStream_t s_ : {s_n, s_m, s_c, s_k}) {
     cudaError_t e = cudaEventRecord(ctx->fev[7], s_);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(own, ctx->fev[7], 0);
     if (e != cudaSuccess && !rc) rc = cuda_fail(e, "fv_frames rejoin");

@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv3x3_tc_kernel(ConvArgs a) {
               Rs[o][c] += v[(dy * 3 + 2) * 3 + c];
             }
           }
-          if (hh == 1 || hh == 2) {
+          if (N >= 48 && (hh == 1 || hh == 2)) {
             // the centre row of output row r0 + hh - 1: its logits -> softmax -> filter weights
             uint32_t u2[16];
             sm100::tmem_ld16_nowait(ta + 32, u2);
@@ -1129,7 +1129,7 @@ template <int R, int N, int S, bool BRES, bool FUSED, bool CO = false, bool TAPN
 int launch(fv_ctx* ctx, const ConvArgs& args) {
   using C = Cfg<R, N, S, BRES, TAPN, LG>;
   static_assert(C::kSmem <= 227 * 1024, "conv tile configuration exceeds shared memory");
-  static_assert(!TAPN || (R == 4 && N >= 48 && !FUSED && !CO), "TAPN: 4-row tiles, 48 columns, plain issue");
+  static_assert(!TAPN || (R == 4 && N >= 32 && !FUSED && !CO), "TAPN: 4-row tiles, >= 32 columns, plain issue");
   static bool attr_set = false;
   if (!attr_set) {
     FV_CUDA(cudaFuncSetAttribute(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN, LG>,
@@ -1368,9 +1368,12 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
   const bool res = cp.n_stages <= kBResStages;
   const bool fu = cp.row_fused;
   if (cp.tapn) {
-    FV_REQUIRE(res && cp.n_pad == 48 && aux, "conv %s: the taps-in-N K-stage conv needs cin <= 64 and 48 columns",
+    // 48 columns: D.head's 27 tap columns + the level-0 logits; 32: D.head alone (the fused K stage)
+    FV_REQUIRE(res && (cp.n_pad == 48 || (cp.n_pad == 32 && !aux->kw[0] && !aux->kw[1])) && aux,
+               "conv %s: the taps-in-N K-stage conv needs cin <= 64 and 48 (32 without logits) columns",
                cp.name.c_str());
-    return launch<4, 48, 5, true, false, false, true>(ctx, a);
+    return cp.n_pad == 48 ? launch<4, 48, 5, true, false, false, true>(ctx, a)
+                          : launch<4, 32, 6, true, false, false, true>(ctx, a);
   }
 #define FV_LAUNCH(R_, N_, S_) \
   (res ? (fu ? launch<R_, N_, S_, true, true>(ctx, a) : launch<R_, N_, S_, true, false>(ctx, a)) \
@@ -1379,11 +1382,16 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
     return res ? launch<4, 32, 5, true, false, true>(ctx, a) : launch<4, 32, 5, false, false, true>(ctx, a);
   if (cp.pair && !aux)
     return res ? launch_pair<4, true>(ctx, a) : launch_pair<4, false>(ctx, a);
+  // D.head alone (the fused K stage's level-0 conv): 8-row tiles -- 30 row-fused dispatches per
+  // 8 output rows instead of 18 per 4 (the launch is bound by those A-operand reads); FV_KHEAD_R=4 A/B
+  static const int khead_r = getenv("FV_KHEAD_R") ? atoi(getenv("FV_KHEAD_R")) : 8;
+  if (cp.n_pad == 16 && cp.head_conv && fu && res && khead_r == 8) return launch<8, 16, 4, true, true>(ctx, a);
   switch (cp.n_pad) {
     case 16: return FV_LAUNCH(4, 16, 6);
     case 32: return FV_LAUNCH(4, 32, 5);
     case 48: return FV_LAUNCH(4, 48, 4);
     case 64:
+      // (8-row tiles here -- single accumulator, 3 stages -- measured slower: E0.conv2 117 -> 171 us)
       return res ? (fu ? launch<4, 64, 5, true, true>(ctx, a) : launch<4, 64, 5, true, false>(ctx, a))
                         : (fu ? launch<4, 64, 4, false, true>(ctx, a) : launch<4, 64, 4, false, false>(ctx, a));
     case 80: return res ? (fu ? launch<2, 80, 5, true, true>(ctx, a) : launch<2, 80, 5, true, false>(ctx, a))

@@ -165,6 +165,13 @@ struct fv_ctx {
   // march-ahead frames (fv_frames, FV_MARCH_AHEAD=k): record conv_fork_ev after the k-th conv launch
   cudaEvent_t conv_fork_ev = nullptr;
   int conv_fork_at = 0, conv_count = 0;
+  // fv_frames graph path: the network's launches stop after D.head (kchain_split); the filter chain
+  // + output stage run as their own graph on kstream, and the next network waits for kw_wait_ev
+  // (the chain's completion) before it rewrites the weight planes / O_d
+  bool kchain_split = false;
+  cudaEvent_t kw_wait_ev = nullptr;
+  cudaStream_t kstream = nullptr;
+  cudaEvent_t kev[3] = {};  // chain done (per output buffer) [2], chain done (latest) [1]
   // fv_frames: render / network / copy streams and their event rings (created on first use)
   cudaStream_t fstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t fev[10] = {};
@@ -346,6 +353,16 @@ struct fv_state {
     cudaGraphExec_t exec = nullptr;
   };
   std::vector<FrameGraph> fgraphs;
+  // fv_frames: the K filter chain + output stage of a frame into image `img`, per image buffer
+  struct ChainGraph {
+    const fv_net* net = nullptr;
+    uint64_t version = 0;
+    const float* img = nullptr;
+    int uses = 0;
+    unsigned long long n_launches = 0;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<ChainGraph> cgraphs;
   cudaStream_t fcap[2] = {nullptr, nullptr};
   cudaEvent_t fcap_ev[2] = {nullptr, nullptr};
 };
@@ -354,6 +371,8 @@ namespace fv {
 int prepare_net(fv_ctx* ctx, const fv_net* net);
 int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb, float* out_o,
                          float* out_od);
+int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const float* od, float* out_rgb,
+                     float* out_o, float* out_od);
 // launchers (return 0 / negative)
 int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
                         const double* pb_map, uint8_t* bits, int32_t* idx, int32_t* k,

@@ -148,7 +148,13 @@ int build_kstage(fv_ctx* ctx, fv_net* net) {
     cp.name = "K.head";
     cp.cin = head.cin;
     cp.cout = 3;
-    cp.n_pad = 16;
+    // FV_KHEAD_TAPN=1: the nine taps of D.head in N (27 of 32 columns, one MMA per halo row and
+    // K-stage; conv_tc.cu TAPN). Measured at C3 on the frame timeline: 108.5 us against 85.3 us for
+    // the row-fused 16-column form (bound by its 18 A-operand reads per stage, ncu tensor pipe 69%;
+    // TAPN trades them for its three-row, cross-lane epilogue), so opt-in.
+    static const bool tapn = getenv("FV_KHEAD_TAPN") && atoi(getenv("FV_KHEAD_TAPN")) == 1;
+    cp.tapn = tapn && cp.cin <= 64;
+    cp.n_pad = cp.tapn ? 32 : 16;
     cp.w_host = head.w_host;
     cp.b_host = head.b_host;
     cp.w_set = cp.b_set = true;
@@ -198,6 +204,9 @@ static bool kfuse(const fv_net* net) {
   return true;
 }
 
+int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const float* od, float* out_rgb,
+                     float* out_o, float* out_od);
+
 // The K stage (network.py:268-293) plus D.head over the decoder hidden states hidden[hp]: the
 // level-0 conv writes D.head's O_d to od_out (and the next frame's feedback channels when feedback
 // is set), the filter chain starts from od_in (forward_K's given O_d) or, when null, from od_out.
@@ -240,10 +249,21 @@ static int kstage_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int hp, float
     rc = conv3x3(ctx, net->kconv[L], &st->hidden[hp][ne - L], 1, nullptr, nullptr, false, &aux);
     if (rc) return rc;
   }
+  if (ctx->kchain_split && !od_in) return 0;  // the filter chain follows as its own graph (fv_frames)
+  return kfilter_launches(ctx, net, st, use_k, od_in ? od_in : od_out, out_rgb, out_o, out_od);
+}
+
+// The K stage's filter chain (forward_K, network.py:280-293) from O_d `od` and the weight planes
+// st->kw, then the output stage; use_k = 0: the output stage on O_d alone (forward_D's ablation).
+int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const float* od, float* out_rgb,
+                     float* out_o, float* out_od) {
+  int rc;
+  const std::vector<int> lv = block_levels(net);
+  const int nb = (int)lv.size();
   if (use_k) {
     // forward_K (network.py:280-293): encoder levels fuse the filter with the following pool, the
     // last block (level 0) with the output stage
-    const float* img = od_in ? od_in : od_out;
+    const float* img = od;
     // blocks 1 .. nb-2 (the small levels) as one cooperative launch when every encoder level there
     // has even width (the paired-pixel filter + pool)
     KChain ch;
@@ -289,7 +309,7 @@ static int kstage_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int hp, float
       }
     }
   } else {
-    rc = finalize(ctx, st, od_in ? od_in : od_out, out_rgb, out_o, out_od);
+    rc = finalize(ctx, st, od, out_rgb, out_o, out_od);
     if (rc) return rc;
   }
   return 0;
@@ -328,6 +348,14 @@ int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, floa
     const int b = ne + j;
     rc = conv3x3(ctx, net->convs[2 * b], srcs, n, &st->dec_a[j], nullptr, true, nullptr);
     if (rc) return rc;
+    if (j == 0 && ctx->kw_wait_ev) {
+      // fv_frames with the filter chain split off: the previous frame's chain (another stream)
+      // still reads the weight planes and O_d this conv2 and the K stage are about to rewrite
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      FV_CUDA(cudaStreamIsCapturing(ctx->stream, &cs));
+      FV_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->kw_wait_ev,
+                                  cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+    }
     ConvAux laux;
     if (fused) {
       const int L = ne - j;
@@ -672,6 +700,8 @@ int fv_state_destroy(fv_state* st) {
   for (auto& e : st->graphs)
     if (e.exec) cudaGraphExecDestroy(e.exec);
   for (auto& e : st->fgraphs)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
+  for (auto& e : st->cgraphs)
     if (e.exec) cudaGraphExecDestroy(e.exec);
   for (auto& s_ : st->fcap)
     if (s_) cudaStreamDestroy(s_);

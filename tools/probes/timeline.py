@@ -41,11 +41,7 @@ os.remove(out / f"timeline_raw{tag}.json")
 # median frame period on the network stream (E0.conv1 starts)
 k = sorted((e for e in ev if e["cat"] == "kernel"), key=lambda e: e["ts"])
 net_s = max(set(e["stream"] for e in k), key=lambda s_: sum(1 for e in k if e["stream"] == s_))
-starts, prev = [], None
-for e in k:
-    if e["stream"] == net_s:
-        if prev is not None and "kapply_final" in prev["name"] and "conv3x3" in e["name"]:
-            starts.append(e["ts"])
-        prev = e
+# frame boundaries: the per-frame parameter-block copy (HtoD) on the network stream
+starts = [e["ts"] for e in sorted(ev, key=lambda e: e["ts"]) if e["cat"] == "gpu_memcpy" and "HtoD" in e["name"]]
 per = sorted(b - a for a, b in zip(starts, starts[1:]))
 print(f"{tag}: {len(ev)} device events, median frame {per[len(per) // 2]:.1f} us", flush=True)

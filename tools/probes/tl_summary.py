@@ -4,12 +4,8 @@ ev = json.load(open(sys.argv[1] if len(sys.argv) > 1 else 'gpurun_out/timeline.j
 ev = [e for e in ev if e['cat'] == 'kernel']
 ev.sort(key=lambda e: e['ts'])
 net_s = max(set(e['stream'] for e in ev), key=lambda s: sum(1 for e in ev if e['stream'] == s))
-bounds, prev = [], None
-for e in ev:
-    if e['stream'] == net_s:
-        if prev and 'kapply_final2' in prev['name'] and 'conv3x3' in e['name']:
-            bounds.append(e['ts'])
-        prev = e
+allev = json.load(open(sys.argv[1] if len(sys.argv) > 1 else 'gpurun_out/timeline.json'))
+bounds = sorted(e['ts'] for e in allev if e['cat'] == 'gpu_memcpy' and 'HtoD' in e['name'])
 def short(n):
     n = re.sub(r'void |fv::|\(anonymous namespace\)::|<unnamed>::', '', n)
     return n[:60]
