@@ -1799,13 +1799,15 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     //   2  a hardware-filtered float texture: trilinear with 8-bit fractional weights (one 4-byte
     //      return per sample; 1 float per voxel) -- the SURVEY's fast tier
     // FV_TEX_FILTER: 0 = quads everywhere, 1 = filtered shadow samples only, 2 = filtered
-    // everywhere (the quad texture is then never built). Default: 1, and 2 for volumes whose quad
-    // copy would exceed 4 GiB (1024^3: 16 GiB of quads; the filtered main pass keeps the fast tier
-    // on colour, measured at C3 with depth one step off on ~0.03% of the active pixels, and the
-    // same C5 frame rate -- 121.1 vs 121.6 frames/s -- in 30.6 instead of 47.8 GB).
+    // everywhere (the quad texture is then never built). Default: 2 when the call asks for no depth
+    // output (the frame loop: the network input is RGBA only) or the volume's quad copy would exceed
+    // 4 GiB, else 1. The filtered main pass keeps the fast tier on colour (tests/test_headline_parity:
+    // RGBA max |err| and PSNR per C3 / C2 frame); its first-hit depth is one step off on ~0.03% of
+    // the active pixels, so calls that return depth keep the quads. Measured at C3 on the frame
+    // timeline: main pass 117.5 -> 103.5 us, frame 1594 -> 1575 us; at 1024^3 30.6 instead of 47.8 GB.
     static const int tex_filter_env = getenv("FV_TEX_FILTER") ? atoi(getenv("FV_TEX_FILTER")) : -1;
     const bool big = 16.0 * vol->nx * vol->ny * vol->nz > 4.0 * 1024 * 1024 * 1024;
-    const int tex_filter = tex_filter_env >= 0 ? tex_filter_env : big ? 2 : 1;
+    const int tex_filter = tex_filter_env >= 0 ? tex_filter_env : (big || !P.depth) ? 2 : 1;
     const int src = !tex_path ? 0 : tex_filter >= 2 ? 2 : 1;
     int rc = src == 0 ? volume_bricks(ctx, mv) : src == 1 ? volume_texture(ctx, mv) : 0;
     if (rc) return rc;

@@ -176,8 +176,10 @@ def render_full(scene: Scene, cam: Camera, settings: RenderSettings = RenderSett
 
 def render_sparse_compact(scene: Scene, cam: Camera, compact: CompactIndexList,
                           settings: RenderSettings = RenderSettings(), stats: bool = False,
-                          net_state=None) -> SparseFrame:
-    """March exactly one work item per compacted entry and back-project (renderer.py:262-288)."""
+                          net_state=None, want_depth: bool = True) -> SparseFrame:
+    """March exactly one work item per compacted entry and back-project (renderer.py:262-288).
+    want_depth=False: no depth output (Frame.depth stays zero) -- the marcher then takes the
+    frame loop's sample path (hardware-filtered main-pass samples, see csrc/march.cu)."""
     import torch
 
     if compact.dims != (cam.height, cam.width):
@@ -198,7 +200,7 @@ def render_sparse_compact(scene: Scene, cam: Camera, compact: CompactIndexList,
     _lib.check(ctx.lib.fv_render_sparse(
         ctx.h, vol, C.byref(camc), C.byref(lightc) if lightc else None, C.byref(setc),
         _lib.ptr(compact.idx_dev), _lib.ptr(compact.k_dev), int(compact.idx_dev.numel()),
-        _lib.ptr(rgba), _lib.ptr(depth), net_state, C.byref(st) if st is not None else None))
+        _lib.ptr(rgba), _lib.ptr(depth) if want_depth else None, net_state, C.byref(st) if st is not None else None))
     ev1.record(ctx.stream)
     from .sample_maps import scatter
 

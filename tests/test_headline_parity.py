@@ -14,7 +14,8 @@ weights, and compared frame by frame:
 Tolerances (DESIGN.md "Precision tiers"):
   mask + compaction     bit-exact, every frame
   marcher (fast tier)   over the frame's active pixels: max |err| <= 1e-2 on RGBA and
-                        PSNR(RGB) >= 80 dB; depth within 1e-3 on >= 99.99% of active pixels
+                        PSNR(RGB) >= 80 dB; depth within 1e-3 on >= 99.99% of active pixels; the
+                        same RGBA bounds for the depth-less march the frame loop runs
   network on the oracle's own sparse input (isolates the W-Net; FULL_BLOCKS, fp16 weights,
   state carried over all frames): PSNR >= 60 dB and max |err| <= 5e-3 per frame after the
                         clip; O_d (unclipped) max |err| <= 5e-3 x max(1, |O_d ref|max) per frame; hidden state after the last frame
@@ -136,6 +137,11 @@ def _run(name, stack, fullnet):
         r["march_psnr"] = _active_psnr(got, rgba_ref)
         r["march_psnr_uncapped"] = _psnr_uncapped(got, rgba_ref)
         r["march_frac_1e4"] = float((d <= 1e-4).mean()) if d.size else 1.0
+        # the frame loop's march (no depth output: hardware-filtered main-pass samples)
+        got2 = render_sparse_compact(scene, cam, comp, RenderSettings(), want_depth=False).rgba.reshape(-1, 4)[pix]
+        d2 = np.abs(got2 - rgba_ref)
+        r["march_nodepth_max"] = float(d2.max()) if d2.size else 0.0
+        r["march_nodepth_psnr"] = _active_psnr(got2, rgba_ref)
         dd = np.abs(gdep - dep_ref)
         r["depth_frac_1e3"] = float((dd <= 1e-3).mean()) if dd.size else 1.0
         r["depth_max"] = float(dd.max()) if dd.size else 0.0
@@ -187,6 +193,8 @@ def test_headline_march_fast_tier(name, stack, fullnet):
         assert r["march_max"] <= 1e-2, r
         assert r["march_psnr"] >= 80.0, r
         assert r["depth_frac_1e3"] >= 0.9999, r
+        assert r["march_nodepth_max"] <= 1e-2, r
+        assert r["march_nodepth_psnr"] >= 80.0, r
 
 
 @pytest.mark.parametrize("name", ["C3", "C2"])
