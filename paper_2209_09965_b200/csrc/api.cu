@@ -598,12 +598,15 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   FV_CUDA(cudaEventRecord(ctx->fev[6], own));
   for (cudaStream_t s_ : {s_n, s_m, s_c, s_k}) FV_CUDA(cudaStreamWaitEvent(s_, ctx->fev[6], 0));
   if (split) FV_CUDA(cudaEventRecord(chain_last, s_k));  // nothing pending: the first network need not wait
-  // frame t+1's mask + march forked off frame t's network after its 4th conv (E1.conv2: the march
+  // frame t+1's mask + march forked off frame t's network after its k-th conv launch (the march
   // then runs next to the network's level 1-3 convs, which leave SMs idle). A/B at C3 (frames/s,
   // e2e), fork after conv 0 (off) / 2 / 4 / 6 / 8: 547.8 / 559.6 / 579.1 / 583.0 / 585.4 and e2e
   // 498 / 506 / 520 / 514 / 492 (later forks collide with the level-0 decoder convs); frames are
   // bit-identical for every fork point. FV_MARCH_AHEAD=0: the march in line before the network.
-  static const int ahead = getenv("FV_MARCH_AHEAD") ? atoi(getenv("FV_MARCH_AHEAD")) : 4;
+  // With the K filter chain split off (it overlaps the frame's first convs), re-measured on the
+  // frame timeline (median us per frame), fork after conv 2 / 3 / 4 / 5 / 6 / 8: 1579 / 1590 / 1566 /
+  // 1575 / 1553 / 1558 -- after E2.conv2 (6) by default.
+  static const int ahead = getenv("FV_MARCH_AHEAD") ? atoi(getenv("FV_MARCH_AHEAD")) : 6;
   // prologue: frame 0's mask (and with march-ahead its march), by-value parameters
   ctx->stream = s_n;
   rc = launch_mask_compact(ctx, frame_ids[0], H, W, &foveas[0], nullptr, nullptr, ctx->idx_scratch, ctx->k_scratch,
