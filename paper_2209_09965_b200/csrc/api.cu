@@ -531,18 +531,59 @@ static int frame_body(fv_ctx* ctx, cudaStream_t s_main, cudaStream_t s_side, cud
 // the next frame fills the SMs the network's small levels leave idle. (Both write disjoint bytes of
 // that buffer: the mask channels 0..4, the march channels 0..3 of active pixels, the network's
 // D.head feedback channels 5..7; the network reads only the current buffer.)
+// The previous frame's K filter chain + output stage (FV_KCHAIN_SPLIT=2), forked off this frame's
+// network after its chain_at-th conv: it reads O_d and the weight planes of the previous frame,
+// which this frame's network rewrites only from its first decoder conv2 on -- that conv waits for
+// the chain's join event (ctx->kw_wait_ev, recorded in the same capture).
+struct ChainFork {
+  cudaStream_t s_main, s_side;
+  cudaEvent_t fork, join;
+  fv_net* net;
+  fv_state* st;
+  float* img;
+};
+
+static int chain_fork_hook(fv_ctx* ctx, void* arg) {
+  const ChainFork& c = *static_cast<const ChainFork*>(arg);
+  FV_CUDA(cudaEventRecord(c.fork, c.s_main));
+  FV_CUDA(cudaStreamWaitEvent(c.s_side, c.fork, 0));
+  const cudaStream_t keep = ctx->stream;
+  ctx->stream = c.s_side;
+  const int rc = kfilter_launches(ctx, c.net, c.st, 1, c.st->od, c.img, nullptr, nullptr);
+  ctx->stream = keep;
+  if (rc) return rc;
+  FV_CUDA(cudaEventRecord(c.join, c.s_side));
+  ctx->kw_wait_ev = c.join;
+  ctx->kw_wait_external = false;
+  return 0;
+}
+
 static int frame_body_ahead(fv_ctx* ctx, cudaStream_t s_main, cudaStream_t s_side, cudaEvent_t ev_fork,
                             cudaEvent_t ev_join, const fv_volume* vol, const fv_net* net, fv_state* st,
                             const fv_camera* cam_next, const fv_light* light, const fv_settings* settings,
-                            const fv_fovea* fovea_next, int frame_next, float* img, int fork_at) {
+                            const fv_fovea* fovea_next, int frame_next, float* img, int fork_at,
+                            const ChainFork* chain = nullptr, int chain_at = 0) {
   const int64_t npix = (int64_t)st->H * st->W;
   ctx->stream = s_main;
   ctx->conv_fork_ev = ev_fork;
   ctx->conv_fork_at = fork_at;
   ctx->conv_count = 0;
+  if (chain) {
+    ctx->conv_hook = chain_fork_hook;
+    ctx->conv_hook_arg = const_cast<ChainFork*>(chain);
+    ctx->conv_hook_at = chain_at;
+  }
   int rc = reconstruct_launches(ctx, const_cast<fv_net*>(net), st, 1, img, nullptr, nullptr);
+  const bool hook_missed = ctx->conv_hook != nullptr;
   ctx->conv_fork_ev = nullptr;
+  ctx->conv_hook = nullptr;
+  ctx->kw_wait_ev = nullptr;
   if (rc) return rc;
+  if (chain && hook_missed) {
+    set_error("fv_frames: the filter chain fork point (conv %d) lies past the first decoder conv2", chain_at);
+    return FV_E_INVALID;
+  }
+  if (chain) FV_CUDA(cudaStreamWaitEvent(s_main, chain->join, 0));
   if (ctx->conv_count < fork_at) FV_CUDA(cudaEventRecord(ev_fork, s_main));
   FV_CUDA(cudaStreamWaitEvent(s_side, ev_fork, 0));
   ctx->stream = s_side;
@@ -570,10 +611,10 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     FV_CUDA(cudaMallocHost(&ctx->dyn_host, sizeof(FrameDyn) * kDynRing));
     for (auto& e : ctx->dyn_ev) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i)
     if (!st->fcap[i]) FV_CUDA(cudaStreamCreateWithFlags(&st->fcap[i], cudaStreamNonBlocking));
+  for (int i = 0; i < 4; ++i)
     if (!st->fcap_ev[i]) FV_CUDA(cudaEventCreateWithFlags(&st->fcap_ev[i], cudaEventDisableTiming));
-  }
   static const bool no_graph = getenv("FV_FRAME_GRAPH") && atoi(getenv("FV_FRAME_GRAPH")) == 0;
   const cudaStream_t own = ctx->stream;
   cudaStream_t s_n = ctx->fstream[1], s_m = ctx->fstream[3], s_c = ctx->fstream[2];
@@ -583,8 +624,15 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   // The K filter chain + output stage of frame t as its own graph on the chain stream (FV_KCHAIN_SPLIT,
   // default on): it overlaps the start of frame t+1's network (which waits for it only before its
   // first decoder conv2 rewrites the weight planes and O_d). FV_KCHAIN_SPLIT=0: in the frame graph.
-  static const bool split = !(getenv("FV_KCHAIN_SPLIT") && atoi(getenv("FV_KCHAIN_SPLIT")) == 0);
-  if (split && !ctx->kstream) {
+  // FV_KCHAIN_SPLIT=2: instead, frame t's chain is folded into frame t+1's graph, forked after that
+  // network's FV_KCHAIN_AT-th conv (default 1: next to E0.conv2), and frame t's output is copied
+  // after frame t+1's graph. Measured on the C3 frame timeline (median us per frame): split stream
+  // 1531.6 / 1531.2, folded after conv 1 / 2 / 3: 1536.4 / 1536.8 / 1532.4 -- kept as the A/B.
+  static const int split_env = getenv("FV_KCHAIN_SPLIT") ? atoi(getenv("FV_KCHAIN_SPLIT")) : 1;
+  static const int chain_at = std::min(7, std::max(1, getenv("FV_KCHAIN_AT") ? atoi(getenv("FV_KCHAIN_AT")) : 1));
+  const bool fold = split_env == 2;  // (needs march-ahead; checked below)
+  const bool split = split_env == 1;
+  if ((split || fold) && !ctx->kstream) {
     int lo = 0, hi = 0;
     FV_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     int prio = 0;
@@ -607,6 +655,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   // frame timeline (median us per frame), fork after conv 2 / 3 / 4 / 5 / 6 / 8: 1579 / 1590 / 1566 /
   // 1575 / 1553 / 1558 -- after E2.conv2 (6) by default.
   static const int ahead = getenv("FV_MARCH_AHEAD") ? atoi(getenv("FV_MARCH_AHEAD")) : 6;
+  const bool folded = fold && ahead > 0;
   // prologue: frame 0's mask (and with march-ahead its march), by-value parameters
   ctx->stream = s_n;
   rc = launch_mask_compact(ctx, frame_ids[0], H, W, &foveas[0], nullptr, nullptr, ctx->idx_scratch, ctx->k_scratch,
@@ -641,14 +690,18 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     d.epoch = ctx->epoch;
     FG_TRY(cudaMemcpyAsync(ctx->dyn_dev, &d, sizeof(FrameDyn), cudaMemcpyHostToDevice, s_n));
     FG_TRY(cudaEventRecord(ctx->dyn_ev[slot], s_n));
-    if (t >= 2) FG_TRY(cudaStreamWaitEvent(s_k, copied[b], 0));  // frame t-2's copy read image b
-    ctx->kchain_split = split;
+    if (!folded && t >= 2) FG_TRY(cudaStreamWaitEvent(s_k, copied[b], 0));  // frame t-2's copy read image b
+    // folded: this graph's chain writes frame t-1's image, whose buffer frame t-3's copy read
+    float* prev_img = folded && t >= 1 ? ctx->rgb_scratch + (int64_t)((t - 1) & 1) * 3 * npix : nullptr;
+    if (folded && t >= 3) FG_TRY(cudaStreamWaitEvent(s_n, copied[(t - 1) & 1], 0));
+    ctx->kchain_split = split || folded;
     ctx->kw_wait_ev = split ? chain_last : nullptr;
+    ctx->kw_wait_external = split;
     // the frame's launch configuration
     fv_state::FrameGraph* g = nullptr;
     for (auto& e : st->fgraphs)
       if (e.vol == vol && e.net == net && e.version == net->version && e.wave_version == ctx->wave_version &&
-          e.x == st->x.p && e.parity == st->parity && e.ahead == ahead && e.img == img &&
+          e.x == st->x.p && e.parity == st->parity && e.ahead == ahead && e.img == img && e.prev_img == prev_img &&
           e.has_light == (light != nullptr) &&
           (!light || memcmp(&e.light, light, sizeof(fv_light)) == 0) &&
           memcmp(&e.settings, settings, sizeof(fv_settings)) == 0) {
@@ -663,7 +716,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       }
       fv_state::FrameGraph e;
       e.vol = vol; e.net = net; e.version = net->version; e.wave_version = ctx->wave_version; e.x = st->x.p;
-      e.parity = st->parity; e.ahead = ahead; e.img = img; e.has_light = light != nullptr;
+      e.parity = st->parity; e.ahead = ahead; e.img = img; e.prev_img = prev_img; e.has_light = light != nullptr;
       if (light) e.light = *light;
       e.settings = *settings;
       st->fgraphs.push_back(e);
@@ -680,8 +733,11 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       const unsigned long long before = ctx->launches;
       cudaError_t e = cudaStreamBeginCapture(st->fcap[0], cudaStreamCaptureModeThreadLocal);
       if (e == cudaSuccess) {
+        const ChainFork cf{st->fcap[0], st->fcap[2], st->fcap_ev[2], st->fcap_ev[3], const_cast<fv_net*>(net), st,
+                           prev_img};
         rc = ahead > 0 ? frame_body_ahead(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st,
-                                          &cams[tn], light, settings, &foveas[tn], frame_ids[tn], img, ahead)
+                                          &cams[tn], light, settings, &foveas[tn], frame_ids[tn], img, ahead,
+                                          prev_img ? &cf : nullptr, chain_at)
                        : frame_body(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st,
                                     &cams[t], light, settings, &foveas[tn], frame_ids[tn], img);
         e = cudaStreamEndCapture(st->fcap[0], &graph);
@@ -698,8 +754,9 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
         if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphLaunch (frame)");
       }
     } else if (ahead > 0) {
+      const ChainFork cf{s_n, s_k, ctx->kev[0], ctx->kev[1], const_cast<fv_net*>(net), st, prev_img};
       rc = frame_body_ahead(ctx, s_n, s_m, fork, join, vol, net, st, &cams[tn], light, settings, &foveas[tn],
-                            frame_ids[tn], img, ahead);
+                            frame_ids[tn], img, ahead, prev_img ? &cf : nullptr, chain_at);
     } else {
       rc = frame_body(ctx, s_n, s_m, fork, join, vol, net, st, &cams[t], light, settings, &foveas[tn],
                       frame_ids[tn], img);
@@ -707,6 +764,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     ctx->dyn_active = nullptr;
     ctx->kchain_split = false;
     ctx->kw_wait_ev = nullptr;
+    ctx->kw_wait_external = false;
     if (g) ++g->uses;
     if (rc) break;
     // reconstruct()'s host-side state change: the input buffers swap, the hidden parity flips
@@ -760,6 +818,31 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       if (rc) break;
       FG_TRY(cudaEventRecord(chain_done[b], s_k));
       FG_TRY(cudaEventRecord(chain_last, s_k));
+    }
+    if (folded) {
+      // frame t-1's image is complete with this graph
+      if (t >= 1) {
+        const bool out = host_rgb_out && host_rgb_out[t - 1];
+        if (out) {
+          FG_TRY(cudaStreamWaitEvent(s_c, net_done[b], 0));
+          FG_TRY(cudaMemcpyAsync(host_rgb_out[t - 1], prev_img, sizeof(float) * 3 * npix, cudaMemcpyDefault, s_c));
+        }
+        FG_TRY(cudaEventRecord(copied[(t - 1) & 1], out ? s_c : s_n));
+      }
+      if (t == n - 1) {
+        // the last frame's chain after its own graph
+        ctx->stream = s_n;
+        rc = kfilter_launches(ctx, const_cast<fv_net*>(net), st, 1, st->od, img, nullptr, nullptr);
+        if (rc) break;
+        FG_TRY(cudaEventRecord(net_done[b], s_n));
+        const bool out = host_rgb_out && host_rgb_out[t];
+        if (out) {
+          FG_TRY(cudaStreamWaitEvent(s_c, net_done[b], 0));
+          FG_TRY(cudaMemcpyAsync(host_rgb_out[t], img, sizeof(float) * 3 * npix, cudaMemcpyDefault, s_c));
+        }
+        FG_TRY(cudaEventRecord(copied[b], out ? s_c : s_n));
+      }
+      continue;
     }
     cudaEvent_t img_ready = split ? chain_done[b] : net_done[b];
     const bool out = host_rgb_out && host_rgb_out[t];

@@ -93,6 +93,20 @@ __device__ __forceinline__ void feedback_store(__half* px, float o0, float o1, f
   *reinterpret_cast<uint4*>(px) = v;
 }
 
+// fv_frames hooks after a conv launch: the march-ahead fork event and the filter-chain callback
+int conv_launched(fv_ctx* ctx) {
+  if (!ctx->conv_fork_ev && !ctx->conv_hook) return 0;
+  ++ctx->conv_count;
+  if (ctx->conv_fork_ev && ctx->conv_count == ctx->conv_fork_at)
+    FV_CUDA(cudaEventRecord(ctx->conv_fork_ev, ctx->stream));
+  if (ctx->conv_hook && ctx->conv_count == ctx->conv_hook_at) {
+    auto hook = ctx->conv_hook;
+    ctx->conv_hook = nullptr;  // once per frame
+    return hook(ctx, ctx->conv_hook_arg);
+  }
+  return 0;
+}
+
 // R output rows per tile, N output channels (MMA N), S pipeline stages; BRES: the whole weight
 // image (<= kBResStages stages, i.e. cin <= 64) is loaded once per CTA and stays in smem, so
 // only activations stream (the weights were ~40% of the L2->SM bytes of a 64->64 conv).
@@ -1118,8 +1132,10 @@ int launch_pair(fv_ctx* ctx, const ConvArgs& args) {
     fprintf(stderr, "[pair prof] %dx%d groups=%d: per leader %.1f tiles, total %.0f cyc; waits full %.0f peer %.0f tempty %.0f\n",
             a.H, a.W, a.groups, sm[5], sm[4], sm[1], sm[0], sm[2]);
   }
-  if (ctx->conv_fork_ev && ++ctx->conv_count == ctx->conv_fork_at)
-    FV_CUDA(cudaEventRecord(ctx->conv_fork_ev, ctx->stream));
+  {
+    const int hrc = conv_launched(ctx);
+    if (hrc) return hrc;
+  }
   FV_CHECK_LAUNCH("conv3x3_pair_kernel");
   ctx->launches += 1;
   return 0;
@@ -1145,8 +1161,10 @@ int launch(fv_ctx* ctx, const ConvArgs& args) {
   ktime_begin(ctx);
   fv::launch_pdl(conv3x3_tc_kernel<R, N, S, BRES, FUSED, CO, TAPN, LG>, grid, kThreads, C::kSmem, ctx->stream, a);
   ktime_end(ctx, FV_KC_CONV, a.flops);
-  if (ctx->conv_fork_ev && ++ctx->conv_count == ctx->conv_fork_at)
-    FV_CUDA(cudaEventRecord(ctx->conv_fork_ev, ctx->stream));
+  {
+    const int hrc = conv_launched(ctx);
+    if (hrc) return hrc;
+  }
   if (a.prof) {
     std::vector<unsigned long long> h((size_t)grid * kProfSlots);
     FV_CUDA(cudaMemcpyAsync(h.data(), a.prof, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));

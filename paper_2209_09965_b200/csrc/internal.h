@@ -170,6 +170,12 @@ struct fv_ctx {
   // (the chain's completion) before it rewrites the weight planes / O_d
   bool kchain_split = false;
   cudaEvent_t kw_wait_ev = nullptr;
+  bool kw_wait_external = false;  // kw_wait_ev recorded outside the capture (an external wait node)
+  // called after the conv_hook_at-th conv launch of a frame (fv_frames: forks the previous frame's
+  // filter chain off the network; counted with conv_fork_ev's counter)
+  int (*conv_hook)(fv_ctx*, void*) = nullptr;
+  void* conv_hook_arg = nullptr;
+  int conv_hook_at = 0;
   cudaStream_t kstream = nullptr;
   cudaEvent_t kev[3] = {};  // chain done (per output buffer) [2], chain done (latest) [1]
   // fv_frames: render / network / copy streams and their event rings (created on first use)
@@ -345,6 +351,7 @@ struct fv_state {
     const void* x = nullptr;
     int parity = 0, ahead = 0;
     const float* img = nullptr;
+    const float* prev_img = nullptr;  // the previous frame's filter chain folded in (FV_KCHAIN_SPLIT=2)
     fv_light light{};
     int has_light = 0;
     fv_settings settings{};
@@ -363,8 +370,8 @@ struct fv_state {
     cudaGraphExec_t exec = nullptr;
   };
   std::vector<ChainGraph> cgraphs;
-  cudaStream_t fcap[2] = {nullptr, nullptr};
-  cudaEvent_t fcap_ev[2] = {nullptr, nullptr};
+  cudaStream_t fcap[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fcap_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace fv {

@@ -354,7 +354,8 @@ int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, floa
       cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
       FV_CUDA(cudaStreamIsCapturing(ctx->stream, &cs));
       FV_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->kw_wait_ev,
-                                  cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+                                  cs == cudaStreamCaptureStatusActive && ctx->kw_wait_external
+                                      ? cudaEventWaitExternal : 0));
     }
     ConvAux laux;
     if (fused) {
