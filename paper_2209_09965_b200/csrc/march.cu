@@ -1260,6 +1260,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
   const unsigned lt_mask = (1u << lane) - 1u;
   const float amb = F.ambient;
   const float step = F.step_sh, inv_step = F.inv_step_sh, mt = F.min_trans;
+  const float lmt = mt > 0.f ? log2f(mt) : -INFINITY;  // LIN: the threshold on log2 T
   const float qsx = F.qs_sh[0], qsy = F.qs_sh[1], qsz = F.qs_sh[2];
   const float kscale = (float)(P.K - 1), e_full = F.e_sh;
   constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
@@ -1318,14 +1319,16 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
               if (ldt <= 0.f && n > 1) { --n; ldt += step; }
               ldt = fminf(ldt, step);
               const float m0 = t0 + 0.5f * step;
-              qax = fmaf(F.ld[0] * F.V.inv_sp[0], m0, fmaf(p[0], F.V.inv_sp[0], -0.5f));
-              qay = fmaf(F.ld[1] * F.V.inv_sp[1], m0, fmaf(p[1], F.V.inv_sp[1], -0.5f));
-              qaz = fmaf(F.ld[2] * F.V.inv_sp[2], m0, fmaf(p[2], F.V.inv_sp[2], -0.5f));
+              // (LIN: q + 1/2, the texel-centre offset, folded into the base)
+              constexpr float kQ0 = LIN ? 0.f : -0.5f;
+              qax = fmaf(F.ld[0] * F.V.inv_sp[0], m0, fmaf(p[0], F.V.inv_sp[0], kQ0));
+              qay = fmaf(F.ld[1] * F.V.inv_sp[1], m0, fmaf(p[1], F.V.inv_sp[1], kQ0));
+              qaz = fmaf(F.ld[2] * F.V.inv_sp[2], m0, fmaf(p[2], F.V.inv_sp[2], kQ0));
               last = n - 1;
               fl = (float)(n - 1) + 0.5f * (ldt - step) * inv_step;
               el = ldt * F.inv_ref;
               s = 0;
-              trans = 1.f;
+              trans = LIN ? 0.f : 1.f;  // LIN: log2 of the transmittance
               my = i;
             }
           }
@@ -1333,6 +1336,45 @@ __global__ void __launch_bounds__(128, MINB) march_wave_shadow_dir_kernel(FastPa
       }
     }
     if (!__any_sync(0xffffffffu, my >= 0)) break;
+    if constexpr (LIN) {
+      // Filtered samples with a lean per-sample path (the pass is issue-bound: ~37 -> ~28
+      // instructions per sample): the sample index clamps to the partial last step with one min;
+      // q < 0 (the half-voxel shell) -> q + 1 through a saturated FMA; the transmittance is kept as
+      // log2 T = sum e_j log2(1 - a_j) (one MUFU per sample) against log2 of the threshold.
+      const float sf = (float)s;
+      float vl[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float fs = fminf(sf + (float)u, fl);
+        const float cx = fmaf(qsx, fs, qax), cy = fmaf(qsy, fs, qay), cz = fmaf(qsz, fs, qaz);
+        // c + [c < 1/2]: (1/2 - c) * 2^126 saturates to 1 for every c < 1/2 down to ~1e-38 below
+        vl[u] = tex3D<float>(F.V.ltex, cx + __saturatef(fmaf(-cx, 8.5070592e37f, 4.2535296e37f)),
+                             cy + __saturatef(fmaf(-cy, 8.5070592e37f, 4.2535296e37f)),
+                             cz + __saturatef(fmaf(-cz, 8.5070592e37f, 4.2535296e37f)));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int si = s + u;
+        const float v = __saturatef(vl[u]);
+        const float xh = fmaf(v, kscale, -0.5f);
+        const float r = xh + kMagic;
+        const int i0 = __float_as_int(r) - __float_as_int(kMagic);
+        const float w = fmaf(v, kscale, -(r - kMagic));
+        const float2 lv = lut_om[i0];
+        const float om = fmaf(w, lv.y, lv.x);
+        if (si <= last && trans > lmt) {
+          trans = fmaf(si == last ? el : e_full, lg2_approx(om), trans);
+          ++n_shadow;
+        }
+      }
+      s += U;
+      if (my >= 0 && (s > last || !(trans > lmt))) {
+        B.shade[my] = amb + (1.f - amb) * ex2_approx(trans);
+        my = -1;
+        last = -1;
+      }
+      continue;
+    }
     // U samples per lane: positions first (all texture loads in flight), then the products
     float4 A[U], Bq[U];
     float tx[U], ty[U], tz[U];
