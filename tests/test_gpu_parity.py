@@ -764,12 +764,17 @@ def test_graph_replay_equals_eager_launches(tmp_path):
     assert np.array_equal(outs["1"][7:], outs["1"][:6])  # fv_frames (graphs) == the stepped frames
 
 
-@pytest.mark.parametrize("knob", ["FV_KCHAIN", "FV_PDL", "FV_MASK_AHEAD", "FV_MARCH_AHEAD"])
-def test_launch_variants_give_identical_frames(tmp_path, knob):
+@pytest.mark.parametrize("knob,vals", [("FV_KCHAIN", ("0", "1")), ("FV_PDL", ("0", "1")),
+                                       ("FV_MASK_AHEAD", ("0", "1")), ("FV_MARCH_AHEAD", ("0", "1")),
+                                       ("FV_KFUSE", ("0", "1")), ("FV_KCHAIN_SPLIT", ("0", "1")),
+                                       ("FV_KCHAIN_SPLIT", ("0", "2")), ("FV_KHEAD_R", ("4", "8"))])
+def test_launch_variants_give_identical_frames(tmp_path, knob, vals):
     """The fused K-stage chain (one cooperative launch for the levels between the first and last K
-    block), the programmatic-dependent launches, the next frame's mask next to the network and the
-    next frame's march forked off the network (FV_MARCH_AHEAD: after its first conv here) leave
-    every frame bit-identical: the same frames with the knob off and on."""
+    block), the programmatic-dependent launches, the next frame's mask next to the network, the
+    next frame's march forked off the network (FV_MARCH_AHEAD: after its first conv here), the K
+    logits fused into the decoder conv2 epilogues, the filter chain on its own stream / folded into
+    the next frame's graph and D.head's tile height leave every frame bit-identical: the same
+    frames with the knob at either value."""
     import os
     import subprocess
     import sys
@@ -777,16 +782,17 @@ def test_launch_variants_give_identical_frames(tmp_path, knob):
 
     root = str(Path(__file__).resolve().parents[1])
     outs = {}
-    for flag in ("0", "1"):
+    for flag in vals:
         out = tmp_path / f"frames_{flag}.npy"
         env = dict(os.environ, **{knob: flag})
         subprocess.run([sys.executable, "-c", _GRAPH_PROBE, root, str(out), "loops"], env=env, check=True,
                        timeout=300)
         outs[flag] = np.load(out)
-    assert np.array_equal(outs["0"], outs["1"])
+    a, b = vals
+    assert np.array_equal(outs[a], outs[b])
     # the pipelined loop ends on frame 5, fv_frames returns frames 0..5: all equal to the stepped ones
-    assert np.array_equal(outs["1"][6], outs["1"][5])
-    assert np.array_equal(outs["1"][7:], outs["1"][:6])
+    assert np.array_equal(outs[b][6], outs[b][5])
+    assert np.array_equal(outs[b][7:], outs[b][:6])
 
 
 def test_record_overflow_falls_back_to_inline_shadows():
