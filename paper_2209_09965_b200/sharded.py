@@ -208,16 +208,24 @@ def exchange_bands(bufs: dict, rank: int, world: int, group=None) -> None:
     tensors, gloo for CPU tensors). bufs: "send_up", "recv_up", "send_dn", "recv_dn" tensors."""
     import torch.distributed as dist
 
+    # gloo moves only host tensors point to point: stage device bands through host copies (the
+    # functional check of the torchrun paths on one GPU, FV_DIST_BACKEND=gloo)
+    staged = dist.get_backend(group) == "gloo" and any(t.is_cuda for t in bufs.values())
+    b = {k: (t.cpu() if staged else t) for k, t in bufs.items()}
     ops = []
     if rank > 0:
-        ops += [dist.P2POp(dist.isend, bufs["send_up"], rank - 1, group),
-                dist.P2POp(dist.irecv, bufs["recv_up"], rank - 1, group)]
+        ops += [dist.P2POp(dist.isend, b["send_up"], rank - 1, group),
+                dist.P2POp(dist.irecv, b["recv_up"], rank - 1, group)]
     if rank + 1 < world:
-        ops += [dist.P2POp(dist.isend, bufs["send_dn"], rank + 1, group),
-                dist.P2POp(dist.irecv, bufs["recv_dn"], rank + 1, group)]
+        ops += [dist.P2POp(dist.isend, b["send_dn"], rank + 1, group),
+                dist.P2POp(dist.irecv, b["recv_dn"], rank + 1, group)]
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    if staged:
+        for k in ("recv_up", "recv_dn"):
+            if bufs[k].numel():
+                bufs[k].copy_(b[k])
 
 
 class StripShardedPipeline:
