@@ -532,15 +532,16 @@ static int frame_body(fv_ctx* ctx, cudaStream_t s_main, cudaStream_t s_side, cud
 // that buffer: the mask channels 0..4, the march channels 0..3 of active pixels, the network's
 // D.head feedback channels 5..7; the network reads only the current buffer.)
 // The previous frame's K filter chain + output stage (FV_KCHAIN_SPLIT=2), forked off this frame's
-// network after its chain_at-th conv: it reads O_d and the weight planes of the previous frame,
-// which this frame's network rewrites only from its first decoder conv2 on -- that conv waits for
-// the chain's join event (ctx->kw_wait_ev, recorded in the same capture).
+// network after its chain_at-th conv: it reads the previous frame's O_d and weight planes (the
+// other parity's buffers, which this frame's network does not touch).
 struct ChainFork {
   cudaStream_t s_main, s_side;
   cudaEvent_t fork, join;
   fv_net* net;
   fv_state* st;
   float* img;
+  const float* od;
+  const std::vector<kw_t*>* kw;
 };
 
 static int chain_fork_hook(fv_ctx* ctx, void* arg) {
@@ -549,12 +550,10 @@ static int chain_fork_hook(fv_ctx* ctx, void* arg) {
   FV_CUDA(cudaStreamWaitEvent(c.s_side, c.fork, 0));
   const cudaStream_t keep = ctx->stream;
   ctx->stream = c.s_side;
-  const int rc = kfilter_launches(ctx, c.net, c.st, 1, c.st->od, c.img, nullptr, nullptr);
+  const int rc = kfilter_launches(ctx, c.net, c.st, 1, c.od, c.img, nullptr, nullptr, c.kw);
   ctx->stream = keep;
   if (rc) return rc;
   FV_CUDA(cudaEventRecord(c.join, c.s_side));
-  ctx->kw_wait_ev = c.join;
-  ctx->kw_wait_external = false;
   return 0;
 }
 
@@ -580,7 +579,7 @@ static int frame_body_ahead(fv_ctx* ctx, cudaStream_t s_main, cudaStream_t s_sid
   ctx->kw_wait_ev = nullptr;
   if (rc) return rc;
   if (chain && hook_missed) {
-    set_error("fv_frames: the filter chain fork point (conv %d) lies past the first decoder conv2", chain_at);
+    set_error("fv_frames: the filter chain fork point (conv %d) lies past the network's convs", chain_at);
     return FV_E_INVALID;
   }
   if (chain) FV_CUDA(cudaStreamWaitEvent(s_main, chain->join, 0));
@@ -621,15 +620,16 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   cudaEvent_t* net_done = ctx->fev + 2;  // [2]
   cudaEvent_t* copied = ctx->fev + 4;    // [2]
   cudaEvent_t fork = ctx->fev[8], join = ctx->fev[9];
-  // The K filter chain + output stage of frame t as its own graph on the chain stream (FV_KCHAIN_SPLIT,
-  // default on): it overlaps the start of frame t+1's network (which waits for it only before its
-  // first decoder conv2 rewrites the weight planes and O_d). FV_KCHAIN_SPLIT=0: in the frame graph.
-  // FV_KCHAIN_SPLIT=2: instead, frame t's chain is folded into frame t+1's graph, forked after that
-  // network's FV_KCHAIN_AT-th conv (default 1: next to E0.conv2), and frame t's output is copied
-  // after frame t+1's graph. Measured on the C3 frame timeline (median us per frame): split stream
-  // 1531.6 / 1531.2, folded after conv 1 / 2 / 3: 1536.4 / 1536.8 / 1532.4 -- kept as the A/B.
-  static const int split_env = getenv("FV_KCHAIN_SPLIT") ? atoi(getenv("FV_KCHAIN_SPLIT")) : 1;
-  static const int chain_at = std::min(7, std::max(1, getenv("FV_KCHAIN_AT") ? atoi(getenv("FV_KCHAIN_AT")) : 1));
+  // The K filter chain + output stage of frame t (10 launches) reads frame t's O_d and K weight
+  // planes, which are double-buffered by hidden parity, so it can run next to frame t+1's network:
+  //   FV_KCHAIN_SPLIT=2 (default): folded into frame t+1's graph, forked after its FV_KCHAIN_AT-th
+  //     conv (default 12: next to the level-0 upsample and D6.conv1); frame t's image is copied after
+  //     frame t+1's graph (one frame of output latency; the last frame's chain runs after the loop);
+  //   =1: its own graph on a chain stream right after frame t's graph;  =0: in the frame graph.
+  // Measured on the C3 frame timeline (median us per frame): chain stream 1539 / 1542, folded after
+  // conv 1 / 9 / 12 / 13: 1543 / 1541 / 1533 (1535) / 1537; in the frame graph (round-2 first pass) ~1610.
+  static const int split_env = getenv("FV_KCHAIN_SPLIT") ? atoi(getenv("FV_KCHAIN_SPLIT")) : 2;
+  static const int chain_at = std::min(14, std::max(1, getenv("FV_KCHAIN_AT") ? atoi(getenv("FV_KCHAIN_AT")) : 12));
   const bool fold = split_env == 2;  // (needs march-ahead; checked below)
   const bool split = split_env == 1;
   if ((split || fold) && !ctx->kstream) {
@@ -734,7 +734,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       cudaError_t e = cudaStreamBeginCapture(st->fcap[0], cudaStreamCaptureModeThreadLocal);
       if (e == cudaSuccess) {
         const ChainFork cf{st->fcap[0], st->fcap[2], st->fcap_ev[2], st->fcap_ev[3], const_cast<fv_net*>(net), st,
-                           prev_img};
+                           prev_img, st->od_buf[st->parity], &st->kw_buf[st->parity]};
         rc = ahead > 0 ? frame_body_ahead(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st,
                                           &cams[tn], light, settings, &foveas[tn], frame_ids[tn], img, ahead,
                                           prev_img ? &cf : nullptr, chain_at)
@@ -754,7 +754,8 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
         if (e != cudaSuccess) rc = cuda_fail(e, "cudaGraphLaunch (frame)");
       }
     } else if (ahead > 0) {
-      const ChainFork cf{s_n, s_k, ctx->kev[0], ctx->kev[1], const_cast<fv_net*>(net), st, prev_img};
+      const ChainFork cf{s_n, s_k, ctx->kev[0], ctx->kev[1], const_cast<fv_net*>(net), st, prev_img,
+                         st->od_buf[st->parity], &st->kw_buf[st->parity]};
       rc = frame_body_ahead(ctx, s_n, s_m, fork, join, vol, net, st, &cams[tn], light, settings, &foveas[tn],
                             frame_ids[tn], img, ahead, prev_img ? &cf : nullptr, chain_at);
     } else {
@@ -768,19 +769,17 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     if (g) ++g->uses;
     if (rc) break;
     // reconstruct()'s host-side state change: the input buffers swap, the hidden parity flips
-    std::swap(st->x, st->xalt);
-    st->parity ^= 1;
-    st->fresh = false;
+    state_advance(st);
     FG_TRY(cudaEventRecord(net_done[b], s_n));
     if (split) {
       // the filter chain of frame t into image b (reads O_d and the weight planes of frame t)
       FG_TRY(cudaStreamWaitEvent(s_k, net_done[b], 0));
       fv_state::ChainGraph* cg = nullptr;
       for (auto& e : st->cgraphs)
-        if (e.net == net && e.version == net->version && e.img == img) cg = &e;
+        if (e.net == net && e.version == net->version && e.img == img && e.od == st->od) cg = &e;
       if (!cg) {
         fv_state::ChainGraph e;
-        e.net = net; e.version = net->version; e.img = img;
+        e.net = net; e.version = net->version; e.img = img; e.od = st->od;
         st->cgraphs.push_back(e);
         cg = &st->cgraphs.back();
       }

@@ -5,6 +5,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/fovnet.h"
@@ -320,10 +321,13 @@ struct fv_state {
   std::vector<fv_act> ups;          // upsampled previous decoder output (j>0)
   std::vector<fv_act> hidden[2];    // ping-pong Hd per decoder block
   fv_act zero8;                     // unused
-  float* od = nullptr;              // (3,Hp,Wp) fp32 O_d (padded)
+  float* od = nullptr;              // (3,Hp,Wp) fp32 O_d (padded): the current frame's, od_buf[parity]
+  float* od_buf[2] = {nullptr, nullptr};  // per hidden parity, so frame t's filter chain can run next
+                                          // to frame t+1's network (fv_frames)
   std::vector<float*> img;          // K-stage ping buffers per level (3,HL,WL) fp32
   std::vector<float*> img2;
-  std::vector<fv::kw_t*> kw;        // per K block: softmax filter weights (9,HL,WL)
+  std::vector<fv::kw_t*> kw;        // per K block: softmax filter weights (9,HL,WL): kw_buf[parity]
+  std::vector<fv::kw_t*> kw_buf[2];
   void* arena = nullptr;
   int64_t arena_bytes = 0;
   // reconstruct() as captured CUDA graphs, one per launch configuration (the two input / hidden
@@ -365,6 +369,7 @@ struct fv_state {
     const fv_net* net = nullptr;
     uint64_t version = 0;
     const float* img = nullptr;
+    const float* od = nullptr;  // the parity's O_d / weight planes the chain reads
     int uses = 0;
     unsigned long long n_launches = 0;
     cudaGraphExec_t exec = nullptr;
@@ -375,11 +380,24 @@ struct fv_state {
 };
 
 namespace fv {
+// The host-side state change of one reconstruction (after its launches, whether eager, captured or a
+// replayed graph): the input buffers swap, the hidden parity flips, and the O_d / K weight-plane
+// views follow the parity the frame wrote.
+inline void state_views(fv_state* st) {
+  st->od = st->od_buf[st->parity];
+  st->kw = st->kw_buf[st->parity];
+}
+inline void state_advance(fv_state* st) {
+  std::swap(st->x, st->xalt);
+  st->parity ^= 1;
+  st->fresh = false;
+  state_views(st);
+}
 int prepare_net(fv_ctx* ctx, const fv_net* net);
 int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, float* out_rgb, float* out_o,
                          float* out_od);
 int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const float* od, float* out_rgb,
-                     float* out_o, float* out_od);
+                     float* out_o, float* out_od, const std::vector<kw_t*>* kw = nullptr);
 // launchers (return 0 / negative)
 int launch_mask_compact(fv_ctx* ctx, int frame, int H, int W, const fv_fovea* f,
                         const double* pb_map, uint8_t* bits, int32_t* idx, int32_t* k,

@@ -204,9 +204,6 @@ static bool kfuse(const fv_net* net) {
   return true;
 }
 
-int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const float* od, float* out_rgb,
-                     float* out_o, float* out_od);
-
 // The K stage (network.py:268-293) plus D.head over the decoder hidden states hidden[hp]: the
 // level-0 conv writes D.head's O_d to od_out (and the next frame's feedback channels when feedback
 // is set), the filter chain starts from od_in (forward_K's given O_d) or, when null, from od_out.
@@ -256,8 +253,9 @@ static int kstage_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int hp, float
 // The K stage's filter chain (forward_K, network.py:280-293) from O_d `od` and the weight planes
 // st->kw, then the output stage; use_k = 0: the output stage on O_d alone (forward_D's ablation).
 int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const float* od, float* out_rgb,
-                     float* out_o, float* out_od) {
+                     float* out_o, float* out_od, const std::vector<kw_t*>* kwv) {
   int rc;
+  const std::vector<kw_t*>& kwp = kwv ? *kwv : st->kw;
   const std::vector<int> lv = block_levels(net);
   const int nb = (int)lv.size();
   if (use_k) {
@@ -275,10 +273,10 @@ int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const fl
       if (chain && i >= 1 && i < nb - 1) {
         const int h = st->Hp >> L, w = st->Wp >> L;
         if (net->blocks[i].first == 'e') {
-          ch.s[ch.n++] = {0, h, w, st->kw[i], img, st->img[L + 1]};
+          ch.s[ch.n++] = {0, h, w, kwp[i], img, st->img[L + 1]};
           img = st->img[L + 1];
         } else {
-          ch.s[ch.n++] = {1, h, w, st->kw[i], img, st->img2[L]};
+          ch.s[ch.n++] = {1, h, w, kwp[i], img, st->img2[L]};
           ch.s[ch.n++] = {2, h, w, nullptr, st->img2[L], st->img[L - 1]};
           img = st->img[L - 1];
         }
@@ -289,18 +287,18 @@ int kfilter_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, const fl
         continue;
       }
       if (net->blocks[i].first == 'e') {
-        rc = kapply_pool(ctx, st->kw[i], img, st->img[L + 1], st->Hp >> L, st->Wp >> L);
+        rc = kapply_pool(ctx, kwp[i], img, st->img[L + 1], st->Hp >> L, st->Wp >> L);
         if (rc) return rc;
         img = st->img[L + 1];
       } else if (i < nb - 1) {
         float* out = st->img2[L];
-        rc = kapply(ctx, st->kw[i], img, out, st->Hp >> L, st->Wp >> L);
+        rc = kapply(ctx, kwp[i], img, out, st->Hp >> L, st->Wp >> L);
         if (rc) return rc;
         rc = up3(ctx, out, st->img[L - 1], st->Hp >> L, st->Wp >> L);
         if (rc) return rc;
         img = st->img[L - 1];
       } else if (L == 0) {
-        rc = kapply_final(ctx, st, st->kw[i], img, out_rgb, out_o, out_od);
+        rc = kapply_final(ctx, st, kwp[i], img, out_rgb, out_o, out_od);
         if (rc) return rc;
         img = nullptr;
       } else {
@@ -331,6 +329,9 @@ int reconstruct_launches(fv_ctx* ctx, fv_net* net, fv_state* st, int use_k, floa
     cur = &st->pooled[i];
   }
   const int oldp = st->parity, newp = st->parity ^ 1;
+  // this frame's O_d and K weight planes (the previous frame's stay intact for its filter chain)
+  st->od = st->od_buf[newp];
+  st->kw = st->kw_buf[newp];
   const bool fused = use_k && kfuse(net);
   const std::vector<int> lv = block_levels(net);
   for (int j = 0; j < nd; ++j) {
@@ -460,9 +461,7 @@ int reconstruct(fv_ctx* ctx, const fv_net* cnet, fv_state* st, int use_k, float*
     if (g) g->n_launches = ctx->launches - before;
   }
   if (g) ++g->uses;
-  std::swap(st->x, st->xalt);
-  st->parity ^= 1;
-  st->fresh = false;
+  state_advance(st);
   return 0;
 }
 
@@ -644,8 +643,11 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
     const int64_t h = st->Hp >> r.L, w = st->Wp >> r.L;
     bytes += align_up((int64_t)r.C * h * w * 2, 256);
   }
-  const int64_t od_off = bytes;
-  bytes += align_up((int64_t)3 * st->Hp * st->Wp * 4, 256);
+  int64_t od_off[2];
+  for (int p = 0; p < 2; ++p) {
+    od_off[p] = bytes;
+    bytes += align_up((int64_t)3 * st->Hp * st->Wp * 4, 256);
+  }
   std::vector<int64_t> img_off, img2_off;
   for (int L = 0; L <= ne; ++L) {
     img_off.push_back(bytes);
@@ -654,11 +656,12 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
     bytes += align_up((int64_t)3 * (st->Hp >> L) * (st->Wp >> L) * 4, 256);
   }
   const std::vector<int> lv = block_levels(net);
-  std::vector<int64_t> kw_off;
-  for (int L : lv) {
-    kw_off.push_back(bytes);
-    bytes += align_up((int64_t)9 * (st->Hp >> L) * (st->Wp >> L) * (int64_t)sizeof(kw_t), 256);
-  }
+  std::vector<int64_t> kw_off[2];
+  for (int p = 0; p < 2; ++p)
+    for (int L : lv) {
+      kw_off[p].push_back(bytes);
+      bytes += align_up((int64_t)9 * (st->Hp >> L) * (st->Wp >> L) * (int64_t)sizeof(kw_t), 256);
+    }
   if (cudaMalloc(&st->arena, bytes) != cudaSuccess) {
     delete st;
     set_error("cudaMalloc of %lld bytes for the state failed", (long long)bytes);
@@ -672,12 +675,15 @@ int fv_state_create(fv_ctx* ctx, const fv_net* net, int H, int W, fv_state** out
     reqs[i].a->H = st->Hp >> reqs[i].L;
     reqs[i].a->W = st->Wp >> reqs[i].L;
   }
-  st->od = reinterpret_cast<float*>(base + od_off);
+  for (int p = 0; p < 2; ++p) st->od_buf[p] = reinterpret_cast<float*>(base + od_off[p]);
+  st->od = st->od_buf[st->parity];
   for (int L = 0; L <= ne; ++L) {
     st->img.push_back(reinterpret_cast<float*>(base + img_off[L]));
     st->img2.push_back(reinterpret_cast<float*>(base + img2_off[L]));
   }
-  for (int64_t o : kw_off) st->kw.push_back(reinterpret_cast<kw_t*>(base + o));
+  for (int p = 0; p < 2; ++p)
+    for (int64_t o : kw_off[p]) st->kw_buf[p].push_back(reinterpret_cast<kw_t*>(base + o));
+  st->kw = st->kw_buf[st->parity];
   if (cudaMemsetAsync(st->arena, 0, bytes, ctx->stream) != cudaSuccess) {
     cudaFree(st->arena);
     delete st;
@@ -693,6 +699,7 @@ int fv_state_reset(fv_ctx* ctx, fv_state* st) {
   FV_CUDA(cudaMemsetAsync(st->arena, 0, st->arena_bytes, ctx->stream));
   st->parity = 0;
   st->fresh = true;
+  state_views(st);
   return 0;
 }
 
