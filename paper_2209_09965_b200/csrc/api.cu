@@ -115,6 +115,7 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   if (ctx->kopen) cudaEventDestroy(ctx->kopen);
   for (auto& e : ctx->fev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev) if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->kdone) if (e) cudaEventDestroy(e);
   if (ctx->kstream) cudaStreamDestroy(ctx->kstream);
   for (auto& s : ctx->fstream) if (s) cudaStreamDestroy(s);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -542,6 +543,7 @@ struct ChainFork {
   float* img;
   const float* od;
   const std::vector<kw_t*>* kw;
+  cudaEvent_t done;  // recorded (an external record node when captured) once the chain is complete
 };
 
 static int chain_fork_hook(fv_ctx* ctx, void* arg) {
@@ -553,6 +555,11 @@ static int chain_fork_hook(fv_ctx* ctx, void* arg) {
   const int rc = kfilter_launches(ctx, c.net, c.st, 1, c.od, c.img, nullptr, nullptr, c.kw);
   ctx->stream = keep;
   if (rc) return rc;
+  // (the external record first: the join below then covers it, so the capture stays joined)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  FV_CUDA(cudaStreamIsCapturing(c.s_side, &cs));
+  FV_CUDA(cudaEventRecordWithFlags(c.done, c.s_side,
+                                   cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0));
   FV_CUDA(cudaEventRecord(c.join, c.s_side));
   return 0;
 }
@@ -639,6 +646,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
     FV_CUDA(cudaStreamGetPriority(s_n, &prio));
     FV_CUDA(cudaStreamCreateWithPriority(&ctx->kstream, cudaStreamNonBlocking, prio));
     for (auto& e : ctx->kev) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ctx->kdone) FV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t s_k = split ? ctx->kstream : s_n;
   cudaEvent_t* chain_done = ctx->kev;  // [2]
@@ -734,7 +742,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       cudaError_t e = cudaStreamBeginCapture(st->fcap[0], cudaStreamCaptureModeThreadLocal);
       if (e == cudaSuccess) {
         const ChainFork cf{st->fcap[0], st->fcap[2], st->fcap_ev[2], st->fcap_ev[3], const_cast<fv_net*>(net), st,
-                           prev_img, st->od_buf[st->parity], &st->kw_buf[st->parity]};
+                           prev_img, st->od_buf[st->parity], &st->kw_buf[st->parity], ctx->kdone[(t - 1) & 1]};
         rc = ahead > 0 ? frame_body_ahead(ctx, st->fcap[0], st->fcap[1], st->fcap_ev[0], st->fcap_ev[1], vol, net, st,
                                           &cams[tn], light, settings, &foveas[tn], frame_ids[tn], img, ahead,
                                           prev_img ? &cf : nullptr, chain_at)
@@ -755,7 +763,7 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       }
     } else if (ahead > 0) {
       const ChainFork cf{s_n, s_k, ctx->kev[0], ctx->kev[1], const_cast<fv_net*>(net), st, prev_img,
-                         st->od_buf[st->parity], &st->kw_buf[st->parity]};
+                         st->od_buf[st->parity], &st->kw_buf[st->parity], ctx->kdone[(t - 1) & 1]};
       rc = frame_body_ahead(ctx, s_n, s_m, fork, join, vol, net, st, &cams[tn], light, settings, &foveas[tn],
                             frame_ids[tn], img, ahead, prev_img ? &cf : nullptr, chain_at);
     } else {
@@ -819,11 +827,11 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
       FG_TRY(cudaEventRecord(chain_last, s_k));
     }
     if (folded) {
-      // frame t-1's image is complete with this graph
+      // frame t-1's image is complete once this graph's chain branch is (its external record node)
       if (t >= 1) {
         const bool out = host_rgb_out && host_rgb_out[t - 1];
         if (out) {
-          FG_TRY(cudaStreamWaitEvent(s_c, net_done[b], 0));
+          FG_TRY(cudaStreamWaitEvent(s_c, ctx->kdone[(t - 1) & 1], 0));
           FG_TRY(cudaMemcpyAsync(host_rgb_out[t - 1], prev_img, sizeof(float) * 3 * npix, cudaMemcpyDefault, s_c));
         }
         FG_TRY(cudaEventRecord(copied[(t - 1) & 1], out ? s_c : s_n));

@@ -179,6 +179,7 @@ struct fv_ctx {
   int conv_hook_at = 0;
   cudaStream_t kstream = nullptr;
   cudaEvent_t kev[3] = {};  // chain done (per output buffer) [2], chain done (latest) [1]
+  cudaEvent_t kdone[2] = {};  // folded chain of the frame writing image b complete (an external record node)
   // fv_frames: render / network / copy streams and their event rings (created on first use)
   cudaStream_t fstream[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t fev[10] = {};
