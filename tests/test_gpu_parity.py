@@ -407,6 +407,33 @@ def test_pipelined_frames_equal_serial_frames(stack, loop, monkeypatch):
         assert torch.equal(pipe.rgb, ref[i]), i
 
 
+@pytest.mark.parametrize("h,w", [(97, 131), (200, 257)])
+def test_frame_loop_on_padded_films_equals_stepped_frames(stack, h, w):
+    """fv_frames (whole-frame graphs, the next frame's march and the previous frame's filter chain
+    forked off each network, O_d / K weight planes double-buffered) on films the network pads and
+    the convs tile partially: every frame equals the frame-by-frame result."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    spec = ExperimentSpec(mode="hifi", width=w, height=h)
+    scene = default_scene("sphere_shells", (48, 48, 48))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=2), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, w, h)
+    pipe = FramePipeline(scene, net, (h, w), stack)
+    frames = [(cams[5 * i], spec.fovea(), i) for i in range(7)]
+    ref = []
+    for c, f, j in frames:
+        pipe.step(c, f, j)
+        ref.append(pipe.rgb.clone())
+    pipe.reset()
+    outs = [torch.empty_like(pipe.rgb) for _ in frames]
+    pipe.run_pipelined(frames, outs)
+    torch.cuda.synchronize()
+    for i in range(len(frames)):
+        assert torch.equal(outs[i], ref[i]), i
+
+
 def test_kernel_timing_counts_algorithmic_conv_flops(stack):
     """Per-launch kernel timing: the conv class sums exactly 2 x 275,071.5 MAC/pixel (SURVEY 8(a)
     a20) over one FULL_BLOCKS frame, every class has positive time, and timing leaves frames unchanged."""
