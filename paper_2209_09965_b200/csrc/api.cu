@@ -662,7 +662,11 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   // With the K filter chain split off (it overlaps the frame's first convs), re-measured on the
   // frame timeline (median us per frame), fork after conv 2 / 3 / 4 / 5 / 6 / 8: 1579 / 1590 / 1566 /
   // 1575 / 1553 / 1558 -- after E2.conv2 (6) by default.
-  static const int ahead = getenv("FV_MARCH_AHEAD") ? atoi(getenv("FV_MARCH_AHEAD")) : 6;
+  // At 4K (C5) every network conv fills the GPU, so there is no idle capacity for the march: the
+  // march in line measured 124.4 / 125.6 against 123.3 / 123.5 frames/s forked after conv 6 --
+  // films above 4 Mpixel march in line by default.
+  static const int ahead_env = getenv("FV_MARCH_AHEAD") ? atoi(getenv("FV_MARCH_AHEAD")) : -1;
+  const int ahead = ahead_env >= 0 ? ahead_env : (npix > 4000000 ? 0 : 6);
   const bool folded = fold && ahead > 0;
   // prologue: frame 0's mask (and with march-ahead its march), by-value parameters
   ctx->stream = s_n;
