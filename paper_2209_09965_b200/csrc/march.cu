@@ -841,7 +841,6 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const bool lit = P.light_kind != FV_LIGHT_NONE;
-  const float amb = lit ? (float)P.ambient : 1.f;
   const float I0 = (float)P.intensity[0], I1 = (float)P.intensity[1], I2 = (float)P.intensity[2];
   const float early = (float)P.early, stepf = (float)P.step;
   const int kPool = B.chunk_pool;
@@ -1125,7 +1124,6 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastPar
     for (int c = lane; c < kPool; c += 32)
       if (pref + c < B.n_chunks_cap) B.chunk_fill[pref + c] = 0;
   }
-#pragma unroll
   if (lane == 0 && n_main) atomicAdd(&P.counters->samples_main, (unsigned long long)n_main);
 }
 

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kRed) ssim_horiz_kernel(const double* __restri
 
 // 2x2 mean downsampling with the odd row/column cropped (metrics.py:90-93)
 __global__ void down2_kernel(const double* __restrict__ in, int h, int w, double* __restrict__ out) {
-  const int ho = h / 2, wo = w / 2;
+  const int wo = w / 2;
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
   if (x >= wo) return;
   const double* r0 = in + (int64_t)(2 * y) * w + 2 * x;
