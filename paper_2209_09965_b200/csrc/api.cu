@@ -115,6 +115,7 @@ int fv_ctx_destroy(fv_ctx* ctx) {
   if (ctx->kopen) cudaEventDestroy(ctx->kopen);
   for (auto& e : ctx->fev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev) if (e) cudaEventDestroy(e);
+  if (ctx->scan_aux) cudaFree(ctx->scan_aux);
   for (auto& e : ctx->kdone) if (e) cudaEventDestroy(e);
   if (ctx->kstream) cudaStreamDestroy(ctx->kstream);
   for (auto& s : ctx->fstream) if (s) cudaStreamDestroy(s);

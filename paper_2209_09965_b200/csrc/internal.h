@@ -133,6 +133,8 @@ struct fv_ctx {
   // mask scan tile status words (epoch-tagged), sized for the largest film seen
   unsigned long long* scan_status = nullptr;
   int scan_tiles_cap = 0;
+  void* scan_aux = nullptr;  // two-pass mask: per-thread bit bytes + per-tile counts
+  int64_t scan_aux_cap = 0;
   unsigned int epoch = 0;
   fv::DevCounters* counters = nullptr;  // device
   int32_t* k_scratch = nullptr;          // device int32 for fv_frame
