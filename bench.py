@@ -469,17 +469,18 @@ def run_ours(args, cfg):
                    "serial_fps": whole_job_rate(k, world, serial_ms / 1e3),
                    "how": "value = K frames through the frame loop (FramePipeline.run_pipelined -> the C ABI's "
                           "fv_frames: each frame one replayed CUDA graph -- frame t's network with frame t+1's "
-                          "mask + march forked off it after its first convs (FV_MARCH_AHEAD), the per-frame "
-                          "camera / fovea read from a device parameter block), CUDA events on the pipeline "
-                          "stream; phase_ms from the same frames in serial order with events between the "
-                          "phases"},
+                          "mask + march forked off it after its 6th conv (FV_MARCH_AHEAD) and frame t-1's K "
+                          "filter chain + output stage after its 12th (FV_KCHAIN_SPLIT / FV_KCHAIN_AT), the "
+                          "per-frame camera / fovea read from a device parameter block), CUDA events on the "
+                          "pipeline stream; phase_ms from the same frames in serial order with events "
+                          "between the phases"},
         "roofline": roof, "stages": stages, "kernels": kernels, "marcher": marcher,
         "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": h * w * 3 * 4, "serial_fv_frame_fps": e2e_serial_fps,
                 "how": f"fv_frames C-ABI call over {ke} frames (run right after the headline region), wall "
                        "clock: per frame camera + fovea by value "
-                       "(H2D as kernel parameters), (H,W,3) f32 image D2H into pinned host memory; the copy of "
-                       "frame t-1 overlaps the compute of frame t (copy stream)"},
+                       "(H2D through the device parameter block), (H,W,3) f32 image D2H into pinned host memory; "
+                       "each image's copy overlaps the following frames' compute (copy stream)"},
         "gpu_launches": launches, "clocks": clk, "cpu_baseline": cpu, "device_memory_gb": device_memory_gb(),
         "sustained": sustained,
     }
