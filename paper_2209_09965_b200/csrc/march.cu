@@ -1845,9 +1845,14 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     // RGBA max |err| and PSNR per C3 / C2 frame); its first-hit depth is one step off on ~0.03% of
     // the active pixels, so calls that return depth keep the quads. Measured at C3 on the frame
     // timeline: main pass 117.5 -> 103.5 us, frame 1594 -> 1575 us; at 1024^3 30.6 instead of 47.8 GB.
+    // The 8-bit weights cost more on coarse grids (features span few voxels): measured over the
+    // active pixels of a foveated frame, filtered main-pass samples reach 76.9 / 89.0 / 95.6 dB at
+    // 40x36x32 / 128^3 / 256^3 (quads 85.6 / 97.6 / 100), so volumes below 128 voxels per axis
+    // keep the quads in the main pass.
     static const int tex_filter_env = getenv("FV_TEX_FILTER") ? atoi(getenv("FV_TEX_FILTER")) : -1;
     const bool big = 16.0 * vol->nx * vol->ny * vol->nz > 4.0 * 1024 * 1024 * 1024;
-    const int tex_filter = tex_filter_env >= 0 ? tex_filter_env : (big || !P.depth) ? 2 : 1;
+    const bool fine = std::min(vol->nx, std::min(vol->ny, vol->nz)) >= 128;
+    const int tex_filter = tex_filter_env >= 0 ? tex_filter_env : (big || (!P.depth && fine)) ? 2 : 1;
     const int src = !tex_path ? 0 : tex_filter >= 2 ? 2 : 1;
     int rc = src == 0 ? volume_bricks(ctx, mv) : src == 1 ? volume_texture(ctx, mv) : 0;
     if (rc) return rc;

@@ -224,6 +224,31 @@ def test_render_anisotropic_volume(golden):
     check_fp32(render_full(sc, cam).rgba, g["aniso_rgba"])
 
 
+def test_filtered_samples_of_out_of_range_volumes_keep_float_texels():
+    """A volume with voxels outside [0, 1] (possible through the C ABI's fv_volume_upload): the
+    filtered texture keeps float texels (unorm16 would clamp before the trilinear, the reference
+    clamps after it), so the depth-less fp32 march (filtered main and shadow samples) stays within
+    the fast tier of the fp64 march of the same volume."""
+    from paper_2209_09965_b200.volume import VolumeGrid
+
+    base = make_procedural_volume("sphere_shells", (128, 128, 128))
+    data = base.data.astype(np.float32) * np.float32(1.6) - np.float32(0.2)  # [-0.2, 1.4]
+    vol = VolumeGrid(base.dims, base.spacing, data, (float(data.min()), float(data.max())), _validated=True)
+    sc = Scene(volume=vol, tf=TransferFunction.default(), light=Light(direction=(-1.0, -1.0, -0.5)))
+    cam = Camera(position=(345.6, 281.6, 384.0), look_at=(64.0, 64.0, 64.0), fov_y=45.0, width=256, height=192)
+    h, w = cam.height, cam.width
+    m = S.build_sample_mask(default_stack(), 0, S.build_tau_map(
+        S.FoveaConfig(focus=((w - 1) / 2, (h - 1) / 2), sigma=0.2, base_density=0.3,
+                      pixel_scale=S.pixel_scale_for_film((h, w))), (h, w)))
+    comp = S.compact_mask(m)
+    pix = np.flatnonzero(m.bits.reshape(-1))
+    ref = render_sparse_compact(sc, cam, comp, RenderSettings(precision="fp64")).rgba.reshape(-1, 4)[pix]
+    got = render_sparse_compact(sc, cam, comp, RenderSettings(), want_depth=False).rgba.reshape(-1, 4)[pix]
+    d = np.abs(got - ref)
+    assert d.max() <= 1e-2, d.max()
+    assert O.psnr(got[:, :3], ref[:, :3]) >= 80.0  # over the active pixels, as the headline tier
+
+
 def test_render_c1_orbit_frames(golden):
     g = np.load(golden / "render_small.npz")
     vol = make_procedural_volume("sphere_shells", (64, 64, 64))
