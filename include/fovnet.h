@@ -73,6 +73,9 @@ typedef struct {
 /* renderer.RenderSettings (renderer.py:44-65); <=0 step/reference = resolve() default */
 #define FV_PREC_FP32 0
 #define FV_PREC_FP64 1
+/* fp32 arithmetic with software trilinear quads in both passes (no hardware-filtered samples):
+   the strict tier, <= ~2e-5 from the fp64 tier on every tested volume */
+#define FV_PREC_FP32_STRICT 2
 typedef struct {
   double step_size;
   double shadow_step_factor;
@@ -81,7 +84,7 @@ typedef struct {
   double ambient;
   double reference_step;
   double shadow_min_transmittance;
-  int32_t precision; /* FV_PREC_FP32 (default) or FV_PREC_FP64 */
+  int32_t precision; /* FV_PREC_FP32 (default, the fast tier), FV_PREC_FP32_STRICT or FV_PREC_FP64 */
   int32_t _pad;
 } fv_settings;
 

@@ -28,7 +28,7 @@ KERNEL_CLASSES = {"mask": FV_KC_MASK, "march_main": FV_KC_MARCH_MAIN, "march_sha
                   "other": FV_KC_OTHER}
 
 LIGHT_NONE, LIGHT_DIRECTIONAL, LIGHT_POINT = 0, 1, 2
-PREC_FP32, PREC_FP64 = 0, 1
+PREC_FP32, PREC_FP64, PREC_FP32_STRICT = 0, 1, 2
 
 
 class FvCamera(C.Structure):

@@ -1806,6 +1806,8 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
   P.step = s->step_size > 0 ? s->step_size : 0.5 * base;
   P.ref = s->reference_step > 0 ? s->reference_step : base;
   FV_REQUIRE(s->shadow_step_factor >= 1, "shadow_step_factor must be >= 1");
+  FV_REQUIRE(s->precision == FV_PREC_FP32 || s->precision == FV_PREC_FP32_STRICT || s->precision == FV_PREC_FP64,
+             "precision must be FV_PREC_FP32, FV_PREC_FP32_STRICT or FV_PREC_FP64, got %d", (int)s->precision);
   P.step_sh = P.step * s->shadow_step_factor;
   P.early = s->early_term_alpha;
   P.ambient = s->ambient;
@@ -1852,7 +1854,10 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
     static const int tex_filter_env = getenv("FV_TEX_FILTER") ? atoi(getenv("FV_TEX_FILTER")) : -1;
     const bool big = 16.0 * vol->nx * vol->ny * vol->nz > 4.0 * 1024 * 1024 * 1024;
     const bool fine = std::min(vol->nx, std::min(vol->ny, vol->nz)) >= 128;
-    const int tex_filter = tex_filter_env >= 0 ? tex_filter_env : (big || (!P.depth && fine)) ? 2 : 1;
+    const int tex_filter = s->precision == FV_PREC_FP32_STRICT ? 0
+                           : tex_filter_env >= 0                ? tex_filter_env
+                           : (big || (!P.depth && fine))        ? 2
+                                                                : 1;
     const int src = !tex_path ? 0 : tex_filter >= 2 ? 2 : 1;
     int rc = src == 0 ? volume_bricks(ctx, mv) : src == 1 ? volume_texture(ctx, mv) : 0;
     if (rc) return rc;

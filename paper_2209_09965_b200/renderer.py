@@ -36,8 +36,9 @@ class Scene:
 class RenderSettings:
     """renderer.RenderSettings (renderer.py:44-65) + the device arithmetic tier.
 
-    precision="fp32" marches in float (the fast tier); "fp64" runs the per-sample
-    arithmetic in double. Step control and sample positions are fp64 in both.
+    precision="fp32" marches in float (the fast tier: hardware-filtered samples); "fp32-strict" in
+    float with software trilinear everywhere (the strict tier); "fp64" runs the per-sample
+    arithmetic in double. Step control and sample positions are fp64 in all three.
     """
 
     step_size: float | None = None
@@ -54,8 +55,8 @@ class RenderSettings:
             raise ValueError("step_size must be > 0")
         if self.shadow_step_factor < 1:
             raise ValueError("shadow_step_factor must be >= 1")
-        if self.precision not in ("fp32", "fp64"):
-            raise ValueError(f"precision must be 'fp32' or 'fp64', got {self.precision!r}")
+        if self.precision not in ("fp32", "fp32-strict", "fp64"):
+            raise ValueError(f"precision must be 'fp32', 'fp32-strict' or 'fp64', got {self.precision!r}")
 
     def resolve(self, vol: VolumeGrid) -> tuple[float, float]:
         base = float(min(vol.spacing))
@@ -73,7 +74,7 @@ class RenderSettings:
         s.ambient = float(self.ambient)
         s.reference_step = float(self.reference_step) if self.reference_step is not None else 0.0
         s.shadow_min_transmittance = float(self.shadow_min_transmittance)
-        s.precision = _lib.PREC_FP64 if self.precision == "fp64" else _lib.PREC_FP32
+        s.precision = {"fp64": _lib.PREC_FP64, "fp32-strict": _lib.PREC_FP32_STRICT}.get(self.precision, _lib.PREC_FP32)
         return s
 
 

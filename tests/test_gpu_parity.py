@@ -249,6 +249,29 @@ def test_filtered_samples_of_out_of_range_volumes_keep_float_texels():
     assert O.psnr(got[:, :3], ref[:, :3]) >= 80.0  # over the active pixels, as the headline tier
 
 
+def test_strict_fp32_tier_on_sharp_edged_volumes():
+    """precision="fp32-strict" (software trilinear in both passes): the SURVEY's strict tier
+    (max |err| <= 1e-4) against the fp64 tier on box_lattice, whose slab edges the hardware
+    filter's 8-bit weights miss by up to ~9e-3 (the fast tier's bound is 1e-2)."""
+    vol = make_procedural_volume("box_lattice", (128, 128, 128))
+    sc = Scene(volume=vol, tf=TransferFunction.default(), light=Light(direction=(0.4, -1.0, 0.7)))
+    cam = Camera(position=(140.8, 422.4, -179.2), look_at=(64.0, 64.0, 64.0), fov_y=40.0, width=320, height=240)
+    h, w = cam.height, cam.width
+    m = S.build_sample_mask(default_stack(), 2, S.build_tau_map(
+        S.FoveaConfig(focus=((w - 1) / 2, (h - 1) / 2), sigma=0.06, base_density=0.07,
+                      pixel_scale=S.pixel_scale_for_film((h, w))), (h, w)))
+    comp = S.compact_mask(m)
+    pix = np.flatnonzero(m.bits.reshape(-1))
+    ref = render_sparse_compact(sc, cam, comp, RenderSettings(precision="fp64")).rgba.reshape(-1, 4)[pix]
+    strict = render_sparse_compact(sc, cam, comp, RenderSettings(precision="fp32-strict"),
+                                   want_depth=False).rgba.reshape(-1, 4)[pix]
+    fast = render_sparse_compact(sc, cam, comp, RenderSettings(), want_depth=False).rgba.reshape(-1, 4)[pix]
+    assert np.abs(strict - ref).max() <= 1e-4
+    assert np.abs(fast - ref).max() <= 1e-2
+    with pytest.raises(ValueError, match="precision"):
+        RenderSettings(precision="fp16")
+
+
 def test_render_c1_orbit_frames(golden):
     g = np.load(golden / "render_small.npz")
     vol = make_procedural_volume("sphere_shells", (64, 64, 64))
