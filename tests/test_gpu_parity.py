@@ -482,6 +482,36 @@ def test_frame_loop_on_padded_films_equals_stepped_frames(stack, h, w):
         assert torch.equal(outs[i], ref[i]), i
 
 
+def test_frame_loop_strict_tier_equals_stepped_frames(stack):
+    """The frame loop with RenderSettings(precision="fp32-strict") (quads in both march passes):
+    every fv_frames frame equals the stepped one, and differs from the fast tier's frames."""
+    from paper_2209_09965_b200.pipeline import FramePipeline
+    from paper_2209_09965_b200.renderer import OrbitPathSpec, orbit_cameras
+    from paper_2209_09965_b200.throughput import ExperimentSpec, default_scene
+
+    h, w = 184, 320
+    spec = ExperimentSpec(mode="hifi", width=w, height=h)
+    scene = default_scene("sphere_shells", (128, 128, 128))
+    net = N.quantized_net(N.init_network(N.NetConfig.from_string(N.FULL_BLOCKS), seed=4), "fp16")
+    cams = orbit_cameras(OrbitPathSpec(n_frames=500), scene.volume, w, h)
+    frames = [(cams[3 * i], spec.fovea(), i) for i in range(5)]
+    outs = {}
+    for prec in ("fp32-strict", "fp32"):
+        pipe = FramePipeline(scene, net, (h, w), stack, RenderSettings(precision=prec))
+        ref = []
+        for c, f, j in frames:
+            pipe.step(c, f, j)
+            ref.append(pipe.rgb.clone())
+        pipe.reset()
+        got = [torch.empty_like(pipe.rgb) for _ in frames]
+        pipe.run_pipelined(frames, got)
+        torch.cuda.synchronize()
+        for i in range(len(frames)):
+            assert torch.equal(got[i], ref[i]), (prec, i)
+        outs[prec] = got
+    assert not all(torch.equal(a, b) for a, b in zip(outs["fp32-strict"], outs["fp32"]))
+
+
 def test_kernel_timing_counts_algorithmic_conv_flops(stack):
     """Per-launch kernel timing: the conv class sums exactly 2 x 275,071.5 MAC/pixel (SURVEY 8(a)
     a20) over one FULL_BLOCKS frame, every class has positive time, and timing leaves frames unchanged."""
