@@ -1738,17 +1738,19 @@ int launch_shadow_dir_t(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int
 int launch_shadow_dir(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads) {
   static const int refill = getenv("FV_SHADOW_REFILL") ? std::min(32, std::max(1, atoi(getenv("FV_SHADOW_REFILL")))) : 8;
   // filtered samples: (samples in flight per lane, resident blocks per SM) -- FV_SHADOW_LIN=U,B (A/B)
+  // (6, 10) since the leaner per-sample path: C3 frame timeline 1529 against 1537 us for (4, 8),
+  // three A/B pairs on one box (shadow 225 against 233 us)
   static const int lin_cfg = getenv("FV_SHADOW_LIN") ? atoi(getenv("FV_SHADOW_LIN")) * 100 +
                                                            atoi(strchr(getenv("FV_SHADOW_LIN"), ',') + 1)
-                                                     : 408;
+                                                     : 610;
   if (F.V.ltex) {
     switch (lin_cfg) {
       case 808: return launch_shadow_dir_t<8, 8, true>(ctx, F, B, threads, refill);
       case 412: return launch_shadow_dir_t<4, 12, true>(ctx, F, B, threads, refill);
       case 812: return launch_shadow_dir_t<8, 12, true>(ctx, F, B, threads, refill);
       case 416: return launch_shadow_dir_t<4, 16, true>(ctx, F, B, threads, refill);
-      case 610: return launch_shadow_dir_t<6, 10, true>(ctx, F, B, threads, refill);
-      default: return launch_shadow_dir_t<4, 8, true>(ctx, F, B, threads, refill);
+      case 408: return launch_shadow_dir_t<4, 8, true>(ctx, F, B, threads, refill);
+      default: return launch_shadow_dir_t<6, 10, true>(ctx, F, B, threads, refill);
     }
   }
   return launch_shadow_dir_t<4, 8>(ctx, F, B, threads, refill);
