@@ -250,11 +250,12 @@ FV_API int fv_debug_conv3x3(fv_ctx* ctx, int cin, int cout, int H, int W, const 
 
 /* ---- whole frame ---------------------------------------------------------- */
 /* A camera path of n frames (bench.cmd_bench_throughput's loop, bench.py:194-209). Each frame --
- * the march of frame t, then frame t's network next to frame t+1's mask + compaction -- is replayed
- * as ONE captured CUDA graph whose kernels read the per-frame camera / fovea / noise frame from a
- * device parameter block (fed by one small host->device copy per frame); frame t's image is
- * copied into host_rgb_out[t] on a copy stream while later frames compute. Every frame equals the
- * corresponding fv_frame call. cams, foveas, frame_ids: n entries each; host_rgb_out: nullable,
+ * frame t's network, with frame t+1's mask + compaction + march and frame t-1's K filter chain +
+ * output stage forked off it (films above 4 Mpixel: frame t's march in line before its network) --
+ * is replayed as ONE captured CUDA graph whose kernels read the per-frame camera / fovea / noise
+ * frame from a device parameter block (fed by one small host->device copy per frame); frame t's
+ * image is copied into host_rgb_out[t] on a copy stream while later frames compute. Every frame
+ * equals the corresponding fv_frame call. cams, foveas, frame_ids: n entries each; host_rgb_out: nullable,
  * n pointers to (H,W,3) f32 buffers, each nullable (no copy for that frame), host (pinned for
  * overlap) or device memory; entries may repeat. Returns once every host copy has landed; device
  * copies are ordered on the context's stream. */

@@ -495,8 +495,9 @@ int fv_frame(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv_state* st,
 }
 
 // ---- fv_frames, whole-frame graph path ------------------------------------------------------
-// One frame = the march of frame t, then frame t's network next to frame t+1's mask + compaction
-// (a forked branch), captured once per launch configuration as ONE CUDA graph and replayed with
+// One frame = frame t's network with frame t+1's mask + march and frame t-1's K filter chain
+// forked off it (frame_body_ahead; frame_body: the march of frame t in line, then its network next
+// to frame t+1's mask), captured once per launch configuration as ONE CUDA graph and replayed with
 // cudaGraphLaunch. The per-frame inputs -- frame t's camera basis and frame t+1's fovea, noise
 // frame and scan epoch -- are read by the kernels from the context's FrameDyn block, which a
 // pinned ring feeds with one small host->device copy ahead of each replay (no host round trip:
@@ -887,6 +888,8 @@ static int frames_graph(fv_ctx* ctx, const fv_volume* vol, const fv_net* net, fv
   return 0;
 }
 
+// fv_frames: the whole-frame graph path above (frames_graph) by default; the stream-juggling path
+// below serves FV_PIPE_OVERLAP=1, FV_MASK_AHEAD=0, FV_FRAME_GRAPH=2, kernel timing and fp64 renders.
 // A path of frames with host outputs, pipelined over four streams:
 //   mask stream   : mask + compaction of frame t+1 (FV_MASK_AHEAD, default on) next to frame t's
 //                   network; waits for rendered[t] (the march of frame t, the last reader of the ray
