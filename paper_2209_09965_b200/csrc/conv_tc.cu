@@ -1278,6 +1278,15 @@ int conv_prepare(fv_ctx* ctx, ConvParam& cp) {
   return 0;
 }
 
+// 4-row tiles (single accumulator, row-pair release) for the row-fused 80-column convs
+// (FV_N80_R=4 measured: D4.conv1 256 -> 80 at 270 x 480 66 -> 53 us, frame conv 1133 -> 1117 us;
+// 4-row tiles halve the streamed weight bytes per output pixel). FV_N80_R=2 keeps 2-row tiles.
+static bool n80_r4() {
+  static const bool on = !(getenv("FV_N80_R") && atoi(getenv("FV_N80_R")) == 2);
+  return on;
+}
+
+
 // Whether conv3x3 has a fused-logits (LG) variant for this conv's shape (see its dispatch)
 bool logits_fusable(const ConvParam& cp) {
   const bool res = cp.n_stages <= kBResStages;
@@ -1410,9 +1419,13 @@ int conv3x3(fv_ctx* ctx, const ConvParam& cp, const fv_act* srcs, int n_src, fv_
     case 48: return FV_LAUNCH(4, 48, 4);
     case 64:
       // (8-row tiles here -- single accumulator, 3 stages -- measured slower: E0.conv2 117 -> 171 us)
+      // (8-row tiles for the streamed-weight ones measured flat / slower: D5.conv1 119 -> 118 us,
+      // D6.conv1 346 -> 359 us)
       return res ? (fu ? launch<4, 64, 5, true, true>(ctx, a) : launch<4, 64, 5, true, false>(ctx, a))
                         : (fu ? launch<4, 64, 4, false, true>(ctx, a) : launch<4, 64, 4, false, false>(ctx, a));
-    case 80: return res ? (fu ? launch<2, 80, 5, true, true>(ctx, a) : launch<2, 80, 5, true, false>(ctx, a))
+    case 80:
+      if (fu && n80_r4()) return res ? launch<4, 80, 4, true, true>(ctx, a) : launch<4, 80, 4, false, true>(ctx, a);
+      return res ? (fu ? launch<2, 80, 5, true, true>(ctx, a) : launch<2, 80, 5, true, false>(ctx, a))
                         : (fu ? launch<2, 80, 4, false, true>(ctx, a) : launch<2, 80, 4, false, false>(ctx, a));
     case 96: return res ? launch<2, 96, 5, true, false>(ctx, a) : launch<2, 96, 4, false, false>(ctx, a);
     case 128: return res ? launch<2, 128, 4, true, false>(ctx, a) : launch<2, 128, 4, false, false>(ctx, a);
