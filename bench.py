@@ -614,6 +614,10 @@ def run_sharded(args, cfg):
                                        "record all-gather (NCCL), replicated reconstruction"),
                        "strips": geo, "l2": "inputs larger than L2"},
             "samples_per_frame_rank0": samples,
+            "record_gather": ({"records_per_rank": pipe.frame_capacity(), "pixel_bound": pipe.cap,
+                               "bytes_per_frame": world * pipe.frame_capacity() * 12,
+                               "how": "sized per frame by the compacted ray count (last frame shown)"}
+                              if strip else None),
             "e2e": {"value": k / e2e_s, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": int(host.numel() * 4),
                     "how": "pipe.step per frame + pinned D2H of the rank's part of the image, wall clock"},

@@ -4,7 +4,8 @@ The march: every rank computes the full sample mask (microseconds) and marches o
 the compacted active-ray list -- 32-ray packets dealt round-robin, so each rank gets a statistically
 equal mix of foveal and peripheral rays (fixed screen tiles would be unbalanced by the fovea). The
 marched rays become 12-byte records (pixel, RGBA fp16 -- the network input is fp16) and ONE
-all_gather_into_tensor (NCCL over NVLink) gives every rank every record.
+all_gather_into_tensor (NCCL over NVLink) gives every rank every record; StripShardedPipeline sizes
+it per frame by the compacted ray count (ray_capacity), not by the pixel count.
 
 The reconstruction (StripShardedPipeline): each rank owns a strip of rows [a, b) of the padded
 frame (a multiple of the network divisor) and runs the unchanged W-Net on a WINDOW [a - E, b + E)
@@ -45,6 +46,13 @@ def packet_owner(k: int, world: int) -> np.ndarray:
 def record_capacity(n_pixels: int, world: int) -> int:
     """Fixed per-rank record count: the most packets any rank can own, times the packet size."""
     n_packets = (n_pixels + PACKET - 1) // PACKET
+    return (n_packets + world - 1) // world * PACKET
+
+
+def ray_capacity(k: int, world: int) -> int:
+    """Per-rank record count for a frame of k compacted rays: the most 32-ray packets any rank owns
+    (packets are dealt round-robin, packet_owner), times the packet size; >= one packet."""
+    n_packets = (max(int(k), 1) + PACKET - 1) // PACKET
     return (n_packets + world - 1) // world * PACKET
 
 
@@ -236,7 +244,7 @@ class StripShardedPipeline:
 
     def __init__(self, scene: Scene, net, dims: tuple[int, int], noise: NoiseStack,
                  settings: RenderSettings = RenderSettings(), rank: int = 0, world: int = 1, group=None,
-                 halo: int | None = None, emulate: bool = False):
+                 halo: int | None = None, emulate: bool = False, size_by_rays: bool = True):
         import ctypes as C
 
         import torch
@@ -246,6 +254,7 @@ class StripShardedPipeline:
         self.pipe = FramePipeline(scene, None, dims, noise, settings)
         self.net = net
         self.rank, self.world, self.group, self.emulate = rank, world, group, emulate
+        self.size_by_rays = size_by_rays
         h, w = dims
         self.h, self.w = h, w
         div = net.config.divisor
@@ -284,8 +293,18 @@ class StripShardedPipeline:
         _lib.check(p.ctx.lib.fv_mask_compact(p.ctx.h, int(frame), self.h, self.w, C.byref(f), None,
                                              _lib.ptr(self.bits), _lib.ptr(p.idx), _lib.ptr(p.k), None))
 
-    def march_shard(self, cam: Camera, rank: int) -> None:
-        """This rank's packets of the compacted list -> fb -> its 12-byte records."""
+    def frame_capacity(self) -> int:
+        """Records per rank for the current frame, from its compacted ray count k (every rank
+        computed the same full mask, so k -- one 4-byte device read after the mask -- is the same
+        on every rank, and so is the all-gather size): ray_capacity(k), not the pixel bound.
+        At C5 fast (k ~ 2.8 M of 8.3 M pixels) that gathers about a third of the pixel-sized bytes."""
+        if not self.size_by_rays:
+            return self.cap
+        return min(self.cap, ray_capacity(int(self.pipe.k[0].item()), self.world))
+
+    def march_shard(self, cam: Camera, rank: int, cap: int | None = None) -> None:
+        """This rank's packets of the compacted list -> fb -> its first `cap` 12-byte records
+        (pixel -1 past its rays)."""
         import ctypes as C
 
         p = self.pipe
@@ -298,14 +317,16 @@ class StripShardedPipeline:
                                             _lib.ptr(self.local_idx), _lib.ptr(self.local_k), n, _lib.ptr(self.fb),
                                             None, None, None))
         _lib.check(ctx.lib.fv_pack_records16(ctx.h, _lib.ptr(self.fb), _lib.ptr(self.local_idx),
-                                             _lib.ptr(self.local_k), self.cap, _lib.ptr(self.rec)))
+                                             _lib.ptr(self.local_k), self.cap if cap is None else cap,
+                                             _lib.ptr(self.rec)))
 
-    def reconstruct_window(self, rank: int) -> None:
+    def reconstruct_window(self, rank: int, n_records: int | None = None) -> None:
         ctx = self.pipe.ctx
         st = self.states[rank]
         w0 = self.geo[rank][2]
         _lib.check(ctx.lib.fv_window_input(ctx.h, st.h, _lib.ptr(self.bits), self.h, self.w, w0))
-        _lib.check(ctx.lib.fv_scatter_records16(ctx.h, st.h, _lib.ptr(self.gathered), int(self.gathered.shape[0]),
+        _lib.check(ctx.lib.fv_scatter_records16(ctx.h, st.h, _lib.ptr(self.gathered),
+                                                int(self.gathered.shape[0] if n_records is None else n_records),
                                                 self.w, w0))
         _lib.check(ctx.lib.fv_reconstruct(ctx.h, self.net_h, st.h, 1, _lib.ptr(self.img[rank]), None, None))
 
@@ -345,22 +366,24 @@ class StripShardedPipeline:
         import torch.distributed as dist
 
         self.mask(fovea, frame)
-        self.march_shard(cam, self.rank)
+        cap = self.frame_capacity()
+        self.march_shard(cam, self.rank, cap)
         if self.world > 1:
-            dist.all_gather_into_tensor(self.gathered, self.rec, group=self.group)
+            dist.all_gather_into_tensor(self.gathered[:self.world * cap], self.rec[:cap], group=self.group)
         else:
-            self.gathered.copy_(self.rec)
-        self.reconstruct_window(self.rank)
+            self.gathered[:cap].copy_(self.rec[:cap])
+        self.reconstruct_window(self.rank, self.world * cap)
         self.exchange()
 
     def step_emulated(self, cam: Camera, fovea: FoveaConfig, frame: int) -> None:
         """Every rank's share of the frame on this GPU, one rank after another."""
         self.mask(fovea, frame)
+        cap = self.frame_capacity()
         for r in range(self.world):
-            self.march_shard(cam, r)
-            self.gathered[r * self.cap:(r + 1) * self.cap].copy_(self.rec)
+            self.march_shard(cam, r, cap)
+            self.gathered[r * cap:(r + 1) * cap].copy_(self.rec[:cap])
         for r in self.ranks:
-            self.reconstruct_window(r)
+            self.reconstruct_window(r, self.world * cap)
         self.exchange()
 
     def owned_rgb(self, rank: int):

@@ -719,6 +719,8 @@ def test_strip_sharded_reconstruction_equals_unsharded_frames(stack, world, h):
         sh.step_emulated(cams[3 * i], spec.fovea(), i)
         torch.cuda.synchronize()
         assert torch.equal(sh.rgb, ref.rgb), i
+        # the all-gather is sized by the frame's ray count, well under the pixel bound
+        assert sh.frame_capacity() < sh.cap
     # without the band exchange the windows drift from the full frame (the exchange is load-bearing)
     sh2 = StripShardedPipeline(scene, net, (h, w), stack, world=world, emulate=True)
     ref.reset()

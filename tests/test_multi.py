@@ -107,6 +107,22 @@ def test_two_rank_ray_sharding_exchange():
     assert abs(counts[0] - counts[1]) <= 32  # packets dealt round-robin
 
 
+def test_ray_capacity_covers_every_rank_share():
+    """The per-frame record count (sized by the compacted ray count k) holds every rank's packets
+    (packet_owner's round-robin deal) and never exceeds the pixel bound."""
+    import numpy as np
+
+    from paper_2209_09965_b200 import sharded as SH
+
+    for k in (0, 1, 31, 32, 33, 1000, 2_776_913, 8_294_400):
+        for world in (1, 2, 3, 8):
+            cap = SH.ray_capacity(k, world)
+            owned = np.bincount(SH.packet_owner(k, world), minlength=world) if k else np.zeros(world)
+            assert owned.max() <= cap and cap % SH.PACKET == 0 and cap >= SH.PACKET
+            assert cap <= SH.record_capacity(max(k, 1), world) <= SH.record_capacity(8_294_400, world)
+            assert cap - owned.max() < SH.PACKET * (1 + (k == 0))
+
+
 def test_strip_geometry_and_band_plans():
     """Row strips partition the padded frame; each window holds its strip plus up to `halo` rows on
     either side; every band a rank receives is exactly the band its neighbour sends (global rows)."""
