@@ -874,13 +874,15 @@ def test_graph_replay_equals_eager_launches(tmp_path):
 @pytest.mark.parametrize("knob,vals", [("FV_KCHAIN", ("0", "1")), ("FV_PDL", ("0", "1")),
                                        ("FV_MASK_AHEAD", ("0", "1")), ("FV_MARCH_AHEAD", ("0", "1")),
                                        ("FV_KFUSE", ("0", "1")), ("FV_KCHAIN_SPLIT", ("0", "1")),
-                                       ("FV_KCHAIN_SPLIT", ("0", "2")), ("FV_KHEAD_R", ("4", "8"))])
+                                       ("FV_KCHAIN_SPLIT", ("0", "2")), ("FV_KHEAD_R", ("4", "8")),
+                                       ("FV_UP_ROWS", ("1", "2")), ("FV_UP_ROWS", ("1", "4")), ("FV_N80_R", ("2", "4"))])
 def test_launch_variants_give_identical_frames(tmp_path, knob, vals):
     """The fused K-stage chain (one cooperative launch for the levels between the first and last K
     block), the programmatic-dependent launches, the next frame's mask next to the network, the
     next frame's march forked off the network (FV_MARCH_AHEAD: after its first conv here), the K
     logits fused into the decoder conv2 epilogues, the filter chain on its own stream / folded into
-    the next frame's graph and D.head's tile height leave every frame bit-identical: the same
+    the next frame's graph, D.head's tile height, the upsample's rows per thread and the 80-column
+    convs' tile height leave every frame bit-identical: the same
     frames with the knob at either value."""
     import os
     import subprocess
