@@ -802,6 +802,7 @@ struct WaveBufs {
   unsigned int* ovf_count;
   unsigned int* hit_count;
   unsigned int* hit_next;
+  int by_hit;              // ray[] indexed by hit-list position (the composite walks the hits only)
 };
 
 __device__ __forceinline__ void write_pixel(const MarchParams& P, int pix, float r0, float r1, float r2,
@@ -835,7 +836,7 @@ template <int kU, int TEX>
 __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& B, const float* lut,
                                            unsigned hit_mask, int n, float last_dt, float ex, float ey,
                                            float ez, float dx, float dy, float dz, double t0, int pix,
-                                           int rid, int& pool_cur, int& pool_end, unsigned int& pool_pref,
+                                           int rid, int hid, int& pool_cur, int& pool_end, unsigned int& pool_pref,
                                            unsigned int& n_main) {
   const MarchParams& P = F.P;
   const int lane = threadIdx.x & 31;
@@ -857,6 +858,7 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
     const double rt0 = __shfl_sync(0xffffffffu, t0, src);
     const int rpix = __shfl_sync(0xffffffffu, pix, src);
     const int rray = __shfl_sync(0xffffffffu, rid, src);
+    const int rslot = B.by_hit ? __shfl_sync(0xffffffffu, hid, src) : rray;  // this ray's header in ray[]
     // (a loop of one pass: `continue` below abandons the ray when the record buffer is full)
     for (int pass = 0; pass < 1; ++pass) {
       float trans = 1.f, depth = 0.f;
@@ -970,7 +972,7 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
         // this pass (the overflow list), so neither this pass's samples nor its pixel count
         if (lane == 0) {
           for (int cc = first; cc >= 0; cc = (cc == chunk) ? -1 : B.chunk_next[cc]) B.chunk_fill[cc] = 0;
-          B.ray[rray] = make_int4(-1, 0, 0, 0);
+          B.ray[rslot] = make_int4(-1, 0, 0, 0);
           B.ovf[atomicAdd(B.ovf_count, 1u)] = rpix;
         }
         continue;
@@ -980,7 +982,7 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
         if (lane == 0) {
           B.chunk_fill[chunk] = fill;
           B.chunk_next[chunk] = -1;
-          B.ray[rray] = make_int4(first, m, __float_as_int(trans), __float_as_int(depth));
+          B.ray[rslot] = make_int4(first, m, __float_as_int(trans), __float_as_int(depth));
         }
       } else {
         if (lane == 0 && rray < B.cap_a) B.chunk_fill[rray] = 0;
@@ -992,7 +994,7 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
         }
         if (lane == 0) {
           write_pixel(P, rpix, rgb0, rgb1, rgb2, trans, depth);
-          B.ray[rray] = make_int4(-1, 0, 0, 0);
+          B.ray[rslot] = make_int4(-1, 0, 0, 0);
         }
       }
       break;
@@ -1040,7 +1042,7 @@ __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B
       ray_box(cam.pos, d, P.ext, t0, tend, hit);
       if (!hit) {
         write_pixel(P, pix, 0.f, 0.f, 0.f, 1.f, 0.f);
-        B.ray[r] = make_int4(-1, 0, 0, 0);
+        if (!B.by_hit) B.ray[r] = make_int4(-1, 0, 0, 0);
         if (r < B.cap_a) B.chunk_fill[r] = 0;
       } else {
         ++hitc;
@@ -1114,7 +1116,7 @@ __global__ void __launch_bounds__(128, MINB) march_wave_main_list_kernel(FastPar
     }
     const double t0 = __hiloint2double(__float_as_int(h2.y), __float_as_int(h2.x));
     march_hits<kU, TEX>(F, B, lut, __ballot_sync(0xffffffffu, valid), __float_as_int(h1.w), h1.z, h0.x, h0.y,
-                        h0.z, h0.w, h1.x, h1.y, t0, __float_as_int(h2.w), __float_as_int(h2.z), pool_cur,
+                        h0.z, h0.w, h1.x, h1.y, t0, __float_as_int(h2.w), __float_as_int(h2.z), i, pool_cur,
                         pool_end, pool_pref, n_main);
   }
   if (lit) {
@@ -1452,8 +1454,12 @@ __global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F,
   // the last are full (the main pass compacts records with ballots), so the fill of chunk j is
   // min(32, records - 32 j): chunk_fill is not read, and a chunk's records, shades and successor
   // link come back in one round trip.
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < k; r += warps) {
+  // by_hit: the headers sit at hit-list positions (the rays that miss the volume were written by
+  // the setup pass and are not visited; the pixel comes from the hit entry, loaded with the header)
+  const int n = B.by_hit ? (int)*B.hit_count : k;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
     const int4 v = B.ray[r];
+    const int hpix = B.by_hit && lane == 0 ? __float_as_int(B.hits[3 * (int64_t)r + 2].w) : 0;
     if (v.x < 0) continue;
     float rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;
     for (int c = v.x, jj = 0; jj < v.y; jj += kChunk) {
@@ -1475,7 +1481,8 @@ __global__ void __launch_bounds__(128) march_wave_composite_kernel(FastParams F,
       rgb2 += __shfl_xor_sync(0xffffffffu, rgb2, o);
     }
     if (lane == 0)
-      write_pixel(P, P.idx ? P.idx[r] : r, rgb0, rgb1, rgb2, __int_as_float(v.z), __int_as_float(v.w));
+      write_pixel(P, B.by_hit ? hpix : (P.idx ? P.idx[r] : r), rgb0, rgb1, rgb2, __int_as_float(v.z),
+                  __int_as_float(v.w));
   }
 }
 
@@ -1692,6 +1699,19 @@ int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads
   if (!per_sm) {
     FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB>, threads, 0));
     per_sm = render_occ(std::max(per_sm, 1));
+  }
+  // samples per lane per warp block (FV_MAIN_U): 1 = 32-sample blocks (C3 main pass 102.8 ->
+  // 97.6 us: a hitting ray takes ~40 samples, so 64-sample blocks fetched many past its end)
+  static const int main_u = getenv("FV_MAIN_U") ? atoi(getenv("FV_MAIN_U")) : 1;
+  if (main_u == 1) {
+    static int per_sm1 = 0;
+    if (!per_sm1) {
+      render_carveout(march_wave_main_list_kernel<1, TEX, FV_MAIN_MINB>);
+      FV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm1, march_wave_main_list_kernel<1, TEX, FV_MAIN_MINB>, threads, 0));
+      per_sm1 = render_occ(std::max(per_sm1, 1));
+    }
+    FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<1, TEX, FV_MAIN_MINB><<<ctx->num_sms * per_sm1, threads, 0, ctx->stream>>>(F, B));
+    return 0;
   }
   FV_TIMED(ctx, FV_KC_MARCH_MAIN, march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB><<<ctx->num_sms * per_sm, threads, 0, ctx->stream>>>(F, B));
   return 0;
@@ -1987,6 +2007,10 @@ int launch_render(fv_ctx* ctx, const fv_volume* vol, const fv_camera* cam, const
       }
       B.hits = reinterpret_cast<float4*>(ctx->wave_hits);
       B.hit_count = &ctx->counters->hit_count;
+      // headers at hit-list positions, composite over the hits only (FV_COMP_HITS=0: by compacted
+      // ray, every ray visited; C3 composite 56.5 -> 42.2 us)
+      static const bool by_hit = !(getenv("FV_COMP_HITS") && atoi(getenv("FV_COMP_HITS")) == 0);
+      B.by_hit = by_hit ? 1 : 0;
       B.hit_next = &ctx->counters->hit_next;
       if (k_max > ctx->wave_ovf_cap) {
         if (ctx->wave_ovf) cudaFree(ctx->wave_ovf);

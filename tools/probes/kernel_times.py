@@ -37,7 +37,7 @@ for j in range(first, first + count):
 torch.cuda.synchronize()
 st = ctx.stats()
 res = {k: ctx.kernel_time(c) for k, c in _lib.KERNEL_CLASSES.items()}
-print(f"frames {first}..{first + count - 1}: rays/frame {st.rays / count:.0f} main samples/frame "
+print(f"frames {first}..{first + count - 1}: rays/frame {st.rays / count:.0f} hits/frame {st.hit_rays / count:.0f} main samples/frame "
       f"{st.samples_main / count / 1e6:.2f} M shadow samples/frame {st.samples_shadow / count / 1e6:.2f} M")
 for k, (ms, work, nl) in res.items():
     if nl:
