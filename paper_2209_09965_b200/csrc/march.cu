@@ -666,9 +666,10 @@ template <int TEX>
 __global__ void __launch_bounds__(128) march_fast_kernel(FastParams F, bool count_rays) {
   const MarchParams& P = F.P;
   __shared__ float lut[4 * 256];
+  const int k = P.k_dev ? *P.k_dev : P.k_max;
+  if ((int64_t)blockIdx.x * blockDim.x >= k) return;  // (the overflow list is usually empty)
   for (int i = threadIdx.x; i < 4 * P.K; i += blockDim.x) lut[i] = P.lut[i];
   __syncthreads();
-  const int k = P.k_dev ? *P.k_dev : P.k_max;
   unsigned int n_main = 0, n_shadow = 0, hitc = 0, nr = 0;
   for (int i0 = blockIdx.x * blockDim.x; i0 < k; i0 += gridDim.x * blockDim.x) {
   const int i = i0 + threadIdx.x;
