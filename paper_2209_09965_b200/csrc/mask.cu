@@ -70,16 +70,23 @@ __device__ __forceinline__ unsigned int tile_bits(const MaskParams& p, unsigned 
   const float* nz = p.noise + (int64_t)(p.frame % p.T) * p.Ht * p.Wt;
   unsigned int bits = 0;
   int u = (int)(base % p.W), v = (int)(base / p.W);
+  int um = u % p.Wt, vm = v % p.Ht;  // the noise tile's coordinates, stepped with (u, v)
 #pragma unroll
   for (int j = 0; j < kPerThread; ++j) {
     const int64_t pix = base + j;
     if (pix < npix) {
-      const double n = (double)__ldg(nz + (v % p.Ht) * p.Wt + (u % p.Wt));
+      const double n = (double)__ldg(nz + vm * p.Wt + um);
       const bool m = n < tau_at(p, u, v);
       bits |= (unsigned)m << j;
       if (p.bits) p.bits[pix] = (uint8_t)m;
     }
-    if (++u == p.W) { u = 0; ++v; }
+    if (++um == p.Wt) um = 0;
+    if (++u == p.W) {
+      u = 0;
+      um = 0;
+      ++v;
+      if (++vm == p.Ht) vm = 0;
+    }
   }
   const int lane = tid & 31, warp = tid >> 5;
   // the network input's group 0 ([0 x 4, m, 0 x 3]: the march's records fill channels 0..3 of the
@@ -87,13 +94,17 @@ __device__ __forceinline__ unsigned int tile_bits(const MaskParams& p, unsigned 
   // wbase + 32 j + l, whose bit lane (32 j + l) / 8 holds
   if (p.net_in) {
     const int64_t wbase = (int64_t)tile * kTile + (int64_t)warp * 32 * kPerThread;
+    unsigned vv = (unsigned)((wbase + lane) / p.W), uu = (unsigned)((wbase + lane) - (int64_t)vv * p.W);
 #pragma unroll
     for (int j = 0; j < kPerThread; ++j) {
       const int q = 32 * j + lane;
       const unsigned b = __shfl_sync(0xffffffffu, bits, q >> 3);
       const int64_t pix = wbase + q;
+      if (j) {  // (u, v) of pixel wbase + q: 32 pixels on from the previous one
+        uu += 32;
+        while (uu >= (unsigned)p.W) { uu -= (unsigned)p.W; ++vv; }
+      }
       if (pix < npix) {
-        const unsigned vv = (unsigned)pix / (unsigned)p.W, uu = (unsigned)pix - vv * (unsigned)p.W;
         const bool m = (b >> (q & 7)) & 1u;
         *reinterpret_cast<uint4*>(p.net_in + ((int64_t)vv * p.net_wp + uu) * 8) =
             make_uint4(0u, 0u, m ? 0x3c00u : 0u, 0u);  // 0x3c00: fp16 1.0 in channel 4
