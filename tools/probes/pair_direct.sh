@@ -1,0 +1,5 @@
+# pair conv (FV_CONV_PAIR=1) with both producers completing on the leader's full barrier (FV_PAIR_DIRECT=1)
+# vs the forwarded phases (FV_PAIR_DIRECT=0) vs the single-CTA engine; correctness first, under timeouts
+FV_CONV_PAIR=1 timeout 240 python -m pytest tests/test_gpu_parity.py -q -x -k "conv3x3" 2>&1 | tail -2
+FV_CONV_PAIR=1 timeout 400 python -m pytest tests/test_gpu_parity.py -q -x -k "forward or end_to_end or pipelined" 2>&1 | tail -2
+for v in "0 1" "1 0" "1 1" "0 1" "1 0" "1 1"; do set -- $v; echo "== FV_CONV_PAIR=$1 FV_PAIR_DIRECT=$2"; FV_CONV_PAIR=$1 FV_PAIR_DIRECT=$2 FV_KTIME_LOG=1 timeout 300 python tools/probes/kernel_times.py 3 8 2> gpurun_out/pd_spans.log | grep conv; python tools/probes/launch_times.py gpurun_out/pd_spans.log 8 | grep conv | head -16 | awk '{printf "%s ", $3} END {print ""}'; done
