@@ -1014,52 +1014,73 @@ __device__ __forceinline__ void march_hits(const FastParams& F, const WaveBufs& 
 // then claims hitting rays a few at a time. A/B on B200 at C3 (main pass incl. setup, us):
 // in-kernel setup 262; list with 1 / 2 / 4 / 8 rays per claim: 171 / 168 / 180 / 211. Two per claim
 // also gave the best pipelined frame rate (the pass then co-runs with the network's convs).
+// one compacted ray's fp64 setup; misses write their pixel here
+__device__ __forceinline__ bool setup_ray(const MarchParams& P, const WaveBufs& B, int r, float4& h0, float4& h1,
+                                          double& t0, int& pix) {
+  pix = P.idx ? P.idx[r] : r;
+  const int u = pix % P.W, v = pix / P.W;
+  const CamView cam = load_cam(P);
+  const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * cam.tan_half * cam.aspect;
+  const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * cam.tan_half;
+  double d[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d[a] = cam.fwd[a] + sx * cam.right[a] + sy * cam.up[a];
+  const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
+  double tend;
+  bool hit;
+  ray_box(cam.pos, d, P.ext, t0, tend, hit);
+  if (!hit) {
+    write_pixel(P, pix, 0.f, 0.f, 0.f, 1.f, 0.f);
+    if (!B.by_hit) B.ray[r] = make_int4(-1, 0, 0, 0);
+    if (r < B.cap_a) B.chunk_fill[r] = 0;
+    return false;
+  }
+  const double L = tend - t0;
+  int n = (int)ceil((L - 1e-12) / P.step);
+  if (n < 1) n = 1;
+  const float last_dt = (float)(L - (double)(n - 1) * P.step);
+  h0 = make_float4((float)(cam.pos[0] + d[0] * t0), (float)(cam.pos[1] + d[1] * t0),
+                   (float)(cam.pos[2] + d[2] * t0), (float)d[0]);
+  h1 = make_float4((float)d[1], (float)d[2], last_dt, __int_as_float(n));
+  return true;
+}
+
+// RPT compacted rays per thread per round (r, r + 256, ...): their fp64 chains are independent, so
+// they overlap; a block's hits are appended with one atomic per round.
+template <int RPT>
 __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B) {
   const MarchParams& P = F.P;
   __shared__ unsigned s_cnt[8], s_off[8], s_base;
   const int k = P.k_dev ? *P.k_dev : P.k_max;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
   unsigned int nrays = 0, hitc = 0;
-  for (int r0 = blockIdx.x * blockDim.x; r0 < k; r0 += gridDim.x * blockDim.x) {
-    const int r = r0 + threadIdx.x;
-    bool hit = false;
-    int pix = 0, n = 0;
-    float4 h0, h1;
-    double t0 = 0.0;
-    if (r < k) {
-      pix = P.idx ? P.idx[r] : r;
-      ++nrays;
-      const int u = pix % P.W, v = pix / P.W;
-      const CamView cam = load_cam(P);
-      const double sx = (((double)u + 0.5) / P.W * 2.0 - 1.0) * cam.tan_half * cam.aspect;
-      const double sy = (1.0 - ((double)v + 0.5) / P.H * 2.0) * cam.tan_half;
-      double d[3];
+  for (int r0 = blockIdx.x * blockDim.x * RPT; r0 < k; r0 += gridDim.x * blockDim.x * RPT) {
+    bool hit[RPT];
+    int pix[RPT];
+    float4 h0[RPT], h1[RPT];
+    double t0[RPT];
 #pragma unroll
-      for (int a = 0; a < 3; ++a) d[a] = cam.fwd[a] + sx * cam.right[a] + sy * cam.up[a];
-      const double nrm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-      d[0] /= nrm; d[1] /= nrm; d[2] /= nrm;
-      double tend;
-      ray_box(cam.pos, d, P.ext, t0, tend, hit);
-      if (!hit) {
-        write_pixel(P, pix, 0.f, 0.f, 0.f, 1.f, 0.f);
-        if (!B.by_hit) B.ray[r] = make_int4(-1, 0, 0, 0);
-        if (r < B.cap_a) B.chunk_fill[r] = 0;
-      } else {
-        ++hitc;
-        const double L = tend - t0;
-        n = (int)ceil((L - 1e-12) / P.step);
-        if (n < 1) n = 1;
-        const float last_dt = (float)(L - (double)(n - 1) * P.step);
-        h0 = make_float4((float)(cam.pos[0] + d[0] * t0), (float)(cam.pos[1] + d[1] * t0),
-                         (float)(cam.pos[2] + d[2] * t0), (float)d[0]);
-        h1 = make_float4((float)d[1], (float)d[2], last_dt, __int_as_float(n));
+    for (int q = 0; q < RPT; ++q) {
+      const int r = r0 + q * blockDim.x + threadIdx.x;
+      hit[q] = false;
+      pix[q] = 0;
+      t0[q] = 0.0;
+      if (r < k) {
+        ++nrays;
+        hit[q] = setup_ray(P, B, r, h0[q], h1[q], t0[q], pix[q]);
+        hitc += hit[q] ? 1u : 0u;
       }
     }
     // one append per block (the shared list counter is contended: one atomic per warp cost ~2x)
-    const unsigned hm = __ballot_sync(0xffffffffu, hit);
-    const int warp = threadIdx.x >> 5;
-    if (lane == 0) s_cnt[warp] = __popc(hm);
+    unsigned hm[RPT], wcnt = 0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      hm[q] = __ballot_sync(0xffffffffu, hit[q]);
+      wcnt += __popc(hm[q]);
+    }
+    if (lane == 0) s_cnt[warp] = wcnt;
     __syncthreads();
     if (threadIdx.x == 0) {
       unsigned t = 0;
@@ -1067,14 +1088,19 @@ __global__ void __launch_bounds__(256) ray_setup_kernel(FastParams F, WaveBufs B
       s_base = t ? atomicAdd(B.hit_count, t) : 0u;
     }
     __syncthreads();
-    const unsigned base = s_base + s_off[warp];
-    __syncthreads();  // (s_cnt / s_off / s_base are rewritten by the next iteration)
-    if (hit) {
-      float4* e = B.hits + 3 * (int64_t)(base + __popc(hm & lt_mask));
-      e[0] = h0;
-      e[1] = h1;
-      e[2] = make_float4(__int_as_float(__double2loint(t0)), __int_as_float(__double2hiint(t0)),
-                         __int_as_float(r), __int_as_float(pix));
+    unsigned base = s_base + s_off[warp];
+    __syncthreads();  // (s_cnt / s_off / s_base are rewritten by the next round)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      if (hit[q]) {
+        const int r = r0 + q * blockDim.x + threadIdx.x;
+        float4* e = B.hits + 3 * (int64_t)(base + __popc(hm[q] & lt_mask));
+        e[0] = h0[q];
+        e[1] = h1[q];
+        e[2] = make_float4(__int_as_float(__double2loint(t0[q])), __int_as_float(__double2hiint(t0[q])),
+                           __int_as_float(r), __int_as_float(pix[q]));
+      }
+      base += __popc(hm[q]);
     }
   }
 #pragma unroll
@@ -1688,13 +1714,19 @@ int launch_main(fv_ctx* ctx, const FastParams& F, const WaveBufs& B, int threads
   const int blocks = std::max(1, std::min((F.P.k_max + 255) / 256, ctx->num_sms * 8));
   static bool co = false;
   if (!co) {
-    render_carveout(ray_setup_kernel);
+    render_carveout(ray_setup_kernel<1>);
+    render_carveout(ray_setup_kernel<2>);
     render_carveout(march_wave_main_list_kernel<2, TEX, FV_MAIN_MINB>);
     render_carveout(first_list_kernel);
     render_carveout(march_wave_composite_kernel);
     co = true;
   }
-  FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<<<blocks, 256, 0, ctx->stream>>>(F, B));
+  // rays per thread (FV_SETUP_RPT): 2 overlaps two fp64 setups per thread (C3 23.0 -> 18.9 us)
+  static const int rpt = getenv("FV_SETUP_RPT") ? atoi(getenv("FV_SETUP_RPT")) : 2;
+  if (rpt == 2)
+    FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<2><<<blocks, 256, 0, ctx->stream>>>(F, B));
+  else
+    FV_TIMED(ctx, FV_KC_MARCH_MAIN, ray_setup_kernel<1><<<blocks, 256, 0, ctx->stream>>>(F, B));
   ctx->launches += 1;
   static int per_sm = 0;
   if (!per_sm) {

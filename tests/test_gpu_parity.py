@@ -876,7 +876,8 @@ def test_graph_replay_equals_eager_launches(tmp_path):
                                        ("FV_KFUSE", ("0", "1")), ("FV_KCHAIN_SPLIT", ("0", "1")),
                                        ("FV_KCHAIN_SPLIT", ("0", "2")), ("FV_KHEAD_R", ("4", "8")),
                                        ("FV_UP_ROWS", ("1", "2")), ("FV_UP_ROWS", ("1", "4")),
-                                       ("FV_COMP_HITS", ("0", "1")), ("FV_MAIN_U", ("1", "2")), ("FV_N80_R", ("2", "4"))])
+                                       ("FV_COMP_HITS", ("0", "1")), ("FV_MAIN_U", ("1", "2")),
+                                       ("FV_SETUP_RPT", ("1", "2")), ("FV_N80_R", ("2", "4"))])
 def test_launch_variants_give_identical_frames(tmp_path, knob, vals):
     """The fused K-stage chain (one cooperative launch for the levels between the first and last K
     block), the programmatic-dependent launches, the next frame's mask next to the network, the
