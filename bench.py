@@ -164,6 +164,7 @@ class CpuFrames:
         from oracle import fovray_oracle as O
 
         self.O, self.cfg = O, cfg
+        self.blas_threads = None  # the BLAS pool's size during the timed frames
         h, w, n = cfg["height"], cfg["width"], cfg["vol"]
         self.stack = O.load_rnkstack(ROOT / "paper_2209_09965_b200" / "data" / "stbn_64x64x8_s1.noise")
         self.tau = O.tau_map(h, w, ((w - 1) / 2, (h - 1) / 2), cfg["sigma"], cfg["pb"], O.pixel_scale_for_film(h, w))
@@ -174,6 +175,8 @@ class CpuFrames:
 
     def frame(self, i):
         """One frame; returns (seconds, (mask, march, net) seconds)."""
+        if self.blas_threads is None:
+            self.blas_threads = blas_threads()
         O, cfg = self.O, self.cfg
         h, w, n = cfg["height"], cfg["width"], cfg["vol"]
         t0 = time.perf_counter()
@@ -196,11 +199,22 @@ class CpuFrames:
 
     def describe(self, frames, phases):
         ph = np.mean(np.asarray(phases), axis=0) if phases else (0, 0, 0)
+        if self.blas_threads is None:
+            self.blas_threads = blas_threads()
         return (f"{frames} whole frames of the reference loop body restated by the oracle (NumPy fp64 mask, C fp64 "
                 f"marcher on all {len(os.sched_getaffinity(0))} host threads over all active rays, NumPy/BLAS "
                 f"fp32 FULL_BLOCKS net at the full film, state carried): mean mask {ph[0]*1e3:.0f} ms, march "
-                f"{ph[1]:.2f} s, net {ph[2]:.2f} s per frame; CPU {cpu_model()}; OPENBLAS_NUM_THREADS="
-                f"{os.environ.get('OPENBLAS_NUM_THREADS', 'unset (all cores)')}")
+                f"{ph[1]:.2f} s, net {ph[2]:.2f} s per frame; CPU {cpu_model()}; BLAS threads "
+                f"{self.blas_threads}; OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS', 'unset')}, "
+                f"OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS', 'unset')}")
+
+
+def blas_threads():
+    """Threads of the BLAS pool NumPy uses right now (threadpoolctl)."""
+    from threadpoolctl import threadpool_info
+
+    n = [p.get("num_threads") for p in threadpool_info() if p.get("user_api") == "blas"]
+    return n[0] if n else None
 
 
 def cpu_model():
@@ -262,11 +276,16 @@ def run_reference(args, cfg):
     k, wu = args.steps, args.warmup
     cf = CpuFrames(cfg)
     per, phases = [], []
-    for s_ in range(wu + k):
-        sec, ph = cf.frame(s_)
-        if s_ >= wu:
-            per.append(sec)
-            phases.append(ph)
+    # torchrun sets OMP_NUM_THREADS=1 for every rank; rank 0 alone runs this arm, so the BLAS pool
+    # is raised to every host thread it may use (the C marcher sizes itself from the affinity mask)
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=len(os.sched_getaffinity(0))):
+        for s_ in range(wu + k):
+            sec, ph = cf.frame(s_)
+            if s_ >= wu:
+                per.append(sec)
+                phases.append(ph)
     fps = 1.0 / float(np.mean(per))
     threads = len(os.sched_getaffinity(0))
     line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus, "steps": k,
